@@ -1,0 +1,252 @@
+/* enserve-b200 — C ABI of the B200-native ensemble-inference hot path.
+ *
+ * This is the drop-in boundary.  Every entry point replaces one function (or
+ * one class method) of the reference's C++ API, /root/reference/proj
+ * ("enserve", arXiv 2208.14049); the reference location is cited on each
+ * declaration.  Plain pointers and sizes only, no C++ or torch types; every
+ * call returns an es_status and never throws.  INTEGRATION.md shows the
+ * reference-side adapter (a PredictorFactory named "b200" plus a ScoreFn) a
+ * maintainer would add to call this library.
+ *
+ * Matrices are D x M int grids, row-major (cell d*M+m), like
+ * AllocationMatrix (include/enserve/core/types.hpp:55-88).
+ */
+#ifndef ENSERVE_B200_H
+#define ENSERVE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ES_ABI_VERSION 1
+#define ES_MAX_WIDTHS 9
+
+/* Error classes of include/enserve/core/errors.hpp:9-51, plus device errors. */
+typedef enum es_status {
+  ES_OK = 0,
+  ES_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument / std::out_of_range */
+  ES_ERR_SPEC = 2,             /* SpecError */
+  ES_ERR_ALLOCATION = 3,       /* AllocationError (worst-fit found no device) */
+  ES_ERR_STARTUP = 4,          /* StartupError (a worker's load() reported OOM) */
+  ES_ERR_BASELINE = 5,         /* BaselineError (BBS needs one GPU per model) */
+  ES_ERR_CAP_EXCEEDED = 6,     /* CapExceededError */
+  ES_ERR_PROTOCOL = 7,         /* ProtocolError */
+  ES_ERR_CUDA = 8,             /* CUDA failure other than out-of-memory */
+  ES_ERR_INTERNAL = 9,
+  ES_ERR_BUFFER = 10           /* caller buffer too small */
+} es_status;
+
+/* DeviceSpec (types.hpp:17-26); ids are the array positions. */
+typedef struct es_device_desc {
+  int kind; /* 0 = CPU, 1 = GPU */
+  double memory_mib;
+  double compute_rate;
+  double batch_overhead_s;
+} es_device_desc;
+
+/* ModelSpec (types.hpp:28-35) + what the device executes. */
+typedef struct es_model_desc {
+  const char* name;
+  double weight_mib;
+  double act_mib_per_sample;
+  double cost_per_sample;
+  int output_width;
+  int arch;                     /* 0 = synthetic_prediction member, 1 = MLP */
+  int n_widths;                 /* MLP: input, hidden..., classes */
+  int widths[ES_MAX_WIDTHS];
+  uint64_t weight_seed;
+} es_model_desc;
+
+/* ClusterSpec (types.hpp:38-52). */
+typedef struct es_cluster_desc {
+  const es_device_desc* devices;
+  int n_devices;
+  const es_model_desc* models;
+  int n_models;
+  const int* batch_menu;
+  int menu_size;
+  int segment_size;
+} es_cluster_desc;
+
+/* CombinationRule (include/enserve/runtime/combine.hpp:14-27). */
+typedef struct es_rule_desc {
+  int kind;            /* 0 = averaging, 1 = majority vote, 2 = weighted averaging */
+  int member_softmax;  /* fold softmax(member output) instead of the raw output */
+  const double* weights;
+} es_rule_desc;
+
+/* PoolOptions (include/enserve/runtime/pipeline.hpp:48-53), device flavour. */
+typedef struct es_pool_opts {
+  const int* device_map; /* cluster device row -> CUDA ordinal; NULL = row % #GPUs */
+  int n_device_map;
+  int copy_outputs;      /* D2H of the combined output in await_run */
+  int warmup;            /* bench: one untimed run first */
+  int sms_per_worker;    /* 0 = all SMs (persistent grid) */
+} es_pool_opts;
+
+/* RunStats (pipeline.hpp:19-25). */
+typedef struct es_run_stats {
+  size_t nb_samples;
+  size_t segments;
+  size_t data_messages;
+  double elapsed_s; /* CUDA-event window: broadcast -> last fold */
+} es_run_stats;
+
+/* BenchResult (pipeline.hpp:35-41); runs[] holds up to 64 repeats. */
+typedef struct es_bench_result {
+  double throughput;
+  double elapsed_s;
+  size_t nb_samples;
+  int n_runs;
+  double runs[64];
+  double rsd;
+} es_bench_result;
+
+typedef struct es_store es_store;
+typedef struct es_system es_system;
+typedef struct es_member es_member;
+
+int es_abi_version(void);
+const char* es_status_name(es_status s);
+/* Message of the last failed call on this thread. */
+const char* es_last_error(void);
+
+/* ------------------------------------------------------------ host core */
+/* ClusterSpec::validate (src/core/types.cpp:31-74). */
+es_status es_cluster_validate(const es_cluster_desc* c, char* warnings, size_t len);
+/* validate_matrix (types.cpp:102-127); violations: [kind, device, model, value] x n. */
+es_status es_matrix_validate(const es_cluster_desc* c, const int* A, int* ok, int* violations,
+                             int cap, int* n);
+/* num_segments / segment_bounds (types.cpp:129-149). */
+es_status es_num_segments(size_t nb, int segment_size, size_t* out);
+es_status es_segment_bounds(int segment_id, int segment_size, size_t nb, size_t* start,
+                            size_t* end);
+/* fit_mem (src/memory/memory_model.cpp:22-32); used_mib[D]. */
+es_status es_fit_mem(const es_cluster_desc* c, const int* A, double* used_mib, int* fits);
+/* more_remaining_memory (memory_model.cpp:34-50); *device = -1 when none. */
+es_status es_more_remaining_memory(const es_cluster_desc* c, const int* A, int kind, int* device);
+/* predict_ensemble_throughput (src/cost/cost_model.cpp:29-46). */
+es_status es_predict_ensemble_throughput(const es_cluster_desc* c, const int* A, double* out);
+/* worst_fit_decreasing (src/opt/optimizer.cpp:37-64); ES_ERR_ALLOCATION names the
+ * model in es_last_error(). */
+es_status es_worst_fit_decreasing(const es_cluster_desc* c, int default_batch, int* A_out);
+/* neighborhood (optimizer.cpp:66-84): writes min(count, cap) matrices. */
+es_status es_neighborhood(const es_cluster_desc* c, const int* A, int* out, int cap, int* count);
+/* enumerated_neighborhood_stats (optimizer.cpp:86-103). */
+es_status es_neighborhood_stats(const es_cluster_desc* c, const int* A, size_t* size,
+                                size_t* forbidden);
+/* count_total_matrices (optimizer.cpp:105-111), decimal string. */
+es_status es_count_total_matrices(int menu_size, int devices, int models, char* buf, size_t len);
+/* count_total_neighs (optimizer.cpp:113-118). */
+es_status es_count_total_neighs(int menu_size, int devices, int models, long long forbidden,
+                                long long* out);
+/* effective_max_iter (optimizer.cpp:173-176). */
+es_status es_effective_max_iter(int devices, int models, int max_iter, int* out);
+/* enumerate_all_matrices (optimizer.cpp:120-171); cap as a decimal string. */
+es_status es_enumerate_matrices(const es_cluster_desc* c, const char* cap, int* out,
+                                size_t out_cap, size_t* count);
+/* sample_indices (include/enserve/util/rng.hpp:26-38) from a fresh mt19937_64(seed). */
+es_status es_sample_indices(uint64_t seed, size_t n, size_t k, size_t* out);
+
+/* ScoreFn (include/enserve/opt/optimizer.hpp:18). */
+typedef double (*es_score_fn)(const int* A, int devices, int models, void* user);
+
+typedef enum es_bench_mode {
+  ES_BENCH_ANALYTIC = 0, /* predict_ensemble_throughput */
+  ES_BENCH_DEVICE = 1,   /* bench() on the GPUs, CUDA-event timed */
+  ES_BENCH_CALLBACK = 2  /* caller's es_score_fn */
+} es_bench_mode;
+
+typedef struct es_bench_cfg {
+  int mode;
+  es_score_fn fn;
+  void* user;
+  es_store* calib;
+  int repeats;
+  const es_pool_opts* opts;
+} es_bench_cfg;
+
+/* OptimizationTrace (optimizer.hpp:33-47); iteration arrays hold iter_cap entries. */
+typedef struct es_greedy_trace {
+  double start_score;
+  double final_score;
+  int stop_reason; /* 0 = local_optimum, 1 = iter_cap */
+  int n_iters;
+  int bench_calls;
+  int iter_cap;
+  int* iter_neighbors;
+  double* iter_best;
+  int* iter_accepted;
+} es_greedy_trace;
+
+/* bounded_greedy (optimizer.cpp:178-227). */
+es_status es_bounded_greedy(const es_cluster_desc* c, const int* A0, int max_iter, int max_neighs,
+                            uint64_t seed, const es_bench_cfg* bench, int* A_out,
+                            es_greedy_trace* trace);
+/* bbs_baseline (optimizer.cpp:229-269); chosen[M]. */
+es_status es_bbs_baseline(const es_cluster_desc* c, const es_bench_cfg* bench, int* A_out,
+                          int* chosen, int* calls);
+
+/* ------------------------------------------------------------ device runtime */
+es_status es_device_count(int* n);
+
+/* SampleStore (include/enserve/runtime/message.hpp:12-34).  copy = 0 borrows X
+ * (must outlive the store). */
+es_status es_store_create(const float* X, size_t nb, size_t width, int copy, es_store** out);
+/* Synthetic features generated on `device`. */
+es_status es_store_synthetic(uint64_t seed, size_t nb, size_t width, int device, es_store** out);
+void es_store_destroy(es_store* s);
+
+/* InferenceSystem (include/enserve/runtime/pipeline.hpp:62-117). */
+es_status es_system_create(const es_cluster_desc* c, const int* A, const es_rule_desc* rule,
+                           const es_pool_opts* opts, es_system** out);
+es_status es_system_begin_run(es_system* s, es_store* X, const es_rule_desc* rule);
+es_status es_system_broadcast(es_system* s, size_t* segments);
+/* Y[nb*C] and winners[nb] may be NULL. */
+es_status es_system_await_run(es_system* s, float* Y, int32_t* winners, es_run_stats* stats);
+es_status es_system_run(es_system* s, es_store* X, float* Y, int32_t* winners,
+                        es_run_stats* stats);
+/* End to end from host memory: H2D of X, members, combine, D2H of Y and labels
+ * all inside the CUDA-event window. */
+es_status es_system_run_host(es_system* s, const float* X, size_t nb, size_t width, float* Y,
+                             int32_t* labels, double* elapsed_s);
+/* workers_per_model[M] (pipeline.hpp:86-89) + launches of the last run. */
+es_status es_system_info(es_system* s, int* workers, int* workers_per_model, int* launches,
+                         int* combine_device);
+/* Device time of each worker's member kernel and of the combine, last run. */
+es_status es_system_timing(es_system* s, double* member_ms, double* combine_ms);
+es_status es_system_shutdown(es_system* s);
+void es_system_destroy(es_system* s);
+
+/* run_inference (pipeline.cpp:418-444), Deploy mode: Y[nb*C], winners[nb]. */
+es_status es_run_inference(const es_cluster_desc* c, const int* A, const es_rule_desc* rule,
+                           es_store* X, const es_pool_opts* opts, float* Y, int32_t* winners,
+                           es_run_stats* stats);
+/* bench (pipeline.cpp:465-501). */
+es_status es_bench(const es_cluster_desc* c, const int* A, es_store* calib, int repeats,
+                   const es_pool_opts* opts, es_bench_result* out);
+
+/* ------------------------------------------------------------ Predictor seam */
+/* PredictorFactory::make + Predictor::load (include/enserve/runtime/backend.hpp:
+ * 16-41): ES_ERR_STARTUP when load() reports out-of-memory. */
+es_status es_member_create(int device, const es_model_desc* model, int model_id, int batch,
+                           double device_load_mib, double capacity_mib, es_member** out);
+/* Predictor::predict (backend.hpp:33): rows x width fp32 host features of
+ * samples first_index.. -> out[rows * C] host. */
+es_status es_member_predict(es_member* m, const float* features, size_t first_index, size_t rows,
+                            size_t width, float* out);
+void es_member_destroy(es_member* m);
+
+/* PredictionAccumulator fold (src/runtime/combine.cpp:93-136) for M host blocks
+ * of rows x C, run by the device combine kernel; winners = argmax per row. */
+es_status es_combine(const es_rule_desc* rule, int M, int C, size_t rows,
+                     const float* const* blocks, float* Y, int32_t* winners);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ENSERVE_B200_H */

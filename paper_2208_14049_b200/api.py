@@ -1,0 +1,776 @@
+"""Python mirror of the enserve API over the enserve-b200 C ABI.
+
+Names, argument meaning and raised error classes follow the reference's C++
+API (/root/reference/proj/include/enserve/**; file:line on each item), so the
+parity tests read like the reference's own doctest suites.  All work happens in
+libenserve_b200.so (C++ host core + sm_100a kernels); this module only marshals.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Callable, Optional, Sequence
+
+import numpy as np
+
+from . import _abi
+from ._abi import lib
+
+
+# ------------------------------------------------------------------ errors
+class EnserveError(RuntimeError):
+    """enserve::Error (include/enserve/core/errors.hpp:9-12)."""
+
+
+class SpecError(EnserveError):
+    """errors.hpp:16-19."""
+
+
+class AllocationError(EnserveError):
+    """errors.hpp:22-27; .model_name parsed from the message."""
+
+    @property
+    def model_name(self) -> str:
+        msg = str(self)
+        return msg.split("'")[1] if "'" in msg else ""
+
+
+class BaselineError(EnserveError):
+    """errors.hpp:30-33."""
+
+
+class CapExceededError(EnserveError):
+    """errors.hpp:36-39."""
+
+
+class StartupError(EnserveError):
+    """errors.hpp:42-45."""
+
+
+class ProtocolError(EnserveError):
+    """errors.hpp:48-51."""
+
+
+class DeviceError(EnserveError):
+    """CUDA failure other than out-of-memory (no reference counterpart)."""
+
+
+class InvalidArgument(ValueError):
+    """std::invalid_argument / std::out_of_range thrown by the reference."""
+
+
+_STATUS = {1: InvalidArgument, 2: SpecError, 3: AllocationError, 4: StartupError,
+           5: BaselineError, 6: CapExceededError, 7: ProtocolError, 8: DeviceError,
+           9: EnserveError, 10: EnserveError}
+
+
+def _check(status: int) -> None:
+    if status != 0:
+        msg = lib().es_last_error().decode(errors="replace")
+        raise _STATUS.get(status, EnserveError)(msg)
+
+
+# ------------------------------------------------------------------ specs
+GPU, CPU = "GPU", "CPU"
+
+
+@dataclass
+class DeviceSpec:
+    """types.hpp:17-26."""
+    id: int = 0
+    kind: str = GPU
+    memory_mib: float = 0.0
+    compute_rate: float = 0.0
+    batch_overhead_s: float = 0.0
+
+    def label(self) -> str:
+        return ("gpu" if self.kind == GPU else "cpu") + str(self.id)
+
+
+@dataclass
+class MemberArch:
+    """What the device executes for a member (spec.hpp MemberArch).
+
+    kind "synthetic": synthetic_prediction(model, sample, class)
+    (src/runtime/backend.cpp:21-29); kind "mlp": dense layers over `widths`.
+    """
+    kind: str = "synthetic"
+    widths: tuple = ()
+    weight_seed: int = 0
+
+    def flops_per_sample(self) -> float:
+        return float(sum(2 * a * b for a, b in zip(self.widths[:-1], self.widths[1:])))
+
+    def parameter_count(self) -> int:
+        return int(sum(a * b + b for a, b in zip(self.widths[:-1], self.widths[1:])))
+
+
+@dataclass
+class ModelSpec:
+    """types.hpp:28-35 (+ arch)."""
+    id: int = 0
+    name: str = ""
+    weight_mib: float = 0.0
+    act_mib_per_sample: float = 0.0
+    cost_per_sample: float = 0.0
+    output_width: int = 1
+    arch: MemberArch = field(default_factory=MemberArch)
+
+
+def mlp_model(id: int, name: str, widths: Sequence[int], seed: int, *,
+              weight_mib: Optional[float] = None, act_mib: Optional[float] = None,
+              cost: Optional[float] = None) -> ModelSpec:
+    """A ModelSpec whose footprint is derived from its MLP shape (bf16 weights
+    and activations), unless given explicitly (runtime.cpp derive_footprint)."""
+    arch = MemberArch("mlp", tuple(int(w) for w in widths), int(seed))
+    mib = 1024.0 * 1024.0
+    return ModelSpec(
+        id=id, name=name,
+        weight_mib=weight_mib if weight_mib is not None else arch.parameter_count() * 2 / mib,
+        act_mib_per_sample=act_mib if act_mib is not None else sum(widths) * 2 / mib,
+        cost_per_sample=cost if cost is not None else arch.flops_per_sample(),
+        output_width=int(widths[-1]), arch=arch)
+
+
+@dataclass
+class ClusterSpec:
+    """types.hpp:38-52."""
+    devices: list = field(default_factory=list)
+    models: list = field(default_factory=list)
+    batch_menu: list = field(default_factory=list)
+    segment_size: int = 128
+
+    def device_count(self) -> int:
+        return len(self.devices)
+
+    def model_count(self) -> int:
+        return len(self.models)
+
+    def min_batch(self) -> int:
+        if not self.batch_menu:
+            raise SpecError("batch menu is empty")
+        return self.batch_menu[0]
+
+    def validate(self) -> list:
+        buf = C.create_string_buffer(4096)
+        with _Desc(self) as d:
+            _check(lib().es_cluster_validate(d.ptr, buf, len(buf)))
+        return [w for w in buf.value.decode().split("\n") if w]
+
+
+class _Desc:
+    """Keeps the ctypes cluster descriptor and its arrays alive."""
+
+    def __init__(self, c: ClusterSpec):
+        nd, nm = len(c.devices), len(c.models)
+        self.devs = (_abi.DeviceDesc * max(nd, 1))()
+        for i, d in enumerate(c.devices):
+            self.devs[i] = _abi.DeviceDesc(0 if d.kind == CPU else 1, d.memory_mib,
+                                           d.compute_rate, d.batch_overhead_s)
+        self.models = (_abi.ModelDesc * max(nm, 1))()
+        self.names = [m.name.encode() for m in c.models]
+        for i, m in enumerate(c.models):
+            md = self.models[i]
+            md.name = self.names[i]
+            md.weight_mib = m.weight_mib
+            md.act_mib_per_sample = m.act_mib_per_sample
+            md.cost_per_sample = m.cost_per_sample
+            md.output_width = m.output_width
+            md.arch = 1 if m.arch.kind == "mlp" else 0
+            md.n_widths = len(m.arch.widths)
+            for j, w in enumerate(m.arch.widths):
+                md.widths[j] = int(w)
+            md.weight_seed = int(m.arch.weight_seed)
+        self.menu = (C.c_int * max(len(c.batch_menu), 1))(*c.batch_menu)
+        self.desc = _abi.ClusterDesc(self.devs, nd, self.models, nm, self.menu,
+                                     len(c.batch_menu), c.segment_size)
+        self.ptr = C.byref(self.desc)
+        self.D, self.M = nd, nm
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
+
+
+# ------------------------------------------------------------------ matrix
+class AllocationMatrix:
+    """D x M batch grid, 0 = no worker (types.hpp:55-88)."""
+
+    def __init__(self, devices: int = 0, models: int = 0, cells=None):
+        if cells is not None:
+            self.cells = np.ascontiguousarray(np.asarray(cells, dtype=np.int32).reshape(devices, models))
+        else:
+            self.cells = np.zeros((devices, models), dtype=np.int32)
+
+    @classmethod
+    def from_array(cls, a) -> "AllocationMatrix":
+        a = np.asarray(a, dtype=np.int32)
+        return cls(a.shape[0], a.shape[1], a)
+
+    def device_count(self) -> int:
+        return self.cells.shape[0]
+
+    def model_count(self) -> int:
+        return self.cells.shape[1]
+
+    def at(self, d: int, m: int) -> int:
+        return int(self.cells[d, m])
+
+    def set(self, d: int, m: int, b: int) -> None:
+        self.cells[d, m] = b
+
+    def worker_count(self) -> int:
+        return int(np.count_nonzero(self.cells))
+
+    def row_worker_count(self, d: int) -> int:
+        return int(np.count_nonzero(self.cells[d]))
+
+    def column_worker_count(self, m: int) -> int:
+        return int(np.count_nonzero(self.cells[:, m]))
+
+    def is_data_parallel(self, m: int) -> bool:
+        return self.column_worker_count(m) >= 2
+
+    def is_colocated(self, d: int) -> bool:
+        return self.row_worker_count(d) >= 2
+
+    def copy(self) -> "AllocationMatrix":
+        return AllocationMatrix.from_array(self.cells.copy())
+
+    def ptr(self):
+        return self.cells.ctypes.data_as(_abi.c_int_p)
+
+    def __eq__(self, other) -> bool:
+        return isinstance(other, AllocationMatrix) and self.cells.shape == other.cells.shape and \
+            bool(np.array_equal(self.cells, other.cells))
+
+    def __repr__(self) -> str:
+        return f"AllocationMatrix({self.cells.tolist()})"
+
+
+@dataclass
+class MatrixViolation:
+    kind: str  # "EntryNotInMenu" | "EmptyColumn"
+    device: int
+    model: int
+    value: int
+
+
+@dataclass
+class MatrixValidation:
+    ok: bool
+    violations: list
+
+
+def validate_matrix(A: AllocationMatrix, cluster: ClusterSpec) -> MatrixValidation:
+    """types.cpp:102-127."""
+    if A.device_count() != cluster.device_count() or A.model_count() != cluster.model_count():
+        raise SpecError(f"matrix is {A.device_count()}x{A.model_count()} but the cluster has "
+                        f"{cluster.device_count()} devices and {cluster.model_count()} models")
+    cap = A.cells.size + A.model_count() + 1
+    buf = (C.c_int * (4 * cap))()
+    ok, n = C.c_int(), C.c_int()
+    with _Desc(cluster) as d:
+        _check(lib().es_matrix_validate(d.ptr, A.ptr(), C.byref(ok), buf, cap, C.byref(n)))
+    v = [MatrixViolation("EmptyColumn" if buf[4 * i] else "EntryNotInMenu", buf[4 * i + 1],
+                         buf[4 * i + 2], buf[4 * i + 3]) for i in range(n.value)]
+    return MatrixValidation(bool(ok.value), v)
+
+
+def num_segments(nb: int, segment_size: int) -> int:
+    """types.cpp:129-134."""
+    out = C.c_size_t()
+    _check(lib().es_num_segments(nb, segment_size, C.byref(out)))
+    return out.value
+
+
+def segment_bounds(segment_id: int, segment_size: int, nb: int) -> tuple:
+    """types.cpp:136-149 -> (start, end)."""
+    s, e = C.c_size_t(), C.c_size_t()
+    _check(lib().es_segment_bounds(segment_id, segment_size, nb, C.byref(s), C.byref(e)))
+    return s.value, e.value
+
+
+@dataclass
+class MemoryReport:
+    used_mib: list
+    fits: bool
+
+
+def fit_mem(A: AllocationMatrix, cluster: ClusterSpec) -> MemoryReport:
+    """memory_model.cpp:22-32."""
+    used = (C.c_double * max(cluster.device_count(), 1))()
+    fits = C.c_int()
+    with _Desc(cluster) as d:
+        _check(lib().es_fit_mem(d.ptr, A.ptr(), used, C.byref(fits)))
+    return MemoryReport(list(used)[: cluster.device_count()], bool(fits.value))
+
+
+def more_remaining_memory(A: AllocationMatrix, kind: str, cluster: ClusterSpec) -> Optional[int]:
+    """memory_model.cpp:34-50."""
+    dev = C.c_int()
+    with _Desc(cluster) as d:
+        _check(lib().es_more_remaining_memory(d.ptr, A.ptr(), 0 if kind == CPU else 1, C.byref(dev)))
+    return None if dev.value < 0 else dev.value
+
+
+def predict_ensemble_throughput(A: AllocationMatrix, cluster: ClusterSpec) -> float:
+    """cost_model.cpp:29-46."""
+    out = C.c_double()
+    with _Desc(cluster) as d:
+        _check(lib().es_predict_ensemble_throughput(d.ptr, A.ptr(), C.byref(out)))
+    return out.value
+
+
+def worst_fit_decreasing(cluster: ClusterSpec, default_batch: int) -> AllocationMatrix:
+    """optimizer.cpp:37-64."""
+    A = AllocationMatrix(cluster.device_count(), cluster.model_count())
+    with _Desc(cluster) as d:
+        _check(lib().es_worst_fit_decreasing(d.ptr, default_batch, A.ptr()))
+    return A
+
+
+def neighborhood(A: AllocationMatrix, cluster: ClusterSpec) -> list:
+    """optimizer.cpp:66-84."""
+    D, M = A.device_count(), A.model_count()
+    cap = (len(cluster.batch_menu) + 1) * D * M + 1
+    out = np.zeros((cap, D, M), dtype=np.int32)
+    n = C.c_int()
+    with _Desc(cluster) as d:
+        _check(lib().es_neighborhood(d.ptr, A.ptr(), out.ctypes.data_as(_abi.c_int_p), cap,
+                                     C.byref(n)))
+    return [AllocationMatrix.from_array(out[i]) for i in range(n.value)]
+
+
+def enumerated_neighborhood_stats(A: AllocationMatrix, cluster: ClusterSpec) -> tuple:
+    """optimizer.cpp:86-103 -> (size, forbidden)."""
+    s, f = C.c_size_t(), C.c_size_t()
+    with _Desc(cluster) as d:
+        _check(lib().es_neighborhood_stats(d.ptr, A.ptr(), C.byref(s), C.byref(f)))
+    return s.value, f.value
+
+
+def count_total_matrices(menu_size: int, devices: int, models: int) -> int:
+    """optimizer.cpp:105-111 (exact)."""
+    buf = C.create_string_buffer(4096)
+    _check(lib().es_count_total_matrices(menu_size, devices, models, buf, len(buf)))
+    return int(buf.value.decode())
+
+
+def count_total_neighs(menu_size: int, devices: int, models: int, forbidden: int) -> int:
+    """optimizer.cpp:113-118."""
+    out = C.c_longlong()
+    _check(lib().es_count_total_neighs(menu_size, devices, models, forbidden, C.byref(out)))
+    return out.value
+
+
+def effective_max_iter(devices: int, models: int, max_iter: int) -> int:
+    """optimizer.cpp:173-176."""
+    out = C.c_int()
+    _check(lib().es_effective_max_iter(devices, models, max_iter, C.byref(out)))
+    return out.value
+
+
+def enumerate_all_matrices(cluster: ClusterSpec, cap: int) -> list:
+    """optimizer.cpp:165-171."""
+    D, M = cluster.device_count(), cluster.model_count()
+    count = C.c_size_t()
+    with _Desc(cluster) as d:
+        _check(lib().es_enumerate_matrices(d.ptr, str(int(cap)).encode(), None, 0, C.byref(count)))
+        out = np.zeros((max(count.value, 1), D, M), dtype=np.int32)
+        _check(lib().es_enumerate_matrices(d.ptr, str(int(cap)).encode(),
+                                           out.ctypes.data_as(_abi.c_int_p), count.value,
+                                           C.byref(count)))
+    return [AllocationMatrix.from_array(out[i]) for i in range(count.value)]
+
+
+def sample_indices(seed: int, n: int, k: int) -> list:
+    """rng.hpp:26-38 on a fresh mt19937_64(seed)."""
+    out = (C.c_size_t * max(min(n, k), 1))()
+    _check(lib().es_sample_indices(seed, n, k, out))
+    return list(out)[: min(n, k)]
+
+
+# ------------------------------------------------------------------ optimizer
+@dataclass
+class GreedyConfig:
+    """optimizer.hpp:23-27."""
+    max_iter: int = 10
+    max_neighs: int = 100
+    rng_seed: int = 0
+
+
+@dataclass
+class GreedyIteration:
+    index: int
+    neighbors_evaluated: int
+    best_score: float
+    accepted: bool
+
+
+@dataclass
+class OptimizationTrace:
+    """optimizer.hpp:40-47."""
+    iterations: list
+    start_score: float
+    final_score: float
+    stop_reason: str
+    calls: int
+
+    def bench_calls(self) -> int:
+        return 1 + sum(it.neighbors_evaluated for it in self.iterations)
+
+
+@dataclass
+class GreedyResult:
+    matrix: AllocationMatrix
+    trace: OptimizationTrace
+
+
+class DeviceBench:
+    """bench(A, calib) on the GPUs as the greedy's ScoreFn (commands.cpp:132-150)."""
+
+    def __init__(self, calib: "SampleStore", repeats: int = 1, **pool):
+        self.calib, self.repeats, self.pool = calib, repeats, pool
+
+
+def _bench_cfg(bench, keep: list):
+    cfg = _abi.BenchCfg()
+    if bench is None or bench == "analytic":
+        cfg.mode = 0
+    elif isinstance(bench, DeviceBench):
+        cfg.mode = 1
+        cfg.calib = bench.calib._h
+        cfg.repeats = bench.repeats
+        opts = _pool_opts(keep, **bench.pool)
+        cfg.opts = C.pointer(opts)
+    elif callable(bench):
+        def trampoline(a_ptr, D, M, _user):
+            arr = np.ctypeslib.as_array(a_ptr, shape=(D * M,)).reshape(D, M).copy()
+            return float(bench(AllocationMatrix.from_array(arr)))
+        cb = _abi.SCORE_FN(trampoline)
+        keep.append(cb)
+        cfg.mode = 2
+        cfg.fn = cb
+    else:
+        raise TypeError("bench must be None/'analytic', a DeviceBench or a callable")
+    keep.append(cfg)
+    return cfg
+
+
+def bounded_greedy(A0: AllocationMatrix, cluster: ClusterSpec, bench=None,
+                   config: GreedyConfig = GreedyConfig()) -> GreedyResult:
+    """optimizer.cpp:178-227; bench = 'analytic' | DeviceBench | callable(A) -> score."""
+    keep: list = []
+    cfg = _bench_cfg(bench, keep)
+    out = AllocationMatrix(A0.device_count(), A0.model_count())
+    cap = effective_max_iter(cluster.device_count(), cluster.model_count(), config.max_iter) + 1
+    nbr = (C.c_int * cap)()
+    best = (C.c_double * cap)()
+    acc = (C.c_int * cap)()
+    tr = _abi.GreedyTrace(0, 0, 0, 0, 0, cap, nbr, best, acc)
+    with _Desc(cluster) as d:
+        _check(lib().es_bounded_greedy(d.ptr, A0.ptr(), config.max_iter, config.max_neighs,
+                                       config.rng_seed, C.byref(cfg), out.ptr(), C.byref(tr)))
+    its = [GreedyIteration(i, nbr[i], best[i], bool(acc[i])) for i in range(tr.n_iters)]
+    trace = OptimizationTrace(its, tr.start_score, tr.final_score,
+                              "local_optimum" if tr.stop_reason == 0 else "iter_cap", tr.bench_calls)
+    return GreedyResult(out, trace)
+
+
+@dataclass
+class BaselineResult:
+    matrix: AllocationMatrix
+    bench_calls: int
+    chosen_batches: list
+
+
+def bbs_baseline(cluster: ClusterSpec, bench=None) -> BaselineResult:
+    """optimizer.cpp:229-269."""
+    keep: list = []
+    cfg = _bench_cfg(bench, keep)
+    out = AllocationMatrix(cluster.device_count(), cluster.model_count())
+    chosen = (C.c_int * max(cluster.model_count(), 1))()
+    calls = C.c_int()
+    with _Desc(cluster) as d:
+        _check(lib().es_bbs_baseline(d.ptr, C.byref(cfg), out.ptr(), chosen, C.byref(calls)))
+    return BaselineResult(out, calls.value, list(chosen)[: cluster.model_count()])
+
+
+# ------------------------------------------------------------------ runtime
+@dataclass
+class CombinationRule:
+    """combine.hpp:14-27 (+ member_softmax)."""
+    kind: str = "avg"  # avg | vote | wavg
+    weights: tuple = ()
+    member_softmax: bool = False
+
+    @staticmethod
+    def averaging(softmax: bool = False) -> "CombinationRule":
+        return CombinationRule("avg", (), softmax)
+
+    @staticmethod
+    def majority_vote(softmax: bool = False) -> "CombinationRule":
+        return CombinationRule("vote", (), softmax)
+
+    @staticmethod
+    def weighted(weights, softmax: bool = False) -> "CombinationRule":
+        w = [float(x) for x in weights]
+        if any(x < 0 for x in w):
+            raise SpecError("combination weights must be nonnegative")
+        if abs(sum(w) - 1.0) > 1e-9:
+            raise SpecError(f"combination weights must sum to 1, got {sum(w)}")
+        return CombinationRule("wavg", tuple(w), softmax)
+
+    def _desc(self, keep: list):
+        kind = {"avg": 0, "vote": 1, "wavg": 2}[self.kind]
+        w = (C.c_double * max(len(self.weights), 1))(*self.weights)
+        keep.append(w)
+        d = _abi.RuleDesc(kind, int(self.member_softmax), C.cast(w, _abi.c_double_p))
+        keep.append(d)
+        return d
+
+
+def _pool_opts(keep: list, device_map=None, copy_outputs=True, warmup=True,
+               sms_per_worker=0) -> _abi.PoolOpts:
+    dm = None
+    n = 0
+    if device_map:
+        dm = (C.c_int * len(device_map))(*device_map)
+        keep.append(dm)
+        n = len(device_map)
+    o = _abi.PoolOpts(C.cast(dm, _abi.c_int_p) if dm is not None else None, n, int(copy_outputs),
+                      int(warmup), int(sms_per_worker))
+    keep.append(o)
+    return o
+
+
+def device_count() -> int:
+    n = C.c_int()
+    _check(lib().es_device_count(C.byref(n)))
+    return n.value
+
+
+class SampleStore:
+    """Immutable nb x width fp32 samples (message.hpp:12-34); device replicas
+    are created lazily per GPU."""
+
+    def __init__(self, X=None, *, synthetic_seed: Optional[int] = None, nb: int = 0,
+                 width: int = 0, device: int = 0):
+        h = C.c_void_p()
+        if X is not None:
+            self._X = np.ascontiguousarray(X, dtype=np.float32)
+            if self._X.ndim != 2:
+                raise SpecError("sample store needs a 2-D array")
+            nb, width = self._X.shape
+            _check(lib().es_store_create(self._X.ctypes.data_as(_abi.c_float_p), nb, width, 0,
+                                         C.byref(h)))
+        else:
+            self._X = None
+            _check(lib().es_store_synthetic(int(synthetic_seed or 0), nb, width, device, C.byref(h)))
+        self._h = h
+        self.nb, self.width = nb, width
+
+    def nb_samples(self) -> int:
+        return self.nb
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().es_store_destroy(self._h)
+            self._h = None
+
+
+@dataclass
+class RunStats:
+    nb_samples: int
+    segments: int
+    data_messages: int
+    elapsed_s: float
+
+
+@dataclass
+class RunOutput:
+    combined: np.ndarray
+    winners: np.ndarray
+    output_width: int
+    stats: RunStats
+
+
+class InferenceSystem:
+    """pipeline.hpp:62-117, GPU-resident."""
+
+    def __init__(self, A: AllocationMatrix, cluster: ClusterSpec, rule: CombinationRule = None,
+                 **pool):
+        self._keep: list = []
+        rule = rule or CombinationRule.averaging()
+        self.cluster = cluster
+        self.C = cluster.models[0].output_width if cluster.models else 1
+        h = C.c_void_p()
+        with _Desc(cluster) as d:
+            _check(lib().es_system_create(d.ptr, A.ptr(), C.byref(rule._desc(self._keep)),
+                                          C.byref(_pool_opts(self._keep, **pool)), C.byref(h)))
+        self._h = h
+        self._store = None
+
+    def worker_count(self) -> int:
+        n = C.c_int()
+        _check(lib().es_system_info(self._h, C.byref(n), None, None, None))
+        return n.value
+
+    def workers_per_model(self) -> list:
+        M = self.cluster.model_count()
+        w = (C.c_int * max(M, 1))()
+        _check(lib().es_system_info(self._h, None, w, None, None))
+        return list(w)[:M]
+
+    def launches_last_run(self) -> int:
+        n = C.c_int()
+        _check(lib().es_system_info(self._h, None, None, C.byref(n), None))
+        return n.value
+
+    def timing(self) -> tuple:
+        """(member_ms per worker, combine_ms) of the last run, CUDA events."""
+        w = self.worker_count()
+        ms = (C.c_double * max(w, 1))()
+        cm = C.c_double()
+        _check(lib().es_system_timing(self._h, ms, C.byref(cm)))
+        return list(ms)[:w], cm.value
+
+    def begin_run(self, X: SampleStore, rule: CombinationRule = None) -> None:
+        keep: list = []
+        self._store = X
+        self._pending = X.nb
+        _check(lib().es_system_begin_run(self._h, X._h,
+                                         C.byref(rule._desc(keep)) if rule else None))
+
+    def broadcast(self) -> int:
+        n = C.c_size_t()
+        _check(lib().es_system_broadcast(self._h, C.byref(n)))
+        return n.value
+
+    def await_run(self, copy: bool = True) -> RunOutput:
+        nb = self._pending
+        Y = np.zeros((nb, self.C), dtype=np.float32) if copy else None
+        W = np.zeros(nb, dtype=np.int32) if copy else None
+        st = _abi.RunStats()
+        _check(lib().es_system_await_run(
+            self._h, Y.ctypes.data_as(_abi.c_float_p) if copy else None,
+            W.ctypes.data_as(_abi.c_int32_p) if copy else None, C.byref(st)))
+        return RunOutput(Y, W, self.C, RunStats(st.nb_samples, st.segments, st.data_messages,
+                                               st.elapsed_s))
+
+    def run(self, X: SampleStore, rule: CombinationRule = None, copy: bool = True) -> RunOutput:
+        self.begin_run(X, rule)
+        self.broadcast()
+        return self.await_run(copy)
+
+    def run_host(self, X: np.ndarray, Y: np.ndarray = None, labels: np.ndarray = None) -> float:
+        """End-to-end from host memory; returns the CUDA-event seconds."""
+        X = np.ascontiguousarray(X, dtype=np.float32)
+        nb, width = X.shape
+        el = C.c_double()
+        _check(lib().es_system_run_host(
+            self._h, X.ctypes.data_as(_abi.c_float_p), nb, width,
+            Y.ctypes.data_as(_abi.c_float_p) if Y is not None else None,
+            labels.ctypes.data_as(_abi.c_int32_p) if labels is not None else None, C.byref(el)))
+        return el.value
+
+    def shutdown(self) -> None:
+        if self._h:
+            _check(lib().es_system_shutdown(self._h))
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib().es_system_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+        return False
+
+
+def run_inference(X: SampleStore, A: AllocationMatrix, cluster: ClusterSpec,
+                  rule: CombinationRule = None, **pool) -> RunOutput:
+    """pipeline.cpp:418-444, Deploy mode."""
+    keep: list = []
+    rule = rule or CombinationRule.averaging()
+    Cw = cluster.models[0].output_width
+    Y = np.zeros((X.nb, Cw), dtype=np.float32)
+    W = np.zeros(X.nb, dtype=np.int32)
+    st = _abi.RunStats()
+    with _Desc(cluster) as d:
+        _check(lib().es_run_inference(d.ptr, A.ptr(), C.byref(rule._desc(keep)), X._h,
+                                      C.byref(_pool_opts(keep, **pool)),
+                                      Y.ctypes.data_as(_abi.c_float_p),
+                                      W.ctypes.data_as(_abi.c_int32_p), C.byref(st)))
+    return RunOutput(Y, W, Cw, RunStats(st.nb_samples, st.segments, st.data_messages, st.elapsed_s))
+
+
+@dataclass
+class BenchResult:
+    """pipeline.hpp:35-41."""
+    throughput: float
+    elapsed_s: float
+    nb_samples: int
+    runs: list
+    rsd: float
+
+
+def bench(A: AllocationMatrix, calib: SampleStore, cluster: ClusterSpec, repeats: int,
+          **pool) -> BenchResult:
+    """pipeline.cpp:465-501 on the GPUs (CUDA-event timed)."""
+    keep: list = []
+    r = _abi.BenchResultC()
+    with _Desc(cluster) as d:
+        _check(lib().es_bench(d.ptr, A.ptr(), calib._h if calib is not None else None, repeats,
+                              C.byref(_pool_opts(keep, **pool)), C.byref(r)))
+    return BenchResult(r.throughput, r.elapsed_s, r.nb_samples, list(r.runs)[: r.n_runs], r.rsd)
+
+
+class Member:
+    """Predictor seam (backend.hpp:25-34): es_member_create = make + load."""
+
+    def __init__(self, model: ModelSpec, batch: int, device: int = 0,
+                 device_load_mib: float = 0.0, capacity_mib: float = float("inf")):
+        keep: list = []
+        c = ClusterSpec(models=[model])
+        d = _Desc(c)
+        keep.append(d)
+        h = C.c_void_p()
+        _check(lib().es_member_create(device, C.byref(d.models[0]), model.id, batch,
+                                      device_load_mib, capacity_mib, C.byref(h)))
+        self._h = h
+        self.C = model.output_width
+
+    def predict(self, features: np.ndarray, first_index: int = 0) -> np.ndarray:
+        f = np.ascontiguousarray(features, dtype=np.float32)
+        out = np.zeros((f.shape[0], self.C), dtype=np.float32)
+        _check(lib().es_member_predict(self._h, f.ctypes.data_as(_abi.c_float_p), first_index,
+                                       f.shape[0], f.shape[1], out.ctypes.data_as(_abi.c_float_p)))
+        return out
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().es_member_destroy(self._h)
+            self._h = None
+
+
+def combine(rule: CombinationRule, blocks: Sequence[np.ndarray]) -> tuple:
+    """Device fold of per-model blocks (combine.cpp:93-136) -> (Y, winners)."""
+    keep: list = []
+    arrs = [np.ascontiguousarray(b, dtype=np.float32) for b in blocks]
+    rows, Cw = arrs[0].shape
+    ptrs = (_abi.c_float_p * len(arrs))(*[a.ctypes.data_as(_abi.c_float_p) for a in arrs])
+    Y = np.zeros((rows, Cw), dtype=np.float32)
+    W = np.zeros(rows, dtype=np.int32)
+    _check(lib().es_combine(C.byref(rule._desc(keep)), len(arrs), Cw, rows, ptrs,
+                            Y.ctypes.data_as(_abi.c_float_p), W.ctypes.data_as(_abi.c_int32_p)))
+    return Y, W

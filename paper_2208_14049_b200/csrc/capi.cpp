@@ -1,0 +1,613 @@
+// The C ABI (include/enserve_b200.h) over the enserve-b200 C++ host core and
+// GPU runtime.  Exceptions never cross the boundary: each one maps to the
+// es_status of its reference error class, with the message kept per thread.
+#include "enserve_b200.h"
+
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <random>
+#include <string>
+
+#include "enserve/placement.hpp"
+#include "enserve/rng.hpp"
+#include "enserve/runtime.hpp"
+#include "enserve/search.hpp"
+
+using namespace enserve;
+
+struct es_store {
+  std::shared_ptr<SampleStore> store;
+};
+
+struct es_system {
+  std::unique_ptr<InferenceSystem> sys;
+  int models = 0;
+};
+
+struct es_member {
+  std::unique_ptr<B200Predictor> predictor;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <typename F>
+es_status guard(F&& body) {
+  try {
+    return body();
+  } catch (const AllocationError& e) {
+    g_last_error = e.what();
+    return ES_ERR_ALLOCATION;
+  } catch (const StartupError& e) {
+    g_last_error = e.what();
+    return ES_ERR_STARTUP;
+  } catch (const SpecError& e) {
+    g_last_error = e.what();
+    return ES_ERR_SPEC;
+  } catch (const BaselineError& e) {
+    g_last_error = e.what();
+    return ES_ERR_BASELINE;
+  } catch (const CapExceededError& e) {
+    g_last_error = e.what();
+    return ES_ERR_CAP_EXCEEDED;
+  } catch (const ProtocolError& e) {
+    g_last_error = e.what();
+    return ES_ERR_PROTOCOL;
+  } catch (const DeviceError& e) {
+    g_last_error = e.what();
+    return ES_ERR_CUDA;
+  } catch (const std::invalid_argument& e) {
+    g_last_error = e.what();
+    return ES_ERR_INVALID_ARGUMENT;
+  } catch (const std::out_of_range& e) {
+    g_last_error = e.what();
+    return ES_ERR_INVALID_ARGUMENT;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return ES_ERR_INTERNAL;
+  } catch (...) {
+    g_last_error = "unknown exception";
+    return ES_ERR_INTERNAL;
+  }
+}
+
+void need(bool ok, const char* what) {
+  if (!ok) throw std::invalid_argument(what);
+}
+
+ModelSpec to_model(const es_model_desc& d, int id) {
+  ModelSpec m;
+  m.id = id;
+  m.name = d.name ? d.name : "m" + std::to_string(id);
+  m.weight_mib = d.weight_mib;
+  m.act_mib_per_sample = d.act_mib_per_sample;
+  m.cost_per_sample = d.cost_per_sample;
+  m.output_width = d.output_width;
+  if (d.arch == 1) {
+    need(d.n_widths >= 2 && d.n_widths <= ES_MAX_WIDTHS, "MLP needs 2..9 widths");
+    m.arch.kind = MemberArch::Kind::MLP;
+    m.arch.widths.assign(d.widths, d.widths + d.n_widths);
+    m.arch.weight_seed = d.weight_seed;
+  } else {
+    m.arch.kind = MemberArch::Kind::Synthetic;
+  }
+  return m;
+}
+
+ClusterSpec to_cluster(const es_cluster_desc* c) {
+  need(c != nullptr, "cluster descriptor is NULL");
+  ClusterSpec s;
+  for (int d = 0; d < c->n_devices; ++d) {
+    const es_device_desc& x = c->devices[d];
+    s.devices.push_back({d, x.kind == 0 ? DeviceKind::CPU : DeviceKind::GPU, x.memory_mib,
+                         x.compute_rate, x.batch_overhead_s});
+  }
+  for (int m = 0; m < c->n_models; ++m) s.models.push_back(to_model(c->models[m], m));
+  if (c->menu_size > 0) s.batch_menu.assign(c->batch_menu, c->batch_menu + c->menu_size);
+  s.segment_size = c->segment_size;
+  return s;
+}
+
+AllocationMatrix to_matrix(const int* A, int D, int M) {
+  need(A != nullptr || D * M == 0, "matrix is NULL");
+  AllocationMatrix out(D, M);
+  for (int d = 0; d < D; ++d)
+    for (int m = 0; m < M; ++m) out.set(d, m, A[d * M + m]);
+  return out;
+}
+
+void write_matrix(const AllocationMatrix& A, int* out) {
+  std::memcpy(out, A.cells().data(), A.cells().size() * sizeof(int));
+}
+
+CombinationRule to_rule(const es_rule_desc* r, int M) {
+  if (!r) return CombinationRule::averaging();
+  const bool sm = r->member_softmax != 0;
+  switch (r->kind) {
+    case 1: return CombinationRule::majority_vote(sm);
+    case 2:
+      need(r->weights != nullptr, "weighted averaging needs weights");
+      return CombinationRule::weighted(std::vector<double>(r->weights, r->weights + M), sm);
+    default: return CombinationRule::averaging(sm);
+  }
+}
+
+PoolOptions to_opts(const es_pool_opts* o) {
+  PoolOptions p;
+  if (!o) return p;
+  if (o->device_map && o->n_device_map > 0)
+    p.device_map.assign(o->device_map, o->device_map + o->n_device_map);
+  p.copy_outputs = o->copy_outputs != 0;
+  p.warmup = o->warmup != 0;
+  p.sms_per_worker = o->sms_per_worker;
+  return p;
+}
+
+ScoreFn make_score(const ClusterSpec& cluster, const es_bench_cfg* cfg) {
+  const int mode = cfg ? cfg->mode : ES_BENCH_ANALYTIC;
+  if (mode == ES_BENCH_ANALYTIC)
+    return [&cluster](const AllocationMatrix& A) { return predict_ensemble_throughput(A, cluster); };
+  if (mode == ES_BENCH_CALLBACK) {
+    need(cfg->fn != nullptr, "callback bench needs fn");
+    return [cfg](const AllocationMatrix& A) {
+      return cfg->fn(A.cells().data(), A.device_count(), A.model_count(), cfg->user);
+    };
+  }
+  need(cfg->calib != nullptr, "device bench needs a calibration store");
+  PoolOptions opts = to_opts(cfg->opts);
+  std::shared_ptr<const SampleStore> calib = cfg->calib->store;
+  const int repeats = cfg->repeats > 0 ? cfg->repeats : 1;
+  return [&cluster, calib, repeats, opts](const AllocationMatrix& A) {
+    return bench(A, calib, cluster, repeats, opts).throughput;
+  };
+}
+
+}  // namespace
+
+extern "C" {
+
+int es_abi_version(void) { return ES_ABI_VERSION; }
+
+const char* es_status_name(es_status s) {
+  switch (s) {
+    case ES_OK: return "ES_OK";
+    case ES_ERR_INVALID_ARGUMENT: return "ES_ERR_INVALID_ARGUMENT";
+    case ES_ERR_SPEC: return "ES_ERR_SPEC";
+    case ES_ERR_ALLOCATION: return "ES_ERR_ALLOCATION";
+    case ES_ERR_STARTUP: return "ES_ERR_STARTUP";
+    case ES_ERR_BASELINE: return "ES_ERR_BASELINE";
+    case ES_ERR_CAP_EXCEEDED: return "ES_ERR_CAP_EXCEEDED";
+    case ES_ERR_PROTOCOL: return "ES_ERR_PROTOCOL";
+    case ES_ERR_CUDA: return "ES_ERR_CUDA";
+    case ES_ERR_INTERNAL: return "ES_ERR_INTERNAL";
+    case ES_ERR_BUFFER: return "ES_ERR_BUFFER";
+  }
+  return "ES_ERR_UNKNOWN";
+}
+
+const char* es_last_error(void) { return g_last_error.c_str(); }
+
+// ------------------------------------------------------------ host core
+es_status es_cluster_validate(const es_cluster_desc* c, char* warnings, size_t len) {
+  return guard([&] {
+    std::vector<std::string> w;
+    to_cluster(c).validate(&w);
+    std::string all;
+    for (const std::string& s : w) all += s + "\n";
+    if (warnings && len) std::snprintf(warnings, len, "%s", all.c_str());
+    return ES_OK;
+  });
+}
+
+es_status es_matrix_validate(const es_cluster_desc* c, const int* A, int* ok, int* violations,
+                             int cap, int* n) {
+  return guard([&] {
+    ClusterSpec s = to_cluster(c);
+    MatrixValidation v = validate_matrix(to_matrix(A, c->n_devices, c->n_models), s);
+    *ok = v.ok ? 1 : 0;
+    if (n) *n = static_cast<int>(v.violations.size());
+    for (int i = 0; violations && i < static_cast<int>(v.violations.size()) && i < cap; ++i) {
+      const MatrixViolation& x = v.violations[i];
+      violations[4 * i + 0] = x.kind == MatrixViolation::Kind::EmptyColumn ? 1 : 0;
+      violations[4 * i + 1] = x.device;
+      violations[4 * i + 2] = x.model;
+      violations[4 * i + 3] = x.value;
+    }
+    return ES_OK;
+  });
+}
+
+es_status es_num_segments(size_t nb, int segment_size, size_t* out) {
+  return guard([&] {
+    *out = num_segments(nb, segment_size);
+    return ES_OK;
+  });
+}
+
+es_status es_segment_bounds(int segment_id, int segment_size, size_t nb, size_t* start,
+                            size_t* end) {
+  return guard([&] {
+    Segment s = segment_bounds(segment_id, segment_size, nb);
+    *start = s.start;
+    *end = s.end;
+    return ES_OK;
+  });
+}
+
+es_status es_fit_mem(const es_cluster_desc* c, const int* A, double* used_mib, int* fits) {
+  return guard([&] {
+    MemoryReport r = fit_mem(to_matrix(A, c->n_devices, c->n_models), to_cluster(c));
+    for (std::size_t d = 0; used_mib && d < r.per_device.size(); ++d) used_mib[d] = r.per_device[d].used_mib;
+    *fits = r.fits ? 1 : 0;
+    return ES_OK;
+  });
+}
+
+es_status es_more_remaining_memory(const es_cluster_desc* c, const int* A, int kind, int* device) {
+  return guard([&] {
+    ClusterSpec s = to_cluster(c);
+    std::optional<int> d = more_remaining_memory(to_matrix(A, c->n_devices, c->n_models), 0,
+                                                 kind == 0 ? DeviceKind::CPU : DeviceKind::GPU, s);
+    *device = d.value_or(-1);
+    return ES_OK;
+  });
+}
+
+es_status es_predict_ensemble_throughput(const es_cluster_desc* c, const int* A, double* out) {
+  return guard([&] {
+    *out = predict_ensemble_throughput(to_matrix(A, c->n_devices, c->n_models), to_cluster(c));
+    return ES_OK;
+  });
+}
+
+es_status es_worst_fit_decreasing(const es_cluster_desc* c, int default_batch, int* A_out) {
+  return guard([&] {
+    write_matrix(worst_fit_decreasing(to_cluster(c), default_batch), A_out);
+    return ES_OK;
+  });
+}
+
+es_status es_neighborhood(const es_cluster_desc* c, const int* A, int* out, int cap, int* count) {
+  return guard([&] {
+    std::vector<AllocationMatrix> n =
+        neighborhood(to_matrix(A, c->n_devices, c->n_models), to_cluster(c));
+    *count = static_cast<int>(n.size());
+    const int cells = c->n_devices * c->n_models;
+    for (int i = 0; out && i < *count && i < cap; ++i) write_matrix(n[i], out + i * cells);
+    return ES_OK;
+  });
+}
+
+es_status es_neighborhood_stats(const es_cluster_desc* c, const int* A, size_t* size,
+                                size_t* forbidden) {
+  return guard([&] {
+    NeighborhoodStats s =
+        enumerated_neighborhood_stats(to_matrix(A, c->n_devices, c->n_models), to_cluster(c));
+    *size = s.size;
+    *forbidden = s.forbidden;
+    return ES_OK;
+  });
+}
+
+es_status es_count_total_matrices(int menu_size, int devices, int models, char* buf, size_t len) {
+  return guard([&] {
+    std::string s = count_total_matrices(menu_size, devices, models).str();
+    if (s.size() + 1 > len) return ES_ERR_BUFFER;
+    std::memcpy(buf, s.c_str(), s.size() + 1);
+    return ES_OK;
+  });
+}
+
+es_status es_count_total_neighs(int menu_size, int devices, int models, long long forbidden,
+                                long long* out) {
+  return guard([&] {
+    *out = count_total_neighs(menu_size, devices, models, forbidden);
+    return ES_OK;
+  });
+}
+
+es_status es_effective_max_iter(int devices, int models, int max_iter, int* out) {
+  return guard([&] {
+    *out = effective_max_iter(devices, models, max_iter);
+    return ES_OK;
+  });
+}
+
+es_status es_enumerate_matrices(const es_cluster_desc* c, const char* cap, int* out,
+                                size_t out_cap, size_t* count) {
+  return guard([&] {
+    ClusterSpec s = to_cluster(c);
+    const std::size_t cells = static_cast<std::size_t>(c->n_devices) * c->n_models;
+    std::size_t i = 0;
+    for_each_matrix(s, BigUInt::parse(cap ? cap : "0"), [&](const AllocationMatrix& A) {
+      if (out && i < out_cap) write_matrix(A, out + i * cells);
+      ++i;
+    });
+    *count = i;
+    return ES_OK;
+  });
+}
+
+es_status es_sample_indices(uint64_t seed, size_t n, size_t k, size_t* out) {
+  return guard([&] {
+    std::mt19937_64 gen(seed);
+    std::vector<std::size_t> v = sample_indices(gen, n, k);
+    std::memcpy(out, v.data(), v.size() * sizeof(std::size_t));
+    return ES_OK;
+  });
+}
+
+es_status es_bounded_greedy(const es_cluster_desc* c, const int* A0, int max_iter, int max_neighs,
+                            uint64_t seed, const es_bench_cfg* bcfg, int* A_out,
+                            es_greedy_trace* trace) {
+  return guard([&] {
+    ClusterSpec s = to_cluster(c);
+    int calls = 0;
+    ScoreFn inner = make_score(s, bcfg);
+    ScoreFn counted = [&](const AllocationMatrix& A) {
+      ++calls;
+      return inner(A);
+    };
+    GreedyResult r = bounded_greedy(to_matrix(A0, c->n_devices, c->n_models), s, counted,
+                                    {max_iter, max_neighs, seed});
+    write_matrix(r.matrix, A_out);
+    if (trace) {
+      trace->start_score = r.trace.start_score;
+      trace->final_score = r.trace.final_score;
+      trace->stop_reason = r.trace.stop_reason == StopReason::local_optimum ? 0 : 1;
+      trace->n_iters = static_cast<int>(r.trace.iterations.size());
+      trace->bench_calls = calls;
+      for (int i = 0; i < trace->n_iters && i < trace->iter_cap; ++i) {
+        const GreedyIteration& it = r.trace.iterations[i];
+        if (trace->iter_neighbors) trace->iter_neighbors[i] = it.neighbors_evaluated;
+        if (trace->iter_best) trace->iter_best[i] = it.best_score;
+        if (trace->iter_accepted) trace->iter_accepted[i] = it.accepted ? 1 : 0;
+      }
+    }
+    return ES_OK;
+  });
+}
+
+es_status es_bbs_baseline(const es_cluster_desc* c, const es_bench_cfg* bcfg, int* A_out,
+                          int* chosen, int* calls) {
+  return guard([&] {
+    ClusterSpec s = to_cluster(c);
+    ClusterScoreFn fn;
+    const int mode = bcfg ? bcfg->mode : ES_BENCH_ANALYTIC;
+    if (mode == ES_BENCH_ANALYTIC) {
+      fn = [](const AllocationMatrix& A, const ClusterSpec& cl) {
+        return predict_ensemble_throughput(A, cl);
+      };
+    } else if (mode == ES_BENCH_CALLBACK) {
+      need(bcfg->fn != nullptr, "callback bench needs fn");
+      fn = [bcfg](const AllocationMatrix& A, const ClusterSpec&) {
+        return bcfg->fn(A.cells().data(), A.device_count(), A.model_count(), bcfg->user);
+      };
+    } else {
+      need(bcfg->calib != nullptr, "device bench needs a calibration store");
+      PoolOptions opts = to_opts(bcfg->opts);
+      auto calib = bcfg->calib->store;
+      const int repeats = bcfg->repeats > 0 ? bcfg->repeats : 1;
+      fn = [calib, repeats, opts](const AllocationMatrix& A, const ClusterSpec& cl) {
+        return bench(A, calib, cl, repeats, opts).throughput;
+      };
+    }
+    BaselineResult r = bbs_baseline(s, fn);
+    write_matrix(r.matrix, A_out);
+    for (std::size_t m = 0; chosen && m < r.chosen_batches.size(); ++m) chosen[m] = r.chosen_batches[m];
+    *calls = r.bench_calls;
+    return ES_OK;
+  });
+}
+
+// ------------------------------------------------------------ device runtime
+es_status es_device_count(int* n) {
+  return guard([&] {
+    *n = 0;
+    if (cudaGetDeviceCount(n) != cudaSuccess) {
+      cudaGetLastError();
+      *n = 0;
+    }
+    return ES_OK;
+  });
+}
+
+es_status es_store_create(const float* X, size_t nb, size_t width, int copy, es_store** out) {
+  return guard([&] {
+    need(X != nullptr || nb * width == 0, "features are NULL");
+    auto h = std::make_unique<es_store>();
+    if (copy)
+      h->store = std::make_shared<SampleStore>(std::vector<float>(X, X + nb * width), nb, width);
+    else
+      h->store = SampleStore::borrow(X, nb, width);
+    *out = h.release();
+    return ES_OK;
+  });
+}
+
+es_status es_store_synthetic(uint64_t seed, size_t nb, size_t width, int device, es_store** out) {
+  return guard([&] {
+    auto h = std::make_unique<es_store>();
+    h->store = SampleStore::synthetic(seed, nb, width, device);
+    *out = h.release();
+    return ES_OK;
+  });
+}
+
+void es_store_destroy(es_store* s) { delete s; }
+
+es_status es_system_create(const es_cluster_desc* c, const int* A, const es_rule_desc* rule,
+                           const es_pool_opts* opts, es_system** out) {
+  return guard([&] {
+    ClusterSpec s = to_cluster(c);
+    auto h = std::make_unique<es_system>();
+    h->models = c->n_models;
+    h->sys = std::make_unique<InferenceSystem>(to_matrix(A, c->n_devices, c->n_models), s,
+                                               to_rule(rule, c->n_models), to_opts(opts));
+    *out = h.release();
+    return ES_OK;
+  });
+}
+
+es_status es_system_begin_run(es_system* s, es_store* X, const es_rule_desc* rule) {
+  return guard([&] {
+    need(s && X, "NULL handle");
+    if (rule)
+      s->sys->begin_run(X->store, to_rule(rule, s->models));
+    else
+      s->sys->begin_run(X->store);
+    return ES_OK;
+  });
+}
+
+es_status es_system_broadcast(es_system* s, size_t* segments) {
+  return guard([&] {
+    need(s != nullptr, "NULL handle");
+    std::size_t n = s->sys->broadcast();
+    if (segments) *segments = n;
+    return ES_OK;
+  });
+}
+
+namespace {
+void export_run(const RunOutput& out, float* Y, int32_t* winners, es_run_stats* stats) {
+  if (Y && !out.combined.empty()) std::memcpy(Y, out.combined.data(), out.combined.size() * sizeof(float));
+  if (winners && !out.winners.empty())
+    std::memcpy(winners, out.winners.data(), out.winners.size() * sizeof(int32_t));
+  if (stats) {
+    stats->nb_samples = out.stats.nb_samples;
+    stats->segments = out.stats.segments;
+    stats->data_messages = out.stats.data_messages;
+    stats->elapsed_s = out.stats.elapsed_s;
+  }
+}
+}  // namespace
+
+es_status es_system_await_run(es_system* s, float* Y, int32_t* winners, es_run_stats* stats) {
+  return guard([&] {
+    need(s != nullptr, "NULL handle");
+    export_run(s->sys->await_run(), Y, winners, stats);
+    return ES_OK;
+  });
+}
+
+es_status es_system_run(es_system* s, es_store* X, float* Y, int32_t* winners,
+                        es_run_stats* stats) {
+  return guard([&] {
+    need(s && X, "NULL handle");
+    export_run(s->sys->run(X->store), Y, winners, stats);
+    return ES_OK;
+  });
+}
+
+es_status es_system_run_host(es_system* s, const float* X, size_t nb, size_t width, float* Y,
+                             int32_t* labels, double* elapsed_s) {
+  return guard([&] {
+    need(s && X, "NULL handle");
+    double t = s->sys->run_host(X, nb, width, Y, labels);
+    if (elapsed_s) *elapsed_s = t;
+    return ES_OK;
+  });
+}
+
+es_status es_system_info(es_system* s, int* workers, int* workers_per_model, int* launches,
+                         int* combine_device) {
+  return guard([&] {
+    need(s != nullptr, "NULL handle");
+    if (workers) *workers = s->sys->worker_count();
+    if (workers_per_model) {
+      std::vector<int> w = s->sys->workers_per_model();
+      std::memcpy(workers_per_model, w.data(), w.size() * sizeof(int));
+    }
+    if (launches) *launches = s->sys->launches_last_run();
+    if (combine_device) *combine_device = s->sys->combine_device();
+    return ES_OK;
+  });
+}
+
+es_status es_system_timing(es_system* s, double* member_ms, double* combine_ms) {
+  return guard([&] {
+    need(s != nullptr, "NULL handle");
+    for (int w = 0; member_ms && w < s->sys->worker_count(); ++w) member_ms[w] = s->sys->last_member_ms(w);
+    if (combine_ms) *combine_ms = s->sys->last_combine_ms();
+    return ES_OK;
+  });
+}
+
+es_status es_system_shutdown(es_system* s) {
+  return guard([&] {
+    need(s != nullptr, "NULL handle");
+    s->sys->shutdown();
+    return ES_OK;
+  });
+}
+
+void es_system_destroy(es_system* s) { delete s; }
+
+es_status es_run_inference(const es_cluster_desc* c, const int* A, const es_rule_desc* rule,
+                           es_store* X, const es_pool_opts* opts, float* Y, int32_t* winners,
+                           es_run_stats* stats) {
+  return guard([&] {
+    need(X != nullptr, "no sample store");
+    ClusterSpec s = to_cluster(c);
+    InferenceResult r = run_inference(X->store, to_matrix(A, c->n_devices, c->n_models), s,
+                                      to_rule(rule, c->n_models), Mode::Deploy, to_opts(opts));
+    export_run(*r.output, Y, winners, stats);
+    return ES_OK;
+  });
+}
+
+es_status es_bench(const es_cluster_desc* c, const int* A, es_store* calib, int repeats,
+                   const es_pool_opts* opts, es_bench_result* out) {
+  return guard([&] {
+    ClusterSpec s = to_cluster(c);
+    BenchResult r = bench(to_matrix(A, c->n_devices, c->n_models), calib ? calib->store : nullptr,
+                          s, repeats, to_opts(opts));
+    out->throughput = r.throughput;
+    out->elapsed_s = r.elapsed_s;
+    out->nb_samples = r.nb_samples;
+    out->n_runs = static_cast<int>(std::min<std::size_t>(r.runs.size(), 64));
+    for (int i = 0; i < out->n_runs; ++i) out->runs[i] = r.runs[i];
+    out->rsd = r.rsd;
+    return ES_OK;
+  });
+}
+
+// ------------------------------------------------------------ Predictor seam
+es_status es_member_create(int device, const es_model_desc* model, int model_id, int batch,
+                           double device_load_mib, double capacity_mib, es_member** out) {
+  return guard([&] {
+    need(model != nullptr, "model descriptor is NULL");
+    auto h = std::make_unique<es_member>();
+    h->predictor = std::make_unique<B200Predictor>(device, to_model(*model, model_id), batch,
+                                                   device_load_mib, capacity_mib);
+    if (!h->predictor->load()) throw StartupError("member load() reported out-of-memory");
+    *out = h.release();
+    return ES_OK;
+  });
+}
+
+es_status es_member_predict(es_member* m, const float* features, size_t first_index, size_t rows,
+                            size_t width, float* out) {
+  return guard([&] {
+    need(m != nullptr, "NULL handle");
+    m->predictor->predict(features, first_index, rows, width, out);
+    return ES_OK;
+  });
+}
+
+void es_member_destroy(es_member* m) { delete m; }
+
+es_status es_combine(const es_rule_desc* rule, int M, int C, size_t rows,
+                     const float* const* blocks, float* Y, int32_t* winners) {
+  return guard([&] {
+    combine_blocks(to_rule(rule, M), M, C, rows, blocks, Y, winners);
+    return ES_OK;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,871 @@
+// enserve-b200 runtime: device members, sample stores, the GPU InferenceSystem
+// and bench().  See runtime.hpp for the mapping onto the reference pipeline.
+#include "enserve/runtime.hpp"
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+
+#include "../cuda/aux_kernels.cuh"
+#include "../cuda/mlp_kernel.cuh"
+#include "enserve/placement.hpp"
+
+namespace enserve {
+
+namespace {
+
+[[noreturn]] void throw_cuda(cudaError_t e, const char* what) {
+  cudaGetLastError();  // clear a sticky launch error so later calls report fresh state
+  throw DeviceError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define ES_CUDA(call)                                  \
+  do {                                                 \
+    cudaError_t es_err_ = (call);                      \
+    if (es_err_ != cudaSuccess) throw_cuda(es_err_, #call); \
+  } while (0)
+
+#define ES_LAUNCH(call)                                                       \
+  do {                                                                        \
+    if ((call) != 0) throw_cuda(cudaGetLastError(), "kernel launch " #call); \
+  } while (0)
+
+int visible_devices() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n < 1)
+    throw DeviceError("no CUDA device visible to the enserve-b200 runtime");
+  return n;
+}
+
+// RAII device selection.
+struct OnDevice {
+  int prev = 0;
+  explicit OnDevice(int dev) {
+    cudaGetDevice(&prev);
+    ES_CUDA(cudaSetDevice(dev));
+  }
+  ~OnDevice() { cudaSetDevice(prev); }
+};
+
+bool member_kernel_simt() {
+  const char* v = std::getenv("ES_MEMBER_KERNEL");
+  return v && std::strcmp(v, "simt") == 0;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- rule
+CombinationRule CombinationRule::weighted(std::vector<double> weights, bool softmax) {
+  double total = 0.0;
+  for (double w : weights) {
+    if (w < 0) throw SpecError("combination weights must be nonnegative");
+    total += w;
+  }
+  if (std::abs(total - 1.0) > 1e-9)
+    throw SpecError("combination weights must sum to 1, got " + std::to_string(total));
+  return {Kind::weighted_averaging, std::move(weights), softmax};
+}
+
+std::string CombinationRule::name() const {
+  switch (kind) {
+    case Kind::majority_vote: return "vote";
+    case Kind::weighted_averaging: return "wavg";
+    default: return "avg";
+  }
+}
+
+CombinationRule CombinationRule::from_name(const std::string& name, int model_count) {
+  if (name == "avg") return averaging();
+  if (name == "vote") return majority_vote();
+  if (name == "wavg") return weighted(std::vector<double>(model_count, 1.0 / model_count));
+  throw SpecError("unknown combination rule '" + name + "'");
+}
+
+// ---------------------------------------------------------------- store
+SampleStore::SampleStore(std::vector<float> data, std::size_t nb, std::size_t width)
+    : owned_(std::move(data)), nb_(nb), width_(width) {
+  if (owned_.size() != nb * width)
+    throw SpecError("sample store size does not match nb_samples * width");
+  host_ = owned_.data();
+}
+
+std::shared_ptr<SampleStore> SampleStore::borrow(const float* data, std::size_t nb,
+                                                 std::size_t width) {
+  std::shared_ptr<SampleStore> s(new SampleStore());
+  s->host_ = data;
+  s->nb_ = nb;
+  s->width_ = width;
+  return s;
+}
+
+std::shared_ptr<SampleStore> SampleStore::synthetic(std::uint64_t seed, std::size_t nb,
+                                                    std::size_t width, int device) {
+  std::shared_ptr<SampleStore> s(new SampleStore());
+  s->nb_ = nb;
+  s->width_ = width;
+  s->synthetic_ = true;
+  s->synthetic_seed_ = seed;
+  s->device_replica(device);
+  return s;
+}
+
+SampleStore::~SampleStore() {
+  for (std::size_t d = 0; d < replicas_.size(); ++d)
+    if (replicas_[d]) {
+      cudaSetDevice(static_cast<int>(d));
+      cudaFree(replicas_[d]);
+    }
+}
+
+const void* SampleStore::device_replica(int device) const {
+  if (replicas_.size() <= static_cast<std::size_t>(device)) replicas_.resize(device + 1, nullptr);
+  if (replicas_[device]) return replicas_[device];
+  OnDevice on(device);
+  const std::size_t n = nb_ * width_;
+  void* bf = nullptr;
+  ES_CUDA(cudaMalloc(&bf, std::max<std::size_t>(n, 1) * sizeof(__nv_bfloat16)));
+  if (synthetic_) {
+    ES_LAUNCH(es::generate_features_bf16(synthetic_seed_, n, static_cast<__nv_bfloat16*>(bf), 0));
+  } else if (n > 0) {
+    // Stage through fp32 in bounded chunks, convert on device.
+    const std::size_t chunk = std::min<std::size_t>(n, std::size_t(1) << 26);
+    float* stage = nullptr;
+    ES_CUDA(cudaMalloc(&stage, chunk * sizeof(float)));
+    for (std::size_t off = 0; off < n; off += chunk) {
+      const std::size_t len = std::min(chunk, n - off);
+      ES_CUDA(cudaMemcpy(stage, host_ + off, len * sizeof(float), cudaMemcpyHostToDevice));
+      ES_LAUNCH(es::convert_f32_to_bf16(stage, static_cast<__nv_bfloat16*>(bf) + off, len, 0));
+    }
+    ES_CUDA(cudaDeviceSynchronize());
+    cudaFree(stage);
+  }
+  ES_CUDA(cudaDeviceSynchronize());
+  replicas_[device] = bf;
+  return bf;
+}
+
+// ---------------------------------------------------------------- member
+class DeviceMember {
+ public:
+  // load(): false = out of memory (tile plan does not fit an SM, or a device
+  // allocation failed); other CUDA errors throw.
+  bool load(int device, const ModelSpec& model, int batch) {
+    device_ = device;
+    model_ = model;
+    batch_ = batch;
+    C_ = model.output_width;
+    if (model.arch.kind == MemberArch::Kind::Synthetic) return true;
+    const MemberArch& a = model.arch;
+    if (a.layers() != 2)
+      throw SpecError(model.name + ": the sm_100a member kernel runs 2-layer MLPs (one hidden layer)");
+    K_ = a.widths[0];
+    H_ = a.widths[1];
+    if (!es::mlp2_plan(K_, H_, C_, batch, &plan_)) return false;
+    OnDevice on(device);
+    const std::size_t w1 = static_cast<std::size_t>(H_) * K_ * 2, b1 = H_ * 4u,
+                      w2 = static_cast<std::size_t>(C_) * H_ * 2, b2 = C_ * 4u;
+    auto up = [](std::size_t x) { return (x + 255) / 256 * 256; };
+    off_b1_ = up(w1);
+    off_w2_ = off_b1_ + up(b1);
+    off_b2_ = off_w2_ + up(w2);
+    bytes_ = off_b2_ + up(b2);
+    cudaError_t e = cudaMalloc(&weights_, bytes_);
+    if (e == cudaErrorMemoryAllocation) {
+      cudaGetLastError();
+      weights_ = nullptr;
+      return false;
+    }
+    ES_CUDA(e);
+    uint8_t* base = static_cast<uint8_t*>(weights_);
+    for (int l = 0; l < 2; ++l) {
+      const int fi = a.widths[l], fo = a.widths[l + 1];
+      const float limit = static_cast<float>(std::sqrt(6.0 / static_cast<double>(fi + fo)));
+      ES_LAUNCH(es::generate_dense_layer(
+          a.weight_seed, l, fi, fo, limit,
+          reinterpret_cast<__nv_bfloat16*>(base + (l == 0 ? 0 : off_w2_)),
+          reinterpret_cast<float*>(base + (l == 0 ? off_b1_ : off_b2_)), 0));
+    }
+    ES_CUDA(cudaDeviceSynchronize());
+    return true;
+  }
+
+  ~DeviceMember() {
+    if (weights_) {
+      cudaSetDevice(device_);
+      cudaFree(weights_);
+    }
+  }
+
+  // Logits for every row of segments [s0, s1) into out (rows indexed globally).
+  // Returns the number of kernel launches issued.
+  int forward(const void* x, long long nb, int seg_size, long long s0, long long s1, float* out,
+              int grid, cudaStream_t stream) const {
+    if (s1 <= s0 || nb == 0) return 0;
+    if (model_.arch.kind == MemberArch::Kind::Synthetic) {
+      ES_LAUNCH(es::synthetic_member_launch(model_.id, C_, seg_size, s0, s1, nb, out, stream));
+      return 1;
+    }
+    const uint8_t* base = static_cast<const uint8_t*>(weights_);
+    if (member_kernel_simt()) {
+      const long long r0 = s0 * seg_size, r1 = std::min<long long>(s1 * seg_size, nb);
+      ES_LAUNCH(es::mlp2_simt_launch(
+          static_cast<const __nv_bfloat16*>(x), nb, K_,
+          reinterpret_cast<const __nv_bfloat16*>(base), reinterpret_cast<const float*>(base + off_b1_),
+          H_, reinterpret_cast<const __nv_bfloat16*>(base + off_w2_),
+          reinterpret_cast<const float*>(base + off_b2_), C_, r0, r1, out, stream));
+      return 1;
+    }
+    es::Mlp2Args args;
+    args.L = plan_;
+    args.b = batch_;
+    args.seg_size = seg_size;
+    args.seg_begin = s0;
+    args.seg_end = s1;
+    args.nb = nb;
+    args.bias1 = reinterpret_cast<const float*>(base + off_b1_);
+    args.bias2 = reinterpret_cast<const float*>(base + off_b2_);
+    args.out = out;
+    ES_LAUNCH(es::mlp2_launch(args, x, base, base + off_w2_, grid, stream));
+    return 1;
+  }
+
+  int device() const { return device_; }
+  std::size_t weight_bytes() const { return bytes_; }
+  const es::Mlp2Layout& plan() const { return plan_; }
+
+ private:
+  int device_ = 0;
+  ModelSpec model_;
+  int batch_ = 1;
+  int K_ = 0, H_ = 0, C_ = 1;
+  es::Mlp2Layout plan_{};
+  void* weights_ = nullptr;
+  std::size_t bytes_ = 0, off_b1_ = 0, off_w2_ = 0, off_b2_ = 0;
+};
+
+// ---------------------------------------------------------------- system
+struct InferenceSystem::Worker {
+  int model = 0;
+  int row = 0;   // cluster device id
+  int phys = 0;  // CUDA ordinal
+  int batch = 1;
+  int colocated = 1;
+  std::unique_ptr<DeviceMember> member;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev_begin = nullptr, ev_done = nullptr;
+  long long seg_begin = 0, seg_end = 0;  // this run's share
+  float* staging = nullptr;              // remote worker: local logits [nb][C]
+  std::size_t staging_rows = 0;
+};
+
+struct InferenceSystem::Impl {
+  cudaStream_t main = nullptr;
+  cudaEvent_t start = nullptr, combine_begin = nullptr, end = nullptr;
+  std::vector<float*> logits;  // per model, on combine device
+  float* y = nullptr;
+  int32_t* labels = nullptr;
+  std::size_t cap_rows = 0;
+  // run_host staging
+  float* x32 = nullptr;
+  void* x16 = nullptr;
+  std::size_t host_cap = 0;
+  std::shared_ptr<const SampleStore> store;
+  CombinationRule rule;
+  std::size_t segments = 0;
+};
+
+InferenceSystem::InferenceSystem(const AllocationMatrix& A, const ClusterSpec& cluster,
+                                 CombinationRule rule, PoolOptions options)
+    : matrix_(A), cluster_(cluster), rule_(std::move(rule)), options_(std::move(options)),
+      impl_(std::make_unique<Impl>()) {
+  MatrixValidation verdict = validate_matrix(A, cluster);
+  if (!verdict.ok) {
+    std::string what = "allocation matrix is invalid:";
+    for (const MatrixViolation& v : verdict.violations) what += " " + v.describe() + ";";
+    throw SpecError(what);
+  }
+  output_width_ = cluster.models.front().output_width;
+  for (const ModelSpec& m : cluster.models)
+    if (m.output_width != output_width_) throw SpecError("ensemble models disagree on output width");
+  if (output_width_ > es::kMaxClasses)
+    throw SpecError("output width above " + std::to_string(es::kMaxClasses) + " classes");
+  if (cluster.model_count() > es::kMaxMembers)
+    throw SpecError("more than " + std::to_string(es::kMaxMembers) + " ensemble members");
+  if (rule_.kind == CombinationRule::Kind::weighted_averaging &&
+      rule_.weights.size() != static_cast<std::size_t>(cluster.model_count()))
+    throw SpecError("weighted averaging needs one weight per model");
+
+  const int gpus = visible_devices();
+  auto phys_of = [&](int row) {
+    if (!options_.device_map.empty()) {
+      if (row >= static_cast<int>(options_.device_map.size()) || options_.device_map[row] >= gpus)
+        throw SpecError("device_map has no valid CUDA ordinal for " + cluster.devices[row].label());
+      return options_.device_map[row];
+    }
+    return row % gpus;
+  };
+
+  // One worker per nonzero cell, row-major (pipeline.cpp:106-124).
+  bool oom = false;
+  for (int d = 0; d < A.device_count() && !oom; ++d) {
+    const double load = device_load(A, d, cluster_);
+    for (int m = 0; m < A.model_count(); ++m) {
+      const int b = A.at(d, m);
+      if (b == 0) continue;
+      auto w = std::make_unique<Worker>();
+      w->model = m;
+      w->row = d;
+      w->phys = phys_of(d);
+      w->batch = b;
+      w->colocated = A.row_worker_count(d);
+      // Predictor::load(): the declared footprint must fit (the reference
+      // backend's rule, backend.cpp:41), and the real device must host it.
+      w->member = std::make_unique<DeviceMember>();
+      if (load > cluster_.devices[d].memory_mib ||
+          !w->member->load(w->phys, cluster_.models[m], b)) {
+        oom = true;
+        break;
+      }
+      OnDevice on(w->phys);
+      ES_CUDA(cudaStreamCreateWithFlags(&w->stream, cudaStreamNonBlocking));
+      ES_CUDA(cudaEventCreate(&w->ev_begin));
+      ES_CUDA(cudaEventCreate(&w->ev_done));
+      workers_.push_back(std::move(w));
+    }
+  }
+  if (oom) {
+    shutdown();
+    throw StartupError("a worker reported out-of-memory during startup");
+  }
+  combine_dev_ = workers_.front()->phys;
+  OnDevice on(combine_dev_);
+  ES_CUDA(cudaStreamCreateWithFlags(&impl_->main, cudaStreamNonBlocking));
+  ES_CUDA(cudaEventCreate(&impl_->start));
+  ES_CUDA(cudaEventCreate(&impl_->combine_begin));
+  ES_CUDA(cudaEventCreate(&impl_->end));
+  impl_->logits.assign(cluster.model_count(), nullptr);
+}
+
+InferenceSystem::~InferenceSystem() {
+  try {
+    shutdown();
+  } catch (...) {
+  }
+}
+
+void InferenceSystem::shutdown() {
+  if (shut_down_) return;
+  shut_down_ = true;
+  for (auto& w : workers_) {
+    cudaSetDevice(w->phys);
+    if (w->stream) cudaStreamSynchronize(w->stream);
+    if (w->staging) cudaFree(w->staging);
+    if (w->stream) cudaStreamDestroy(w->stream);
+    if (w->ev_begin) cudaEventDestroy(w->ev_begin);
+    if (w->ev_done) cudaEventDestroy(w->ev_done);
+    w->member.reset();
+  }
+  if (impl_ && impl_->main) {
+    cudaSetDevice(combine_dev_);
+    cudaStreamSynchronize(impl_->main);
+    for (float* p : impl_->logits) cudaFree(p);
+    cudaFree(impl_->y);
+    cudaFree(impl_->labels);
+    cudaFree(impl_->x32);
+    cudaFree(impl_->x16);
+    cudaEventDestroy(impl_->start);
+    cudaEventDestroy(impl_->combine_begin);
+    cudaEventDestroy(impl_->end);
+    cudaStreamDestroy(impl_->main);
+    impl_->main = nullptr;
+  }
+}
+
+std::vector<int> InferenceSystem::workers_per_model() const {
+  std::vector<int> n(cluster_.model_count(), 0);
+  for (const auto& w : workers_) ++n[w->model];
+  return n;
+}
+
+void InferenceSystem::begin_run(std::shared_ptr<const SampleStore> X) { begin_run(std::move(X), rule_); }
+
+void InferenceSystem::begin_run(std::shared_ptr<const SampleStore> X, CombinationRule rule) {
+  if (!X) throw SpecError("no sample store");
+  if (shut_down_) throw Error("inference system is shut down");
+  if (run_open_) throw Error("previous run still open");
+  if (rule.kind == CombinationRule::Kind::weighted_averaging &&
+      rule.weights.size() != static_cast<std::size_t>(cluster_.model_count()))
+    throw SpecError("weighted averaging needs one weight per model");
+  for (const ModelSpec& m : cluster_.models)
+    if (m.arch.kind == MemberArch::Kind::MLP && static_cast<std::size_t>(m.arch.widths[0]) != X->width())
+      throw SpecError(m.name + ": input width " + std::to_string(m.arch.widths[0]) +
+                      " differs from the store's " + std::to_string(X->width()));
+  const std::size_t nb = X->nb_samples();
+  const int C = output_width_;
+  // Device replicas (untimed, like the reference's begin_run).
+  for (const auto& w : workers_) X->device_replica(w->phys);
+  {
+    OnDevice on(combine_dev_);
+    if (nb > impl_->cap_rows) {
+      for (float*& p : impl_->logits) {
+        cudaFree(p);
+        p = nullptr;
+      }
+      cudaFree(impl_->y);
+      cudaFree(impl_->labels);
+      const std::size_t rows = std::max<std::size_t>(nb, 1);
+      for (float*& p : impl_->logits) ES_CUDA(cudaMalloc(&p, rows * C * sizeof(float)));
+      ES_CUDA(cudaMalloc(&impl_->y, rows * C * sizeof(float)));
+      ES_CUDA(cudaMalloc(&impl_->labels, rows * sizeof(int32_t)));
+      impl_->cap_rows = rows;
+    }
+  }
+  // Segment shares: a model's workers split its segments into contiguous,
+  // equal runs in worker (row-major) order; each segment exactly once.
+  const std::size_t S = num_segments(nb, cluster_.segment_size);
+  std::vector<int> per_model = workers_per_model();
+  std::vector<int> seen(cluster_.model_count(), 0);
+  for (auto& w : workers_) {
+    const int k = seen[w->model]++, n = per_model[w->model];
+    w->seg_begin = static_cast<long long>(S * k / n);
+    w->seg_end = static_cast<long long>(S * (k + 1) / n);
+    if (w->phys != combine_dev_ && w->staging_rows < nb) {
+      OnDevice on(w->phys);
+      cudaFree(w->staging);
+      ES_CUDA(cudaMalloc(&w->staging, std::max<std::size_t>(nb, 1) * C * sizeof(float)));
+      w->staging_rows = nb;
+    }
+  }
+  impl_->store = std::move(X);
+  impl_->rule = std::move(rule);
+  impl_->segments = S;
+  run_open_ = true;
+}
+
+std::size_t InferenceSystem::broadcast() {
+  if (!run_open_) throw Error("broadcast without begin_run");
+  const SampleStore& X = *impl_->store;
+  const long long nb = static_cast<long long>(X.nb_samples());
+  const int C = output_width_;
+  launches_ = 0;
+  {
+    OnDevice on(combine_dev_);
+    ES_CUDA(cudaEventRecord(impl_->start, impl_->main));
+  }
+  for (auto& w : workers_) {
+    OnDevice on(w->phys);
+    ES_CUDA(cudaStreamWaitEvent(w->stream, impl_->start, 0));
+    ES_CUDA(cudaEventRecord(w->ev_begin, w->stream));
+    const bool remote = w->phys != combine_dev_;
+    float* out = remote ? w->staging : impl_->logits[w->model];
+    int grid = es::num_sms(w->phys);
+    if (options_.sms_per_worker > 0) grid = std::min(grid, options_.sms_per_worker);
+    launches_ += w->member->forward(X.device_replica(w->phys), nb, cluster_.segment_size,
+                                    w->seg_begin, w->seg_end, out, grid, w->stream);
+    if (remote && w->seg_end > w->seg_begin) {
+      const long long r0 = w->seg_begin * cluster_.segment_size;
+      const long long r1 = std::min<long long>(w->seg_end * cluster_.segment_size, nb);
+      ES_CUDA(cudaMemcpyPeerAsync(impl_->logits[w->model] + r0 * C, combine_dev_,
+                                  w->staging + r0 * C, w->phys,
+                                  static_cast<std::size_t>(r1 - r0) * C * sizeof(float), w->stream));
+    }
+    ES_CUDA(cudaEventRecord(w->ev_done, w->stream));
+  }
+  OnDevice on(combine_dev_);
+  for (auto& w : workers_) ES_CUDA(cudaStreamWaitEvent(impl_->main, w->ev_done, 0));
+  ES_CUDA(cudaEventRecord(impl_->combine_begin, impl_->main));
+  es::CombineArgs ca;
+  const CombinationRule& rule = impl_->rule;
+  ca.M = cluster_.model_count();
+  ca.C = C;
+  ca.rows = nb;
+  ca.y = impl_->y;
+  ca.argmax = impl_->labels;
+  ca.softmax = rule.member_softmax ? 1 : 0;
+  ca.rule = rule.kind == CombinationRule::Kind::majority_vote ? es::kVote
+            : rule.kind == CombinationRule::Kind::weighted_averaging ? es::kWeighted
+                                                                       : es::kAverage;
+  const float inv = 1.0f / static_cast<float>(ca.M);
+  for (int m = 0; m < ca.M; ++m) {
+    ca.logits[m] = impl_->logits[m];
+    ca.weight[m] = rule.kind == CombinationRule::Kind::weighted_averaging
+                       ? static_cast<float>(rule.weights[m])
+                       : inv;
+  }
+  if (nb > 0) {
+    ES_LAUNCH(es::combine_launch(ca, impl_->main));
+    ++launches_;
+  }
+  ES_CUDA(cudaEventRecord(impl_->end, impl_->main));
+  return impl_->segments;
+}
+
+RunOutput InferenceSystem::await_run() {
+  if (!run_open_) throw Error("await without begin_run");
+  run_open_ = false;
+  OnDevice on(combine_dev_);
+  cudaError_t e = cudaEventSynchronize(impl_->end);
+  if (e != cudaSuccess) throw_cuda(e, "run failed on device");
+  for (auto& w : workers_) {
+    OnDevice wd(w->phys);
+    ES_CUDA(cudaStreamSynchronize(w->stream));
+  }
+  float ms = 0.0f;
+  ES_CUDA(cudaEventElapsedTime(&ms, impl_->start, impl_->end));
+  const SampleStore& X = *impl_->store;
+  const std::size_t nb = X.nb_samples();
+  RunOutput out;
+  out.output_width = output_width_;
+  out.stats.nb_samples = nb;
+  out.stats.segments = impl_->segments;
+  out.stats.data_messages = impl_->segments * static_cast<std::size_t>(cluster_.model_count());
+  out.stats.segment_rows.resize(impl_->segments);
+  for (std::size_t s = 0; s < impl_->segments; ++s)
+    out.stats.segment_rows[s] = segment_bounds(static_cast<int>(s), cluster_.segment_size, nb).size();
+  out.stats.elapsed_s = ms * 1e-3;
+  if (options_.copy_outputs && nb > 0) {
+    out.combined.resize(nb * output_width_);
+    out.winners.resize(nb);
+    ES_CUDA(cudaMemcpy(out.combined.data(), impl_->y, out.combined.size() * sizeof(float),
+                       cudaMemcpyDeviceToHost));
+    ES_CUDA(cudaMemcpy(out.winners.data(), impl_->labels, nb * sizeof(int32_t),
+                       cudaMemcpyDeviceToHost));
+  }
+  return out;
+}
+
+RunOutput InferenceSystem::run(std::shared_ptr<const SampleStore> X) { return run(std::move(X), rule_); }
+
+RunOutput InferenceSystem::run(std::shared_ptr<const SampleStore> X, CombinationRule rule) {
+  begin_run(std::move(X), std::move(rule));
+  broadcast();
+  return await_run();
+}
+
+double InferenceSystem::last_member_ms(int worker) const {
+  const Worker& w = *workers_.at(worker);
+  OnDevice on(w.phys);
+  float ms = 0.0f;
+  if (cudaEventElapsedTime(&ms, w.ev_begin, w.ev_done) != cudaSuccess) return -1.0;
+  return ms;
+}
+
+double InferenceSystem::last_combine_ms() const {
+  OnDevice on(combine_dev_);
+  float ms = 0.0f;
+  if (cudaEventElapsedTime(&ms, impl_->combine_begin, impl_->end) != cudaSuccess) return -1.0;
+  return ms;
+}
+
+double InferenceSystem::run_host(const float* X, std::size_t nb, std::size_t width, float* Y_out,
+                                 std::int32_t* labels_out) {
+  for (const auto& w : workers_)
+    if (w->phys != combine_dev_) throw SpecError("run_host needs every worker on one GPU");
+  if (run_open_) throw Error("previous run still open");
+  OnDevice on(combine_dev_);
+  const std::size_t n = nb * width;
+  if (n > impl_->host_cap) {
+    cudaFree(impl_->x32);
+    cudaFree(impl_->x16);
+    impl_->x32 = nullptr;
+    impl_->x16 = nullptr;
+    ES_CUDA(cudaMalloc(&impl_->x32, std::max<std::size_t>(n, 1) * sizeof(float)));
+    ES_CUDA(cudaMalloc(&impl_->x16, std::max<std::size_t>(n, 1) * sizeof(__nv_bfloat16)));
+    impl_->host_cap = n;
+  }
+  const int C = output_width_;
+  // Segment shares as in begin_run; X itself is staged inside the window.
+  const std::size_t S = num_segments(nb, cluster_.segment_size);
+  std::vector<int> per_model = workers_per_model();
+  std::vector<int> seen(cluster_.model_count(), 0);
+  for (auto& w : workers_) {
+    const int k = seen[w->model]++, cnt = per_model[w->model];
+    w->seg_begin = static_cast<long long>(S * k / cnt);
+    w->seg_end = static_cast<long long>(S * (k + 1) / cnt);
+  }
+  if (nb > impl_->cap_rows) {
+    for (float*& p : impl_->logits) {
+      cudaFree(p);
+      p = nullptr;
+    }
+    cudaFree(impl_->y);
+    cudaFree(impl_->labels);
+    for (float*& p : impl_->logits) ES_CUDA(cudaMalloc(&p, nb * C * sizeof(float)));
+    ES_CUDA(cudaMalloc(&impl_->y, nb * C * sizeof(float)));
+    ES_CUDA(cudaMalloc(&impl_->labels, nb * sizeof(int32_t)));
+    impl_->cap_rows = nb;
+  }
+  launches_ = 0;
+  ES_CUDA(cudaEventRecord(impl_->start, impl_->main));
+  ES_CUDA(cudaMemcpyAsync(impl_->x32, X, n * sizeof(float), cudaMemcpyHostToDevice, impl_->main));
+  ES_LAUNCH(es::convert_f32_to_bf16(impl_->x32, static_cast<__nv_bfloat16*>(impl_->x16), n,
+                                    impl_->main));
+  ++launches_;
+  cudaEvent_t ready;
+  ES_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  ES_CUDA(cudaEventRecord(ready, impl_->main));
+  for (auto& w : workers_) {
+    ES_CUDA(cudaStreamWaitEvent(w->stream, ready, 0));
+    launches_ += w->member->forward(impl_->x16, static_cast<long long>(nb), cluster_.segment_size,
+                                    w->seg_begin, w->seg_end, impl_->logits[w->model],
+                                    es::num_sms(w->phys), w->stream);
+    ES_CUDA(cudaEventRecord(w->ev_done, w->stream));
+    ES_CUDA(cudaStreamWaitEvent(impl_->main, w->ev_done, 0));
+  }
+  es::CombineArgs ca;
+  ca.M = cluster_.model_count();
+  ca.C = C;
+  ca.rows = static_cast<long long>(nb);
+  ca.y = impl_->y;
+  ca.argmax = impl_->labels;
+  ca.softmax = rule_.member_softmax ? 1 : 0;
+  ca.rule = rule_.kind == CombinationRule::Kind::majority_vote ? es::kVote
+            : rule_.kind == CombinationRule::Kind::weighted_averaging ? es::kWeighted
+                                                                        : es::kAverage;
+  for (int m = 0; m < ca.M; ++m) {
+    ca.logits[m] = impl_->logits[m];
+    ca.weight[m] = rule_.kind == CombinationRule::Kind::weighted_averaging
+                       ? static_cast<float>(rule_.weights[m])
+                       : 1.0f / static_cast<float>(ca.M);
+  }
+  ES_LAUNCH(es::combine_launch(ca, impl_->main));
+  ++launches_;
+  if (Y_out)
+    ES_CUDA(cudaMemcpyAsync(Y_out, impl_->y, nb * C * sizeof(float), cudaMemcpyDeviceToHost,
+                            impl_->main));
+  if (labels_out)
+    ES_CUDA(cudaMemcpyAsync(labels_out, impl_->labels, nb * sizeof(int32_t),
+                            cudaMemcpyDeviceToHost, impl_->main));
+  ES_CUDA(cudaEventRecord(impl_->end, impl_->main));
+  ES_CUDA(cudaEventSynchronize(impl_->end));
+  cudaEventDestroy(ready);
+  float ms = 0.0f;
+  ES_CUDA(cudaEventElapsedTime(&ms, impl_->start, impl_->end));
+  return ms * 1e-3;
+}
+
+// ---------------------------------------------------------------- free functions
+InferenceResult run_inference(std::shared_ptr<const SampleStore> X, const AllocationMatrix& A,
+                              const ClusterSpec& cluster, CombinationRule rule, Mode mode,
+                              PoolOptions options) {
+  if (!X) throw SpecError("no sample store");
+  if (mode == Mode::Benchmark && X->nb_samples() == 0)
+    throw SpecError("benchmark mode needs a nonempty sample store");
+  InferenceSystem system(A, cluster, std::move(rule), options);
+  RunOutput out = system.run(X);
+  system.shutdown();
+  InferenceResult result;
+  if (mode == Mode::Deploy) {
+    result.output = std::move(out);
+  } else {
+    BenchResult s;
+    s.nb_samples = out.stats.nb_samples;
+    s.elapsed_s = std::max(out.stats.elapsed_s, 1e-9);
+    s.throughput = static_cast<double>(s.nb_samples) / s.elapsed_s;
+    s.runs = {s.throughput};
+    result.score = s;
+  }
+  return result;
+}
+
+double median(std::vector<double> values) {
+  if (values.empty()) return 0.0;
+  std::sort(values.begin(), values.end());
+  const std::size_t h = values.size() / 2;
+  return values.size() % 2 ? values[h] : 0.5 * (values[h - 1] + values[h]);
+}
+
+double relative_standard_deviation(const std::vector<double>& values) {
+  if (values.size() < 2) return 0.0;
+  double mean = 0.0;
+  for (double v : values) mean += v;
+  mean /= static_cast<double>(values.size());
+  if (mean == 0.0) return 0.0;
+  double ss = 0.0;
+  for (double v : values) ss += (v - mean) * (v - mean);
+  return std::sqrt(ss / static_cast<double>(values.size() - 1)) / mean;
+}
+
+BenchResult bench(const AllocationMatrix& A, std::shared_ptr<const SampleStore> calib,
+                  const ClusterSpec& cluster, int repeats, PoolOptions options) {
+  if (repeats < 1) throw std::invalid_argument("repeats must be >= 1");
+  if (!calib || calib->nb_samples() == 0) throw SpecError("empty calibration set");
+  BenchResult result;
+  result.nb_samples = calib->nb_samples();
+  try {
+    if (!validate_matrix(A, cluster).ok) return result;
+  } catch (const SpecError&) {
+    return result;
+  }
+  if (!fit_mem(A, cluster).fits) return result;
+  options.copy_outputs = false;
+  try {
+    InferenceSystem system(A, cluster, CombinationRule::averaging(true), options);
+    if (options.warmup) system.run(calib);
+    std::vector<double> elapsed;
+    for (int r = 0; r < repeats; ++r) {
+      RunOutput out = system.run(calib);
+      elapsed.push_back(std::max(out.stats.elapsed_s, 1e-9));
+      result.runs.push_back(static_cast<double>(calib->nb_samples()) / elapsed.back());
+    }
+    system.shutdown();
+    result.elapsed_s = median(elapsed);
+    result.throughput = median(result.runs);
+    result.rsd = relative_standard_deviation(result.runs);
+  } catch (const StartupError&) {
+    result.runs.clear();
+    result.throughput = 0.0;
+  }
+  return result;
+}
+
+// ---------------------------------------------------------------- compat seams
+struct B200Predictor::State {
+  int device = 0;
+  ModelSpec model;
+  int batch = 1;
+  double load_mib = 0.0, capacity_mib = 0.0;
+  std::unique_ptr<DeviceMember> member;
+  cudaStream_t stream = nullptr;
+  float* x32 = nullptr;
+  __nv_bfloat16* x16 = nullptr;
+  float* out = nullptr;
+  std::size_t cap = 0, cap_out = 0;
+};
+
+B200Predictor::B200Predictor(int device, ModelSpec model, int batch, double device_load_mib,
+                             double capacity_mib)
+    : s_(std::make_unique<State>()) {
+  s_->device = device;
+  s_->model = std::move(model);
+  s_->batch = batch;
+  s_->load_mib = device_load_mib;
+  s_->capacity_mib = capacity_mib;
+}
+
+B200Predictor::~B200Predictor() {
+  if (!s_) return;
+  cudaSetDevice(s_->device);
+  if (s_->stream) cudaStreamSynchronize(s_->stream);
+  cudaFree(s_->x32);
+  cudaFree(s_->x16);
+  cudaFree(s_->out);
+  if (s_->stream) cudaStreamDestroy(s_->stream);
+  s_->member.reset();
+}
+
+bool B200Predictor::load() {
+  if (s_->load_mib > s_->capacity_mib) return false;
+  auto m = std::make_unique<DeviceMember>();
+  if (!m->load(s_->device, s_->model, s_->batch)) return false;
+  OnDevice on(s_->device);
+  ES_CUDA(cudaStreamCreateWithFlags(&s_->stream, cudaStreamNonBlocking));
+  s_->member = std::move(m);
+  return true;
+}
+
+void B200Predictor::predict(const float* features, std::size_t first_index, std::size_t rows,
+                            std::size_t width, float* out) {
+  if (!s_->member) throw Error("predict before a successful load()");
+  const int C = s_->model.output_width;
+  if (rows == 0) return;
+  OnDevice on(s_->device);
+  const std::size_t n = rows * width;
+  if (n > s_->cap) {
+    cudaFree(s_->x32);
+    cudaFree(s_->x16);
+    ES_CUDA(cudaMalloc(&s_->x32, n * sizeof(float)));
+    ES_CUDA(cudaMalloc(&s_->x16, n * sizeof(__nv_bfloat16)));
+    s_->cap = n;
+  }
+  if (rows > s_->cap_out) {
+    cudaFree(s_->out);
+    ES_CUDA(cudaMalloc(&s_->out, rows * C * sizeof(float)));
+    s_->cap_out = rows;
+  }
+  ES_CUDA(cudaMemcpyAsync(s_->x32, features, n * sizeof(float), cudaMemcpyHostToDevice, s_->stream));
+  ES_LAUNCH(es::convert_f32_to_bf16(s_->x32, s_->x16, n, s_->stream));
+  if (s_->model.arch.kind == MemberArch::Kind::Synthetic) {
+    // Keyed on absolute sample indices (backend.hpp:43-45): write the rows at
+    // their global offset into a shifted view of the output buffer.
+    const long long first = static_cast<long long>(first_index);
+    ES_LAUNCH(es::synthetic_member_launch(s_->model.id, C, 1, first, first + static_cast<long long>(rows),
+                                          first + static_cast<long long>(rows),
+                                          s_->out - first * C, s_->stream));
+  } else {
+    s_->member->forward(s_->x16, static_cast<long long>(rows), static_cast<int>(rows), 0, 1, s_->out,
+                        es::num_sms(s_->device), s_->stream);
+  }
+  ES_CUDA(cudaMemcpyAsync(out, s_->out, rows * C * sizeof(float), cudaMemcpyDeviceToHost, s_->stream));
+  ES_CUDA(cudaStreamSynchronize(s_->stream));
+}
+
+void combine_blocks(const CombinationRule& rule, int M, int C, std::size_t rows,
+                    const float* const* blocks, float* y, std::int32_t* winners) {
+  if (M < 1 || M > es::kMaxMembers || C < 1 || C > es::kMaxClasses)
+    throw SpecError("combine: unsupported member or class count");
+  if (rule.kind == CombinationRule::Kind::weighted_averaging &&
+      rule.weights.size() != static_cast<std::size_t>(M))
+    throw SpecError("weighted averaging needs one weight per model");
+  if (rows == 0) return;
+  visible_devices();
+  const std::size_t n = rows * C;
+  std::vector<float*> dev(M, nullptr);
+  float* dy = nullptr;
+  int32_t* dl = nullptr;
+  try {
+    for (int m = 0; m < M; ++m) {
+      ES_CUDA(cudaMalloc(&dev[m], n * sizeof(float)));
+      ES_CUDA(cudaMemcpy(dev[m], blocks[m], n * sizeof(float), cudaMemcpyHostToDevice));
+    }
+    ES_CUDA(cudaMalloc(&dy, n * sizeof(float)));
+    ES_CUDA(cudaMalloc(&dl, rows * sizeof(int32_t)));
+    es::CombineArgs ca;
+    ca.M = M;
+    ca.C = C;
+    ca.rows = static_cast<long long>(rows);
+    ca.y = dy;
+    ca.argmax = dl;
+    ca.softmax = rule.member_softmax ? 1 : 0;
+    ca.rule = rule.kind == CombinationRule::Kind::majority_vote ? es::kVote
+              : rule.kind == CombinationRule::Kind::weighted_averaging ? es::kWeighted
+                                                                         : es::kAverage;
+    for (int m = 0; m < M; ++m) {
+      ca.logits[m] = dev[m];
+      ca.weight[m] = rule.kind == CombinationRule::Kind::weighted_averaging
+                         ? static_cast<float>(rule.weights[m])
+                         : 1.0f / static_cast<float>(M);
+    }
+    ES_LAUNCH(es::combine_launch(ca, 0));
+    ES_CUDA(cudaMemcpy(y, dy, n * sizeof(float), cudaMemcpyDeviceToHost));
+    if (winners) ES_CUDA(cudaMemcpy(winners, dl, rows * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  } catch (...) {
+    for (float* p : dev) cudaFree(p);
+    cudaFree(dy);
+    cudaFree(dl);
+    throw;
+  }
+  for (float* p : dev) cudaFree(p);
+  cudaFree(dy);
+  cudaFree(dl);
+}
+
+void derive_footprint(ModelSpec& model) {
+  if (model.arch.kind != MemberArch::Kind::MLP) return;
+  constexpr double kMiB = 1024.0 * 1024.0;
+  if (model.weight_mib <= 0)
+    model.weight_mib = static_cast<double>(model.arch.parameter_count()) * 2.0 / kMiB;
+  if (model.act_mib_per_sample <= 0) {
+    double per = 0.0;
+    for (int w : model.arch.widths) per += w * 2.0;
+    model.act_mib_per_sample = per / kMiB;
+  }
+  if (model.cost_per_sample <= 0) model.cost_per_sample = model.arch.flops_per_sample();
+}
+
+}  // namespace enserve

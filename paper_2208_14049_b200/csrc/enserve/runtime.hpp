@@ -1,0 +1,209 @@
+// enserve-b200 runtime: the GPU InferenceSystem behind the reference's API.
+//
+// API mirror of /root/reference/proj/include/enserve/runtime/pipeline.hpp:17-135
+// and combine.hpp:14-27 (CombinationRule), with the reference's thread pipeline
+// (batcher -> predictor -> sender -> accumulator, pipeline.cpp:141-279) replaced
+// by device work:
+//   * one persistent member kernel per nonzero cell (worker), on its own CUDA
+//     stream, walking its share of the segments tile by tile (tile = the
+//     worker's batch b, the batcher split of pipeline.cpp:155-162);
+//   * per-model logits land directly at their row offset in a [nb x C] buffer on
+//     the combining device (peer copy when the worker sits on another GPU);
+//   * one K3 combine launch folds all members in model-id order.
+// The timed window is the reference's (broadcast -> last fold,
+// pipeline.cpp:309 / :268-269), measured with CUDA events on the combining
+// device; X upload happens in begin_run, untimed, as in pipeline.cpp:285-302.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <optional>
+#include <string>
+#include <vector>
+
+#include "enserve/spec.hpp"
+
+namespace enserve {
+
+// ---- combination rule (combine.hpp:14-27) -----------------------------------
+struct CombinationRule {
+  enum class Kind { averaging, majority_vote, weighted_averaging };
+  Kind kind = Kind::averaging;
+  std::vector<double> weights;  // weighted_averaging: one per model, >= 0, sum 1
+  // Fold softmax(member logits) instead of the raw member output.  Off keeps
+  // the reference's fold bit-for-bit; the B200 ensemble workload turns it on.
+  bool member_softmax = false;
+
+  static CombinationRule averaging(bool softmax = false) { return {Kind::averaging, {}, softmax}; }
+  static CombinationRule majority_vote(bool softmax = false) {
+    return {Kind::majority_vote, {}, softmax};
+  }
+  static CombinationRule weighted(std::vector<double> weights, bool softmax = false);
+  std::string name() const;
+  static CombinationRule from_name(const std::string& name, int model_count);
+};
+
+// ---- immutable samples (message.hpp:12-34) ----------------------------------
+// nb x width fp32 features.  Device replicas (bf16, row-major) are created on
+// first use per GPU and reused by every later run, like the reference's shared
+// SampleStore.
+class SampleStore {
+ public:
+  SampleStore(std::vector<float> data, std::size_t nb, std::size_t width);
+  // Non-owning: `data` must outlive the store.
+  static std::shared_ptr<SampleStore> borrow(const float* data, std::size_t nb, std::size_t width);
+  // Synthetic features generated on `device` (x = U[0,1) keyed by seed and flat
+  // index); no host copy exists.
+  static std::shared_ptr<SampleStore> synthetic(std::uint64_t seed, std::size_t nb,
+                                                std::size_t width, int device);
+  ~SampleStore();
+  SampleStore(const SampleStore&) = delete;
+  SampleStore& operator=(const SampleStore&) = delete;
+
+  std::size_t nb_samples() const { return nb_; }
+  std::size_t width() const { return width_; }
+  const float* host_data() const { return host_; }
+  // bf16 [nb][width] on `device` (uploads + converts on first call).
+  const void* device_replica(int device) const;
+
+ private:
+  SampleStore() = default;
+  std::vector<float> owned_;
+  const float* host_ = nullptr;
+  std::size_t nb_ = 0;
+  std::size_t width_ = 0;
+  std::uint64_t synthetic_seed_ = 0;
+  bool synthetic_ = false;
+  mutable std::vector<void*> replicas_;  // indexed by CUDA ordinal
+};
+
+// ---- run bookkeeping (pipeline.hpp:17-53) -----------------------------------
+enum class Mode { Deploy, Benchmark };
+
+struct RunStats {
+  std::size_t nb_samples = 0;
+  std::size_t segments = 0;
+  std::size_t data_messages = 0;
+  std::vector<std::size_t> segment_rows;
+  double elapsed_s = 0.0;
+};
+
+struct RunOutput {
+  std::vector<float> combined;
+  std::vector<int> winners;  // argmax per sample (lowest index on ties), every rule
+  int output_width = 0;
+  RunStats stats;
+};
+
+struct BenchResult {
+  double throughput = 0.0;
+  double elapsed_s = 0.0;
+  std::size_t nb_samples = 0;
+  std::vector<double> runs;
+  double rsd = 0.0;
+};
+
+struct InferenceResult {
+  std::optional<RunOutput> output;
+  std::optional<BenchResult> score;
+};
+
+struct PoolOptions {
+  // Cluster device row d runs on CUDA ordinal device_map[d]; empty = d modulo
+  // the visible GPU count (lets a 1-GPU box host a multi-device matrix).
+  std::vector<int> device_map;
+  bool copy_outputs = true;   // D2H of the combined output in await_run
+  bool warmup = true;         // bench: one untimed run first (module load, clocks)
+  int sms_per_worker = 0;     // 0 = every SM of the device (persistent grid)
+};
+
+// Per-model executable member on one GPU (the Predictor of backend.hpp:25-34).
+class DeviceMember;
+
+class InferenceSystem {
+ public:
+  InferenceSystem(const AllocationMatrix& A, const ClusterSpec& cluster, CombinationRule rule,
+                  PoolOptions options = {});
+  ~InferenceSystem();
+  InferenceSystem(const InferenceSystem&) = delete;
+  InferenceSystem& operator=(const InferenceSystem&) = delete;
+
+  RunOutput run(std::shared_ptr<const SampleStore> X);
+  RunOutput run(std::shared_ptr<const SampleStore> X, CombinationRule rule);
+  void begin_run(std::shared_ptr<const SampleStore> X);
+  void begin_run(std::shared_ptr<const SampleStore> X, CombinationRule rule);
+  std::size_t broadcast();
+  RunOutput await_run();
+  void shutdown();
+
+  // End-to-end variant: X from (preferably pinned) host memory, combined output
+  // and labels back to host, all copies inside the CUDA-event window.  Single
+  // physical GPU only.
+  double run_host(const float* X, std::size_t nb, std::size_t width, float* Y_out,
+                  std::int32_t* labels_out);
+
+  int worker_count() const { return static_cast<int>(workers_.size()); }
+  std::vector<int> workers_per_model() const;
+  const AllocationMatrix& matrix() const { return matrix_; }
+  const ClusterSpec& cluster() const { return cluster_; }
+  // Kernel launches enqueued by the last broadcast() (members + combine + copies).
+  int launches_last_run() const { return launches_; }
+  // Device time of the last run's member kernels / combine (ms), from events.
+  double last_member_ms(int worker) const;
+  double last_combine_ms() const;
+  int combine_device() const { return combine_dev_; }
+
+ private:
+  struct Worker;
+  struct Impl;
+  AllocationMatrix matrix_;
+  ClusterSpec cluster_;
+  CombinationRule rule_;
+  PoolOptions options_;
+  int output_width_ = 0;
+  int combine_dev_ = 0;
+  std::vector<std::unique_ptr<Worker>> workers_;
+  std::unique_ptr<Impl> impl_;
+  int launches_ = 0;
+  bool shut_down_ = false;
+  bool run_open_ = false;
+};
+
+InferenceResult run_inference(std::shared_ptr<const SampleStore> X, const AllocationMatrix& A,
+                              const ClusterSpec& cluster, CombinationRule rule, Mode mode,
+                              PoolOptions options = {});
+
+BenchResult bench(const AllocationMatrix& A, std::shared_ptr<const SampleStore> calib,
+                  const ClusterSpec& cluster, int repeats, PoolOptions options = {});
+
+double median(std::vector<double> values);
+double relative_standard_deviation(const std::vector<double>& values);
+
+// The reference Predictor (backend.hpp:25-34) on one GPU — the per-batch
+// compat path the reference's own thread pipeline can drive through the C ABI
+// (es_member_*): every predict() is an H2D of the batch, one member launch and
+// a D2H of its logits.
+class B200Predictor {
+ public:
+  B200Predictor(int device, ModelSpec model, int batch, double device_load_mib,
+                double capacity_mib);
+  ~B200Predictor();
+  bool load();
+  void predict(const float* features, std::size_t first_index, std::size_t rows,
+               std::size_t width, float* out);
+
+ private:
+  struct State;
+  std::unique_ptr<State> s_;
+};
+
+// PredictionAccumulator's fold (combine.cpp:93-136) of M host blocks on the
+// device: y[rows*C], winners[rows] (argmax, lowest index on ties).
+void combine_blocks(const CombinationRule& rule, int M, int C, std::size_t rows,
+                    const float* const* blocks, float* y, std::int32_t* winners);
+
+// Fill ModelSpec footprint fields from its MLP architecture (bf16 weights,
+// bf16 activations per sample) when they are zero.
+void derive_footprint(ModelSpec& model);
+
+}  // namespace enserve

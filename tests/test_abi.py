@@ -1,0 +1,73 @@
+"""The C-ABI boundary: libenserve_b200.so loads, exports exactly what
+include/enserve_b200.h declares, and maps the reference's error classes."""
+from __future__ import annotations
+
+import ctypes
+import re
+import subprocess
+from pathlib import Path
+
+import pytest
+
+import paper_2208_14049_b200 as es
+from paper_2208_14049_b200 import _abi
+
+HEADER = Path(__file__).resolve().parent.parent / "include" / "enserve_b200.h"
+
+
+def declared_symbols():
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"^\s*(?:es_status|void|int|const char\*)\s+(es_\w+)\s*\(",
+                                 text, flags=re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    names = declared_symbols()
+    assert len(names) >= 40
+    lib = ctypes.CDLL(str(es.LIB_PATH))
+    for n in names:
+        assert hasattr(lib, n), n
+    assert sorted(_abi.EXPORTED) == names
+
+
+def test_library_is_built_for_sm100a_with_tcgen05_and_tma():
+    sass = subprocess.run(["cuobjdump", "-sass", str(es.LIB_PATH)], capture_output=True,
+                          text=True).stdout
+    if not sass:
+        pytest.skip("cuobjdump unavailable")
+    assert "UTCHMMA" in sass      # tcgen05.mma
+    assert "UTMALDG" in sass      # TMA tile loads
+    assert "LDTM" in sass         # tcgen05.ld (TMEM -> registers)
+    elf = subprocess.run(["cuobjdump", "-lelf", str(es.LIB_PATH)], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in elf
+
+
+def test_abi_version_and_status_names():
+    lib = es.lib()
+    assert lib.es_abi_version() == 1
+    assert lib.es_status_name(4) == b"ES_ERR_STARTUP"
+
+
+def test_error_classes_cross_the_boundary():
+    c = es.ClusterSpec([es.DeviceSpec(0, es.GPU, 1000.0, 1.0, 0.0)],
+                       [es.ModelSpec(0, "oversized", 5000.0, 0.0, 1.0, 4)], [8], 128)
+    with pytest.raises(es.AllocationError) as ei:
+        es.worst_fit_decreasing(c, 8)
+    assert ei.value.model_name == "oversized"
+    with pytest.raises(es.SpecError):
+        es.worst_fit_decreasing(c, 12)
+    with pytest.raises(es.InvalidArgument):
+        es.segment_bounds(3, 128, 300)
+    with pytest.raises(es.BaselineError):
+        es.bbs_baseline(es.ClusterSpec([es.DeviceSpec(0, es.GPU, 1e5, 1.0, 0.0)],
+                                       [es.ModelSpec(0, "a", 1.0, 0.0, 1.0, 4),
+                                        es.ModelSpec(1, "b", 1.0, 0.0, 1.0, 4)], [8], 128))
+
+
+def test_product_does_not_link_the_oracle():
+    deps = subprocess.run(["ldd", str(es.LIB_PATH)], capture_output=True, text=True).stdout
+    assert "oracle" not in deps and "enserve_ref" not in deps
+    import paper_2208_14049_b200.api as api
+    src = Path(api.__file__).read_text() + Path(_abi.__file__).read_text()
+    assert "oracle" not in src.replace("ORACLE", "")
