@@ -3,6 +3,9 @@
 #include "cpu_member.h"
 
 #include <math.h>
+#if defined(__AVX2__)
+#include <immintrin.h>
+#endif
 #include <stdlib.h>
 #include <string.h>
 
@@ -125,6 +128,38 @@ static void dense_block(const float* x, int fi, const float* wt, const float* b,
                         int po, int relu_q, int quantize, float* y) {
   for (int j0 = 0; j0 < po; j0 += JB) {
     float acc[RB][JB];
+#if defined(__AVX2__) && defined(__FMA__)
+    /* 4 rows x 16 outputs in 8 ymm registers; acc[r][j] += x[r][k] * w[k][j]
+     * with one fused multiply-add per k, k ascending. */
+    __m256 a00 = _mm256_setzero_ps(), a01 = _mm256_setzero_ps();
+    __m256 a10 = _mm256_setzero_ps(), a11 = _mm256_setzero_ps();
+    __m256 a20 = _mm256_setzero_ps(), a21 = _mm256_setzero_ps();
+    __m256 a30 = _mm256_setzero_ps(), a31 = _mm256_setzero_ps();
+    for (int k = 0; k < fi; ++k) {
+      const float* wrow = wt + (size_t)k * po + j0;
+      __m256 w0 = _mm256_loadu_ps(wrow), w1 = _mm256_loadu_ps(wrow + 8);
+      __m256 x0 = _mm256_broadcast_ss(x + k);
+      __m256 x1 = _mm256_broadcast_ss(x + (size_t)fi + k);
+      __m256 x2 = _mm256_broadcast_ss(x + 2 * (size_t)fi + k);
+      __m256 x3 = _mm256_broadcast_ss(x + 3 * (size_t)fi + k);
+      a00 = _mm256_fmadd_ps(x0, w0, a00);
+      a01 = _mm256_fmadd_ps(x0, w1, a01);
+      a10 = _mm256_fmadd_ps(x1, w0, a10);
+      a11 = _mm256_fmadd_ps(x1, w1, a11);
+      a20 = _mm256_fmadd_ps(x2, w0, a20);
+      a21 = _mm256_fmadd_ps(x2, w1, a21);
+      a30 = _mm256_fmadd_ps(x3, w0, a30);
+      a31 = _mm256_fmadd_ps(x3, w1, a31);
+    }
+    _mm256_storeu_ps(acc[0], a00);
+    _mm256_storeu_ps(acc[0] + 8, a01);
+    _mm256_storeu_ps(acc[1], a10);
+    _mm256_storeu_ps(acc[1] + 8, a11);
+    _mm256_storeu_ps(acc[2], a20);
+    _mm256_storeu_ps(acc[2] + 8, a21);
+    _mm256_storeu_ps(acc[3], a30);
+    _mm256_storeu_ps(acc[3] + 8, a31);
+#else
     memset(acc, 0, sizeof(acc));
     for (int k = 0; k < fi; ++k) {
       const float* wrow = wt + (size_t)k * po + j0;
@@ -133,6 +168,7 @@ static void dense_block(const float* x, int fi, const float* wt, const float* b,
         for (int j = 0; j < JB; ++j) acc[r][j] += xv * wrow[j];
       }
     }
+#endif
     for (int r = 0; r < RB; ++r) {
       for (int j = 0; j < JB; ++j) {
         float v = acc[r][j] + b[j0 + j];

@@ -89,6 +89,18 @@ class CpuMlp:
         orc().orc_mlp_forward(self._h, _fp(X), X.shape[0], _fp(out))
         return out
 
+    def logit_scale(self, X: np.ndarray) -> np.ndarray:
+        """Conditioning of every logit: |b_c| + sum_j |W[c,j]| |a_j| over the last
+        layer's (bf16) inputs a — the magnitude a rounding flip in a hidden
+        activation is measured against."""
+        a = round_bf16(np.asarray(X, dtype=np.float32)).astype(np.float64)
+        for l in range(len(self.widths) - 2):
+            w, b = self.layer(l)
+            a = round_bf16(np.maximum(a @ w.T.astype(np.float64) + b, 0.0).astype(np.float32))
+            a = a.astype(np.float64)
+        w, b = self.layer(len(self.widths) - 2)
+        return (np.abs(a) @ np.abs(w.T.astype(np.float64)) + np.abs(b)).astype(np.float32)
+
     def layer(self, l: int):
         fi, fo = self.widths[l], self.widths[l + 1]
         w = np.zeros((fo, fi), dtype=np.float32)
@@ -100,6 +112,13 @@ class CpuMlp:
         if getattr(self, "_h", None):
             orc().orc_mlp_destroy(self._h)
             self._h = None
+
+
+def round_bf16(x: np.ndarray) -> np.ndarray:
+    """Round-to-nearest-even to bf16, kept in fp32 (finite inputs)."""
+    u = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
+    return u.astype(np.uint32).view(np.float32)
 
 
 def features(seed: int, rows: int, width: int) -> np.ndarray:
