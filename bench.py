@@ -61,28 +61,38 @@ class ClockSampler:
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
         self.rows = []
-        self._stop = threading.Event()
+        self._proc = None
         self._t = threading.Thread(target=self._run, daemon=True)
 
     def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        try:
+            for line in self._proc.stdout:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 8:
+                    self.rows.append(parts)
+        except Exception:
+            pass
 
     def __enter__(self):
-        self._t.start()
+        try:
+            self._proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t.start()
+            time.sleep(0.3)  # first sample lands before the timed region starts
+        except Exception:
+            self._proc = None
         return self
 
     def __exit__(self, *exc):
-        self._stop.set()
-        self._t.join(timeout=10)
+        if self._proc is not None:
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=5)
+            except Exception:
+                self._proc.kill()
+            self._t.join(timeout=5)
 
     def summary(self) -> dict:
         if not self.rows:
@@ -229,8 +239,14 @@ def run_b200(args, dist: Dist) -> dict | None:
     pk = peaks()
     gpu = dist.local
     cluster = make_cluster(es)
-    choice = choose_matrix(es, cluster, gpu, args.calib_nb, args.seed)
-    A = choice["A2"]
+    if args.matrix:
+        A = es.AllocationMatrix.from_array([[int(b) for b in args.matrix.split(",")]])
+        choice = {"A1": es.worst_fit_decreasing(cluster, cluster.min_batch()), "A2": A,
+                  "A1_score": 0.0, "A2_score": 0.0, "bench_calls": 0,
+                  "bbs": {"applicable": False, "reason": "matrix given on the command line"}}
+    else:
+        choice = choose_matrix(es, cluster, gpu, args.calib_nb, args.seed)
+        A = choice["A2"]
     rule = es.CombinationRule.averaging(softmax=True)
     X = es.SampleStore(synthetic_seed=args.seed + dist.rank * 7919, nb=args.nb, width=784,
                        device=gpu)
@@ -258,7 +274,7 @@ def run_b200(args, dist: Dist) -> dict | None:
     combine_ms /= args.steps
 
     # e2e: host (pinned) X in, combined probabilities + labels out, per step
-    e2e_nb = min(args.e2e_nb, args.nb)
+    e2e_nb = max(1, min(args.e2e_nb, args.nb))
     try:
         import torch
         Xh_t = torch.empty((e2e_nb, 784), dtype=torch.float32, pin_memory=True)
@@ -271,10 +287,11 @@ def run_b200(args, dist: Dist) -> dict | None:
         Lh = np.empty(e2e_nb, np.int32)
     rng = np.random.default_rng(args.seed + dist.rank)
     Xh[:] = rng.random((e2e_nb, 784), dtype=np.float32)
-    for _ in range(max(1, args.warmup // 2)):
+    e2e_steps = args.steps if args.e2e else 1
+    for _ in range(max(1, args.warmup // 2) if args.e2e else 0):
         system.run_host(Xh, Yh, Lh)
     dist.barrier()
-    e2e_s = [system.run_host(Xh, Yh, Lh) for _ in range(args.steps)]
+    e2e_s = [system.run_host(Xh, Yh, Lh) for _ in range(e2e_steps)]
     dist.barrier()
     e2e_total = dist.max(float(sum(e2e_s)))
     system.close()
@@ -316,7 +333,7 @@ def run_b200(args, dist: Dist) -> dict | None:
         "combine_ms": round(combine_ms, 4),
         "combine_hbm_gbs": round(args.nb * (4 * 40 + 44) / (combine_ms * 1e-3) / 1e9, 1)
         if combine_ms > 0 else None,
-        "e2e": {"value": round(n * e2e_nb * args.steps / e2e_total, 1), "unit": "samples/s",
+        "e2e": {"value": round(n * e2e_nb * e2e_steps / e2e_total, 1), "unit": "samples/s",
                 "h2d_bytes_per_step": e2e_nb * 784 * 4,
                 "d2h_bytes_per_step": e2e_nb * (10 * 4 + 4),
                 "samples_per_step": e2e_nb},
@@ -360,7 +377,7 @@ def run_reference(args, dist: Dist) -> dict | None:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--nb", type=int, default=1 << 22)
@@ -368,6 +385,10 @@ def main():
     ap.add_argument("--calib-nb", type=int, default=1 << 16)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--no-e2e", dest="e2e", action="store_false",
+                    help="profiling: a single e2e step")
+    ap.add_argument("--matrix", default="",
+                    help="profiling: batch per member (e.g. 64,64,128,128), skips the greedy")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         args.warmup = 3

@@ -85,6 +85,8 @@ typedef struct es_pool_opts {
   int copy_outputs;      /* D2H of the combined output in await_run */
   int warmup;            /* bench: one untimed run first */
   int sms_per_worker;    /* 0 = all SMs (persistent grid) */
+  int overlap_colocated; /* 1 = one stream per worker; 0 = co-located workers
+                            time-share one stream per GPU */
 } es_pool_opts;
 
 /* RunStats (pipeline.hpp:19-25). */

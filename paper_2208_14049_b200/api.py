@@ -534,7 +534,8 @@ class CombinationRule:
 
 
 def _pool_opts(keep: list, device_map=None, copy_outputs=True, warmup=True,
-               sms_per_worker=0) -> _abi.PoolOpts:
+               sms_per_worker=0, overlap_colocated=False) -> _abi.PoolOpts:
+    """PoolOptions (runtime.hpp)."""
     dm = None
     n = 0
     if device_map:
@@ -542,7 +543,7 @@ def _pool_opts(keep: list, device_map=None, copy_outputs=True, warmup=True,
         keep.append(dm)
         n = len(device_map)
     o = _abi.PoolOpts(C.cast(dm, _abi.c_int_p) if dm is not None else None, n, int(copy_outputs),
-                      int(warmup), int(sms_per_worker))
+                      int(warmup), int(sms_per_worker), int(overlap_colocated))
     keep.append(o)
     return o
 

@@ -144,6 +144,7 @@ PoolOptions to_opts(const es_pool_opts* o) {
   p.copy_outputs = o->copy_outputs != 0;
   p.warmup = o->warmup != 0;
   p.sms_per_worker = o->sms_per_worker;
+  p.overlap_colocated = o->overlap_colocated != 0;
   return p;
 }
 

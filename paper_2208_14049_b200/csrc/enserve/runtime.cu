@@ -257,6 +257,7 @@ struct InferenceSystem::Worker {
   int colocated = 1;
   std::unique_ptr<DeviceMember> member;
   cudaStream_t stream = nullptr;
+  bool owns_stream = true;
   cudaEvent_t ev_begin = nullptr, ev_done = nullptr;
   long long seg_begin = 0, seg_end = 0;  // this run's share
   float* staging = nullptr;              // remote worker: local logits [nb][C]
@@ -332,7 +333,19 @@ InferenceSystem::InferenceSystem(const AllocationMatrix& A, const ClusterSpec& c
         break;
       }
       OnDevice on(w->phys);
-      ES_CUDA(cudaStreamCreateWithFlags(&w->stream, cudaStreamNonBlocking));
+      // Co-located workers time-share their GPU (cost_model.cpp:17): each
+      // member kernel is a persistent full-device grid, so they queue on one
+      // stream per GPU in worker order (unless asked to overlap).
+      cudaStream_t shared = nullptr;
+      if (!options_.overlap_colocated)
+        for (const auto& o : workers_)
+          if (o->phys == w->phys) shared = o->stream;
+      if (shared) {
+        w->stream = shared;
+        w->owns_stream = false;
+      } else {
+        ES_CUDA(cudaStreamCreateWithFlags(&w->stream, cudaStreamNonBlocking));
+      }
       ES_CUDA(cudaEventCreate(&w->ev_begin));
       ES_CUDA(cudaEventCreate(&w->ev_done));
       workers_.push_back(std::move(w));
@@ -361,11 +374,14 @@ InferenceSystem::~InferenceSystem() {
 void InferenceSystem::shutdown() {
   if (shut_down_) return;
   shut_down_ = true;
-  for (auto& w : workers_) {
+  for (auto& w : workers_) {  // drain every stream before any is destroyed
     cudaSetDevice(w->phys);
     if (w->stream) cudaStreamSynchronize(w->stream);
+  }
+  for (auto& w : workers_) {
+    cudaSetDevice(w->phys);
     if (w->staging) cudaFree(w->staging);
-    if (w->stream) cudaStreamDestroy(w->stream);
+    if (w->stream && w->owns_stream) cudaStreamDestroy(w->stream);
     if (w->ev_begin) cudaEventDestroy(w->ev_begin);
     if (w->ev_done) cudaEventDestroy(w->ev_done);
     w->member.reset();

@@ -115,6 +115,7 @@ struct PoolOptions {
   bool copy_outputs = true;   // D2H of the combined output in await_run
   bool warmup = true;         // bench: one untimed run first (module load, clocks)
   int sms_per_worker = 0;     // 0 = every SM of the device (persistent grid)
+  bool overlap_colocated = false;  // one stream per worker instead of per GPU
 };
 
 // Per-model executable member on one GPU (the Predictor of backend.hpp:25-34).
