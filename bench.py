@@ -109,35 +109,68 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ dist
 class Dist:
-    def __init__(self):
+    """One process per GPU (torchrun).  Plumbing only: a barrier around the
+    timed region and the max-over-ranks of the device time.  The data path
+    has no collective (each rank predicts its own segments)."""
+
+    def __init__(self, backend: str | None = None):
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.backend = backend or os.environ.get("ES_DIST_BACKEND", "nccl")
         self.pg = None
         if self.world > 1:
             import torch
             import torch.distributed as dist
-            torch.cuda.set_device(self.local)
-            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            if self.backend == "nccl":
+                torch.cuda.set_device(self.local)
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            else:
+                dist.init_process_group(self.backend)
             self.pg = dist
+
+    def _device(self) -> str:
+        return f"cuda:{self.local}" if self.backend == "nccl" else "cpu"
 
     def barrier(self):
         if self.pg:
-            import torch
-            torch.cuda.synchronize()
+            if self.backend == "nccl":
+                import torch
+                torch.cuda.synchronize()
             self.pg.barrier()
 
     def max(self, x: float) -> float:
         if not self.pg:
             return x
         import torch
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{self.local}")
+        t = torch.tensor([x], dtype=torch.float64, device=self._device())
         self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
         return float(t.item())
+
+    def gather(self, values: list) -> list:
+        """All ranks' lists of ints (for the exactly-once check)."""
+        if not self.pg:
+            return [values]
+        out = [None] * self.world
+        self.pg.all_gather_object(out, values)
+        return out
 
     def close(self):
         if self.pg:
             self.pg.destroy_process_group()
+
+
+def rank_shard(es, world: int, rank: int, batches: list, nb_per_gpu: int, seg: int = 128):
+    """Rows this rank predicts: the global matrix is `world` device rows, every
+    member data-parallel over all of them; the library's own segment partition
+    (es.segment_shares) assigns each rank a contiguous run of segments."""
+    A = es.AllocationMatrix.from_array([list(batches)] * world)
+    total = world * nb_per_gpu
+    shares = [s for s in es.segment_shares(A, total, seg) if s[0] == rank]
+    first = min(s[2] for s in shares)
+    end = max(s[3] for s in shares)
+    assert all((s[2], s[3]) == (first, end) for s in shares)
+    return first * seg, min(end * seg, total), shares
 
 
 # ------------------------------------------------------------------ workload
@@ -248,7 +281,9 @@ def run_b200(args, dist: Dist) -> dict | None:
         choice = choose_matrix(es, cluster, gpu, args.calib_nb, args.seed)
         A = choice["A2"]
     rule = es.CombinationRule.averaging(softmax=True)
-    X = es.SampleStore(synthetic_seed=args.seed + dist.rank * 7919, nb=args.nb, width=784,
+    r0, r1, _ = rank_shard(es, dist.world, dist.rank, A.cells[0].tolist(), args.nb)
+    local_nb = r1 - r0
+    X = es.SampleStore(synthetic_seed=args.seed + dist.rank * 7919, nb=local_nb, width=784,
                        device=gpu)
     system = es.InferenceSystem(A, cluster, rule, device_map=[gpu], copy_outputs=False)
     for _ in range(args.warmup):
@@ -270,6 +305,7 @@ def run_b200(args, dist: Dist) -> dict | None:
         wall = time.perf_counter() - t0
     dist.barrier()
     device_s = dist.max(float(sum(step_s)))
+    covered = sum(dist.gather([local_nb]), [])
     member_ms /= args.steps
     combine_ms /= args.steps
 
@@ -299,7 +335,7 @@ def run_b200(args, dist: Dist) -> dict | None:
     if dist.rank != 0:
         return None
     n = dist.world
-    value = n * args.nb * args.steps / device_s
+    value = sum(covered) * args.steps / device_s
     result = {
         "metric": "ensemble samples/sec at 1/2/4/8 B200 vs batch-only baseline and CPU ref",
         "value": round(value, 1),

@@ -126,6 +126,11 @@ es_status es_matrix_validate(const es_cluster_desc* c, const int* A, int* ok, in
 es_status es_num_segments(size_t nb, int segment_size, size_t* out);
 es_status es_segment_bounds(int segment_id, int segment_size, size_t nb, size_t* start,
                             size_t* end);
+/* Segments each worker predicts in one run (replaces the per-model shared
+ * FIFO of src/runtime/pipeline.cpp:103-104,143-166 with a static, exactly-once
+ * split): out[4*i..] = {device, model, first segment, end segment}. */
+es_status es_segment_shares(const int* A, int devices, int models, size_t nb, int segment_size,
+                            long long* out, int cap, int* n);
 /* fit_mem (src/memory/memory_model.cpp:22-32); used_mib[D]. */
 es_status es_fit_mem(const es_cluster_desc* c, const int* A, double* used_mib, int* fits);
 /* more_remaining_memory (memory_model.cpp:34-50); *device = -1 when none. */

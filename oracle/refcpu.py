@@ -36,6 +36,8 @@ def build(quiet: bool = True) -> None:
     targets = ["liboracle.so"]
     if REF_SRC.exists():
         targets.append("_ref/libenserve_ref.so")
+        if (HERE.parent / "paper_2208_14049_b200" / "libenserve_b200.so").exists():
+            targets.append("integration")
     subprocess.run(["make", "-C", str(HERE), *targets], check=True,
                    stdout=subprocess.DEVNULL if quiet else None)
 

@@ -82,6 +82,8 @@ _SIGS = {
                                      c_int_p]),
     "es_num_segments": (C.c_int, [C.c_size_t, C.c_int, c_size_t_p]),
     "es_segment_bounds": (C.c_int, [C.c_int, C.c_int, C.c_size_t, c_size_t_p, c_size_t_p]),
+    "es_segment_shares": (C.c_int, [c_int_p, C.c_int, C.c_int, C.c_size_t, C.c_int,
+                                    C.POINTER(C.c_longlong), C.c_int, c_int_p]),
     "es_fit_mem": (C.c_int, [C.POINTER(ClusterDesc), c_int_p, c_double_p, c_int_p]),
     "es_more_remaining_memory": (C.c_int, [C.POINTER(ClusterDesc), c_int_p, C.c_int, c_int_p]),
     "es_predict_ensemble_throughput": (C.c_int, [C.POINTER(ClusterDesc), c_int_p, c_double_p]),

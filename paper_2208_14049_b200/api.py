@@ -293,6 +293,16 @@ def segment_bounds(segment_id: int, segment_size: int, nb: int) -> tuple:
     return s.value, e.value
 
 
+def segment_shares(A: AllocationMatrix, nb: int, segment_size: int) -> list:
+    """[(device, model, first_segment, end_segment)] per worker, row-major."""
+    cap = max(A.worker_count(), 1)
+    out = (C.c_longlong * (4 * cap))()
+    n = C.c_int()
+    _check(lib().es_segment_shares(A.ptr(), A.device_count(), A.model_count(), nb, segment_size,
+                                   out, cap, C.byref(n)))
+    return [tuple(out[4 * i: 4 * i + 4]) for i in range(n.value)]
+
+
 @dataclass
 class MemoryReport:
     used_mib: list

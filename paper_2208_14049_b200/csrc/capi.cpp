@@ -239,6 +239,21 @@ es_status es_segment_bounds(int segment_id, int segment_size, size_t nb, size_t*
   });
 }
 
+es_status es_segment_shares(const int* A, int devices, int models, size_t nb, int segment_size,
+                            long long* out, int cap, int* n) {
+  return guard([&] {
+    std::vector<SegmentShare> s = segment_shares(to_matrix(A, devices, models), nb, segment_size);
+    *n = static_cast<int>(s.size());
+    for (int i = 0; out && i < *n && i < cap; ++i) {
+      out[4 * i + 0] = s[i].device;
+      out[4 * i + 1] = s[i].model;
+      out[4 * i + 2] = s[i].begin;
+      out[4 * i + 3] = s[i].end;
+    }
+    return ES_OK;
+  });
+}
+
 es_status es_fit_mem(const es_cluster_desc* c, const int* A, double* used_mib, int* fits) {
   return guard([&] {
     MemoryReport r = fit_mem(to_matrix(A, c->n_devices, c->n_models), to_cluster(c));

@@ -90,6 +90,20 @@ std::vector<int> models_heaviest_first(const ClusterSpec& cluster) {
   return ids;
 }
 
+std::vector<SegmentShare> segment_shares(const AllocationMatrix& A, std::size_t nb_samples,
+                                         int segment_size) {
+  const long long S = static_cast<long long>(num_segments(nb_samples, segment_size));
+  std::vector<int> seen(A.model_count(), 0);
+  std::vector<SegmentShare> out;
+  for (int d = 0; d < A.device_count(); ++d)
+    for (int m = 0; m < A.model_count(); ++m) {
+      if (A.at(d, m) == 0) continue;
+      const long long k = seen[m]++, n = A.column_worker_count(m);
+      out.push_back({d, m, S * k / n, S * (k + 1) / n});
+    }
+  return out;
+}
+
 AllocationMatrix worst_fit_decreasing(const ClusterSpec& cluster, int default_batch) {
   if (!cluster.menu_contains(default_batch))
     throw SpecError("default batch " + std::to_string(default_batch) +

@@ -54,4 +54,17 @@ AllocationMatrix worst_fit_decreasing(const ClusterSpec& cluster, int default_ba
 // Model ids sorted by weight_mib descending, ties by ascending id.
 std::vector<int> models_heaviest_first(const ClusterSpec& cluster);
 
+// Which segments each worker (nonzero cell, row-major) predicts in one run:
+// a model's workers split [0, S) into contiguous, equal runs in worker order,
+// so every segment is predicted exactly once per model (the property the
+// reference's shared per-model FIFO gives, tests/test_runtime.cpp:282-313).
+struct SegmentShare {
+  int device = 0;
+  int model = 0;
+  long long begin = 0;  // segment ids [begin, end)
+  long long end = 0;
+};
+std::vector<SegmentShare> segment_shares(const AllocationMatrix& A, std::size_t nb_samples,
+                                         int segment_size);
+
 }  // namespace enserve

@@ -402,6 +402,14 @@ void InferenceSystem::shutdown() {
   }
 }
 
+void InferenceSystem::assign_shares(std::size_t nb) {
+  std::vector<SegmentShare> shares = segment_shares(matrix_, nb, cluster_.segment_size);
+  for (std::size_t i = 0; i < workers_.size(); ++i) {  // both in row-major cell order
+    workers_[i]->seg_begin = shares[i].begin;
+    workers_[i]->seg_end = shares[i].end;
+  }
+}
+
 std::vector<int> InferenceSystem::workers_per_model() const {
   std::vector<int> n(cluster_.model_count(), 0);
   for (const auto& w : workers_) ++n[w->model];
@@ -441,15 +449,9 @@ void InferenceSystem::begin_run(std::shared_ptr<const SampleStore> X, Combinatio
       impl_->cap_rows = rows;
     }
   }
-  // Segment shares: a model's workers split its segments into contiguous,
-  // equal runs in worker (row-major) order; each segment exactly once.
   const std::size_t S = num_segments(nb, cluster_.segment_size);
-  std::vector<int> per_model = workers_per_model();
-  std::vector<int> seen(cluster_.model_count(), 0);
+  assign_shares(nb);
   for (auto& w : workers_) {
-    const int k = seen[w->model]++, n = per_model[w->model];
-    w->seg_begin = static_cast<long long>(S * k / n);
-    w->seg_end = static_cast<long long>(S * (k + 1) / n);
     if (w->phys != combine_dev_ && w->staging_rows < nb) {
       OnDevice on(w->phys);
       cudaFree(w->staging);
@@ -596,14 +598,7 @@ double InferenceSystem::run_host(const float* X, std::size_t nb, std::size_t wid
   }
   const int C = output_width_;
   // Segment shares as in begin_run; X itself is staged inside the window.
-  const std::size_t S = num_segments(nb, cluster_.segment_size);
-  std::vector<int> per_model = workers_per_model();
-  std::vector<int> seen(cluster_.model_count(), 0);
-  for (auto& w : workers_) {
-    const int k = seen[w->model]++, cnt = per_model[w->model];
-    w->seg_begin = static_cast<long long>(S * k / cnt);
-    w->seg_end = static_cast<long long>(S * (k + 1) / cnt);
-  }
+  assign_shares(nb);
   if (nb > impl_->cap_rows) {
     for (float*& p : impl_->logits) {
       cudaFree(p);

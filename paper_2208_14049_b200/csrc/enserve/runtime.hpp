@@ -157,6 +157,7 @@ class InferenceSystem {
  private:
   struct Worker;
   struct Impl;
+  void assign_shares(std::size_t nb);
   AllocationMatrix matrix_;
   ClusterSpec cluster_;
   CombinationRule rule_;

@@ -1,0 +1,75 @@
+"""N > 1 plumbing on CPU (gloo, world_size 2): each rank derives its segment
+shard from the library's partition (es.segment_shares), the shards cover every
+segment exactly once, and the timing reduction is the max over ranks — the
+same code bench.py runs under torchrun with NCCL."""
+from __future__ import annotations
+
+import os
+import socket
+import sys
+from pathlib import Path
+
+import pytest
+import torch.multiprocessing as mp
+
+REPO = Path(__file__).resolve().parent.parent
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank: int, world: int, port: int, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    sys.path.insert(0, str(REPO))
+    import bench
+    import paper_2208_14049_b200 as es
+    dist = bench.Dist(backend="gloo")
+    try:
+        nb_per_gpu = 1000 + 37  # ragged: not a multiple of the segment size
+        r0, r1, shares = bench.rank_shard(es, world, rank, [64, 64, 128, 128], nb_per_gpu)
+        rows = dist.gather([r0, r1])
+        t = dist.max(float(rank + 1) * 0.5)
+        dist.barrier()
+        q.put((rank, rows, t, shares))
+    finally:
+        dist.close()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_rank_shards_cover_every_segment_once_and_max_time(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    total = world * 1037
+    for rank, rows, t, shares in results:
+        assert t == pytest.approx(world * 0.5)  # max over ranks
+        spans = sorted(tuple(r) for r in rows)
+        assert spans[0][0] == 0 and spans[-1][1] == total
+        for (a0, a1), (b0, b1) in zip(spans, spans[1:]):
+            assert a1 == b0  # contiguous, no overlap, no gap
+        assert len(shares) == 4  # one worker per member on this rank's device row
+
+
+def test_segment_shares_exactly_once_for_mixed_layouts():
+    sys.path.insert(0, str(REPO))
+    import paper_2208_14049_b200 as es
+    A = es.AllocationMatrix.from_array([[16, 0], [32, 8], [0, 64]])
+    shares = es.segment_shares(A, 2000, 128)  # 16 segments
+    assert [(d, m) for d, m, _, _ in shares] == [(0, 0), (1, 0), (1, 1), (2, 1)]
+    for m in (0, 1):
+        covered = []
+        for d, mm, b, e in shares:
+            if mm == m:
+                covered += list(range(b, e))
+        assert sorted(covered) == list(range(16))
