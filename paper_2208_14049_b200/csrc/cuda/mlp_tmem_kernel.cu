@@ -1,0 +1,387 @@
+// K1 v2 — fused two-layer MLP member, hidden layer resident in TMEM
+// (design in mlp_tmem_kernel.cuh).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "mlp_tmem_kernel.cuh"
+#include "tma_host.hpp"
+
+namespace es {
+
+using namespace sm100;
+
+namespace {
+
+constexpr int kThreads = 320;             // w0 TMA, w1 MMA, w2..w9 epilogue
+constexpr int kEpiThreads = 256;
+constexpr uint32_t kSmemBudget = 232448;  // 227 KB
+constexpr uint32_t kMinSmem = 120 * 1024; // one CTA per SM: TMEM is allocated whole
+constexpr int kMaxT = 4;
+
+struct Tiles {
+  long long per_seg = 1, total = 0;
+};
+
+__device__ __forceinline__ Tiles tile_space(const MlpTArgs& a) {
+  Tiles t;
+  t.per_seg = (a.seg_size + a.b - 1) / a.b;
+  const long long nseg = a.seg_end - a.seg_begin;
+  if (nseg <= 0) return t;
+  const long long last = a.seg_end - 1;
+  const long long last_len = min((long long)a.seg_size, a.nb - last * a.seg_size);
+  t.total = (nseg - 1) * t.per_seg + (last_len + a.b - 1) / a.b;
+  return t;
+}
+
+// Tiles of group g for this CTA: returns how many (<= T) exist.
+__device__ __forceinline__ int group_tiles(const MlpTArgs& a, const Tiles& ts, int g,
+                                           long long (&row0)[kMaxT], int (&rows)[kMaxT]) {
+  int n = 0;
+  for (int k = 0; k < a.L.T; ++k) {
+    const long long t = blockIdx.x + static_cast<long long>(g * a.L.T + k) * gridDim.x;
+    if (t >= ts.total) break;
+    const long long seg = a.seg_begin + t / ts.per_seg;
+    const long long s1 = min(seg * a.seg_size + a.seg_size, a.nb);
+    const long long r0 = seg * a.seg_size + (t % ts.per_seg) * a.b;
+    row0[k] = r0;
+    rows[k] = static_cast<int>(min((long long)a.b, s1 - r0));
+    ++n;
+  }
+  return n;
+}
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  __nv_bfloat162 p = __floats2bfloat162_rn(lo, hi);  // .x (low 16 bits) = lo
+  return *reinterpret_cast<uint32_t*>(&p);
+}
+
+__device__ __forceinline__ void epi_barrier() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    member_mlp2_tmem_sm100(const __grid_constant__ CUtensorMap tm_x,
+                           const __grid_constant__ CUtensorMap tm_w1,
+                           const __grid_constant__ CUtensorMap tm_w2, const MlpTArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  const MlpTLayout& L = args.L;
+  uint8_t* sW2 = smem + L.off_w2;
+  float* sBias = reinterpret_cast<float*>(smem + L.off_bias);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.off_bar);
+  uint64_t* full = bars;                  // [stages]
+  uint64_t* empty = full + L.stages;      // [stages]
+  uint64_t* acc_full = empty + L.stages;  // [2] group layer-1 accumulators ready
+  uint64_t* acc_empty = acc_full + 2;     // [2] group TMEM buffer free
+  uint64_t* a_full = acc_empty + 2;       // [kMaxT] bf16 hidden of tile k in TMEM
+  uint64_t* acc2_full = a_full + kMaxT;   // [kMaxT] layer-2 accumulators ready
+  uint64_t* w2_full = acc2_full + kMaxT;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w2_full + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int H = L.H;
+  const Tiles ts = tile_space(args);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < L.stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], 4);
+    }
+    for (int k = 0; k < kMaxT; ++k) {
+      mbar_init(&a_full[k], 8);
+      mbar_init(&acc2_full[k], 1);
+    }
+    mbar_init(w2_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tm_x);
+    tma_prefetch(&tm_w1);
+    tma_prefetch(&tm_w2);
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, static_cast<uint32_t>(L.tmem_cols));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ TMA producer
+      const uint64_t pol_stream = l2_policy_evict_first();
+      const uint64_t pol_keep = l2_policy_evict_last();
+      mbar_arrive_expect_tx(w2_full, static_cast<uint32_t>(H / 64) * 2048u);
+      for (int kc = 0; kc < H / 64; ++kc)
+        tma_load_2d(sW2 + kc * 2048, &tm_w2, w2_full, kc * 64, 0, pol_keep);
+      int stage = 0;
+      uint32_t phase = 0;
+      long long row0[kMaxT];
+      int rows[kMaxT];
+      for (int g = 0;; ++g) {
+        const int n = group_tiles(args, ts, g, row0, rows);
+        if (n == 0) break;
+        for (int kc = 0; kc < L.kchunks; ++kc) {
+          mbar_wait(&empty[stage], phase ^ 1u);
+          uint8_t* st = smem + static_cast<size_t>(stage) * L.stage_bytes;
+          mbar_arrive_expect_tx(&full[stage], static_cast<uint32_t>(n) * 16384u +
+                                                  static_cast<uint32_t>(H) * 128u);
+          for (int k = 0; k < n; ++k)
+            tma_load_2d(st + k * 16384, &tm_x, &full[stage], kc * 64,
+                        static_cast<int32_t>(row0[k]), pol_stream);
+          uint8_t* sw = st + L.T * 16384;
+          for (int mc = 0; mc < H / 128; ++mc)
+            tma_load_2d(sw + mc * 16384, &tm_w1, &full[stage], kc * 64, mc * 128, pol_keep);
+          if (++stage == L.stages) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ UMMA issuer
+      const uint32_t idesc1 = idesc_bf16_f32(128, L.NH);
+      const uint32_t idesc2 = idesc_bf16_f32(128, 16);
+      const uint32_t sW2_addr = smem_u32(sW2);
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t a_par = 0;  // bit k: parity of the next a_full[k] completion
+      bool w2_ready = false;
+      // Layer-2 work still owed for the previous group.
+      int pend_buf = -1, pend_n = 0, pend_next = 0;
+      auto layer2 = [&](int buf, int k, bool waited) {
+        if (!w2_ready) {
+          mbar_wait(w2_full, 0);
+          w2_ready = true;
+        }
+        if (!waited) mbar_wait(&a_full[k], (a_par >> k) & 1u);
+        a_par ^= 1u << k;
+        tc_fence_after();
+        const uint32_t tile = tmem_base + static_cast<uint32_t>(buf * L.group_cols + k * H);
+        const uint32_t d2 = tile + static_cast<uint32_t>(H / 4);
+        for (int hh = 0; hh < 2; ++hh)
+          for (int kk = 0; kk < H / 32; ++kk) {  // 16 hidden units per step, H/2 per half
+            const int h0 = hh * (H / 2) + kk * 16;
+            const uint32_t a = tile + static_cast<uint32_t>(hh * (H / 2) + kk * 8);
+            const uint64_t b = sdesc_k128(sW2_addr + (h0 >> 6) * 2048 + (h0 & 63) * 2);
+            umma_bf16_ta(d2, a, b, idesc2, (hh | kk) != 0);
+          }
+        umma_commit(&acc2_full[k]);
+      };
+      auto drain_pending = [&]() {
+        for (; pend_next < pend_n; ++pend_next) layer2(pend_buf, pend_next, false);
+        pend_buf = -1;
+      };
+      long long row0[kMaxT];
+      int rows[kMaxT];
+      for (int g = 0;; ++g) {
+        const int n = group_tiles(args, ts, g, row0, rows);
+        if (n == 0) break;
+        const int buf = g % L.nbuf;
+        const uint32_t use = static_cast<uint32_t>(g / L.nbuf);
+        if (pend_buf == buf) drain_pending();  // single buffer: finish the last group
+        mbar_wait(&acc_empty[buf], (use & 1u) ^ 1u);
+        tc_fence_after();
+        const uint32_t d0 = tmem_base + static_cast<uint32_t>(buf * L.group_cols);
+        for (int kc = 0; kc < L.kchunks; ++kc) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sx = smem_u32(smem + static_cast<size_t>(stage) * L.stage_bytes);
+          const uint32_t sw = sx + static_cast<uint32_t>(L.T) * 16384u;
+          for (int k = 0; k < n; ++k)
+            for (int h = 0; h < L.nh; ++h)
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const uint64_t a = sdesc_k128(sx + k * 16384 + j * 32);
+                const uint64_t b = sdesc_k128(sw + h * L.NH * 128 + j * 32);
+                umma_bf16(d0 + static_cast<uint32_t>(k * H + h * L.NH), a, b, idesc1,
+                          (kc | j) != 0);
+              }
+          umma_commit(&empty[stage]);
+          if (++stage == L.stages) {
+            stage = 0;
+            phase ^= 1u;
+          }
+          // Overlap: issue the previous group's layer 2 as its hidden tiles land.
+          while (pend_buf >= 0 && pend_next < pend_n &&
+                 mbar_test(&a_full[pend_next], (a_par >> pend_next) & 1u)) {
+            layer2(pend_buf, pend_next, true);
+            ++pend_next;
+          }
+          if (pend_buf >= 0 && pend_next == pend_n) pend_buf = -1;
+        }
+        umma_commit(&acc_full[buf]);
+        if (pend_buf >= 0) drain_pending();
+        pend_buf = buf;
+        pend_n = n;
+        pend_next = 0;
+      }
+      if (pend_buf >= 0) drain_pending();
+    }
+  } else {
+    // -------------------------------------------------------------- epilogue
+    const int ew = warp - 2;           // 0..7
+    const int q = warp & 3;            // TMEM lane quadrant
+    const int half = ew >> 2;          // hidden columns [half*H/2, (half+1)*H/2)
+    const uint32_t lane_field = static_cast<uint32_t>(q * 32) << 16;
+    for (int i = threadIdx.x - 64; i < H; i += kEpiThreads) sBias[i] = args.bias1[i];
+    epi_barrier();
+    float b2[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) b2[c] = c < L.C ? __ldg(args.bias2 + c) : 0.0f;
+    uint32_t acc2_par = 0;
+    long long row0[kMaxT];
+    int rows[kMaxT];
+    const int hw = H / 2;
+    for (int g = 0;; ++g) {
+      const int n = group_tiles(args, ts, g, row0, rows);
+      if (n == 0) break;
+      const int buf = g % L.nbuf;
+      const uint32_t use = static_cast<uint32_t>(g / L.nbuf);
+      mbar_wait(&acc_full[buf], use & 1u);
+      tc_fence_after();
+      for (int k = 0; k < n; ++k) {
+        const uint32_t col0 =
+            static_cast<uint32_t>(buf * L.group_cols + k * H + half * hw);
+        const float* bias = sBias + half * hw;
+        for (int i = 0; i < hw / 32; ++i) {
+          uint32_t r[32];
+          tmem_ld32_raw(tmem_base + lane_field + col0 + 32 * i, r);
+          tmem_ld_wait();
+          uint32_t p[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float lo = fmaxf(__uint_as_float(r[2 * j]) + bias[32 * i + 2 * j], 0.0f);
+            const float hi =
+                fmaxf(__uint_as_float(r[2 * j + 1]) + bias[32 * i + 2 * j + 1], 0.0f);
+            p[j] = pack_bf16x2(lo, hi);
+          }
+          // Columns [col0 + 16i, +16) were read in iteration i/2 (<= i): safe.
+          tmem_st16(tmem_base + lane_field + col0 + 16 * i, p);
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&a_full[k]);
+      }
+      if (half == 0) {
+        for (int k = 0; k < n; ++k) {
+          mbar_wait(&acc2_full[k], (acc2_par >> k) & 1u);
+          acc2_par ^= 1u << k;
+          tc_fence_after();
+          float z[16];
+          tmem_ld16(tmem_base + lane_field +
+                        static_cast<uint32_t>(buf * L.group_cols + k * H + H / 4),
+                    z);
+          const int r = q * 32 + lane;
+          if (r < rows[k]) {
+            float* o = args.out + (row0[k] + r) * L.C;
+#pragma unroll
+            for (int c = 0; c < 16; ++c)
+              if (c < L.C) o[c] = z[c] + b2[c];
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[buf]);
+      }
+    }
+  }
+
+  __syncthreads();
+  if (warp == 1) {
+    __syncwarp();
+    tc_fence_after();
+    tmem_dealloc(tmem_base, static_cast<uint32_t>(L.tmem_cols));
+  }
+}
+
+uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace
+
+bool mlpt_plan(int K, int H, int C, int b, MlpTLayout* out) {
+  if (K < 1 || K % 8 != 0 || H < 128 || H % 128 != 0 || H > 512 || C < 1 || C > 16 || b < 1 ||
+      b > 128)
+    return false;
+  const int kchunks = (K + 63) / 64;
+  const int nh = (H + 255) / 256;
+  const int NH = H / nh;
+  if (NH % 16 != 0) return false;
+  bool found = false;
+  MlpTLayout best;
+  for (int T = 1; T <= kMaxT; ++T) {
+    for (int nbuf = 1; nbuf <= 2; ++nbuf) {
+      const int cols = nbuf * T * H;
+      if (cols > 512) continue;
+      MlpTLayout L;
+      L.H = H;
+      L.C = C;
+      L.K = K;
+      L.kchunks = kchunks;
+      L.T = T;
+      L.nbuf = nbuf;
+      L.nh = nh;
+      L.NH = NH;
+      L.group_cols = T * H;
+      int tc = 32;
+      while (tc < cols) tc <<= 1;
+      L.tmem_cols = tc;
+      L.stage_bytes = static_cast<uint32_t>(T) * 16384u + static_cast<uint32_t>(H) * 128u;
+      const uint32_t tail = static_cast<uint32_t>(H / 64) * 2048u + static_cast<uint32_t>(H) * 4u +
+                            512u + 1024u;
+      const int stages = static_cast<int>(std::min<uint32_t>(8, (kSmemBudget - tail) / L.stage_bytes));
+      if (stages < 2) continue;
+      L.stages = stages;
+      L.off_w2 = static_cast<uint32_t>(stages) * L.stage_bytes;
+      L.off_bias = L.off_w2 + static_cast<uint32_t>(H / 64) * 2048u;
+      L.off_bar = align_up(L.off_bias + static_cast<uint32_t>(H) * 4u, 64);
+      L.smem_bytes = std::max(L.off_bar + 512u + 1024u, kMinSmem);
+      if (L.smem_bytes > kSmemBudget) continue;
+      // Cycle model per group (profiles/r1_summary.md): tensor time vs TMA
+      // ingress (~44 B/clk/SM sustained) vs an un-overlapped epilogue when the
+      // TMEM buffer is single.
+      const double mma = static_cast<double>(kchunks) * T * 2.0 * H;
+      const double ingress = static_cast<double>(kchunks) * L.stage_bytes / 44.0;
+      const double epi = T * (H / 64.0) * 110.0 + 400.0;
+      const double per_group = std::max(mma, ingress) + (nbuf == 1 ? epi : 0.0);
+      L.est_cycles_per_sample = static_cast<float>(per_group / (static_cast<double>(T) * b));
+      if (!found || L.est_cycles_per_sample < best.est_cycles_per_sample) {
+        best = L;
+        found = true;
+      }
+    }
+  }
+  if (found) *out = best;
+  return found;
+}
+
+int mlpt_launch(const MlpTArgs& args, const void* x, const void* w1, const void* w2, int grid,
+                cudaStream_t stream) {
+  const MlpTLayout& L = args.L;
+  CUtensorMap mx, mw1, mw2;
+  if (make_bf16_map(&mx, x, static_cast<uint64_t>(L.K), static_cast<uint64_t>(args.nb), 128) != 0)
+    return -1;
+  if (make_bf16_map(&mw1, w1, static_cast<uint64_t>(L.K), static_cast<uint64_t>(L.H), 128) != 0)
+    return -1;
+  if (make_bf16_map(&mw2, w2, static_cast<uint64_t>(L.H), static_cast<uint64_t>(L.C), 16) != 0)
+    return -1;
+  if (ensure_smem_attr(member_mlp2_tmem_sm100, static_cast<int>(kSmemBudget)) != 0) return -4;
+  const long long per_seg = (args.seg_size + args.b - 1) / args.b;
+  const long long tiles = (args.seg_end - args.seg_begin) * per_seg;
+  if (tiles <= 0) return 0;
+  grid = static_cast<int>(std::min<long long>(grid, (tiles + L.T - 1) / L.T));
+  member_mlp2_tmem_sm100<<<grid, kThreads, L.smem_bytes, stream>>>(mx, mw1, mw2, args);
+  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+
+}  // namespace es

@@ -13,6 +13,7 @@
 
 #include "../cuda/aux_kernels.cuh"
 #include "../cuda/mlp_kernel.cuh"
+#include "../cuda/mlp_tmem_kernel.cuh"
 #include "enserve/placement.hpp"
 
 namespace enserve {
@@ -165,7 +166,12 @@ class DeviceMember {
       throw SpecError(model.name + ": the sm_100a member kernel runs 2-layer MLPs (one hidden layer)");
     K_ = a.widths[0];
     H_ = a.widths[1];
-    if (!es::mlp2_plan(K_, H_, C_, batch, &plan_)) return false;
+    // Two sm_100a schedules of the same member; the TMEM-resident
+    // one unless it cannot hold this (H, b) or ES_MLP_KERNEL=swapab.
+    const char* pick = std::getenv("ES_MLP_KERNEL");
+    const bool want_swapab = pick && std::strcmp(pick, "swapab") == 0;
+    use_tmem_ = !want_swapab && es::mlpt_plan(K_, H_, C_, batch, &tplan_);
+    if (!use_tmem_ && !es::mlp2_plan(K_, H_, C_, batch, &plan_)) return false;
     OnDevice on(device);
     const std::size_t w1 = static_cast<std::size_t>(H_) * K_ * 2, b1 = H_ * 4u,
                       w2 = static_cast<std::size_t>(C_) * H_ * 2, b2 = C_ * 4u;
@@ -220,6 +226,20 @@ class DeviceMember {
           reinterpret_cast<const float*>(base + off_b2_), C_, r0, r1, out, stream));
       return 1;
     }
+    if (use_tmem_) {
+      es::MlpTArgs targs;
+      targs.L = tplan_;
+      targs.b = batch_;
+      targs.seg_size = seg_size;
+      targs.seg_begin = s0;
+      targs.seg_end = s1;
+      targs.nb = nb;
+      targs.bias1 = reinterpret_cast<const float*>(base + off_b1_);
+      targs.bias2 = reinterpret_cast<const float*>(base + off_b2_);
+      targs.out = out;
+      ES_LAUNCH(es::mlpt_launch(targs, x, base, base + off_w2_, grid, stream));
+      return 1;
+    }
     es::Mlp2Args args;
     args.L = plan_;
     args.b = batch_;
@@ -244,6 +264,8 @@ class DeviceMember {
   int batch_ = 1;
   int K_ = 0, H_ = 0, C_ = 1;
   es::Mlp2Layout plan_{};
+  es::MlpTLayout tplan_{};
+  bool use_tmem_ = false;
   void* weights_ = nullptr;
   std::size_t bytes_ = 0, off_b1_ = 0, off_w2_ = 0, off_b2_ = 0;
 };

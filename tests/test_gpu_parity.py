@@ -149,23 +149,48 @@ def mlp_cluster(hidden, batches, seeds=None, devices=1, nb_classes=10):
                           [8, 16, 32, 64, 128], 128)
 
 
+@pytest.fixture(params=["tmem", "swapab"])
+def mlp_kernel(request):
+    """Both sm_100a schedules of K1."""
+    old = os.environ.get("ES_MLP_KERNEL")
+    os.environ["ES_MLP_KERNEL"] = request.param
+    yield request.param
+    if old is None:
+        del os.environ["ES_MLP_KERNEL"]
+    else:
+        os.environ["ES_MLP_KERNEL"] = old
+
+
 @pytest.mark.parametrize("H", [128, 256, 384, 512])
 @pytest.mark.parametrize("b", [8, 16, 32, 64, 128])
-def test_member_kernel_matches_cpu_oracle(H, b):
-    nb = 300  # segments of 128 / 128 / 44: ragged tail and partial tiles
+def test_member_kernel_matches_cpu_oracle(H, b, mlp_kernel):
+    nb = 300  # one 300-row segment: ragged last tile for every b
     X = refcpu.features(7, nb, 784)
     model = es.mlp_model(0, "m", [784, H, 10], 1234 + H)
     try:
         member = es.Member(model, b)
     except es.StartupError:
         # the tile plan does not fit one SM: documented out-of-memory load()
-        assert H * b >= 384 * 128
+        assert mlp_kernel == "swapab" and H * b >= 384 * 128
         return
     got = member.predict(X)
     cpu = refcpu.CpuMlp([784, H, 10], 1234 + H)
     want = cpu.forward(X)
     assert_logits_close(got, want, cpu.logit_scale(X))
     np.testing.assert_array_equal(np.argmax(got, 1), np.argmax(want, 1))
+
+
+@pytest.mark.parametrize("H,b", [(512, 128), (256, 128), (128, 64), (384, 32)])
+def test_member_kernel_through_segments(H, b, mlp_kernel):
+    """Persistent member kernel over many 128-sample segments (tile groups,
+    double-buffered TMEM, ragged final segment) via the system."""
+    nb = 128 * 37 + 51
+    X = refcpu.features(31, nb, 784)
+    c = mlp_cluster([H], [b])
+    out = es.run_inference(es.SampleStore(X), es.AllocationMatrix.from_array([[b]]), c,
+                           es.CombinationRule.averaging())
+    cpu = refcpu.CpuMlp([784, H, 10], c.models[0].arch.weight_seed)
+    assert_logits_close(out.combined, cpu.forward(X), cpu.logit_scale(X))
 
 
 def test_member_kernel_equals_simt_cross_check():
