@@ -61,7 +61,7 @@ __global__ void dense_layer_kernel(uint64_t seed, int layer, int fan_in, int fan
   }
 }
 
-constexpr int kRowsPerBlock = 256;
+constexpr int kRowsPerBlock = 128;
 
 // Cooperative, vectorised copy of n floats global -> shared.
 __device__ __forceinline__ void stage_in(float* dst, const float* __restrict__ src, int n) {
@@ -84,23 +84,30 @@ __device__ __forceinline__ void stage_out(float* __restrict__ dst, const float* 
   }
 }
 
+// blockDim.x rows per block; every member's [rows][C] slice is staged into
+// shared memory up front (M independent 16-B load streams in flight), then each
+// thread folds its own row across members.  The result reuses member 0's slot:
+// thread r only ever reads and writes row r there, so no barrier is needed
+// between the fold and the write-back.
 __global__ void __launch_bounds__(kRowsPerBlock) combine_kernel(const CombineArgs a) {
-  __shared__ __align__(16) float tile[kRowsPerBlock * kMaxClasses];
-  const long long row0 = static_cast<long long>(blockIdx.x) * kRowsPerBlock;
-  const int nrows = static_cast<int>(min(static_cast<long long>(kRowsPerBlock), a.rows - row0));
+  extern __shared__ __align__(16) float tiles[];
+  const int R = blockDim.x;
+  const long long row0 = static_cast<long long>(blockIdx.x) * R;
+  const int nrows = static_cast<int>(min(static_cast<long long>(R), a.rows - row0));
   const int C = a.C;
   const int n = nrows * C;
   const int r = threadIdx.x;
   const bool active = r < nrows;
 
+  for (int m = 0; m < a.M; ++m) stage_in(tiles + m * R * C, a.logits[m] + row0 * C, n);
+  __syncthreads();
+
   float acc[kMaxClasses];
 #pragma unroll
   for (int c = 0; c < kMaxClasses; ++c) acc[c] = 0.0f;
-
-  for (int m = 0; m < a.M; ++m) {
-    stage_in(tile, a.logits[m] + row0 * C, n);
-    __syncthreads();
-    if (active) {
+  if (active) {
+    for (int m = 0; m < a.M; ++m) {
+      const float* tile = tiles + m * R * C;
       float z[kMaxClasses];
 #pragma unroll
       for (int c = 0; c < kMaxClasses; ++c) z[c] = c < C ? tile[r * C + c] : 0.0f;
@@ -140,15 +147,11 @@ __global__ void __launch_bounds__(kRowsPerBlock) combine_kernel(const CombineArg
           if (c < C) acc[c] = __fadd_rn(acc[c], __fmul_rn(z[c], w));
       }
     }
-    __syncthreads();
-  }
-
-  if (active) {
     int best = 0;
     float top = acc[0];
 #pragma unroll
     for (int c = 0; c < kMaxClasses; ++c) {
-      if (c < C) tile[r * C + c] = acc[c];
+      if (c < C) tiles[r * C + c] = acc[c];
       if (c > 0 && c < C && acc[c] > top) {
         top = acc[c];
         best = c;
@@ -157,7 +160,7 @@ __global__ void __launch_bounds__(kRowsPerBlock) combine_kernel(const CombineArg
     if (a.argmax) a.argmax[row0 + r] = best;
   }
   __syncthreads();
-  stage_out(a.y + row0 * C, tile, n);
+  stage_out(a.y + row0 * C, tiles, n);
 }
 
 // One block per sample: fp32 accumulation over bf16 operands, hidden rounded
@@ -257,8 +260,12 @@ int generate_features_bf16(uint64_t seed, size_t n, __nv_bfloat16* y, cudaStream
 int combine_launch(const CombineArgs& a, cudaStream_t s) {
   if (a.rows <= 0) return 0;
   if (a.M < 1 || a.M > kMaxMembers || a.C < 1 || a.C > kMaxClasses) return -2;
-  const long long blocks = (a.rows + kRowsPerBlock - 1) / kRowsPerBlock;
-  combine_kernel<<<static_cast<unsigned>(blocks), kRowsPerBlock, 0, s>>>(a);
+  // Rows per block: 128, fewer when M*C slices would not fit 48 KB of smem.
+  int R = kRowsPerBlock;
+  while (R > 8 && static_cast<size_t>(a.M) * R * a.C * sizeof(float) > 48 * 1024) R /= 2;
+  const size_t smem = static_cast<size_t>(a.M) * R * a.C * sizeof(float);
+  const long long blocks = (a.rows + R - 1) / R;
+  combine_kernel<<<static_cast<unsigned>(blocks), R, smem, s>>>(a);
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 

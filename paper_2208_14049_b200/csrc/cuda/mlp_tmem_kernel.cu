@@ -350,10 +350,12 @@ bool mlpt_plan(int K, int H, int C, int b, MlpTLayout* out) {
       // Cycle model per group (profiles/r1_summary.md): tensor time vs TMA
       // ingress (~44 B/clk/SM sustained) vs an un-overlapped epilogue when the
       // TMEM buffer is single.
+      // X also has to come from HBM: ~25 B/clk/SM (7.2 TB/s over 148 SMs).
       const double mma = static_cast<double>(kchunks) * T * 2.0 * H;
       const double ingress = static_cast<double>(kchunks) * L.stage_bytes / 44.0;
+      const double hbm = static_cast<double>(T) * b * K * 2.0 / 25.0;
       const double epi = T * (H / 64.0) * 110.0 + 400.0;
-      const double per_group = std::max(mma, ingress) + (nbuf == 1 ? epi : 0.0);
+      const double per_group = std::max({mma, ingress, hbm}) + (nbuf == 1 ? epi : 0.0);
       L.est_cycles_per_sample = static_cast<float>(per_group / (static_cast<double>(T) * b));
       if (!found || L.est_cycles_per_sample < best.est_cycles_per_sample) {
         best = L;

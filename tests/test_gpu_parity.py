@@ -184,6 +184,8 @@ def test_member_kernel_matches_cpu_oracle(H, b, mlp_kernel):
 def test_member_kernel_through_segments(H, b, mlp_kernel):
     """Persistent member kernel over many 128-sample segments (tile groups,
     double-buffered TMEM, ragged final segment) via the system."""
+    if mlp_kernel == "swapab" and H * b >= 384 * 128:
+        pytest.skip("tile does not fit one SM with the swap-AB schedule (load() = OOM)")
     nb = 128 * 37 + 51
     X = refcpu.features(31, nb, 784)
     c = mlp_cluster([H], [b])
