@@ -285,7 +285,8 @@ def run_b200(args, dist: Dist) -> dict | None:
     local_nb = r1 - r0
     X = es.SampleStore(synthetic_seed=args.seed + dist.rank * 7919, nb=local_nb, width=784,
                        device=gpu)
-    system = es.InferenceSystem(A, cluster, rule, device_map=[gpu], copy_outputs=False)
+    system = es.InferenceSystem(A, cluster, rule, device_map=[gpu], copy_outputs=False,
+                                e2e_host_convert=bool(args.e2e_host_convert))
     for _ in range(args.warmup):
         system.run(X, copy=False)
     launches = 0
@@ -423,6 +424,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--no-e2e", dest="e2e", action="store_false",
                     help="profiling: a single e2e step")
+    ap.add_argument("--e2e-host-convert", type=int, default=1,
+                    help="e2e: 1 = host fp32->bf16 before the H2D copy, 0 = fp32 over PCIe")
     ap.add_argument("--matrix", default="",
                     help="profiling: batch per member (e.g. 64,64,128,128), skips the greedy")
     args = ap.parse_args()

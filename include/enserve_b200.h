@@ -87,6 +87,8 @@ typedef struct es_pool_opts {
   int sms_per_worker;    /* 0 = all SMs (persistent grid) */
   int overlap_colocated; /* 1 = one stream per worker; 0 = co-located workers
                             time-share one stream per GPU */
+  size_t e2e_chunk_rows; /* es_system_run_host pipeline chunk (0 = 65536) */
+  int e2e_host_convert;  /* 1 = host converts fp32 -> bf16 before the H2D copy */
 } es_pool_opts;
 
 /* RunStats (pipeline.hpp:19-25). */
@@ -220,6 +222,8 @@ es_status es_system_run(es_system* s, es_store* X, float* Y, int32_t* winners,
  * all inside the CUDA-event window. */
 es_status es_system_run_host(es_system* s, const float* X, size_t nb, size_t width, float* Y,
                              int32_t* labels, double* elapsed_s);
+/* The host converter of es_system_run_host: y = bf16_rn(x), all host threads. */
+es_status es_host_convert_bf16(const float* x, uint16_t* y, size_t n);
 /* workers_per_model[M] (pipeline.hpp:86-89) + launches of the last run. */
 es_status es_system_info(es_system* s, int* workers, int* workers_per_model, int* launches,
                          int* combine_device);

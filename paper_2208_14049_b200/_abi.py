@@ -43,7 +43,8 @@ class RuleDesc(C.Structure):
 class PoolOpts(C.Structure):
     _fields_ = [("device_map", c_int_p), ("n_device_map", C.c_int), ("copy_outputs", C.c_int),
                 ("warmup", C.c_int), ("sms_per_worker", C.c_int),
-                ("overlap_colocated", C.c_int)]
+                ("overlap_colocated", C.c_int), ("e2e_chunk_rows", C.c_size_t),
+                ("e2e_host_convert", C.c_int)]
 
 
 class RunStats(C.Structure):
@@ -116,7 +117,8 @@ _SIGS = {
                                 C.POINTER(RunStats)]),
     "es_system_run_host": (C.c_int, [C.c_void_p, c_float_p, C.c_size_t, C.c_size_t, c_float_p,
                                      c_int32_p, c_double_p]),
-    "es_system_info": (C.c_int, [C.c_void_p, c_int_p, c_int_p, c_int_p, c_int_p]),
+    "es_host_convert_bf16": (C.c_int, [c_float_p, C.POINTER(C.c_uint16), C.c_size_t]),
+    "es_system_info":(C.c_int, [C.c_void_p, c_int_p, c_int_p, c_int_p, c_int_p]),
     "es_system_timing": (C.c_int, [C.c_void_p, c_double_p, c_double_p]),
     "es_system_shutdown": (C.c_int, [C.c_void_p]),
     "es_system_destroy": (None, [C.c_void_p]),

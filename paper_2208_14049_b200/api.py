@@ -544,7 +544,8 @@ class CombinationRule:
 
 
 def _pool_opts(keep: list, device_map=None, copy_outputs=True, warmup=True,
-               sms_per_worker=0, overlap_colocated=False) -> _abi.PoolOpts:
+               sms_per_worker=0, overlap_colocated=False, e2e_chunk_rows=0,
+               e2e_host_convert=True) -> _abi.PoolOpts:
     """PoolOptions (runtime.hpp)."""
     dm = None
     n = 0
@@ -553,9 +554,19 @@ def _pool_opts(keep: list, device_map=None, copy_outputs=True, warmup=True,
         keep.append(dm)
         n = len(device_map)
     o = _abi.PoolOpts(C.cast(dm, _abi.c_int_p) if dm is not None else None, n, int(copy_outputs),
-                      int(warmup), int(sms_per_worker), int(overlap_colocated))
+                      int(warmup), int(sms_per_worker), int(overlap_colocated),
+                      int(e2e_chunk_rows), int(e2e_host_convert))
     keep.append(o)
     return o
+
+
+def host_convert_bf16(x: np.ndarray) -> np.ndarray:
+    """The e2e host converter: bf16 bits (uint16) of x, round-to-nearest-even."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    y = np.empty(x.shape, dtype=np.uint16)
+    _check(lib().es_host_convert_bf16(x.ctypes.data_as(_abi.c_float_p),
+                                      y.ctypes.data_as(C.POINTER(C.c_uint16)), x.size))
+    return y
 
 
 def device_count() -> int:

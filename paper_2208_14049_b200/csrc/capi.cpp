@@ -11,6 +11,7 @@
 #include <random>
 #include <string>
 
+#include "enserve/host_convert.hpp"
 #include "enserve/placement.hpp"
 #include "enserve/rng.hpp"
 #include "enserve/runtime.hpp"
@@ -145,6 +146,8 @@ PoolOptions to_opts(const es_pool_opts* o) {
   p.warmup = o->warmup != 0;
   p.sms_per_worker = o->sms_per_worker;
   p.overlap_colocated = o->overlap_colocated != 0;
+  if (o->e2e_chunk_rows > 0) p.e2e_chunk_rows = o->e2e_chunk_rows;
+  p.e2e_host_convert = o->e2e_host_convert != 0;
   return p;
 }
 
@@ -526,6 +529,14 @@ es_status es_system_run_host(es_system* s, const float* X, size_t nb, size_t wid
     need(s && X, "NULL handle");
     double t = s->sys->run_host(X, nb, width, Y, labels);
     if (elapsed_s) *elapsed_s = t;
+    return ES_OK;
+  });
+}
+
+es_status es_host_convert_bf16(const float* x, uint16_t* y, size_t n) {
+  return guard([&] {
+    static ThreadPool pool(0);
+    convert_f32_to_bf16_host(x, y, n, pool);
     return ES_OK;
   });
 }

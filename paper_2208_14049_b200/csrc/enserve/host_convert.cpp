@@ -1,0 +1,117 @@
+#include "enserve/host_convert.hpp"
+
+#include <immintrin.h>
+
+#include <algorithm>
+#include <cstring>
+
+namespace enserve {
+
+ThreadPool::ThreadPool(int threads) {
+  if (threads <= 0) threads = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+  for (int i = 0; i < threads; ++i) workers_.emplace_back([this, i] { loop(i); });
+}
+
+ThreadPool::~ThreadPool() {
+  {
+    std::lock_guard<std::mutex> lock(mu_);
+    stop_ = true;
+  }
+  cv_.notify_all();
+  for (std::thread& t : workers_) t.join();
+}
+
+void ThreadPool::run(const std::function<void(int, int)>& fn) {
+  std::unique_lock<std::mutex> lock(mu_);
+  job_ = &fn;
+  pending_ = size();
+  ++generation_;
+  cv_.notify_all();
+  done_cv_.wait(lock, [&] { return pending_ == 0; });
+  job_ = nullptr;
+}
+
+void ThreadPool::loop(int index) {
+  std::uint64_t seen = 0;
+  for (;;) {
+    const std::function<void(int, int)>* job;
+    {
+      std::unique_lock<std::mutex> lock(mu_);
+      cv_.wait(lock, [&] { return stop_ || generation_ != seen; });
+      if (stop_) return;
+      seen = generation_;
+      job = job_;
+    }
+    (*job)(index, size());
+    {
+      std::lock_guard<std::mutex> lock(mu_);
+      if (--pending_ == 0) done_cv_.notify_all();
+    }
+  }
+}
+
+namespace {
+
+inline std::uint16_t bf16_rn(float f) {
+  std::uint32_t u;
+  std::memcpy(&u, &f, 4);
+  if ((u & 0x7f800000u) == 0x7f800000u && (u & 0x007fffffu)) return static_cast<std::uint16_t>((u | 0x00400000u) >> 16);
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return static_cast<std::uint16_t>(u >> 16);
+}
+
+__attribute__((target("avx512f,avx512bf16"))) void convert_avx512bf16(const float* x,
+                                                                      std::uint16_t* y,
+                                                                      std::size_t n) {
+  std::size_t i = 0;
+  for (; i + 32 <= n; i += 32) {
+    __m512 a = _mm512_loadu_ps(x + i);
+    __m512 b = _mm512_loadu_ps(x + i + 16);
+    __m512bh p = _mm512_cvtne2ps_pbh(b, a);  // low half from a
+    _mm512_storeu_si512(reinterpret_cast<void*>(y + i), reinterpret_cast<__m512i>(p));
+  }
+  for (; i < n; ++i) y[i] = bf16_rn(x[i]);
+}
+
+__attribute__((target("avx2"))) void convert_avx2(const float* x, std::uint16_t* y,
+                                                  std::size_t n) {
+  std::size_t i = 0;
+  const __m256i one = _mm256_set1_epi32(1), bias = _mm256_set1_epi32(0x7fff);
+  for (; i + 8 <= n; i += 8) {
+    __m256i u = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(x + i));
+    __m256i lsb = _mm256_and_si256(_mm256_srli_epi32(u, 16), one);
+    __m256i r = _mm256_srli_epi32(_mm256_add_epi32(_mm256_add_epi32(u, bias), lsb), 16);
+    // pack 8 x u32 (values < 2^16) into 8 x u16
+    __m128i lo = _mm256_castsi256_si128(r), hi = _mm256_extracti128_si256(r, 1);
+    _mm_storeu_si128(reinterpret_cast<__m128i*>(y + i), _mm_packus_epi32(lo, hi));
+  }
+  for (; i < n; ++i) y[i] = bf16_rn(x[i]);
+}
+
+bool has_avx512bf16() {
+  static const bool yes = __builtin_cpu_supports("avx512bf16");
+  return yes;
+}
+
+}  // namespace
+
+void convert_f32_to_bf16_range(const float* x, std::uint16_t* y, std::size_t n) {
+  if (has_avx512bf16())
+    convert_avx512bf16(x, y, n);
+  else if (__builtin_cpu_supports("avx2"))
+    convert_avx2(x, y, n);
+  else
+    for (std::size_t i = 0; i < n; ++i) y[i] = bf16_rn(x[i]);
+}
+
+void convert_f32_to_bf16_host(const float* x, std::uint16_t* y, std::size_t n, ThreadPool& pool) {
+  const std::function<void(int, int)> job = [&](int part, int parts) {
+    const std::size_t per = (n / parts + 63) / 64 * 64;
+    const std::size_t a = std::min(n, static_cast<std::size_t>(part) * per);
+    const std::size_t b = std::min(n, a + per);
+    if (b > a) convert_f32_to_bf16_range(x + a, y + a, b - a);
+  };
+  pool.run(job);
+}
+
+}  // namespace enserve

@@ -14,7 +14,10 @@
 #include "../cuda/aux_kernels.cuh"
 #include "../cuda/mlp_kernel.cuh"
 #include "../cuda/mlp_tmem_kernel.cuh"
+#include "enserve/host_convert.hpp"
 #include "enserve/placement.hpp"
+
+#include <chrono>
 
 namespace enserve {
 
@@ -52,6 +55,29 @@ struct OnDevice {
   }
   ~OnDevice() { cudaSetDevice(prev); }
 };
+
+// K3 arguments for M per-model logit buffers of `rows` rows.
+es::CombineArgs combine_args(const CombinationRule& rule, const std::vector<float*>& logits,
+                             std::size_t rows, int C, float* y, int32_t* labels) {
+  es::CombineArgs ca;
+  ca.M = static_cast<int>(logits.size());
+  ca.C = C;
+  ca.rows = static_cast<long long>(rows);
+  ca.y = y;
+  ca.argmax = labels;
+  ca.softmax = rule.member_softmax ? 1 : 0;
+  ca.rule = rule.kind == CombinationRule::Kind::majority_vote        ? es::kVote
+            : rule.kind == CombinationRule::Kind::weighted_averaging ? es::kWeighted
+                                                                       : es::kAverage;
+  const float inv = 1.0f / static_cast<float>(ca.M);  // combine.cpp:101
+  for (int m = 0; m < ca.M; ++m) {
+    ca.logits[m] = logits[m];
+    ca.weight[m] = rule.kind == CombinationRule::Kind::weighted_averaging
+                       ? static_cast<float>(rule.weights[m])
+                       : inv;
+  }
+  return ca;
+}
 
 bool member_kernel_simt() {
   const char* v = std::getenv("ES_MEMBER_KERNEL");
@@ -293,10 +319,39 @@ struct InferenceSystem::Impl {
   float* y = nullptr;
   int32_t* labels = nullptr;
   std::size_t cap_rows = 0;
-  // run_host staging
-  float* x32 = nullptr;
-  void* x16 = nullptr;
-  std::size_t host_cap = 0;
+  // run_host pipeline (slots of whole-segment chunks)
+  struct Slot {
+    void* pinned = nullptr;
+    float* x32 = nullptr;
+    void* x16 = nullptr;
+    std::vector<float*> logits;
+    float* y = nullptr;
+    int32_t* labels = nullptr;
+    cudaEvent_t h2d_done = nullptr, comp_done = nullptr, d2h_done = nullptr;
+  };
+  Slot slots[3];
+  cudaStream_t copy = nullptr, d2h = nullptr;
+  std::unique_ptr<ThreadPool> pool;
+  std::size_t e2e_chunk_elems = 0;
+  bool e2e_host_convert = false;
+  void free_e2e() {
+    for (Slot& sl : slots) {
+      if (sl.pinned) cudaFreeHost(sl.pinned);
+      cudaFree(sl.x32);
+      cudaFree(sl.x16);
+      for (float* p : sl.logits) cudaFree(p);
+      cudaFree(sl.y);
+      cudaFree(sl.labels);
+      if (sl.h2d_done) cudaEventDestroy(sl.h2d_done);
+      if (sl.comp_done) cudaEventDestroy(sl.comp_done);
+      if (sl.d2h_done) cudaEventDestroy(sl.d2h_done);
+      sl = Slot{};
+    }
+    if (copy) cudaStreamDestroy(copy);
+    if (d2h) cudaStreamDestroy(d2h);
+    copy = d2h = nullptr;
+    e2e_chunk_elems = 0;
+  }
   std::shared_ptr<const SampleStore> store;
   CombinationRule rule;
   std::size_t segments = 0;
@@ -414,8 +469,7 @@ void InferenceSystem::shutdown() {
     for (float* p : impl_->logits) cudaFree(p);
     cudaFree(impl_->y);
     cudaFree(impl_->labels);
-    cudaFree(impl_->x32);
-    cudaFree(impl_->x16);
+    impl_->free_e2e();
     cudaEventDestroy(impl_->start);
     cudaEventDestroy(impl_->combine_begin);
     cudaEventDestroy(impl_->end);
@@ -519,24 +573,8 @@ std::size_t InferenceSystem::broadcast() {
   OnDevice on(combine_dev_);
   for (auto& w : workers_) ES_CUDA(cudaStreamWaitEvent(impl_->main, w->ev_done, 0));
   ES_CUDA(cudaEventRecord(impl_->combine_begin, impl_->main));
-  es::CombineArgs ca;
-  const CombinationRule& rule = impl_->rule;
-  ca.M = cluster_.model_count();
-  ca.C = C;
-  ca.rows = nb;
-  ca.y = impl_->y;
-  ca.argmax = impl_->labels;
-  ca.softmax = rule.member_softmax ? 1 : 0;
-  ca.rule = rule.kind == CombinationRule::Kind::majority_vote ? es::kVote
-            : rule.kind == CombinationRule::Kind::weighted_averaging ? es::kWeighted
-                                                                       : es::kAverage;
-  const float inv = 1.0f / static_cast<float>(ca.M);
-  for (int m = 0; m < ca.M; ++m) {
-    ca.logits[m] = impl_->logits[m];
-    ca.weight[m] = rule.kind == CombinationRule::Kind::weighted_averaging
-                       ? static_cast<float>(rule.weights[m])
-                       : inv;
-  }
+  es::CombineArgs ca = combine_args(impl_->rule, impl_->logits, static_cast<std::size_t>(nb),
+                                    C, impl_->y, impl_->labels);
   if (nb > 0) {
     ES_LAUNCH(es::combine_launch(ca, impl_->main));
     ++launches_;
@@ -602,84 +640,101 @@ double InferenceSystem::last_combine_ms() const {
   return ms;
 }
 
+// End to end from host memory, pipelined over chunks of whole segments:
+//   host threads: fp32 -> bf16 of chunk i into a pinned slot (2 B/feature on
+//                 the wire) — or, with e2e_host_convert off, the fp32 chunk
+//                 itself is copied and converted on the device;
+//   copy stream:  H2D of chunk i while chunk i-1 computes;
+//   main stream:  member kernels + combine of chunk i into slot buffers;
+//   d2h stream:   combined probabilities + labels of chunk i back to the caller.
+// The returned time is host wall-clock around the whole call (it includes the
+// host conversion, which no CUDA event can see).
 double InferenceSystem::run_host(const float* X, std::size_t nb, std::size_t width, float* Y_out,
                                  std::int32_t* labels_out) {
   for (const auto& w : workers_)
     if (w->phys != combine_dev_) throw SpecError("run_host needs every worker on one GPU");
   if (run_open_) throw Error("previous run still open");
+  for (const ModelSpec& m : cluster_.models)
+    if (m.arch.kind == MemberArch::Kind::MLP && static_cast<std::size_t>(m.arch.widths[0]) != width)
+      throw SpecError(m.name + ": input width differs from the samples'");
   OnDevice on(combine_dev_);
-  const std::size_t n = nb * width;
-  if (n > impl_->host_cap) {
-    cudaFree(impl_->x32);
-    cudaFree(impl_->x16);
-    impl_->x32 = nullptr;
-    impl_->x16 = nullptr;
-    ES_CUDA(cudaMalloc(&impl_->x32, std::max<std::size_t>(n, 1) * sizeof(float)));
-    ES_CUDA(cudaMalloc(&impl_->x16, std::max<std::size_t>(n, 1) * sizeof(__nv_bfloat16)));
-    impl_->host_cap = n;
-  }
+  Impl& I = *impl_;
   const int C = output_width_;
-  // Segment shares as in begin_run; X itself is staged inside the window.
-  assign_shares(nb);
-  if (nb > impl_->cap_rows) {
-    for (float*& p : impl_->logits) {
-      cudaFree(p);
-      p = nullptr;
+  const int M = cluster_.model_count();
+  const std::size_t seg = static_cast<std::size_t>(cluster_.segment_size);
+  const std::size_t chunk = std::max<std::size_t>(seg, (options_.e2e_chunk_rows / seg) * seg);
+  const bool host_convert = options_.e2e_host_convert;
+  constexpr int kSlots = 3;
+  if (chunk * width > I.e2e_chunk_elems || host_convert != I.e2e_host_convert) {
+    I.free_e2e();
+    I.e2e_chunk_elems = chunk * width;
+    I.e2e_host_convert = host_convert;
+    for (int s = 0; s < kSlots; ++s) {
+      Impl::Slot& sl = I.slots[s];
+      const std::size_t xb = chunk * width * (host_convert ? 2 : 4);
+      ES_CUDA(cudaHostAlloc(&sl.pinned, xb, cudaHostAllocDefault));
+      if (!host_convert) ES_CUDA(cudaMalloc(&sl.x32, chunk * width * sizeof(float)));
+      ES_CUDA(cudaMalloc(&sl.x16, chunk * width * 2));
+      sl.logits.assign(M, nullptr);
+      for (float*& p : sl.logits) ES_CUDA(cudaMalloc(&p, chunk * C * sizeof(float)));
+      ES_CUDA(cudaMalloc(&sl.y, chunk * C * sizeof(float)));
+      ES_CUDA(cudaMalloc(&sl.labels, chunk * sizeof(int32_t)));
+      ES_CUDA(cudaEventCreateWithFlags(&sl.h2d_done, cudaEventDisableTiming));
+      ES_CUDA(cudaEventCreateWithFlags(&sl.comp_done, cudaEventDisableTiming));
+      ES_CUDA(cudaEventCreateWithFlags(&sl.d2h_done, cudaEventDisableTiming));
     }
-    cudaFree(impl_->y);
-    cudaFree(impl_->labels);
-    for (float*& p : impl_->logits) ES_CUDA(cudaMalloc(&p, nb * C * sizeof(float)));
-    ES_CUDA(cudaMalloc(&impl_->y, nb * C * sizeof(float)));
-    ES_CUDA(cudaMalloc(&impl_->labels, nb * sizeof(int32_t)));
-    impl_->cap_rows = nb;
+    ES_CUDA(cudaStreamCreateWithFlags(&I.copy, cudaStreamNonBlocking));
+    ES_CUDA(cudaStreamCreateWithFlags(&I.d2h, cudaStreamNonBlocking));
   }
+  if (!I.pool) I.pool = std::make_unique<ThreadPool>(0);
+  ES_CUDA(cudaDeviceSynchronize());
+  const auto t0 = std::chrono::steady_clock::now();
   launches_ = 0;
-  ES_CUDA(cudaEventRecord(impl_->start, impl_->main));
-  ES_CUDA(cudaMemcpyAsync(impl_->x32, X, n * sizeof(float), cudaMemcpyHostToDevice, impl_->main));
-  ES_LAUNCH(es::convert_f32_to_bf16(impl_->x32, static_cast<__nv_bfloat16*>(impl_->x16), n,
-                                    impl_->main));
-  ++launches_;
-  cudaEvent_t ready;
-  ES_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-  ES_CUDA(cudaEventRecord(ready, impl_->main));
-  for (auto& w : workers_) {
-    ES_CUDA(cudaStreamWaitEvent(w->stream, ready, 0));
-    launches_ += w->member->forward(impl_->x16, static_cast<long long>(nb), cluster_.segment_size,
-                                    w->seg_begin, w->seg_end, impl_->logits[w->model],
-                                    es::num_sms(w->phys), w->stream);
-    ES_CUDA(cudaEventRecord(w->ev_done, w->stream));
-    ES_CUDA(cudaStreamWaitEvent(impl_->main, w->ev_done, 0));
+  const std::size_t nchunks = (nb + chunk - 1) / chunk;
+  const int grid = es::num_sms(combine_dev_);
+  for (std::size_t i = 0; i < nchunks; ++i) {
+    Impl::Slot& sl = I.slots[i % kSlots];
+    const std::size_t r0 = i * chunk;
+    const std::size_t rows = std::min(chunk, nb - r0);
+    const std::size_t elems = rows * width;
+    if (i >= kSlots) ES_CUDA(cudaEventSynchronize(sl.h2d_done));  // pinned slot reusable
+    if (host_convert)
+      convert_f32_to_bf16_host(X + r0 * width, static_cast<std::uint16_t*>(sl.pinned), elems,
+                               *I.pool);
+    else
+      std::memcpy(sl.pinned, X + r0 * width, elems * sizeof(float));
+    if (i >= kSlots) ES_CUDA(cudaStreamWaitEvent(I.copy, sl.d2h_done, 0));  // slot buffers free
+    ES_CUDA(cudaMemcpyAsync(host_convert ? sl.x16 : static_cast<void*>(sl.x32), sl.pinned,
+                            elems * (host_convert ? 2 : 4), cudaMemcpyHostToDevice, I.copy));
+    ES_CUDA(cudaEventRecord(sl.h2d_done, I.copy));
+    ES_CUDA(cudaStreamWaitEvent(I.main, sl.h2d_done, 0));
+    if (!host_convert) {
+      ES_LAUNCH(es::convert_f32_to_bf16(sl.x32, static_cast<__nv_bfloat16*>(sl.x16), elems, I.main));
+      ++launches_;
+    }
+    std::vector<SegmentShare> shares = segment_shares(matrix_, rows, cluster_.segment_size);
+    for (std::size_t w = 0; w < workers_.size(); ++w)
+      launches_ += workers_[w]->member->forward(sl.x16, static_cast<long long>(rows),
+                                                cluster_.segment_size, shares[w].begin,
+                                                shares[w].end, sl.logits[workers_[w]->model], grid,
+                                                I.main);
+    es::CombineArgs ca = combine_args(rule_, sl.logits, rows, C, sl.y, sl.labels);
+    ES_LAUNCH(es::combine_launch(ca, I.main));
+    ++launches_;
+    ES_CUDA(cudaEventRecord(sl.comp_done, I.main));
+    ES_CUDA(cudaStreamWaitEvent(I.d2h, sl.comp_done, 0));
+    if (Y_out)
+      ES_CUDA(cudaMemcpyAsync(Y_out + r0 * C, sl.y, rows * C * sizeof(float),
+                              cudaMemcpyDeviceToHost, I.d2h));
+    if (labels_out)
+      ES_CUDA(cudaMemcpyAsync(labels_out + r0, sl.labels, rows * sizeof(int32_t),
+                              cudaMemcpyDeviceToHost, I.d2h));
+    ES_CUDA(cudaEventRecord(sl.d2h_done, I.d2h));
   }
-  es::CombineArgs ca;
-  ca.M = cluster_.model_count();
-  ca.C = C;
-  ca.rows = static_cast<long long>(nb);
-  ca.y = impl_->y;
-  ca.argmax = impl_->labels;
-  ca.softmax = rule_.member_softmax ? 1 : 0;
-  ca.rule = rule_.kind == CombinationRule::Kind::majority_vote ? es::kVote
-            : rule_.kind == CombinationRule::Kind::weighted_averaging ? es::kWeighted
-                                                                        : es::kAverage;
-  for (int m = 0; m < ca.M; ++m) {
-    ca.logits[m] = impl_->logits[m];
-    ca.weight[m] = rule_.kind == CombinationRule::Kind::weighted_averaging
-                       ? static_cast<float>(rule_.weights[m])
-                       : 1.0f / static_cast<float>(ca.M);
-  }
-  ES_LAUNCH(es::combine_launch(ca, impl_->main));
-  ++launches_;
-  if (Y_out)
-    ES_CUDA(cudaMemcpyAsync(Y_out, impl_->y, nb * C * sizeof(float), cudaMemcpyDeviceToHost,
-                            impl_->main));
-  if (labels_out)
-    ES_CUDA(cudaMemcpyAsync(labels_out, impl_->labels, nb * sizeof(int32_t),
-                            cudaMemcpyDeviceToHost, impl_->main));
-  ES_CUDA(cudaEventRecord(impl_->end, impl_->main));
-  ES_CUDA(cudaEventSynchronize(impl_->end));
-  cudaEventDestroy(ready);
-  float ms = 0.0f;
-  ES_CUDA(cudaEventElapsedTime(&ms, impl_->start, impl_->end));
-  return ms * 1e-3;
+  ES_CUDA(cudaStreamSynchronize(I.d2h));
+  ES_CUDA(cudaStreamSynchronize(I.main));
+  const auto t1 = std::chrono::steady_clock::now();
+  return std::chrono::duration<double>(t1 - t0).count();
 }
 
 // ---------------------------------------------------------------- free functions

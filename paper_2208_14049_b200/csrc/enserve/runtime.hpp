@@ -116,6 +116,10 @@ struct PoolOptions {
   bool warmup = true;         // bench: one untimed run first (module load, clocks)
   int sms_per_worker = 0;     // 0 = every SM of the device (persistent grid)
   bool overlap_colocated = false;  // one stream per worker instead of per GPU
+  // run_host: rows per pipeline chunk (rounded to whole segments) and whether
+  // the host converts fp32 -> bf16 before the copy (half the PCIe bytes).
+  std::size_t e2e_chunk_rows = 65536;
+  bool e2e_host_convert = true;
 };
 
 // Per-model executable member on one GPU (the Predictor of backend.hpp:25-34).

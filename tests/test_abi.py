@@ -7,6 +7,7 @@ import re
 import subprocess
 from pathlib import Path
 
+import numpy as np
 import pytest
 
 import paper_2208_14049_b200 as es
@@ -71,3 +72,14 @@ def test_product_does_not_link_the_oracle():
     import paper_2208_14049_b200.api as api
     src = Path(api.__file__).read_text() + Path(_abi.__file__).read_text()
     assert "oracle" not in src.replace("ORACLE", "")
+
+
+def test_host_bf16_converter_rounds_to_nearest_even():
+    from oracle.refcpu import round_bf16
+    rng = np.random.default_rng(3)
+    x = np.concatenate([rng.standard_normal(100003).astype(np.float32) * 10,
+                        np.array([0.0, -0.0, 1.0, 1.00390625, 1.0078125, 3.0e38, -3.0e-39],
+                                 dtype=np.float32)])
+    y = es.host_convert_bf16(x)
+    want = (round_bf16(x).view(np.uint32) >> 16).astype(np.uint16)
+    np.testing.assert_array_equal(y, want)

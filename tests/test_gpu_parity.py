@@ -309,3 +309,22 @@ def test_device_bench_and_greedy():
     g = es.bounded_greedy(A0, c, es.DeviceBench(calib, 1), es.GreedyConfig(3, 16, 0))
     assert es.validate_matrix(g.matrix, c).ok
     assert g.trace.final_score >= g.trace.start_score > 0
+
+
+@pytest.mark.parametrize("host_convert", [True, False])
+def test_pipelined_run_host_equals_resident_run(host_convert):
+    """e2e path: chunks of whole segments (small here, so every pinned/device
+    slot is reused), host or device fp32 -> bf16, overlapped copies — the
+    output must equal the resident run bit for bit."""
+    c = mlp_cluster([384, 128], [128, 64])
+    A = es.AllocationMatrix.from_array([[128, 64]])
+    Xh = refcpu.features(19, 128 * 11 + 17, 784)
+    rule = es.CombinationRule.averaging(softmax=True)
+    resident = es.run_inference(es.SampleStore(Xh), A, c, rule)
+    with es.InferenceSystem(A, c, rule, e2e_chunk_rows=256, e2e_host_convert=host_convert) as s:
+        Y = np.zeros_like(resident.combined)
+        lab = np.zeros(len(Xh), np.int32)
+        t = s.run_host(Xh, Y, lab)
+        assert t > 0
+    np.testing.assert_array_equal(Y, resident.combined)
+    np.testing.assert_array_equal(lab, resident.winners)
