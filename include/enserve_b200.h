@@ -88,7 +88,10 @@ typedef struct es_pool_opts {
   int overlap_colocated; /* 1 = one stream per worker; 0 = co-located workers
                             time-share one stream per GPU */
   size_t e2e_chunk_rows; /* es_system_run_host pipeline chunk (0 = 65536) */
-  int e2e_host_convert;  /* 1 = host converts fp32 -> bf16 before the H2D copy */
+  int e2e_host_convert;  /* 1 = host threads convert fp32 -> bf16 for every other
+                            chunk (all chunks if X is pageable), the rest is
+                            DMA'd as fp32 from the caller's pinned buffer;
+                            0 = every chunk DMA'd as fp32 (pinned X) */
 } es_pool_opts;
 
 /* RunStats (pipeline.hpp:19-25). */

@@ -333,7 +333,6 @@ struct InferenceSystem::Impl {
   cudaStream_t copy = nullptr, d2h = nullptr;
   std::unique_ptr<ThreadPool> pool;
   std::size_t e2e_chunk_elems = 0;
-  bool e2e_host_convert = false;
   void free_e2e() {
     for (Slot& sl : slots) {
       if (sl.pinned) cudaFreeHost(sl.pinned);
@@ -663,17 +662,23 @@ double InferenceSystem::run_host(const float* X, std::size_t nb, std::size_t wid
   const int M = cluster_.model_count();
   const std::size_t seg = static_cast<std::size_t>(cluster_.segment_size);
   const std::size_t chunk = std::max<std::size_t>(seg, (options_.e2e_chunk_rows / seg) * seg);
-  const bool host_convert = options_.e2e_host_convert;
+  // Chunk routes: "convert" = host threads write bf16 into a
+  // pinned slot, 2 B/feature cross PCIe; "direct" = DMA straight from the
+  // caller's pinned fp32 buffer, converted on the device (no host-memory
+  // pass).  Alternating them balances host-memory bandwidth against PCIe.
+  cudaPointerAttributes pa{};
+  const bool pinned_input =
+      cudaPointerGetAttributes(&pa, X) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+  cudaGetLastError();
+  const int mode = options_.e2e_host_convert ? (pinned_input ? 0 : 1) : (pinned_input ? 2 : 1);
   constexpr int kSlots = 3;
-  if (chunk * width > I.e2e_chunk_elems || host_convert != I.e2e_host_convert) {
+  if (chunk * width > I.e2e_chunk_elems) {
     I.free_e2e();
     I.e2e_chunk_elems = chunk * width;
-    I.e2e_host_convert = host_convert;
     for (int s = 0; s < kSlots; ++s) {
       Impl::Slot& sl = I.slots[s];
-      const std::size_t xb = chunk * width * (host_convert ? 2 : 4);
-      ES_CUDA(cudaHostAlloc(&sl.pinned, xb, cudaHostAllocDefault));
-      if (!host_convert) ES_CUDA(cudaMalloc(&sl.x32, chunk * width * sizeof(float)));
+      ES_CUDA(cudaHostAlloc(&sl.pinned, chunk * width * 2, cudaHostAllocDefault));
+      ES_CUDA(cudaMalloc(&sl.x32, chunk * width * sizeof(float)));
       ES_CUDA(cudaMalloc(&sl.x16, chunk * width * 2));
       sl.logits.assign(M, nullptr);
       for (float*& p : sl.logits) ES_CUDA(cudaMalloc(&p, chunk * C * sizeof(float)));
@@ -697,18 +702,20 @@ double InferenceSystem::run_host(const float* X, std::size_t nb, std::size_t wid
     const std::size_t r0 = i * chunk;
     const std::size_t rows = std::min(chunk, nb - r0);
     const std::size_t elems = rows * width;
+    const bool convert = mode == 1 || (mode == 0 && i % 2 == 0);
     if (i >= kSlots) ES_CUDA(cudaEventSynchronize(sl.h2d_done));  // pinned slot reusable
-    if (host_convert)
+    if (convert)
       convert_f32_to_bf16_host(X + r0 * width, static_cast<std::uint16_t*>(sl.pinned), elems,
                                *I.pool);
-    else
-      std::memcpy(sl.pinned, X + r0 * width, elems * sizeof(float));
     if (i >= kSlots) ES_CUDA(cudaStreamWaitEvent(I.copy, sl.d2h_done, 0));  // slot buffers free
-    ES_CUDA(cudaMemcpyAsync(host_convert ? sl.x16 : static_cast<void*>(sl.x32), sl.pinned,
-                            elems * (host_convert ? 2 : 4), cudaMemcpyHostToDevice, I.copy));
+    if (convert)
+      ES_CUDA(cudaMemcpyAsync(sl.x16, sl.pinned, elems * 2, cudaMemcpyHostToDevice, I.copy));
+    else
+      ES_CUDA(cudaMemcpyAsync(sl.x32, X + r0 * width, elems * sizeof(float),
+                              cudaMemcpyHostToDevice, I.copy));
     ES_CUDA(cudaEventRecord(sl.h2d_done, I.copy));
     ES_CUDA(cudaStreamWaitEvent(I.main, sl.h2d_done, 0));
-    if (!host_convert) {
+    if (!convert) {
       ES_LAUNCH(es::convert_f32_to_bf16(sl.x32, static_cast<__nv_bfloat16*>(sl.x16), elems, I.main));
       ++launches_;
     }

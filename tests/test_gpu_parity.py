@@ -312,13 +312,19 @@ def test_device_bench_and_greedy():
 
 
 @pytest.mark.parametrize("host_convert", [True, False])
-def test_pipelined_run_host_equals_resident_run(host_convert):
+@pytest.mark.parametrize("pinned", [True, False])
+def test_pipelined_run_host_equals_resident_run(host_convert, pinned):
     """e2e path: chunks of whole segments (small here, so every pinned/device
     slot is reused), host or device fp32 -> bf16, overlapped copies — the
     output must equal the resident run bit for bit."""
     c = mlp_cluster([384, 128], [128, 64])
     A = es.AllocationMatrix.from_array([[128, 64]])
     Xh = refcpu.features(19, 128 * 11 + 17, 784)
+    if pinned:  # page-locked input enables the direct-DMA chunks
+        import torch
+        buf = torch.empty(Xh.shape, dtype=torch.float32, pin_memory=True)
+        buf.numpy()[:] = Xh
+        Xh = buf.numpy()
     rule = es.CombinationRule.averaging(softmax=True)
     resident = es.run_inference(es.SampleStore(Xh), A, c, rule)
     with es.InferenceSystem(A, c, rule, e2e_chunk_rows=256, e2e_host_convert=host_convert) as s:
