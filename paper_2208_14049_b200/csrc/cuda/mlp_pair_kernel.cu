@@ -1,0 +1,406 @@
+// K1 v3 — fused two-layer MLP member on SM pairs (design in mlp_pair_kernel.cuh).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "mlp_pair_kernel.cuh"
+#include "tma_host.hpp"
+
+namespace es {
+
+using namespace sm100;
+
+namespace {
+
+constexpr int kThreads = 320;             // w0 TMA, w1 TMEM + UMMA (leader), w2..w9 epilogue
+constexpr int kEpiThreads = 256;
+constexpr uint32_t kSmemBudget = 232448;
+constexpr uint32_t kMinSmem = 120 * 1024;
+constexpr int kMaxT = 2;
+constexpr uint16_t kBoth = 0b11;
+
+struct Tiles {
+  long long per_seg = 1, total = 0;
+};
+
+__device__ __forceinline__ Tiles tile_space(const MlpPArgs& a) {
+  Tiles t;
+  t.per_seg = (a.seg_size + a.b - 1) / a.b;
+  const long long nseg = a.seg_end - a.seg_begin;
+  if (nseg <= 0) return t;
+  const long long last = a.seg_end - 1;
+  const long long last_len = min((long long)a.seg_size, a.nb - last * a.seg_size);
+  t.total = (nseg - 1) * t.per_seg + (last_len + a.b - 1) / a.b;
+  return t;
+}
+
+// Group g of this pair: pair-tile tp = pair + (g*T + k) * pairs covers tiles
+// 2*tp (even CTA) and 2*tp + 1 (odd CTA).  Returns how many pair-tiles exist
+// (both CTAs agree); rows = 0 marks this CTA's tile as absent.
+__device__ __forceinline__ int group_tiles(const MlpPArgs& a, const Tiles& ts, int g,
+                                           uint32_t rank, long long (&row0)[kMaxT],
+                                           int (&rows)[kMaxT]) {
+  const long long pair = blockIdx.x >> 1, pairs = gridDim.x >> 1;
+  int n = 0;
+  for (int k = 0; k < a.L.T; ++k) {
+    const long long tp = pair + static_cast<long long>(g * a.L.T + k) * pairs;
+    if (2 * tp >= ts.total) break;
+    const long long t = 2 * tp + rank;
+    if (t < ts.total) {
+      const long long seg = a.seg_begin + t / ts.per_seg;
+      const long long s1 = min(seg * a.seg_size + a.seg_size, a.nb);
+      const long long r0 = seg * a.seg_size + (t % ts.per_seg) * a.b;
+      row0[k] = r0;
+      rows[k] = static_cast<int>(min((long long)a.b, s1 - r0));
+    } else {
+      row0[k] = 0;  // load something valid; nothing is written back
+      rows[k] = 0;
+    }
+    ++n;
+  }
+  return n;
+}
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  __nv_bfloat162 p = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&p);
+}
+
+__device__ __forceinline__ void epi_barrier() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    member_mlp2_pair_sm100(const __grid_constant__ CUtensorMap tm_x,
+                           const __grid_constant__ CUtensorMap tm_w1,
+                           const __grid_constant__ CUtensorMap tm_w2, const MlpPArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  const MlpPLayout& L = args.L;
+  uint8_t* sW2 = smem + L.off_w2;
+  float* sBias = reinterpret_cast<float*>(smem + L.off_bias);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.off_bar);
+  uint64_t* full = bars;                  // [stages]   (leader's is used)
+  uint64_t* empty = full + L.stages;      // [stages]   (each SM's own)
+  uint64_t* acc_full = empty + L.stages;  // [2]        (multicast commit)
+  uint64_t* acc_empty = acc_full + 2;     // [2]        (leader's; 8 remote arrivals)
+  uint64_t* a_full = acc_empty + 2;       // [kMaxT]    (leader's; 16 remote arrivals)
+  uint64_t* acc2_full = a_full + kMaxT;   // [kMaxT]    (multicast commit)
+  uint64_t* w2_full = acc2_full + kMaxT;  //            (leader's)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w2_full + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int H = L.H;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const Tiles ts = tile_space(args);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < L.stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], 8);
+    }
+    for (int k = 0; k < kMaxT; ++k) {
+      mbar_init(&a_full[k], 16);
+      mbar_init(&acc2_full[k], 1);
+    }
+    mbar_init(w2_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tm_x);
+    tma_prefetch(&tm_w1);
+    tma_prefetch(&tm_w2);
+  }
+  if (warp == 1) tmem_alloc_pair(tmem_slot, static_cast<uint32_t>(L.tmem_cols));
+  tc_fence_before();
+  cluster_sync();  // barrier inits and TMEM of both SMs visible to both
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ TMA (both SMs)
+      const uint64_t pol_stream = l2_policy_evict_first();
+      const uint64_t pol_keep = l2_policy_evict_last();
+      if (leader) mbar_arrive_expect_tx(w2_full, 2u * static_cast<uint32_t>(H / 64) * 1024u);
+      for (int kc = 0; kc < H / 64; ++kc)
+        tma_load_2d_pair(sW2 + kc * 1024, &tm_w2, w2_full, kc * 64, static_cast<int32_t>(rank) * 8,
+                         pol_keep);
+      int stage = 0;
+      uint32_t phase = 0;
+      long long row0[kMaxT];
+      int rows[kMaxT];
+      const uint32_t half_w = static_cast<uint32_t>(L.NH / 2);
+      for (int g = 0;; ++g) {
+        const int n = group_tiles(args, ts, g, rank, row0, rows);
+        if (n == 0) break;
+        for (int kc = 0; kc < L.kchunks; ++kc) {
+          mbar_wait(&empty[stage], phase ^ 1u);
+          uint8_t* st = smem + static_cast<size_t>(stage) * L.stage_bytes;
+          if (leader)
+            mbar_arrive_expect_tx(&full[stage], 2u * (static_cast<uint32_t>(n) * 16384u +
+                                                      static_cast<uint32_t>(H) * 64u));
+          for (int k = 0; k < n; ++k)
+            tma_load_2d_pair(st + k * 16384, &tm_x, &full[stage], kc * 64,
+                             static_cast<int32_t>(row0[k]), pol_stream);
+          uint8_t* sw = st + L.T * 16384;
+          for (int h = 0; h < L.nh; ++h)
+            tma_load_2d_pair(sw + h * half_w * 128u, &tm_w1, &full[stage], kc * 64,
+                             static_cast<int32_t>(h * L.NH + rank * half_w), pol_keep);
+          if (++stage == L.stages) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      // ------------------------------------------------------------ pair UMMA issuer
+      const uint32_t idesc1 = idesc_bf16_f32(256, L.NH);
+      const uint32_t idesc2 = idesc_bf16_f32(256, 16);
+      const uint32_t sW2_addr = smem_u32(sW2);
+      const uint32_t half_w = static_cast<uint32_t>(L.NH / 2);
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t a_par = 0;
+      bool w2_ready = false;
+      int pend_buf = -1, pend_n = 0, pend_next = 0;
+      auto layer2 = [&](int buf, int k, bool waited) {
+        if (!w2_ready) {
+          mbar_wait(w2_full, 0);
+          w2_ready = true;
+        }
+        if (!waited) mbar_wait_cluster(&a_full[k], (a_par >> k) & 1u);
+        a_par ^= 1u << k;
+        tc_fence_after();
+        const uint32_t tile = tmem_base + static_cast<uint32_t>(buf * L.group_cols + k * H);
+        const uint32_t d2 = tile + static_cast<uint32_t>(H / 4);
+        for (int hh = 0; hh < 2; ++hh)
+          for (int kk = 0; kk < H / 32; ++kk) {
+            const int h0 = hh * (H / 2) + kk * 16;
+            const uint32_t a = tile + static_cast<uint32_t>(hh * (H / 2) + kk * 8);
+            const uint64_t b = sdesc_k128(sW2_addr + (h0 >> 6) * 1024 + (h0 & 63) * 2);
+            umma_bf16_pair_ta(d2, a, b, idesc2, (hh | kk) != 0);
+          }
+        umma_commit_pair(&acc2_full[k], kBoth);
+      };
+      auto drain_pending = [&]() {
+        for (; pend_next < pend_n; ++pend_next) layer2(pend_buf, pend_next, false);
+        pend_buf = -1;
+      };
+      long long row0[kMaxT];
+      int rows[kMaxT];
+      for (int g = 0;; ++g) {
+        const int n = group_tiles(args, ts, g, rank, row0, rows);
+        if (n == 0) break;
+        const int buf = g % L.nbuf;
+        const uint32_t use = static_cast<uint32_t>(g / L.nbuf);
+        if (pend_buf == buf) drain_pending();
+        mbar_wait_cluster(&acc_empty[buf], (use & 1u) ^ 1u);
+        tc_fence_after();
+        const uint32_t d0 = tmem_base + static_cast<uint32_t>(buf * L.group_cols);
+        for (int kc = 0; kc < L.kchunks; ++kc) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sx = smem_u32(smem + static_cast<size_t>(stage) * L.stage_bytes);
+          const uint32_t sw = sx + static_cast<uint32_t>(L.T) * 16384u;
+          for (int k = 0; k < n; ++k)
+            for (int h = 0; h < L.nh; ++h)
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const uint64_t a = sdesc_k128(sx + k * 16384 + j * 32);
+                const uint64_t b = sdesc_k128(sw + h * half_w * 128u + j * 32);
+                umma_bf16_pair(d0 + static_cast<uint32_t>(k * H + h * L.NH), a, b, idesc1,
+                               (kc | j) != 0);
+              }
+          umma_commit_pair(&empty[stage], kBoth);
+          if (++stage == L.stages) {
+            stage = 0;
+            phase ^= 1u;
+          }
+          while (pend_buf >= 0 && pend_next < pend_n &&
+                 mbar_test_cluster(&a_full[pend_next], (a_par >> pend_next) & 1u)) {
+            layer2(pend_buf, pend_next, true);
+            ++pend_next;
+          }
+          if (pend_buf >= 0 && pend_next == pend_n) pend_buf = -1;
+        }
+        umma_commit_pair(&acc_full[buf], kBoth);
+        if (pend_buf >= 0) drain_pending();
+        pend_buf = buf;
+        pend_n = n;
+        pend_next = 0;
+      }
+      if (pend_buf >= 0) drain_pending();
+    }
+  } else {
+    // -------------------------------------------------------------- epilogue (both SMs)
+    const int ew = warp - 2;
+    const int q = warp & 3;
+    const int half = ew >> 2;
+    const uint32_t lane_field = static_cast<uint32_t>(q * 32) << 16;
+    for (int i = threadIdx.x - 64; i < H; i += kEpiThreads) sBias[i] = args.bias1[i];
+    epi_barrier();
+    float b2[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) b2[c] = c < L.C ? __ldg(args.bias2 + c) : 0.0f;
+    uint32_t acc2_par = 0;
+    long long row0[kMaxT];
+    int rows[kMaxT];
+    const int hw = H / 2;
+    for (int g = 0;; ++g) {
+      const int n = group_tiles(args, ts, g, rank, row0, rows);
+      if (n == 0) break;
+      const int buf = g % L.nbuf;
+      const uint32_t use = static_cast<uint32_t>(g / L.nbuf);
+      mbar_wait(&acc_full[buf], use & 1u);
+      tc_fence_after();
+      for (int k = 0; k < n; ++k) {
+        const uint32_t col0 = static_cast<uint32_t>(buf * L.group_cols + k * H + half * hw);
+        const float* bias = sBias + half * hw;
+        for (int i = 0; i < hw / 32; ++i) {
+          uint32_t r[32];
+          tmem_ld32_raw(tmem_base + lane_field + col0 + 32 * i, r);
+          tmem_ld_wait();
+          uint32_t p[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float lo = fmaxf(__uint_as_float(r[2 * j]) + bias[32 * i + 2 * j], 0.0f);
+            const float hi =
+                fmaxf(__uint_as_float(r[2 * j + 1]) + bias[32 * i + 2 * j + 1], 0.0f);
+            p[j] = pack_bf16x2(lo, hi);
+          }
+          tmem_st16(tmem_base + lane_field + col0 + 16 * i, p);
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&a_full[k]), 0));
+      }
+      if (half == 0) {
+        for (int k = 0; k < n; ++k) {
+          mbar_wait(&acc2_full[k], (acc2_par >> k) & 1u);
+          acc2_par ^= 1u << k;
+          tc_fence_after();
+          float z[16];
+          tmem_ld16(tmem_base + lane_field +
+                        static_cast<uint32_t>(buf * L.group_cols + k * H + H / 4),
+                    z);
+          const int r = q * 32 + lane;
+          if (r < rows[k]) {
+            float* o = args.out + (row0[k] + r) * L.C;
+#pragma unroll
+            for (int c = 0; c < 16; ++c)
+              if (c < L.C) o[c] = z[c] + b2[c];
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&acc_empty[buf]), 0));
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // the peer is done with every pair UMMA before TMEM goes away
+  if (warp == 1) {
+    __syncwarp();
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, static_cast<uint32_t>(L.tmem_cols));
+  }
+}
+
+uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace
+
+bool mlpp_plan(int K, int H, int C, int b, MlpPLayout* out) {
+  if (K < 1 || K % 8 != 0 || H < 128 || H % 128 != 0 || H > 512 || C < 1 || C > 16 || b < 1 ||
+      b > 128)
+    return false;
+  const int kchunks = (K + 63) / 64;
+  const int nh = (H + 255) / 256;
+  const int NH = H / nh;
+  if (NH % 32 != 0) return false;  // N % 16 per UMMA, NH/2 rows 8-row aligned per SM
+  bool found = false;
+  MlpPLayout best;
+  for (int T = 1; T <= kMaxT; ++T) {
+    for (int nbuf = 1; nbuf <= 2; ++nbuf) {
+      const int cols = nbuf * T * H;
+      if (cols > 512) continue;
+      MlpPLayout L;
+      L.H = H;
+      L.C = C;
+      L.K = K;
+      L.kchunks = kchunks;
+      L.T = T;
+      L.nbuf = nbuf;
+      L.nh = nh;
+      L.NH = NH;
+      L.group_cols = T * H;
+      int tc = 32;
+      while (tc < cols) tc <<= 1;
+      L.tmem_cols = tc;
+      L.stage_bytes = static_cast<uint32_t>(T) * 16384u + static_cast<uint32_t>(H) * 64u;
+      const uint32_t tail = static_cast<uint32_t>(H / 64) * 1024u + static_cast<uint32_t>(H) * 4u +
+                            512u + 1024u;
+      const int stages =
+          static_cast<int>(std::min<uint32_t>(8, (kSmemBudget - tail) / L.stage_bytes));
+      if (stages < 2) continue;
+      L.stages = stages;
+      L.off_w2 = static_cast<uint32_t>(stages) * L.stage_bytes;
+      L.off_bias = L.off_w2 + static_cast<uint32_t>(H / 64) * 1024u;
+      L.off_bar = align_up(L.off_bias + static_cast<uint32_t>(H) * 4u, 64);
+      L.smem_bytes = std::max(L.off_bar + 512u + 1024u, kMinSmem);
+      if (L.smem_bytes > kSmemBudget) continue;
+      // Per-SM cycles per group: tensor (the pair shares one M=256 UMMA) vs TMA
+      // ingress (~44 B/clk) vs HBM share (~25 B/clk) + un-overlapped epilogue.
+      const double mma = static_cast<double>(kchunks) * T * 2.0 * H;
+      const double ingress = static_cast<double>(kchunks) * L.stage_bytes / 44.0;
+      const double hbm = static_cast<double>(T) * b * K * 2.0 / 25.0;
+      const double epi = T * (H / 64.0) * 110.0 + 600.0;
+      const double per_group = std::max({mma, ingress, hbm}) + (nbuf == 1 ? epi : 0.0);
+      L.est_cycles_per_sample = static_cast<float>(per_group / (static_cast<double>(T) * b));
+      if (!found || L.est_cycles_per_sample < best.est_cycles_per_sample) {
+        best = L;
+        found = true;
+      }
+    }
+  }
+  if (found) *out = best;
+  return found;
+}
+
+int mlpp_launch(const MlpPArgs& args, const void* x, const void* w1, const void* w2, int grid,
+                cudaStream_t stream) {
+  const MlpPLayout& L = args.L;
+  CUtensorMap mx, mw1, mw2;
+  if (make_bf16_map(&mx, x, static_cast<uint64_t>(L.K), static_cast<uint64_t>(args.nb), 128) != 0)
+    return -1;
+  if (make_bf16_map(&mw1, w1, static_cast<uint64_t>(L.K), static_cast<uint64_t>(L.H),
+                    static_cast<uint32_t>(L.NH / 2)) != 0)
+    return -1;
+  if (make_bf16_map(&mw2, w2, static_cast<uint64_t>(L.H), static_cast<uint64_t>(L.C), 8) != 0)
+    return -1;
+  if (ensure_smem_attr(member_mlp2_pair_sm100, static_cast<int>(kSmemBudget)) != 0) return -4;
+  const long long per_seg = (args.seg_size + args.b - 1) / args.b;
+  const long long tiles = (args.seg_end - args.seg_begin) * per_seg;
+  if (tiles <= 0) return 0;
+  const long long pair_groups = (tiles + 2LL * L.T - 1) / (2LL * L.T);
+  grid = static_cast<int>(std::min<long long>(grid / 2, pair_groups)) * 2;
+  if (grid < 2) grid = 2;
+  member_mlp2_pair_sm100<<<grid, kThreads, L.smem_bytes, stream>>>(mx, mw1, mw2, args);
+  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+
+}  // namespace es

@@ -13,6 +13,7 @@
 
 #include "../cuda/aux_kernels.cuh"
 #include "../cuda/mlp_kernel.cuh"
+#include "../cuda/mlp_pair_kernel.cuh"
 #include "../cuda/mlp_tmem_kernel.cuh"
 #include "enserve/host_convert.hpp"
 #include "enserve/placement.hpp"
@@ -194,10 +195,19 @@ class DeviceMember {
     H_ = a.widths[1];
     // Two sm_100a schedules of the same member; the TMEM-resident
     // one unless it cannot hold this (H, b) or ES_MLP_KERNEL=swapab.
+    // ES_MLP_KERNEL = pair | tmem | swapab pins one; by default the SM-pair or
+    // single-SM TMEM schedule with the lower modelled cycles per sample.
     const char* pick = std::getenv("ES_MLP_KERNEL");
-    const bool want_swapab = pick && std::strcmp(pick, "swapab") == 0;
-    use_tmem_ = !want_swapab && es::mlpt_plan(K_, H_, C_, batch, &tplan_);
-    if (!use_tmem_ && !es::mlp2_plan(K_, H_, C_, batch, &plan_)) return false;
+    const std::string want = pick ? pick : "";
+    const bool pair_ok = (want.empty() || want == "pair") && es::mlpp_plan(K_, H_, C_, batch, &pplan_);
+    const bool tmem_ok = (want.empty() || want == "tmem") && es::mlpt_plan(K_, H_, C_, batch, &tplan_);
+    kind_ = Kind::SwapAB;
+    if (pair_ok && (!tmem_ok || pplan_.est_cycles_per_sample <= tplan_.est_cycles_per_sample))
+      kind_ = Kind::Pair;
+    else if (tmem_ok)
+      kind_ = Kind::Tmem;
+    else if (!es::mlp2_plan(K_, H_, C_, batch, &plan_))
+      return false;
     OnDevice on(device);
     const std::size_t w1 = static_cast<std::size_t>(H_) * K_ * 2, b1 = H_ * 4u,
                       w2 = static_cast<std::size_t>(C_) * H_ * 2, b2 = C_ * 4u;
@@ -252,7 +262,21 @@ class DeviceMember {
           reinterpret_cast<const float*>(base + off_b2_), C_, r0, r1, out, stream));
       return 1;
     }
-    if (use_tmem_) {
+    if (kind_ == Kind::Pair) {
+      es::MlpPArgs pargs;
+      pargs.L = pplan_;
+      pargs.b = batch_;
+      pargs.seg_size = seg_size;
+      pargs.seg_begin = s0;
+      pargs.seg_end = s1;
+      pargs.nb = nb;
+      pargs.bias1 = reinterpret_cast<const float*>(base + off_b1_);
+      pargs.bias2 = reinterpret_cast<const float*>(base + off_b2_);
+      pargs.out = out;
+      ES_LAUNCH(es::mlpp_launch(pargs, x, base, base + off_w2_, grid, stream));
+      return 1;
+    }
+    if (kind_ == Kind::Tmem) {
       es::MlpTArgs targs;
       targs.L = tplan_;
       targs.b = batch_;
@@ -291,7 +315,8 @@ class DeviceMember {
   int K_ = 0, H_ = 0, C_ = 1;
   es::Mlp2Layout plan_{};
   es::MlpTLayout tplan_{};
-  bool use_tmem_ = false;
+  es::MlpPLayout pplan_{};
+  enum class Kind { SwapAB, Tmem, Pair } kind_ = Kind::SwapAB;
   void* weights_ = nullptr;
   std::size_t bytes_ = 0, off_b1_ = 0, off_w2_ = 0, off_b2_ = 0;
 };

@@ -149,7 +149,7 @@ def mlp_cluster(hidden, batches, seeds=None, devices=1, nb_classes=10):
                           [8, 16, 32, 64, 128], 128)
 
 
-@pytest.fixture(params=["tmem", "swapab"])
+@pytest.fixture(params=["pair", "tmem", "swapab"])
 def mlp_kernel(request):
     """Both sm_100a schedules of K1."""
     old = os.environ.get("ES_MLP_KERNEL")
