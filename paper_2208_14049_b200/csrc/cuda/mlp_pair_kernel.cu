@@ -5,6 +5,7 @@
 #include <algorithm>
 
 #include "mlp_pair_kernel.cuh"
+#include "epilogue.cuh"
 #include "tma_host.hpp"
 
 namespace es {
@@ -62,11 +63,6 @@ __device__ __forceinline__ int group_tiles(const MlpPArgs& a, const Tiles& ts, i
   return n;
 }
 
-__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
-  __nv_bfloat162 p = __floats2bfloat162_rn(lo, hi);
-  return *reinterpret_cast<uint32_t*>(&p);
-}
-
 __device__ __forceinline__ void epi_barrier() {
   asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
 }
@@ -89,7 +85,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* a_full = acc_empty + 2;       // [kMaxT]    (leader's; 16 remote arrivals)
   uint64_t* acc2_full = a_full + kMaxT;   // [kMaxT]    (multicast commit)
   uint64_t* w2_full = acc2_full + kMaxT;  //            (leader's)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w2_full + 1);
+  uint64_t* d2_empty = w2_full + 1;       // [kMaxT]    (leader's; 8 remote arrivals)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d2_empty + kMaxT);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -105,11 +102,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&acc_full[i], 1);
-      mbar_init(&acc_empty[i], 8);
+      mbar_init(&acc_empty[i], L.d2_sep ? 16 : 8);
     }
     for (int k = 0; k < kMaxT; ++k) {
       mbar_init(&a_full[k], 16);
       mbar_init(&acc2_full[k], 1);
+      mbar_init(&d2_empty[k], 8);
     }
     mbar_init(w2_full, 1);
     fence_barrier_init();
@@ -172,6 +170,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       uint32_t a_par = 0;
+      uint32_t d2_par = ~0u;
       bool w2_ready = false;
       int pend_buf = -1, pend_n = 0, pend_next = 0;
       auto layer2 = [&](int buf, int k, bool waited) {
@@ -183,7 +182,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         a_par ^= 1u << k;
         tc_fence_after();
         const uint32_t tile = tmem_base + static_cast<uint32_t>(buf * L.group_cols + k * H);
-        const uint32_t d2 = tile + static_cast<uint32_t>(H / 4);
+        uint32_t d2 = tile + static_cast<uint32_t>(H / 4);
+        if (L.d2_sep) {
+          mbar_wait_cluster(&d2_empty[k], (d2_par >> k) & 1u);
+          d2_par ^= 1u << k;
+          d2 = tmem_base + static_cast<uint32_t>(L.d2_col + 16 * k);
+        }
         for (int hh = 0; hh < 2; ++hh)
           for (int kk = 0; kk < H / 32; ++kk) {
             const int h0 = hh * (H / 2) + kk * 16;
@@ -267,34 +271,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int k = 0; k < n; ++k) {
         const uint32_t col0 = static_cast<uint32_t>(buf * L.group_cols + k * H + half * hw);
         const float* bias = sBias + half * hw;
-        for (int i = 0; i < hw / 32; ++i) {
-          uint32_t r[32];
-          tmem_ld32_raw(tmem_base + lane_field + col0 + 32 * i, r);
-          tmem_ld_wait();
-          uint32_t p[16];
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const float lo = fmaxf(__uint_as_float(r[2 * j]) + bias[32 * i + 2 * j], 0.0f);
-            const float hi =
-                fmaxf(__uint_as_float(r[2 * j + 1]) + bias[32 * i + 2 * j + 1], 0.0f);
-            p[j] = pack_bf16x2(lo, hi);
-          }
-          tmem_st16(tmem_base + lane_field + col0 + 16 * i, p);
-        }
-        tmem_st_wait();
+        hidden_to_bf16(tmem_base + lane_field + col0, bias, hw);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&a_full[k]), 0));
       }
+      if (L.d2_sep && lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&acc_empty[buf]), 0));
       if (half == 0) {
         for (int k = 0; k < n; ++k) {
           mbar_wait(&acc2_full[k], (acc2_par >> k) & 1u);
           acc2_par ^= 1u << k;
           tc_fence_after();
           float z[16];
-          tmem_ld16(tmem_base + lane_field +
-                        static_cast<uint32_t>(buf * L.group_cols + k * H + H / 4),
-                    z);
+          const uint32_t d2col = L.d2_sep ? static_cast<uint32_t>(L.d2_col + 16 * k)
+                                          : static_cast<uint32_t>(buf * L.group_cols + k * H + H / 4);
+          tmem_ld16(tmem_base + lane_field + d2col, z);
           const int r = q * 32 + lane;
           if (r < rows[k]) {
             float* o = args.out + (row0[k] + r) * L.C;
@@ -302,10 +293,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             for (int c = 0; c < 16; ++c)
               if (c < L.C) o[c] = z[c] + b2[c];
           }
+          if (L.d2_sep) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&d2_empty[k]), 0));
+          }
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&acc_empty[buf]), 0));
+        if (!L.d2_sep) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&acc_empty[buf]), 0));
+        }
       }
     }
   }
@@ -348,8 +346,10 @@ bool mlpp_plan(int K, int H, int C, int b, MlpPLayout* out) {
       L.nh = nh;
       L.NH = NH;
       L.group_cols = T * H;
+      L.d2_sep = cols + 16 * T <= 512 ? 1 : 0;
+      L.d2_col = cols;
       int tc = 32;
-      while (tc < cols) tc <<= 1;
+      while (tc < cols + (L.d2_sep ? 16 * T : 0)) tc <<= 1;
       L.tmem_cols = tc;
       L.stage_bytes = static_cast<uint32_t>(T) * 16384u + static_cast<uint32_t>(H) * 64u;
       const uint32_t tail = static_cast<uint32_t>(H / 64) * 1024u + static_cast<uint32_t>(H) * 4u +
@@ -369,7 +369,8 @@ bool mlpp_plan(int K, int H, int C, int b, MlpPLayout* out) {
       const double ingress = static_cast<double>(kchunks) * L.stage_bytes / 44.0;
       const double hbm = static_cast<double>(T) * b * K * 2.0 / 25.0;
       const double epi = T * (H / 64.0) * 110.0 + 600.0;
-      const double per_group = std::max({mma, ingress, hbm}) + (nbuf == 1 ? epi : 0.0);
+      const double per_group =
+          std::max({mma, ingress, hbm}) + (nbuf == 1 ? (L.d2_sep ? 0.6 * epi : epi) : 0.0);
       L.est_cycles_per_sample = static_cast<float>(per_group / (static_cast<double>(T) * b));
       if (!found || L.est_cycles_per_sample < best.est_cycles_per_sample) {
         best = L;

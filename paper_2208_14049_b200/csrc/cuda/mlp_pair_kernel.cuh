@@ -29,6 +29,8 @@ struct MlpPLayout {
   int NH = 0;         // their N (each SM holds NH/2 rows of the W1 chunk)
   int stages = 0;
   int group_cols = 0;
+  int d2_sep = 0;     // layer-2 accumulators at d2_col + 16 k, outside the hidden
+  int d2_col = 0;     // columns (see mlp_tmem_kernel.cuh)
   int tmem_cols = 0;
   uint32_t stage_bytes = 0;  // T * 16 KB + H * 64 (half of the W1 chunk)
   uint32_t off_w2 = 0, off_bias = 0, off_bar = 0, smem_bytes = 0;

@@ -6,6 +6,7 @@
 #include <algorithm>
 
 #include "mlp_tmem_kernel.cuh"
+#include "epilogue.cuh"
 #include "tma_host.hpp"
 
 namespace es {
@@ -52,11 +53,6 @@ __device__ __forceinline__ int group_tiles(const MlpTArgs& a, const Tiles& ts, i
   return n;
 }
 
-__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
-  __nv_bfloat162 p = __floats2bfloat162_rn(lo, hi);  // .x (low 16 bits) = lo
-  return *reinterpret_cast<uint32_t*>(&p);
-}
-
 __device__ __forceinline__ void epi_barrier() {
   asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
 }
@@ -79,7 +75,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* a_full = acc_empty + 2;       // [kMaxT] bf16 hidden of tile k in TMEM
   uint64_t* acc2_full = a_full + kMaxT;   // [kMaxT] layer-2 accumulators ready
   uint64_t* w2_full = acc2_full + kMaxT;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w2_full + 1);
+  uint64_t* d2_empty = w2_full + 1;       // [kMaxT] separate D2 drained (d2_sep)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d2_empty + kMaxT);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -93,11 +90,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&acc_full[i], 1);
-      mbar_init(&acc_empty[i], 4);
+      mbar_init(&acc_empty[i], L.d2_sep ? 8 : 4);
     }
     for (int k = 0; k < kMaxT; ++k) {
       mbar_init(&a_full[k], 8);
       mbar_init(&acc2_full[k], 1);
+      mbar_init(&d2_empty[k], 4);
     }
     mbar_init(w2_full, 1);
     fence_barrier_init();
@@ -154,7 +152,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t sW2_addr = smem_u32(sW2);
       int stage = 0;
       uint32_t phase = 0;
-      uint32_t a_par = 0;  // bit k: parity of the next a_full[k] completion
+      uint32_t a_par = 0;    // bit k: parity of the next a_full[k] completion
+      uint32_t d2_par = ~0u; // bit k: parity to wait on d2_empty[k] (first use free)
       bool w2_ready = false;
       // Layer-2 work still owed for the previous group.
       int pend_buf = -1, pend_n = 0, pend_next = 0;
@@ -167,7 +166,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         a_par ^= 1u << k;
         tc_fence_after();
         const uint32_t tile = tmem_base + static_cast<uint32_t>(buf * L.group_cols + k * H);
-        const uint32_t d2 = tile + static_cast<uint32_t>(H / 4);
+        uint32_t d2 = tile + static_cast<uint32_t>(H / 4);
+        if (L.d2_sep) {
+          mbar_wait(&d2_empty[k], (d2_par >> k) & 1u);
+          d2_par ^= 1u << k;
+          d2 = tmem_base + static_cast<uint32_t>(L.d2_col + 16 * k);
+        }
         for (int hh = 0; hh < 2; ++hh)
           for (int kk = 0; kk < H / 32; ++kk) {  // 16 hidden units per step, H/2 per half
             const int h0 = hh * (H / 2) + kk * 16;
@@ -253,35 +257,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t col0 =
             static_cast<uint32_t>(buf * L.group_cols + k * H + half * hw);
         const float* bias = sBias + half * hw;
-        for (int i = 0; i < hw / 32; ++i) {
-          uint32_t r[32];
-          tmem_ld32_raw(tmem_base + lane_field + col0 + 32 * i, r);
-          tmem_ld_wait();
-          uint32_t p[16];
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const float lo = fmaxf(__uint_as_float(r[2 * j]) + bias[32 * i + 2 * j], 0.0f);
-            const float hi =
-                fmaxf(__uint_as_float(r[2 * j + 1]) + bias[32 * i + 2 * j + 1], 0.0f);
-            p[j] = pack_bf16x2(lo, hi);
-          }
-          // Columns [col0 + 16i, +16) were read in iteration i/2 (<= i): safe.
-          tmem_st16(tmem_base + lane_field + col0 + 16 * i, p);
-        }
-        tmem_st_wait();
+        hidden_to_bf16(tmem_base + lane_field + col0, bias, hw);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&a_full[k]);
       }
+      // Separate D2: the hidden columns are free for the next group as soon as
+      // every warp has converted them (the UMMA thread orders layer 2 first).
+      if (L.d2_sep && lane == 0) mbar_arrive(&acc_empty[buf]);
       if (half == 0) {
         for (int k = 0; k < n; ++k) {
           mbar_wait(&acc2_full[k], (acc2_par >> k) & 1u);
           acc2_par ^= 1u << k;
           tc_fence_after();
           float z[16];
-          tmem_ld16(tmem_base + lane_field +
-                        static_cast<uint32_t>(buf * L.group_cols + k * H + H / 4),
-                    z);
+          const uint32_t d2col = L.d2_sep ? static_cast<uint32_t>(L.d2_col + 16 * k)
+                                          : static_cast<uint32_t>(buf * L.group_cols + k * H + H / 4);
+          tmem_ld16(tmem_base + lane_field + d2col, z);
           const int r = q * 32 + lane;
           if (r < rows[k]) {
             float* o = args.out + (row0[k] + r) * L.C;
@@ -289,10 +281,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int c = 0; c < 16; ++c)
               if (c < L.C) o[c] = z[c] + b2[c];
           }
+          if (L.d2_sep) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&d2_empty[k]);
+          }
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&acc_empty[buf]);
+        if (!L.d2_sep) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&acc_empty[buf]);
+        }
       }
     }
   }
@@ -333,8 +332,10 @@ bool mlpt_plan(int K, int H, int C, int b, MlpTLayout* out) {
       L.nh = nh;
       L.NH = NH;
       L.group_cols = T * H;
+      L.d2_sep = cols + 16 * T <= 512 ? 1 : 0;
+      L.d2_col = cols;
       int tc = 32;
-      while (tc < cols) tc <<= 1;
+      while (tc < cols + (L.d2_sep ? 16 * T : 0)) tc <<= 1;
       L.tmem_cols = tc;
       L.stage_bytes = static_cast<uint32_t>(T) * 16384u + static_cast<uint32_t>(H) * 128u;
       const uint32_t tail = static_cast<uint32_t>(H / 64) * 2048u + static_cast<uint32_t>(H) * 4u +
@@ -355,7 +356,8 @@ bool mlpt_plan(int K, int H, int C, int b, MlpTLayout* out) {
       const double ingress = static_cast<double>(kchunks) * L.stage_bytes / 44.0;
       const double hbm = static_cast<double>(T) * b * K * 2.0 / 25.0;
       const double epi = T * (H / 64.0) * 110.0 + 400.0;
-      const double per_group = std::max({mma, ingress, hbm}) + (nbuf == 1 ? epi : 0.0);
+      const double per_group =
+          std::max({mma, ingress, hbm}) + (nbuf == 1 ? (L.d2_sep ? 0.6 * epi : epi) : 0.0);
       L.est_cycles_per_sample = static_cast<float>(per_group / (static_cast<double>(T) * b));
       if (!found || L.est_cycles_per_sample < best.est_cycles_per_sample) {
         best = L;
