@@ -202,7 +202,10 @@ class DeviceMember {
     const bool pair_ok = (want.empty() || want == "pair") && es::mlpp_plan(K_, H_, C_, batch, &pplan_);
     const bool tmem_ok = (want.empty() || want == "tmem") && es::mlpt_plan(K_, H_, C_, batch, &tplan_);
     kind_ = Kind::SwapAB;
-    if (pair_ok && (!tmem_ok || pplan_.est_cycles_per_sample <= tplan_.est_cycles_per_sample))
+    // Measured on B200 (profiles/r1_summary.md): SM pairs win from H = 384 up
+    // (half the W1 ingress per SM); below, the single-SM schedule's shorter
+    // barrier round trips win.
+    if (pair_ok && (!tmem_ok || !want.empty() || H_ >= 384))
       kind_ = Kind::Pair;
     else if (tmem_ok)
       kind_ = Kind::Tmem;
