@@ -45,4 +45,16 @@ __device__ __forceinline__ void hidden_to_bf16(uint32_t base, const float* bias,
   sm100::tmem_st_wait();
 }
 
+// Layer-2 accumulators: `parts` independent 16-column partial sums (so the
+// dependent UMMA chain is parts times shorter), reduced here in fixed order.
+__device__ __forceinline__ void read_d2(uint32_t addr, int parts, float (&z)[16]) {
+  sm100::tmem_ld16(addr, z);
+  for (int p = 1; p < parts; ++p) {
+    float t[16];
+    sm100::tmem_ld16(addr + 16u * p, t);
+#pragma unroll
+    for (int c = 0; c < 16; ++c) z[c] += t[c];
+  }
+}
+
 }  // namespace es

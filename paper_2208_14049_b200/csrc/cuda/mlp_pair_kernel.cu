@@ -63,6 +63,17 @@ __device__ __forceinline__ int group_tiles(const MlpPArgs& a, const Tiles& ts, i
   return n;
 }
 
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+#define TRACE(g, i)                                                       \
+  do {                                                                    \
+    if (args.trace && blockIdx.x == 0 && (g) < 32) args.trace[(g) * 16 + (i)] = global_ns(); \
+  } while (0)
+
 __device__ __forceinline__ void epi_barrier() {
   asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
 }
@@ -142,6 +153,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (n == 0) break;
         for (int kc = 0; kc < L.kchunks; ++kc) {
           mbar_wait(&empty[stage], phase ^ 1u);
+          if (kc == 0) TRACE(g, 7);
           uint8_t* st = smem + static_cast<size_t>(stage) * L.stage_bytes;
           if (leader)
             mbar_arrive_expect_tx(&full[stage], 2u * (static_cast<uint32_t>(n) * 16384u +
@@ -172,13 +184,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t a_par = 0;
       uint32_t d2_par = ~0u;
       bool w2_ready = false;
-      int pend_buf = -1, pend_n = 0, pend_next = 0;
+      int pend_buf = -1, pend_n = 0, pend_next = 0, pend_g = 0;
       auto layer2 = [&](int buf, int k, bool waited) {
         if (!w2_ready) {
           mbar_wait(w2_full, 0);
           w2_ready = true;
         }
         if (!waited) mbar_wait_cluster(&a_full[k], (a_par >> k) & 1u);
+        if (k == 0) TRACE(pend_g, 8);
         a_par ^= 1u << k;
         tc_fence_after();
         const uint32_t tile = tmem_base + static_cast<uint32_t>(buf * L.group_cols + k * H);
@@ -186,16 +199,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (L.d2_sep) {
           mbar_wait_cluster(&d2_empty[k], (d2_par >> k) & 1u);
           d2_par ^= 1u << k;
-          d2 = tmem_base + static_cast<uint32_t>(L.d2_col + 16 * k);
+          d2 = tmem_base + static_cast<uint32_t>(L.d2_col + 16 * L.d2_parts * k);
         }
+        // Descriptors advance by (bytes >> 4) in their low field: precomputed
+        // bases keep the single issuing thread at a few ALU ops per UMMA.
+        const uint64_t w2d = sdesc_k128(sW2_addr);
+        const uint32_t pmask = static_cast<uint32_t>(L.d2_parts - 1);  // parts: 1 or 4
+        uint32_t step = 0;
         for (int hh = 0; hh < 2; ++hh)
-          for (int kk = 0; kk < H / 32; ++kk) {
-            const int h0 = hh * (H / 2) + kk * 16;
+          for (int kk = 0; kk < H / 32; ++kk, ++step) {  // 16 hidden units per step
+            const uint32_t h0 = static_cast<uint32_t>(hh * (H / 2) + kk * 16);
             const uint32_t a = tile + static_cast<uint32_t>(hh * (H / 2) + kk * 8);
-            const uint64_t b = sdesc_k128(sW2_addr + (h0 >> 6) * 1024 + (h0 & 63) * 2);
-            umma_bf16_pair_ta(d2, a, b, idesc2, (hh | kk) != 0);
+            const uint64_t b = w2d + (h0 >> 6) * 64u + (h0 & 63u) / 8u;
+            umma_bf16_pair_ta(d2 + 16u * (step & pmask), a, b, idesc2, step > pmask);
           }
         umma_commit_pair(&acc2_full[k], kBoth);
+        if (k == 0) TRACE(pend_g, 9);
       };
       auto drain_pending = [&]() {
         for (; pend_next < pend_n; ++pend_next) layer2(pend_buf, pend_next, false);
@@ -209,7 +228,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int buf = g % L.nbuf;
         const uint32_t use = static_cast<uint32_t>(g / L.nbuf);
         if (pend_buf == buf) drain_pending();
+        TRACE(g, 0);
         mbar_wait_cluster(&acc_empty[buf], (use & 1u) ^ 1u);
+        TRACE(g, 1);
         tc_fence_after();
         const uint32_t d0 = tmem_base + static_cast<uint32_t>(buf * L.group_cols);
         for (int kc = 0; kc < L.kchunks; ++kc) {
@@ -217,12 +238,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           tc_fence_after();
           const uint32_t sx = smem_u32(smem + static_cast<size_t>(stage) * L.stage_bytes);
           const uint32_t sw = sx + static_cast<uint32_t>(L.T) * 16384u;
+          const uint64_t xd = sdesc_k128(sx), wd = sdesc_k128(sw);
           for (int k = 0; k < n; ++k)
             for (int h = 0; h < L.nh; ++h)
 #pragma unroll
               for (int j = 0; j < 4; ++j) {
-                const uint64_t a = sdesc_k128(sx + k * 16384 + j * 32);
-                const uint64_t b = sdesc_k128(sw + h * half_w * 128u + j * 32);
+                const uint64_t a = xd + static_cast<uint64_t>(k * 1024 + j * 2);
+                const uint64_t b = wd + static_cast<uint64_t>(h * half_w * 8u + j * 2);
                 umma_bf16_pair(d0 + static_cast<uint32_t>(k * H + h * L.NH), a, b, idesc1,
                                (kc | j) != 0);
               }
@@ -239,10 +261,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (pend_buf >= 0 && pend_next == pend_n) pend_buf = -1;
         }
         umma_commit_pair(&acc_full[buf], kBoth);
+        TRACE(g, 2);
         if (pend_buf >= 0) drain_pending();
         pend_buf = buf;
         pend_n = n;
         pend_next = 0;
+        pend_g = g;
       }
       if (pend_buf >= 0) drain_pending();
     }
@@ -267,32 +291,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int buf = g % L.nbuf;
       const uint32_t use = static_cast<uint32_t>(g / L.nbuf);
       mbar_wait(&acc_full[buf], use & 1u);
+      if (warp == 2 && lane == 0) TRACE(g, 3);
       tc_fence_after();
       for (int k = 0; k < n; ++k) {
         const uint32_t col0 = static_cast<uint32_t>(buf * L.group_cols + k * H + half * hw);
         const float* bias = sBias + half * hw;
         hidden_to_bf16(tmem_base + lane_field + col0, bias, hw);
+        if (warp == 2 && lane == 0 && k == 0) TRACE(g, 4);
+        if (warp == 9 && lane == 0 && k == 0) TRACE(g, 10);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&a_full[k]), 0));
       }
       if (L.d2_sep && lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&acc_empty[buf]), 0));
       if (half == 0) {
-        for (int k = 0; k < n; ++k) {
+        // Pull every tile's D2 into registers first, release the TMEM, then
+        // finish the logits off the UMMA thread's critical path.
+        float z[kMaxT][16];
+#pragma unroll
+        for (int k = 0; k < kMaxT; ++k) {
+          if (k >= n) continue;
           mbar_wait(&acc2_full[k], (acc2_par >> k) & 1u);
+          if (warp == 2 && lane == 0 && k == 0) TRACE(g, 5);
           acc2_par ^= 1u << k;
           tc_fence_after();
-          float z[16];
-          const uint32_t d2col = L.d2_sep ? static_cast<uint32_t>(L.d2_col + 16 * k)
-                                          : static_cast<uint32_t>(buf * L.group_cols + k * H + H / 4);
-          tmem_ld16(tmem_base + lane_field + d2col, z);
-          const int r = q * 32 + lane;
-          if (r < rows[k]) {
-            float* o = args.out + (row0[k] + r) * L.C;
-#pragma unroll
-            for (int c = 0; c < 16; ++c)
-              if (c < L.C) o[c] = z[c] + b2[c];
-          }
+          const uint32_t d2col =
+              L.d2_sep ? static_cast<uint32_t>(L.d2_col + 16 * L.d2_parts * k)
+                       : static_cast<uint32_t>(buf * L.group_cols + k * H + H / 4);
+          read_d2(tmem_base + lane_field + d2col, L.d2_parts, z[k]);
           if (L.d2_sep) {
             tc_fence_before();
             __syncwarp();
@@ -304,6 +330,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&acc_empty[buf]), 0));
         }
+        const int r = q * 32 + lane;
+#pragma unroll
+        for (int k = 0; k < kMaxT; ++k) {
+          if (k >= n || r >= rows[k]) continue;
+          float* o = args.out + (row0[k] + r) * L.C;
+#pragma unroll
+          for (int c = 0; c < 16; ++c)
+            if (c < L.C) o[c] = z[k][c] + b2[c];
+        }
+        if (warp == 2 && lane == 0) TRACE(g, 6);
       }
     }
   }
@@ -346,10 +382,13 @@ bool mlpp_plan(int K, int H, int C, int b, MlpPLayout* out) {
       L.nh = nh;
       L.NH = NH;
       L.group_cols = T * H;
+      // Layer-2 partial accumulators: 4 when there is room (inside the
+      // drained half-0 columns [H/4, H/2), or after the hidden columns).
       L.d2_sep = cols + 16 * T <= 512 ? 1 : 0;
+      L.d2_parts = L.d2_sep ? (cols + 64 * T <= 512 ? 4 : 1) : (H >= 256 ? 4 : 1);
       L.d2_col = cols;
       int tc = 32;
-      while (tc < cols + (L.d2_sep ? 16 * T : 0)) tc <<= 1;
+      while (tc < cols + (L.d2_sep ? 16 * L.d2_parts * T : 0)) tc <<= 1;
       L.tmem_cols = tc;
       L.stage_bytes = static_cast<uint32_t>(T) * 16384u + static_cast<uint32_t>(H) * 64u;
       const uint32_t tail = static_cast<uint32_t>(H / 64) * 1024u + static_cast<uint32_t>(H) * 4u +

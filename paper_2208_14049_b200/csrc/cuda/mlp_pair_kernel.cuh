@@ -29,8 +29,9 @@ struct MlpPLayout {
   int NH = 0;         // their N (each SM holds NH/2 rows of the W1 chunk)
   int stages = 0;
   int group_cols = 0;
-  int d2_sep = 0;     // layer-2 accumulators at d2_col + 16 k, outside the hidden
-  int d2_col = 0;     // columns (see mlp_tmem_kernel.cuh)
+  int d2_sep = 0;     // layer-2 accumulators outside the hidden columns
+  int d2_col = 0;     //   (see mlp_tmem_kernel.cuh)
+  int d2_parts = 1;   // independent layer-2 partial accumulators (16 columns each)
   int tmem_cols = 0;
   uint32_t stage_bytes = 0;  // T * 16 KB + H * 64 (half of the W1 chunk)
   uint32_t off_w2 = 0, off_bias = 0, off_bar = 0, smem_bytes = 0;
@@ -45,6 +46,9 @@ struct MlpPArgs {
   const float* bias1 = nullptr;
   const float* bias2 = nullptr;
   float* out = nullptr;
+  // Optional timeline of CTA 0 (globaltimer ns): [group][8] for groups < 32,
+  // see the TRACE() points in the kernel.  nullptr = off.
+  unsigned long long* trace = nullptr;
 };
 
 bool mlpp_plan(int K, int H, int C, int b, MlpPLayout* out);

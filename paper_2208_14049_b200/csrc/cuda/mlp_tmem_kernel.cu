@@ -170,14 +170,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (L.d2_sep) {
           mbar_wait(&d2_empty[k], (d2_par >> k) & 1u);
           d2_par ^= 1u << k;
-          d2 = tmem_base + static_cast<uint32_t>(L.d2_col + 16 * k);
+          d2 = tmem_base + static_cast<uint32_t>(L.d2_col + 16 * L.d2_parts * k);
         }
+        // Descriptors advance by (bytes >> 4) in their low field: precomputed
+        // bases keep the single issuing thread at a few ALU ops per UMMA.
+        const uint64_t w2d = sdesc_k128(sW2_addr);
+        const uint32_t pmask = static_cast<uint32_t>(L.d2_parts - 1);  // parts: 1 or 4
+        uint32_t step = 0;
         for (int hh = 0; hh < 2; ++hh)
-          for (int kk = 0; kk < H / 32; ++kk) {  // 16 hidden units per step, H/2 per half
-            const int h0 = hh * (H / 2) + kk * 16;
+          for (int kk = 0; kk < H / 32; ++kk, ++step) {  // 16 hidden units per step
+            const uint32_t h0 = static_cast<uint32_t>(hh * (H / 2) + kk * 16);
             const uint32_t a = tile + static_cast<uint32_t>(hh * (H / 2) + kk * 8);
-            const uint64_t b = sdesc_k128(sW2_addr + (h0 >> 6) * 2048 + (h0 & 63) * 2);
-            umma_bf16_ta(d2, a, b, idesc2, (hh | kk) != 0);
+            const uint64_t b = w2d + (h0 >> 6) * 128u + (h0 & 63u) / 8u;
+            umma_bf16_ta(d2 + 16u * (step & pmask), a, b, idesc2, step > pmask);
           }
         umma_commit(&acc2_full[k]);
       };
@@ -201,12 +206,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_after();
           const uint32_t sx = smem_u32(smem + static_cast<size_t>(stage) * L.stage_bytes);
           const uint32_t sw = sx + static_cast<uint32_t>(L.T) * 16384u;
+          const uint64_t xd = sdesc_k128(sx), wd = sdesc_k128(sw);
           for (int k = 0; k < n; ++k)
             for (int h = 0; h < L.nh; ++h)
 #pragma unroll
               for (int j = 0; j < 4; ++j) {
-                const uint64_t a = sdesc_k128(sx + k * 16384 + j * 32);
-                const uint64_t b = sdesc_k128(sw + h * L.NH * 128 + j * 32);
+                const uint64_t a = xd + static_cast<uint64_t>(k * 1024 + j * 2);
+                const uint64_t b = wd + static_cast<uint64_t>(h * L.NH * 8 + j * 2);
                 umma_bf16(d0 + static_cast<uint32_t>(k * H + h * L.NH), a, b, idesc1,
                           (kc | j) != 0);
               }
@@ -266,21 +272,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       // every warp has converted them (the UMMA thread orders layer 2 first).
       if (L.d2_sep && lane == 0) mbar_arrive(&acc_empty[buf]);
       if (half == 0) {
-        for (int k = 0; k < n; ++k) {
+        // Pull every tile's D2 into registers first, release the TMEM, then
+        // finish the logits off the UMMA thread's critical path.
+        float z[kMaxT][16];
+#pragma unroll
+        for (int k = 0; k < kMaxT; ++k) {
+          if (k >= n) continue;
           mbar_wait(&acc2_full[k], (acc2_par >> k) & 1u);
           acc2_par ^= 1u << k;
           tc_fence_after();
-          float z[16];
-          const uint32_t d2col = L.d2_sep ? static_cast<uint32_t>(L.d2_col + 16 * k)
-                                          : static_cast<uint32_t>(buf * L.group_cols + k * H + H / 4);
-          tmem_ld16(tmem_base + lane_field + d2col, z);
-          const int r = q * 32 + lane;
-          if (r < rows[k]) {
-            float* o = args.out + (row0[k] + r) * L.C;
-#pragma unroll
-            for (int c = 0; c < 16; ++c)
-              if (c < L.C) o[c] = z[c] + b2[c];
-          }
+          const uint32_t d2col =
+              L.d2_sep ? static_cast<uint32_t>(L.d2_col + 16 * L.d2_parts * k)
+                       : static_cast<uint32_t>(buf * L.group_cols + k * H + H / 4);
+          read_d2(tmem_base + lane_field + d2col, L.d2_parts, z[k]);
           if (L.d2_sep) {
             tc_fence_before();
             __syncwarp();
@@ -291,6 +295,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&acc_empty[buf]);
+        }
+        const int r = q * 32 + lane;
+#pragma unroll
+        for (int k = 0; k < kMaxT; ++k) {
+          if (k >= n || r >= rows[k]) continue;
+          float* o = args.out + (row0[k] + r) * L.C;
+#pragma unroll
+          for (int c = 0; c < 16; ++c)
+            if (c < L.C) o[c] = z[k][c] + b2[c];
         }
       }
     }
@@ -332,10 +345,13 @@ bool mlpt_plan(int K, int H, int C, int b, MlpTLayout* out) {
       L.nh = nh;
       L.NH = NH;
       L.group_cols = T * H;
+      // Layer-2 partial accumulators: 4 when there is room (inside the
+      // drained half-0 columns [H/4, H/2), or after the hidden columns).
       L.d2_sep = cols + 16 * T <= 512 ? 1 : 0;
+      L.d2_parts = L.d2_sep ? (cols + 64 * T <= 512 ? 4 : 1) : (H >= 256 ? 4 : 1);
       L.d2_col = cols;
       int tc = 32;
-      while (tc < cols + (L.d2_sep ? 16 * T : 0)) tc <<= 1;
+      while (tc < cols + (L.d2_sep ? 16 * L.d2_parts * T : 0)) tc <<= 1;
       L.tmem_cols = tc;
       L.stage_bytes = static_cast<uint32_t>(T) * 16384u + static_cast<uint32_t>(H) * 128u;
       const uint32_t tail = static_cast<uint32_t>(H / 64) * 2048u + static_cast<uint32_t>(H) * 4u +

@@ -38,8 +38,9 @@ struct MlpTLayout {
   int stages = 0;
   int group_cols = 0; // T * H
   int d2_sep = 0;     // layer-2 accumulators outside the hidden columns
-  int d2_col = 0;     //   (then at d2_col + 16 k, so the next group's layer 1
-                      //    is not gated by the logits epilogue)
+  int d2_col = 0;     //   (then at d2_col + 16 * d2_parts * k, so the next
+                      //    group's layer 1 is not gated by the logits epilogue)
+  int d2_parts = 1;   // independent layer-2 partial accumulators (16 columns each)
   int tmem_cols = 0;
   uint32_t stage_bytes = 0;  // T * 16 KB (X tiles) + H * 128 (W1 chunk)
   uint32_t off_w2 = 0, off_bias = 0, off_bar = 0, smem_bytes = 0;
