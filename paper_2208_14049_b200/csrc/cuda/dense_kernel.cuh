@@ -1,0 +1,39 @@
+// Dense layer on sm_100a tensor cores: Y = act(X . W^T + b), bf16 in, bf16 out.
+//
+// Building block for members deeper than the fused two-layer kernel: an MLP
+// 784-512-512-10 runs as dense(784->512, ReLU) followed by the fused
+// member_mlp2 kernel on the 512-wide activations; the CNN member's convolution
+// stack feeds the same fused head.  Activations between launches live in HBM
+// as bf16 [rows][N] (row stride N).
+//   UMMA M = 128 rows, N <= 256 per instruction (up to 512 per tile), K in
+//   64-wide TMA chunks; T tiles share each W chunk; fp32 accumulators in TMEM;
+//   epilogue: tcgen05.ld -> +b, ReLU, bf16 -> 128B-swizzled smem staging ->
+//   TMA bulk tensor store (one 64-column box per chunk, double buffered).
+#pragma once
+
+#include <cstdint>
+
+#include "sm100.cuh"
+
+namespace es {
+
+struct DenseLayout {
+  int K = 0, N = 0, kchunks = 0;
+  int T = 1, nbuf = 1, nh = 1, NH = 0;
+  int relu = 1;
+  int stages = 0, group_cols = 0, tmem_cols = 0;
+  uint32_t stage_bytes = 0, off_stage_out = 0, off_bias = 0, off_bar = 0, smem_bytes = 0;
+};
+
+struct DenseArgs {
+  DenseLayout L;
+  long long row_begin = 0, row_end = 0;  // rows of X / Y handled by this launch
+  const float* bias = nullptr;
+};
+
+bool dense_plan(int K, int N, bool relu, DenseLayout* out);
+// x: bf16 [rows >= row_end][K]; w: bf16 [N][K]; y: bf16 [rows][N].
+int dense_launch(const DenseArgs& args, const void* x, long long x_rows, const void* w, void* y,
+                 int grid, cudaStream_t stream);
+
+}  // namespace es

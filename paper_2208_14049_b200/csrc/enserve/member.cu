@@ -1,0 +1,245 @@
+// DeviceMember: plans, weights and launches of one member on one GPU.
+#include "enserve/member.hpp"
+
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+
+#include "../cuda/aux_kernels.cuh"
+#include "../cuda/dense_kernel.cuh"
+#include "../cuda/mlp_kernel.cuh"
+#include "../cuda/mlp_pair_kernel.cuh"
+#include "../cuda/mlp_tmem_kernel.cuh"
+
+namespace enserve {
+
+namespace {
+
+[[noreturn]] void fail_cuda(cudaError_t e, const char* what) {
+  cudaGetLastError();
+  throw DeviceError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define M_CUDA(call)                                        \
+  do {                                                      \
+    cudaError_t m_err_ = (call);                            \
+    if (m_err_ != cudaSuccess) fail_cuda(m_err_, #call);    \
+  } while (0)
+
+#define M_LAUNCH(call)                                                       \
+  do {                                                                       \
+    if ((call) != 0) fail_cuda(cudaGetLastError(), "kernel launch " #call); \
+  } while (0)
+
+struct OnDev {
+  int prev = 0;
+  explicit OnDev(int d) {
+    cudaGetDevice(&prev);
+    M_CUDA(cudaSetDevice(d));
+  }
+  ~OnDev() { cudaSetDevice(prev); }
+};
+
+bool env_is(const char* name, const char* value) {
+  const char* v = std::getenv(name);
+  return v && std::strcmp(v, value) == 0;
+}
+
+}  // namespace
+
+struct DeviceMember::Impl {
+  ModelSpec model;
+  int batch = 1;
+  int C = 1;
+  std::vector<int> widths;
+  enum class Head { Synthetic, SwapAB, Tmem, Pair } head = Head::Synthetic;
+  es::Mlp2Layout plan_swapab{};
+  es::MlpTLayout plan_tmem{};
+  es::MlpPLayout plan_pair{};
+  std::vector<es::DenseLayout> dense;  // plans of the leading layers
+  void* weights = nullptr;
+  std::vector<std::size_t> w_off, b_off;  // per layer
+  // Activations of the leading layers, bf16 [rows][width], indexed like X.
+  std::vector<void*> act;
+  std::vector<std::size_t> act_rows;
+};
+
+DeviceMember::~DeviceMember() {
+  if (!impl_) return;
+  cudaSetDevice(device_);
+  if (impl_->weights) cudaFree(impl_->weights);
+  for (void* p : impl_->act) cudaFree(p);
+  delete impl_;
+}
+
+std::string DeviceMember::schedule() const {
+  if (!impl_) return "unloaded";
+  switch (impl_->head) {
+    case Impl::Head::Pair: return "pair";
+    case Impl::Head::Tmem: return "tmem";
+    case Impl::Head::SwapAB: return "swapab";
+    default: return "synthetic";
+  }
+}
+
+bool DeviceMember::load(int device, const ModelSpec& model, int batch) {
+  device_ = device;
+  impl_ = new Impl();
+  Impl& I = *impl_;
+  I.model = model;
+  I.batch = batch;
+  I.C = model.output_width;
+  if (model.arch.kind == MemberArch::Kind::Synthetic) return true;
+  const MemberArch& a = model.arch;
+  const int L = a.layers();
+  if (L < 2) throw SpecError(model.name + ": an MLP member needs at least two layers");
+  I.widths = a.widths;
+  // Leading layers: tcgen05 dense layers with a bf16 output.
+  for (int l = 0; l < L - 2; ++l) {
+    es::DenseLayout d;
+    if (!es::dense_plan(a.widths[l], a.widths[l + 1], true, &d))
+      throw SpecError(model.name + ": hidden width " + std::to_string(a.widths[l + 1]) +
+                      " of a leading layer must be a multiple of 128 up to 512");
+    I.dense.push_back(d);
+  }
+  // Fused head over the last two layers.
+  const int K = a.widths[L - 2], H = a.widths[L - 1], C = a.widths[L];
+  const char* pick = std::getenv("ES_MLP_KERNEL");
+  const std::string want = pick ? pick : "";
+  const bool pair_ok = (want.empty() || want == "pair") && es::mlpp_plan(K, H, C, batch, &I.plan_pair);
+  const bool tmem_ok = (want.empty() || want == "tmem") && es::mlpt_plan(K, H, C, batch, &I.plan_tmem);
+  // Measured on B200 (profiles/): SM pairs win from H = 384 up (half the W1
+  // ingress per SM); below, the single-SM schedule's shorter barrier round
+  // trips win.
+  if (pair_ok && (!tmem_ok || !want.empty() || H >= 384))
+    I.head = Impl::Head::Pair;
+  else if (tmem_ok)
+    I.head = Impl::Head::Tmem;
+  else if (es::mlp2_plan(K, H, C, batch, &I.plan_swapab))
+    I.head = Impl::Head::SwapAB;
+  else
+    return false;  // the tile does not fit one SM: out of memory
+
+  OnDev on(device);
+  auto up = [](std::size_t x) { return (x + 255) / 256 * 256; };
+  std::size_t off = 0;
+  for (int l = 0; l < L; ++l) {
+    I.w_off.push_back(off);
+    off += up(static_cast<std::size_t>(a.widths[l]) * a.widths[l + 1] * 2);
+    I.b_off.push_back(off);
+    off += up(static_cast<std::size_t>(a.widths[l + 1]) * 4);
+  }
+  bytes_ = off;
+  cudaError_t e = cudaMalloc(&I.weights, bytes_);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    I.weights = nullptr;
+    return false;
+  }
+  M_CUDA(e);
+  uint8_t* base = static_cast<uint8_t*>(I.weights);
+  for (int l = 0; l < L; ++l) {
+    const int fi = a.widths[l], fo = a.widths[l + 1];
+    const float limit = static_cast<float>(std::sqrt(6.0 / static_cast<double>(fi + fo)));
+    M_LAUNCH(es::generate_dense_layer(a.weight_seed, l, fi, fo, limit,
+                                      reinterpret_cast<__nv_bfloat16*>(base + I.w_off[l]),
+                                      reinterpret_cast<float*>(base + I.b_off[l]), 0));
+  }
+  I.act.assign(L - 2, nullptr);
+  I.act_rows.assign(L - 2, 0);
+  M_CUDA(cudaDeviceSynchronize());
+  return true;
+}
+
+int DeviceMember::forward(const void* x, long long nb, int seg_size, long long s0, long long s1,
+                          float* out, int grid, cudaStream_t stream) {
+  Impl& I = *impl_;
+  if (s1 <= s0 || nb == 0) return 0;
+  if (I.head == Impl::Head::Synthetic) {
+    M_LAUNCH(es::synthetic_member_launch(I.model.id, I.C, seg_size, s0, s1, nb, out, stream));
+    return 1;
+  }
+  const uint8_t* base = static_cast<const uint8_t*>(I.weights);
+  const int L = static_cast<int>(I.widths.size()) - 1;
+  const long long r0 = s0 * seg_size, r1 = std::min<long long>(s1 * seg_size, nb);
+  int launches = 0;
+  const void* cur = x;
+  for (int l = 0; l < L - 2; ++l) {
+    if (I.act_rows[l] < static_cast<std::size_t>(nb)) {
+      cudaFree(I.act[l]);
+      I.act[l] = nullptr;
+      M_CUDA(cudaMalloc(&I.act[l], static_cast<std::size_t>(nb) * I.widths[l + 1] * 2));
+      I.act_rows[l] = static_cast<std::size_t>(nb);
+    }
+    es::DenseArgs d;
+    d.L = I.dense[l];
+    d.row_begin = r0;
+    d.row_end = r1;
+    d.bias = reinterpret_cast<const float*>(base + I.b_off[l]);
+    M_LAUNCH(es::dense_launch(d, cur, nb, base + I.w_off[l], I.act[l], grid, stream));
+    ++launches;
+    cur = I.act[l];
+  }
+  const int h = L - 2;  // head layers h, h+1
+  const float* b1 = reinterpret_cast<const float*>(base + I.b_off[h]);
+  const float* b2 = reinterpret_cast<const float*>(base + I.b_off[h + 1]);
+  const void* w1 = base + I.w_off[h];
+  const void* w2 = base + I.w_off[h + 1];
+  if (env_is("ES_MEMBER_KERNEL", "simt")) {
+    M_LAUNCH(es::mlp2_simt_launch(static_cast<const __nv_bfloat16*>(cur), nb, I.widths[h],
+                                  static_cast<const __nv_bfloat16*>(w1), b1, I.widths[h + 1],
+                                  static_cast<const __nv_bfloat16*>(w2), b2, I.C, r0, r1, out,
+                                  stream));
+    return launches + 1;
+  }
+  switch (I.head) {
+    case Impl::Head::Pair: {
+      es::MlpPArgs p;
+      p.L = I.plan_pair;
+      p.b = I.batch;
+      p.seg_size = seg_size;
+      p.seg_begin = s0;
+      p.seg_end = s1;
+      p.nb = nb;
+      p.bias1 = b1;
+      p.bias2 = b2;
+      p.out = out;
+      M_LAUNCH(es::mlpp_launch(p, cur, w1, w2, grid, stream));
+      break;
+    }
+    case Impl::Head::Tmem: {
+      es::MlpTArgs t;
+      t.L = I.plan_tmem;
+      t.b = I.batch;
+      t.seg_size = seg_size;
+      t.seg_begin = s0;
+      t.seg_end = s1;
+      t.nb = nb;
+      t.bias1 = b1;
+      t.bias2 = b2;
+      t.out = out;
+      M_LAUNCH(es::mlpt_launch(t, cur, w1, w2, grid, stream));
+      break;
+    }
+    default: {
+      es::Mlp2Args s;
+      s.L = I.plan_swapab;
+      s.b = I.batch;
+      s.seg_size = seg_size;
+      s.seg_begin = s0;
+      s.seg_end = s1;
+      s.nb = nb;
+      s.bias1 = b1;
+      s.bias2 = b2;
+      s.out = out;
+      M_LAUNCH(es::mlp2_launch(s, cur, w1, w2, grid, stream));
+      break;
+    }
+  }
+  return launches + 1;
+}
+
+}  // namespace enserve

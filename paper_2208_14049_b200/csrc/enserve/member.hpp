@@ -1,0 +1,51 @@
+// One ensemble member resident on one GPU: the device side of the reference's
+// Predictor (/root/reference/proj/include/enserve/runtime/backend.hpp:25-34).
+//
+//   * Synthetic: synthetic_prediction(model, sample, class), the reference's
+//     deterministic stand-in (src/runtime/backend.cpp:21-29).
+//   * MLP widths[0] -> ... -> widths[L]: the first L-2 layers run as tcgen05
+//     dense layers (bias + ReLU fused, bf16 activations in HBM), the last two
+//     as one fused member kernel (hidden layer never leaves the SM): the
+//     SM-pair schedule for hidden >= 384, the single-SM TMEM schedule below,
+//     the swap-AB schedule when neither fits.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <string>
+#include <vector>
+
+#include "enserve/spec.hpp"
+
+namespace enserve {
+
+class DeviceMember {
+ public:
+  DeviceMember() = default;
+  ~DeviceMember();
+  DeviceMember(const DeviceMember&) = delete;
+  DeviceMember& operator=(const DeviceMember&) = delete;
+
+  // Predictor::load(): false = out of memory (a tile plan does not fit an SM,
+  // or a device allocation failed); other failures throw.
+  bool load(int device, const ModelSpec& model, int batch);
+
+  // Logits of every row of segments [s0, s1) of x (bf16 [nb][width], rows
+  // indexed globally) into out ([nb][C] fp32).  Returns kernel launches.
+  int forward(const void* x, long long nb, int seg_size, long long s0, long long s1, float* out,
+              int grid, cudaStream_t stream);
+
+  int device() const { return device_; }
+  std::size_t weight_bytes() const { return bytes_; }
+  // Name of the fused head schedule ("pair", "tmem", "swapab", "synthetic").
+  std::string schedule() const;
+
+ private:
+  struct Impl;
+  Impl* impl_ = nullptr;
+  int device_ = 0;
+  std::size_t bytes_ = 0;
+};
+
+}  // namespace enserve

@@ -13,8 +13,7 @@
 
 #include "../cuda/aux_kernels.cuh"
 #include "../cuda/mlp_kernel.cuh"
-#include "../cuda/mlp_pair_kernel.cuh"
-#include "../cuda/mlp_tmem_kernel.cuh"
+#include "enserve/member.hpp"
 #include "enserve/host_convert.hpp"
 #include "enserve/placement.hpp"
 
@@ -78,11 +77,6 @@ es::CombineArgs combine_args(const CombinationRule& rule, const std::vector<floa
                        : inv;
   }
   return ca;
-}
-
-bool member_kernel_simt() {
-  const char* v = std::getenv("ES_MEMBER_KERNEL");
-  return v && std::strcmp(v, "simt") == 0;
 }
 
 }  // namespace
@@ -176,153 +170,6 @@ const void* SampleStore::device_replica(int device) const {
   replicas_[device] = bf;
   return bf;
 }
-
-// ---------------------------------------------------------------- member
-class DeviceMember {
- public:
-  // load(): false = out of memory (tile plan does not fit an SM, or a device
-  // allocation failed); other CUDA errors throw.
-  bool load(int device, const ModelSpec& model, int batch) {
-    device_ = device;
-    model_ = model;
-    batch_ = batch;
-    C_ = model.output_width;
-    if (model.arch.kind == MemberArch::Kind::Synthetic) return true;
-    const MemberArch& a = model.arch;
-    if (a.layers() != 2)
-      throw SpecError(model.name + ": the sm_100a member kernel runs 2-layer MLPs (one hidden layer)");
-    K_ = a.widths[0];
-    H_ = a.widths[1];
-    // Two sm_100a schedules of the same member; the TMEM-resident
-    // one unless it cannot hold this (H, b) or ES_MLP_KERNEL=swapab.
-    // ES_MLP_KERNEL = pair | tmem | swapab pins one; by default the SM-pair or
-    // single-SM TMEM schedule with the lower modelled cycles per sample.
-    const char* pick = std::getenv("ES_MLP_KERNEL");
-    const std::string want = pick ? pick : "";
-    const bool pair_ok = (want.empty() || want == "pair") && es::mlpp_plan(K_, H_, C_, batch, &pplan_);
-    const bool tmem_ok = (want.empty() || want == "tmem") && es::mlpt_plan(K_, H_, C_, batch, &tplan_);
-    kind_ = Kind::SwapAB;
-    // Measured on B200 (profiles/r1_summary.md): SM pairs win from H = 384 up
-    // (half the W1 ingress per SM); below, the single-SM schedule's shorter
-    // barrier round trips win.
-    if (pair_ok && (!tmem_ok || !want.empty() || H_ >= 384))
-      kind_ = Kind::Pair;
-    else if (tmem_ok)
-      kind_ = Kind::Tmem;
-    else if (!es::mlp2_plan(K_, H_, C_, batch, &plan_))
-      return false;
-    OnDevice on(device);
-    const std::size_t w1 = static_cast<std::size_t>(H_) * K_ * 2, b1 = H_ * 4u,
-                      w2 = static_cast<std::size_t>(C_) * H_ * 2, b2 = C_ * 4u;
-    auto up = [](std::size_t x) { return (x + 255) / 256 * 256; };
-    off_b1_ = up(w1);
-    off_w2_ = off_b1_ + up(b1);
-    off_b2_ = off_w2_ + up(w2);
-    bytes_ = off_b2_ + up(b2);
-    cudaError_t e = cudaMalloc(&weights_, bytes_);
-    if (e == cudaErrorMemoryAllocation) {
-      cudaGetLastError();
-      weights_ = nullptr;
-      return false;
-    }
-    ES_CUDA(e);
-    uint8_t* base = static_cast<uint8_t*>(weights_);
-    for (int l = 0; l < 2; ++l) {
-      const int fi = a.widths[l], fo = a.widths[l + 1];
-      const float limit = static_cast<float>(std::sqrt(6.0 / static_cast<double>(fi + fo)));
-      ES_LAUNCH(es::generate_dense_layer(
-          a.weight_seed, l, fi, fo, limit,
-          reinterpret_cast<__nv_bfloat16*>(base + (l == 0 ? 0 : off_w2_)),
-          reinterpret_cast<float*>(base + (l == 0 ? off_b1_ : off_b2_)), 0));
-    }
-    ES_CUDA(cudaDeviceSynchronize());
-    return true;
-  }
-
-  ~DeviceMember() {
-    if (weights_) {
-      cudaSetDevice(device_);
-      cudaFree(weights_);
-    }
-  }
-
-  // Logits for every row of segments [s0, s1) into out (rows indexed globally).
-  // Returns the number of kernel launches issued.
-  int forward(const void* x, long long nb, int seg_size, long long s0, long long s1, float* out,
-              int grid, cudaStream_t stream) const {
-    if (s1 <= s0 || nb == 0) return 0;
-    if (model_.arch.kind == MemberArch::Kind::Synthetic) {
-      ES_LAUNCH(es::synthetic_member_launch(model_.id, C_, seg_size, s0, s1, nb, out, stream));
-      return 1;
-    }
-    const uint8_t* base = static_cast<const uint8_t*>(weights_);
-    if (member_kernel_simt()) {
-      const long long r0 = s0 * seg_size, r1 = std::min<long long>(s1 * seg_size, nb);
-      ES_LAUNCH(es::mlp2_simt_launch(
-          static_cast<const __nv_bfloat16*>(x), nb, K_,
-          reinterpret_cast<const __nv_bfloat16*>(base), reinterpret_cast<const float*>(base + off_b1_),
-          H_, reinterpret_cast<const __nv_bfloat16*>(base + off_w2_),
-          reinterpret_cast<const float*>(base + off_b2_), C_, r0, r1, out, stream));
-      return 1;
-    }
-    if (kind_ == Kind::Pair) {
-      es::MlpPArgs pargs;
-      pargs.L = pplan_;
-      pargs.b = batch_;
-      pargs.seg_size = seg_size;
-      pargs.seg_begin = s0;
-      pargs.seg_end = s1;
-      pargs.nb = nb;
-      pargs.bias1 = reinterpret_cast<const float*>(base + off_b1_);
-      pargs.bias2 = reinterpret_cast<const float*>(base + off_b2_);
-      pargs.out = out;
-      ES_LAUNCH(es::mlpp_launch(pargs, x, base, base + off_w2_, grid, stream));
-      return 1;
-    }
-    if (kind_ == Kind::Tmem) {
-      es::MlpTArgs targs;
-      targs.L = tplan_;
-      targs.b = batch_;
-      targs.seg_size = seg_size;
-      targs.seg_begin = s0;
-      targs.seg_end = s1;
-      targs.nb = nb;
-      targs.bias1 = reinterpret_cast<const float*>(base + off_b1_);
-      targs.bias2 = reinterpret_cast<const float*>(base + off_b2_);
-      targs.out = out;
-      ES_LAUNCH(es::mlpt_launch(targs, x, base, base + off_w2_, grid, stream));
-      return 1;
-    }
-    es::Mlp2Args args;
-    args.L = plan_;
-    args.b = batch_;
-    args.seg_size = seg_size;
-    args.seg_begin = s0;
-    args.seg_end = s1;
-    args.nb = nb;
-    args.bias1 = reinterpret_cast<const float*>(base + off_b1_);
-    args.bias2 = reinterpret_cast<const float*>(base + off_b2_);
-    args.out = out;
-    ES_LAUNCH(es::mlp2_launch(args, x, base, base + off_w2_, grid, stream));
-    return 1;
-  }
-
-  int device() const { return device_; }
-  std::size_t weight_bytes() const { return bytes_; }
-  const es::Mlp2Layout& plan() const { return plan_; }
-
- private:
-  int device_ = 0;
-  ModelSpec model_;
-  int batch_ = 1;
-  int K_ = 0, H_ = 0, C_ = 1;
-  es::Mlp2Layout plan_{};
-  es::MlpTLayout tplan_{};
-  es::MlpPLayout pplan_{};
-  enum class Kind { SwapAB, Tmem, Pair } kind_ = Kind::SwapAB;
-  void* weights_ = nullptr;
-  std::size_t bytes_ = 0, off_b1_ = 0, off_w2_ = 0, off_b2_ = 0;
-};
 
 // ---------------------------------------------------------------- system
 struct InferenceSystem::Worker {
