@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   const DenseLayout& L = args.L;
-  uint8_t* sOut = smem + L.off_stage_out;  // [2 halves][2 buffers][128 rows][128 B]
+  uint8_t* sOut = smem + L.off_stage_out;  // [2 halves][128 rows][128 B]
   float* sBias = reinterpret_cast<float*>(smem + L.off_bias);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.off_bar);
   uint64_t* full = bars;
@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool issuer = (warp & 3) == 2 && lane == 0;  // one thread per half issues stores
     for (int i = threadIdx.x - 64; i < N; i += 256) sBias[i] = args.bias[i];
     asm volatile("bar.sync 1, 256;" ::: "memory");
-    uint8_t* myout = sOut + half * 2 * 16384;
+    uint8_t* myout = sOut + half * 16384;
     int it = 0;  // staging buffers used by this half
     long long row0[kMaxT];
     for (int g = 0;; ++g) {
@@ -167,11 +167,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld32_raw(tmem_base + lane_field + col, ra);
           tmem_ld32_raw(tmem_base + lane_field + col + 32, rb);
           tmem_ld_wait();
-          // Staging buffer it%2 is free once the store issued two chunks ago
-          // has read it.
-          if (issuer) tma_store_wait_read<1>();
+          // The half's staging tile is free once the previous store read it.
+          if (issuer) tma_store_wait_read<0>();
           half_barrier(half);
-          uint8_t* stg = myout + (it & 1) * 16384 + row * 128;
+          uint8_t* stg = myout + row * 128;
           const float* bias = sBias + c * 64;
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
@@ -195,7 +194,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           fence_proxy_async_smem();
           half_barrier(half);
           if (issuer) {
-            tma_store_2d(&tm_y, myout + (it & 1) * 16384, c * 64, static_cast<int32_t>(row0[k]));
+            tma_store_2d(&tm_y, myout, c * 64, static_cast<int32_t>(row0[k]));
             tma_store_commit();
           }
         }
@@ -245,12 +244,12 @@ bool dense_plan(int K, int N, bool relu, DenseLayout* out) {
       while (tc < cols) tc <<= 1;
       L.tmem_cols = tc;
       L.stage_bytes = static_cast<uint32_t>(T) * 16384u + static_cast<uint32_t>(N) * 128u;
-      const uint32_t tail = 4 * 16384u + static_cast<uint32_t>(N) * 4u + 256u + 1024u;
+      const uint32_t tail = 2 * 16384u + static_cast<uint32_t>(N) * 4u + 256u + 1024u;
       const int stages = static_cast<int>(std::min<uint32_t>(8, (kSmemBudget - tail) / L.stage_bytes));
       if (stages < 2) continue;
       L.stages = stages;
       L.off_stage_out = static_cast<uint32_t>(stages) * L.stage_bytes;
-      L.off_bias = L.off_stage_out + 4 * 16384u;
+      L.off_bias = L.off_stage_out + 2 * 16384u;
       L.off_bar = align_up(L.off_bias + static_cast<uint32_t>(N) * 4u, 64);
       L.smem_bytes = std::max(L.off_bar + 256u + 1024u, kMinSmem);
       if (L.smem_bytes > kSmemBudget) continue;

@@ -8,7 +8,7 @@
 //   UMMA M = 128 rows, N <= 256 per instruction (up to 512 per tile), K in
 //   64-wide TMA chunks; T tiles share each W chunk; fp32 accumulators in TMEM;
 //   epilogue: tcgen05.ld -> +b, ReLU, bf16 -> 128B-swizzled smem staging ->
-//   TMA bulk tensor store (one 64-column box per chunk, double buffered).
+//   TMA bulk tensor store (one 64-column box per chunk and column half).
 #pragma once
 
 #include <cstdint>

@@ -101,8 +101,10 @@ bool DeviceMember::load(int device, const ModelSpec& model, int batch) {
   for (int l = 0; l < L - 2; ++l) {
     es::DenseLayout d;
     if (!es::dense_plan(a.widths[l], a.widths[l + 1], true, &d))
-      throw SpecError(model.name + ": hidden width " + std::to_string(a.widths[l + 1]) +
-                      " of a leading layer must be a multiple of 128 up to 512");
+      throw SpecError(model.name + ": leading layer " + std::to_string(a.widths[l]) + "->" +
+                      std::to_string(a.widths[l + 1]) +
+                      " has no tile plan (input width a multiple of 8, output width a "
+                      "multiple of 128 up to 512)");
     I.dense.push_back(d);
   }
   // Fused head over the last two layers.

@@ -9,7 +9,7 @@ import pytest
 import paper_2208_14049_b200 as es
 from conftest import gpu
 from oracle import refcpu, restate
-from test_gpu_parity import assert_logits_close
+from test_gpu_parity import RTOL_BF16, assert_logits_close
 
 pytestmark = pytest.mark.gpu
 
@@ -23,7 +23,9 @@ def test_deep_mlp_member_matches_cpu_oracle(widths, b):
     got = es.Member(model, b).predict(X)
     cpu = refcpu.CpuMlp(widths, 4242)
     want = cpu.forward(X)
-    assert_logits_close(got, want, cpu.logit_scale(X))
+    # Every bf16-rounded activation layer brings its own rounding-flip budget
+    # (DESIGN.md §Tolerances): rtol scales with the number of hidden layers.
+    assert_logits_close(got, want, cpu.logit_scale(X), rtol=RTOL_BF16 * (len(widths) - 2))
     np.testing.assert_array_equal(np.argmax(got, 1), np.argmax(want, 1))
 
 
@@ -40,4 +42,11 @@ def test_heterogeneous_depths_in_one_ensemble_match_reference_pipeline():
     out = es.run_inference(es.SampleStore(X), A, c, es.CombinationRule.averaging(softmax=True))
     Yr, _, _ = refcpu.ref_run_ensemble(c, A.cells, X, rule=0, softmax=True)
     np.testing.assert_allclose(out.combined, Yr, rtol=0, atol=1e-3)
-    np.testing.assert_array_equal(out.winners, np.argmax(Yr, 1))
+    # Winners agree wherever the reference's top two probabilities are further
+    # apart than the two tolerances; inside that band either may win, but the
+    # winner must still be one of the reference's top two.
+    top = np.argsort(Yr, axis=1)[:, -2:]
+    gap = np.take_along_axis(Yr, top[:, 1:], 1)[:, 0] - np.take_along_axis(Yr, top[:, :1], 1)[:, 0]
+    clear = gap > 2e-3
+    np.testing.assert_array_equal(out.winners[clear], top[clear, 1])
+    assert np.all((out.winners == top[:, 1]) | (out.winners == top[:, 0]))
