@@ -54,8 +54,10 @@ typedef struct es_model_desc {
   double act_mib_per_sample;
   double cost_per_sample;
   int output_width;
-  int arch;                     /* 0 = synthetic_prediction member, 1 = MLP */
-  int n_widths;                 /* MLP: input, hidden..., classes */
+  int arch;                     /* 0 = synthetic_prediction member, 1 = MLP, 2 = CNN */
+  int n_widths;                 /* MLP: input, hidden..., classes;
+                                   CNN: 6 = {S, P, c1, c2, hidden, classes} (S x S image,
+                                   conv PxP/P -> c1, conv 3x3 -> c2, dense -> hidden -> classes) */
   int widths[ES_MAX_WIDTHS];
   uint64_t weight_seed;
 } es_model_desc;

@@ -216,6 +216,159 @@ void orc_mlp_forward(const orc_mlp* m, const float* x, size_t rows, float* out) 
   free(c);
 }
 
+/* ---------------------------------------------------------------- CNN */
+typedef struct {
+  int fi, fo, po;
+  float* w;  /* [fo][fi] */
+  float* wt; /* [fi][po] */
+  float* b;  /* [po] */
+} orc_layer;
+
+static void layer_init(orc_layer* L, uint64_t seed, int l, int fi, int fo, int quantize) {
+  L->fi = fi;
+  L->fo = fo;
+  L->po = (fo + 15) / 16 * 16;
+  L->w = (float*)malloc(sizeof(float) * (size_t)fi * fo);
+  L->wt = (float*)calloc((size_t)fi * L->po, sizeof(float));
+  L->b = (float*)calloc((size_t)L->po, sizeof(float));
+  for (int o = 0; o < fo; ++o) {
+    for (int i = 0; i < fi; ++i) {
+      uint64_t idx = (uint64_t)o * fi + i;
+      float v = orc_weight(seed, l, idx, fi, fo);
+      if (quantize) v = orc_round_bf16(v);
+      L->w[idx] = v;
+      L->wt[(size_t)i * L->po + o] = v;
+    }
+    L->b[o] = orc_bias(seed, l, (uint64_t)o);
+  }
+}
+
+static void layer_free(orc_layer* L) {
+  free(L->w);
+  free(L->wt);
+  free(L->b);
+}
+
+/* y[rows][po] for rows a multiple of RB (x rows of stride fi). */
+static void layer_apply(const orc_layer* L, const float* x, size_t rows, int relu_q, int quantize,
+                        float* y) {
+  for (size_t r = 0; r < rows; r += RB)
+    dense_block(x + r * (size_t)L->fi, L->fi, L->wt, L->b, L->po, relu_q, quantize,
+                y + r * (size_t)L->po);
+}
+
+struct orc_cnn {
+  int S, P, G, c1, c2, hidden, C, quantize;
+  orc_layer L[4];
+};
+
+orc_cnn* orc_cnn_create(int S, int P, int c1, int c2, int hidden, int C, uint64_t seed,
+                        int quantize_bf16) {
+  if (P < 1 || S < P || S % P != 0 || c1 < 1 || c2 < 1 || hidden < 1 || C < 1) return NULL;
+  orc_cnn* m = (orc_cnn*)calloc(1, sizeof(orc_cnn));
+  m->S = S;
+  m->P = P;
+  m->G = S / P;
+  m->c1 = c1;
+  m->c2 = c2;
+  m->hidden = hidden;
+  m->C = C;
+  m->quantize = quantize_bf16;
+  layer_init(&m->L[0], seed, 0, P * P, c1, quantize_bf16);
+  layer_init(&m->L[1], seed, 1, 9 * c1, c2, quantize_bf16);
+  layer_init(&m->L[2], seed, 2, m->G * m->G * c2, hidden, quantize_bf16);
+  layer_init(&m->L[3], seed, 3, hidden, C, quantize_bf16);
+  return m;
+}
+
+void orc_cnn_destroy(orc_cnn* m) {
+  if (!m) return;
+  for (int l = 0; l < 4; ++l) layer_free(&m->L[l]);
+  free(m);
+}
+
+int orc_cnn_classes(const orc_cnn* m) { return m->C; }
+
+void orc_cnn_layer(const orc_cnn* m, int l, float* w, float* b) {
+  const orc_layer* L = &m->L[l];
+  if (w) memcpy(w, L->w, sizeof(float) * (size_t)L->fi * L->fo);
+  if (b) memcpy(b, L->b, sizeof(float) * (size_t)L->fo);
+}
+
+/* Logits and/or hidden activations, RB samples at a time. */
+static void cnn_run(const orc_cnn* m, const float* x, size_t rows, float* logits, float* hid) {
+  const int S = m->S, P = m->P, G = m->G, G2 = G * G, c1 = m->c1, c2 = m->c2;
+  const size_t gp = (size_t)(G2 + RB - 1) / RB * RB; /* pixel rows, padded to RB */
+  const int po1 = m->L[0].po, po2 = m->L[1].po, poh = m->L[2].po, poc = m->L[3].po;
+  const int feat = G2 * c2;
+  float* x1 = (float*)calloc(gp * (size_t)(P * P), sizeof(float));
+  float* y1 = (float*)calloc(gp * (size_t)po1, sizeof(float));
+  float* x2 = (float*)calloc(gp * (size_t)(9 * c1), sizeof(float));
+  float* y2 = (float*)calloc(gp * (size_t)po2, sizeof(float));
+  float* f = (float*)calloc((size_t)RB * feat, sizeof(float));
+  float* h = (float*)calloc((size_t)RB * poh, sizeof(float));
+  float* hc = (float*)calloc((size_t)RB * m->hidden, sizeof(float));
+  float* z = (float*)calloc((size_t)RB * poc, sizeof(float));
+  for (size_t r0 = 0; r0 < rows; r0 += RB) {
+    const size_t nr = rows - r0 < RB ? rows - r0 : RB;
+    memset(f, 0, sizeof(float) * (size_t)RB * feat);
+    for (size_t s = 0; s < nr; ++s) {
+      const float* img = x + (r0 + s) * (size_t)(S * S);
+      for (int p = 0; p < G2; ++p) {
+        const int i = p / G, j = p % G;
+        for (int a = 0; a < P; ++a)
+          for (int b = 0; b < P; ++b) {
+            float v = img[(P * i + a) * S + P * j + b];
+            x1[(size_t)p * (P * P) + a * P + b] = m->quantize ? orc_round_bf16(v) : v;
+          }
+      }
+      layer_apply(&m->L[0], x1, gp, 1, m->quantize, y1);
+      for (int p = 0; p < G2; ++p) {
+        const int i = p / G, j = p % G;
+        for (int t = 0; t < 9; ++t) {
+          const int ii = i + t / 3 - 1, jj = j + t % 3 - 1;
+          float* dst = x2 + (size_t)p * (9 * c1) + (size_t)t * c1;
+          if (ii < 0 || ii >= G || jj < 0 || jj >= G)
+            memset(dst, 0, sizeof(float) * (size_t)c1);
+          else
+            memcpy(dst, y1 + (size_t)(ii * G + jj) * po1, sizeof(float) * (size_t)c1);
+        }
+      }
+      layer_apply(&m->L[1], x2, gp, 1, m->quantize, y2);
+      for (int p = 0; p < G2; ++p)
+        memcpy(f + s * (size_t)feat + (size_t)p * c2, y2 + (size_t)p * po2, sizeof(float) * (size_t)c2);
+    }
+    dense_block(f, feat, m->L[2].wt, m->L[2].b, poh, 1, m->quantize, h);
+    for (int r = 0; r < RB; ++r)
+      memcpy(hc + (size_t)r * m->hidden, h + (size_t)r * poh, sizeof(float) * (size_t)m->hidden);
+    if (hid)
+      for (size_t r = 0; r < nr; ++r)
+        memcpy(hid + (r0 + r) * (size_t)m->hidden, hc + r * (size_t)m->hidden,
+               sizeof(float) * (size_t)m->hidden);
+    if (logits) {
+      dense_block(hc, m->hidden, m->L[3].wt, m->L[3].b, poc, 0, m->quantize, z);
+      for (size_t r = 0; r < nr; ++r)
+        memcpy(logits + (r0 + r) * (size_t)m->C, z + r * (size_t)poc, sizeof(float) * (size_t)m->C);
+    }
+  }
+  free(x1);
+  free(y1);
+  free(x2);
+  free(y2);
+  free(f);
+  free(h);
+  free(hc);
+  free(z);
+}
+
+void orc_cnn_forward(const orc_cnn* m, const float* x, size_t rows, float* out) {
+  cnn_run(m, x, rows, out, NULL);
+}
+
+void orc_cnn_hidden(const orc_cnn* m, const float* x, size_t rows, float* out) {
+  cnn_run(m, x, rows, NULL, out);
+}
+
 void orc_softmax_rows(const float* z, size_t rows, int C, float* p) {
   for (size_t r = 0; r < rows; ++r) {
     const float* zr = z + r * (size_t)C;

@@ -56,6 +56,25 @@ void orc_mlp_forward(const orc_mlp* m, const float* x, size_t rows, float* out);
 /* Copies the (quantised) weights of layer l as stored [fan_out][fan_in]. */
 void orc_mlp_layer(const orc_mlp* m, int l, float* w, float* b);
 
+/* CNN member: an S x S one-channel image (x row of S*S), conv P x P stride P
+ * -> c1 (ReLU), conv 3 x 3 pad 1 -> c2 (ReLU), dense (S/P)^2*c2 -> hidden
+ * (ReLU) -> C.  Weight matrices, in generation order (layer index):
+ *   0: [c1][P*P],     K index a*P + b (pixel (P*i+a, P*j+b) of block (i, j));
+ *   1: [c2][9*c1],    K index tap*c1 + channel, tap = 3*(dh+1) + (dw+1);
+ *   2: [hidden][G*G*c2], K index (h*G + w)*c2 + channel (HWC flatten);
+ *   3: [C][hidden].
+ * The convolutions are dense layers over im2col rows (zero outside the
+ * image); bf16 mode rounds X, every weight and every post-ReLU activation. */
+typedef struct orc_cnn orc_cnn;
+orc_cnn* orc_cnn_create(int S, int P, int c1, int c2, int hidden, int C, uint64_t seed,
+                        int quantize_bf16);
+void orc_cnn_destroy(orc_cnn* m);
+int orc_cnn_classes(const orc_cnn* m);
+void orc_cnn_forward(const orc_cnn* m, const float* x, size_t rows, float* out);
+/* The last layer's inputs (post-ReLU hidden activations) [rows][hidden]. */
+void orc_cnn_hidden(const orc_cnn* m, const float* x, size_t rows, float* out);
+void orc_cnn_layer(const orc_cnn* m, int l, float* w, float* b);
+
 /* p = softmax(z) per row, fp32, expf(z - max) / sum. */
 void orc_softmax_rows(const float* z, size_t rows, int C, float* p);
 

@@ -51,8 +51,9 @@ struct ref_cluster {
   int segment_size;
 };
 
-// Member architecture for the CPU MLP backend: layers[m] dense layers with
-// widths[m*9 .. m*9+layers[m]] (input, hidden..., classes).
+// Member architecture for the CPU backend: layers[m] dense layers with
+// widths[m*9 .. m*9+layers[m]] (input, hidden..., classes), or layers[m] = -1
+// for a CNN member with widths[m*9 .. m*9+5] = {S, P, c1, c2, hidden, classes}.
 struct ref_roster {
   const int* layers;
   const int* widths;
@@ -102,27 +103,42 @@ class CpuMlpBackend : public PredictorFactory {
  public:
   CpuMlpBackend(const ref_roster* r, int n_models) : softmax_(r->softmax != 0) {
     for (int m = 0; m < n_models; ++m) {
-      mlps_.emplace_back(orc_mlp_create(r->layers[m], r->widths + 9 * m, r->seeds[m],
-                                        r->quantize_bf16),
-                         &orc_mlp_destroy);
+      Member mem;
+      const int* w = r->widths + 9 * m;
+      if (r->layers[m] < 0)
+        mem.cnn.reset(orc_cnn_create(w[0], w[1], w[2], w[3], w[4], w[5], r->seeds[m],
+                                     r->quantize_bf16));
+      else
+        mem.mlp.reset(orc_mlp_create(r->layers[m], w, r->seeds[m], r->quantize_bf16));
+      members_.push_back(std::move(mem));
     }
   }
   std::unique_ptr<Predictor> make(const WorkerContext& ctx) const override {
-    return std::make_unique<CpuMlpPredictor>(ctx, mlps_.at(ctx.model.id).get(), softmax_);
+    return std::make_unique<CpuMemberPredictor>(ctx, &members_.at(ctx.model.id), softmax_);
   }
-  std::string name() const override { return "oracle-cpu-mlp"; }
+  std::string name() const override { return "oracle-cpu-member"; }
 
  private:
-  class CpuMlpPredictor : public Predictor {
+  struct Member {
+    std::unique_ptr<orc_mlp, void (*)(orc_mlp*)> mlp{nullptr, &orc_mlp_destroy};
+    std::unique_ptr<orc_cnn, void (*)(orc_cnn*)> cnn{nullptr, &orc_cnn_destroy};
+  };
+  class CpuMemberPredictor : public Predictor {
    public:
-    CpuMlpPredictor(const WorkerContext& ctx, const orc_mlp* mlp, bool softmax)
-        : ctx_(ctx), mlp_(mlp), softmax_(softmax) {}
+    CpuMemberPredictor(const WorkerContext& ctx, const Member* m, bool softmax)
+        : ctx_(ctx), m_(m), softmax_(softmax) {}
     // Same capacity rule as SyntheticPredictor::load (backend.cpp:41).
     bool load() override { return ctx_.device_load_mib <= ctx_.device.memory_mib; }
     void predict(const SampleView& in, std::span<float> out) override {
-      orc_mlp_forward(mlp_, in.features.data(), in.rows, out.data());
+      int C;
+      if (m_->cnn) {
+        orc_cnn_forward(m_->cnn.get(), in.features.data(), in.rows, out.data());
+        C = orc_cnn_classes(m_->cnn.get());
+      } else {
+        orc_mlp_forward(m_->mlp.get(), in.features.data(), in.rows, out.data());
+        C = orc_mlp_classes(m_->mlp.get());
+      }
       if (softmax_) {
-        int C = orc_mlp_classes(mlp_);
         std::vector<float> z(out.begin(), out.end());
         orc_softmax_rows(z.data(), in.rows, C, out.data());
       }
@@ -130,10 +146,10 @@ class CpuMlpBackend : public PredictorFactory {
 
    private:
     WorkerContext ctx_;
-    const orc_mlp* mlp_;
+    const Member* m_;
     bool softmax_;
   };
-  std::vector<std::unique_ptr<orc_mlp, void (*)(orc_mlp*)>> mlps_;
+  std::vector<Member> members_;
   bool softmax_;
 };
 

@@ -57,6 +57,12 @@ def orc() -> C.CDLL:
         lib.orc_mlp_destroy.argtypes = [C.c_void_p]
         lib.orc_mlp_forward.argtypes = [C.c_void_p, f32p, C.c_size_t, f32p]
         lib.orc_mlp_layer.argtypes = [C.c_void_p, C.c_int, f32p, f32p]
+        lib.orc_cnn_create.restype = C.c_void_p
+        lib.orc_cnn_create.argtypes = [C.c_int] * 6 + [C.c_uint64, C.c_int]
+        lib.orc_cnn_destroy.argtypes = [C.c_void_p]
+        lib.orc_cnn_forward.argtypes = [C.c_void_p, f32p, C.c_size_t, f32p]
+        lib.orc_cnn_hidden.argtypes = [C.c_void_p, f32p, C.c_size_t, f32p]
+        lib.orc_cnn_layer.argtypes = [C.c_void_p, C.c_int, f32p, f32p]
         lib.orc_softmax_rows.argtypes = [f32p, C.c_size_t, C.c_int, f32p]
         lib.orc_fold.argtypes = [C.c_int, C.c_int, C.c_size_t, C.c_int, C.POINTER(f32p), f64p,
                                  f32p, i32p]
@@ -114,6 +120,57 @@ class CpuMlp:
         if getattr(self, "_h", None):
             orc().orc_mlp_destroy(self._h)
             self._h = None
+
+
+class CpuCnn:
+    """Oracle CPU CNN member (cpu_member.c orc_cnn_*): widths = (S, P, c1, c2,
+    hidden, classes)."""
+
+    def __init__(self, widths, seed: int, quantize_bf16: bool = True):
+        self.widths = [int(w) for w in widths]
+        self._h = orc().orc_cnn_create(*self.widths, seed, int(quantize_bf16))
+        if not self._h:
+            raise ValueError("bad CNN shape")
+        S, P, c1, c2, hidden, Cn = self.widths
+        G = S // P
+        self.dims = [(P * P, c1), (9 * c1, c2), (G * G * c2, hidden), (hidden, Cn)]
+
+    def forward(self, X: np.ndarray) -> np.ndarray:
+        X = np.ascontiguousarray(X, dtype=np.float32)
+        out = np.zeros((X.shape[0], self.widths[-1]), dtype=np.float32)
+        orc().orc_cnn_forward(self._h, _fp(X), X.shape[0], _fp(out))
+        return out
+
+    def logit_scale(self, X: np.ndarray) -> np.ndarray:
+        """As CpuMlp.logit_scale: |b_c| + sum_j |W[c,j]| |a_j| over the last
+        layer's (bf16) inputs."""
+        X = np.ascontiguousarray(X, dtype=np.float32)
+        hidden = self.widths[4]
+        a = np.zeros((X.shape[0], hidden), dtype=np.float32)
+        orc().orc_cnn_hidden(self._h, _fp(X), X.shape[0], _fp(a))
+        w, b = self.layer(3)
+        return (np.abs(a.astype(np.float64)) @ np.abs(w.T.astype(np.float64))
+                + np.abs(b)).astype(np.float32)
+
+    def layer(self, l: int):
+        fi, fo = self.dims[l]
+        w = np.zeros((fo, fi), dtype=np.float32)
+        b = np.zeros(fo, dtype=np.float32)
+        orc().orc_cnn_layer(self._h, l, _fp(w), _fp(b))
+        return w, b
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            orc().orc_cnn_destroy(self._h)
+            self._h = None
+
+
+def cpu_member(arch):
+    """The oracle member for a product MemberArch-like object (kind, widths,
+    weight_seed)."""
+    if getattr(arch, "kind", "mlp") == "cnn":
+        return CpuCnn(arch.widths, arch.weight_seed)
+    return CpuMlp(arch.widths, arch.weight_seed)
 
 
 def round_bf16(x: np.ndarray) -> np.ndarray:
@@ -258,7 +315,7 @@ class RefCluster:
             arch = getattr(m, "arch", None)
             ws = list(getattr(arch, "widths", ()) or ())
             if ws:
-                layers[i] = len(ws) - 1
+                layers[i] = -1 if getattr(arch, "kind", "mlp") == "cnn" else len(ws) - 1
                 for j, w in enumerate(ws):
                     widths[9 * i + j] = w
                 seeds[i] = getattr(arch, "weight_seed", 0)

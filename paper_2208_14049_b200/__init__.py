@@ -12,7 +12,7 @@ from .api import (AllocationError, AllocationMatrix, BaselineError, CapExceededE
                   MemberArch, ModelSpec, ProtocolError, SampleStore, SpecError, StartupError,
                   bbs_baseline, bench, bounded_greedy, combine, count_total_matrices,
                   count_total_neighs, device_count, effective_max_iter, enumerate_all_matrices,
-                  enumerated_neighborhood_stats, fit_mem, mlp_model, more_remaining_memory,
+                  enumerated_neighborhood_stats, fit_mem, mlp_model, cnn_model, more_remaining_memory,
                   neighborhood, num_segments, predict_ensemble_throughput, run_inference,
                   sample_indices, segment_bounds, validate_matrix, worst_fit_decreasing)
 

@@ -92,17 +92,42 @@ class MemberArch:
     """What the device executes for a member (spec.hpp MemberArch).
 
     kind "synthetic": synthetic_prediction(model, sample, class)
-    (src/runtime/backend.cpp:21-29); kind "mlp": dense layers over `widths`.
+    (src/runtime/backend.cpp:21-29); kind "mlp": dense layers over `widths`;
+    kind "cnn": widths = (S, P, c1, c2, hidden, classes) -- an S x S image,
+    conv PxP stride P -> c1, conv 3x3 pad 1 -> c2, dense -> hidden -> classes.
     """
     kind: str = "synthetic"
     widths: tuple = ()
     weight_seed: int = 0
 
+    def layer_dims(self) -> list:
+        """(fan_in, fan_out) of every weight matrix, in generation order."""
+        w = self.widths
+        if self.kind == "cnn":
+            S, P, c1, c2, hidden, C = w
+            G = S // P
+            return [(P * P, c1), (9 * c1, c2), (G * G * c2, hidden), (hidden, C)]
+        return list(zip(w[:-1], w[1:]))
+
+    def input_width(self) -> int:
+        return self.widths[0] ** 2 if self.kind == "cnn" else self.widths[0]
+
     def flops_per_sample(self) -> float:
-        return float(sum(2 * a * b for a, b in zip(self.widths[:-1], self.widths[1:])))
+        d = self.layer_dims()
+        if self.kind == "cnn":
+            G2 = (self.widths[0] // self.widths[1]) ** 2
+            return float(2 * (G2 * d[0][0] * d[0][1] + G2 * d[1][0] * d[1][1]
+                              + d[2][0] * d[2][1] + d[3][0] * d[3][1]))
+        return float(sum(2 * a * b for a, b in d))
 
     def parameter_count(self) -> int:
-        return int(sum(a * b + b for a, b in zip(self.widths[:-1], self.widths[1:])))
+        return int(sum(a * b + b for a, b in self.layer_dims()))
+
+    def activation_elems(self) -> int:
+        if self.kind == "cnn":
+            S, P, c1, c2, hidden, C = self.widths
+            return S * S + (S // P) ** 2 * (c1 + c2) + hidden + C
+        return int(sum(self.widths))
 
 
 @dataclass
@@ -130,6 +155,23 @@ def mlp_model(id: int, name: str, widths: Sequence[int], seed: int, *,
         act_mib_per_sample=act_mib if act_mib is not None else sum(widths) * 2 / mib,
         cost_per_sample=cost if cost is not None else arch.flops_per_sample(),
         output_width=int(widths[-1]), arch=arch)
+
+
+def cnn_model(id: int, name: str, seed: int, *, S: int = 28, P: int = 4, c1: int = 64,
+              c2: int = 32, hidden: int = 128, classes: int = 10,
+              weight_mib: Optional[float] = None, act_mib: Optional[float] = None,
+              cost: Optional[float] = None) -> ModelSpec:
+    """A CNN member ("CNN-s" by default: 28x28 -> conv4x4/4 64 -> conv3x3 32 ->
+    128 -> 10), footprint derived like mlp_model's."""
+    arch = MemberArch("cnn", (int(S), int(P), int(c1), int(c2), int(hidden), int(classes)),
+                      int(seed))
+    mib = 1024.0 * 1024.0
+    return ModelSpec(
+        id=id, name=name,
+        weight_mib=weight_mib if weight_mib is not None else arch.parameter_count() * 2 / mib,
+        act_mib_per_sample=act_mib if act_mib is not None else arch.activation_elems() * 2 / mib,
+        cost_per_sample=cost if cost is not None else arch.flops_per_sample(),
+        output_width=int(classes), arch=arch)
 
 
 @dataclass
@@ -176,7 +218,7 @@ class _Desc:
             md.act_mib_per_sample = m.act_mib_per_sample
             md.cost_per_sample = m.cost_per_sample
             md.output_width = m.output_width
-            md.arch = 1 if m.arch.kind == "mlp" else 0
+            md.arch = {"mlp": 1, "cnn": 2}.get(m.arch.kind, 0)
             md.n_widths = len(m.arch.widths)
             for j, w in enumerate(m.arch.widths):
                 md.widths[j] = int(w)

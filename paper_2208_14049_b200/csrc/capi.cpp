@@ -93,6 +93,11 @@ ModelSpec to_model(const es_model_desc& d, int id) {
     m.arch.kind = MemberArch::Kind::MLP;
     m.arch.widths.assign(d.widths, d.widths + d.n_widths);
     m.arch.weight_seed = d.weight_seed;
+  } else if (d.arch == 2) {
+    need(d.n_widths == 6, "CNN needs widths {S, P, c1, c2, hidden, classes}");
+    m.arch.kind = MemberArch::Kind::CNN;
+    m.arch.widths.assign(d.widths, d.widths + d.n_widths);
+    m.arch.weight_seed = d.weight_seed;
   } else {
     m.arch.kind = MemberArch::Kind::Synthetic;
   }

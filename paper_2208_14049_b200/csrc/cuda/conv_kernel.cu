@@ -1,0 +1,369 @@
+// Convolution stack of the CNN member (design in conv_kernel.cuh).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+
+#include "conv_kernel.cuh"
+#include "sm100.cuh"
+#include "tma_host.hpp"
+
+namespace es {
+
+using namespace sm100;
+
+namespace {
+
+// w0 TMA producer, w1 UMMA issuer, w2..w5 im2col + conv1 epilogue,
+// w6..w9 conv2 epilogue (each group covers the four TMEM lane quadrants).
+constexpr int kThreads = 320;
+constexpr uint32_t kSmemBudget = 232448;
+constexpr int kMargin = 16;  // rows before/after each padded grid; tap shifts reach pad+1
+
+__device__ __forceinline__ uint32_t pack_relu_bf16(uint32_t a, uint32_t b, float ba, float bb) {
+  const float lo = fmaxf(__uint_as_float(a) + ba, 0.0f);
+  const float hi = fmaxf(__uint_as_float(b) + bb, 0.0f);
+  __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    conv_stack_sm100(const __grid_constant__ CUtensorMap tm_x, const ConvArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  const ConvLayout& L = args.L;
+  uint8_t* sRaw = smem + L.off_raw;
+  uint8_t* sA1 = smem + L.off_a1;
+  uint8_t* sA2 = smem + L.off_a2;
+  uint8_t* sW1 = smem + L.off_w1;
+  uint8_t* sW2 = smem + L.off_w2;
+  float* sB1 = reinterpret_cast<float*>(smem + L.off_b1);
+  float* sB2 = reinterpret_cast<float*>(smem + L.off_b2);
+  uint64_t* raw_full = reinterpret_cast<uint64_t*>(smem + L.off_bar);
+  uint64_t* raw_empty = raw_full + L.raw_stages;
+  uint64_t* a1_full = raw_empty + L.raw_stages;  // every pair below: one per buffer
+  uint64_t* a1_empty = a1_full + 2;
+  uint64_t* c1_full = a1_empty + 2;
+  uint64_t* c1_empty = c1_full + 2;
+  uint64_t* a2_full = c1_empty + 2;
+  uint64_t* a2_empty = a2_full + 2;
+  uint64_t* c2_full = a2_empty + 2;
+  uint64_t* c2_empty = c2_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(c2_empty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const long long tiles = (args.row_end - args.row_begin + L.T - 1) / L.T;
+  const int my_tiles =
+      blockIdx.x < tiles ? static_cast<int>((tiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+  const int kp = L.c1 / 8;  // 16-byte planes of conv2's K per tap
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < L.raw_stages; ++s) {
+      mbar_init(&raw_full[s], 1);
+      mbar_init(&raw_empty[s], 128);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&a1_full[b], 128);
+      mbar_init(&a1_empty[b], 1);
+      mbar_init(&c1_full[b], 1);
+      mbar_init(&c1_empty[b], 4);
+      mbar_init(&a2_full[b], 128);
+      mbar_init(&a2_empty[b], 1);
+      mbar_init(&c2_full[b], 1);
+      mbar_init(&c2_empty[b], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) tma_prefetch(&tm_x);
+  if (warp == 1) tmem_alloc(tmem_slot, static_cast<uint32_t>(L.tmem_cols));
+
+  // Resident operands: weights in the planar K-major layout (plane k of row o
+  // = K elements 8k..8k+7), biases, and both padded grids zeroed once -- the
+  // conv1 epilogue only ever rewrites interior rows, so borders stay zero.
+  {
+    const uint4* w1 = static_cast<const uint4*>(args.w1);  // [c1][16] bf16 = 2 chunks per row
+    for (int i = threadIdx.x; i < L.c1 * 2; i += kThreads) {
+      const int o = i >> 1, k = i & 1;
+      *reinterpret_cast<uint4*>(sW1 + (k * L.c1 + o) * 16) = w1[i];
+    }
+    const uint4* w2 = static_cast<const uint4*>(args.w2);  // [c2][9*c1] bf16 = 9*kp chunks per row
+    for (int i = threadIdx.x; i < 9 * kp * L.c2; i += kThreads) {
+      const int o = i / (9 * kp), rem = i % (9 * kp);  // rem = tap * kp + plane
+      *reinterpret_cast<uint4*>(sW2 + (rem * L.c2 + o) * 16) = w2[i];
+    }
+    for (int i = threadIdx.x; i < L.c1; i += kThreads) sB1[i] = args.b1[i];
+    for (int i = threadIdx.x; i < L.c2; i += kThreads) sB2[i] = args.b2[i];
+    uint4* z = reinterpret_cast<uint4*>(sA2);
+    for (int i = threadIdx.x; i < static_cast<int>(2 * L.a2_bytes / 16); i += kThreads)
+      z[i] = make_uint4(0, 0, 0, 0);
+  }
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int G2 = L.G * L.G, P2 = L.pad * L.pad;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      const uint64_t pol = l2_policy_evict_first();
+      const int rows16 = L.S * L.S / 16;  // the map views x as [rows * S*S/16][16]
+      for (int k = 0; k < my_tiles; ++k) {
+        const int st = k % L.raw_stages;
+        const uint32_t use = static_cast<uint32_t>(k / L.raw_stages);
+        mbar_wait(&raw_empty[st], (use & 1u) ^ 1u);
+        const long long s0 = args.row_begin + (blockIdx.x + static_cast<long long>(k) * gridDim.x) * L.T;
+        mbar_arrive_expect_tx(&raw_full[st], static_cast<uint32_t>(L.T * L.S * L.S * 2));
+        tma_load_2d(sRaw + st * L.raw_stride, &tm_x, &raw_full[st], 0,
+                    static_cast<int32_t>(s0 * rows16), pol);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ UMMA issuer
+    if (lane == 0) {
+      const uint32_t id1 = idesc_bf16_f32(128, L.c1), id2 = idesc_bf16_f32(128, L.c2);
+      const uint32_t w1a = smem_u32(sW1), w2a = smem_u32(sW2);
+      const uint64_t w1d = sdesc_planar(w1a, static_cast<uint32_t>(L.c1 * 16));
+      auto conv1 = [&](int k) {
+        const int b = k & 1;
+        const uint32_t u = static_cast<uint32_t>(k >> 1) & 1u;
+        mbar_wait(&a1_full[b], u);
+        mbar_wait(&c1_empty[b], u ^ 1u);
+        tc_fence_after();
+        const uint32_t a = smem_u32(sA1 + b * L.a1_bytes);
+        for (int mb = 0; mb < L.mb1; ++mb)
+          umma_bf16(tmem_base + static_cast<uint32_t>(b * L.tmem_c1 + mb * L.c1),
+                    sdesc_planar(a + static_cast<uint32_t>(mb * 128 * 16), L.a1_plane), w1d, id1, 0);
+        umma_commit(&a1_empty[b]);
+        umma_commit(&c1_full[b]);
+      };
+      auto conv2 = [&](int k) {
+        const int b = k & 1;
+        const uint32_t u = static_cast<uint32_t>(k >> 1) & 1u;
+        mbar_wait(&a2_full[b], u);
+        mbar_wait(&c2_empty[b], u ^ 1u);
+        tc_fence_after();
+        const uint32_t a = smem_u32(sA2 + b * L.a2_bytes);
+        for (int mb = 0; mb < L.mb2; ++mb) {
+          const uint32_t d =
+              tmem_base + static_cast<uint32_t>(2 * L.tmem_c1 + b * L.tmem_c2 + mb * L.c2);
+          for (int t = 0; t < 9; ++t) {
+            // Output row q reads grid row q + (dh * pad + dw) at tap (dh, dw).
+            const int o = (t / 3 - 1) * L.pad + (t % 3 - 1);
+            const uint32_t arow = a + static_cast<uint32_t>((kMargin + mb * 128 + o) * 16);
+            const uint32_t brow = w2a + static_cast<uint32_t>(t * kp * L.c2 * 16);
+            for (int j = 0; j < kp / 2; ++j)
+              umma_bf16(d, sdesc_planar(arow + 2u * j * L.a2_plane, L.a2_plane),
+                        sdesc_planar(brow + static_cast<uint32_t>(2 * j * L.c2 * 16),
+                                     static_cast<uint32_t>(L.c2 * 16)),
+                        id2, (t | j) != 0);
+          }
+        }
+        umma_commit(&a2_empty[b]);
+        umma_commit(&c2_full[b]);
+      };
+      // conv1 runs one tile ahead of conv2 (conv2 of tile k waits for the
+      // conv1 epilogue of tile k, which overlaps conv1 of tile k+1).
+      for (int k = 0; k < my_tiles; ++k) {
+        conv1(k);
+        if (k > 0) conv2(k - 1);
+      }
+      if (my_tiles > 0) conv2(my_tiles - 1);
+    }
+  } else if (warp < 6) {
+    // --------------------------------------- im2col builders + conv1 epilogue
+    const int ta = threadIdx.x - 64;  // 0..127
+    const int q = warp & 3;
+    const uint32_t lane_field = static_cast<uint32_t>(q * 32) << 16;
+    auto build = [&](int k) {
+      const int st = k % L.raw_stages;
+      const uint32_t ru = static_cast<uint32_t>(k / L.raw_stages) & 1u;
+      const int b = k & 1;
+      const uint32_t u = static_cast<uint32_t>(k >> 1) & 1u;
+      mbar_wait(&raw_full[st], ru);
+      mbar_wait(&a1_empty[b], u ^ 1u);
+      const uint8_t* raw = sRaw + st * L.raw_stride;
+      uint8_t* a1 = sA1 + b * L.a1_bytes;
+      const int rows = L.T * G2;
+      for (int r = ta; r < rows; r += 128) {
+        const int n = r / G2, p = r % G2, i = p / L.G, j = p % L.G;
+        // Patch row a of pixel block (i, j): 4 bf16 = 8 bytes, K index a*4 + b.
+        const uint8_t* src = raw + (static_cast<size_t>(n) * L.S * L.S + (4 * i) * L.S + 4 * j) * 2;
+        const uint2 v0 = *reinterpret_cast<const uint2*>(src);
+        const uint2 v1 = *reinterpret_cast<const uint2*>(src + L.S * 2);
+        const uint2 v2 = *reinterpret_cast<const uint2*>(src + L.S * 4);
+        const uint2 v3 = *reinterpret_cast<const uint2*>(src + L.S * 6);
+        *reinterpret_cast<uint4*>(a1 + r * 16) = make_uint4(v0.x, v0.y, v1.x, v1.y);
+        *reinterpret_cast<uint4*>(a1 + L.a1_plane + r * 16) = make_uint4(v2.x, v2.y, v3.x, v3.y);
+      }
+      fence_proxy_async_smem();
+      mbar_arrive(&raw_empty[st]);
+      mbar_arrive(&a1_full[b]);
+    };
+    auto epi1 = [&](int k) {
+      const int b = k & 1;
+      const uint32_t u = static_cast<uint32_t>(k >> 1) & 1u;
+      mbar_wait(&c1_full[b], u);
+      mbar_wait(&a2_empty[b], u ^ 1u);
+      tc_fence_after();
+      uint8_t* a2 = sA2 + b * L.a2_bytes;
+      const int rows = L.T * G2;
+      for (int mb = 0; mb < L.mb1; ++mb) {
+        const int r = mb * 128 + q * 32 + lane;
+        const int n = r / G2, p = r % G2, i = p / L.G, j = p % L.G;
+        const int grow = kMargin + n * P2 + (i + 1) * L.pad + (j + 1);
+        for (int c0 = 0; c0 < L.c1; c0 += 32) {
+          uint32_t v[32];
+          tmem_ld32_raw(tmem_base + lane_field + static_cast<uint32_t>(b * L.tmem_c1 + mb * L.c1 + c0), v);
+          tmem_ld_wait();
+          if (r < rows) {
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+              const int c = g * 8;
+              const float* bias = sB1 + c0 + c;
+              const uint4 pk = make_uint4(pack_relu_bf16(v[c], v[c + 1], bias[0], bias[1]),
+                                          pack_relu_bf16(v[c + 2], v[c + 3], bias[2], bias[3]),
+                                          pack_relu_bf16(v[c + 4], v[c + 5], bias[4], bias[5]),
+                                          pack_relu_bf16(v[c + 6], v[c + 7], bias[6], bias[7]));
+              *reinterpret_cast<uint4*>(a2 + (c0 / 8 + g) * L.a2_plane + grow * 16) = pk;
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&c1_empty[b]);
+      fence_proxy_async_smem();
+      mbar_arrive(&a2_full[b]);
+    };
+    if (my_tiles > 0) build(0);
+    for (int k = 0; k < my_tiles; ++k) {
+      if (k + 1 < my_tiles) build(k + 1);
+      epi1(k);
+    }
+  } else {
+    // ------------------------------------------------------- conv2 epilogue
+    const int q = warp & 3;
+    const uint32_t lane_field = static_cast<uint32_t>(q * 32) << 16;
+    const int row_bytes = G2 * L.c2 * 2;
+    for (int k = 0; k < my_tiles; ++k) {
+      const int b = k & 1;
+      const uint32_t u = static_cast<uint32_t>(k >> 1) & 1u;
+      mbar_wait(&c2_full[b], u);
+      tc_fence_after();
+      const long long s0 = args.row_begin + (blockIdx.x + static_cast<long long>(k) * gridDim.x) * L.T;
+      for (int mb = 0; mb < L.mb2; ++mb) {
+        const int r = mb * 128 + q * 32 + lane;  // padded-grid row of the tile
+        const int n = r / P2, rr = r % P2, h = rr / L.pad, w = rr % L.pad;
+        const bool valid = r < L.T * P2 && h >= 1 && h <= L.G && w >= 1 && w <= L.G &&
+                           s0 + n < args.row_end;
+        uint8_t* dst = static_cast<uint8_t*>(args.out) + (s0 + n) * row_bytes +
+                       ((h - 1) * L.G + (w - 1)) * L.c2 * 2;
+        for (int c0 = 0; c0 < L.c2; c0 += 32) {
+          uint32_t v[32];
+          tmem_ld32_raw(tmem_base + lane_field +
+                            static_cast<uint32_t>(2 * L.tmem_c1 + b * L.tmem_c2 + mb * L.c2 + c0),
+                        v);
+          tmem_ld_wait();
+          if (valid) {
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+              const int c = g * 8;
+              const float* bias = sB2 + c0 + c;
+              const uint4 pk = make_uint4(pack_relu_bf16(v[c], v[c + 1], bias[0], bias[1]),
+                                          pack_relu_bf16(v[c + 2], v[c + 3], bias[2], bias[3]),
+                                          pack_relu_bf16(v[c + 4], v[c + 5], bias[4], bias[5]),
+                                          pack_relu_bf16(v[c + 6], v[c + 7], bias[6], bias[7]));
+              *reinterpret_cast<uint4*>(dst + (c0 + c) * 2) = pk;
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&c2_empty[b]);
+    }
+  }
+
+  __syncthreads();
+  if (warp == 1) {
+    __syncwarp();
+    tc_fence_after();
+    tmem_dealloc(tmem_base, static_cast<uint32_t>(L.tmem_cols));
+  }
+}
+
+uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace
+
+bool conv_plan(int S, int P, int c1, int c2, ConvLayout* out) {
+  if (P != 4 || S < P || S % P != 0 || (S * S) % 16 != 0) return false;
+  if (c1 < 32 || c1 % 32 != 0 || c1 > 256 || c2 < 32 || c2 % 32 != 0 || c2 > 256) return false;
+  ConvLayout L;
+  L.S = S;
+  L.P = P;
+  L.G = S / P;
+  L.c1 = c1;
+  L.c2 = c2;
+  L.pad = L.G + 2;
+  if (L.pad + 1 > kMargin) return false;
+  const int P2 = L.pad * L.pad, G2 = L.G * L.G;
+  for (int T = std::max(1, 256 / P2); T >= 1; --T) {
+    L.T = T;
+    L.mb1 = (T * G2 + 127) / 128;
+    L.mb2 = (T * P2 + 127) / 128;
+    if (T * S * S / 16 > 256) continue;  // TMA box rows
+    L.tmem_c1 = L.mb1 * c1;
+    L.tmem_c2 = L.mb2 * c2;
+    const int cols = 2 * (L.tmem_c1 + L.tmem_c2);
+    if (cols > 512) continue;
+    int tc = 32;
+    while (tc < cols) tc <<= 1;
+    L.tmem_cols = tc;
+    L.raw_stages = 4;
+    L.raw_stride = align_up(static_cast<uint32_t>(T * S * S * 2), 128);
+    L.a1_plane = static_cast<uint32_t>(L.mb1 * 128 * 16);
+    L.a1_bytes = 2 * L.a1_plane;
+    L.a2_rows = static_cast<uint32_t>(kMargin + L.mb2 * 128 + kMargin);
+    L.a2_plane = L.a2_rows * 16;
+    L.a2_bytes = static_cast<uint32_t>(c1 / 8) * L.a2_plane;
+    L.off_raw = 0;
+    L.off_a1 = align_up(L.off_raw + L.raw_stages * L.raw_stride, 128);
+    L.off_a2 = align_up(L.off_a1 + 2 * L.a1_bytes, 128);
+    L.off_w1 = align_up(L.off_a2 + 2 * L.a2_bytes, 128);
+    L.off_w2 = align_up(L.off_w1 + static_cast<uint32_t>(c1 * 32), 128);
+    L.off_b1 = align_up(L.off_w2 + static_cast<uint32_t>(9 * c1 * c2 * 2), 16);
+    L.off_b2 = align_up(L.off_b1 + static_cast<uint32_t>(c1 * 4), 16);
+    L.off_bar = align_up(L.off_b2 + static_cast<uint32_t>(c2 * 4), 8);
+    const uint32_t bars = static_cast<uint32_t>(2 * L.raw_stages + 16) * 8u + 16u;
+    L.smem_bytes = L.off_bar + bars + 1024u;  // + alignment slack of the dynamic base
+    if (L.smem_bytes > kSmemBudget) continue;
+    *out = L;
+    return true;
+  }
+  return false;
+}
+
+int conv_launch(const ConvArgs& args, const void* x, long long x_rows, int grid, cudaStream_t stream) {
+  const ConvLayout& L = args.L;
+  const long long rows16 = x_rows * (L.S * L.S / 16);
+  if (rows16 > INT_MAX) return -1;
+  CUtensorMap mx;
+  if (make_bf16_map_plain(&mx, x, 16, static_cast<uint64_t>(rows16),
+                          static_cast<uint32_t>(L.T * L.S * L.S / 16)) != 0)
+    return -1;
+  if (ensure_smem_attr(conv_stack_sm100, static_cast<int>(kSmemBudget)) != 0) return -4;
+  const long long tiles = (args.row_end - args.row_begin + L.T - 1) / L.T;
+  if (tiles <= 0) return 0;
+  grid = static_cast<int>(std::min<long long>(grid, tiles));
+  conv_stack_sm100<<<grid, kThreads, L.smem_bytes, stream>>>(mx, args);
+  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+
+}  // namespace es

@@ -1,0 +1,59 @@
+// Convolution stack of the CNN member on sm_100a tensor cores.
+//
+//   x [S*S] (one channel)  --conv P x P, stride P, c1 filters, +b, ReLU-->
+//   a1 [G][G][c1]          --conv 3 x 3, pad 1, c2 filters, +b, ReLU-->
+//   a2 [G][G][c2] (bf16, HWC order: the fused member_mlp2 head's input row)
+//
+// Both convolutions are implicit GEMMs on tcgen05 inside ONE persistent kernel;
+// the c1-channel intermediate never leaves shared memory:
+//   * a tile is T whole samples, so no halo crosses tiles;
+//   * conv1: TMA brings the raw images; builder warps write the im2col rows
+//     (one row per output pixel, K = P*P) into a K-major planar operand; one
+//     UMMA (M=128, N=c1, K=16) per 128 rows;
+//   * conv1's epilogue writes relu(acc+b) as bf16 into a zero-bordered
+//     (G+2) x (G+2) grid per sample, again K-major planar (channels = K);
+//   * conv2: output pixel q (in padded coordinates) at tap (dh, dw) reads row
+//     q + dh*(G+2) + dw of that grid, so each of the 9 taps is the SAME operand
+//     with the descriptor start moved by whole rows (16 B each) -- nine
+//     accumulating UMMAs per K step, no im2col copy, no re-read from memory;
+//   * conv2's epilogue keeps the G x G interior and stores bf16 rows to HBM.
+// Every operand is K-major without swizzle (sdesc_planar in sm100.cuh).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace es {
+
+struct ConvLayout {
+  int S = 28, P = 4, G = 7, c1 = 64, c2 = 32;
+  int pad = 9;           // G + 2: side of the zero-bordered grid
+  int T = 3;             // samples per tile
+  int mb1 = 2, mb2 = 2;  // 128-row M blocks of conv1 / conv2
+  int raw_stages = 4;
+  uint32_t raw_stride = 0;                     // bytes per raw image stage
+  uint32_t a1_plane = 0, a1_bytes = 0;         // conv1 operand: [2 planes][mb1*128][16 B]
+  uint32_t a2_rows = 0, a2_plane = 0, a2_bytes = 0;  // [c1/8 planes][a2_rows][16 B]
+  uint32_t off_raw = 0, off_a1 = 0, off_a2 = 0, off_w1 = 0, off_w2 = 0, off_b1 = 0, off_b2 = 0;
+  uint32_t off_bar = 0, smem_bytes = 0;
+  int tmem_c1 = 0, tmem_c2 = 0, tmem_cols = 0;  // columns per buffer, total allocation
+};
+
+struct ConvArgs {
+  ConvLayout L;
+  long long row_begin = 0, row_end = 0;  // samples handled by this launch
+  const void* w1 = nullptr;              // bf16 [c1][P*P]
+  const float* b1 = nullptr;
+  const void* w2 = nullptr;  // bf16 [c2][9*c1], K index = tap*c1 + channel, tap = 3*(dh+1)+(dw+1)
+  const float* b2 = nullptr;
+  void* out = nullptr;  // bf16 [rows][G*G*c2]
+};
+
+// False when the shape has no plan (P != 4, S % P, channel counts not
+// multiples of 32, grids larger than 13 x 13).
+bool conv_plan(int S, int P, int c1, int c2, ConvLayout* out);
+// x: bf16 [x_rows][S*S].
+int conv_launch(const ConvArgs& args, const void* x, long long x_rows, int grid, cudaStream_t stream);
+
+}  // namespace es

@@ -181,6 +181,20 @@ __device__ __forceinline__ uint64_t sdesc_k128(uint32_t smem_addr) {
   return d;
 }
 
+// K-major, no swizzle, "planar" layout: K split into 8-element (16 B) planes,
+// each plane [rows][16 B] contiguous, so 8-row core matrices sit 128 B apart
+// (SBO) and the second K core matrix of a K=16 step one plane further (LBO).
+// Rows are uniformly 16 B apart, so the start address may move by single rows
+// (implicit-GEMM tap shifts, conv_kernel.cu).
+__device__ __forceinline__ uint64_t sdesc_planar(uint32_t smem_addr, uint32_t plane_bytes) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((smem_addr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>((plane_bytes >> 4) & 0x3FFFu) << 16;  // LBO: next K core matrix
+  d |= static_cast<uint64_t>(128u >> 4) << 32;                     // SBO: next 8 rows
+  d |= static_cast<uint64_t>(1u) << 46;
+  return d;  // layout type 0: SWIZZLE_NONE
+}
+
 // 32 lanes x 32 bits x 16 columns: thread i of the warp gets TMEM lane
 // (lane_base + i), columns [col, col+16).
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {

@@ -9,6 +9,7 @@
 #include <cstring>
 
 #include "../cuda/aux_kernels.cuh"
+#include "../cuda/conv_kernel.cuh"
 #include "../cuda/dense_kernel.cuh"
 #include "../cuda/mlp_kernel.cuh"
 #include "../cuda/mlp_pair_kernel.cuh"
@@ -54,16 +55,19 @@ struct DeviceMember::Impl {
   ModelSpec model;
   int batch = 1;
   int C = 1;
-  std::vector<int> widths;
+  std::vector<std::pair<int, int>> dims;  // (fan_in, fan_out) per weight matrix
   enum class Head { Synthetic, SwapAB, Tmem, Pair } head = Head::Synthetic;
   es::Mlp2Layout plan_swapab{};
   es::MlpTLayout plan_tmem{};
   es::MlpPLayout plan_pair{};
-  std::vector<es::DenseLayout> dense;  // plans of the leading layers
+  std::vector<es::DenseLayout> dense;  // MLP: plans of the leading layers
+  bool cnn = false;
+  es::ConvLayout conv{};  // CNN: the convolution stack (layers 0 and 1)
   void* weights = nullptr;
   std::vector<std::size_t> w_off, b_off;  // per layer
-  // Activations of the leading layers, bf16 [rows][width], indexed like X.
+  // Outputs of the leading layers, bf16 [rows][width], indexed like X.
   std::vector<void*> act;
+  std::vector<int> act_width;
   std::vector<std::size_t> act_rows;
 };
 
@@ -94,21 +98,31 @@ bool DeviceMember::load(int device, const ModelSpec& model, int batch) {
   I.C = model.output_width;
   if (model.arch.kind == MemberArch::Kind::Synthetic) return true;
   const MemberArch& a = model.arch;
-  const int L = a.layers();
-  if (L < 2) throw SpecError(model.name + ": an MLP member needs at least two layers");
-  I.widths = a.widths;
-  // Leading layers: tcgen05 dense layers with a bf16 output.
-  for (int l = 0; l < L - 2; ++l) {
-    es::DenseLayout d;
-    if (!es::dense_plan(a.widths[l], a.widths[l + 1], true, &d))
-      throw SpecError(model.name + ": leading layer " + std::to_string(a.widths[l]) + "->" +
-                      std::to_string(a.widths[l + 1]) +
-                      " has no tile plan (input width a multiple of 8, output width a "
-                      "multiple of 128 up to 512)");
-    I.dense.push_back(d);
+  I.dims = a.layer_dims();
+  const int L = static_cast<int>(I.dims.size());
+  if (L < 2) throw SpecError(model.name + ": a member needs at least two layers");
+  if (a.kind == MemberArch::Kind::CNN) {
+    // Leading layers: the fused convolution stack, bf16 [(S/P)^2 * c2] rows out.
+    I.cnn = true;
+    if (!es::conv_plan(a.widths[0], a.widths[1], a.widths[2], a.widths[3], &I.conv))
+      throw SpecError(model.name + ": CNN shape has no tile plan (patch 4, image side a "
+                      "multiple of 4 up to 52, conv channels multiples of 32 up to 256)");
+    I.act_width.push_back(I.dims[2].first);
+  } else {
+    // Leading layers: tcgen05 dense layers with a bf16 output.
+    for (int l = 0; l < L - 2; ++l) {
+      es::DenseLayout d;
+      if (!es::dense_plan(I.dims[l].first, I.dims[l].second, true, &d))
+        throw SpecError(model.name + ": leading layer " + std::to_string(I.dims[l].first) + "->" +
+                        std::to_string(I.dims[l].second) +
+                        " has no tile plan (input width a multiple of 8, output width a "
+                        "multiple of 128 up to 512)");
+      I.dense.push_back(d);
+      I.act_width.push_back(I.dims[l].second);
+    }
   }
   // Fused head over the last two layers.
-  const int K = a.widths[L - 2], H = a.widths[L - 1], C = a.widths[L];
+  const int K = I.dims[L - 2].first, H = I.dims[L - 2].second, C = I.dims[L - 1].second;
   const char* pick = std::getenv("ES_MLP_KERNEL");
   const std::string want = pick ? pick : "";
   const bool pair_ok = (want.empty() || want == "pair") && es::mlpp_plan(K, H, C, batch, &I.plan_pair);
@@ -130,9 +144,9 @@ bool DeviceMember::load(int device, const ModelSpec& model, int batch) {
   std::size_t off = 0;
   for (int l = 0; l < L; ++l) {
     I.w_off.push_back(off);
-    off += up(static_cast<std::size_t>(a.widths[l]) * a.widths[l + 1] * 2);
+    off += up(static_cast<std::size_t>(I.dims[l].first) * I.dims[l].second * 2);
     I.b_off.push_back(off);
-    off += up(static_cast<std::size_t>(a.widths[l + 1]) * 4);
+    off += up(static_cast<std::size_t>(I.dims[l].second) * 4);
   }
   bytes_ = off;
   cudaError_t e = cudaMalloc(&I.weights, bytes_);
@@ -144,14 +158,14 @@ bool DeviceMember::load(int device, const ModelSpec& model, int batch) {
   M_CUDA(e);
   uint8_t* base = static_cast<uint8_t*>(I.weights);
   for (int l = 0; l < L; ++l) {
-    const int fi = a.widths[l], fo = a.widths[l + 1];
+    const int fi = I.dims[l].first, fo = I.dims[l].second;
     const float limit = static_cast<float>(std::sqrt(6.0 / static_cast<double>(fi + fo)));
     M_LAUNCH(es::generate_dense_layer(a.weight_seed, l, fi, fo, limit,
                                       reinterpret_cast<__nv_bfloat16*>(base + I.w_off[l]),
                                       reinterpret_cast<float*>(base + I.b_off[l]), 0));
   }
-  I.act.assign(L - 2, nullptr);
-  I.act_rows.assign(L - 2, 0);
+  I.act.assign(I.act_width.size(), nullptr);
+  I.act_rows.assign(I.act_width.size(), 0);
   M_CUDA(cudaDeviceSynchronize());
   return true;
 }
@@ -165,17 +179,33 @@ int DeviceMember::forward(const void* x, long long nb, int seg_size, long long s
     return 1;
   }
   const uint8_t* base = static_cast<const uint8_t*>(I.weights);
-  const int L = static_cast<int>(I.widths.size()) - 1;
+  const int L = static_cast<int>(I.dims.size());
   const long long r0 = s0 * seg_size, r1 = std::min<long long>(s1 * seg_size, nb);
   int launches = 0;
   const void* cur = x;
-  for (int l = 0; l < L - 2; ++l) {
+  for (std::size_t l = 0; l < I.act.size(); ++l) {
     if (I.act_rows[l] < static_cast<std::size_t>(nb)) {
       cudaFree(I.act[l]);
       I.act[l] = nullptr;
-      M_CUDA(cudaMalloc(&I.act[l], static_cast<std::size_t>(nb) * I.widths[l + 1] * 2));
+      M_CUDA(cudaMalloc(&I.act[l], static_cast<std::size_t>(nb) * I.act_width[l] * 2));
       I.act_rows[l] = static_cast<std::size_t>(nb);
     }
+  }
+  if (I.cnn) {
+    es::ConvArgs c;
+    c.L = I.conv;
+    c.row_begin = r0;
+    c.row_end = r1;
+    c.w1 = base + I.w_off[0];
+    c.b1 = reinterpret_cast<const float*>(base + I.b_off[0]);
+    c.w2 = base + I.w_off[1];
+    c.b2 = reinterpret_cast<const float*>(base + I.b_off[1]);
+    c.out = I.act[0];
+    M_LAUNCH(es::conv_launch(c, cur, nb, grid, stream));
+    ++launches;
+    cur = I.act[0];
+  }
+  for (std::size_t l = 0; l < I.dense.size(); ++l) {
     es::DenseArgs d;
     d.L = I.dense[l];
     d.row_begin = r0;
@@ -191,8 +221,8 @@ int DeviceMember::forward(const void* x, long long nb, int seg_size, long long s
   const void* w1 = base + I.w_off[h];
   const void* w2 = base + I.w_off[h + 1];
   if (env_is("ES_MEMBER_KERNEL", "simt")) {
-    M_LAUNCH(es::mlp2_simt_launch(static_cast<const __nv_bfloat16*>(cur), nb, I.widths[h],
-                                  static_cast<const __nv_bfloat16*>(w1), b1, I.widths[h + 1],
+    M_LAUNCH(es::mlp2_simt_launch(static_cast<const __nv_bfloat16*>(cur), nb, I.dims[h].first,
+                                  static_cast<const __nv_bfloat16*>(w1), b1, I.dims[h].second,
                                   static_cast<const __nv_bfloat16*>(w2), b2, I.C, r0, r1, out,
                                   stream));
     return launches + 1;

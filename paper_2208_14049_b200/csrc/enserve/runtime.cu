@@ -376,8 +376,9 @@ void InferenceSystem::begin_run(std::shared_ptr<const SampleStore> X, Combinatio
       rule.weights.size() != static_cast<std::size_t>(cluster_.model_count()))
     throw SpecError("weighted averaging needs one weight per model");
   for (const ModelSpec& m : cluster_.models)
-    if (m.arch.kind == MemberArch::Kind::MLP && static_cast<std::size_t>(m.arch.widths[0]) != X->width())
-      throw SpecError(m.name + ": input width " + std::to_string(m.arch.widths[0]) +
+    if (m.arch.kind != MemberArch::Kind::Synthetic &&
+        static_cast<std::size_t>(m.arch.input_width()) != X->width())
+      throw SpecError(m.name + ": input width " + std::to_string(m.arch.input_width()) +
                       " differs from the store's " + std::to_string(X->width()));
   const std::size_t nb = X->nb_samples();
   const int C = output_width_;
@@ -529,7 +530,8 @@ double InferenceSystem::run_host(const float* X, std::size_t nb, std::size_t wid
     if (w->phys != combine_dev_) throw SpecError("run_host needs every worker on one GPU");
   if (run_open_) throw Error("previous run still open");
   for (const ModelSpec& m : cluster_.models)
-    if (m.arch.kind == MemberArch::Kind::MLP && static_cast<std::size_t>(m.arch.widths[0]) != width)
+    if (m.arch.kind != MemberArch::Kind::Synthetic &&
+        static_cast<std::size_t>(m.arch.input_width()) != width)
       throw SpecError(m.name + ": input width differs from the samples'");
   OnDevice on(combine_dev_);
   Impl& I = *impl_;
@@ -826,14 +828,12 @@ void combine_blocks(const CombinationRule& rule, int M, int C, std::size_t rows,
 }
 
 void derive_footprint(ModelSpec& model) {
-  if (model.arch.kind != MemberArch::Kind::MLP) return;
+  if (model.arch.kind == MemberArch::Kind::Synthetic) return;
   constexpr double kMiB = 1024.0 * 1024.0;
   if (model.weight_mib <= 0)
     model.weight_mib = static_cast<double>(model.arch.parameter_count()) * 2.0 / kMiB;
   if (model.act_mib_per_sample <= 0) {
-    double per = 0.0;
-    for (int w : model.arch.widths) per += w * 2.0;
-    model.act_mib_per_sample = per / kMiB;
+    model.act_mib_per_sample = model.arch.activation_elems() * 2.0 / kMiB;
   }
   if (model.cost_per_sample <= 0) model.cost_per_sample = model.arch.flops_per_sample();
 }

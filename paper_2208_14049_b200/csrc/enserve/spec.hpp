@@ -14,6 +14,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 namespace enserve {
@@ -69,14 +70,23 @@ struct DeviceSpec {
 //    between layers, bf16 operands with fp32 accumulation.  Weights are
 //    synthetic Glorot-uniform keyed by weight_seed.
 struct MemberArch {
-  enum class Kind { Synthetic, MLP };
+  // MLP: widths = {input, hidden..., classes}.
+  // CNN: widths = {S, P, c1, c2, hidden, classes}: an S x S one-channel image,
+  //   conv P x P stride P -> c1, conv 3 x 3 pad 1 -> c2 (both ReLU), then
+  //   dense (S/P)^2*c2 -> hidden (ReLU) -> classes.
+  enum class Kind { Synthetic, MLP, CNN };
   Kind kind = Kind::Synthetic;
   std::vector<int> widths;
   std::uint64_t weight_seed = 0;
 
-  int layers() const { return widths.empty() ? 0 : static_cast<int>(widths.size()) - 1; }
+  // Weight matrices [fan_out][fan_in] in generation order (layer index =
+  // position); the CNN's convolutions are matrices over their im2col rows.
+  std::vector<std::pair<int, int>> layer_dims() const;  // (fan_in, fan_out)
+  int layers() const { return static_cast<int>(layer_dims().size()); }
+  int input_width() const;
   std::size_t parameter_count() const;
-  double flops_per_sample() const;  // 2 * sum(fan_in * fan_out)
+  double flops_per_sample() const;  // 2 * MACs per sample
+  double activation_elems() const;  // elements each sample touches, input included
 };
 
 struct ModelSpec {

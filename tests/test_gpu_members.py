@@ -50,3 +50,56 @@ def test_heterogeneous_depths_in_one_ensemble_match_reference_pipeline():
     clear = gap > 2e-3
     np.testing.assert_array_equal(out.winners[clear], top[clear, 1])
     assert np.all((out.winners == top[:, 1]) | (out.winners == top[:, 0]))
+
+
+# ------------------------------------------------------------------ K2 CNN
+CNN_SHAPES = [(28, 4, 64, 32, 128, 10), (28, 4, 32, 64, 256, 10), (16, 4, 64, 32, 128, 10)]
+
+
+@pytest.mark.parametrize("shape", CNN_SHAPES)
+@pytest.mark.parametrize("b", [32, 128])
+def test_cnn_member_matches_cpu_oracle(shape, b):
+    S = shape[0]
+    X = refcpu.features(43, 500, S * S)  # 500 = 166 tiles of 3 samples + 2
+    model = es.cnn_model(0, "cnn", 77, S=shape[0], P=shape[1], c1=shape[2], c2=shape[3],
+                         hidden=shape[4], classes=shape[5])
+    got = es.Member(model, b).predict(X)
+    cpu = refcpu.CpuCnn(shape, 77)
+    want = cpu.forward(X)
+    # Three bf16-rounded activation layers (conv1, conv2, hidden).
+    assert_logits_close(got, want, cpu.logit_scale(X), rtol=RTOL_BF16 * 3)
+    np.testing.assert_array_equal(np.argmax(got, 1), np.argmax(want, 1))
+
+
+@pytest.mark.parametrize("first", [0, 1, 5])
+def test_cnn_member_rows_are_independent_of_the_call_window(first):
+    """A window starting mid-tile and ending ragged gives the same rows as the
+    whole batch (backend.hpp:43-45: output depends on the sample only)."""
+    X = refcpu.features(44, 200, 784)
+    m = es.Member(es.cnn_model(0, "cnn", 78), 64)
+    whole = m.predict(X)
+    part = m.predict(X[first:first + 67], first_index=first)
+    np.testing.assert_array_equal(part, whole[first:first + 67])
+
+
+def test_cnn_in_data_parallel_ensemble_matches_reference_pipeline():
+    """The cfg2 shape: MLP and CNN members co-located, the CNN data-parallel
+    across two devices mapped onto one GPU (segment ranges split mid-image-
+    tile), against the reference runtime driving the oracle members."""
+    if not refcpu.ref_available():
+        pytest.skip("oracle/_ref not built")
+    models = [es.mlp_model(0, "mlp256", [784, 256, 10], 1),
+              es.mlp_model(1, "mlp512x2", [784, 512, 512, 10], 2),
+              es.mlp_model(2, "mlp384", [784, 384, 10], 3),
+              es.cnn_model(3, "cnn-s", 4)]
+    c = es.ClusterSpec([gpu(0, 180000.0, 1e15, 0.0), gpu(1, 180000.0, 1e15, 0.0)], models,
+                       [8, 16, 32, 64, 128], 128)
+    A = es.AllocationMatrix.from_array([[128, 64, 128, 32], [0, 0, 0, 128]])
+    X = refcpu.features(79, 128 * 7 + 61, 784)
+    out = es.run_inference(es.SampleStore(X), A, c, es.CombinationRule.averaging(softmax=True))
+    Yr, _, _ = refcpu.ref_run_ensemble(c, A.cells, X, rule=0, softmax=True)
+    np.testing.assert_allclose(out.combined, Yr, rtol=0, atol=1e-3)
+    top = np.argsort(Yr, axis=1)[:, -2:]
+    gap = np.take_along_axis(Yr, top[:, 1:], 1)[:, 0] - np.take_along_axis(Yr, top[:, :1], 1)[:, 0]
+    clear = gap > 2e-3
+    np.testing.assert_array_equal(out.winners[clear], top[clear, 1])

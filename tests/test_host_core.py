@@ -81,6 +81,24 @@ def test_cluster_validation():
     assert len(c.validate()) == 1
 
 
+def test_cnn_member_spec_and_footprint():
+    m = es.cnn_model(0, "cnn-s", 4)
+    # conv 4x4/4 (16->64) and 3x3 (576->32) applied at 49 pixels, dense 1568->128->10.
+    assert m.arch.layer_dims() == [(16, 64), (576, 32), (1568, 128), (128, 10)]
+    assert m.arch.input_width() == 784
+    assert m.cost_per_sample == 2 * (49 * 16 * 64 + 49 * 576 * 32 + 1568 * 128 + 128 * 10)
+    assert m.arch.parameter_count() == 16 * 64 + 64 + 576 * 32 + 32 + 1568 * 128 + 128 + 1290
+    c = es.ClusterSpec([es.DeviceSpec(0, es.GPU, 1000.0, 1.0, 0.0)], [m], [8, 16], 128)
+    assert c.validate() == []
+    bad = es.cnn_model(0, "cnn-bad", 4, S=30)  # patch 4 does not divide 30
+    with pytest.raises(es.SpecError):
+        es.ClusterSpec([es.DeviceSpec(0, es.GPU, 1000.0, 1.0, 0.0)], [bad], [8], 128).validate()
+    wrong_c = es.cnn_model(0, "cnn-c", 4)
+    wrong_c.output_width = 7
+    with pytest.raises(es.SpecError):
+        es.ClusterSpec([es.DeviceSpec(0, es.GPU, 1000.0, 1.0, 0.0)], [wrong_c], [8], 128).validate()
+
+
 # ------------------------------------------------------------- test_memory.cpp
 def test_memory_model():
     c = es.ClusterSpec([gpu(0, 16000.0)], [model(0, "a", 1000.0, 10.0), model(1, "b", 500.0, 2.0)],

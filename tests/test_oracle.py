@@ -217,3 +217,48 @@ def test_cpu_member_matches_float64_reference_within_bf16_tolerance():
     scale = np.abs(z).max(axis=1, keepdims=True)
     assert np.max(np.abs(got - z) / scale) < 2e-3  # bf16 hidden re-rounding dominates
     assert (np.argmax(got, 1) == np.argmax(z, 1)).mean() > 0.98
+
+
+def _cnn_numpy(cnn, x):
+    """The CNN member's definition (cpu_member.h) written directly in numpy:
+    patch convolution, zero-padded 3x3 convolution over HWC activations, HWC
+    flatten, two dense layers; bf16 rounding of X, weights and activations."""
+    S, P, c1, c2, hidden, _ = cnn.widths
+    G = S // P
+    w0, b0 = cnn.layer(0)
+    w1, b1 = cnn.layer(1)
+    w2, b2 = cnn.layer(2)
+    w3, b3 = cnn.layer(3)
+    q = refcpu.round_bf16
+    img = q(x.reshape(S, S).astype(np.float32)).astype(np.float64)
+    patches = img.reshape(G, P, G, P).transpose(0, 2, 1, 3).reshape(G, G, P * P)
+    a1 = q(np.maximum(patches @ w0.T + b0, 0).astype(np.float32)).astype(np.float64)
+    pad = np.zeros((G + 2, G + 2, c1))
+    pad[1:G + 1, 1:G + 1] = a1
+    cols = np.concatenate([pad[dh:dh + G, dw:dw + G] for dh in range(3) for dw in range(3)], axis=2)
+    a2 = q(np.maximum(cols @ w1.T + b1, 0).astype(np.float32)).astype(np.float64)
+    h = q(np.maximum(a2.reshape(-1) @ w2.T + b2, 0).astype(np.float32)).astype(np.float64)
+    return h @ w3.T + b3
+
+
+@pytest.mark.parametrize("widths", [(28, 4, 64, 32, 128, 10), (16, 4, 32, 64, 64, 7)])
+def test_cpu_cnn_member_matches_numpy_definition(widths):
+    cnn = refcpu.CpuCnn(widths, seed=5)
+    X = refcpu.features(3, 6, widths[0] * widths[0])
+    got = cnn.forward(X)
+    want = np.stack([_cnn_numpy(cnn, x) for x in X])
+    # Same quantisation points; fp32-vs-float64 accumulation can still flip a
+    # bf16 activation rounding, so the bound is the MLP test's (2e-3 of the row).
+    scale = np.abs(want).max(axis=1, keepdims=True)
+    assert np.max(np.abs(got - want) / scale) < 2e-3
+    np.testing.assert_array_equal(np.argmax(got, 1), np.argmax(want, 1))
+
+
+def test_cpu_cnn_weights_use_the_shared_generator():
+    cnn = refcpu.CpuCnn((28, 4, 64, 32, 128, 10), seed=9)
+    for layer, (fi, fo) in enumerate(cnn.dims):
+        w, b = cnn.layer(layer)
+        for idx in (0, 7, fi * fo - 1):
+            v = refcpu.round_bf16(np.float32(refcpu.orc().orc_weight(9, layer, idx, fi, fo)))
+            assert w.reshape(-1)[idx] == v
+        assert b[0] == np.float32(refcpu.orc().orc_bias(9, layer, 0))
