@@ -16,19 +16,38 @@ using namespace sm100;
 
 namespace {
 
-// w0 TMA producer, w1 UMMA issuer, w2..w5 im2col + conv1 epilogue,
-// w6..w9 conv2 epilogue (each group covers the four TMEM lane quadrants).
+// w0 TMA producer, w1 UMMA issuer, w2..w5 conv1 epilogue, w6..w9 im2col
+// builders + conv2 epilogue (each group covers the four TMEM lane quadrants).
+// Ten warps: extra role warps share the UMMA warp's sub-partition and slow its
+// issue loop down (measured with tools/trace_conv.cu).
 constexpr int kThreads = 320;
 constexpr uint32_t kSmemBudget = 232448;
-constexpr int kMargin = 16;  // rows before/after each padded grid; tap shifts reach pad+1
+constexpr int kMargin = 16;  // zero rows before/after the tile's grids; taps reach R+1 rows
 
+// bf16x2 {relu(a + ba), relu(b + bb)} (a in the low half), one cvt.relu.
 __device__ __forceinline__ uint32_t pack_relu_bf16(uint32_t a, uint32_t b, float ba, float bb) {
-  const float lo = fmaxf(__uint_as_float(a) + ba, 0.0f);
-  const float hi = fmaxf(__uint_as_float(b) + bb, 0.0f);
-  __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
-  return *reinterpret_cast<uint32_t*>(&h);
+  const float lo = __uint_as_float(a) + ba;
+  const float hi = __uint_as_float(b) + bb;
+  uint32_t d;
+  asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+  return d;
 }
 
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Stamp slot i of local tile k (CTA 0 only; slots listed in tools/trace_conv.cu).
+#define TRACE(k, i)                                                                         \
+  do {                                                                                      \
+    if (args.trace && blockIdx.x == 0 && (k) < 32) args.trace[(k) * 16 + (i)] = global_ns(); \
+  } while (0)
+
+// KP2 = c1 / 16: K steps per tap, unrolled so the issue loop is pure uniform
+// adds (tools/umma_rate.cu).
+template <int KP2>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_stack_sm100(const __grid_constant__ CUtensorMap tm_x, const ConvArgs args) {
   extern __shared__ uint8_t smem_raw[];
@@ -54,7 +73,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* c2_empty = c2_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(c2_empty + 2);
 
-  const int warp = threadIdx.x >> 5;
+  const int warp = warp_uniform_id();
   const int lane = threadIdx.x & 31;
   const long long tiles = (args.row_end - args.row_begin + L.T - 1) / L.T;
   const int my_tiles =
@@ -82,7 +101,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) tmem_alloc(tmem_slot, static_cast<uint32_t>(L.tmem_cols));
 
   // Resident operands: weights in the planar K-major layout (plane k of row o
-  // = K elements 8k..8k+7), biases, and both padded grids zeroed once -- the
+  // = K elements 8k..8k+7), biases, and both grid buffers zeroed once -- the
   // conv1 epilogue only ever rewrites interior rows, so borders stay zero.
   {
     const uint4* w1 = static_cast<const uint4*>(args.w1);  // [c1][16] bf16 = 2 chunks per row
@@ -106,7 +125,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int G2 = L.G * L.G, P2 = L.pad * L.pad;
+  const int G2 = L.G * L.G, P2 = L.R * L.R;
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -116,107 +135,102 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int k = 0; k < my_tiles; ++k) {
         const int st = k % L.raw_stages;
         const uint32_t use = static_cast<uint32_t>(k / L.raw_stages);
-        mbar_wait(&raw_empty[st], (use & 1u) ^ 1u);
+        mbar_sleep_wait(&raw_empty[st], (use & 1u) ^ 1u);
         const long long s0 = args.row_begin + (blockIdx.x + static_cast<long long>(k) * gridDim.x) * L.T;
         mbar_arrive_expect_tx(&raw_full[st], static_cast<uint32_t>(L.T * L.S * L.S * 2));
         tma_load_2d(sRaw + st * L.raw_stride, &tm_x, &raw_full[st], 0,
                     static_cast<int32_t>(s0 * rows16), pol);
+        TRACE(k, 0);
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ UMMA issuer
-    if (lane == 0) {
-      const uint32_t id1 = idesc_bf16_f32(128, L.c1), id2 = idesc_bf16_f32(128, L.c2);
-      const uint32_t w1a = smem_u32(sW1), w2a = smem_u32(sW2);
-      const uint64_t w1d = sdesc_planar(w1a, static_cast<uint32_t>(L.c1 * 16));
-      auto conv1 = [&](int k) {
-        const int b = k & 1;
-        const uint32_t u = static_cast<uint32_t>(k >> 1) & 1u;
-        mbar_wait(&a1_full[b], u);
-        mbar_wait(&c1_empty[b], u ^ 1u);
-        tc_fence_after();
-        const uint32_t a = smem_u32(sA1 + b * L.a1_bytes);
-        for (int mb = 0; mb < L.mb1; ++mb)
-          umma_bf16(tmem_base + static_cast<uint32_t>(b * L.tmem_c1 + mb * L.c1),
-                    sdesc_planar(a + static_cast<uint32_t>(mb * 128 * 16), L.a1_plane), w1d, id1, 0);
+    // The whole warp walks the schedule (uniform descriptor arithmetic); one
+    // elected lane issues.  Descriptors advance by adding 16-byte units to
+    // the start-address field: taps move the A start by whole grid rows.
+    // __shfl_sync(.., 0) marks the bases warp-uniform for the compiler.
+    const uint32_t tbase = __shfl_sync(0xffffffffu, tmem_base, 0);
+    const uint32_t a1_base = __shfl_sync(0xffffffffu, smem_u32(sA1), 0);
+    const uint32_t a2_base = __shfl_sync(0xffffffffu, smem_u32(sA2), 0);
+    const uint32_t id1 = idesc_bf16_f32(128, L.c1), id2 = idesc_bf16_f32(128, L.c2);
+    const uint64_t w1d = sdesc_planar(__shfl_sync(0xffffffffu, smem_u32(sW1), 0),
+                                      static_cast<uint32_t>(L.c1 * 16));
+    const uint64_t w2d = sdesc_planar(__shfl_sync(0xffffffffu, smem_u32(sW2), 0),
+                                      static_cast<uint32_t>(L.c2 * 16));
+    const uint32_t a2_step = L.a2_plane / 8;  // two planes (K += 16), in 16-byte units
+    auto conv1 = [&](int k) {
+      const int b = k & 1;
+      const uint32_t u = static_cast<uint32_t>(k >> 1) & 1u;
+      mbar_sleep_wait(&a1_full[b], u);
+      mbar_sleep_wait(&c1_empty[b], u ^ 1u);
+      TRACE(k, 1);
+      tc_fence_after();
+      const uint64_t ad = sdesc_planar(a1_base + b * L.a1_bytes, L.a1_plane);
+      for (int mb = 0; mb < L.mb1; ++mb)
+        if (elect_one())
+          umma_bf16(tbase + static_cast<uint32_t>(b * L.tmem_c1 + mb * L.c1),
+                    ad + static_cast<uint64_t>(mb * 128), w1d, id1, 0);
+      if (elect_one()) {
         umma_commit(&a1_empty[b]);
         umma_commit(&c1_full[b]);
-      };
-      auto conv2 = [&](int k) {
-        const int b = k & 1;
-        const uint32_t u = static_cast<uint32_t>(k >> 1) & 1u;
-        mbar_wait(&a2_full[b], u);
-        mbar_wait(&c2_empty[b], u ^ 1u);
-        tc_fence_after();
-        const uint32_t a = smem_u32(sA2 + b * L.a2_bytes);
-        for (int mb = 0; mb < L.mb2; ++mb) {
-          const uint32_t d =
-              tmem_base + static_cast<uint32_t>(2 * L.tmem_c1 + b * L.tmem_c2 + mb * L.c2);
-          for (int t = 0; t < 9; ++t) {
-            // Output row q reads grid row q + (dh * pad + dw) at tap (dh, dw).
-            const int o = (t / 3 - 1) * L.pad + (t % 3 - 1);
-            const uint32_t arow = a + static_cast<uint32_t>((kMargin + mb * 128 + o) * 16);
-            const uint32_t brow = w2a + static_cast<uint32_t>(t * kp * L.c2 * 16);
-            for (int j = 0; j < kp / 2; ++j)
-              umma_bf16(d, sdesc_planar(arow + 2u * j * L.a2_plane, L.a2_plane),
-                        sdesc_planar(brow + static_cast<uint32_t>(2 * j * L.c2 * 16),
-                                     static_cast<uint32_t>(L.c2 * 16)),
-                        id2, (t | j) != 0);
+      }
+      __syncwarp();
+    };
+    auto conv2 = [&](int k) {
+      const int b = k & 1;
+      const uint32_t u = static_cast<uint32_t>(k >> 1) & 1u;
+      mbar_sleep_wait(&a2_full[b], u);
+      mbar_sleep_wait(&c2_empty[b], u ^ 1u);
+      TRACE(k, 2);
+      tc_fence_after();
+      const uint64_t ad0 = sdesc_planar(a2_base + b * L.a2_bytes, L.a2_plane);
+      for (int mb = 0; mb < L.mb2; ++mb) {
+        const uint32_t d =
+            tbase + static_cast<uint32_t>(2 * L.tmem_c1 + b * L.tmem_c2 + mb * L.c2);
+        const uint64_t adm = ad0 + static_cast<uint64_t>(kMargin + mb * 128);
+#pragma unroll
+        for (int t = 0; t < 9; ++t)
+#pragma unroll
+          for (int j = 0; j < KP2; ++j) {
+            // Output row q reads grid row q + (dh * R + dw) at tap (dh, dw).
+            const uint64_t ad =
+                adm + static_cast<uint64_t>((t / 3 - 1) * L.R + (t % 3 - 1) + j * static_cast<int>(a2_step));
+            const uint64_t bd = w2d + static_cast<uint64_t>((t * KP2 + j) * 2 * L.c2);
+            if (elect_one()) umma_bf16(d, ad, bd, id2, (t | j) != 0);
           }
-        }
+      }
+      if (elect_one()) {
         umma_commit(&a2_empty[b]);
         umma_commit(&c2_full[b]);
-      };
-      // conv1 runs one tile ahead of conv2 (conv2 of tile k waits for the
-      // conv1 epilogue of tile k, which overlaps conv1 of tile k+1).
-      for (int k = 0; k < my_tiles; ++k) {
-        conv1(k);
-        if (k > 0) conv2(k - 1);
       }
-      if (my_tiles > 0) conv2(my_tiles - 1);
+      __syncwarp();
+      TRACE(k, 3);
+    };
+    // conv1 runs one tile ahead of conv2 (conv2 of tile k waits for the
+    // conv1 epilogue of tile k, which overlaps conv1 of tile k+1).
+    for (int k = 0; k < my_tiles; ++k) {
+      conv1(k);
+      if (k > 0) conv2(k - 1);
     }
+    if (my_tiles > 0) conv2(my_tiles - 1);
   } else if (warp < 6) {
-    // --------------------------------------- im2col builders + conv1 epilogue
+    // ------------------------------------------------------- conv1 epilogue
     const int ta = threadIdx.x - 64;  // 0..127
     const int q = warp & 3;
     const uint32_t lane_field = static_cast<uint32_t>(q * 32) << 16;
-    auto build = [&](int k) {
-      const int st = k % L.raw_stages;
-      const uint32_t ru = static_cast<uint32_t>(k / L.raw_stages) & 1u;
+    for (int k = 0; k < my_tiles; ++k) {
       const int b = k & 1;
       const uint32_t u = static_cast<uint32_t>(k >> 1) & 1u;
-      mbar_wait(&raw_full[st], ru);
-      mbar_wait(&a1_empty[b], u ^ 1u);
-      const uint8_t* raw = sRaw + st * L.raw_stride;
-      uint8_t* a1 = sA1 + b * L.a1_bytes;
-      const int rows = L.T * G2;
-      for (int r = ta; r < rows; r += 128) {
-        const int n = r / G2, p = r % G2, i = p / L.G, j = p % L.G;
-        // Patch row a of pixel block (i, j): 4 bf16 = 8 bytes, K index a*4 + b.
-        const uint8_t* src = raw + (static_cast<size_t>(n) * L.S * L.S + (4 * i) * L.S + 4 * j) * 2;
-        const uint2 v0 = *reinterpret_cast<const uint2*>(src);
-        const uint2 v1 = *reinterpret_cast<const uint2*>(src + L.S * 2);
-        const uint2 v2 = *reinterpret_cast<const uint2*>(src + L.S * 4);
-        const uint2 v3 = *reinterpret_cast<const uint2*>(src + L.S * 6);
-        *reinterpret_cast<uint4*>(a1 + r * 16) = make_uint4(v0.x, v0.y, v1.x, v1.y);
-        *reinterpret_cast<uint4*>(a1 + L.a1_plane + r * 16) = make_uint4(v2.x, v2.y, v3.x, v3.y);
-      }
-      fence_proxy_async_smem();
-      mbar_arrive(&raw_empty[st]);
-      mbar_arrive(&a1_full[b]);
-    };
-    auto epi1 = [&](int k) {
-      const int b = k & 1;
-      const uint32_t u = static_cast<uint32_t>(k >> 1) & 1u;
-      mbar_wait(&c1_full[b], u);
-      mbar_wait(&a2_empty[b], u ^ 1u);
+      mbar_sleep_wait(&c1_full[b], u);
+      mbar_sleep_wait(&a2_empty[b], u ^ 1u);
+      if (ta == 0) TRACE(k, 6);
       tc_fence_after();
       uint8_t* a2 = sA2 + b * L.a2_bytes;
       const int rows = L.T * G2;
       for (int mb = 0; mb < L.mb1; ++mb) {
         const int r = mb * 128 + q * 32 + lane;
         const int n = r / G2, p = r % G2, i = p / L.G, j = p % L.G;
-        const int grow = kMargin + n * P2 + (i + 1) * L.pad + (j + 1);
+        const int grow = kMargin + n * P2 + (i + 1) * L.R + (j + 1);
         for (int c0 = 0; c0 < L.c1; c0 += 32) {
           uint32_t v[32];
           tmem_ld32_raw(tmem_base + lane_field + static_cast<uint32_t>(b * L.tmem_c1 + mb * L.c1 + c0), v);
@@ -240,28 +254,52 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) mbar_arrive(&c1_empty[b]);
       fence_proxy_async_smem();
       mbar_arrive(&a2_full[b]);
-    };
-    if (my_tiles > 0) build(0);
-    for (int k = 0; k < my_tiles; ++k) {
-      if (k + 1 < my_tiles) build(k + 1);
-      epi1(k);
+      if (ta == 0) TRACE(k, 7);
     }
   } else {
-    // ------------------------------------------------------- conv2 epilogue
+    // ----------------------------------- im2col builders + conv2 epilogue
+    const int ta = threadIdx.x - 192;  // 0..127
     const int q = warp & 3;
     const uint32_t lane_field = static_cast<uint32_t>(q * 32) << 16;
     const int row_bytes = G2 * L.c2 * 2;
-    for (int k = 0; k < my_tiles; ++k) {
+    auto build = [&](int k) {
+      const int st = k % L.raw_stages;
+      const uint32_t ru = static_cast<uint32_t>(k / L.raw_stages) & 1u;
       const int b = k & 1;
       const uint32_t u = static_cast<uint32_t>(k >> 1) & 1u;
-      mbar_wait(&c2_full[b], u);
+      mbar_sleep_wait(&raw_full[st], ru);
+      mbar_sleep_wait(&a1_empty[b], u ^ 1u);
+      if (ta == 0) TRACE(k, 4);
+      const uint8_t* raw = sRaw + st * L.raw_stride;
+      uint8_t* a1 = sA1 + b * L.a1_bytes;
+      const int rows = L.T * G2;
+      for (int r = ta; r < rows; r += 128) {
+        const int n = r / G2, p = r % G2, i = p / L.G, j = p % L.G;
+        // Patch row a of pixel block (i, j): 4 bf16 = 8 bytes, K index a*4 + b.
+        const uint8_t* src = raw + (static_cast<size_t>(n) * L.S * L.S + (4 * i) * L.S + 4 * j) * 2;
+        const uint2 v0 = *reinterpret_cast<const uint2*>(src);
+        const uint2 v1 = *reinterpret_cast<const uint2*>(src + L.S * 2);
+        const uint2 v2 = *reinterpret_cast<const uint2*>(src + L.S * 4);
+        const uint2 v3 = *reinterpret_cast<const uint2*>(src + L.S * 6);
+        *reinterpret_cast<uint4*>(a1 + r * 16) = make_uint4(v0.x, v0.y, v1.x, v1.y);
+        *reinterpret_cast<uint4*>(a1 + L.a1_plane + r * 16) = make_uint4(v2.x, v2.y, v3.x, v3.y);
+      }
+      fence_proxy_async_smem();
+      mbar_arrive(&raw_empty[st]);
+      mbar_arrive(&a1_full[b]);
+      if (ta == 0) TRACE(k, 5);
+    };
+    auto epi2 = [&](int k) {
+      const int b = k & 1;
+      const uint32_t u = static_cast<uint32_t>(k >> 1) & 1u;
+      mbar_sleep_wait(&c2_full[b], u);
+      if (warp == 6 && lane == 0) TRACE(k, 8);
       tc_fence_after();
       const long long s0 = args.row_begin + (blockIdx.x + static_cast<long long>(k) * gridDim.x) * L.T;
       for (int mb = 0; mb < L.mb2; ++mb) {
-        const int r = mb * 128 + q * 32 + lane;  // padded-grid row of the tile
-        const int n = r / P2, rr = r % P2, h = rr / L.pad, w = rr % L.pad;
-        const bool valid = r < L.T * P2 && h >= 1 && h <= L.G && w >= 1 && w <= L.G &&
-                           s0 + n < args.row_end;
+        const int r = mb * 128 + q * 32 + lane;  // grid row of the tile
+        const int n = r / P2, rr = r % P2, h = rr / L.R, w = rr % L.R;
+        const bool valid = r < L.T * P2 && h >= 1 && w >= 1 && s0 + n < args.row_end;
         uint8_t* dst = static_cast<uint8_t*>(args.out) + (s0 + n) * row_bytes +
                        ((h - 1) * L.G + (w - 1)) * L.c2 * 2;
         for (int c0 = 0; c0 < L.c2; c0 += 32) {
@@ -287,6 +325,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&c2_empty[b]);
+      if (warp == 6 && lane == 0) TRACE(k, 9);
+    };
+    // conv1 of tile k+1 is issued before conv2 of tile k, so builds run two
+    // tiles ahead: the build of tile k+1 never waits behind the epilogue of
+    // tile k-1 (which waits for conv2 of tile k-1).
+    for (int k = 0; k < my_tiles && k < 2; ++k) build(k);
+    for (int k = 0; k < my_tiles; ++k) {
+      if (k + 2 < my_tiles) build(k + 2);
+      epi2(k);
     }
   }
 
@@ -304,16 +351,16 @@ uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
 
 bool conv_plan(int S, int P, int c1, int c2, ConvLayout* out) {
   if (P != 4 || S < P || S % P != 0 || (S * S) % 16 != 0) return false;
-  if (c1 < 32 || c1 % 32 != 0 || c1 > 256 || c2 < 32 || c2 % 32 != 0 || c2 > 256) return false;
+  if ((c1 != 32 && c1 != 64 && c1 != 128) || c2 < 32 || c2 % 32 != 0 || c2 > 256) return false;
   ConvLayout L;
   L.S = S;
   L.P = P;
   L.G = S / P;
   L.c1 = c1;
   L.c2 = c2;
-  L.pad = L.G + 2;
-  if (L.pad + 1 > kMargin) return false;
-  const int P2 = L.pad * L.pad, G2 = L.G * L.G;
+  L.R = L.G + 1;
+  if (L.R + 1 > kMargin) return false;
+  const int P2 = L.R * L.R, G2 = L.G * L.G;
   for (int T = std::max(1, 256 / P2); T >= 1; --T) {
     L.T = T;
     L.mb1 = (T * G2 + 127) / 128;
@@ -358,12 +405,20 @@ int conv_launch(const ConvArgs& args, const void* x, long long x_rows, int grid,
   if (make_bf16_map_plain(&mx, x, 16, static_cast<uint64_t>(rows16),
                           static_cast<uint32_t>(L.T * L.S * L.S / 16)) != 0)
     return -1;
-  if (ensure_smem_attr(conv_stack_sm100, static_cast<int>(kSmemBudget)) != 0) return -4;
   const long long tiles = (args.row_end - args.row_begin + L.T - 1) / L.T;
   if (tiles <= 0) return 0;
   grid = static_cast<int>(std::min<long long>(grid, tiles));
-  conv_stack_sm100<<<grid, kThreads, L.smem_bytes, stream>>>(mx, args);
-  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+  auto go = [&](auto kernel) {
+    if (ensure_smem_attr(kernel, static_cast<int>(kSmemBudget)) != 0) return -4;
+    kernel<<<grid, kThreads, L.smem_bytes, stream>>>(mx, args);
+    return cudaGetLastError() == cudaSuccess ? 0 : -3;
+  };
+  switch (L.c1) {
+    case 32: return go(conv_stack_sm100<2>);
+    case 64: return go(conv_stack_sm100<4>);
+    case 128: return go(conv_stack_sm100<8>);
+    default: return -1;
+  }
 }
 
 }  // namespace es

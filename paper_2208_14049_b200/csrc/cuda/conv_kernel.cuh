@@ -10,12 +10,17 @@
 //   * conv1: TMA brings the raw images; builder warps write the im2col rows
 //     (one row per output pixel, K = P*P) into a K-major planar operand; one
 //     UMMA (M=128, N=c1, K=16) per 128 rows;
-//   * conv1's epilogue writes relu(acc+b) as bf16 into a zero-bordered
-//     (G+2) x (G+2) grid per sample, again K-major planar (channels = K);
-//   * conv2: output pixel q (in padded coordinates) at tap (dh, dw) reads row
-//     q + dh*(G+2) + dw of that grid, so each of the 9 taps is the SAME operand
-//     with the descriptor start moved by whole rows (16 B each) -- nine
-//     accumulating UMMAs per K step, no im2col copy, no re-read from memory;
+//   * conv1's epilogue writes relu(acc+b) as bf16 into a zero-bordered grid,
+//     again K-major planar (channels = K).  Grid rows have stride R = G+1 and
+//     samples stride R*R: pixel (h, w), 1 <= h, w <= G, sits at row
+//     s*R*R + h*R + w, and row 0 / column 0 of each sample are zero -- the
+//     right neighbour of column G is the next row's column 0 and the bottom
+//     neighbour of row G is the next sample's row 0, so ONE shared border
+//     serves both sides (49 of 64 rows useful at G = 7, 2 samples per M block);
+//   * conv2: output pixel q at tap (dh, dw) reads grid row q + dh*R + dw, so
+//     each of the 9 taps is the SAME operand with the descriptor start moved
+//     by whole rows (16 B each) -- nine accumulating UMMAs per K step, no
+//     im2col copy, no re-read from memory;
 //   * conv2's epilogue keeps the G x G interior and stores bf16 rows to HBM.
 // Every operand is K-major without swizzle (sdesc_planar in sm100.cuh).
 #pragma once
@@ -28,8 +33,8 @@ namespace es {
 
 struct ConvLayout {
   int S = 28, P = 4, G = 7, c1 = 64, c2 = 32;
-  int pad = 9;           // G + 2: side of the zero-bordered grid
-  int T = 3;             // samples per tile
+  int R = 8;             // G + 1: grid row stride (shared zero border)
+  int T = 4;             // samples per tile
   int mb1 = 2, mb2 = 2;  // 128-row M blocks of conv1 / conv2
   int raw_stages = 4;
   uint32_t raw_stride = 0;                     // bytes per raw image stage
@@ -48,10 +53,13 @@ struct ConvArgs {
   const void* w2 = nullptr;  // bf16 [c2][9*c1], K index = tap*c1 + channel, tap = 3*(dh+1)+(dw+1)
   const float* b2 = nullptr;
   void* out = nullptr;  // bf16 [rows][G*G*c2]
+  // Design evidence (tools/trace_conv.cu): globaltimer stamps of CTA 0's
+  // first 32 tiles, [tile][16]; nullptr in the product.
+  unsigned long long* trace = nullptr;
 };
 
-// False when the shape has no plan (P != 4, S % P, channel counts not
-// multiples of 32, grids larger than 13 x 13).
+// False when the shape has no plan (P != 4, S % P != 0, c1 not in
+// {32, 64, 128}, c2 not a multiple of 32 up to 256, grids larger than 13 x 13).
 bool conv_plan(int S, int P, int c1, int c2, ConvLayout* out);
 // x: bf16 [x_rows][S*S].
 int conv_launch(const ConvArgs& args, const void* x, long long x_rows, int grid, cudaStream_t stream);

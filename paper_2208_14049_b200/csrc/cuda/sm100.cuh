@@ -66,6 +66,38 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// try_wait with a suspend-time hint: the waiting warp sleeps until the phase
+// completes (or the hint expires) instead of re-issuing the probe, so idle
+// roles stop taking issue slots from the busy ones on their SM sub-partition.
+__device__ __forceinline__ void mbar_sleep_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(0x989680)
+      : "memory");
+}
+
+// One lane of a converged warp (elect.sync).  Issuing tcgen05 work from a
+// converged warp keeps descriptor arithmetic in uniform registers; the same
+// loop under `if (lane == 0)` pays an R2UR round trip per instruction
+// (tools/umma_rate.cu: ~42 vs ~120 clk per UMMA).
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
+// Warp index the compiler can prove warp-uniform.
+__device__ __forceinline__ int warp_uniform_id() {
+  return __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
+}
+
 // ---------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");

@@ -106,7 +106,7 @@ bool DeviceMember::load(int device, const ModelSpec& model, int batch) {
     I.cnn = true;
     if (!es::conv_plan(a.widths[0], a.widths[1], a.widths[2], a.widths[3], &I.conv))
       throw SpecError(model.name + ": CNN shape has no tile plan (patch 4, image side a "
-                      "multiple of 4 up to 52, conv channels multiples of 32 up to 256)");
+                      "multiple of 4 up to 52, c1 in {32, 64, 128}, c2 a multiple of 32 up to 256)");
     I.act_width.push_back(I.dims[2].first);
   } else {
     // Leading layers: tcgen05 dense layers with a bf16 output.

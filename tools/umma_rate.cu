@@ -1,0 +1,199 @@
+// Design evidence, not product: issue-to-completion rate of back-to-back
+// tcgen05.mma (M=128, K=16, bf16) for operand layouts the member kernels use.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O2 -std=c++17 -I../paper_2208_14049_b200/csrc \
+//        umma_rate.cu -o umma_rate
+#include <cuda_runtime.h>
+
+#include <cstdio>
+
+#include "cuda/sm100.cuh"
+
+using namespace es::sm100;
+
+// layout 0: SW128 K-major (A and B); 1: planar no-swizzle (A and B);
+// shift: A start moved by `shift` rows of 16 B (planar only).
+__global__ void __launch_bounds__(128, 1) rate(int layout, int N, int shift, int reps,
+                                               unsigned long long* out) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  for (int i = threadIdx.x; i < 96 * 1024 / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  if (threadIdx.x < 32) tmem_alloc(&slot, 256);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  if (threadIdx.x == 0) {
+    const uint32_t a = smem_u32(smem), b = smem_u32(smem + 64 * 1024);
+    const uint32_t idesc = idesc_bf16_f32(128, N);
+    uint64_t ad, bd;
+    if (layout == 0) {
+      ad = sdesc_k128(a);
+      bd = sdesc_k128(b);
+    } else {
+      ad = sdesc_planar(a + shift * 16, 160 * 16);
+      bd = sdesc_planar(b, N * 16);
+    }
+    const long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) umma_bf16(tmem, ad, bd, idesc, r != 0);
+    umma_commit(&bar);
+    mbar_wait(&bar, 0);
+    const long long t1 = clock64();
+    if (blockIdx.x == 0) out[0] = static_cast<unsigned long long>(t1 - t0);
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) tmem_dealloc(tmem, 256);
+}
+
+// Descriptors recomputed per MMA (as the conv kernel's tap loop does): issued
+// from lane 0 only (mode 0) or from a converged warp with elect.sync (mode 1).
+__global__ void __launch_bounds__(128, 1) rate_varying(int mode, int N, int reps,
+                                                       unsigned long long* out) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  for (int i = threadIdx.x; i < 96 * 1024 / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  if (threadIdx.x < 32) tmem_alloc(&slot, 256);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  const uint32_t a = smem_u32(smem), b = smem_u32(smem + 64 * 1024);
+  const uint32_t idesc = idesc_bf16_f32(128, N);
+  if (mode == 0) {
+    if (threadIdx.x == 0) {
+      const long long t0 = clock64();
+      for (int r = 0; r < reps; ++r) {
+        const int t = r % 9, j = (r / 9) & 3;
+        umma_bf16(tmem, sdesc_planar(a + (16 + (t / 3 - 1) * 9 + t % 3) * 16 + j * 2 * 2560, 2560),
+                  sdesc_planar(b + t * 2048 + j * 256, N * 16), idesc, r != 0);
+      }
+      umma_commit(&bar);
+      mbar_wait(&bar, 0);
+      if (blockIdx.x == 0) out[0] = static_cast<unsigned long long>(clock64() - t0);
+    }
+  } else if (threadIdx.x < 32) {
+    const long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+      const int t = r % 9, j = (r / 9) & 3;
+      const uint64_t ad = sdesc_planar(a + (16 + (t / 3 - 1) * 9 + t % 3) * 16 + j * 2 * 2560, 2560);
+      const uint64_t bd = sdesc_planar(b + t * 2048 + j * 256, N * 16);
+      if (elect_one()) umma_bf16(tmem, ad, bd, idesc, r != 0);
+      __syncwarp();
+    }
+    if (elect_one()) umma_commit(&bar);
+    __syncwarp();
+    mbar_wait(&bar, 0);
+    if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = static_cast<unsigned long long>(clock64() - t0);
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) tmem_dealloc(tmem, 256);
+}
+
+// Descriptors from a per-tap table, loops unrolled (9 taps x 4 K steps):
+// mode 2 = converged warp (warp index made provably uniform) + elect.sync,
+// mode 3 = lane 0 only.
+__global__ void __launch_bounds__(128, 1) rate_table(int mode, int N, int reps, int pad,
+                                                     unsigned long long* out) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  for (int i = threadIdx.x; i < 96 * 1024 / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  if (threadIdx.x < 32) tmem_alloc(&slot, 256);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  const uint32_t a = smem_u32(smem), b = smem_u32(smem + 64 * 1024);
+  const uint32_t idesc = idesc_bf16_f32(128, N);
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
+  const uint64_t ad0 = sdesc_planar(a + 16 * 16, 2560), bd0 = sdesc_planar(b, N * 16);
+  int otab[9];
+#pragma unroll
+  for (int t = 0; t < 9; ++t) otab[t] = (t / 3 - 1) * pad + (t % 3 - 1);
+  auto body = [&](bool elect) {
+    const long long t0 = clock64();
+    for (int r = 0; r < reps; r += 36) {
+#pragma unroll
+      for (int t = 0; t < 9; ++t)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint64_t ad = ad0 + static_cast<uint64_t>(otab[t] + j * 320);
+          const uint64_t bd = bd0 + static_cast<uint64_t>(t * 4 * N + j * 2 * N);
+          if (!elect || elect_one()) umma_bf16(tmem, ad, bd, idesc, (r | t | j) != 0);
+        }
+    }
+    if (!elect || elect_one()) umma_commit(&bar);
+    __syncwarp(elect ? 0xffffffffu : 1u);
+    mbar_wait(&bar, 0);
+    if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = static_cast<unsigned long long>(clock64() - t0);
+  };
+  if (mode == 2) {
+    if (warp == 0) body(true);
+  } else if (threadIdx.x == 0) {
+    body(false);
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) tmem_dealloc(tmem, 256);
+}
+
+int main() {
+  unsigned long long* d;
+  cudaMalloc(&d, 8);
+  cudaFuncSetAttribute(rate, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  const int reps = 512;
+  for (int layout = 0; layout < 2; ++layout)
+    for (int N : {32, 64, 128, 256})
+      for (int shift : {0, 1, 3}) {
+        if (layout == 0 && shift) continue;
+        rate<<<148, 128, 100 * 1024>>>(layout, N, shift, reps, d);
+        unsigned long long c = 0;
+        cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
+        std::printf("%-7s N=%3d shift=%d: %6.1f clk/MMA  (%5.0f MAC/clk) %s\n",
+                    layout ? "planar" : "sw128", N, shift, double(c) / reps,
+                    128.0 * N * 16 * reps / double(c), cudaGetErrorString(cudaGetLastError()));
+      }
+  cudaFuncSetAttribute(rate_varying, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  for (int mode = 0; mode < 2; ++mode)
+    for (int N : {32, 64, 128}) {
+      rate_varying<<<148, 128, 100 * 1024>>>(mode, N, reps, d);
+      unsigned long long c = 0;
+      cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
+      std::printf("varying desc, %s N=%3d: %6.1f clk/MMA %s\n", mode ? "warp+elect" : "lane0     ", N,
+                  double(c) / reps, cudaGetErrorString(cudaGetLastError()));
+    }
+  cudaFuncSetAttribute(rate_table, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  for (int mode = 2; mode < 4; ++mode)
+    for (int N : {32, 64, 128}) {
+      rate_table<<<148, 128, 100 * 1024>>>(mode, N, 504, 9, d);
+      unsigned long long c = 0;
+      cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
+      std::printf("tap table, %s N=%3d: %6.1f clk/MMA %s\n", mode == 2 ? "warp+elect" : "lane0     ",
+                  N, double(c) / 504, cudaGetErrorString(cudaGetLastError()));
+    }
+  return 0;
+}
