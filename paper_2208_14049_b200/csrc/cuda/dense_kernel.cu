@@ -50,7 +50,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* acc_empty = acc_full + 2;     // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
-  const int warp = threadIdx.x >> 5;
+  const int warp = warp_uniform_id();
   const int lane = threadIdx.x & 31;
   const int N = L.N;
 
@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // warp-uniform
 
   if (warp == 0) {
     if (lane == 0) {
@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // the whole warp walks the schedule; one elected lane issues
       const uint32_t idesc = idesc_bf16_f32(128, L.NH);
       int stage = 0;
       uint32_t phase = 0;
@@ -128,16 +128,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int h = 0; h < L.nh; ++h)
 #pragma unroll
               for (int j = 0; j < 4; ++j)
-                umma_bf16(d0 + static_cast<uint32_t>(k * N + h * L.NH),
+                if (elect_one()) umma_bf16(d0 + static_cast<uint32_t>(k * N + h * L.NH),
                           xd + static_cast<uint64_t>(k * 1024 + j * 2),
                           wd + static_cast<uint64_t>(h * L.NH * 8 + j * 2), idesc, (kc | j) != 0);
-          umma_commit(&empty[stage]);
+          if (elect_one()) umma_commit(&empty[stage]);
           if (++stage == L.stages) {
             stage = 0;
             phase ^= 1u;
           }
         }
-        umma_commit(&acc_full[buf]);
+        if (elect_one()) umma_commit(&acc_full[buf]);
       }
     }
   } else {

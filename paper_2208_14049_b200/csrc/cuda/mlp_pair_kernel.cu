@@ -99,7 +99,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* d2_empty = w2_full + 1;       // [kMaxT]    (leader's; 8 remote arrivals)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d2_empty + kMaxT);
 
-  const int warp = threadIdx.x >> 5;
+  const int warp = warp_uniform_id();
   const int lane = threadIdx.x & 31;
   const int H = L.H;
   const uint32_t rank = cluster_ctarank();
@@ -132,7 +132,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   tc_fence_before();
   cluster_sync();  // barrier inits and TMEM of both SMs visible to both
   tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // warp-uniform
 
   if (warp == 0) {
     if (lane == 0) {
@@ -173,7 +173,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && leader) {
+    if (leader) {  // the whole warp walks the schedule; one elected lane issues
       // ------------------------------------------------------------ pair UMMA issuer
       const uint32_t idesc1 = idesc_bf16_f32(256, L.NH);
       const uint32_t idesc2 = idesc_bf16_f32(256, 16);
@@ -211,9 +211,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint32_t h0 = static_cast<uint32_t>(hh * (H / 2) + kk * 16);
             const uint32_t a = tile + static_cast<uint32_t>(hh * (H / 2) + kk * 8);
             const uint64_t b = w2d + (h0 >> 6) * 64u + (h0 & 63u) / 8u;
-            umma_bf16_pair_ta(d2 + 16u * (step & pmask), a, b, idesc2, step > pmask);
+            if (elect_one()) umma_bf16_pair_ta(d2 + 16u * (step & pmask), a, b, idesc2, step > pmask);
           }
-        umma_commit_pair(&acc2_full[k], kBoth);
+        if (elect_one()) umma_commit_pair(&acc2_full[k], kBoth);
         if (k == 0) TRACE(pend_g, 9);
       };
       auto drain_pending = [&]() {
@@ -245,22 +245,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               for (int j = 0; j < 4; ++j) {
                 const uint64_t a = xd + static_cast<uint64_t>(k * 1024 + j * 2);
                 const uint64_t b = wd + static_cast<uint64_t>(h * half_w * 8u + j * 2);
-                umma_bf16_pair(d0 + static_cast<uint32_t>(k * H + h * L.NH), a, b, idesc1,
+                if (elect_one()) umma_bf16_pair(d0 + static_cast<uint32_t>(k * H + h * L.NH), a, b, idesc1,
                                (kc | j) != 0);
               }
-          umma_commit_pair(&empty[stage], kBoth);
+          if (elect_one()) umma_commit_pair(&empty[stage], kBoth);
           if (++stage == L.stages) {
             stage = 0;
             phase ^= 1u;
           }
           while (pend_buf >= 0 && pend_next < pend_n &&
-                 mbar_test_cluster(&a_full[pend_next], (a_par >> pend_next) & 1u)) {
+                 __shfl_sync(0xffffffffu, mbar_test_cluster(&a_full[pend_next], (a_par >> pend_next) & 1u), 0)) {
             layer2(pend_buf, pend_next, true);
             ++pend_next;
           }
           if (pend_buf >= 0 && pend_next == pend_n) pend_buf = -1;
         }
-        umma_commit_pair(&acc_full[buf], kBoth);
+        if (elect_one()) umma_commit_pair(&acc_full[buf], kBoth);
         TRACE(g, 2);
         if (pend_buf >= 0) drain_pending();
         pend_buf = buf;

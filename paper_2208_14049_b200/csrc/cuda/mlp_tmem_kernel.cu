@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* d2_empty = w2_full + 1;       // [kMaxT] separate D2 drained (d2_sep)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d2_empty + kMaxT);
 
-  const int warp = threadIdx.x >> 5;
+  const int warp = warp_uniform_id();
   const int lane = threadIdx.x & 31;
   const int H = L.H;
   const Tiles ts = tile_space(args);
@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // warp-uniform
 
   if (warp == 0) {
     if (lane == 0) {
@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // the whole warp walks the schedule; one elected lane issues
       // ------------------------------------------------------------ UMMA issuer
       const uint32_t idesc1 = idesc_bf16_f32(128, L.NH);
       const uint32_t idesc2 = idesc_bf16_f32(128, 16);
@@ -182,9 +182,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t h0 = static_cast<uint32_t>(hh * (H / 2) + kk * 16);
             const uint32_t a = tile + static_cast<uint32_t>(hh * (H / 2) + kk * 8);
             const uint64_t b = w2d + (h0 >> 6) * 128u + (h0 & 63u) / 8u;
-            umma_bf16_ta(d2 + 16u * (step & pmask), a, b, idesc2, step > pmask);
+            if (elect_one()) umma_bf16_ta(d2 + 16u * (step & pmask), a, b, idesc2, step > pmask);
           }
-        umma_commit(&acc2_full[k]);
+        if (elect_one()) umma_commit(&acc2_full[k]);
       };
       auto drain_pending = [&]() {
         for (; pend_next < pend_n; ++pend_next) layer2(pend_buf, pend_next, false);
@@ -213,23 +213,23 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int j = 0; j < 4; ++j) {
                 const uint64_t a = xd + static_cast<uint64_t>(k * 1024 + j * 2);
                 const uint64_t b = wd + static_cast<uint64_t>(h * L.NH * 8 + j * 2);
-                umma_bf16(d0 + static_cast<uint32_t>(k * H + h * L.NH), a, b, idesc1,
+                if (elect_one()) umma_bf16(d0 + static_cast<uint32_t>(k * H + h * L.NH), a, b, idesc1,
                           (kc | j) != 0);
               }
-          umma_commit(&empty[stage]);
+          if (elect_one()) umma_commit(&empty[stage]);
           if (++stage == L.stages) {
             stage = 0;
             phase ^= 1u;
           }
           // Overlap: issue the previous group's layer 2 as its hidden tiles land.
           while (pend_buf >= 0 && pend_next < pend_n &&
-                 mbar_test(&a_full[pend_next], (a_par >> pend_next) & 1u)) {
+                 __shfl_sync(0xffffffffu, mbar_test(&a_full[pend_next], (a_par >> pend_next) & 1u), 0)) {
             layer2(pend_buf, pend_next, true);
             ++pend_next;
           }
           if (pend_buf >= 0 && pend_next == pend_n) pend_buf = -1;
         }
-        umma_commit(&acc_full[buf]);
+        if (elect_one()) umma_commit(&acc_full[buf]);
         if (pend_buf >= 0) drain_pending();
         pend_buf = buf;
         pend_n = n;
