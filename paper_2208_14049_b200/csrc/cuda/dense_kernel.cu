@@ -18,11 +18,19 @@ constexpr uint32_t kSmemBudget = 232448;
 constexpr uint32_t kMinSmem = 120 * 1024;
 constexpr int kMaxT = 4;
 
-__device__ __forceinline__ int group_rows(const DenseArgs& a, int g, long long (&row0)[kMaxT]) {
+// The CTA's i-th work unit: T consecutive 128-row tiles x one column block.
+// Consecutive units of a row group walk its column blocks, so the X tiles are
+// re-read from L2 while hot.  Returns the number of tiles (0 = no more work).
+__device__ __forceinline__ int unit_rows(const DenseArgs& a, int i, int* cb, long long (&row0)[kMaxT]) {
   const long long tiles = (a.row_end - a.row_begin + 127) / 128;
+  const long long groups = (tiles + a.L.T - 1) / a.L.T;
+  const long long u = blockIdx.x + static_cast<long long>(i) * gridDim.x;
+  if (u >= groups * a.L.ncb) return 0;
+  *cb = static_cast<int>(u % a.L.ncb);
+  const long long g = u / a.L.ncb;
   int n = 0;
   for (int k = 0; k < a.L.T; ++k) {
-    const long long t = blockIdx.x + static_cast<long long>(g * a.L.T + k) * gridDim.x;
+    const long long t = g * a.L.T + k;
     if (t >= tiles) break;
     row0[k] = a.row_begin + t * 128;
     ++n;
@@ -34,6 +42,9 @@ __device__ __forceinline__ void half_barrier(int half) {
   asm volatile("bar.sync %0, 128;" ::"r"(2 + half) : "memory");
 }
 
+// kLogits: the member's last layer -- N = 16 (>= C) columns, no activation,
+// fp32 logits [rows][C] stored straight from the epilogue registers.
+template <bool kLogits>
 __global__ void __launch_bounds__(kThreads, 1)
     dense_sm100(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
                 const __grid_constant__ CUtensorMap tm_y, const DenseArgs args) {
@@ -42,7 +53,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   const DenseLayout& L = args.L;
   uint8_t* sOut = smem + L.off_stage_out;  // [2 halves][128 rows][128 B]
-  float* sBias = reinterpret_cast<float*>(smem + L.off_bias);
+  float* sBias = reinterpret_cast<float*>(smem + L.off_bias);  // all N_total columns
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.off_bar);
   uint64_t* full = bars;
   uint64_t* empty = full + L.stages;
@@ -52,7 +63,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = warp_uniform_id();
   const int lane = threadIdx.x & 31;
-  const int N = L.N;
+  const int N = L.N;  // columns per block
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < L.stages; ++s) {
@@ -68,7 +79,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tm_x);
     tma_prefetch(&tm_w);
-    tma_prefetch(&tm_y);
+    if (!kLogits) tma_prefetch(&tm_y);
   }
   if (warp == 1) tmem_alloc(tmem_slot, static_cast<uint32_t>(L.tmem_cols));
   tc_fence_before();
@@ -83,8 +94,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       long long row0[kMaxT];
-      for (int g = 0;; ++g) {
-        const int n = group_rows(args, g, row0);
+      int cb = 0;
+      for (int i = 0;; ++i) {
+        const int n = unit_rows(args, i, &cb, row0);
         if (n == 0) break;
         for (int kc = 0; kc < L.kchunks; ++kc) {
           mbar_wait(&empty[stage], phase ^ 1u);
@@ -95,8 +107,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load_2d(st + k * 16384, &tm_x, &full[stage], kc * 64,
                         static_cast<int32_t>(row0[k]), pol_stream);
           uint8_t* sw = st + L.T * 16384;
-          for (int c = 0; c < N / 64; ++c)  // 64-row boxes of W
-            tma_load_2d(sw + c * 8192, &tm_w, &full[stage], kc * 64, c * 64, pol_keep);
+          if (kLogits) {
+            tma_load_2d(sw, &tm_w, &full[stage], kc * 64, 0, pol_keep);  // one 16-row box
+          } else {
+            for (int c = 0; c < N / 64; ++c)  // 64-row boxes of the column block of W
+              tma_load_2d(sw + c * 8192, &tm_w, &full[stage], kc * 64, cb * N + c * 64, pol_keep);
+          }
           if (++stage == L.stages) {
             stage = 0;
             phase ^= 1u;
@@ -110,11 +126,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       long long row0[kMaxT];
-      for (int g = 0;; ++g) {
-        const int n = group_rows(args, g, row0);
+      int cb = 0;
+      for (int i = 0;; ++i) {
+        const int n = unit_rows(args, i, &cb, row0);
         if (n == 0) break;
-        const int buf = g % L.nbuf;
-        const uint32_t use = static_cast<uint32_t>(g / L.nbuf);
+        const int buf = i % L.nbuf;
+        const uint32_t use = static_cast<uint32_t>(i / L.nbuf);
         mbar_wait(&acc_empty[buf], (use & 1u) ^ 1u);
         tc_fence_after();
         const uint32_t d0 = tmem_base + static_cast<uint32_t>(buf * L.group_cols);
@@ -128,9 +145,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int h = 0; h < L.nh; ++h)
 #pragma unroll
               for (int j = 0; j < 4; ++j)
-                if (elect_one()) umma_bf16(d0 + static_cast<uint32_t>(k * N + h * L.NH),
-                          xd + static_cast<uint64_t>(k * 1024 + j * 2),
-                          wd + static_cast<uint64_t>(h * L.NH * 8 + j * 2), idesc, (kc | j) != 0);
+                if (elect_one())
+                  umma_bf16(d0 + static_cast<uint32_t>(k * N + h * L.NH),
+                            xd + static_cast<uint64_t>(k * 1024 + j * 2),
+                            wd + static_cast<uint64_t>(h * L.NH * 8 + j * 2), idesc, (kc | j) != 0);
           if (elect_one()) umma_commit(&empty[stage]);
           if (++stage == L.stages) {
             stage = 0;
@@ -144,58 +162,73 @@ __global__ void __launch_bounds__(kThreads, 1)
     // -------------------------------------------------------------- epilogue
     const int ew = warp - 2;
     const int q = warp & 3;
-    const int half = ew >> 2;  // columns [half*N/2, (half+1)*N/2)
+    const int half = ew >> 2;  // bf16 mode: columns [half*N/2, (half+1)*N/2) of the block
     const uint32_t lane_field = static_cast<uint32_t>(q * 32) << 16;
     const int row = q * 32 + lane;  // row within the tile
     const bool issuer = (warp & 3) == 2 && lane == 0;  // one thread per half issues stores
-    for (int i = threadIdx.x - 64; i < N; i += 256) sBias[i] = args.bias[i];
+    for (int i = threadIdx.x - 64; i < L.N_total; i += 256) sBias[i] = args.bias[i];
     asm volatile("bar.sync 1, 256;" ::: "memory");
     uint8_t* myout = sOut + half * 16384;
-    int it = 0;  // staging buffers used by this half
     long long row0[kMaxT];
-    for (int g = 0;; ++g) {
-      const int n = group_rows(args, g, row0);
+    int cb = 0;
+    for (int i = 0;; ++i) {
+      const int n = unit_rows(args, i, &cb, row0);
       if (n == 0) break;
-      const int buf = g % L.nbuf;
-      const uint32_t use = static_cast<uint32_t>(g / L.nbuf);
+      const int buf = i % L.nbuf;
+      const uint32_t use = static_cast<uint32_t>(i / L.nbuf);
       mbar_wait(&acc_full[buf], use & 1u);
       tc_fence_after();
-      for (int k = 0; k < n; ++k) {
-        for (int c = half * (N / 128); c < (half + 1) * (N / 128); ++c, ++it) {
-          const uint32_t col = static_cast<uint32_t>(buf * L.group_cols + k * N + c * 64);
-          uint32_t ra[32], rb[32];
-          tmem_ld32_raw(tmem_base + lane_field + col, ra);
-          tmem_ld32_raw(tmem_base + lane_field + col + 32, rb);
-          tmem_ld_wait();
-          // The half's staging tile is free once the previous store read it.
-          if (issuer) tma_store_wait_read<0>();
-          half_barrier(half);
-          uint8_t* stg = myout + row * 128;
-          const float* bias = sBias + c * 64;
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            uint32_t p[4];
-#pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              const int e = u * 8 + v * 2;
-              const uint32_t lo_bits = e < 32 ? ra[e] : rb[e - 32];
-              const uint32_t hi_bits = e + 1 < 32 ? ra[e + 1] : rb[e + 1 - 32];
-              float lo = __uint_as_float(lo_bits) + bias[e];
-              float hi = __uint_as_float(hi_bits) + bias[e + 1];
-              if (L.relu) {
-                lo = fmaxf(lo, 0.0f);
-                hi = fmaxf(hi, 0.0f);
-              }
-              __nv_bfloat162 pk = __floats2bfloat162_rn(lo, hi);
-              p[v] = *reinterpret_cast<uint32_t*>(&pk);
+      if (kLogits) {
+        if (half == 0) {
+          for (int k = 0; k < n; ++k) {
+            float v[16];
+            tmem_ld16(tmem_base + lane_field + static_cast<uint32_t>(buf * L.group_cols + k * 16), v);
+            tmem_ld_wait();
+            const long long r = row0[k] + row;
+            if (r < args.row_end) {
+              float* o = static_cast<float*>(args.logits) + r * L.C;
+              for (int c = 0; c < L.C; ++c) o[c] = v[c] + sBias[c];
             }
-            *reinterpret_cast<uint4*>(stg + ((u ^ (row & 7)) << 4)) = make_uint4(p[0], p[1], p[2], p[3]);
           }
-          fence_proxy_async_smem();
-          half_barrier(half);
-          if (issuer) {
-            tma_store_2d(&tm_y, myout, c * 64, static_cast<int32_t>(row0[k]));
-            tma_store_commit();
+        }
+      } else {
+        for (int k = 0; k < n; ++k) {
+          for (int c = half * (N / 128); c < (half + 1) * (N / 128); ++c) {
+            const uint32_t col = static_cast<uint32_t>(buf * L.group_cols + k * N + c * 64);
+            uint32_t ra[32], rb[32];
+            tmem_ld32_raw(tmem_base + lane_field + col, ra);
+            tmem_ld32_raw(tmem_base + lane_field + col + 32, rb);
+            tmem_ld_wait();
+            // The half's staging tile is free once the previous store read it.
+            if (issuer) tma_store_wait_read<0>();
+            half_barrier(half);
+            uint8_t* stg = myout + row * 128;
+            const float* bias = sBias + cb * N + c * 64;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              uint32_t p[4];
+#pragma unroll
+              for (int v = 0; v < 4; ++v) {
+                const int e = u * 8 + v * 2;
+                const uint32_t lo_bits = e < 32 ? ra[e] : rb[e - 32];
+                const uint32_t hi_bits = e + 1 < 32 ? ra[e + 1] : rb[e + 1 - 32];
+                float lo = __uint_as_float(lo_bits) + bias[e];
+                float hi = __uint_as_float(hi_bits) + bias[e + 1];
+                if (L.relu) {
+                  lo = fmaxf(lo, 0.0f);
+                  hi = fmaxf(hi, 0.0f);
+                }
+                __nv_bfloat162 pk = __floats2bfloat162_rn(lo, hi);
+                p[v] = *reinterpret_cast<uint32_t*>(&pk);
+              }
+              *reinterpret_cast<uint4*>(stg + ((u ^ (row & 7)) << 4)) = make_uint4(p[0], p[1], p[2], p[3]);
+            }
+            fence_proxy_async_smem();
+            half_barrier(half);
+            if (issuer) {
+              tma_store_2d(&tm_y, myout, cb * N + c * 64, static_cast<int32_t>(row0[k]));
+              tma_store_commit();
+            }
           }
         }
       }
@@ -203,7 +236,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[buf]);
     }
-    if (issuer) tma_store_wait_all<0>();
+    if (!kLogits && issuer) tma_store_wait_all<0>();
   }
 
   __syncthreads();
@@ -216,10 +249,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
 
-}  // namespace
-
-bool dense_plan(int K, int N, bool relu, DenseLayout* out) {
-  if (K < 1 || K % 8 != 0 || N < 128 || N % 128 != 0 || N > 512) return false;
+// Shared planner: N = columns per block (16 for logits), N_total = all columns.
+bool plan(int K, int N, int N_total, bool relu, bool logits, int C, DenseLayout* out) {
   const int kchunks = (K + 63) / 64;
   const int nh = (N + 255) / 256;
   const int NH = N / nh;
@@ -233,6 +264,10 @@ bool dense_plan(int K, int N, bool relu, DenseLayout* out) {
       DenseLayout L;
       L.K = K;
       L.N = N;
+      L.N_total = N_total;
+      L.ncb = N_total / N;
+      L.logits = logits ? 1 : 0;
+      L.C = C;
       L.kchunks = kchunks;
       L.T = T;
       L.nbuf = nbuf;
@@ -244,18 +279,20 @@ bool dense_plan(int K, int N, bool relu, DenseLayout* out) {
       while (tc < cols) tc <<= 1;
       L.tmem_cols = tc;
       L.stage_bytes = static_cast<uint32_t>(T) * 16384u + static_cast<uint32_t>(N) * 128u;
-      const uint32_t tail = 2 * 16384u + static_cast<uint32_t>(N) * 4u + 256u + 1024u;
+      const uint32_t out_bytes = logits ? 0u : 2 * 16384u;
+      const uint32_t tail = out_bytes + static_cast<uint32_t>(N_total) * 4u + 256u + 1024u + 64u;
+      if (tail >= kSmemBudget) continue;
       const int stages = static_cast<int>(std::min<uint32_t>(8, (kSmemBudget - tail) / L.stage_bytes));
       if (stages < 2) continue;
       L.stages = stages;
       L.off_stage_out = static_cast<uint32_t>(stages) * L.stage_bytes;
-      L.off_bias = L.off_stage_out + 2 * 16384u;
-      L.off_bar = align_up(L.off_bias + static_cast<uint32_t>(N) * 4u, 64);
+      L.off_bias = L.off_stage_out + out_bytes;
+      L.off_bar = align_up(L.off_bias + static_cast<uint32_t>(N_total) * 4u, 64);
       L.smem_bytes = std::max(L.off_bar + 256u + 1024u, kMinSmem);
       if (L.smem_bytes > kSmemBudget) continue;
-      const double mma = static_cast<double>(kchunks) * T * 2.0 * N;
+      const double mma = static_cast<double>(kchunks) * T * std::max(2.0 * N, 4 * 46.0);
       const double ingress = static_cast<double>(kchunks) * L.stage_bytes / 44.0;
-      const double epi = T * (N / 64.0) * 120.0 + 400.0;
+      const double epi = T * (logits ? 200.0 : (N / 64.0) * 120.0) + 400.0;
       const double cost = (std::max(mma, ingress) + (nbuf == 1 ? epi : 0.0)) / T;
       if (!found || cost < best_cost) {
         best = L;
@@ -267,23 +304,53 @@ bool dense_plan(int K, int N, bool relu, DenseLayout* out) {
   return found;
 }
 
+}  // namespace
+
+bool dense_plan(int K, int N, bool relu, DenseLayout* out) {
+  if (K < 1 || K % 8 != 0 || N < 128 || N % 128 != 0) return false;
+  // Column blocks of up to 512 (the TMEM width of one accumulator tile).
+  int block = 0;
+  for (int b : {512, 384, 256, 128})
+    if (N % b == 0) {
+      block = b;
+      break;
+    }
+  return plan(K, block, N, relu, false, 0, out);
+}
+
+bool dense_logits_plan(int K, int C, DenseLayout* out) {
+  if (K < 1 || K % 8 != 0 || C < 1 || C > 16) return false;
+  return plan(K, 16, 16, false, true, C, out);
+}
+
 int dense_launch(const DenseArgs& args, const void* x, long long x_rows, const void* w, void* y,
                  int grid, cudaStream_t stream) {
   const DenseLayout& L = args.L;
   CUtensorMap mx, mw, my;
   if (make_bf16_map(&mx, x, static_cast<uint64_t>(L.K), static_cast<uint64_t>(x_rows), 128) != 0)
     return -1;
-  if (make_bf16_map(&mw, w, static_cast<uint64_t>(L.K), static_cast<uint64_t>(L.N), 64) != 0)
-    return -1;
-  // Y clipped at row_end: rows of a tile past the worker's range are not written.
-  if (make_bf16_map(&my, y, static_cast<uint64_t>(L.N), static_cast<uint64_t>(args.row_end), 128) != 0)
-    return -1;
-  if (ensure_smem_attr(dense_sm100, static_cast<int>(kSmemBudget)) != 0) return -4;
+  if (L.logits) {
+    // W [C][K]: one 16-row box, rows C..15 zero-filled.
+    if (make_bf16_map(&mw, w, static_cast<uint64_t>(L.K), static_cast<uint64_t>(L.C), 16) != 0)
+      return -1;
+    my = mx;  // unused
+  } else {
+    if (make_bf16_map(&mw, w, static_cast<uint64_t>(L.K), static_cast<uint64_t>(L.N_total), 64) != 0)
+      return -1;
+    // Y clipped at row_end: rows of a tile past the worker's range are not written.
+    if (make_bf16_map(&my, y, static_cast<uint64_t>(L.N_total), static_cast<uint64_t>(args.row_end),
+                      128) != 0)
+      return -1;
+  }
   const long long tiles = (args.row_end - args.row_begin + 127) / 128;
   if (tiles <= 0) return 0;
-  grid = static_cast<int>(std::min<long long>(grid, (tiles + L.T - 1) / L.T));
-  dense_sm100<<<grid, kThreads, L.smem_bytes, stream>>>(mx, mw, my, args);
-  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+  grid = static_cast<int>(std::min<long long>(grid, (tiles + L.T - 1) / L.T * L.ncb));
+  auto go = [&](auto kernel) {
+    if (ensure_smem_attr(kernel, static_cast<int>(kSmemBudget)) != 0) return -4;
+    kernel<<<grid, kThreads, L.smem_bytes, stream>>>(mx, mw, my, args);
+    return cudaGetLastError() == cudaSuccess ? 0 : -3;
+  };
+  return L.logits ? go(dense_sm100<true>) : go(dense_sm100<false>);
 }
 
 }  // namespace es

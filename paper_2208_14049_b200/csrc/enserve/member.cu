@@ -56,11 +56,15 @@ struct DeviceMember::Impl {
   int batch = 1;
   int C = 1;
   std::vector<std::pair<int, int>> dims;  // (fan_in, fan_out) per weight matrix
-  enum class Head { Synthetic, SwapAB, Tmem, Pair } head = Head::Synthetic;
+  // Dense: too wide for a fused head -- the hidden layer through the dense
+  // kernel, the last layer in its logits mode.
+  enum class Head { Synthetic, SwapAB, Tmem, Pair, Dense } head = Head::Synthetic;
   es::Mlp2Layout plan_swapab{};
   es::MlpTLayout plan_tmem{};
   es::MlpPLayout plan_pair{};
-  std::vector<es::DenseLayout> dense;  // MLP: plans of the leading layers
+  std::vector<es::DenseLayout> dense;  // dense-kernel layers, in order
+  std::vector<int> dense_layer;        // their weight-matrix index
+  es::DenseLayout logits{};            // Head::Dense: the last layer
   bool cnn = false;
   es::ConvLayout conv{};  // CNN: the convolution stack (layers 0 and 1)
   void* weights = nullptr;
@@ -85,6 +89,7 @@ std::string DeviceMember::schedule() const {
     case Impl::Head::Pair: return "pair";
     case Impl::Head::Tmem: return "tmem";
     case Impl::Head::SwapAB: return "swapab";
+    case Impl::Head::Dense: return "dense";
     default: return "synthetic";
   }
 }
@@ -118,6 +123,7 @@ bool DeviceMember::load(int device, const ModelSpec& model, int batch) {
                         " has no tile plan (input width a multiple of 8, output width a "
                         "multiple of 128 up to 512)");
       I.dense.push_back(d);
+      I.dense_layer.push_back(l);
       I.act_width.push_back(I.dims[l].second);
     }
   }
@@ -134,10 +140,21 @@ bool DeviceMember::load(int device, const ModelSpec& model, int batch) {
     I.head = Impl::Head::Pair;
   else if (tmem_ok)
     I.head = Impl::Head::Tmem;
-  else if (es::mlp2_plan(K, H, C, batch, &I.plan_swapab))
+  else if ((want.empty() || want == "swapab") && es::mlp2_plan(K, H, C, batch, &I.plan_swapab))
     I.head = Impl::Head::SwapAB;
-  else
-    return false;  // the tile does not fit one SM: out of memory
+  else if (want.empty() || want == "dense") {
+    // Hidden layer wider than one SM's TMEM: no fused head.
+    es::DenseLayout d;
+    if (!es::dense_plan(K, H, true, &d) || !es::dense_logits_plan(H, C, &I.logits))
+      throw SpecError(model.name + ": layers " + std::to_string(K) + "->" + std::to_string(H) +
+                      "->" + std::to_string(C) + " have no tile plan");
+    I.dense.push_back(d);
+    I.dense_layer.push_back(L - 2);
+    I.act_width.push_back(H);
+    I.head = Impl::Head::Dense;
+  } else {
+    return false;  // the requested schedule does not fit one SM
+  }
 
   OnDev on(device);
   auto up = [](std::size_t x) { return (x + 255) / 256 * 256; };
@@ -205,15 +222,27 @@ int DeviceMember::forward(const void* x, long long nb, int seg_size, long long s
     ++launches;
     cur = I.act[0];
   }
-  for (std::size_t l = 0; l < I.dense.size(); ++l) {
+  for (std::size_t i = 0; i < I.dense.size(); ++i) {
+    const int l = I.dense_layer[i];
+    void* y = I.act[i + (I.cnn ? 1 : 0)];
     es::DenseArgs d;
-    d.L = I.dense[l];
+    d.L = I.dense[i];
     d.row_begin = r0;
     d.row_end = r1;
     d.bias = reinterpret_cast<const float*>(base + I.b_off[l]);
-    M_LAUNCH(es::dense_launch(d, cur, nb, base + I.w_off[l], I.act[l], grid, stream));
+    M_LAUNCH(es::dense_launch(d, cur, nb, base + I.w_off[l], y, grid, stream));
     ++launches;
-    cur = I.act[l];
+    cur = y;
+  }
+  if (I.head == Impl::Head::Dense) {
+    es::DenseArgs d;
+    d.L = I.logits;
+    d.row_begin = r0;
+    d.row_end = r1;
+    d.bias = reinterpret_cast<const float*>(base + I.b_off[L - 1]);
+    d.logits = out;
+    M_LAUNCH(es::dense_launch(d, cur, nb, base + I.w_off[L - 1], nullptr, grid, stream));
+    return launches + 1;
   }
   const int h = L - 2;  // head layers h, h+1
   const float* b1 = reinterpret_cast<const float*>(base + I.b_off[h]);

@@ -29,6 +29,20 @@ def test_deep_mlp_member_matches_cpu_oracle(widths, b):
     np.testing.assert_array_equal(np.argmax(got, 1), np.argmax(want, 1))
 
 
+@pytest.mark.parametrize("widths", [[784, 1024, 10], [784, 2048, 10], [784, 640, 16],
+                                    [784, 2048, 2048, 10]])
+def test_wide_mlp_member_matches_cpu_oracle(widths):
+    """Hidden layers wider than one SM's TMEM: dense kernel in column blocks,
+    last layer in the dense kernel's logits mode."""
+    X = refcpu.features(42, 333, 784)
+    model = es.mlp_model(0, "wide", widths, 4343)
+    got = es.Member(model, 64).predict(X)
+    cpu = refcpu.CpuMlp(widths, 4343)
+    want = cpu.forward(X)
+    assert_logits_close(got, want, cpu.logit_scale(X), rtol=RTOL_BF16 * (len(widths) - 2))
+    np.testing.assert_array_equal(np.argmax(got, 1), np.argmax(want, 1))
+
+
 def test_heterogeneous_depths_in_one_ensemble_match_reference_pipeline():
     if not refcpu.ref_available():
         pytest.skip("oracle/_ref not built")
@@ -53,7 +67,8 @@ def test_heterogeneous_depths_in_one_ensemble_match_reference_pipeline():
 
 
 # ------------------------------------------------------------------ K2 CNN
-CNN_SHAPES = [(28, 4, 64, 32, 128, 10), (28, 4, 32, 64, 256, 10), (16, 4, 64, 32, 128, 10)]
+CNN_SHAPES = [(28, 4, 64, 32, 128, 10), (28, 4, 32, 64, 256, 10), (16, 4, 64, 32, 128, 10),
+              (28, 4, 128, 32, 1024, 10)]
 
 
 @pytest.mark.parametrize("shape", CNN_SHAPES)
@@ -90,7 +105,7 @@ def test_cnn_in_data_parallel_ensemble_matches_reference_pipeline():
         pytest.skip("oracle/_ref not built")
     models = [es.mlp_model(0, "mlp256", [784, 256, 10], 1),
               es.mlp_model(1, "mlp512x2", [784, 512, 512, 10], 2),
-              es.mlp_model(2, "mlp384", [784, 384, 10], 3),
+              es.mlp_model(2, "mlp1024", [784, 1024, 10], 3),
               es.cnn_model(3, "cnn-s", 4)]
     c = es.ClusterSpec([gpu(0, 180000.0, 1e15, 0.0), gpu(1, 180000.0, 1e15, 0.0)], models,
                        [8, 16, 32, 64, 128], 128)

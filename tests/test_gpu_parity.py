@@ -149,9 +149,10 @@ def mlp_cluster(hidden, batches, seeds=None, devices=1, nb_classes=10):
                           [8, 16, 32, 64, 128], 128)
 
 
-@pytest.fixture(params=["pair", "tmem", "swapab"])
+@pytest.fixture(params=["pair", "tmem", "swapab", "dense"])
 def mlp_kernel(request):
-    """Both sm_100a schedules of K1."""
+    """Every sm_100a schedule of K1: the fused heads and the
+    dense-layer chain wide members fall back to."""
     old = os.environ.get("ES_MLP_KERNEL")
     os.environ["ES_MLP_KERNEL"] = request.param
     yield request.param
