@@ -1,13 +1,14 @@
 #!/usr/bin/env python
 """Headline benchmark: ensemble samples/s (BASELINE.json `metric`).
 
-Workload (N = 1): cfg2 of BASELINE.json — 4 heterogeneous MLP members
-(784-512-10, 784-384-10, 784-256-10, 784-128-10) co-located on one B200,
-batch sizes chosen by the bounded greedy over calib_data with the
-device-timed bench (worst-fit-decreasing start), averaging of per-member
-softmax probabilities + argmax.  A "step" is one InferenceSystem.run over
-`--nb` samples already resident in HBM (bf16 replica, > L2, so no flush is
-needed): 4 member kernels + 1 combine kernel.
+Workload (N = 1): cfg2 of BASELINE.json — 4 heterogeneous MLP/CNN members
+co-located on one B200 (SURVEY.md §8-D roster: MLP-256 784-256-10,
+MLP-512-512 784-512-512-10, MLP-1024 784-1024-10, CNN-s 28x28 -> conv4x4/4
+64 -> conv3x3 32 -> 128 -> 10), batch sizes chosen by the bounded greedy over
+calib_data with the device-timed bench (worst-fit-decreasing start),
+averaging of per-member softmax probabilities + argmax.  A "step" is one
+InferenceSystem.run over `--nb` samples already resident in HBM (bf16
+replica, > L2, so no flush is needed): 7 member kernels + 1 combine kernel.
 
 N > 1 (torchrun, one process per GPU): the same ensemble replicated on every
 GPU (each model data-parallel over the N devices), each rank runs its own
@@ -33,8 +34,13 @@ import numpy as np
 REPO = Path(__file__).resolve().parent
 sys.path.insert(0, str(REPO))
 
-ROSTER = [("mlp512", [784, 512, 10], 11), ("mlp384", [784, 384, 10], 12),
-          ("mlp256", [784, 256, 10], 13), ("mlp128", [784, 128, 10], 14)]
+# (name, kind, widths, weight seed); SURVEY.md §8-D "cfg2 = {MLP-256,
+# MLP-512-512, MLP-1024, CNN-s}"
+ROSTER = [("mlp256", "mlp", [784, 256, 10], 11), ("mlp512x2", "mlp", [784, 512, 512, 10], 12),
+          ("mlp1024", "mlp", [784, 1024, 10], 13), ("cnn-s", "cnn", [28, 4, 64, 32, 128, 10], 14)]
+WORKLOAD = ("cfg2: 4 heterogeneous MLP/CNN members (784-256-10, 784-512-512-10, 784-1024-10, "
+            "CNN-s 28x28-c4x4/4:64-c3x3:32-128-10) co-located on 1 B200, batches from bounded "
+            "greedy over calib_data; avg of softmax + argmax")
 MENU = [8, 16, 32, 64, 128]
 PEAKS_PATH = REPO / "MEASURED_PEAKS.json"
 PROFILE_TRAFFIC = REPO / "profiles" / "roofline_traffic.json"
@@ -174,8 +180,19 @@ def rank_shard(es, world: int, rank: int, batches: list, nb_per_gpu: int, seg: i
 
 
 # ------------------------------------------------------------------ workload
+def roster_models(es):
+    out = []
+    for i, (name, kind, w, seed) in enumerate(ROSTER):
+        if kind == "cnn":
+            out.append(es.cnn_model(i, name, seed, S=w[0], P=w[1], c1=w[2], c2=w[3], hidden=w[4],
+                                    classes=w[5]))
+        else:
+            out.append(es.mlp_model(i, name, w, seed))
+    return out
+
+
 def make_cluster(es, devices: int = 1):
-    models = [es.mlp_model(i, n, w, s) for i, (n, w, s) in enumerate(ROSTER)]
+    models = roster_models(es)
     devs = [es.DeviceSpec(d, es.GPU, 183359.0, 1e15, 0.0) for d in range(devices)]
     return es.ClusterSpec(devs, models, list(MENU), 128)
 
@@ -197,38 +214,76 @@ def choose_matrix(es, cluster, local_gpu: int, calib_nb: int, seed: int) -> dict
             "greedy_s": time.time() - t0, "bbs": bbs}
 
 
-def roofline_for(es, cluster, A, member_ms: list, nb: int, pk: dict) -> dict:
-    """Dominant kernel = the member kernel with the largest device time."""
-    i = int(np.argmax(member_ms))
+def launch_work(arch, names: list) -> list:
+    """Algorithmic (FLOP, HBM bytes) per sample of each member launch, in
+    launch order (DeviceMember::kernel_names): bytes = bf16 input row + the
+    launch's output row (bf16 activations, fp32 logits); weights are read once
+    per launch and amortised over the samples."""
+    dims = arch.layer_dims()
+    if arch.kind == "cnn":
+        G2 = (arch.widths[0] // arch.widths[1]) ** 2
+        flops = [2 * G2 * a * b if l < 2 else 2 * a * b for l, (a, b) in enumerate(dims)]
+        widths = [arch.widths[0] ** 2, G2 * arch.widths[2], G2 * arch.widths[3]] + \
+            [b for _, b in dims[2:]]
+    else:
+        flops = [2 * a * b for a, b in dims]
+        widths = [dims[0][0]] + [b for _, b in dims]
+    L = len(dims)
+    out, l = [], 0
+    for n in names:
+        take = 2 if n.startswith("conv_stack") or n.startswith("member_mlp2") or \
+            n.startswith("mlp2_simt") else 1
+        f = float(sum(flops[l:l + take]))
+        last = l + take == L
+        b = widths[l] * 2 + widths[l + take] * (4 if last else 2)
+        out.append((f, float(b)))
+        l += take
+    return out
+
+
+def roofline_for(es, cluster, A, kernels: list, nb: int, pk: dict) -> dict:
+    """Dominant kernel = the member launch with the largest device time.
+    kernels: per worker [(name, ms)] averaged over the timed steps."""
     workers = [(d, m) for d in range(A.device_count()) for m in range(A.model_count())
                if A.at(d, m)]
-    m = workers[i][1]
-    arch = cluster.models[m].arch
-    flops = arch.flops_per_sample() * nb
-    achieved = flops / (member_ms[i] * 1e-3) / 1e12
-    peak = pk["bf16_tflops_sustained"]
-    traffic = None
+    peak_t, peak_b = pk["bf16_tflops_sustained"], pk["hbm_gbs"]
+    ridge = peak_t * 1e12 / (peak_b * 1e9)
+    traffic_db = {}
     try:
-        t = json.loads(PROFILE_TRAFFIC.read_text())
-        traffic = t.get(cluster.models[m].name)
+        traffic_db = json.loads(PROFILE_TRAFFIC.read_text())
     except Exception:
         pass
-    x_bytes = 784 * 2 * nb
-    per_kernel = []
+    per_kernel, best = [], None
     for j, (d, mm) in enumerate(workers):
-        a = cluster.models[mm].arch
-        tf = a.flops_per_sample() * nb / (member_ms[j] * 1e-3) / 1e12
-        gbs = (x_bytes + nb * 40) / (member_ms[j] * 1e-3) / 1e9
-        per_kernel.append({"member": cluster.models[mm].name, "batch": A.at(d, mm),
-                           "ms": round(member_ms[j], 4), "tflops": round(tf, 1),
-                           "tensor_frac": round(tf / peak, 3), "hbm_gbs": round(gbs, 1),
-                           "hbm_frac": round(gbs / pk["hbm_gbs"], 3)})
-    return {"bound": "tensor", "kernel": f"member_mlp2_sm100[{cluster.models[m].name}]",
-            "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s",
-            "frac": round(achieved / peak, 4), "traffic": traffic,
-            "algorithmic_per_launch": {"flop": flops, "flop_per_sample": arch.flops_per_sample(),
+        model = cluster.models[mm]
+        work = launch_work(model.arch, [n for n, _ in kernels[j]])
+        for (name, ms), (f, b) in zip(kernels[j], work):
+            tf = f * nb / (ms * 1e-3) / 1e12
+            gbs = b * nb / (ms * 1e-3) / 1e9
+            bound = "tensor" if f / b >= ridge else "hbm"
+            frac = tf / peak_t if bound == "tensor" else gbs / peak_b
+            row = {"member": model.name, "kernel": name, "batch": A.at(d, mm),
+                   "ms": round(ms, 4), "tflops": round(tf, 1), "tensor_frac": round(tf / peak_t, 3),
+                   "hbm_gbs": round(gbs, 1), "hbm_frac": round(gbs / peak_b, 3),
+                   "flop_per_sample": f, "bytes_per_sample": b, "bound": bound,
+                   "frac": round(frac, 4)}
+            per_kernel.append(row)
+            if best is None or ms > best["ms"]:
+                best = row
+    key = f"{best['member']}/{best['kernel']}"
+    tensor = best["bound"] == "tensor"
+    achieved = best["tflops"] if tensor else best["hbm_gbs"]
+    peak = peak_t if tensor else peak_b
+    return {"bound": best["bound"], "kernel": f"{best['kernel']}[{best['member']}]",
+            "achieved": achieved, "peak": peak, "unit": "TFLOP/s" if tensor else "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": traffic_db.get(key),
+            "algorithmic_per_launch": {"flop": best["flop_per_sample"] * nb,
+                                       "bytes": best["bytes_per_sample"] * nb,
+                                       "flop_per_sample": best["flop_per_sample"],
+                                       "bytes_per_sample": best["bytes_per_sample"],
                                        "samples": nb},
-            "peak_source": f"{pk['source']} bf16 dense, sustained (kernel timed inside a long step)",
+            "peak_source": f"{pk['source']} " + ("bf16 dense, sustained (kernel timed inside a "
+                                                 "long step)" if tensor else "HBM copy"),
             "per_kernel": per_kernel}
 
 
@@ -292,6 +347,7 @@ def run_b200(args, dist: Dist) -> dict | None:
     launches = 0
     step_s = []
     member_ms = np.zeros(system.worker_count())
+    kern = [None] * system.worker_count()
     combine_ms = 0.0
     dist.barrier()
     with ClockSampler(gpu) as clocks:
@@ -303,12 +359,17 @@ def run_b200(args, dist: Dist) -> dict | None:
             ms, cm = system.timing()
             member_ms += np.asarray(ms)
             combine_ms += cm
+            for w in range(system.worker_count()):
+                kt = system.kernel_timing(w)
+                kern[w] = kt if kern[w] is None else [(n, a + b) for (n, a), (_, b)
+                                                      in zip(kern[w], kt)]
         wall = time.perf_counter() - t0
     dist.barrier()
     device_s = dist.max(float(sum(step_s)))
     covered = sum(dist.gather([local_nb]), [])
     member_ms /= args.steps
     combine_ms /= args.steps
+    kern = [[(n, t / args.steps) for n, t in k] for k in kern]
 
     # e2e: host (pinned) X in, combined probabilities + labels out, per step
     e2e_nb = max(1, min(args.e2e_nb, args.nb))
@@ -328,7 +389,11 @@ def run_b200(args, dist: Dist) -> dict | None:
     for _ in range(max(1, args.warmup // 2) if args.e2e else 0):
         system.run_host(Xh, Yh, Lh)
     dist.barrier()
-    e2e_s = [system.run_host(Xh, Yh, Lh) for _ in range(e2e_steps)]
+    e2e_s, h2d, d2h = [], 0, 0
+    for _ in range(e2e_steps):
+        e2e_s.append(system.run_host(Xh, Yh, Lh))
+        hb, db = system.last_transfer()
+        h2d, d2h = h2d + hb, d2h + db
     dist.barrier()
     e2e_total = dist.max(float(sum(e2e_s)))
     system.close()
@@ -351,8 +416,7 @@ def run_b200(args, dist: Dist) -> dict | None:
         "dtype": "bf16",
         "data": "synthetic (U[0,1) features generated on device; Glorot-uniform synthetic weights)",
         "config": {
-            "workload": "cfg2: 4 heterogeneous MLP members (784-{512,384,256,128}-10) co-located on "
-                        "1 B200, batches from bounded greedy over calib_data; avg of softmax + argmax",
+            "workload": WORKLOAD,
             "samples_per_gpu_per_step": args.nb,
             "x_bytes_per_gpu": args.nb * 784 * 2,
             "l2": "inputs (bf16 X) larger than L2, no flush",
@@ -366,13 +430,16 @@ def run_b200(args, dist: Dist) -> dict | None:
             "parallelism": f"ensemble replicated per GPU, dp{n} over samples",
             "segment_size": 128,
         },
-        "roofline": roofline_for(es, cluster, A, list(member_ms), args.nb, pk),
+        "roofline": roofline_for(es, cluster, A, kern, args.nb, pk),
+        "member_ms": [round(float(x), 4) for x in member_ms],
         "combine_ms": round(combine_ms, 4),
-        "combine_hbm_gbs": round(args.nb * (4 * 40 + 44) / (combine_ms * 1e-3) / 1e9, 1)
+        "combine_hbm_gbs": round(args.nb * (len(ROSTER) * 40 + 44) / (combine_ms * 1e-3) / 1e9, 1)
         if combine_ms > 0 else None,
         "e2e": {"value": round(n * e2e_nb * e2e_steps / e2e_total, 1), "unit": "samples/s",
-                "h2d_bytes_per_step": e2e_nb * 784 * 4,
-                "d2h_bytes_per_step": e2e_nb * (10 * 4 + 4),
+                "h2d_bytes_per_step": h2d // e2e_steps,
+                "d2h_bytes_per_step": d2h // e2e_steps,
+                "input": "pinned fp32 X; chunks alternate host fp32->bf16 conversion (2 B/feature "
+                         "on the wire) and fp32 DMA + device conversion",
                 "samples_per_step": e2e_nb},
         "gpu_launches": launches,
         "clocks": clocks.summary(),
@@ -404,7 +471,7 @@ def run_reference(args, dist: Dist) -> dict | None:
         "value": value, "unit": "samples/s", "n_gpus": dist.world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32 (bf16-quantised operands)",
-        "data": "synthetic", "config": {"workload": "cfg2 roster on host cores (reference runtime)"},
+        "data": "synthetic", "config": {"workload": WORKLOAD + " -- on host cores (reference runtime)"},
         "cpu_baseline": base,
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},

@@ -234,6 +234,13 @@ es_status es_system_info(es_system* s, int* workers, int* workers_per_model, int
                          int* combine_device);
 /* Device time of each worker's member kernel and of the combine, last run. */
 es_status es_system_timing(es_system* s, double* member_ms, double* combine_ms);
+/* Host<->device bytes the last es_system_run_host moved. */
+es_status es_system_last_transfer(es_system* s, size_t* h2d_bytes, size_t* d2h_bytes);
+/* Per-launch device time of one worker's member kernels in the last run
+ * (ms[cap], -1 where the worker had no rows), their kernel names joined by
+ * ';' into names[names_len], and the launch count per run. */
+es_status es_system_kernel_timing(es_system* s, int worker, double* ms, char* names,
+                                  size_t names_len, int cap, int* count);
 es_status es_system_shutdown(es_system* s);
 void es_system_destroy(es_system* s);
 

@@ -120,6 +120,9 @@ _SIGS = {
     "es_host_convert_bf16": (C.c_int, [c_float_p, C.POINTER(C.c_uint16), C.c_size_t]),
     "es_system_info":(C.c_int, [C.c_void_p, c_int_p, c_int_p, c_int_p, c_int_p]),
     "es_system_timing": (C.c_int, [C.c_void_p, c_double_p, c_double_p]),
+    "es_system_last_transfer": (C.c_int, [C.c_void_p, c_size_t_p, c_size_t_p]),
+    "es_system_kernel_timing": (C.c_int, [C.c_void_p, C.c_int, c_double_p, C.c_char_p,
+                                          C.c_size_t, C.c_int, c_int_p]),
     "es_system_shutdown": (C.c_int, [C.c_void_p]),
     "es_system_destroy": (None, [C.c_void_p]),
     "es_run_inference": (C.c_int, [C.POINTER(ClusterDesc), c_int_p, C.POINTER(RuleDesc),

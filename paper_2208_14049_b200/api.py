@@ -702,6 +702,21 @@ class InferenceSystem:
         _check(lib().es_system_timing(self._h, ms, C.byref(cm)))
         return list(ms)[:w], cm.value
 
+    def last_transfer(self) -> tuple:
+        """(h2d_bytes, d2h_bytes) moved by the last run_host."""
+        h, d = C.c_size_t(), C.c_size_t()
+        _check(lib().es_system_last_transfer(self._h, C.byref(h), C.byref(d)))
+        return h.value, d.value
+
+    def kernel_timing(self, worker: int) -> list:
+        """[(kernel name, ms)] of one worker's launches in the last run (CUDA
+        events recorded on the worker's stream between launches)."""
+        ms = (C.c_double * 16)()
+        names = C.create_string_buffer(512)
+        n = C.c_int()
+        _check(lib().es_system_kernel_timing(self._h, worker, ms, names, 512, 16, C.byref(n)))
+        return list(zip(names.value.decode().split(";"), list(ms)[:n.value]))
+
     def begin_run(self, X: SampleStore, rule: CombinationRule = None) -> None:
         keep: list = []
         self._store = X

@@ -570,6 +570,34 @@ es_status es_system_timing(es_system* s, double* member_ms, double* combine_ms) 
   });
 }
 
+es_status es_system_last_transfer(es_system* s, size_t* h2d_bytes, size_t* d2h_bytes) {
+  return guard([&] {
+    need(s != nullptr, "NULL handle");
+    if (h2d_bytes) *h2d_bytes = s->sys->h2d_bytes_last();
+    if (d2h_bytes) *d2h_bytes = s->sys->d2h_bytes_last();
+    return ES_OK;
+  });
+}
+
+es_status es_system_kernel_timing(es_system* s, int worker, double* ms, char* names,
+                                  size_t names_len, int cap, int* count) {
+  return guard([&] {
+    need(s != nullptr, "NULL handle");
+    need(worker >= 0 && worker < s->sys->worker_count(), "worker out of range");
+    const std::vector<double> t = s->sys->last_kernel_ms(worker);
+    const std::vector<std::string> n = s->sys->kernel_names(worker);
+    if (count) *count = static_cast<int>(n.size());
+    for (int i = 0; ms && i < cap && i < static_cast<int>(n.size()); ++i)
+      ms[i] = i < static_cast<int>(t.size()) ? t[i] : -1.0;
+    if (names && names_len) {
+      std::string joined;
+      for (std::size_t i = 0; i < n.size(); ++i) joined += (i ? ";" : "") + n[i];
+      std::snprintf(names, names_len, "%s", joined.c_str());
+    }
+    return ES_OK;
+  });
+}
+
 es_status es_system_shutdown(es_system* s) {
   return guard([&] {
     need(s != nullptr, "NULL handle");

@@ -16,13 +16,21 @@ using namespace sm100;
 
 namespace {
 
-// w0 TMA producer, w1 UMMA issuer, w2..w5 conv1 epilogue, w6..w9 im2col
-// builders + conv2 epilogue (each group covers the four TMEM lane quadrants).
+// w0 TMA producer + im2col builder, w1 UMMA issuer, w2..w5 conv1 epilogue,
+// w6..w9 conv2 epilogue (each group covers the four TMEM lane quadrants).
 // Ten warps: extra role warps share the UMMA warp's sub-partition and slow its
 // issue loop down (measured with tools/trace_conv.cu).
 constexpr int kThreads = 320;
+// split schedule: four more conv2-epilogue warps (10-13), see epi2_split.
+template <bool SPLIT>
+constexpr int threads_for() { return SPLIT ? 448 : kThreads; }
 constexpr uint32_t kSmemBudget = 232448;
 constexpr int kMargin = 16;  // zero rows before/after the tile's grids; taps reach R+1 rows
+constexpr int kXchStride = 20;  // fp32 per exchanged row (16 + 4: conflict-free 16-byte stores)
+
+__device__ __forceinline__ void epi2_bar(int group) {  // four conv2-epilogue warps
+  asm volatile("bar.sync %0, 128;" ::"r"(1 + group) : "memory");
+}
 
 // bf16x2 {relu(a + ba), relu(b + bb)} (a in the low half), one cvt.relu.
 __device__ __forceinline__ uint32_t pack_relu_bf16(uint32_t a, uint32_t b, float ba, float bb) {
@@ -46,13 +54,12 @@ __device__ __forceinline__ unsigned long long global_ns() {
   } while (0)
 
 // KP2 = c1 / 16: K steps per tap, unrolled so the issue loop is pure uniform
-// adds (tools/umma_rate.cu).
-template <int KP2>
-__global__ void __launch_bounds__(kThreads, 1)
+// adds (tools/umma_rate.cu).  SPLIT: the conv2 schedule (conv_kernel.cuh).
+template <int KP2, bool SPLIT>
+__global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
     conv_stack_sm100(const __grid_constant__ CUtensorMap tm_x, const ConvArgs args) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   const ConvLayout& L = args.L;
   uint8_t* sRaw = smem + L.off_raw;
   uint8_t* sA1 = smem + L.off_a1;
@@ -61,9 +68,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sW2 = smem + L.off_w2;
   float* sB1 = reinterpret_cast<float*>(smem + L.off_b1);
   float* sB2 = reinterpret_cast<float*>(smem + L.off_b2);
+  int* sRowOff = reinterpret_cast<int*>(smem + L.off_rows);  // im2col source offset per row
   uint64_t* raw_full = reinterpret_cast<uint64_t*>(smem + L.off_bar);
-  uint64_t* raw_empty = raw_full + L.raw_stages;
-  uint64_t* a1_full = raw_empty + L.raw_stages;  // every pair below: one per buffer
+  uint64_t* a1_full = raw_full + 2 * L.raw_stages;  // every pair below: one per buffer
   uint64_t* a1_empty = a1_full + 2;
   uint64_t* c1_full = a1_empty + 2;
   uint64_t* c1_empty = c1_full + 2;
@@ -83,17 +90,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < L.raw_stages; ++s) {
       mbar_init(&raw_full[s], 1);
-      mbar_init(&raw_empty[s], 128);
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&a1_full[b], 128);
+      mbar_init(&a1_full[b], 1);
       mbar_init(&a1_empty[b], 1);
       mbar_init(&c1_full[b], 1);
       mbar_init(&c1_empty[b], 4);
       mbar_init(&a2_full[b], 128);
       mbar_init(&a2_empty[b], 1);
       mbar_init(&c2_full[b], 1);
-      mbar_init(&c2_empty[b], 4);
+      mbar_init(&c2_empty[b], SPLIT ? 8 : 4);
     }
     fence_barrier_init();
   }
@@ -105,19 +111,32 @@ __global__ void __launch_bounds__(kThreads, 1)
   // conv1 epilogue only ever rewrites interior rows, so borders stay zero.
   {
     const uint4* w1 = static_cast<const uint4*>(args.w1);  // [c1][16] bf16 = 2 chunks per row
-    for (int i = threadIdx.x; i < L.c1 * 2; i += kThreads) {
+    for (int i = threadIdx.x; i < L.c1 * 2; i += threads_for<SPLIT>()) {
       const int o = i >> 1, k = i & 1;
       *reinterpret_cast<uint4*>(sW1 + (k * L.c1 + o) * 16) = w1[i];
     }
     const uint4* w2 = static_cast<const uint4*>(args.w2);  // [c2][9*c1] bf16 = 9*kp chunks per row
-    for (int i = threadIdx.x; i < 9 * kp * L.c2; i += kThreads) {
+    for (int i = threadIdx.x; i < 9 * kp * L.c2; i += threads_for<SPLIT>()) {
       const int o = i / (9 * kp), rem = i % (9 * kp);  // rem = tap * kp + plane
-      *reinterpret_cast<uint4*>(sW2 + (rem * L.c2 + o) * 16) = w2[i];
+      if (SPLIT) {
+        // [dw][plane][g*c2 + o]: B of UMMA (dw, K step) holds the three dh taps.
+        const int tap = rem / kp, plane = rem % kp, g = tap / 3, dwi = tap % 3;
+        *reinterpret_cast<uint4*>(sW2 + ((dwi * kp + plane) * L.n2 + g * L.c2 + o) * 16) = w2[i];
+      } else {
+        *reinterpret_cast<uint4*>(sW2 + (rem * L.c2 + o) * 16) = w2[i];
+      }
     }
-    for (int i = threadIdx.x; i < L.c1; i += kThreads) sB1[i] = args.b1[i];
-    for (int i = threadIdx.x; i < L.c2; i += kThreads) sB2[i] = args.b2[i];
+    for (int r = threadIdx.x; r < L.T * L.G * L.G; r += threads_for<SPLIT>()) {
+      const int G2r = L.G * L.G, n = r / G2r, p = r % G2r, i = p / L.G, j = p % L.G;
+      sRowOff[r] = (n * L.S * L.S + (4 * i) * L.S + 4 * j) * 2;  // patch (i, j) of sample n
+    }
+    for (int i = threadIdx.x; i < L.c1; i += threads_for<SPLIT>()) sB1[i] = args.b1[i];
+    for (int i = threadIdx.x; i < L.c2; i += threads_for<SPLIT>()) sB2[i] = args.b2[i];
+    if (SPLIT)
+      for (int i = threadIdx.x; i < kXchStride; i += threads_for<SPLIT>())
+        reinterpret_cast<float*>(smem + L.off_xch)[2 * 2 * 4 * 2 * L.R * kXchStride + i] = 0.0f;
     uint4* z = reinterpret_cast<uint4*>(sA2);
-    for (int i = threadIdx.x; i < static_cast<int>(2 * L.a2_bytes / 16); i += kThreads)
+    for (int i = threadIdx.x; i < static_cast<int>(2 * L.a2_bytes / 16); i += threads_for<SPLIT>())
       z[i] = make_uint4(0, 0, 0, 0);
   }
   fence_proxy_async_smem();
@@ -128,20 +147,49 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int G2 = L.G * L.G, P2 = L.R * L.R;
 
   if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      const uint64_t pol = l2_policy_evict_first();
-      const int rows16 = L.S * L.S / 16;  // the map views x as [rows * S*S/16][16]
-      for (int k = 0; k < my_tiles; ++k) {
-        const int st = k % L.raw_stages;
-        const uint32_t use = static_cast<uint32_t>(k / L.raw_stages);
-        mbar_sleep_wait(&raw_empty[st], (use & 1u) ^ 1u);
-        const long long s0 = args.row_begin + (blockIdx.x + static_cast<long long>(k) * gridDim.x) * L.T;
-        mbar_arrive_expect_tx(&raw_full[st], static_cast<uint32_t>(L.T * L.S * L.S * 2));
-        tma_load_2d(sRaw + st * L.raw_stride, &tm_x, &raw_full[st], 0,
-                    static_cast<int32_t>(s0 * rows16), pol);
-        TRACE(k, 0);
+    // ---------------------------------------------- TMA producer + im2col build
+    // One warp: lane 0 keeps raw_stages image loads in flight; the whole warp
+    // writes conv1's im2col rows of tile k (one row per output pixel: the
+    // 4x4 patch as two 16-byte K planes), then refills the freed stage.
+    // Source offsets per row come from a table, so the loop is loads/stores.
+    const uint64_t pol = l2_policy_evict_first();
+    const int rows16 = L.S * L.S / 16;  // the map views x as [rows * S*S/16][16]
+    auto load = [&](int k) {
+      const int st = k % L.raw_stages;
+      const long long s0 = args.row_begin + (blockIdx.x + static_cast<long long>(k) * gridDim.x) * L.T;
+      mbar_arrive_expect_tx(&raw_full[st], static_cast<uint32_t>(L.T * L.S * L.S * 2));
+      tma_load_2d(sRaw + st * L.raw_stride, &tm_x, &raw_full[st], 0,
+                  static_cast<int32_t>(s0 * rows16), pol);
+      TRACE(k, 0);
+    };
+    if (lane == 0)
+      for (int k = 0; k < my_tiles && k < L.raw_stages; ++k) load(k);
+    const int rows = L.T * G2;
+    for (int k = 0; k < my_tiles; ++k) {
+      const int st = k % L.raw_stages;
+      const int b = k & 1;
+      mbar_sleep_wait(&raw_full[st], static_cast<uint32_t>(k / L.raw_stages) & 1u);
+      mbar_sleep_wait(&a1_empty[b], (static_cast<uint32_t>(k >> 1) & 1u) ^ 1u);
+      if (lane == 0) TRACE(k, 4);
+      const uint8_t* raw = sRaw + st * L.raw_stride;
+      uint8_t* a1 = sA1 + b * L.a1_bytes;
+      for (int r = lane; r < rows; r += 32) {
+        const uint8_t* src = raw + sRowOff[r];
+        const uint2 v0 = *reinterpret_cast<const uint2*>(src);
+        const uint2 v1 = *reinterpret_cast<const uint2*>(src + L.S * 2);
+        const uint2 v2 = *reinterpret_cast<const uint2*>(src + L.S * 4);
+        const uint2 v3 = *reinterpret_cast<const uint2*>(src + L.S * 6);
+        *reinterpret_cast<uint4*>(a1 + r * 16) = make_uint4(v0.x, v0.y, v1.x, v1.y);
+        *reinterpret_cast<uint4*>(a1 + L.a1_plane + r * 16) = make_uint4(v2.x, v2.y, v3.x, v3.y);
       }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&a1_full[b]);
+        TRACE(k, 5);
+        if (k + L.raw_stages < my_tiles) load(k + L.raw_stages);  // stage st is free again
+      }
+      __syncwarp();
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ UMMA issuer
@@ -152,11 +200,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tbase = __shfl_sync(0xffffffffu, tmem_base, 0);
     const uint32_t a1_base = __shfl_sync(0xffffffffu, smem_u32(sA1), 0);
     const uint32_t a2_base = __shfl_sync(0xffffffffu, smem_u32(sA2), 0);
-    const uint32_t id1 = idesc_bf16_f32(128, L.c1), id2 = idesc_bf16_f32(128, L.c2);
+    const uint32_t id1 = idesc_bf16_f32(128, L.c1), id2 = idesc_bf16_f32(128, L.n2);
     const uint64_t w1d = sdesc_planar(__shfl_sync(0xffffffffu, smem_u32(sW1), 0),
                                       static_cast<uint32_t>(L.c1 * 16));
     const uint64_t w2d = sdesc_planar(__shfl_sync(0xffffffffu, smem_u32(sW2), 0),
-                                      static_cast<uint32_t>(L.c2 * 16));
+                                      static_cast<uint32_t>(L.n2 * 16));
     const uint32_t a2_step = L.a2_plane / 8;  // two planes (K += 16), in 16-byte units
     auto conv1 = [&](int k) {
       const int b = k & 1;
@@ -176,7 +224,41 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       __syncwarp();
     };
+    auto conv2_split = [&](int k) {
+      // One accumulator slot per 128-row block, alternating over the running
+      // block count: the epilogue of block i overlaps the UMMAs of block i+1.
+      const int b = k & 1;
+      const uint32_t u = static_cast<uint32_t>(k >> 1) & 1u;
+      mbar_sleep_wait(&a2_full[b], u);
+      TRACE(k, 2);
+      const uint64_t ad0 = sdesc_planar(a2_base + b * L.a2_bytes, L.a2_plane);
+      for (int mb = 0; mb < L.mb2; ++mb) {
+        const int blk = k * L.mb2 + mb, sl = blk & 1;
+        mbar_sleep_wait(&c2_empty[sl], (static_cast<uint32_t>(blk >> 1) & 1u) ^ 1u);
+        tc_fence_after();
+        const uint32_t d = tbase + static_cast<uint32_t>(2 * L.tmem_c1 + sl * L.n2);
+        const uint64_t adm = ad0 + static_cast<uint64_t>(kMargin + mb * 128);
+#pragma unroll
+        for (int dwi = 0; dwi < 3; ++dwi)
+#pragma unroll
+          for (int j = 0; j < KP2; ++j) {
+            const uint64_t ad = adm + static_cast<uint64_t>(dwi - 1 + j * static_cast<int>(a2_step));
+            const uint64_t bd = w2d + static_cast<uint64_t>((dwi * KP2 + j) * 2 * L.n2);
+            if (elect_one()) umma_bf16(d, ad, bd, id2, (dwi | j) != 0);
+          }
+        if (elect_one()) {
+          if (mb == L.mb2 - 1) umma_commit(&a2_empty[b]);
+          umma_commit(&c2_full[sl]);
+        }
+        __syncwarp();
+      }
+      TRACE(k, 3);
+    };
     auto conv2 = [&](int k) {
+      if (SPLIT) {
+        conv2_split(k);
+        return;
+      }
       const int b = k & 1;
       const uint32_t u = static_cast<uint32_t>(k >> 1) & 1u;
       mbar_sleep_wait(&a2_full[b], u);
@@ -233,17 +315,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int grow = kMargin + n * P2 + (i + 1) * L.R + (j + 1);
         for (int c0 = 0; c0 < L.c1; c0 += 32) {
           uint32_t v[32];
-          tmem_ld32_raw(tmem_base + lane_field + static_cast<uint32_t>(b * L.tmem_c1 + mb * L.c1 + c0), v);
-          tmem_ld_wait();
-          if (r < rows) {
+          if (args.debug & 1) {
+#pragma unroll
+            for (int c = 0; c < 32; ++c) v[c] = static_cast<uint32_t>(c);
+          } else {
+            tmem_ld32_raw(tmem_base + lane_field + static_cast<uint32_t>(b * L.tmem_c1 + mb * L.c1 + c0), v);
+            tmem_ld_wait();
+          }
+          if (r < rows && !(args.debug & 2)) {
 #pragma unroll
             for (int g = 0; g < 4; ++g) {
               const int c = g * 8;
-              const float* bias = sB1 + c0 + c;
-              const uint4 pk = make_uint4(pack_relu_bf16(v[c], v[c + 1], bias[0], bias[1]),
-                                          pack_relu_bf16(v[c + 2], v[c + 3], bias[2], bias[3]),
-                                          pack_relu_bf16(v[c + 4], v[c + 5], bias[4], bias[5]),
-                                          pack_relu_bf16(v[c + 6], v[c + 7], bias[6], bias[7]));
+              const float4 bl = *reinterpret_cast<const float4*>(sB1 + c0 + c);
+              const float4 bh = *reinterpret_cast<const float4*>(sB1 + c0 + c + 4);
+              const uint4 pk = make_uint4(pack_relu_bf16(v[c], v[c + 1], bl.x, bl.y),
+                                          pack_relu_bf16(v[c + 2], v[c + 3], bl.z, bl.w),
+                                          pack_relu_bf16(v[c + 4], v[c + 5], bh.x, bh.y),
+                                          pack_relu_bf16(v[c + 6], v[c + 7], bh.z, bh.w));
               *reinterpret_cast<uint4*>(a2 + (c0 / 8 + g) * L.a2_plane + grow * 16) = pk;
             }
           }
@@ -257,39 +345,124 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (ta == 0) TRACE(k, 7);
     }
   } else {
-    // ----------------------------------- im2col builders + conv2 epilogue
-    const int ta = threadIdx.x - 192;  // 0..127
+    // ---------------------------------------------------------- conv2 epilogue
     const int q = warp & 3;
     const uint32_t lane_field = static_cast<uint32_t>(q * 32) << 16;
     const int row_bytes = G2 * L.c2 * 2;
-    auto build = [&](int k) {
-      const int st = k % L.raw_stages;
-      const uint32_t ru = static_cast<uint32_t>(k / L.raw_stages) & 1u;
-      const int b = k & 1;
-      const uint32_t u = static_cast<uint32_t>(k >> 1) & 1u;
-      mbar_sleep_wait(&raw_full[st], ru);
-      mbar_sleep_wait(&a1_empty[b], u ^ 1u);
-      if (ta == 0) TRACE(k, 4);
-      const uint8_t* raw = sRaw + st * L.raw_stride;
-      uint8_t* a1 = sA1 + b * L.a1_bytes;
-      const int rows = L.T * G2;
-      for (int r = ta; r < rows; r += 128) {
-        const int n = r / G2, p = r % G2, i = p / L.G, j = p % L.G;
-        // Patch row a of pixel block (i, j): 4 bf16 = 8 bytes, K index a*4 + b.
-        const uint8_t* src = raw + (static_cast<size_t>(n) * L.S * L.S + (4 * i) * L.S + 4 * j) * 2;
-        const uint2 v0 = *reinterpret_cast<const uint2*>(src);
-        const uint2 v1 = *reinterpret_cast<const uint2*>(src + L.S * 2);
-        const uint2 v2 = *reinterpret_cast<const uint2*>(src + L.S * 4);
-        const uint2 v3 = *reinterpret_cast<const uint2*>(src + L.S * 6);
-        *reinterpret_cast<uint4*>(a1 + r * 16) = make_uint4(v0.x, v0.y, v1.x, v1.y);
-        *reinterpret_cast<uint4*>(a1 + L.a1_plane + r * 16) = make_uint4(v2.x, v2.y, v3.x, v3.y);
+    // split: out[q] = D[q-R][g0] + D[q][g1] + D[q+R][g2] (conv_kernel.cuh).
+    // Eight warps: group eg = 0 (warps 6-9) takes channels
+    // [0, c2/2), group 1 (warps 10-13) [c2/2, c2), 16 at a time.
+    const int eg = (warp - 6) >> 2;
+    float* xch = reinterpret_cast<float*>(smem + L.off_xch);
+    int xi = 0;  // running exchange count: xch buffer = xi & 1
+    auto epi2_split = [&](int k) {
+      const long long s0 = args.row_begin + (blockIdx.x + static_cast<long long>(k) * gridDim.x) * L.T;
+      const int R = L.R;
+      const int xrow = 2 * R * kXchStride;  // one quadrant's [2][R][kXchStride]
+      const int zrow = 2 * 2 * 4 * xrow;    // the zero row after both buffers
+      for (int mb = 0; mb < L.mb2; ++mb) {
+        const int blk = k * L.mb2 + mb, sl = blk & 1;
+        mbar_sleep_wait(&c2_full[sl], static_cast<uint32_t>(blk >> 1) & 1u);
+        if (warp == 6 && lane == 0 && mb == 0) TRACE(k, 8);
+        if (warp == 6 && lane == 0) TRACE(k, 10 + 3 * mb);
+        tc_fence_after();
+        const int r = mb * 128 + q * 32 + lane;  // grid row of the tile
+        const int n = r / P2, rr = r % P2, h = rr / R, w = rr % R;
+        const bool valid = r < L.T * P2 && h >= 1 && w >= 1 && s0 + n < args.row_end;
+        uint8_t* dst = static_cast<uint8_t*>(args.out) + (s0 + n) * row_bytes +
+                       ((h - 1) * L.G + (w - 1)) * L.c2 * 2;
+        const uint32_t col = tmem_base + lane_field + static_cast<uint32_t>(2 * L.tmem_c1 + sl * L.n2);
+        const bool take_up = lane < R, take_dn = lane >= 32 - R;
+        for (int c0 = eg * (L.c2 >> 1); c0 < (eg + 1) * (L.c2 >> 1); c0 += 16) {
+          uint32_t r0[16], r1[16], r2[16];
+          if (args.debug & 4) {
+#pragma unroll
+            for (int c = 0; c < 16; ++c) r0[c] = r1[c] = r2[c] = static_cast<uint32_t>(c + lane);
+          } else {
+            tmem_ld16_raw(col + static_cast<uint32_t>(c0), r0);
+            tmem_ld16_raw(col + static_cast<uint32_t>(L.c2 + c0), r1);
+            tmem_ld16_raw(col + static_cast<uint32_t>(2 * L.c2 + c0), r2);
+            tmem_ld_wait();
+          }
+          float g0[16], g1[16], g2[16];
+#pragma unroll
+          for (int c = 0; c < 16; ++c) {
+            g0[c] = __uint_as_float(r0[c]);
+            g1[c] = __uint_as_float(r1[c]);
+            g2[c] = __uint_as_float(r2[c]);
+          }
+          // Rows crossing a lane-quadrant boundary: the last R lanes publish
+          // their g0 partials (read by the next quadrant's first R lanes),
+          // the first R lanes their g2 partials (read by the previous one's
+          // last R lanes).
+          const int xbuf = ((xi & 1) * 2 + eg) * 4 * xrow;
+          ++xi;
+          const bool xon = !(args.debug & 8);
+          if (take_dn && xon) {
+            float* d0 = xch + xbuf + q * xrow + (lane - (32 - R)) * kXchStride;
+#pragma unroll
+            for (int c = 0; c < 16; c += 4)
+              *reinterpret_cast<float4*>(d0 + c) = make_float4(g0[c], g0[c + 1], g0[c + 2], g0[c + 3]);
+          }
+          if (take_up && xon) {
+            float* d2 = xch + xbuf + q * xrow + (R + lane) * kXchStride;
+#pragma unroll
+            for (int c = 0; c < 16; c += 4)
+              *reinterpret_cast<float4*>(d2 + c) = make_float4(g2[c], g2[c + 1], g2[c + 2], g2[c + 3]);
+          }
+          if (xon) epi2_bar(eg);
+          if (warp == 6 && lane == 0) TRACE(k, 11 + 3 * mb);
+          // Branch-free: lanes that take their partner from a shuffle read the
+          // zero row (one broadcast address) instead of an exchanged row.
+          const float* up_src =
+              xch + ((take_up && q > 0) ? xbuf + (q - 1) * xrow + lane * kXchStride : zrow);
+          const float* dn_src =
+              xch + ((take_dn && q < 3) ? xbuf + (q + 1) * xrow + (R + lane - (32 - R)) * kXchStride
+                                        : zrow);
+          float v[16];
+          if (!xon) {
+#pragma unroll
+            for (int c = 0; c < 16; ++c) v[c] = g0[c] + g1[c] + g2[c];
+          } else
+#pragma unroll
+          for (int c = 0; c < 16; c += 4) {
+            const float4 u4 = *reinterpret_cast<const float4*>(up_src + c);
+            const float4 d4 = *reinterpret_cast<const float4*>(dn_src + c);
+            const float ux[4] = {u4.x, u4.y, u4.z, u4.w}, dx[4] = {d4.x, d4.y, d4.z, d4.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float up = __shfl_up_sync(0xffffffffu, g0[c + e], R);
+              const float dn = __shfl_down_sync(0xffffffffu, g2[c + e], R);
+              v[c + e] = g1[c + e] + (take_up ? ux[e] : up) + (take_dn ? dx[e] : dn);
+            }
+          }
+          if (warp == 6 && lane == 0) TRACE(k, 12 + 3 * mb);
+          if (valid && !(args.debug & 16)) {
+#pragma unroll
+            for (int g = 0; g < 2; ++g) {
+              const int c = g * 8;
+              const float4 bl = *reinterpret_cast<const float4*>(sB2 + c0 + c);
+              const float4 bh = *reinterpret_cast<const float4*>(sB2 + c0 + c + 4);
+              const uint4 pk = make_uint4(
+                  pack_relu_bf16(__float_as_uint(v[c]), __float_as_uint(v[c + 1]), bl.x, bl.y),
+                  pack_relu_bf16(__float_as_uint(v[c + 2]), __float_as_uint(v[c + 3]), bl.z, bl.w),
+                  pack_relu_bf16(__float_as_uint(v[c + 4]), __float_as_uint(v[c + 5]), bh.x, bh.y),
+                  pack_relu_bf16(__float_as_uint(v[c + 6]), __float_as_uint(v[c + 7]), bh.z, bh.w));
+              *reinterpret_cast<uint4*>(dst + (c0 + c) * 2) = pk;
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&c2_empty[sl]);
       }
-      fence_proxy_async_smem();
-      mbar_arrive(&raw_empty[st]);
-      mbar_arrive(&a1_full[b]);
-      if (ta == 0) TRACE(k, 5);
+      if (warp == 6 && lane == 0) TRACE(k, 9);
     };
     auto epi2 = [&](int k) {
+      if (SPLIT) {
+        epi2_split(k);
+        return;
+      }
       const int b = k & 1;
       const uint32_t u = static_cast<uint32_t>(k >> 1) & 1u;
       mbar_sleep_wait(&c2_full[b], u);
@@ -312,11 +485,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int g = 0; g < 4; ++g) {
               const int c = g * 8;
-              const float* bias = sB2 + c0 + c;
-              const uint4 pk = make_uint4(pack_relu_bf16(v[c], v[c + 1], bias[0], bias[1]),
-                                          pack_relu_bf16(v[c + 2], v[c + 3], bias[2], bias[3]),
-                                          pack_relu_bf16(v[c + 4], v[c + 5], bias[4], bias[5]),
-                                          pack_relu_bf16(v[c + 6], v[c + 7], bias[6], bias[7]));
+              const float4 bl = *reinterpret_cast<const float4*>(sB2 + c0 + c);
+              const float4 bh = *reinterpret_cast<const float4*>(sB2 + c0 + c + 4);
+              const uint4 pk = make_uint4(pack_relu_bf16(v[c], v[c + 1], bl.x, bl.y),
+                                          pack_relu_bf16(v[c + 2], v[c + 3], bl.z, bl.w),
+                                          pack_relu_bf16(v[c + 4], v[c + 5], bh.x, bh.y),
+                                          pack_relu_bf16(v[c + 6], v[c + 7], bh.z, bh.w));
               *reinterpret_cast<uint4*>(dst + (c0 + c) * 2) = pk;
             }
           }
@@ -330,11 +504,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // conv1 of tile k+1 is issued before conv2 of tile k, so builds run two
     // tiles ahead: the build of tile k+1 never waits behind the epilogue of
     // tile k-1 (which waits for conv2 of tile k-1).
-    for (int k = 0; k < my_tiles && k < 2; ++k) build(k);
-    for (int k = 0; k < my_tiles; ++k) {
-      if (k + 2 < my_tiles) build(k + 2);
-      epi2(k);
-    }
+    for (int k = 0; k < my_tiles; ++k) epi2(k);
   }
 
   __syncthreads();
@@ -349,7 +519,7 @@ uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
 
 }  // namespace
 
-bool conv_plan(int S, int P, int c1, int c2, ConvLayout* out) {
+bool conv_plan(int S, int P, int c1, int c2, ConvLayout* out, int schedule) {
   if (P != 4 || S < P || S % P != 0 || (S * S) % 16 != 0) return false;
   if ((c1 != 32 && c1 != 64 && c1 != 128) || c2 < 32 || c2 % 32 != 0 || c2 > 256) return false;
   ConvLayout L;
@@ -361,13 +531,23 @@ bool conv_plan(int S, int P, int c1, int c2, ConvLayout* out) {
   L.R = L.G + 1;
   if (L.R + 1 > kMargin) return false;
   const int P2 = L.R * L.R, G2 = L.G * L.G;
+  const bool split_ok = 3 * c2 <= 256 && 128 % P2 == 0 && 32 % L.R == 0;
+  if (schedule == 2 && !split_ok) return false;
+  // Measured on B200 (tools/trace_conv.cu, 2^20 CNN-s samples): tap 3.80 ms,
+  // split 4.19 ms -- split issues 2.1x fewer UMMA operand bytes but its
+  // lane-shift epilogue (shuffles + boundary exchange) costs more MIO
+  // bandwidth than it saves, so split is opt-in (ES_CONV_SCHEDULE=split).
+  L.split = split_ok && schedule == 2;
+  L.n2 = L.split ? 3 * c2 : c2;
   for (int T = std::max(1, 256 / P2); T >= 1; --T) {
     L.T = T;
     L.mb1 = (T * G2 + 127) / 128;
     L.mb2 = (T * P2 + 127) / 128;
     if (T * S * S / 16 > 256) continue;  // TMA box rows
     L.tmem_c1 = L.mb1 * c1;
-    L.tmem_c2 = L.mb2 * c2;
+    // split: one N = 3*c2 slot per 128-row block, two slots; tap: a
+    // double-buffered [mb2][c2] accumulator per tile.
+    L.tmem_c2 = L.split ? L.n2 : L.mb2 * c2;
     const int cols = 2 * (L.tmem_c1 + L.tmem_c2);
     if (cols > 512) continue;
     int tc = 32;
@@ -387,7 +567,11 @@ bool conv_plan(int S, int P, int c1, int c2, ConvLayout* out) {
     L.off_w2 = align_up(L.off_w1 + static_cast<uint32_t>(c1 * 32), 128);
     L.off_b1 = align_up(L.off_w2 + static_cast<uint32_t>(9 * c1 * c2 * 2), 16);
     L.off_b2 = align_up(L.off_b1 + static_cast<uint32_t>(c1 * 4), 16);
-    L.off_bar = align_up(L.off_b2 + static_cast<uint32_t>(c2 * 4), 8);
+    L.off_rows = align_up(L.off_b2 + static_cast<uint32_t>(c2 * 4), 16);
+    L.off_xch = align_up(L.off_rows + static_cast<uint32_t>(T * G2 * 4), 16);
+    const uint32_t xch =
+        L.split ? static_cast<uint32_t>((2 * 2 * 4 * 2 * L.R + 1) * kXchStride * 4) : 0u;  // + zero row
+    L.off_bar = align_up(L.off_xch + xch, 8);
     const uint32_t bars = static_cast<uint32_t>(2 * L.raw_stages + 16) * 8u + 16u;
     L.smem_bytes = L.off_bar + bars + 1024u;  // + alignment slack of the dynamic base
     if (L.smem_bytes > kSmemBudget) continue;
@@ -410,13 +594,17 @@ int conv_launch(const ConvArgs& args, const void* x, long long x_rows, int grid,
   grid = static_cast<int>(std::min<long long>(grid, tiles));
   auto go = [&](auto kernel) {
     if (ensure_smem_attr(kernel, static_cast<int>(kSmemBudget)) != 0) return -4;
-    kernel<<<grid, kThreads, L.smem_bytes, stream>>>(mx, args);
+    kernel<<<grid, L.split ? threads_for<true>() : threads_for<false>(), L.smem_bytes, stream>>>(mx,
+                                                                                                args);
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
   };
-  switch (L.c1) {
-    case 32: return go(conv_stack_sm100<2>);
-    case 64: return go(conv_stack_sm100<4>);
-    case 128: return go(conv_stack_sm100<8>);
+  switch (L.c1 * 2 + (L.split ? 1 : 0)) {
+    case 64: return go(conv_stack_sm100<2, false>);
+    case 65: return go(conv_stack_sm100<2, true>);
+    case 128: return go(conv_stack_sm100<4, false>);
+    case 129: return go(conv_stack_sm100<4, true>);
+    case 256: return go(conv_stack_sm100<8, false>);
+    case 257: return go(conv_stack_sm100<8, true>);
     default: return -1;
   }
 }

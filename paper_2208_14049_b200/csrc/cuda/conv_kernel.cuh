@@ -23,6 +23,23 @@
 //     im2col copy, no re-read from memory;
 //   * conv2's epilogue keeps the G x G interior and stores bf16 rows to HBM.
 // Every operand is K-major without swizzle (sdesc_planar in sm100.cuh).
+//
+// conv2 schedules.  A tcgen05 M=128, K=16 UMMA costs max(~46, N/2) clk
+// whatever its operands (tools/umma_rate.cu, measured on B200), so c2 = 32
+// output channels as N runs the tensor core at 16/46 of its rate:
+//   * "tap" (any shape): 9 taps x c1/16 K steps of N = c2 per 128-row block;
+//   * "split" (3*c2 <= 256, grid blocks aligned to 128 rows): the three
+//     vertical taps dh = -1, 0, +1 of one horizontal offset dw go into ONE
+//     UMMA as N = 3*c2 columns (B rows g*c2 + o = tap (g-1, dw), output o),
+//     with A shifted by dw only: 3 x c1/16 UMMAs of N = 96 per block instead
+//     of 36 of N = 32.  Column group g of accumulator row p then holds the
+//     dh = g-1 partial evaluated at row p, and the output is
+//         out[q] = D[q - R][g=0] + D[q][g=1] + D[q + R][g=2],
+//     a +-R lane shift done with warp shuffles (R | 32), plus an R-row
+//     exchange through shared memory between neighbouring TMEM lane
+//     quadrants.  Rows outside the 128-row block are zero-border rows (whole
+//     samples per block, R*R | 128), so no block needs another's partials.
+//     Measured slower than tap on B200 (see conv_plan): opt-in.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -34,6 +51,8 @@ namespace es {
 struct ConvLayout {
   int S = 28, P = 4, G = 7, c1 = 64, c2 = 32;
   int R = 8;             // G + 1: grid row stride (shared zero border)
+  bool split = false;    // conv2 schedule (see above)
+  int n2 = 32;           // conv2 UMMA N: c2 (tap) or 3*c2 (split)
   int T = 4;             // samples per tile
   int mb1 = 2, mb2 = 2;  // 128-row M blocks of conv1 / conv2
   int raw_stages = 4;
@@ -43,6 +62,8 @@ struct ConvLayout {
   uint32_t off_raw = 0, off_a1 = 0, off_a2 = 0, off_w1 = 0, off_w2 = 0, off_b1 = 0, off_b2 = 0;
   uint32_t off_bar = 0, smem_bytes = 0;
   int tmem_c1 = 0, tmem_c2 = 0, tmem_cols = 0;  // columns per buffer, total allocation
+  uint32_t off_rows = 0;  // im2col source offset per tile row, int [T*G*G]
+  uint32_t off_xch = 0;  // split: boundary-row exchange, [2][4 quadrants][2][R][kXchStride] fp32
 };
 
 struct ConvArgs {
@@ -56,11 +77,18 @@ struct ConvArgs {
   // Design evidence (tools/trace_conv.cu): globaltimer stamps of CTA 0's
   // first 32 tiles, [tile][16]; nullptr in the product.
   unsigned long long* trace = nullptr;
+  // Design evidence only (tools/trace_conv.cu): bits switch epilogue parts
+  // off to find the bottleneck (1: conv1 TMEM loads, 2: conv1 smem stores,
+  // 4: conv2 TMEM loads, 8: conv2 shuffles/exchange, 16: conv2 global
+  // stores).  0 in the product.
+  int debug = 0;
 };
 
 // False when the shape has no plan (P != 4, S % P != 0, c1 not in
 // {32, 64, 128}, c2 not a multiple of 32 up to 256, grids larger than 13 x 13).
-bool conv_plan(int S, int P, int c1, int c2, ConvLayout* out);
+// schedule: 0 = default (tap, the faster one measured), 1 = tap, 2 = split
+// (false if the shape does not allow it).
+bool conv_plan(int S, int P, int c1, int c2, ConvLayout* out, int schedule = 0);
 // x: bf16 [x_rows][S*S].
 int conv_launch(const ConvArgs& args, const void* x, long long x_rows, int grid, cudaStream_t stream);
 

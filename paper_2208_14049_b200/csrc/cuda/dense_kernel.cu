@@ -49,8 +49,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     dense_sm100(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
                 const __grid_constant__ CUtensorMap tm_y, const DenseArgs args) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   const DenseLayout& L = args.L;
   uint8_t* sOut = smem + L.off_stage_out;  // [2 halves][128 rows][128 B]
   float* sBias = reinterpret_cast<float*>(smem + L.off_bias);  // all N_total columns

@@ -62,8 +62,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                            const __grid_constant__ CUtensorMap tm_w1,
                            const __grid_constant__ CUtensorMap tm_w2, const MlpTArgs args) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   const MlpTLayout& L = args.L;
   uint8_t* sW2 = smem + L.off_w2;
   float* sBias = reinterpret_cast<float*>(smem + L.off_bias);

@@ -109,7 +109,10 @@ bool DeviceMember::load(int device, const ModelSpec& model, int batch) {
   if (a.kind == MemberArch::Kind::CNN) {
     // Leading layers: the fused convolution stack, bf16 [(S/P)^2 * c2] rows out.
     I.cnn = true;
-    if (!es::conv_plan(a.widths[0], a.widths[1], a.widths[2], a.widths[3], &I.conv))
+    const char* cs = std::getenv("ES_CONV_SCHEDULE");  // tests: "tap" | "split"
+    const int sched = cs && std::strcmp(cs, "tap") == 0 ? 1 : cs && std::strcmp(cs, "split") == 0 ? 2 : 0;
+    if (!es::conv_plan(a.widths[0], a.widths[1], a.widths[2], a.widths[3], &I.conv, sched) &&
+        !(sched == 2 && es::conv_plan(a.widths[0], a.widths[1], a.widths[2], a.widths[3], &I.conv, 1)))
       throw SpecError(model.name + ": CNN shape has no tile plan (patch 4, image side a "
                       "multiple of 4 up to 52, c1 in {32, 64, 128}, c2 a multiple of 32 up to 256)");
     I.act_width.push_back(I.dims[2].first);
@@ -187,12 +190,36 @@ bool DeviceMember::load(int device, const ModelSpec& model, int batch) {
   return true;
 }
 
+std::vector<std::string> DeviceMember::kernel_names() const {
+  std::vector<std::string> n;
+  if (!impl_) return n;
+  const Impl& I = *impl_;
+  if (I.head == Impl::Head::Synthetic) return {"synthetic_member_kernel"};
+  if (I.cnn) n.push_back(I.conv.split ? "conv_stack_sm100[split]" : "conv_stack_sm100[tap]");
+  for (std::size_t i = 0; i < I.dense.size(); ++i) n.push_back("dense_sm100");
+  if (env_is("ES_MEMBER_KERNEL", "simt") && I.head != Impl::Head::Dense) {
+    n.push_back("mlp2_simt_kernel");
+    return n;
+  }
+  switch (I.head) {
+    case Impl::Head::Pair: n.push_back("member_mlp2_pair_sm100"); break;
+    case Impl::Head::Tmem: n.push_back("member_mlp2_tmem_sm100"); break;
+    case Impl::Head::SwapAB: n.push_back("member_mlp2_sm100"); break;
+    default: n.push_back("dense_sm100[logits]"); break;
+  }
+  return n;
+}
+
 int DeviceMember::forward(const void* x, long long nb, int seg_size, long long s0, long long s1,
-                          float* out, int grid, cudaStream_t stream) {
+                          float* out, int grid, cudaStream_t stream, const cudaEvent_t* marks) {
   Impl& I = *impl_;
   if (s1 <= s0 || nb == 0) return 0;
+  auto mark = [&](int i) {
+    if (marks) M_CUDA(cudaEventRecord(marks[i], stream));
+  };
   if (I.head == Impl::Head::Synthetic) {
     M_LAUNCH(es::synthetic_member_launch(I.model.id, I.C, seg_size, s0, s1, nb, out, stream));
+    mark(0);
     return 1;
   }
   const uint8_t* base = static_cast<const uint8_t*>(I.weights);
@@ -219,7 +246,7 @@ int DeviceMember::forward(const void* x, long long nb, int seg_size, long long s
     c.b2 = reinterpret_cast<const float*>(base + I.b_off[1]);
     c.out = I.act[0];
     M_LAUNCH(es::conv_launch(c, cur, nb, grid, stream));
-    ++launches;
+    mark(launches++);
     cur = I.act[0];
   }
   for (std::size_t i = 0; i < I.dense.size(); ++i) {
@@ -231,7 +258,7 @@ int DeviceMember::forward(const void* x, long long nb, int seg_size, long long s
     d.row_end = r1;
     d.bias = reinterpret_cast<const float*>(base + I.b_off[l]);
     M_LAUNCH(es::dense_launch(d, cur, nb, base + I.w_off[l], y, grid, stream));
-    ++launches;
+    mark(launches++);
     cur = y;
   }
   if (I.head == Impl::Head::Dense) {
@@ -242,6 +269,7 @@ int DeviceMember::forward(const void* x, long long nb, int seg_size, long long s
     d.bias = reinterpret_cast<const float*>(base + I.b_off[L - 1]);
     d.logits = out;
     M_LAUNCH(es::dense_launch(d, cur, nb, base + I.w_off[L - 1], nullptr, grid, stream));
+    mark(launches);
     return launches + 1;
   }
   const int h = L - 2;  // head layers h, h+1
@@ -254,6 +282,7 @@ int DeviceMember::forward(const void* x, long long nb, int seg_size, long long s
                                   static_cast<const __nv_bfloat16*>(w1), b1, I.dims[h].second,
                                   static_cast<const __nv_bfloat16*>(w2), b2, I.C, r0, r1, out,
                                   stream));
+    mark(launches);
     return launches + 1;
   }
   switch (I.head) {
@@ -300,6 +329,7 @@ int DeviceMember::forward(const void* x, long long nb, int seg_size, long long s
       break;
     }
   }
+  mark(launches);
   return launches + 1;
 }
 

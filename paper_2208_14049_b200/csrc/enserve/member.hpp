@@ -33,8 +33,15 @@ class DeviceMember {
 
   // Logits of every row of segments [s0, s1) of x (bf16 [nb][width], rows
   // indexed globally) into out ([nb][C] fp32).  Returns kernel launches.
+  // `marks` (optional, >= max_launches() events): marks[i] is recorded on
+  // `stream` right after launch i, so launch i's device time is the interval
+  // from the previous mark (or the caller's start event) to marks[i].
   int forward(const void* x, long long nb, int seg_size, long long s0, long long s1, float* out,
-              int grid, cudaStream_t stream);
+              int grid, cudaStream_t stream, const cudaEvent_t* marks = nullptr);
+
+  // Kernel names forward() launches, in order (one per launch).
+  std::vector<std::string> kernel_names() const;
+  int max_launches() const { return static_cast<int>(kernel_names().size()); }
 
   int device() const { return device_; }
   std::size_t weight_bytes() const { return bytes_; }

@@ -182,6 +182,7 @@ struct InferenceSystem::Worker {
   cudaStream_t stream = nullptr;
   bool owns_stream = true;
   cudaEvent_t ev_begin = nullptr, ev_done = nullptr;
+  std::vector<cudaEvent_t> marks;  // one per member launch (DeviceMember::forward)
   long long seg_begin = 0, seg_end = 0;  // this run's share
   float* staging = nullptr;              // remote worker: local logits [nb][C]
   std::size_t staging_rows = 0;
@@ -299,6 +300,8 @@ InferenceSystem::InferenceSystem(const AllocationMatrix& A, const ClusterSpec& c
       }
       ES_CUDA(cudaEventCreate(&w->ev_begin));
       ES_CUDA(cudaEventCreate(&w->ev_done));
+      w->marks.resize(w->member->max_launches());
+      for (auto& e : w->marks) ES_CUDA(cudaEventCreate(&e));
       workers_.push_back(std::move(w));
     }
   }
@@ -335,6 +338,7 @@ void InferenceSystem::shutdown() {
     if (w->stream && w->owns_stream) cudaStreamDestroy(w->stream);
     if (w->ev_begin) cudaEventDestroy(w->ev_begin);
     if (w->ev_done) cudaEventDestroy(w->ev_done);
+    for (auto e : w->marks) cudaEventDestroy(e);
     w->member.reset();
   }
   if (impl_ && impl_->main) {
@@ -435,7 +439,8 @@ std::size_t InferenceSystem::broadcast() {
     int grid = es::num_sms(w->phys);
     if (options_.sms_per_worker > 0) grid = std::min(grid, options_.sms_per_worker);
     launches_ += w->member->forward(X.device_replica(w->phys), nb, cluster_.segment_size,
-                                    w->seg_begin, w->seg_end, out, grid, w->stream);
+                                    w->seg_begin, w->seg_end, out, grid, w->stream,
+                                    w->marks.empty() ? nullptr : w->marks.data());
     if (remote && w->seg_end > w->seg_begin) {
       const long long r0 = w->seg_begin * cluster_.segment_size;
       const long long r1 = std::min<long long>(w->seg_end * cluster_.segment_size, nb);
@@ -508,6 +513,27 @@ double InferenceSystem::last_member_ms(int worker) const {
   return ms;
 }
 
+std::vector<double> InferenceSystem::last_kernel_ms(int worker) const {
+  const Worker& w = *workers_.at(worker);
+  OnDevice on(w.phys);
+  std::vector<double> out;
+  cudaEvent_t prev = w.ev_begin;
+  for (cudaEvent_t e : w.marks) {
+    float ms = 0.0f;
+    if (cudaEventElapsedTime(&ms, prev, e) != cudaSuccess) {
+      cudaGetLastError();
+      return {};
+    }
+    out.push_back(ms);
+    prev = e;
+  }
+  return out;
+}
+
+std::vector<std::string> InferenceSystem::kernel_names(int worker) const {
+  return workers_.at(worker)->member->kernel_names();
+}
+
 double InferenceSystem::last_combine_ms() const {
   OnDevice on(combine_dev_);
   float ms = 0.0f;
@@ -572,6 +598,7 @@ double InferenceSystem::run_host(const float* X, std::size_t nb, std::size_t wid
   ES_CUDA(cudaDeviceSynchronize());
   const auto t0 = std::chrono::steady_clock::now();
   launches_ = 0;
+  h2d_bytes_ = d2h_bytes_ = 0;
   const std::size_t nchunks = (nb + chunk - 1) / chunk;
   const int grid = es::num_sms(combine_dev_);
   for (std::size_t i = 0; i < nchunks; ++i) {
@@ -585,6 +612,8 @@ double InferenceSystem::run_host(const float* X, std::size_t nb, std::size_t wid
       convert_f32_to_bf16_host(X + r0 * width, static_cast<std::uint16_t*>(sl.pinned), elems,
                                *I.pool);
     if (i >= kSlots) ES_CUDA(cudaStreamWaitEvent(I.copy, sl.d2h_done, 0));  // slot buffers free
+    h2d_bytes_ += elems * (convert ? 2 : sizeof(float));
+    d2h_bytes_ += (Y_out ? rows * C * sizeof(float) : 0) + (labels_out ? rows * sizeof(int32_t) : 0);
     if (convert)
       ES_CUDA(cudaMemcpyAsync(sl.x16, sl.pinned, elems * 2, cudaMemcpyHostToDevice, I.copy));
     else

@@ -153,9 +153,16 @@ class InferenceSystem {
   const ClusterSpec& cluster() const { return cluster_; }
   // Kernel launches enqueued by the last broadcast() (members + combine + copies).
   int launches_last_run() const { return launches_; }
+  // Bytes the last run_host moved host->device and device->host.
+  std::size_t h2d_bytes_last() const { return h2d_bytes_; }
+  std::size_t d2h_bytes_last() const { return d2h_bytes_; }
   // Device time of the last run's member kernels / combine (ms), from events.
   double last_member_ms(int worker) const;
   double last_combine_ms() const;
+  // Per-launch device time of the worker's member kernels in the last run
+  // (empty if the worker had no rows), and their kernel names.
+  std::vector<double> last_kernel_ms(int worker) const;
+  std::vector<std::string> kernel_names(int worker) const;
   int combine_device() const { return combine_dev_; }
 
  private:
@@ -171,6 +178,7 @@ class InferenceSystem {
   std::vector<std::unique_ptr<Worker>> workers_;
   std::unique_ptr<Impl> impl_;
   int launches_ = 0;
+  std::size_t h2d_bytes_ = 0, d2h_bytes_ = 0;
   bool shut_down_ = false;
   bool run_open_ = false;
 };

@@ -73,7 +73,13 @@ CNN_SHAPES = [(28, 4, 64, 32, 128, 10), (28, 4, 32, 64, 256, 10), (16, 4, 64, 32
 
 @pytest.mark.parametrize("shape", CNN_SHAPES)
 @pytest.mark.parametrize("b", [32, 128])
-def test_cnn_member_matches_cpu_oracle(shape, b):
+@pytest.mark.parametrize("schedule", ["auto", "split"])
+def test_cnn_member_matches_cpu_oracle(shape, b, schedule, monkeypatch):
+    """Both conv2 schedules (conv_kernel.cuh): "auto" is the tap-by-tap
+    schedule, "split" the dh-split one where the shape allows it (7x7 grids;
+    other shapes fall back to tap)."""
+    if schedule != "auto":
+        monkeypatch.setenv("ES_CONV_SCHEDULE", schedule)
     S = shape[0]
     X = refcpu.features(43, 500, S * S)  # 500 = 166 tiles of 3 samples + 2
     model = es.cnn_model(0, "cnn", 77, S=shape[0], P=shape[1], c1=shape[2], c2=shape[3],

@@ -17,6 +17,8 @@
 int main(int argc, char** argv) {
   const int c1 = argc > 1 ? std::atoi(argv[1]) : 64;
   const int c2 = argc > 2 ? std::atoi(argv[2]) : 32;
+  const int sched = argc > 3 ? std::atoi(argv[3]) : 0;  // conv_plan schedule
+  const int debug = argc > 4 ? std::atoi(argv[4]) : 0;  // ConvArgs::debug bits
   const long long nb = 1 << 20;
   const int S = 28, P = 4, G = 7;
   __nv_bfloat16 *x, *w1, *w2, *y;
@@ -33,12 +35,13 @@ int main(int argc, char** argv) {
   es::generate_dense_layer(7, 0, 16, c1, std::sqrt(6.0f / (16 + c1)), w1, b1, 0);
   es::generate_dense_layer(7, 1, 9 * c1, c2, std::sqrt(6.0f / (9 * c1 + c2)), w2, b2, 0);
   es::ConvArgs a;
-  if (!es::conv_plan(S, P, c1, c2, &a.L)) {
+  if (!es::conv_plan(S, P, c1, c2, &a.L, sched)) {
     std::printf("no plan\n");
     return 1;
   }
-  std::printf("c1=%d c2=%d T=%d mb1=%d mb2=%d smem=%u tmem=%d\n", c1, c2, a.L.T, a.L.mb1, a.L.mb2,
-              a.L.smem_bytes, a.L.tmem_cols);
+  std::printf("c1=%d c2=%d %s T=%d mb1=%d mb2=%d smem=%u tmem=%d\n", c1, c2,
+              a.L.split ? "split" : "tap", a.L.T, a.L.mb1, a.L.mb2, a.L.smem_bytes, a.L.tmem_cols);
+  a.debug = debug;
   a.row_begin = 0;
   a.row_end = nb;
   a.w1 = w1;
@@ -69,8 +72,10 @@ int main(int argc, char** argv) {
   std::printf("tile  tma  build_go build_end  c1_go  epi1_go epi1_end  c2_go  c2_iss  epi2_go epi2_end\n");
   for (int k = 0; k < 32; ++k) {
     auto r = [&](int i) { return t[k * 16 + i] ? double(t[k * 16 + i] - t0) / 1e3 : -1.0; };
-    std::printf("%4d %6.2f %8.2f %9.2f %6.2f %8.2f %8.2f %6.2f %7.2f %8.2f %8.2f\n", k, r(0), r(4),
+    std::printf("%4d %6.2f %8.2f %9.2f %6.2f %8.2f %8.2f %6.2f %7.2f %8.2f %8.2f", k, r(0), r(4),
                 r(5), r(1), r(6), r(7), r(2), r(3), r(8), r(9));
+    for (int i = 10; i < 16; ++i) std::printf(" %7.2f", r(i));
+    std::printf("\n");
   }
   return 0;
 }

@@ -15,8 +15,7 @@ using namespace es::sm100;
 __global__ void __launch_bounds__(128, 1) rate(int layout, int N, int shift, int reps,
                                                unsigned long long* out) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   __shared__ uint64_t bar;
   __shared__ uint32_t slot;
   for (int i = threadIdx.x; i < 96 * 1024 / 16; i += blockDim.x)
@@ -58,8 +57,7 @@ __global__ void __launch_bounds__(128, 1) rate(int layout, int N, int shift, int
 __global__ void __launch_bounds__(128, 1) rate_varying(int mode, int N, int reps,
                                                        unsigned long long* out) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   __shared__ uint64_t bar;
   __shared__ uint32_t slot;
   for (int i = threadIdx.x; i < 96 * 1024 / 16; i += blockDim.x)
@@ -112,8 +110,7 @@ __global__ void __launch_bounds__(128, 1) rate_varying(int mode, int N, int reps
 __global__ void __launch_bounds__(128, 1) rate_table(int mode, int N, int reps, int pad,
                                                      unsigned long long* out) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   __shared__ uint64_t bar;
   __shared__ uint32_t slot;
   for (int i = threadIdx.x; i < 96 * 1024 / 16; i += blockDim.x)
@@ -161,7 +158,197 @@ __global__ void __launch_bounds__(128, 1) rate_table(int mode, int N, int reps, 
   if (threadIdx.x < 32) tmem_dealloc(tmem, 256);
 }
 
+// Independent accumulators: MMA r accumulates into chain r % chains (TMEM
+// columns chain * N), so consecutive MMAs carry no accumulator dependency.
+template <int CH>
+__global__ void __launch_bounds__(128, 1) rate_chains(int N, int reps, unsigned long long* out,
+                                                      int M = 128) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align_smem_1024(smem_raw);
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  for (int i = threadIdx.x; i < 96 * 1024 / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  if (threadIdx.x < 32) tmem_alloc(&slot, 512);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  if (threadIdx.x == 0) {
+    const uint32_t a = smem_u32(smem), b = smem_u32(smem + 64 * 1024);
+    const uint32_t idesc = idesc_bf16_f32(M, N);
+    const uint64_t ad = sdesc_planar(a, 160 * 16), bd = sdesc_planar(b, N * 16);
+    const long long t0 = clock64();
+    for (int r = 0; r < reps; r += CH) {
+#pragma unroll
+      for (int c = 0; c < CH; ++c)
+        umma_bf16(tmem + static_cast<uint32_t>(c * N), ad, bd, idesc, r > 0);
+    }
+    umma_commit(&bar);
+    mbar_wait(&bar, 0);
+    if (blockIdx.x == 0) out[0] = static_cast<unsigned long long>(clock64() - t0);
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) tmem_dealloc(tmem, 512);
+}
+
+// A operand from TMEM (tcgen05.mma ... [a_tmem]): only B is read from smem.
+template <int CH>
+__global__ void __launch_bounds__(128, 1) rate_ta(int N, int reps, unsigned long long* out) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align_smem_1024(smem_raw);
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  for (int i = threadIdx.x; i < 96 * 1024 / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  if (threadIdx.x < 32) tmem_alloc(&slot, 512);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  if (threadIdx.x == 0) {
+    const uint32_t b = smem_u32(smem + 64 * 1024);
+    const uint32_t idesc = idesc_bf16_f32(128, N);
+    const uint64_t bd = sdesc_planar(b, N * 16);
+    const long long t0 = clock64();
+    for (int r = 0; r < reps; r += CH) {
+#pragma unroll
+      for (int c = 0; c < CH; ++c)
+        umma_bf16_ta(tmem + static_cast<uint32_t>(c * N), tmem + 256u + static_cast<uint32_t>(c * 8),
+                     bd, idesc, r > 0);
+    }
+    umma_commit(&bar);
+    mbar_wait(&bar, 0);
+    if (blockIdx.x == 0) out[0] = static_cast<unsigned long long>(clock64() - t0);
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) tmem_dealloc(tmem, 512);
+}
+
+// The conv kernel's split conv2 block: 3 dw shifts x 4 K steps, A planar
+// (plane 4608 B, start moved by -1/0/+1 rows), B planar N = 96.
+__global__ void __launch_bounds__(128, 1) rate_split(int N, int reps, int shift_on,
+                                                     unsigned long long* out, int dcol = 0,
+                                                     int boff = 0) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align_smem_1024(smem_raw);
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  for (int i = threadIdx.x; i < 96 * 1024 / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  if (threadIdx.x < 32) tmem_alloc(&slot, 512);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
+  if (warp == 0) {
+    const uint32_t a = smem_u32(smem), b = smem_u32(smem + 40 * 1024 + boff);
+    const uint32_t idesc = idesc_bf16_f32(128, N);
+    const uint64_t ad0 = sdesc_planar(a + 16 * 16, 4608), bd0 = sdesc_planar(b, N * 16);
+    const uint32_t dt = tmem + static_cast<uint32_t>(dcol);
+    const long long t0 = clock64();
+    for (int r = 0; r < reps; r += 12) {
+#pragma unroll
+      for (int dwi = 0; dwi < 3; ++dwi)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint64_t ad = ad0 + static_cast<uint64_t>((dwi - 1) * shift_on + j * 576);
+          const uint64_t bd = bd0 + static_cast<uint64_t>((dwi * 4 + j) * 2 * N);
+          if (elect_one()) umma_bf16(dt, ad, bd, idesc, (r | dwi | j) != 0);
+        }
+    }
+    if (elect_one()) umma_commit(&bar);
+    __syncwarp();
+    mbar_wait(&bar, 0);
+    if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = static_cast<unsigned long long>(clock64() - t0);
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) tmem_dealloc(tmem, 512);
+}
+
 int main() {
+  {
+    unsigned long long* d;
+    cudaMalloc(&d, 8);
+    cudaFuncSetAttribute(rate_split, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    for (int N : {32, 96})
+      for (int sh = 0; sh < 2; ++sh) {
+        rate_split<<<148, 128, 100 * 1024>>>(N, 504, sh, d, 0, 0);
+        unsigned long long c = 0;
+        cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
+        std::printf("split pattern N=%d shifts=%d: %6.1f clk/MMA %s\n", N, sh, double(c) / 504,
+                    cudaGetErrorString(cudaGetLastError()));
+      }
+    for (int dcol : {0, 96, 256, 352})
+      for (int boff : {0, 128, 512}) {
+        rate_split<<<148, 128, 100 * 1024>>>(96, 504, 1, d, dcol, boff);
+        unsigned long long c = 0;
+        cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
+        std::printf("split N=96 dcol=%d boff=%d: %6.1f clk/MMA %s\n", dcol, boff, double(c) / 504,
+                    cudaGetErrorString(cudaGetLastError()));
+      }
+    cudaFree(d);
+  }
+  {
+    unsigned long long* d;
+    cudaMalloc(&d, 8);
+    cudaFuncSetAttribute(rate_chains<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    for (int N : {32, 64, 128, 256}) {
+      rate_chains<1><<<148, 128, 100 * 1024>>>(N, 512, d, 64);
+      unsigned long long c = 0;
+      cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
+      std::printf("M=64 N=%3d: %6.1f clk/MMA  (%5.0f MAC/clk) %s\n", N, double(c) / 512,
+                  64.0 * N * 16 * 512 / double(c), cudaGetErrorString(cudaGetLastError()));
+    }
+    cudaFuncSetAttribute(rate_ta<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    cudaFuncSetAttribute(rate_ta<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    for (int N : {16, 32, 64, 128, 256})
+      for (int ci = 0; ci < 2; ++ci) {
+        if (N * (1 << ci) > 256) continue;
+        (ci ? rate_ta<2> : rate_ta<1>)<<<148, 128, 100 * 1024>>>(N, 512, d);
+        unsigned long long c = 0;
+        cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
+        std::printf("A=tmem chains=%d N=%3d: %6.1f clk/MMA  (%5.0f MAC/clk) %s\n", 1 << ci, N,
+                    double(c) / 512, 128.0 * N * 16 * 512 / double(c),
+                    cudaGetErrorString(cudaGetLastError()));
+      }
+    cudaFree(d);
+  }
+  {
+    unsigned long long* d;
+    cudaMalloc(&d, 8);
+    auto fns = {rate_chains<1>, rate_chains<2>, rate_chains<4>, rate_chains<8>};
+    for (auto f : fns) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    for (int N : {16, 32, 64, 96, 128})
+      for (int ci = 0; ci < 4; ++ci) {
+        const int chains = 1 << ci;
+        if (N * chains > 512) continue;
+        auto f = ci == 0 ? rate_chains<1> : ci == 1 ? rate_chains<2> : ci == 2 ? rate_chains<4> : rate_chains<8>;
+        f<<<148, 128, 100 * 1024>>>(N, 512, d, 128);
+        unsigned long long c = 0;
+        cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
+        std::printf("chains=%d N=%3d: %6.1f clk/MMA  (%5.0f MAC/clk) %s\n", chains, N,
+                    double(c) / 512, 128.0 * N * 16 * 512 / double(c),
+                    cudaGetErrorString(cudaGetLastError()));
+      }
+    cudaFree(d);
+  }
   unsigned long long* d;
   cudaMalloc(&d, 8);
   cudaFuncSetAttribute(rate, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
