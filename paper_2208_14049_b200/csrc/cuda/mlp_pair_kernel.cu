@@ -100,7 +100,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
   const int warp = warp_uniform_id();
   const int lane = threadIdx.x & 31;
-  const int H = L.H;
+  const int H = L.H;    // all hidden units (W2 columns, biases)
+  const int HP = L.HP;  // hidden units per pass (TMEM-resident at a time)
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
   const Tiles ts = tile_space(args);
@@ -150,25 +151,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int g = 0;; ++g) {
         const int n = group_tiles(args, ts, g, rank, row0, rows);
         if (n == 0) break;
-        for (int kc = 0; kc < L.kchunks; ++kc) {
-          mbar_wait(&empty[stage], phase ^ 1u);
-          if (kc == 0) TRACE(g, 7);
-          uint8_t* st = smem + static_cast<size_t>(stage) * L.stage_bytes;
-          if (leader)
-            mbar_arrive_expect_tx(&full[stage], 2u * (static_cast<uint32_t>(n) * 16384u +
-                                                      static_cast<uint32_t>(H) * 64u));
-          for (int k = 0; k < n; ++k)
-            tma_load_2d_pair(st + k * 16384, &tm_x, &full[stage], kc * 64,
-                             static_cast<int32_t>(row0[k]), pol_stream);
-          uint8_t* sw = st + L.T * 16384;
-          for (int h = 0; h < L.nh; ++h)
-            tma_load_2d_pair(sw + h * half_w * 128u, &tm_w1, &full[stage], kc * 64,
-                             static_cast<int32_t>(h * L.NH + rank * half_w), pol_keep);
-          if (++stage == L.stages) {
-            stage = 0;
-            phase ^= 1u;
+        for (int hp = 0; hp < L.passes; ++hp)  // hidden passes re-stream the X tiles
+          for (int kc = 0; kc < L.kchunks; ++kc) {
+            mbar_wait(&empty[stage], phase ^ 1u);
+            if (kc == 0 && hp == 0) TRACE(g, 7);
+            uint8_t* st = smem + static_cast<size_t>(stage) * L.stage_bytes;
+            if (leader)
+              mbar_arrive_expect_tx(&full[stage], 2u * (static_cast<uint32_t>(n) * 16384u +
+                                                        static_cast<uint32_t>(HP) * 64u));
+            for (int k = 0; k < n; ++k)
+              tma_load_2d_pair(st + k * 16384, &tm_x, &full[stage], kc * 64,
+                               static_cast<int32_t>(row0[k]), pol_stream);
+            uint8_t* sw = st + L.T * 16384;
+            for (int h = 0; h < L.nh; ++h)
+              tma_load_2d_pair(sw + h * half_w * 128u, &tm_w1, &full[stage], kc * 64,
+                               static_cast<int32_t>(hp * HP + h * L.NH + rank * half_w), pol_keep);
+            if (++stage == L.stages) {
+              stage = 0;
+              phase ^= 1u;
+            }
           }
-        }
       }
     }
   } else if (warp == 1) {
@@ -183,7 +185,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t a_par = 0;
       uint32_t d2_par = ~0u;
       bool w2_ready = false;
-      int pend_buf = -1, pend_n = 0, pend_next = 0, pend_g = 0;
+      int pend_buf = -1, pend_n = 0, pend_next = 0, pend_g = 0, pend_hp = 0;
       auto layer2 = [&](int buf, int k, bool waited) {
         if (!w2_ready) {
           mbar_wait(w2_full, 0);
@@ -193,8 +195,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (k == 0) TRACE(pend_g, 8);
         a_par ^= 1u << k;
         tc_fence_after();
-        const uint32_t tile = tmem_base + static_cast<uint32_t>(buf * L.group_cols + k * H);
-        uint32_t d2 = tile + static_cast<uint32_t>(H / 4);
+        const uint32_t tile = tmem_base + static_cast<uint32_t>(buf * L.group_cols + k * HP);
+        uint32_t d2 = tile + static_cast<uint32_t>(HP / 4);
         if (L.d2_sep) {
           mbar_wait_cluster(&d2_empty[k], (d2_par >> k) & 1u);
           d2_par ^= 1u << k;
@@ -206,9 +208,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const uint32_t pmask = static_cast<uint32_t>(L.d2_parts - 1);  // parts: 1 or 4
         uint32_t step = 0;
         for (int hh = 0; hh < 2; ++hh)
-          for (int kk = 0; kk < H / 32; ++kk, ++step) {  // 16 hidden units per step
-            const uint32_t h0 = static_cast<uint32_t>(hh * (H / 2) + kk * 16);
-            const uint32_t a = tile + static_cast<uint32_t>(hh * (H / 2) + kk * 8);
+          for (int kk = 0; kk < HP / 32; ++kk, ++step) {  // 16 hidden units per step
+            const uint32_t h0 = static_cast<uint32_t>(pend_hp * HP + hh * (HP / 2) + kk * 16);
+            const uint32_t a = tile + static_cast<uint32_t>(hh * (HP / 2) + kk * 8);
             const uint64_t b = w2d + (h0 >> 6) * 64u + (h0 & 63u) / 8u;
             if (elect_one()) umma_bf16_pair_ta(d2 + 16u * (step & pmask), a, b, idesc2, step > pmask);
           }
@@ -221,11 +223,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       };
       long long row0[kMaxT];
       int rows[kMaxT];
-      for (int g = 0;; ++g) {
+      for (int v = 0;; ++v) {  // v = group * passes + hidden pass
+        const int g = v / L.passes, hp = v % L.passes;
         const int n = group_tiles(args, ts, g, rank, row0, rows);
         if (n == 0) break;
-        const int buf = g % L.nbuf;
-        const uint32_t use = static_cast<uint32_t>(g / L.nbuf);
+        const int buf = v % L.nbuf;
+        const uint32_t use = static_cast<uint32_t>(v / L.nbuf);
         if (pend_buf == buf) drain_pending();
         TRACE(g, 0);
         mbar_wait_cluster(&acc_empty[buf], (use & 1u) ^ 1u);
@@ -244,7 +247,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               for (int j = 0; j < 4; ++j) {
                 const uint64_t a = xd + static_cast<uint64_t>(k * 1024 + j * 2);
                 const uint64_t b = wd + static_cast<uint64_t>(h * half_w * 8u + j * 2);
-                if (elect_one()) umma_bf16_pair(d0 + static_cast<uint32_t>(k * H + h * L.NH), a, b, idesc1,
+                if (elect_one()) umma_bf16_pair(d0 + static_cast<uint32_t>(k * HP + h * L.NH), a, b, idesc1,
                                (kc | j) != 0);
               }
           if (elect_one()) umma_commit_pair(&empty[stage], kBoth);
@@ -266,6 +269,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         pend_n = n;
         pend_next = 0;
         pend_g = g;
+        pend_hp = hp;
       }
       if (pend_buf >= 0) drain_pending();
     }
@@ -283,18 +287,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint32_t acc2_par = 0;
     long long row0[kMaxT];
     int rows[kMaxT];
-    const int hw = H / 2;
-    for (int g = 0;; ++g) {
+    const int hw = HP / 2;
+    float zs[kMaxT][16];  // logits summed over the hidden passes
+    for (int v = 0;; ++v) {
+      const int g = v / L.passes, hp = v % L.passes;
       const int n = group_tiles(args, ts, g, rank, row0, rows);
       if (n == 0) break;
-      const int buf = g % L.nbuf;
-      const uint32_t use = static_cast<uint32_t>(g / L.nbuf);
+      const int buf = v % L.nbuf;
+      const uint32_t use = static_cast<uint32_t>(v / L.nbuf);
       mbar_wait(&acc_full[buf], use & 1u);
       if (warp == 2 && lane == 0) TRACE(g, 3);
       tc_fence_after();
       for (int k = 0; k < n; ++k) {
-        const uint32_t col0 = static_cast<uint32_t>(buf * L.group_cols + k * H + half * hw);
-        const float* bias = sBias + half * hw;
+        const uint32_t col0 = static_cast<uint32_t>(buf * L.group_cols + k * HP + half * hw);
+        const float* bias = sBias + hp * HP + half * hw;
         hidden_to_bf16(tmem_base + lane_field + col0, bias, hw);
         if (warp == 2 && lane == 0 && k == 0) TRACE(g, 4);
         if (warp == 9 && lane == 0 && k == 0) TRACE(g, 10);
@@ -316,8 +322,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           tc_fence_after();
           const uint32_t d2col =
               L.d2_sep ? static_cast<uint32_t>(L.d2_col + 16 * L.d2_parts * k)
-                       : static_cast<uint32_t>(buf * L.group_cols + k * H + H / 4);
+                       : static_cast<uint32_t>(buf * L.group_cols + k * HP + HP / 4);
           read_d2(tmem_base + lane_field + d2col, L.d2_parts, z[k]);
+#pragma unroll
+          for (int c = 0; c < 16; ++c) zs[k][c] = hp == 0 ? z[k][c] : zs[k][c] + z[k][c];
           if (L.d2_sep) {
             tc_fence_before();
             __syncwarp();
@@ -332,11 +340,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int r = q * 32 + lane;
 #pragma unroll
         for (int k = 0; k < kMaxT; ++k) {
-          if (k >= n || r >= rows[k]) continue;
+          if (hp + 1 < L.passes || k >= n || r >= rows[k]) continue;
           float* o = args.out + (row0[k] + r) * L.C;
 #pragma unroll
           for (int c = 0; c < 16; ++c)
-            if (c < L.C) o[c] = z[k][c] + b2[c];
+            if (c < L.C) o[c] = zs[k][c] + b2[c];
         }
         if (warp == 2 && lane == 0) TRACE(g, 6);
       }
@@ -358,21 +366,29 @@ uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
 }  // namespace
 
 bool mlpp_plan(int K, int H, int C, int b, MlpPLayout* out) {
-  if (K < 1 || K % 8 != 0 || H < 128 || H % 128 != 0 || H > 512 || C < 1 || C > 16 || b < 1 ||
+  if (K < 1 || K % 8 != 0 || H < 128 || H % 128 != 0 || H > 2048 || C < 1 || C > 16 || b < 1 ||
       b > 128)
     return false;
+  // Hidden layers wider than one SM's TMEM run in passes of HP <= 512 units:
+  // each pass re-streams the X tiles, and the layer-2 partials of the passes
+  // are summed in the epilogue's registers.
+  const int passes = (H + 511) / 512;
+  if (H % passes != 0 || (H / passes) % 128 != 0) return false;
+  const int HP = H / passes;
   const int kchunks = (K + 63) / 64;
-  const int nh = (H + 255) / 256;
-  const int NH = H / nh;
+  const int nh = (HP + 255) / 256;
+  const int NH = HP / nh;
   if (NH % 32 != 0) return false;  // N % 16 per UMMA, NH/2 rows 8-row aligned per SM
   bool found = false;
   MlpPLayout best;
   for (int T = 1; T <= kMaxT; ++T) {
     for (int nbuf = 1; nbuf <= 2; ++nbuf) {
-      const int cols = nbuf * T * H;
+      const int cols = nbuf * T * HP;
       if (cols > 512) continue;
       MlpPLayout L;
       L.H = H;
+      L.HP = HP;
+      L.passes = passes;
       L.C = C;
       L.K = K;
       L.kchunks = kchunks;
@@ -380,16 +396,16 @@ bool mlpp_plan(int K, int H, int C, int b, MlpPLayout* out) {
       L.nbuf = nbuf;
       L.nh = nh;
       L.NH = NH;
-      L.group_cols = T * H;
+      L.group_cols = T * HP;
       // Layer-2 partial accumulators: 4 when there is room (inside the
       // drained half-0 columns [H/4, H/2), or after the hidden columns).
       L.d2_sep = cols + 16 * T <= 512 ? 1 : 0;
-      L.d2_parts = L.d2_sep ? (cols + 64 * T <= 512 ? 4 : 1) : (H >= 256 ? 4 : 1);
+      L.d2_parts = L.d2_sep ? (cols + 64 * T <= 512 ? 4 : 1) : (HP >= 256 ? 4 : 1);
       L.d2_col = cols;
       int tc = 32;
       while (tc < cols + (L.d2_sep ? 16 * L.d2_parts * T : 0)) tc <<= 1;
       L.tmem_cols = tc;
-      L.stage_bytes = static_cast<uint32_t>(T) * 16384u + static_cast<uint32_t>(H) * 64u;
+      L.stage_bytes = static_cast<uint32_t>(T) * 16384u + static_cast<uint32_t>(HP) * 64u;
       const uint32_t tail = static_cast<uint32_t>(H / 64) * 1024u + static_cast<uint32_t>(H) * 4u +
                             512u + 1024u;
       const int stages =
@@ -403,12 +419,12 @@ bool mlpp_plan(int K, int H, int C, int b, MlpPLayout* out) {
       if (L.smem_bytes > kSmemBudget) continue;
       // Per-SM cycles per group: tensor (the pair shares one M=256 UMMA) vs TMA
       // ingress (~44 B/clk) vs HBM share (~25 B/clk) + un-overlapped epilogue.
-      const double mma = static_cast<double>(kchunks) * T * 2.0 * H;
+      const double mma = static_cast<double>(kchunks) * T * 2.0 * HP;
       const double ingress = static_cast<double>(kchunks) * L.stage_bytes / 44.0;
-      const double hbm = static_cast<double>(T) * b * K * 2.0 / 25.0;
-      const double epi = T * (H / 64.0) * 110.0 + 600.0;
-      const double per_group =
-          std::max({mma, ingress, hbm}) + (nbuf == 1 ? (L.d2_sep ? 0.6 * epi : epi) : 0.0);
+      const double hbm = static_cast<double>(T) * b * K * 2.0 / 25.0 / passes;
+      const double epi = T * (HP / 64.0) * 110.0 + 600.0;
+      const double per_group = passes * (std::max({mma, ingress, hbm}) +
+                                         (nbuf == 1 ? (L.d2_sep ? 0.6 * epi : epi) : 0.0));
       L.est_cycles_per_sample = static_cast<float>(per_group / (static_cast<double>(T) * b));
       if (!found || L.est_cycles_per_sample < best.est_cycles_per_sample) {
         best = L;
@@ -427,7 +443,7 @@ int mlpp_launch(const MlpPArgs& args, const void* x, const void* w1, const void*
   if (make_bf16_map(&mx, x, static_cast<uint64_t>(L.K), static_cast<uint64_t>(args.nb), 128) != 0)
     return -1;
   if (make_bf16_map(&mw1, w1, static_cast<uint64_t>(L.K), static_cast<uint64_t>(L.H),
-                    static_cast<uint32_t>(L.NH / 2)) != 0)
+                    static_cast<uint32_t>(L.NH / 2)) != 0)  // rows of all passes
     return -1;
   if (make_bf16_map(&mw2, w2, static_cast<uint64_t>(L.H), static_cast<uint64_t>(L.C), 8) != 0)
     return -1;

@@ -10,6 +10,10 @@
 //   epilogue:  each SM turns its own 128 rows to bf16 in its own TMEM
 //   layer 2:   D2[s, c] = H[s, h] W2[c, h]       cta_group::2, A from TMEM of
 //              both SMs, W2 rows split 8 + 8 across the pair (N = 16)
+// Hidden layers wider than 512 (one SM's TMEM) run in passes of HP <= 512
+// units: every pass re-streams the tile's X chunks with the next W1 rows, its
+// layer-2 partial (W2 columns of the pass) is read out by the epilogue and
+// summed in registers; logits are written after the last pass.
 // Barriers the leader's UMMA thread waits on (full, a_full, acc_empty, w2_full)
 // live in the leader; the peer's TMA completes bytes on them directly and its
 // epilogue arrives remotely.  Commits multicast to both SMs.
@@ -23,6 +27,8 @@ namespace es {
 
 struct MlpPLayout {
   int H = 0, C = 0, K = 0, kchunks = 0;
+  int HP = 0;         // hidden units per pass (H / passes <= 512: one SM's TMEM)
+  int passes = 1;     // hidden passes; each re-streams X, layer-2 partials summed
   int T = 1;          // 128-row tiles per SM per group
   int nbuf = 1;
   int nh = 1;         // pair UMMAs per tile per k-step
