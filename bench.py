@@ -34,13 +34,44 @@ import numpy as np
 REPO = Path(__file__).resolve().parent
 sys.path.insert(0, str(REPO))
 
-# (name, kind, widths, weight seed); SURVEY.md §8-D "cfg2 = {MLP-256,
-# MLP-512-512, MLP-1024, CNN-s}"
+# (name, kind, widths, weight seed[, weight_mib, act_mib]); SURVEY.md §8-D rosters.
 ROSTER = [("mlp256", "mlp", [784, 256, 10], 11), ("mlp512x2", "mlp", [784, 512, 512, 10], 12),
           ("mlp1024", "mlp", [784, 1024, 10], 13), ("cnn-s", "cnn", [28, 4, 64, 32, 128, 10], 14)]
-WORKLOAD = ("cfg2: 4 heterogeneous MLP/CNN members (784-256-10, 784-512-512-10, 784-1024-10, "
-            "CNN-s 28x28-c4x4/4:64-c3x3:32-128-10) co-located on 1 B200, batches from bounded "
-            "greedy over calib_data; avg of softmax + argmax")
+# The twelve of cfg3/cfg5: MLP widths 128..2048 and three CNNs, with the
+# memory budgets of the reference's "dozen" acceptance spec (weights
+# 4600 - 100 m MiB, 10 MiB per sample: tests/acceptance.cpp:217-225), so WFD
+# packs them exactly as the reference does.
+DOZEN = [("mlp2048", "mlp", [784, 2048, 10]), ("mlp1024x2", "mlp", [784, 1024, 1024, 10]),
+         ("cnn-s", "cnn", [28, 4, 64, 32, 128, 10]), ("mlp1024", "mlp", [784, 1024, 10]),
+         ("mlp512x2", "mlp", [784, 512, 512, 10]), ("cnn-w", "cnn", [28, 4, 32, 64, 256, 10]),
+         ("mlp768", "mlp", [784, 768, 10]), ("mlp512", "mlp", [784, 512, 10]),
+         ("mlp384x2", "mlp", [784, 384, 384, 10]), ("mlp256", "mlp", [784, 256, 10]),
+         ("cnn-s2", "cnn", [28, 4, 64, 32, 128, 10]), ("mlp128", "mlp", [784, 128, 10])]
+DOZEN = [(n, k, w, 31 + m, 4600.0 - 100.0 * m, 10.0) for m, (n, k, w) in enumerate(DOZEN)]
+CONFIGS = {
+    "cfg1": {"roster": [("mlp256a", "mlp", [784, 256, 10], 1), ("mlp256b", "mlp", [784, 256, 10], 2)],
+             "devices": 1, "device_mib": 183359.0, "matrix": "fixed", "batches": [32, 32],
+             "softmax": False,
+             "workload": "cfg1: 2-member MLP ensemble (784-256-10 x 2), batch 32, averaging rule, "
+                         "1 device, as run by the CPU reference"},
+    "cfg2": {"roster": ROSTER, "devices": 1, "device_mib": 183359.0, "matrix": "greedy",
+             "softmax": True,
+             "workload": "cfg2: 4 heterogeneous MLP/CNN members (784-256-10, 784-512-512-10, "
+                         "784-1024-10, CNN-s 28x28-c4x4/4:64-c3x3:32-128-10) co-located on 1 B200, "
+                         "batches from bounded greedy over calib_data; avg of softmax + argmax"},
+    "cfg3": {"roster": DOZEN, "devices": 4, "device_mib": 16000.0, "matrix": "wfd", "softmax": True,
+             "workload": "cfg3: 12 heterogeneous members (MLP 128..2048 wide, 3 CNNs; reference "
+                         "dozen memory spec) worst-fit-decreasing packed into 4 device rows; avg of "
+                         "softmax + argmax"},
+    "cfg4": {"roster": [("mlp2048x2", "mlp", [784, 2048, 2048, 10], 41)], "devices": 1,
+             "device_mib": 183359.0, "matrix": "greedy", "softmax": True,
+             "workload": "cfg4: single DNN (MLP 784-2048-2048-10) data-parallel, per-GPU batch "
+                         "slices; batch from bounded greedy (batch-size-only baseline applies)"},
+    "cfg5": {"roster": DOZEN, "devices": 8, "device_mib": 16000.0, "matrix": "greedy",
+             "softmax": True,
+             "workload": "cfg5: full allocation optimizer sweep (worst-fit-decreasing + bounded "
+                         "greedy, device-timed bench) for the 12-member ensemble on 8 device rows"},
+}
 MENU = [8, 16, 32, 64, 128]
 PEAKS_PATH = REPO / "MEASURED_PEAKS.json"
 PROFILE_TRAFFIC = REPO / "profiles" / "roofline_traffic.json"
@@ -180,37 +211,51 @@ def rank_shard(es, world: int, rank: int, batches: list, nb_per_gpu: int, seg: i
 
 
 # ------------------------------------------------------------------ workload
-def roster_models(es):
+def roster_models(es, roster):
     out = []
-    for i, (name, kind, w, seed) in enumerate(ROSTER):
+    for i, r in enumerate(roster):
+        name, kind, w, seed = r[:4]
+        extra = {} if len(r) < 6 else {"weight_mib": r[4], "act_mib": r[5]}
         if kind == "cnn":
             out.append(es.cnn_model(i, name, seed, S=w[0], P=w[1], c1=w[2], c2=w[3], hidden=w[4],
-                                    classes=w[5]))
+                                    classes=w[5], **extra))
         else:
-            out.append(es.mlp_model(i, name, w, seed))
+            out.append(es.mlp_model(i, name, w, seed, **extra))
     return out
 
 
-def make_cluster(es, devices: int = 1):
-    models = roster_models(es)
-    devs = [es.DeviceSpec(d, es.GPU, 183359.0, 1e15, 0.0) for d in range(devices)]
+def make_cluster(es, cfg: dict, devices: int = 0):
+    models = roster_models(es, cfg["roster"])
+    devs = [es.DeviceSpec(d, es.GPU, cfg["device_mib"], 1e15, 0.0)
+            for d in range(devices or cfg["devices"])]
     return es.ClusterSpec(devs, models, list(MENU), 128)
 
 
-def choose_matrix(es, cluster, local_gpu: int, calib_nb: int, seed: int) -> dict:
-    """WFD (A1) then bounded greedy (A2) with the device-timed bench on calib."""
-    calib = es.SampleStore(synthetic_seed=seed + 1, nb=calib_nb, width=784, device=local_gpu)
+def choose_matrix(es, cluster, cfg: dict, device_map: list, calib_nb: int, seed: int) -> dict:
+    """A1 = WFD at the smallest batch; A2 = bounded greedy from A1 with the
+    device-timed bench on calib ("greedy"), A1 itself ("wfd"), or the
+    config's fixed batches ("fixed").  The batch-size-only baseline (BBS) is
+    run wherever the reference's bbs_baseline applies."""
+    calib = es.SampleStore(synthetic_seed=seed + 1, nb=calib_nb, width=784, device=device_map[0])
     t0 = time.time()
     A1 = es.worst_fit_decreasing(cluster, cluster.min_batch())
-    g = es.bounded_greedy(A1, cluster, es.DeviceBench(calib, 3, device_map=[local_gpu]),
-                          es.GreedyConfig(10, 100, seed))
+    score = lambda A: es.bench(A, calib, cluster, 3, device_map=device_map).throughput  # noqa: E731
+    if cfg["matrix"] == "greedy":
+        g = es.bounded_greedy(A1, cluster, es.DeviceBench(calib, 3, device_map=device_map),
+                              es.GreedyConfig(10, 100, seed))
+        A2, s1, s2, calls = g.matrix, g.trace.start_score, g.trace.final_score, g.trace.calls
+    else:
+        A2 = A1 if cfg["matrix"] == "wfd" else es.AllocationMatrix.from_array([cfg["batches"]])
+        s1, s2, calls = score(A1), score(A2), 2
     bbs = {"applicable": False}
     try:
-        es.bbs_baseline(cluster, es.DeviceBench(calib, 3, device_map=[local_gpu]))
+        r = es.bbs_baseline(cluster, es.DeviceBench(calib, 3, device_map=device_map))
+        bbs = {"applicable": True, "matrix": r.matrix.cells.tolist(),
+               "score": round(score(r.matrix), 1), "bench_calls": r.bench_calls,
+               "chosen_batches": r.chosen_batches}
     except es.BaselineError as e:
         bbs = {"applicable": False, "reason": str(e)}
-    return {"A1": A1, "A2": g.matrix, "A1_score": g.trace.start_score,
-            "A2_score": g.trace.final_score, "bench_calls": g.trace.calls,
+    return {"A1": A1, "A2": A2, "A1_score": s1, "A2_score": s2, "bench_calls": calls,
             "greedy_s": time.time() - t0, "bbs": bbs}
 
 
@@ -287,11 +332,12 @@ def roofline_for(es, cluster, A, kernels: list, nb: int, pk: dict) -> dict:
             "per_kernel": per_kernel}
 
 
-def cpu_baseline(cluster, A_cells: np.ndarray, budget_s: float = 12.0) -> dict:
+def cpu_baseline(cluster, A_cells: np.ndarray, budget_s: float = 12.0, softmax: bool = True) -> dict:
     """The reference InferenceSystem (compiled from /root/reference by
     oracle/Makefile) with the oracle CPU member, on this box's host cores:
-    every model data-parallel over floor(cores / M) CPU 'devices' so all
-    cores compute.  Bounded sample; returns samples/s."""
+    every model data-parallel over floor(cores / M) CPU 'devices' (batch =
+    its largest batch in A) so all cores compute.  Bounded sample; returns
+    samples/s."""
     from oracle import refcpu
     import paper_2208_14049_b200 as es
     cores = refcpu.host_cores()
@@ -299,8 +345,8 @@ def cpu_baseline(cluster, A_cells: np.ndarray, budget_s: float = 12.0) -> dict:
     D = max(1, cores // M)
     cpu_cluster = es.ClusterSpec([es.DeviceSpec(d, es.CPU, 1e9, 1.0, 0.0) for d in range(D)],
                                  cluster.models, list(MENU), cluster.segment_size)
-    A = np.tile(np.asarray(A_cells)[0], (D, 1)).astype(np.int32)
-    sysr = refcpu.RefSystem(cpu_cluster, A, softmax=True)
+    A = np.tile(np.asarray(A_cells).max(axis=0), (D, 1)).astype(np.int32)
+    sysr = refcpu.RefSystem(cpu_cluster, A, softmax=softmax)
     nb = 512 * D
     X = refcpu.features(5, nb, 784)
     el, _ = sysr.run(X)  # warm-up + size the sample to the budget
@@ -326,68 +372,85 @@ def run_b200(args, dist: Dist) -> dict | None:
     import paper_2208_14049_b200 as es
     pk = peaks()
     gpu = dist.local
-    cluster = make_cluster(es)
+    cfg = CONFIGS[args.config]
+    # Multi-row configs (cfg3: 4 rows, cfg5: 8) place members on device rows;
+    # one process drives every visible GPU (row d -> GPU d mod count, logits
+    # of remote rows peer-copied to the combining GPU).  Under torchrun rank 0
+    # runs them and the other ranks only join the barriers.  Single-row
+    # configs are replicated: each rank predicts its own segment shard.
+    multirow = cfg["devices"] > 1
+    ngpu = es.device_count()
+    device_map = [d % ngpu for d in range(cfg["devices"])] if multirow else [gpu]
+    cluster = make_cluster(es, cfg)
     if args.matrix:
-        A = es.AllocationMatrix.from_array([[int(b) for b in args.matrix.split(",")]])
+        A = es.AllocationMatrix.from_array([[int(b) for b in r.split(",")]
+                                            for r in args.matrix.split(";")])
         choice = {"A1": es.worst_fit_decreasing(cluster, cluster.min_batch()), "A2": A,
                   "A1_score": 0.0, "A2_score": 0.0, "bench_calls": 0,
                   "bbs": {"applicable": False, "reason": "matrix given on the command line"}}
+    elif multirow and dist.rank != 0:
+        choice = None
     else:
-        choice = choose_matrix(es, cluster, gpu, args.calib_nb, args.seed)
+        choice = choose_matrix(es, cluster, cfg, device_map, args.calib_nb, args.seed)
+    rule = es.CombinationRule.averaging(softmax=cfg["softmax"])
+    active = not multirow or dist.rank == 0
+    local_nb = 0
+    if active:
         A = choice["A2"]
-    rule = es.CombinationRule.averaging(softmax=True)
-    r0, r1, _ = rank_shard(es, dist.world, dist.rank, A.cells[0].tolist(), args.nb)
-    local_nb = r1 - r0
-    X = es.SampleStore(synthetic_seed=args.seed + dist.rank * 7919, nb=local_nb, width=784,
-                       device=gpu)
-    system = es.InferenceSystem(A, cluster, rule, device_map=[gpu], copy_outputs=False,
-                                e2e_host_convert=bool(args.e2e_host_convert))
-    for _ in range(args.warmup):
-        system.run(X, copy=False)
+        if multirow:
+            r0, r1 = 0, args.nb
+        else:
+            r0, r1, _ = rank_shard(es, dist.world, dist.rank, A.cells[0].tolist(), args.nb)
+        local_nb = r1 - r0
+        X = es.SampleStore(synthetic_seed=args.seed + dist.rank * 7919, nb=local_nb, width=784,
+                           device=device_map[0])
+        system = es.InferenceSystem(A, cluster, rule, device_map=device_map, copy_outputs=False,
+                                    e2e_host_convert=bool(args.e2e_host_convert))
+        for _ in range(args.warmup):
+            system.run(X, copy=False)
     launches = 0
     step_s = []
-    member_ms = np.zeros(system.worker_count())
-    kern = [None] * system.worker_count()
+    kern = []
     combine_ms = 0.0
     dist.barrier()
     with ClockSampler(gpu) as clocks:
         t0 = time.perf_counter()
-        for _ in range(args.steps):
+        for _ in range(args.steps if active else 0):
             out = system.run(X, copy=False)
             step_s.append(out.stats.elapsed_s)
             launches += system.launches_last_run()
-            ms, cm = system.timing()
-            member_ms += np.asarray(ms)
-            combine_ms += cm
-            for w in range(system.worker_count()):
-                kt = system.kernel_timing(w)
-                kern[w] = kt if kern[w] is None else [(n, a + b) for (n, a), (_, b)
-                                                      in zip(kern[w], kt)]
+            combine_ms += system.timing()[1]
+            kt = [system.kernel_timing(w) for w in range(system.worker_count())]
+            kern = kt if not kern else [[(n, a + b) for (n, a), (_, b) in zip(k0, k1)]
+                                        for k0, k1 in zip(kern, kt)]
         wall = time.perf_counter() - t0
     dist.barrier()
     device_s = dist.max(float(sum(step_s)))
     covered = sum(dist.gather([local_nb]), [])
-    member_ms /= args.steps
-    combine_ms /= args.steps
+    combine_ms /= max(1, args.steps)
     kern = [[(n, t / args.steps) for n, t in k] for k in kern]
 
-    # e2e: host (pinned) X in, combined probabilities + labels out, per step
-    e2e_nb = max(1, min(args.e2e_nb, args.nb))
-    try:
-        import torch
-        Xh_t = torch.empty((e2e_nb, 784), dtype=torch.float32, pin_memory=True)
-        Xh = Xh_t.numpy()
-        Yh = torch.empty((e2e_nb, 10), dtype=torch.float32, pin_memory=True).numpy()
-        Lh = torch.empty((e2e_nb,), dtype=torch.int32, pin_memory=True).numpy()
-    except Exception:
-        Xh = np.empty((e2e_nb, 784), np.float32)
-        Yh = np.empty((e2e_nb, 10), np.float32)
-        Lh = np.empty(e2e_nb, np.int32)
-    rng = np.random.default_rng(args.seed + dist.rank)
-    Xh[:] = rng.random((e2e_nb, 784), dtype=np.float32)
-    e2e_steps = args.steps if args.e2e else 1
-    for _ in range(max(1, args.warmup // 2) if args.e2e else 0):
-        system.run_host(Xh, Yh, Lh)
+    # e2e: host (pinned) X in, combined probabilities + labels out, per step.
+    # Needs every worker on one GPU (run_host); skipped for multi-GPU rows.
+    e2e = None
+    if active and len(set(device_map)) == 1:
+        e2e_nb = max(1, min(args.e2e_nb, args.nb))
+        try:
+            import torch
+            Xh = torch.empty((e2e_nb, 784), dtype=torch.float32, pin_memory=True).numpy()
+            Yh = torch.empty((e2e_nb, 10), dtype=torch.float32, pin_memory=True).numpy()
+            Lh = torch.empty((e2e_nb,), dtype=torch.int32, pin_memory=True).numpy()
+        except Exception:
+            Xh = np.empty((e2e_nb, 784), np.float32)
+            Yh = np.empty((e2e_nb, 10), np.float32)
+            Lh = np.empty(e2e_nb, np.int32)
+        rng = np.random.default_rng(args.seed + dist.rank)
+        Xh[:] = rng.random((e2e_nb, 784), dtype=np.float32)
+        e2e_steps = args.steps if args.e2e else 1
+        for _ in range(max(1, args.warmup // 2) if args.e2e else 0):
+            system.run_host(Xh, Yh, Lh)
+    else:
+        e2e_steps, e2e_nb = 0, 0
     dist.barrier()
     e2e_s, h2d, d2h = [], 0, 0
     for _ in range(e2e_steps):
@@ -396,12 +459,21 @@ def run_b200(args, dist: Dist) -> dict | None:
         h2d, d2h = h2d + hb, d2h + db
     dist.barrier()
     e2e_total = dist.max(float(sum(e2e_s)))
-    system.close()
+    e2e_ranks = sum(1 for v in dist.gather([len(e2e_s)]) if v[0] > 0)
+    if e2e_steps:
+        e2e = {"value": round(e2e_ranks * e2e_nb * e2e_steps / e2e_total, 1), "unit": "samples/s",
+               "h2d_bytes_per_step": h2d // e2e_steps, "d2h_bytes_per_step": d2h // e2e_steps,
+               "input": "pinned fp32 X; chunks alternate host fp32->bf16 conversion (2 B/feature "
+                        "on the wire) and fp32 DMA + device conversion",
+               "samples_per_step": e2e_nb}
+    if active:
+        system.close()
 
     if dist.rank != 0:
         return None
     n = dist.world
     value = sum(covered) * args.steps / device_s
+    ngpus_used = len(set(device_map)) if multirow else n
     result = {
         "metric": "ensemble samples/sec at 1/2/4/8 B200 vs batch-only baseline and CPU ref",
         "value": round(value, 1),
@@ -411,42 +483,45 @@ def run_b200(args, dist: Dist) -> dict | None:
         "warmup": args.warmup,
         "ms_per_step": round(device_s / args.steps * 1e3, 4),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if multirow else "weak",
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (U[0,1) features generated on device; Glorot-uniform synthetic weights)",
         "config": {
-            "workload": WORKLOAD,
-            "samples_per_gpu_per_step": args.nb,
+            "workload": cfg["workload"],
+            "config": args.config,
+            "samples_per_gpu_per_step": args.nb if not multirow else None,
+            "samples_per_step": sum(covered),
             "x_bytes_per_gpu": args.nb * 784 * 2,
             "l2": "inputs (bf16 X) larger than L2, no flush",
+            "device_rows": cfg["devices"],
+            "device_map": device_map,
+            "gpus_used": ngpus_used,
             "matrix_A1_wfd": choice["A1"].cells.tolist(),
-            "matrix_A2_greedy": A.cells.tolist(),
+            "matrix_A2": A.cells.tolist(),
+            "matrix_rule": cfg["matrix"],
             "A1_score": round(choice["A1_score"], 1),
             "A2_score": round(choice["A2_score"], 1),
             "greedy_bench_calls": choice["bench_calls"],
             "calib_samples": args.calib_nb,
             "batch_only_baseline": choice["bbs"],
-            "parallelism": f"ensemble replicated per GPU, dp{n} over samples",
+            "parallelism": (f"members placed on {cfg['devices']} device rows over {ngpus_used} "
+                            f"GPU(s), remote logits peer-copied to the combining GPU") if multirow
+            else f"ensemble replicated per GPU, dp{n} over samples",
             "segment_size": 128,
         },
         "roofline": roofline_for(es, cluster, A, kern, args.nb, pk),
-        "member_ms": [round(float(x), 4) for x in member_ms],
+        "member_ms": [round(sum(t for _, t in k), 4) for k in kern],
         "combine_ms": round(combine_ms, 4),
-        "combine_hbm_gbs": round(args.nb * (len(ROSTER) * 40 + 44) / (combine_ms * 1e-3) / 1e9, 1)
+        "combine_hbm_gbs": round(args.nb * (len(cfg["roster"]) * 40 + 44) / (combine_ms * 1e-3) / 1e9, 1)
         if combine_ms > 0 else None,
-        "e2e": {"value": round(n * e2e_nb * e2e_steps / e2e_total, 1), "unit": "samples/s",
-                "h2d_bytes_per_step": h2d // e2e_steps,
-                "d2h_bytes_per_step": d2h // e2e_steps,
-                "input": "pinned fp32 X; chunks alternate host fp32->bf16 conversion (2 B/feature "
-                         "on the wire) and fp32 DMA + device conversion",
-                "samples_per_step": e2e_nb},
+        "e2e": e2e,
         "gpu_launches": launches,
         "clocks": clocks.summary(),
         "host_wall_s": round(wall, 4),
     }
     if args.cpu_baseline and n == 1:
-        result["cpu_baseline"] = cpu_baseline(cluster, A.cells)
+        result["cpu_baseline"] = cpu_baseline(cluster, A.cells, softmax=cfg["softmax"])
     return result
 
 
@@ -458,12 +533,14 @@ def run_reference(args, dist: Dist) -> dict | None:
         return None
     import paper_2208_14049_b200 as es
     from oracle import refcpu
-    cluster = make_cluster(es)
-    # The reference cannot time a GPU bench: take the b200 arm's default matrix
-    # shape with the batch sizes WFD gives (A1), which is what the reference's
-    # optimizer starts from.
-    A1 = es.worst_fit_decreasing(cluster, 32)
-    base = cpu_baseline(cluster, A1.cells, budget_s=max(4.0, 2.0 * args.steps))
+    cfg = CONFIGS[args.config]
+    cluster = make_cluster(es, cfg)
+    # The reference cannot time a GPU bench: take the b200 arm's matrix shape
+    # with the batch sizes WFD gives (A1), which is what the reference's
+    # optimizer starts from (cfg1: its fixed batch 32).
+    A1 = es.worst_fit_decreasing(cluster, 32 if cfg["matrix"] != "fixed" else cfg["batches"][0])
+    base = cpu_baseline(cluster, A1.cells, budget_s=max(4.0, 2.0 * args.steps),
+                        softmax=cfg["softmax"])
     value = base["value"]
     return {
         "impl": "reference",
@@ -471,7 +548,8 @@ def run_reference(args, dist: Dist) -> dict | None:
         "value": value, "unit": "samples/s", "n_gpus": dist.world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32 (bf16-quantised operands)",
-        "data": "synthetic", "config": {"workload": WORKLOAD + " -- on host cores (reference runtime)"},
+        "data": "synthetic", "config": {"workload": cfg["workload"] + " -- on host cores (reference runtime)",
+                                       "config": args.config},
         "cpu_baseline": base,
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -494,7 +572,10 @@ def main():
     ap.add_argument("--e2e-host-convert", type=int, default=1,
                     help="e2e: 1 = host fp32->bf16 before the H2D copy, 0 = fp32 over PCIe")
     ap.add_argument("--matrix", default="",
-                    help="profiling: batch per member (e.g. 64,64,128,128), skips the greedy")
+                    help="profiling: batch per member, rows separated by ';' (e.g. 64,64,128,128), "
+                         "skips the greedy")
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS),
+                    help="BASELINE.json config (default cfg2, the metric's config)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         args.warmup = 3
