@@ -26,6 +26,7 @@ struct DenseLayout {
   int logits = 0, C = 0;          // final-layer mode: fp32 logits, C <= 16 columns
   int T = 1, nbuf = 1, nh = 1, NH = 0;
   int relu = 1;
+  int pair = 0;                   // dense_pair_sm100 layout (SM pairs, cta_group::2)
   int stages = 0, group_cols = 0, tmem_cols = 0;
   uint32_t stage_bytes = 0, off_stage_out = 0, off_bias = 0, off_bar = 0, smem_bytes = 0;
 };
@@ -45,5 +46,11 @@ bool dense_logits_plan(int K, int C, DenseLayout* out);
 // logits mode, which writes args.logits).
 int dense_launch(const DenseArgs& args, const void* x, long long x_rows, const void* w, void* y,
                  int grid, cudaStream_t stream);
+
+// The same hidden layer on SM pairs (dense_pair_kernel.cu): each SM of a
+// 2-CTA cluster streams half of every W chunk.  N a multiple of 128.
+bool dense_pair_plan(int K, int N, bool relu, DenseLayout* out);
+int dense_pair_launch(const DenseArgs& args, const void* x, long long x_rows, const void* w, void* y,
+                      int grid, cudaStream_t stream);
 
 }  // namespace es

@@ -49,6 +49,13 @@ bool env_is(const char* name, const char* value) {
   return v && std::strcmp(v, value) == 0;
 }
 
+// Hidden dense layers: the SM-pair kernel (half of every W chunk per SM) unless
+// ES_DENSE_KERNEL=single; the single-SM kernel when no pair plan exists.
+bool plan_dense(int K, int N, es::DenseLayout* d) {
+  if (!env_is("ES_DENSE_KERNEL", "single") && es::dense_pair_plan(K, N, true, d)) return true;
+  return es::dense_plan(K, N, true, d);
+}
+
 }  // namespace
 
 struct DeviceMember::Impl {
@@ -120,7 +127,7 @@ bool DeviceMember::load(int device, const ModelSpec& model, int batch) {
     // Leading layers: tcgen05 dense layers with a bf16 output.
     for (int l = 0; l < L - 2; ++l) {
       es::DenseLayout d;
-      if (!es::dense_plan(I.dims[l].first, I.dims[l].second, true, &d))
+      if (!plan_dense(I.dims[l].first, I.dims[l].second, &d))
         throw SpecError(model.name + ": leading layer " + std::to_string(I.dims[l].first) + "->" +
                         std::to_string(I.dims[l].second) +
                         " has no tile plan (input width a multiple of 8, output width a "
@@ -148,7 +155,7 @@ bool DeviceMember::load(int device, const ModelSpec& model, int batch) {
   else if (want.empty() || want == "dense") {
     // Hidden layer wider than one SM's TMEM: no fused head.
     es::DenseLayout d;
-    if (!es::dense_plan(K, H, true, &d) || !es::dense_logits_plan(H, C, &I.logits))
+    if (!plan_dense(K, H, &d) || !es::dense_logits_plan(H, C, &I.logits))
       throw SpecError(model.name + ": layers " + std::to_string(K) + "->" + std::to_string(H) +
                       "->" + std::to_string(C) + " have no tile plan");
     I.dense.push_back(d);
@@ -196,7 +203,7 @@ std::vector<std::string> DeviceMember::kernel_names() const {
   const Impl& I = *impl_;
   if (I.head == Impl::Head::Synthetic) return {"synthetic_member_kernel"};
   if (I.cnn) n.push_back(I.conv.split ? "conv_stack_sm100[split]" : "conv_stack_sm100[tap]");
-  for (std::size_t i = 0; i < I.dense.size(); ++i) n.push_back("dense_sm100");
+  for (const auto& d : I.dense) n.push_back(d.pair ? "dense_pair_sm100" : "dense_sm100");
   if (env_is("ES_MEMBER_KERNEL", "simt") && I.head != Impl::Head::Dense) {
     n.push_back("mlp2_simt_kernel");
     return n;
@@ -257,7 +264,8 @@ int DeviceMember::forward(const void* x, long long nb, int seg_size, long long s
     d.row_begin = r0;
     d.row_end = r1;
     d.bias = reinterpret_cast<const float*>(base + I.b_off[l]);
-    M_LAUNCH(es::dense_launch(d, cur, nb, base + I.w_off[l], y, grid, stream));
+    M_LAUNCH(d.L.pair ? es::dense_pair_launch(d, cur, nb, base + I.w_off[l], y, grid, stream)
+                      : es::dense_launch(d, cur, nb, base + I.w_off[l], y, grid, stream));
     mark(launches++);
     cur = y;
   }

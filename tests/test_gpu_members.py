@@ -17,7 +17,12 @@ pytestmark = pytest.mark.gpu
 @pytest.mark.parametrize("widths", [[784, 512, 512, 10], [784, 256, 384, 128, 10],
                                     [784, 128, 256, 10]])
 @pytest.mark.parametrize("b", [32, 128])
-def test_deep_mlp_member_matches_cpu_oracle(widths, b):
+@pytest.mark.parametrize("dense", ["pair", "single"])
+def test_deep_mlp_member_matches_cpu_oracle(widths, b, dense, monkeypatch):
+    """Leading layers on the SM-pair dense kernel (default) and on the
+    single-SM one (ES_DENSE_KERNEL=single)."""
+    if dense == "single":
+        monkeypatch.setenv("ES_DENSE_KERNEL", "single")
     X = refcpu.features(41, 700, 784)
     model = es.mlp_model(0, "deep", widths, 4242)
     got = es.Member(model, b).predict(X)
@@ -30,10 +35,12 @@ def test_deep_mlp_member_matches_cpu_oracle(widths, b):
 
 
 @pytest.mark.parametrize("widths", [[784, 1024, 10], [784, 2048, 10], [784, 640, 16],
-                                    [784, 2048, 2048, 10]])
+                                    [784, 2048, 2048, 10], [784, 1536, 1024, 10]])
 def test_wide_mlp_member_matches_cpu_oracle(widths):
-    """Hidden layers wider than one SM's TMEM: dense kernel in column blocks,
-    last layer in the dense kernel's logits mode."""
+    """Hidden layers wider than one SM's TMEM: the pair kernel's hidden
+    passes (1024, 1536, 2048), or -- when the width does not split into
+    128-multiple passes (640) -- the dense kernel in column blocks with the
+    last layer in its logits mode."""
     X = refcpu.features(42, 333, 784)
     model = es.mlp_model(0, "wide", widths, 4343)
     got = es.Member(model, 64).predict(X)
