@@ -17,6 +17,6 @@ cap mlp256_tmem member_mlp2_tmem mlp:784,256,10
 cap mlp512_pair member_mlp2_pair mlp:784,512,10
 cap cnn_conv conv_stack cnn
 cap cnn_head member_mlp2 cnn
-cap mlp1024_dense dense_sm100 mlp:784,1024,10
-cap mlp512x2_dense dense_sm100 mlp:784,512,512,10
+cap mlp1024_pair member_mlp2_pair mlp:784,1024,10
+cap mlp512x2_dense dense_pair mlp:784,512,512,10
 cap combine combine_kernel mlp:784,128,10

@@ -9,9 +9,13 @@ tag=${1:-cur}
 topk=${2:-conv_stack}
 out=gpurun_out
 mkdir -p $out
-timeout 900 python bench.py > $out/${tag}_bench.json 2> $out/${tag}_bench.err
-cat $out/${tag}_bench.json
-matrix=$(python -c "import json;print(','.join(map(str,json.load(open('$out/${tag}_bench.json'))['config']['matrix_A2_greedy'][0])))")
+if [ -z "${MATRIX:-}" ]; then
+  timeout 900 python bench.py > $out/${tag}_bench.json 2> $out/${tag}_bench.err
+  cat $out/${tag}_bench.json
+  matrix=$(python -c "import json;print(','.join(map(str,json.load(open('$out/${tag}_bench.json'))['config']['matrix_A2'][0])))")
+else
+  matrix=$MATRIX  # bench already run: profile this matrix only
+fi
 echo "matrix $matrix"
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file $out/${tag}_launches.csv python bench.py --matrix $matrix --steps 2 --warmup 3 \
