@@ -268,6 +268,46 @@ void es_member_destroy(es_member* m);
 es_status es_combine(const es_rule_desc* rule, int M, int C, size_t rows,
                      const float* const* blocks, float* Y, int32_t* winners);
 
+/* ------------------------------------------------ spec / matrix / cache documents */
+/* On-disk formats of include/enserve/core/spec_io.hpp and
+ * include/enserve/server/cache.hpp: a reference-written
+ * file loads here and vice versa, and cache keys are identical.  Text results
+ * go to buf[len] (NUL-terminated; *needed = bytes required, buf may be NULL to
+ * ask); ES_ERR_BUFFER when len is too small. */
+typedef struct es_spec es_spec;
+/* cluster_to_json (spec_io.cpp:7-28) dumped like nlohmann's dump(indent)
+ * (indent < 0: compact).  with_arch adds each member's architecture as an
+ * optional "arch" object the reference parser ignores. */
+es_status es_cluster_to_json(const es_cluster_desc* c, int indent, int with_arch, char* buf,
+                             size_t len, size_t* needed);
+/* cluster_from_documents (spec_io.cpp:82-89; overlay may be NULL) +
+ * cluster_from_json (:47-80): SpecError on a malformed document. */
+es_status es_spec_from_json(const char* base_json, const char* overlay_json, es_spec** out);
+/* load_json_file (spec_io.cpp:135-143) of a --cluster and an optional
+ * --ensemble file, merged. */
+es_status es_spec_load(const char* path, const char* overlay_path, es_spec** out);
+/* The parsed cluster as a descriptor (pointers valid while the handle lives). */
+es_status es_spec_describe(es_spec* s, es_cluster_desc* out);
+void es_spec_destroy(es_spec* s);
+/* save_json_file (spec_io.cpp:145-149): the document indented by 2 + "\n". */
+es_status es_save_json_file(const char* path, const char* json_text);
+/* matrix_to_json / matrix_from_json (spec_io.cpp:91-133). */
+es_status es_matrix_to_json(const es_cluster_desc* c, const int* A, int indent, char* buf,
+                            size_t len, size_t* needed);
+es_status es_matrix_from_json(const es_cluster_desc* c, const char* json_text, int* A_out);
+/* digest_hex (cache.cpp:11-20): FNV-1a 64, 16 hex digits + NUL. */
+es_status es_digest_hex(const char* text, char out[17]);
+/* cache_key (cache.cpp:22-33) of the cluster and the optimizer settings. */
+es_status es_cache_key(const es_cluster_desc* c, int max_iter, int max_neighs, uint64_t rng_seed,
+                       int default_batch, const char* bench_mode, size_t calib_samples,
+                       int repeats, char out[17]);
+/* MatrixCache::lookup / store (cache.cpp:35-88): corrupt, stale or invalid
+ * entries are misses (*hit = 0), never errors. */
+es_status es_cache_lookup(const char* directory, const char* key, const es_cluster_desc* c,
+                          int* A_out, double* score, int64_t* created_at, int* hit);
+es_status es_cache_store(const char* directory, const char* key, const es_cluster_desc* c,
+                         const int* A, double score, int64_t created_at);
+
 #ifdef __cplusplus
 }
 #endif

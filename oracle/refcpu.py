@@ -38,6 +38,7 @@ def build(quiet: bool = True) -> None:
         targets.append("_ref/libenserve_ref.so")
         if (HERE.parent / "paper_2208_14049_b200" / "libenserve_b200.so").exists():
             targets.append("integration")
+        targets.append("spec_golden")  # the reference's spec/cache units (tests/golden/spec_io.json)
     subprocess.run(["make", "-C", str(HERE), *targets], check=True,
                    stdout=subprocess.DEVNULL if quiet else None)
 

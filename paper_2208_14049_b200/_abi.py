@@ -75,6 +75,23 @@ class GreedyTrace(C.Structure):
 
 # name -> (restype, argtypes)
 _SIGS = {
+    "es_cluster_to_json": (C.c_int, [C.POINTER(ClusterDesc), C.c_int, C.c_int, C.c_char_p,
+                                     C.c_size_t, c_size_t_p]),
+    "es_spec_from_json": (C.c_int, [C.c_char_p, C.c_char_p, C.POINTER(C.c_void_p)]),
+    "es_spec_load": (C.c_int, [C.c_char_p, C.c_char_p, C.POINTER(C.c_void_p)]),
+    "es_spec_describe": (C.c_int, [C.c_void_p, C.POINTER(ClusterDesc)]),
+    "es_spec_destroy": (None, [C.c_void_p]),
+    "es_save_json_file": (C.c_int, [C.c_char_p, C.c_char_p]),
+    "es_matrix_to_json": (C.c_int, [C.POINTER(ClusterDesc), c_int_p, C.c_int, C.c_char_p,
+                                    C.c_size_t, c_size_t_p]),
+    "es_matrix_from_json": (C.c_int, [C.POINTER(ClusterDesc), C.c_char_p, c_int_p]),
+    "es_digest_hex": (C.c_int, [C.c_char_p, C.c_char_p]),
+    "es_cache_key": (C.c_int, [C.POINTER(ClusterDesc), C.c_int, C.c_int, C.c_uint64, C.c_int,
+                               C.c_char_p, C.c_size_t, C.c_int, C.c_char_p]),
+    "es_cache_lookup": (C.c_int, [C.c_char_p, C.c_char_p, C.POINTER(ClusterDesc), c_int_p,
+                                  c_double_p, C.POINTER(C.c_int64), c_int_p]),
+    "es_cache_store": (C.c_int, [C.c_char_p, C.c_char_p, C.POINTER(ClusterDesc), c_int_p,
+                                 C.c_double, C.c_int64]),
     "es_abi_version": (C.c_int, []),
     "es_status_name": (C.c_char_p, [C.c_int]),
     "es_last_error": (C.c_char_p, []),

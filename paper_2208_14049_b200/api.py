@@ -853,3 +853,130 @@ def combine(rule: CombinationRule, blocks: Sequence[np.ndarray]) -> tuple:
     _check(lib().es_combine(C.byref(rule._desc(keep)), len(arrs), Cw, rows, ptrs,
                             Y.ctypes.data_as(_abi.c_float_p), W.ctypes.data_as(_abi.c_int32_p)))
     return Y, W
+
+
+# ------------------------------------------------------------------ documents
+def _text(call) -> str:
+    """Two-pass text result: ask for the size, then fill."""
+    need = C.c_size_t()
+    _check(call(None, 0, C.byref(need)))
+    buf = C.create_string_buffer(need.value)
+    _check(call(buf, need.value, C.byref(need)))
+    return buf.value.decode()
+
+
+def _cluster_from_desc(d: "_abi.ClusterDesc") -> ClusterSpec:
+    devs = [DeviceSpec(i, CPU if d.devices[i].kind == 0 else GPU, d.devices[i].memory_mib,
+                       d.devices[i].compute_rate, d.devices[i].batch_overhead_s)
+            for i in range(d.n_devices)]
+    models = []
+    for i in range(d.n_models):
+        m = d.models[i]
+        kind = {1: "mlp", 2: "cnn"}.get(m.arch, "synthetic")
+        arch = MemberArch(kind, tuple(m.widths[j] for j in range(m.n_widths)), int(m.weight_seed))
+        models.append(ModelSpec(i, m.name.decode(), m.weight_mib, m.act_mib_per_sample,
+                                m.cost_per_sample, m.output_width, arch))
+    return ClusterSpec(devs, models, [d.batch_menu[i] for i in range(d.menu_size)], d.segment_size)
+
+
+def _spec_handle_to_cluster(h: C.c_void_p) -> ClusterSpec:
+    try:
+        d = _abi.ClusterDesc()
+        _check(lib().es_spec_describe(h, C.byref(d)))
+        return _cluster_from_desc(d)
+    finally:
+        lib().es_spec_destroy(h)
+
+
+def cluster_to_json(cluster: ClusterSpec, indent: int = -1, with_arch: bool = False) -> str:
+    """spec_io.cpp:7-28, dumped like nlohmann's dump(indent)."""
+    with _Desc(cluster) as d:
+        return _text(lambda b, n, need: lib().es_cluster_to_json(d.ptr, indent, int(with_arch),
+                                                                 b, n, need))
+
+
+def cluster_from_json(text: str, overlay: Optional[str] = None) -> ClusterSpec:
+    """cluster_from_documents + cluster_from_json (spec_io.cpp:47-89)."""
+    h = C.c_void_p()
+    _check(lib().es_spec_from_json(text.encode(), overlay.encode() if overlay else None,
+                                   C.byref(h)))
+    return _spec_handle_to_cluster(h)
+
+
+def load_spec(path: str, overlay_path: Optional[str] = None) -> ClusterSpec:
+    """A --cluster file merged with an optional --ensemble file."""
+    h = C.c_void_p()
+    _check(lib().es_spec_load(str(path).encode(),
+                              str(overlay_path).encode() if overlay_path else None, C.byref(h)))
+    return _spec_handle_to_cluster(h)
+
+
+def save_json_file(path: str, text: str) -> None:
+    """spec_io.cpp:145-149 (indent 2 + newline)."""
+    _check(lib().es_save_json_file(str(path).encode(), text.encode()))
+
+
+def matrix_to_json(A: AllocationMatrix, cluster: ClusterSpec, indent: int = -1) -> str:
+    with _Desc(cluster) as d:
+        return _text(lambda b, n, need: lib().es_matrix_to_json(d.ptr, A.ptr(), indent, b, n, need))
+
+
+def matrix_from_json(text: str, cluster: ClusterSpec) -> AllocationMatrix:
+    A = AllocationMatrix(cluster.device_count(), cluster.model_count())
+    with _Desc(cluster) as d:
+        _check(lib().es_matrix_from_json(d.ptr, text.encode(), A.ptr()))
+    return A
+
+
+def digest_hex(text: str) -> str:
+    out = C.create_string_buffer(17)
+    _check(lib().es_digest_hex(text.encode(), out))
+    return out.value.decode()
+
+
+@dataclass
+class OptimizerKey:
+    """cache.hpp OptimizerKey: settings that change the optimized matrix."""
+    greedy: GreedyConfig = field(default_factory=GreedyConfig)
+    default_batch: int = 0
+    bench_mode: str = "measured"
+    calib_samples: int = 0
+    repeats: int = 1
+
+
+def cache_key(cluster: ClusterSpec, key: OptimizerKey) -> str:
+    """cache.cpp:22-33."""
+    out = C.create_string_buffer(17)
+    with _Desc(cluster) as d:
+        _check(lib().es_cache_key(d.ptr, key.greedy.max_iter, key.greedy.max_neighs,
+                                  key.greedy.rng_seed, key.default_batch, key.bench_mode.encode(),
+                                  key.calib_samples, key.repeats, out))
+    return out.value.decode()
+
+
+@dataclass
+class MatrixCacheEntry:
+    key: str
+    matrix: AllocationMatrix
+    score: float = 0.0
+    created_at: int = 0
+
+
+class MatrixCache:
+    """One JSON document per key under a directory (cache.cpp:35-88)."""
+
+    def __init__(self, directory: str):
+        self.directory = str(directory)
+
+    def lookup(self, key: str, cluster: ClusterSpec) -> Optional[MatrixCacheEntry]:
+        A = AllocationMatrix(cluster.device_count(), cluster.model_count())
+        score, created, hit = C.c_double(), C.c_int64(), C.c_int()
+        with _Desc(cluster) as d:
+            _check(lib().es_cache_lookup(self.directory.encode(), key.encode(), d.ptr, A.ptr(),
+                                         C.byref(score), C.byref(created), C.byref(hit)))
+        return MatrixCacheEntry(key, A, score.value, created.value) if hit.value else None
+
+    def store(self, entry: MatrixCacheEntry, cluster: ClusterSpec) -> None:
+        with _Desc(cluster) as d:
+            _check(lib().es_cache_store(self.directory.encode(), entry.key.encode(), d.ptr,
+                                        entry.matrix.ptr(), entry.score, entry.created_at))

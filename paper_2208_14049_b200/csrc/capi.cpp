@@ -12,6 +12,7 @@
 #include <string>
 
 #include "enserve/host_convert.hpp"
+#include "enserve/spec_io.hpp"
 #include "enserve/placement.hpp"
 #include "enserve/rng.hpp"
 #include "enserve/runtime.hpp"
@@ -30,6 +31,14 @@ struct es_system {
 
 struct es_member {
   std::unique_ptr<B200Predictor> predictor;
+};
+
+// A parsed spec document: the ClusterSpec plus the C views es_spec_describe
+// hands out (valid while the handle lives).
+struct es_spec {
+  enserve::ClusterSpec cluster;
+  std::vector<es_device_desc> devices;
+  std::vector<es_model_desc> models;
 };
 
 namespace {
@@ -666,6 +675,188 @@ es_status es_combine(const es_rule_desc* rule, int M, int C, size_t rows,
                      const float* const* blocks, float* Y, int32_t* winners) {
   return guard([&] {
     combine_blocks(to_rule(rule, M), M, C, rows, blocks, Y, winners);
+    return ES_OK;
+  });
+}
+
+
+// ------------------------------------------------------------ spec / matrix / cache documents
+namespace {
+
+es_status put_text(const std::string& text, char* buf, size_t len, size_t* needed) {
+  if (needed) *needed = text.size() + 1;
+  if (!buf) return ES_OK;
+  if (len < text.size() + 1) {
+    g_last_error = "buffer too small";
+    return ES_ERR_BUFFER;
+  }
+  std::memcpy(buf, text.c_str(), text.size() + 1);
+  return ES_OK;
+}
+
+es_spec* make_spec(ClusterSpec c) {
+  auto* s = new es_spec();
+  s->cluster = std::move(c);
+  for (const DeviceSpec& d : s->cluster.devices)
+    s->devices.push_back({d.kind == DeviceKind::CPU ? 0 : 1, d.memory_mib, d.compute_rate,
+                          d.batch_overhead_s});
+  for (const ModelSpec& m : s->cluster.models) {
+    es_model_desc x{};
+    x.name = m.name.c_str();
+    x.weight_mib = m.weight_mib;
+    x.act_mib_per_sample = m.act_mib_per_sample;
+    x.cost_per_sample = m.cost_per_sample;
+    x.output_width = m.output_width;
+    x.arch = m.arch.kind == MemberArch::Kind::MLP ? 1 : m.arch.kind == MemberArch::Kind::CNN ? 2 : 0;
+    x.n_widths = static_cast<int>(std::min<std::size_t>(m.arch.widths.size(), ES_MAX_WIDTHS));
+    for (int i = 0; i < x.n_widths; ++i) x.widths[i] = m.arch.widths[i];
+    x.weight_seed = m.arch.weight_seed;
+    s->models.push_back(x);
+  }
+  return s;
+}
+
+OptimizerKey opt_key(int max_iter, int max_neighs, uint64_t seed, int default_batch,
+                     const char* bench_mode, size_t calib_samples, int repeats) {
+  OptimizerKey k;
+  k.greedy.max_iter = max_iter;
+  k.greedy.max_neighs = max_neighs;
+  k.greedy.rng_seed = seed;
+  k.default_batch = default_batch;
+  k.bench_mode = bench_mode ? bench_mode : "";
+  k.calib_samples = calib_samples;
+  k.repeats = repeats;
+  return k;
+}
+
+js::Value parse_text(const char* text, const char* what) {
+  need(text != nullptr, what);
+  try {
+    return js::parse(text);
+  } catch (const std::exception& e) {
+    throw SpecError(e.what());
+  }
+}
+
+}  // namespace
+
+es_status es_cluster_to_json(const es_cluster_desc* c, int indent, int with_arch, char* buf,
+                             size_t len, size_t* needed) {
+  return guard([&] {
+    return put_text(js::dump(cluster_to_json(to_cluster(c), with_arch != 0), indent), buf, len,
+                    needed);
+  });
+}
+
+es_status es_spec_from_json(const char* base_json, const char* overlay_json, es_spec** out) {
+  return guard([&] {
+    need(out != nullptr, "out is NULL");
+    const js::Value base = parse_text(base_json, "spec text is NULL");
+    const js::Value overlay = overlay_json ? parse_text(overlay_json, "") : js::Value();
+    *out = make_spec(cluster_from_documents(base, overlay));
+    return ES_OK;
+  });
+}
+
+es_status es_spec_load(const char* path, const char* overlay_path, es_spec** out) {
+  return guard([&] {
+    need(path != nullptr && out != nullptr, "path or out is NULL");
+    const js::Value base = load_json_file(path);
+    const js::Value overlay = overlay_path ? load_json_file(overlay_path) : js::Value();
+    *out = make_spec(cluster_from_documents(base, overlay));
+    return ES_OK;
+  });
+}
+
+es_status es_spec_describe(es_spec* s, es_cluster_desc* out) {
+  return guard([&] {
+    need(s != nullptr && out != nullptr, "NULL handle");
+    out->devices = s->devices.data();
+    out->n_devices = static_cast<int>(s->devices.size());
+    out->models = s->models.data();
+    out->n_models = static_cast<int>(s->models.size());
+    out->batch_menu = s->cluster.batch_menu.data();
+    out->menu_size = static_cast<int>(s->cluster.batch_menu.size());
+    out->segment_size = s->cluster.segment_size;
+    return ES_OK;
+  });
+}
+
+void es_spec_destroy(es_spec* s) { delete s; }
+
+es_status es_save_json_file(const char* path, const char* json_text) {
+  return guard([&] {
+    need(path != nullptr, "path is NULL");
+    save_json_file(path, parse_text(json_text, "text is NULL"));
+    return ES_OK;
+  });
+}
+
+es_status es_matrix_to_json(const es_cluster_desc* c, const int* A, int indent, char* buf,
+                            size_t len, size_t* needed) {
+  return guard([&] {
+    const ClusterSpec s = to_cluster(c);
+    return put_text(js::dump(matrix_to_json(to_matrix(A, c->n_devices, c->n_models), s), indent),
+                    buf, len, needed);
+  });
+}
+
+es_status es_matrix_from_json(const es_cluster_desc* c, const char* json_text, int* A_out) {
+  return guard([&] {
+    need(A_out != nullptr, "A_out is NULL");
+    write_matrix(matrix_from_json(parse_text(json_text, "text is NULL"), to_cluster(c)), A_out);
+    return ES_OK;
+  });
+}
+
+es_status es_digest_hex(const char* text, char out[17]) {
+  return guard([&] {
+    need(text != nullptr && out != nullptr, "NULL argument");
+    std::memcpy(out, digest_hex(text).c_str(), 17);
+    return ES_OK;
+  });
+}
+
+es_status es_cache_key(const es_cluster_desc* c, int max_iter, int max_neighs, uint64_t rng_seed,
+                       int default_batch, const char* bench_mode, size_t calib_samples,
+                       int repeats, char out[17]) {
+  return guard([&] {
+    need(out != nullptr, "out is NULL");
+    const std::string k = cache_key(to_cluster(c), opt_key(max_iter, max_neighs, rng_seed,
+                                                           default_batch, bench_mode,
+                                                           calib_samples, repeats));
+    std::memcpy(out, k.c_str(), 17);
+    return ES_OK;
+  });
+}
+
+es_status es_cache_lookup(const char* directory, const char* key, const es_cluster_desc* c,
+                          int* A_out, double* score, int64_t* created_at, int* hit) {
+  return guard([&] {
+    need(directory != nullptr && key != nullptr && hit != nullptr, "NULL argument");
+    MatrixCache cache(directory);
+    auto e = cache.lookup(key, to_cluster(c));
+    *hit = e ? 1 : 0;
+    if (e) {
+      if (A_out) write_matrix(e->matrix, A_out);
+      if (score) *score = e->score;
+      if (created_at) *created_at = e->created_at;
+    }
+    return ES_OK;
+  });
+}
+
+es_status es_cache_store(const char* directory, const char* key, const es_cluster_desc* c,
+                         const int* A, double score, int64_t created_at) {
+  return guard([&] {
+    need(directory != nullptr && key != nullptr, "NULL argument");
+    MatrixCache cache(directory);
+    MatrixCacheEntry e;
+    e.key = key;
+    e.matrix = to_matrix(A, c->n_devices, c->n_models);
+    e.score = score;
+    e.created_at = created_at;
+    cache.store(e, to_cluster(c));
     return ES_OK;
   });
 }

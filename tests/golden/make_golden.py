@@ -11,6 +11,11 @@ that has /root/reference):  python tests/golden/make_golden.py
                              greedy trajectories of seeded random clusters
                              (tests/test_fixtures.hpp:67-94 instances), from the
                              reference library.
+  spec_io.json               spec / matrix documents, cache keys, digests and
+                             spec error messages printed by the reference's own
+                             spec_io.cpp + cache.cpp (oracle/spec_golden.cpp,
+                             built by `make -C oracle spec_golden` against the
+                             nlohmann::json 3.11.3 header of this image).
 """
 from __future__ import annotations
 
@@ -75,10 +80,21 @@ def placement_cases():
     return out
 
 
+def spec_io_cases():
+    import subprocess
+    root = HERE.parent.parent
+    subprocess.run(["make", "-C", str(root / "oracle"), "spec_golden"], check=True,
+                   capture_output=True)
+    out = subprocess.run([str(root / "oracle" / "_ref" / "spec_golden")], check=True,
+                         capture_output=True, text=True).stdout
+    return json.loads(out)
+
+
 def main():
     (HERE / "synthetic_prediction.json").write_text(json.dumps({"cases": synthetic_cases()}))
     (HERE / "weights.json").write_text(json.dumps({"cases": weight_cases()}))
     (HERE / "placement.json").write_text(json.dumps({"cases": placement_cases()}, indent=0))
+    (HERE / "spec_io.json").write_text(json.dumps(spec_io_cases(), indent=1) + "\n")
     print("golden fixtures written")
 
 
