@@ -308,6 +308,15 @@ es_status es_cache_lookup(const char* directory, const char* key, const es_clust
 es_status es_cache_store(const char* directory, const char* key, const es_cluster_desc* c,
                          const int* A, double score, int64_t created_at);
 
+/* ------------------------------------------------------------ operator commands */
+/* tools/enserve_cli.cpp main() + src/cli/commands.cpp:
+ * optimize | bench --matrix F | count | baseline over --cluster/--ensemble
+ * spec files, with --cache-dir, --bench-mode measured|analytic and the b200
+ * backend (measured = device-timed bench on this box's GPUs).  argv[0] is the
+ * program name.  Report on stdout, errors on stderr; returns the exit code
+ * (0 ok, 1 error, 2 allocation error). */
+int es_cli_main(int argc, const char* const* argv);
+
 #ifdef __cplusplus
 }
 #endif

@@ -11,6 +11,7 @@
 #include <string>
 #include <vector>
 
+#include "enserve/cli/commands.hpp"
 #include "enserve/core/spec_io.hpp"
 #include "enserve/opt/optimizer.hpp"
 #include "enserve/server/cache.hpp"
@@ -109,6 +110,25 @@ int main() {
                         {"calib_samples", 1024}, {"repeats", 3}, {"key", cache_key(c, k)}});
       }
     e["cache_keys"] = keys;
+    // The CLI commands in analytic mode (src/cli/commands.cpp), wall time dropped.
+    json cmds = json::object();
+    for (int seed : {0, 31337}) {
+      CommandOptions o;
+      o.bench_mode = "analytic";
+      o.seed = static_cast<std::uint64_t>(seed);
+      auto strip = [](json r) {
+        r.erase("wall_time_s");
+        return r;
+      };
+      const std::string sfx = "_seed" + std::to_string(seed);
+      cmds["optimize" + sfx] = strip(cmd_optimize(c, o));
+      cmds["baseline" + sfx] = strip(cmd_baseline(c, o));
+      if (seed == 0) {
+        cmds["count"] = strip(cmd_count(c, o));
+        cmds["bench_wfd"] = strip(cmd_bench(c, A, o));
+      }
+    }
+    e["commands"] = cmds;
     // Round trip through the reference parser.
     e["roundtrip_compact"] = cluster_to_json(cluster_from_json(json::parse(spec.dump()))).dump();
     out["clusters"][name] = e;

@@ -75,6 +75,7 @@ class GreedyTrace(C.Structure):
 
 # name -> (restype, argtypes)
 _SIGS = {
+    "es_cli_main": (C.c_int, [C.c_int, C.POINTER(C.c_char_p)]),
     "es_cluster_to_json": (C.c_int, [C.POINTER(ClusterDesc), C.c_int, C.c_int, C.c_char_p,
                                      C.c_size_t, c_size_t_p]),
     "es_spec_from_json": (C.c_int, [C.c_char_p, C.c_char_p, C.POINTER(C.c_void_p)]),

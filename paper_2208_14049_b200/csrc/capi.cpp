@@ -13,6 +13,7 @@
 
 #include "enserve/host_convert.hpp"
 #include "enserve/spec_io.hpp"
+#include "enserve/commands.hpp"
 #include "enserve/placement.hpp"
 #include "enserve/rng.hpp"
 #include "enserve/runtime.hpp"
@@ -859,6 +860,18 @@ es_status es_cache_store(const char* directory, const char* key, const es_cluste
     cache.store(e, to_cluster(c));
     return ES_OK;
   });
+}
+
+
+// ------------------------------------------------------------ operator commands
+int es_cli_main(int argc, const char* const* argv) {
+  try {
+    std::vector<std::string> args;
+    for (int i = 1; i < argc; ++i) args.emplace_back(argv[i] ? argv[i] : "");
+    return cli_main(args);
+  } catch (...) {
+    return 1;
+  }
 }
 
 }  // extern "C"
