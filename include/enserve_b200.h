@@ -308,6 +308,22 @@ es_status es_cache_lookup(const char* directory, const char* key, const es_clust
 es_status es_cache_store(const char* directory, const char* key, const es_cluster_desc* c,
                          const int* A, double score, int64_t created_at);
 
+/* ------------------------------------------------ B200-calibrated cost model */
+/* the reference's analytic bench (src/cost/cost_model.cpp:
+ * 13-46) with its inputs fitted to this box.  With compute_rate R = 1,
+ * 1/throughput(m, b) = c_m + o/b is fitted by least squares in relative error
+ * (cost_out[n_models] = c_m in seconds per sample, *overhead_out = o >= 0,
+ * *rms_out = relative RMS misfit). */
+es_status es_fit_cost_model(const int* model, const int* batch, const double* throughput, int n,
+                            int n_models, double* cost_out, double* overhead_out, double* rms_out);
+/* Benches every model of c alone on CUDA device `device` at every menu batch
+ * (device-timed bench over calib_nb synthetic samples, median of repeats)
+ * and fits; measured_out[n_models * menu_size] (may be NULL) receives the
+ * throughputs, model-major. */
+es_status es_calibrate_cost_model(const es_cluster_desc* c, int device, size_t calib_nb,
+                                  int repeats, double* cost_out, double* overhead_out,
+                                  double* rms_out, double* measured_out);
+
 /* ------------------------------------------------------------ operator commands */
 /* tools/enserve_cli.cpp main() + src/cli/commands.cpp:
  * optimize | bench --matrix F | count | baseline over --cluster/--ensemble

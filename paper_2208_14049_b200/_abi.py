@@ -75,6 +75,10 @@ class GreedyTrace(C.Structure):
 
 # name -> (restype, argtypes)
 _SIGS = {
+    "es_fit_cost_model": (C.c_int, [c_int_p, c_int_p, c_double_p, C.c_int, C.c_int, c_double_p,
+                                    c_double_p, c_double_p]),
+    "es_calibrate_cost_model": (C.c_int, [C.POINTER(ClusterDesc), C.c_int, C.c_size_t, C.c_int,
+                                          c_double_p, c_double_p, c_double_p, c_double_p]),
     "es_cli_main": (C.c_int, [C.c_int, C.POINTER(C.c_char_p)]),
     "es_cluster_to_json": (C.c_int, [C.POINTER(ClusterDesc), C.c_int, C.c_int, C.c_char_p,
                                      C.c_size_t, c_size_t_p]),

@@ -980,3 +980,52 @@ class MatrixCache:
         with _Desc(cluster) as d:
             _check(lib().es_cache_store(self.directory.encode(), entry.key.encode(), d.ptr,
                                         entry.matrix.ptr(), entry.score, entry.created_at))
+
+
+# ------------------------------------------------------------------ calibrated cost model (§8-F F4)
+@dataclass
+class CostFit:
+    """Fitted inputs of the analytic cost model (compute_rate = 1)."""
+    cost_per_sample: list
+    batch_overhead_s: float
+    rms_rel_error: float
+    measured: Optional[list] = None  # [(model, batch, samples/s)] when benched here
+
+
+def fit_cost_model(samples: Sequence[tuple], n_models: int) -> CostFit:
+    """samples: (model, batch, throughput) triples -> least-squares fit of
+    1/throughput = c_m + o/b (calibrate.hpp)."""
+    n = len(samples)
+    mi = (C.c_int * max(n, 1))(*[int(s[0]) for s in samples])
+    bi = (C.c_int * max(n, 1))(*[int(s[1]) for s in samples])
+    th = (C.c_double * max(n, 1))(*[float(s[2]) for s in samples])
+    cost = (C.c_double * n_models)()
+    o, rms = C.c_double(), C.c_double()
+    _check(lib().es_fit_cost_model(mi, bi, th, n, n_models, cost, C.byref(o), C.byref(rms)))
+    return CostFit(list(cost), o.value, rms.value)
+
+
+def calibrate_cost_model(cluster: ClusterSpec, device: int = 0, calib_nb: int = 65536,
+                         repeats: int = 3) -> CostFit:
+    """Bench every member alone on `device` at every menu batch, then fit."""
+    M, B = cluster.model_count(), len(cluster.batch_menu)
+    cost = (C.c_double * M)()
+    meas = (C.c_double * (M * B))()
+    o, rms = C.c_double(), C.c_double()
+    with _Desc(cluster) as d:
+        _check(lib().es_calibrate_cost_model(d.ptr, device, calib_nb, repeats, cost, C.byref(o),
+                                             C.byref(rms), meas))
+    samples = [(m, cluster.batch_menu[j], meas[m * B + j]) for m in range(M) for j in range(B)]
+    return CostFit(list(cost), o.value, rms.value, samples)
+
+
+def apply_cost_fit(cluster: ClusterSpec, fit: CostFit) -> ClusterSpec:
+    """GPU rows: compute_rate 1, the fitted overhead; models: fitted costs."""
+    import copy
+    out = copy.deepcopy(cluster)
+    for d in out.devices:
+        if d.kind == GPU:
+            d.compute_rate, d.batch_overhead_s = 1.0, fit.batch_overhead_s
+    for m, c in zip(out.models, fit.cost_per_sample):
+        m.cost_per_sample = c
+    return out

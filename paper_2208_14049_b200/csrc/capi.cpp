@@ -14,6 +14,7 @@
 #include "enserve/host_convert.hpp"
 #include "enserve/spec_io.hpp"
 #include "enserve/commands.hpp"
+#include "enserve/calibrate.hpp"
 #include "enserve/placement.hpp"
 #include "enserve/rng.hpp"
 #include "enserve/runtime.hpp"
@@ -872,6 +873,39 @@ int es_cli_main(int argc, const char* const* argv) {
   } catch (...) {
     return 1;
   }
+}
+
+
+// ------------------------------------------------------------ calibrated cost model
+es_status es_fit_cost_model(const int* model, const int* batch, const double* throughput, int n,
+                            int n_models, double* cost_out, double* overhead_out, double* rms_out) {
+  return guard([&] {
+    need(n >= 0 && n_models > 0 && cost_out != nullptr, "bad arguments");
+    std::vector<CostSample> s;
+    for (int i = 0; i < n; ++i) s.push_back({model[i], batch[i], throughput[i]});
+    const CostFit f = fit_cost_model(s, n_models);
+    for (int m = 0; m < n_models; ++m) cost_out[m] = f.cost_per_sample[m];
+    if (overhead_out) *overhead_out = f.batch_overhead_s;
+    if (rms_out) *rms_out = f.rms_rel_error;
+    return ES_OK;
+  });
+}
+
+es_status es_calibrate_cost_model(const es_cluster_desc* c, int device, size_t calib_nb,
+                                  int repeats, double* cost_out, double* overhead_out,
+                                  double* rms_out, double* measured_out) {
+  return guard([&] {
+    need(cost_out != nullptr, "cost_out is NULL");
+    const ClusterSpec s = to_cluster(c);
+    std::vector<CostSample> meas;
+    const CostFit f = calibrate_cost_model(s, device, calib_nb, repeats, &meas);
+    for (int m = 0; m < s.model_count(); ++m) cost_out[m] = f.cost_per_sample[m];
+    if (overhead_out) *overhead_out = f.batch_overhead_s;
+    if (rms_out) *rms_out = f.rms_rel_error;
+    if (measured_out)
+      for (std::size_t i = 0; i < meas.size(); ++i) measured_out[i] = meas[i].throughput;
+    return ES_OK;
+  });
 }
 
 }  // extern "C"

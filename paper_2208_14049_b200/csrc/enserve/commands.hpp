@@ -40,6 +40,12 @@ js::Value cmd_count(const ClusterSpec& cluster, const CommandOptions& options); 
 js::Value cmd_baseline(const ClusterSpec& cluster, const CommandOptions& options); // :208-242
 std::string render_report(const js::Value& report);                                // :262-280
 
+// F4: fit the analytic cost model to this box (calibrate.hpp) and report the
+// fit, the measured throughputs and the analytic prediction of each; with
+// out_path, save the calibrated spec (member architectures included).
+js::Value cmd_calibrate(const ClusterSpec& cluster, const CommandOptions& options,
+                        const std::string& out_path);
+
 // tools/enserve_cli.cpp main(): returns the process exit code (0 ok, 1 error,
 // 2 allocation error) and writes the report to stdout, errors to stderr.
 int cli_main(const std::vector<std::string>& args);
