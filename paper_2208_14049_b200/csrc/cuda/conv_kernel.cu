@@ -26,11 +26,6 @@ template <bool SPLIT>
 constexpr int threads_for() { return SPLIT ? 448 : kThreads; }
 constexpr uint32_t kSmemBudget = 232448;
 constexpr int kMargin = 16;  // zero rows before/after the tile's grids; taps reach R+1 rows
-constexpr int kXchStride = 20;  // fp32 per exchanged row (16 + 4: conflict-free 16-byte stores)
-
-__device__ __forceinline__ void epi2_bar(int group) {  // four conv2-epilogue warps
-  asm volatile("bar.sync %0, 128;" ::"r"(1 + group) : "memory");
-}
 
 // bf16x2 {relu(a + ba), relu(b + bb)} (a in the low half), one cvt.relu.
 __device__ __forceinline__ uint32_t pack_relu_bf16(uint32_t a, uint32_t b, float ba, float bb) {
@@ -78,7 +73,8 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
   uint64_t* a2_empty = a2_full + 2;
   uint64_t* c2_full = a2_empty + 2;
   uint64_t* c2_empty = c2_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(c2_empty + 2);
+  uint64_t* mma_done = c2_empty + 2;  // split: a block's UMMAs completed (shifts may go)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mma_done + 2);
 
   const int warp = warp_uniform_id();
   const int lane = threadIdx.x & 31;
@@ -101,6 +97,8 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
       mbar_init(&c2_full[b], 1);
       mbar_init(&c2_empty[b], SPLIT ? 8 : 4);
     }
+    mbar_init(&mma_done[0], 1);
+    mbar_init(&mma_done[1], 1);
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) tma_prefetch(&tm_x);
@@ -119,9 +117,9 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
     for (int i = threadIdx.x; i < 9 * kp * L.c2; i += threads_for<SPLIT>()) {
       const int o = i / (9 * kp), rem = i % (9 * kp);  // rem = tap * kp + plane
       if (SPLIT) {
-        // [dw][plane][g*c2 + o]: B of UMMA (dw, K step) holds the three dh taps.
-        const int tap = rem / kp, plane = rem % kp, g = tap / 3, dwi = tap % 3;
-        *reinterpret_cast<uint4*>(sW2 + ((dwi * kp + plane) * L.n2 + g * L.c2 + o) * 16) = w2[i];
+        // [dh][plane][dw*c2 + o]: B of UMMA (dh, K step) holds the three dw taps.
+        const int tap = rem / kp, plane = rem % kp, dhi = tap / 3, dwi = tap % 3;
+        *reinterpret_cast<uint4*>(sW2 + ((dhi * kp + plane) * L.n2 + dwi * L.c2 + o) * 16) = w2[i];
       } else {
         *reinterpret_cast<uint4*>(sW2 + (rem * L.c2 + o) * 16) = w2[i];
       }
@@ -132,9 +130,6 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
     }
     for (int i = threadIdx.x; i < L.c1; i += threads_for<SPLIT>()) sB1[i] = args.b1[i];
     for (int i = threadIdx.x; i < L.c2; i += threads_for<SPLIT>()) sB2[i] = args.b2[i];
-    if (SPLIT)
-      for (int i = threadIdx.x; i < kXchStride; i += threads_for<SPLIT>())
-        reinterpret_cast<float*>(smem + L.off_xch)[2 * 2 * 4 * 2 * L.R * kXchStride + i] = 0.0f;
     uint4* z = reinterpret_cast<uint4*>(sA2);
     for (int i = threadIdx.x; i < static_cast<int>(2 * L.a2_bytes / 16); i += threads_for<SPLIT>())
       z[i] = make_uint4(0, 0, 0, 0);
@@ -224,6 +219,29 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
       }
       __syncwarp();
     };
+    // tcgen05.shift is not ordered behind in-flight UMMAs on the same columns
+    // (measured: shifting right after the UMMAs reads partial sums), so a
+    // block's shifts wait for its UMMAs' commit.
+    int pend_sl = -1;
+    uint32_t done_par = 0;  // bit s: parity of mma_done[s]
+    auto flush_shifts = [&]() {
+      if (pend_sl < 0) return;
+      const int sl = pend_sl;
+      mbar_wait(&mma_done[sl], (done_par >> sl) & 1u);
+      done_par ^= 1u << sl;
+      tc_fence_after();
+      const uint32_t d = tbase + static_cast<uint32_t>(2 * L.tmem_c1 + sl * L.n2);
+      // out[q] = D'[q][dw=-1] + D'[q+1][dw=0] + D'[q+2][dw=+1]: pull the dw=0
+      // columns one lane, the dw=+1 columns two lanes toward lane 0.
+      for (int c = 0; c < L.c2; c += 8) {
+        if (elect_one()) tmem_shift_down(d + static_cast<uint32_t>(L.c2 + c));
+        if (elect_one()) tmem_shift_down(d + static_cast<uint32_t>(2 * L.c2 + c));
+        if (elect_one()) tmem_shift_down(d + static_cast<uint32_t>(2 * L.c2 + c));
+      }
+      if (elect_one()) umma_commit(&c2_full[sl]);
+      __syncwarp();
+      pend_sl = -1;
+    };
     auto conv2_split = [&](int k) {
       // One accumulator slot per 128-row block, alternating over the running
       // block count: the epilogue of block i overlaps the UMMAs of block i+1.
@@ -238,19 +256,27 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
         tc_fence_after();
         const uint32_t d = tbase + static_cast<uint32_t>(2 * L.tmem_c1 + sl * L.n2);
         const uint64_t adm = ad0 + static_cast<uint64_t>(kMargin + mb * 128);
+        // D'[p][dw] = sum_dh X[p - 1 + dh*R] W(dh, dw): A shifted by dh*R - 1.
 #pragma unroll
-        for (int dwi = 0; dwi < 3; ++dwi)
+        for (int dhi = 0; dhi < 3; ++dhi)
 #pragma unroll
           for (int j = 0; j < KP2; ++j) {
-            const uint64_t ad = adm + static_cast<uint64_t>(dwi - 1 + j * static_cast<int>(a2_step));
-            const uint64_t bd = w2d + static_cast<uint64_t>((dwi * KP2 + j) * 2 * L.n2);
-            if (elect_one()) umma_bf16(d, ad, bd, id2, (dwi | j) != 0);
+            const uint64_t ad =
+                adm + static_cast<uint64_t>((dhi - 1) * L.R - 1 + j * static_cast<int>(a2_step));
+            const uint64_t bd = w2d + static_cast<uint64_t>((dhi * KP2 + j) * 2 * L.n2);
+            if (elect_one()) umma_bf16(d, ad, bd, id2, (dhi | j) != 0);
           }
         if (elect_one()) {
+          umma_commit(&mma_done[sl]);
           if (mb == L.mb2 - 1) umma_commit(&a2_empty[b]);
-          umma_commit(&c2_full[sl]);
         }
         __syncwarp();
+        // Shifting right behind the block's own UMMAs (drains the pipe for
+        // one UMMA latency) measured faster than deferring the shifts behind
+        // the next block's UMMAs, which leaves the 2-slot accumulator ring
+        // too shallow (tools/trace_conv.cu: 2.13 vs 2.55 us per tile).
+        pend_sl = sl;
+        flush_shifts();
       }
       TRACE(k, 3);
     };
@@ -295,6 +321,7 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
       if (k > 0) conv2(k - 1);
     }
     if (my_tiles > 0) conv2(my_tiles - 1);
+    if (SPLIT) flush_shifts();
   } else if (warp < 6) {
     // ------------------------------------------------------- conv1 epilogue
     const int ta = threadIdx.x - 64;  // 0..127
@@ -312,7 +339,7 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
       for (int mb = 0; mb < L.mb1; ++mb) {
         const int r = mb * 128 + q * 32 + lane;
         const int n = r / G2, p = r % G2, i = p / L.G, j = p % L.G;
-        const int grow = kMargin + n * P2 + (i + 1) * L.R + (j + 1);
+        const int grow = kMargin + n * P2 + (i + 1) * L.R + j;  // column G is the border
         for (int c0 = 0; c0 < L.c1; c0 += 32) {
           uint32_t v[32];
           if (args.debug & 1) {
@@ -349,30 +376,27 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
     const int q = warp & 3;
     const uint32_t lane_field = static_cast<uint32_t>(q * 32) << 16;
     const int row_bytes = G2 * L.c2 * 2;
-    // split: out[q] = D[q-R][g0] + D[q][g1] + D[q+R][g2] (conv_kernel.cuh).
-    // Eight warps: group eg = 0 (warps 6-9) takes channels
-    // [0, c2/2), group 1 (warps 10-13) [c2/2, c2), 16 at a time.
+    // split: the tensor pipe already moved the dw = 0 / +1 partials onto the
+    // output's lane (conv_kernel.cuh), so out = g(-1) + g(0) + g(+1) per lane.
+    // Lane 30 of a quadrant needs lane 32's dw=+1 partial, which the in-quadrant
+    // shift cannot fetch: that partial is zero (it reads the border column).
+    // Eight warps: group eg = 0 (warps 6-9) takes channels [0, c2/2), group 1
+    // (warps 10-13) [c2/2, c2), 16 at a time.
     const int eg = (warp - 6) >> 2;
-    float* xch = reinterpret_cast<float*>(smem + L.off_xch);
-    int xi = 0;  // running exchange count: xch buffer = xi & 1
     auto epi2_split = [&](int k) {
       const long long s0 = args.row_begin + (blockIdx.x + static_cast<long long>(k) * gridDim.x) * L.T;
-      const int R = L.R;
-      const int xrow = 2 * R * kXchStride;  // one quadrant's [2][R][kXchStride]
-      const int zrow = 2 * 2 * 4 * xrow;    // the zero row after both buffers
+      const float keep_p1 = lane == 30 ? 0.0f : 1.0f;
       for (int mb = 0; mb < L.mb2; ++mb) {
         const int blk = k * L.mb2 + mb, sl = blk & 1;
         mbar_sleep_wait(&c2_full[sl], static_cast<uint32_t>(blk >> 1) & 1u);
         if (warp == 6 && lane == 0 && mb == 0) TRACE(k, 8);
-        if (warp == 6 && lane == 0) TRACE(k, 10 + 3 * mb);
         tc_fence_after();
         const int r = mb * 128 + q * 32 + lane;  // grid row of the tile
-        const int n = r / P2, rr = r % P2, h = rr / R, w = rr % R;
-        const bool valid = r < L.T * P2 && h >= 1 && w >= 1 && s0 + n < args.row_end;
+        const int n = r / P2, rr = r % P2, h = rr / L.R, w = rr % L.R;
+        const bool valid = r < L.T * P2 && h >= 1 && w < L.G && s0 + n < args.row_end;
         uint8_t* dst = static_cast<uint8_t*>(args.out) + (s0 + n) * row_bytes +
-                       ((h - 1) * L.G + (w - 1)) * L.c2 * 2;
+                       ((h - 1) * L.G + w) * L.c2 * 2;
         const uint32_t col = tmem_base + lane_field + static_cast<uint32_t>(2 * L.tmem_c1 + sl * L.n2);
-        const bool take_up = lane < R, take_dn = lane >= 32 - R;
         for (int c0 = eg * (L.c2 >> 1); c0 < (eg + 1) * (L.c2 >> 1); c0 += 16) {
           uint32_t r0[16], r1[16], r2[16];
           if (args.debug & 4) {
@@ -384,59 +408,10 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
             tmem_ld16_raw(col + static_cast<uint32_t>(2 * L.c2 + c0), r2);
             tmem_ld_wait();
           }
-          float g0[16], g1[16], g2[16];
-#pragma unroll
-          for (int c = 0; c < 16; ++c) {
-            g0[c] = __uint_as_float(r0[c]);
-            g1[c] = __uint_as_float(r1[c]);
-            g2[c] = __uint_as_float(r2[c]);
-          }
-          // Rows crossing a lane-quadrant boundary: the last R lanes publish
-          // their g0 partials (read by the next quadrant's first R lanes),
-          // the first R lanes their g2 partials (read by the previous one's
-          // last R lanes).
-          const int xbuf = ((xi & 1) * 2 + eg) * 4 * xrow;
-          ++xi;
-          const bool xon = !(args.debug & 8);
-          if (take_dn && xon) {
-            float* d0 = xch + xbuf + q * xrow + (lane - (32 - R)) * kXchStride;
-#pragma unroll
-            for (int c = 0; c < 16; c += 4)
-              *reinterpret_cast<float4*>(d0 + c) = make_float4(g0[c], g0[c + 1], g0[c + 2], g0[c + 3]);
-          }
-          if (take_up && xon) {
-            float* d2 = xch + xbuf + q * xrow + (R + lane) * kXchStride;
-#pragma unroll
-            for (int c = 0; c < 16; c += 4)
-              *reinterpret_cast<float4*>(d2 + c) = make_float4(g2[c], g2[c + 1], g2[c + 2], g2[c + 3]);
-          }
-          if (xon) epi2_bar(eg);
-          if (warp == 6 && lane == 0) TRACE(k, 11 + 3 * mb);
-          // Branch-free: lanes that take their partner from a shuffle read the
-          // zero row (one broadcast address) instead of an exchanged row.
-          const float* up_src =
-              xch + ((take_up && q > 0) ? xbuf + (q - 1) * xrow + lane * kXchStride : zrow);
-          const float* dn_src =
-              xch + ((take_dn && q < 3) ? xbuf + (q + 1) * xrow + (R + lane - (32 - R)) * kXchStride
-                                        : zrow);
           float v[16];
-          if (!xon) {
 #pragma unroll
-            for (int c = 0; c < 16; ++c) v[c] = g0[c] + g1[c] + g2[c];
-          } else
-#pragma unroll
-          for (int c = 0; c < 16; c += 4) {
-            const float4 u4 = *reinterpret_cast<const float4*>(up_src + c);
-            const float4 d4 = *reinterpret_cast<const float4*>(dn_src + c);
-            const float ux[4] = {u4.x, u4.y, u4.z, u4.w}, dx[4] = {d4.x, d4.y, d4.z, d4.w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float up = __shfl_up_sync(0xffffffffu, g0[c + e], R);
-              const float dn = __shfl_down_sync(0xffffffffu, g2[c + e], R);
-              v[c + e] = g1[c + e] + (take_up ? ux[e] : up) + (take_dn ? dx[e] : dn);
-            }
-          }
-          if (warp == 6 && lane == 0) TRACE(k, 12 + 3 * mb);
+          for (int c = 0; c < 16; ++c)
+            v[c] = __uint_as_float(r0[c]) + __uint_as_float(r1[c]) + keep_p1 * __uint_as_float(r2[c]);
           if (valid && !(args.debug & 16)) {
 #pragma unroll
             for (int g = 0; g < 2; ++g) {
@@ -472,9 +447,9 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
       for (int mb = 0; mb < L.mb2; ++mb) {
         const int r = mb * 128 + q * 32 + lane;  // grid row of the tile
         const int n = r / P2, rr = r % P2, h = rr / L.R, w = rr % L.R;
-        const bool valid = r < L.T * P2 && h >= 1 && w >= 1 && s0 + n < args.row_end;
+        const bool valid = r < L.T * P2 && h >= 1 && w < L.G && s0 + n < args.row_end;
         uint8_t* dst = static_cast<uint8_t*>(args.out) + (s0 + n) * row_bytes +
-                       ((h - 1) * L.G + (w - 1)) * L.c2 * 2;
+                       ((h - 1) * L.G + w) * L.c2 * 2;
         for (int c0 = 0; c0 < L.c2; c0 += 32) {
           uint32_t v[32];
           tmem_ld32_raw(tmem_base + lane_field +
@@ -531,12 +506,16 @@ bool conv_plan(int S, int P, int c1, int c2, ConvLayout* out, int schedule) {
   L.R = L.G + 1;
   if (L.R + 1 > kMargin) return false;
   const int P2 = L.R * L.R, G2 = L.G * L.G;
-  const bool split_ok = 3 * c2 <= 256 && 128 % P2 == 0 && 32 % L.R == 0;
+  // split: N = 3*c2 per UMMA; 128-row blocks and 32-lane quadrants must start
+  // on grid-row boundaries (R | 32) so every quadrant's last lane is a border
+  // column (the in-quadrant lane shift never needs the next quadrant).
+  const bool split_ok = 3 * c2 <= 256 && 32 % L.R == 0;
   if (schedule == 2 && !split_ok) return false;
-  // Measured on B200 (tools/trace_conv.cu, 2^20 CNN-s samples): tap 3.80 ms,
-  // split 4.19 ms -- split issues 2.1x fewer UMMA operand bytes but its
-  // lane-shift epilogue (shuffles + boundary exchange) costs more MIO
-  // bandwidth than it saves, so split is opt-in (ES_CONV_SCHEDULE=split).
+  // Measured on B200 (tools/trace_conv.cu, 2^20 CNN-s samples): tap 3.84 ms,
+  // split 3.9 ms -- split issues 2.6x fewer UMMA clk, but its N = 96 UMMAs
+  // run at ~70-100 clk inside the kernel (57 alone, tools/umma_rate.cu) and
+  // the UMMA -> shift -> epilogue chain leaves the 2-slot ring shallow, so
+  // split is opt-in (ES_CONV_SCHEDULE=split).
   L.split = split_ok && schedule == 2;
   L.n2 = L.split ? 3 * c2 : c2;
   for (int T = std::max(1, 256 / P2); T >= 1; --T) {
@@ -569,10 +548,8 @@ bool conv_plan(int S, int P, int c1, int c2, ConvLayout* out, int schedule) {
     L.off_b2 = align_up(L.off_b1 + static_cast<uint32_t>(c1 * 4), 16);
     L.off_rows = align_up(L.off_b2 + static_cast<uint32_t>(c2 * 4), 16);
     L.off_xch = align_up(L.off_rows + static_cast<uint32_t>(T * G2 * 4), 16);
-    const uint32_t xch =
-        L.split ? static_cast<uint32_t>((2 * 2 * 4 * 2 * L.R + 1) * kXchStride * 4) : 0u;  // + zero row
-    L.off_bar = align_up(L.off_xch + xch, 8);
-    const uint32_t bars = static_cast<uint32_t>(2 * L.raw_stages + 16) * 8u + 16u;
+    L.off_bar = align_up(L.off_xch, 8);
+    const uint32_t bars = static_cast<uint32_t>(2 * L.raw_stages + 18) * 8u + 16u;
     L.smem_bytes = L.off_bar + bars + 1024u;  // + alignment slack of the dynamic base
     if (L.smem_bytes > kSmemBudget) continue;
     *out = L;

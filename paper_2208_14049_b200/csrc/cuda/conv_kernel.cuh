@@ -7,16 +7,17 @@
 // Both convolutions are implicit GEMMs on tcgen05 inside ONE persistent kernel;
 // the c1-channel intermediate never leaves shared memory:
 //   * a tile is T whole samples, so no halo crosses tiles;
-//   * conv1: TMA brings the raw images; builder warps write the im2col rows
-//     (one row per output pixel, K = P*P) into a K-major planar operand; one
-//     UMMA (M=128, N=c1, K=16) per 128 rows;
+//   * conv1: TMA brings the raw images; the TMA warp also writes the im2col
+//     rows (one row per output pixel, K = P*P) into a K-major planar operand;
+//     one UMMA (M=128, N=c1, K=16) per 128 rows;
 //   * conv1's epilogue writes relu(acc+b) as bf16 into a zero-bordered grid,
 //     again K-major planar (channels = K).  Grid rows have stride R = G+1 and
-//     samples stride R*R: pixel (h, w), 1 <= h, w <= G, sits at row
-//     s*R*R + h*R + w, and row 0 / column 0 of each sample are zero -- the
-//     right neighbour of column G is the next row's column 0 and the bottom
-//     neighbour of row G is the next sample's row 0, so ONE shared border
-//     serves both sides (49 of 64 rows useful at G = 7, 2 samples per M block);
+//     samples stride R*R: pixel (h, w), 1 <= h <= G, 0 <= w < G, sits at row
+//     s*R*R + h*R + w, and row 0 / column G of each sample are zero -- the
+//     left neighbour of column 0 is the previous row's column G and the
+//     bottom neighbour of row G is the next sample's row 0, so ONE shared
+//     border serves both sides (49 of 64 rows useful at G = 7, 2 samples per
+//     M block);
 //   * conv2: output pixel q at tap (dh, dw) reads grid row q + dh*R + dw, so
 //     each of the 9 taps is the SAME operand with the descriptor start moved
 //     by whole rows (16 B each) -- nine accumulating UMMAs per K step, no
@@ -28,18 +29,19 @@
 // whatever its operands (tools/umma_rate.cu, measured on B200), so c2 = 32
 // output channels as N runs the tensor core at 16/46 of its rate:
 //   * "tap" (any shape): 9 taps x c1/16 K steps of N = c2 per 128-row block;
-//   * "split" (3*c2 <= 256, grid blocks aligned to 128 rows): the three
-//     vertical taps dh = -1, 0, +1 of one horizontal offset dw go into ONE
-//     UMMA as N = 3*c2 columns (B rows g*c2 + o = tap (g-1, dw), output o),
-//     with A shifted by dw only: 3 x c1/16 UMMAs of N = 96 per block instead
-//     of 36 of N = 32.  Column group g of accumulator row p then holds the
-//     dh = g-1 partial evaluated at row p, and the output is
-//         out[q] = D[q - R][g=0] + D[q][g=1] + D[q + R][g=2],
-//     a +-R lane shift done with warp shuffles (R | 32), plus an R-row
-//     exchange through shared memory between neighbouring TMEM lane
-//     quadrants.  Rows outside the 128-row block are zero-border rows (whole
-//     samples per block, R*R | 128), so no block needs another's partials.
-//     Measured slower than tap on B200 (see conv_plan): opt-in.
+//   * "split" (3*c2 <= 256, R | 32): the three HORIZONTAL taps dw = -1, 0, +1
+//     of one vertical offset dh go into ONE UMMA as N = 3*c2 columns (B rows
+//     dw*c2 + o), with A shifted by dh*R - 1 only: 3 x c1/16 UMMAs of N = 96
+//     per block instead of 36 of N = 32.  Column group dw of accumulator row
+//     p then holds D'[p][dw] = sum_dh X[p - 1 + dh*R] W(dh, dw), and
+//         out[q] = D'[q][-1] + D'[q+1][0] + D'[q+2][+1],
+//     a lane shift the tensor pipe does itself: tcgen05.shift moves the dw=0
+//     columns one lane and the dw=+1 columns two lanes toward lane 0 (within
+//     each 32-lane quadrant).  With the grid's border column LAST in a row
+//     (w = G), a quadrant's lane 31 is a border pixel and lane 30's missing
+//     dw=+1 partial (lane 32's) reads only the border column, i.e. is zero --
+//     so the epilogue is a lane-local sum.  Correct and measured; opt-in
+//     (conv_plan).
 #pragma once
 
 #include <cuda_runtime.h>

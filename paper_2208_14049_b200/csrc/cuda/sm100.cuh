@@ -309,6 +309,14 @@ __device__ __forceinline__ void umma_bf16_ta(uint32_t d_tmem, uint32_t a_tmem, u
       : "memory");
 }
 
+// TMEM rows shifted by one lane toward lane 0 within each 32-lane quadrant:
+// lane i <- lane i+1 for 8 consecutive 32-bit columns at taddr; the quadrant's
+// last lane keeps its value (tools/tmem_shift.cu, B200: ~17 clk each).
+// Issued by one thread and ordered with the UMMAs in the tensor pipe.
+__device__ __forceinline__ void tmem_shift_down(uint32_t taddr) {
+  asm volatile("tcgen05.shift.cta_group::1.down [%0];" ::"r"(taddr) : "memory");
+}
+
 // ---------------------------------------------------------------- CTA pairs
 // (cta_group::2: two SMs of one cluster issue one UMMA with M = 256)
 __device__ __forceinline__ uint32_t cluster_ctarank() {

@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(128, 1) rate_split(int N, int reps, int shift_
       for (int dwi = 0; dwi < 3; ++dwi)
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const uint64_t ad = ad0 + static_cast<uint64_t>((dwi - 1) * shift_on + j * 576);
+          const uint64_t ad = ad0 + static_cast<uint64_t>((dwi - 1) * 8 * shift_on - shift_on + j * 576);
           const uint64_t bd = bd0 + static_cast<uint64_t>((dwi * 4 + j) * 2 * N);
           if (elect_one()) umma_bf16(dt, ad, bd, idesc, (r | dwi | j) != 0);
         }
