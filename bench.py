@@ -463,8 +463,9 @@ def run_b200(args, dist: Dist) -> dict | None:
     if e2e_steps:
         e2e = {"value": round(e2e_ranks * e2e_nb * e2e_steps / e2e_total, 1), "unit": "samples/s",
                "h2d_bytes_per_step": h2d // e2e_steps, "d2h_bytes_per_step": d2h // e2e_steps,
-               "input": "pinned fp32 X; chunks alternate host fp32->bf16 conversion (2 B/feature "
-                        "on the wire) and fp32 DMA + device conversion",
+               "input": "pinned fp32 X; 6 of 8 chunks converted fp32->bf16 by host threads "
+                        "(2 B/feature on the wire), the rest DMA'd as fp32 and converted on the "
+                        "device (host-memory bandwidth bound)",
                "samples_per_step": e2e_nb}
     if active:
         system.close()

@@ -94,6 +94,8 @@ typedef struct es_pool_opts {
                             chunk (all chunks if X is pageable), the rest is
                             DMA'd as fp32 from the caller's pinned buffer;
                             0 = every chunk DMA'd as fp32 (pinned X) */
+  int e2e_convert_eighths; /* with e2e_host_convert and pinned X: chunks in 8 the
+                              host converts (0 = default 6) */
 } es_pool_opts;
 
 /* RunStats (pipeline.hpp:19-25). */

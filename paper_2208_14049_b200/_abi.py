@@ -44,7 +44,7 @@ class PoolOpts(C.Structure):
     _fields_ = [("device_map", c_int_p), ("n_device_map", C.c_int), ("copy_outputs", C.c_int),
                 ("warmup", C.c_int), ("sms_per_worker", C.c_int),
                 ("overlap_colocated", C.c_int), ("e2e_chunk_rows", C.c_size_t),
-                ("e2e_host_convert", C.c_int)]
+                ("e2e_host_convert", C.c_int), ("e2e_convert_eighths", C.c_int)]
 
 
 class RunStats(C.Structure):

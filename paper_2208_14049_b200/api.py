@@ -587,7 +587,7 @@ class CombinationRule:
 
 def _pool_opts(keep: list, device_map=None, copy_outputs=True, warmup=True,
                sms_per_worker=0, overlap_colocated=False, e2e_chunk_rows=0,
-               e2e_host_convert=True) -> _abi.PoolOpts:
+               e2e_host_convert=True, e2e_convert_eighths=0) -> _abi.PoolOpts:
     """PoolOptions (runtime.hpp)."""
     dm = None
     n = 0
@@ -597,7 +597,7 @@ def _pool_opts(keep: list, device_map=None, copy_outputs=True, warmup=True,
         n = len(device_map)
     o = _abi.PoolOpts(C.cast(dm, _abi.c_int_p) if dm is not None else None, n, int(copy_outputs),
                       int(warmup), int(sms_per_worker), int(overlap_colocated),
-                      int(e2e_chunk_rows), int(e2e_host_convert))
+                      int(e2e_chunk_rows), int(e2e_host_convert), int(e2e_convert_eighths))
     keep.append(o)
     return o
 

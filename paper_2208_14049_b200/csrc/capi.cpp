@@ -164,6 +164,7 @@ PoolOptions to_opts(const es_pool_opts* o) {
   p.overlap_colocated = o->overlap_colocated != 0;
   if (o->e2e_chunk_rows > 0) p.e2e_chunk_rows = o->e2e_chunk_rows;
   p.e2e_host_convert = o->e2e_host_convert != 0;
+  if (o->e2e_convert_eighths > 0) p.e2e_convert_eighths = o->e2e_convert_eighths;
   return p;
 }
 

@@ -606,7 +606,8 @@ double InferenceSystem::run_host(const float* X, std::size_t nb, std::size_t wid
     const std::size_t r0 = i * chunk;
     const std::size_t rows = std::min(chunk, nb - r0);
     const std::size_t elems = rows * width;
-    const bool convert = mode == 1 || (mode == 0 && i % 2 == 0);
+    const std::size_t k8 = static_cast<std::size_t>(std::clamp(options_.e2e_convert_eighths, 0, 8));
+    const bool convert = mode == 1 || (mode == 0 && (i + 1) * k8 / 8 > i * k8 / 8);
     if (i >= kSlots) ES_CUDA(cudaEventSynchronize(sl.h2d_done));  // pinned slot reusable
     if (convert)
       convert_f32_to_bf16_host(X + r0 * width, static_cast<std::uint16_t*>(sl.pinned), elems,

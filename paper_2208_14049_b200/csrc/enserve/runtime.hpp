@@ -120,6 +120,12 @@ struct PoolOptions {
   // the host converts fp32 -> bf16 before the copy (half the PCIe bytes).
   std::size_t e2e_chunk_rows = 65536;
   bool e2e_host_convert = true;
+  // Pinned input with host conversion on: how many chunks in 8 the host
+  // converts (the rest are DMA'd as fp32 and converted on the device) --
+  // balances host-memory bandwidth against PCIe.  6 measured best on B200
+  // boxes (tools/e2e_sweep.py, cfg2: 4/8 2.03e7, 6/8 2.17e7, 8/8 1.98e7
+  // samples/s): both legs saturate the host's memory bandwidth.
+  int e2e_convert_eighths = 6;
 };
 
 // Per-model executable member on one GPU (the Predictor of backend.hpp:25-34).
