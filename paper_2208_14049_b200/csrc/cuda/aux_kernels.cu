@@ -4,6 +4,9 @@
 
 #include "aux_kernels.cuh"
 
+#include <algorithm>
+#include <cstdlib>
+
 namespace es {
 
 namespace {
@@ -257,9 +260,111 @@ int generate_features_bf16(uint64_t seed, size_t n, __nv_bfloat16* y, cudaStream
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
+// One thread per row, the row's C logits of each member read straight into
+// registers (8-byte loads when C is even; a warp's 32 rows are one contiguous
+// 32*4C-byte run, so the loads of one member hit the same L1 lines), no shared
+// memory and no block barrier: occupancy hides the HBM latency.  Same fold
+// arithmetic, in the same order, as combine_kernel.
+template <int C>
+__global__ void __launch_bounds__(256) combine_rows_kernel(const CombineArgs a) {
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long r = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; r < a.rows;
+       r += stride) {
+    float acc[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) acc[c] = 0.0f;
+    for (int m = 0; m < a.M; ++m) {
+      float z[C];
+      const float* src = a.logits[m] + r * C;
+      if constexpr (C % 2 == 0) {
+#pragma unroll
+        for (int c = 0; c < C; c += 2) {
+          const float2 v = __ldcs(reinterpret_cast<const float2*>(src + c));
+          z[c] = v.x;
+          z[c + 1] = v.y;
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < C; ++c) z[c] = __ldcs(src + c);
+      }
+      if (a.softmax) {
+        float mx = z[0];
+#pragma unroll
+        for (int c = 1; c < C; ++c) mx = z[c] > mx ? z[c] : mx;
+        float sum = 0.0f;
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          z[c] = expf(__fsub_rn(z[c], mx));
+          sum = __fadd_rn(sum, z[c]);
+        }
+        const float inv = __fdiv_rn(1.0f, sum);
+#pragma unroll
+        for (int c = 0; c < C; ++c) z[c] = __fmul_rn(z[c], inv);
+      }
+      if (a.rule == kVote) {
+        int best = 0;
+        float top = z[0];
+#pragma unroll
+        for (int c = 1; c < C; ++c)
+          if (z[c] > top) {
+            top = z[c];
+            best = c;
+          }
+#pragma unroll
+        for (int c = 0; c < C; ++c)
+          if (c == best) acc[c] = __fadd_rn(acc[c], 1.0f);
+      } else {
+        const float w = a.weight[m];
+#pragma unroll
+        for (int c = 0; c < C; ++c) acc[c] = __fadd_rn(acc[c], __fmul_rn(z[c], w));
+      }
+    }
+    int best = 0;
+    float top = acc[0];
+#pragma unroll
+    for (int c = 1; c < C; ++c)
+      if (acc[c] > top) {
+        top = acc[c];
+        best = c;
+      }
+    float* dst = a.y + r * C;
+    if constexpr (C % 2 == 0) {
+#pragma unroll
+      for (int c = 0; c < C; c += 2) __stcs(reinterpret_cast<float2*>(dst + c), make_float2(acc[c], acc[c + 1]));
+    } else {
+#pragma unroll
+      for (int c = 0; c < C; ++c) __stcs(dst + c, acc[c]);
+    }
+    if (a.argmax) a.argmax[r] = best;
+  }
+}
+
+template <int C>
+int launch_rows(const CombineArgs& a, cudaStream_t s) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long want = (a.rows + 255) / 256;
+  const long long blocks = std::min<long long>(want, static_cast<long long>(sms) * 8);
+  combine_rows_kernel<C><<<static_cast<unsigned>(blocks), 256, 0, s>>>(a);
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
 int combine_launch(const CombineArgs& a, cudaStream_t s) {
   if (a.rows <= 0) return 0;
   if (a.M < 1 || a.M > kMaxMembers || a.C < 1 || a.C > kMaxClasses) return -2;
+  if (!std::getenv("ES_COMBINE_STAGED")) {
+    switch (a.C) {
+      case 2: return launch_rows<2>(a, s);
+      case 3: return launch_rows<3>(a, s);
+      case 4: return launch_rows<4>(a, s);
+      case 5: return launch_rows<5>(a, s);
+      case 8: return launch_rows<8>(a, s);
+      case 10: return launch_rows<10>(a, s);
+      case 16: return launch_rows<16>(a, s);
+      default: break;  // other widths: the staged kernel
+    }
+  }
   // Rows per block: 128, fewer when M*C slices would not fit 48 KB of smem.
   int R = kRowsPerBlock;
   while (R > 8 && static_cast<size_t>(a.M) * R * a.C * sizeof(float) > 48 * 1024) R /= 2;
