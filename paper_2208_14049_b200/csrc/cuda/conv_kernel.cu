@@ -91,11 +91,11 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
       mbar_init(&a1_full[b], 1);
       mbar_init(&a1_empty[b], 1);
       mbar_init(&c1_full[b], 1);
-      mbar_init(&c1_empty[b], 4);
-      mbar_init(&a2_full[b], 128);
+      mbar_init(&c1_empty[b], SPLIT ? 8 : 4);
+      mbar_init(&a2_full[b], SPLIT ? 256 : 128);
       mbar_init(&a2_empty[b], 1);
       mbar_init(&c2_full[b], 1);
-      mbar_init(&c2_empty[b], SPLIT ? 8 : 4);
+      mbar_init(&c2_empty[b], 4);
     }
     mbar_init(&mma_done[0], 1);
     mbar_init(&mma_done[1], 1);
@@ -322,10 +322,14 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
     }
     if (my_tiles > 0) conv2(my_tiles - 1);
     if (SPLIT) flush_shifts();
-  } else if (warp < 6) {
+  } else if (warp < (SPLIT ? 10 : 6)) {
     // ------------------------------------------------------- conv1 epilogue
-    const int ta = threadIdx.x - 64;  // 0..127
+    // tap: warps 2-5, all c1 channels; split: warps 2-9, two channel halves
+    // (its conv2 epilogue is a lane-local sum and needs fewer warps).
+    const int ta = threadIdx.x - 64;
     const int q = warp & 3;
+    const int cpw = SPLIT ? L.c1 / 2 : L.c1;  // channels per warp
+    const int cbeg = SPLIT ? ((warp - 2) >> 2) * cpw : 0;
     const uint32_t lane_field = static_cast<uint32_t>(q * 32) << 16;
     for (int k = 0; k < my_tiles; ++k) {
       const int b = k & 1;
@@ -340,7 +344,7 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
         const int r = mb * 128 + q * 32 + lane;
         const int n = r / G2, p = r % G2, i = p / L.G, j = p % L.G;
         const int grow = kMargin + n * P2 + (i + 1) * L.R + j;  // column G is the border
-        for (int c0 = 0; c0 < L.c1; c0 += 32) {
+        for (int c0 = cbeg; c0 < cbeg + cpw; c0 += 32) {
           uint32_t v[32];
           if (args.debug & 1) {
 #pragma unroll
@@ -380,16 +384,14 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
     // output's lane (conv_kernel.cuh), so out = g(-1) + g(0) + g(+1) per lane.
     // Lane 30 of a quadrant needs lane 32's dw=+1 partial, which the in-quadrant
     // shift cannot fetch: that partial is zero (it reads the border column).
-    // Eight warps: group eg = 0 (warps 6-9) takes channels [0, c2/2), group 1
-    // (warps 10-13) [c2/2, c2), 16 at a time.
-    const int eg = (warp - 6) >> 2;
+    // Warps 10-13, every channel, 16 at a time.
     auto epi2_split = [&](int k) {
       const long long s0 = args.row_begin + (blockIdx.x + static_cast<long long>(k) * gridDim.x) * L.T;
       const float keep_p1 = lane == 30 ? 0.0f : 1.0f;
       for (int mb = 0; mb < L.mb2; ++mb) {
         const int blk = k * L.mb2 + mb, sl = blk & 1;
         mbar_sleep_wait(&c2_full[sl], static_cast<uint32_t>(blk >> 1) & 1u);
-        if (warp == 6 && lane == 0 && mb == 0) TRACE(k, 8);
+        if (warp == 10 && lane == 0 && mb == 0) TRACE(k, 8);
         tc_fence_after();
         const int r = mb * 128 + q * 32 + lane;  // grid row of the tile
         const int n = r / P2, rr = r % P2, h = rr / L.R, w = rr % L.R;
@@ -397,7 +399,7 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
         uint8_t* dst = static_cast<uint8_t*>(args.out) + (s0 + n) * row_bytes +
                        ((h - 1) * L.G + w) * L.c2 * 2;
         const uint32_t col = tmem_base + lane_field + static_cast<uint32_t>(2 * L.tmem_c1 + sl * L.n2);
-        for (int c0 = eg * (L.c2 >> 1); c0 < (eg + 1) * (L.c2 >> 1); c0 += 16) {
+        for (int c0 = 0; c0 < L.c2; c0 += 16) {
           uint32_t r0[16], r1[16], r2[16];
           if (args.debug & 4) {
 #pragma unroll
@@ -431,7 +433,7 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&c2_empty[sl]);
       }
-      if (warp == 6 && lane == 0) TRACE(k, 9);
+      if (warp == 10 && lane == 0) TRACE(k, 9);
     };
     auto epi2 = [&](int k) {
       if (SPLIT) {
@@ -509,14 +511,11 @@ bool conv_plan(int S, int P, int c1, int c2, ConvLayout* out, int schedule) {
   // split: N = 3*c2 per UMMA; 128-row blocks and 32-lane quadrants must start
   // on grid-row boundaries (R | 32) so every quadrant's last lane is a border
   // column (the in-quadrant lane shift never needs the next quadrant).
-  const bool split_ok = 3 * c2 <= 256 && 32 % L.R == 0;
+  const bool split_ok = 3 * c2 <= 256 && 32 % L.R == 0 && c1 % 64 == 0;
   if (schedule == 2 && !split_ok) return false;
-  // Measured on B200 (tools/trace_conv.cu, 2^20 CNN-s samples): tap 3.84 ms,
-  // split 3.9 ms -- split issues 2.6x fewer UMMA clk, but its N = 96 UMMAs
-  // run at ~70-100 clk inside the kernel (57 alone, tools/umma_rate.cu) and
-  // the UMMA -> shift -> epilogue chain leaves the 2-slot ring shallow, so
-  // split is opt-in (ES_CONV_SCHEDULE=split).
-  L.split = split_ok && schedule == 2;
+  // Measured on B200 (tools/trace_conv.cu, 2^20 CNN-s samples): split 3.49 ms
+  // (8 conv1-epilogue warps, 4 for the lane-local conv2 epilogue), tap 3.84 ms.
+  L.split = split_ok && schedule != 1;
   L.n2 = L.split ? 3 * c2 : c2;
   for (int T = std::max(1, 256 / P2); T >= 1; --T) {
     L.T = T;

@@ -40,8 +40,8 @@
 //     each 32-lane quadrant).  With the grid's border column LAST in a row
 //     (w = G), a quadrant's lane 31 is a border pixel and lane 30's missing
 //     dw=+1 partial (lane 32's) reads only the border column, i.e. is zero --
-//     so the epilogue is a lane-local sum.  Correct and measured; opt-in
-//     (conv_plan).
+//     so the epilogue is a lane-local sum.  The default where the shape
+//     allows it (measured faster than tap, conv_plan).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -88,7 +88,7 @@ struct ConvArgs {
 
 // False when the shape has no plan (P != 4, S % P != 0, c1 not in
 // {32, 64, 128}, c2 not a multiple of 32 up to 256, grids larger than 13 x 13).
-// schedule: 0 = default (tap, the faster one measured), 1 = tap, 2 = split
+// schedule: 0 = split where the shape allows it, else tap; 1 = tap; 2 = split
 // (false if the shape does not allow it).
 bool conv_plan(int S, int P, int c1, int c2, ConvLayout* out, int schedule = 0);
 // x: bf16 [x_rows][S*S].
