@@ -71,10 +71,10 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
   uint64_t* c1_empty = c1_full + 2;
   uint64_t* a2_full = c1_empty + 2;
   uint64_t* a2_empty = a2_full + 2;
-  uint64_t* c2_full = a2_empty + 2;
-  uint64_t* c2_empty = c2_full + 2;
-  uint64_t* mma_done = c2_empty + 2;  // split: a block's UMMAs completed (shifts may go)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mma_done + 2);
+  uint64_t* c2_full = a2_empty + 2;  // [3]: conv2 accumulator slots (split: 3, tap: 2)
+  uint64_t* c2_empty = c2_full + 3;
+  uint64_t* mma_done = c2_empty + 3;  // [3] split: a block's UMMAs completed (shifts may go)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mma_done + 3);
 
   const int warp = warp_uniform_id();
   const int lane = threadIdx.x & 31;
@@ -94,11 +94,12 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
       mbar_init(&c1_empty[b], SPLIT ? 8 : 4);
       mbar_init(&a2_full[b], SPLIT ? 256 : 128);
       mbar_init(&a2_empty[b], 1);
-      mbar_init(&c2_full[b], 1);
-      mbar_init(&c2_empty[b], 4);
     }
-    mbar_init(&mma_done[0], 1);
-    mbar_init(&mma_done[1], 1);
+    for (int sl = 0; sl < 3; ++sl) {
+      mbar_init(&c2_full[sl], 1);
+      mbar_init(&c2_empty[sl], 4);
+      mbar_init(&mma_done[sl], 1);
+    }
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) tma_prefetch(&tm_x);
@@ -204,43 +205,24 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
     auto conv1 = [&](int k) {
       const int b = k & 1;
       const uint32_t u = static_cast<uint32_t>(k >> 1) & 1u;
+      // conv1 accumulators: split keeps ONE buffer (its epilogue releases it
+      // as soon as the values are in registers) so TMEM holds 3 conv2 slots.
+      const int cb = SPLIT ? 0 : b;
+      const uint32_t cu = SPLIT ? static_cast<uint32_t>(k) & 1u : u;
       mbar_sleep_wait(&a1_full[b], u);
-      mbar_sleep_wait(&c1_empty[b], u ^ 1u);
+      mbar_sleep_wait(&c1_empty[cb], cu ^ 1u);
       TRACE(k, 1);
       tc_fence_after();
       const uint64_t ad = sdesc_planar(a1_base + b * L.a1_bytes, L.a1_plane);
       for (int mb = 0; mb < L.mb1; ++mb)
         if (elect_one())
-          umma_bf16(tbase + static_cast<uint32_t>(b * L.tmem_c1 + mb * L.c1),
+          umma_bf16(tbase + static_cast<uint32_t>(cb * L.tmem_c1 + mb * L.c1),
                     ad + static_cast<uint64_t>(mb * 128), w1d, id1, 0);
       if (elect_one()) {
         umma_commit(&a1_empty[b]);
-        umma_commit(&c1_full[b]);
+        umma_commit(&c1_full[cb]);
       }
       __syncwarp();
-    };
-    // tcgen05.shift is not ordered behind in-flight UMMAs on the same columns
-    // (measured: shifting right after the UMMAs reads partial sums), so a
-    // block's shifts wait for its UMMAs' commit.
-    int pend_sl = -1;
-    uint32_t done_par = 0;  // bit s: parity of mma_done[s]
-    auto flush_shifts = [&]() {
-      if (pend_sl < 0) return;
-      const int sl = pend_sl;
-      mbar_wait(&mma_done[sl], (done_par >> sl) & 1u);
-      done_par ^= 1u << sl;
-      tc_fence_after();
-      const uint32_t d = tbase + static_cast<uint32_t>(2 * L.tmem_c1 + sl * L.n2);
-      // out[q] = D'[q][dw=-1] + D'[q+1][dw=0] + D'[q+2][dw=+1]: pull the dw=0
-      // columns one lane, the dw=+1 columns two lanes toward lane 0.
-      for (int c = 0; c < L.c2; c += 8) {
-        if (elect_one()) tmem_shift_down(d + static_cast<uint32_t>(L.c2 + c));
-        if (elect_one()) tmem_shift_down(d + static_cast<uint32_t>(2 * L.c2 + c));
-        if (elect_one()) tmem_shift_down(d + static_cast<uint32_t>(2 * L.c2 + c));
-      }
-      if (elect_one()) umma_commit(&c2_full[sl]);
-      __syncwarp();
-      pend_sl = -1;
     };
     auto conv2_split = [&](int k) {
       // One accumulator slot per 128-row block, alternating over the running
@@ -251,10 +233,11 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
       TRACE(k, 2);
       const uint64_t ad0 = sdesc_planar(a2_base + b * L.a2_bytes, L.a2_plane);
       for (int mb = 0; mb < L.mb2; ++mb) {
-        const int blk = k * L.mb2 + mb, sl = blk & 1;
-        mbar_sleep_wait(&c2_empty[sl], (static_cast<uint32_t>(blk >> 1) & 1u) ^ 1u);
+        const int blk = k * L.mb2 + mb, sl = blk % 3;
+        mbar_sleep_wait(&c2_empty[sl], (static_cast<uint32_t>(blk / 3) & 1u) ^ 1u);
+        TRACE(k, 10 + 3 * mb);
         tc_fence_after();
-        const uint32_t d = tbase + static_cast<uint32_t>(2 * L.tmem_c1 + sl * L.n2);
+        const uint32_t d = tbase + static_cast<uint32_t>(L.tmem_c1 + sl * L.n2);
         const uint64_t adm = ad0 + static_cast<uint64_t>(kMargin + mb * 128);
         // D'[p][dw] = sum_dh X[p - 1 + dh*R] W(dh, dw): A shifted by dh*R - 1.
 #pragma unroll
@@ -271,12 +254,7 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
           if (mb == L.mb2 - 1) umma_commit(&a2_empty[b]);
         }
         __syncwarp();
-        // Shifting right behind the block's own UMMAs (drains the pipe for
-        // one UMMA latency) measured faster than deferring the shifts behind
-        // the next block's UMMAs, which leaves the 2-slot accumulator ring
-        // too shallow (tools/trace_conv.cu: 2.13 vs 2.55 us per tile).
-        pend_sl = sl;
-        flush_shifts();
+        TRACE(k, 11 + 3 * mb);
       }
       TRACE(k, 3);
     };
@@ -321,56 +299,74 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
       if (k > 0) conv2(k - 1);
     }
     if (my_tiles > 0) conv2(my_tiles - 1);
-    if (SPLIT) flush_shifts();
   } else if (warp < (SPLIT ? 10 : 6)) {
     // ------------------------------------------------------- conv1 epilogue
     // tap: warps 2-5, all c1 channels; split: warps 2-9, two channel halves
     // (its conv2 epilogue is a lane-local sum and needs fewer warps).
     const int ta = threadIdx.x - 64;
     const int q = warp & 3;
-    const int cpw = SPLIT ? L.c1 / 2 : L.c1;  // channels per warp
-    const int cbeg = SPLIT ? ((warp - 2) >> 2) * cpw : 0;
+    const int cbeg = SPLIT ? ((warp - 2) >> 2) * (L.c1 / 2) : 0;  // split: c1 = 64, 32 per warp
     const uint32_t lane_field = static_cast<uint32_t>(q * 32) << 16;
+    const int rows = L.T * G2;
+    // relu(acc + b1) as bf16 into grid buffer a2 for 32 channels from c0.
+    auto emit = [&](uint8_t* a2, int mb, int c0, const uint32_t (&v)[32]) {
+      const int r = mb * 128 + q * 32 + lane;
+      if (r >= rows || (args.debug & 2)) return;
+      const int n = r / G2, p = r % G2, i = p / L.G, j = p % L.G;
+      const int grow = kMargin + n * P2 + (i + 1) * L.R + j;  // column G is the border
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        const int c = g * 8;
+        const float4 bl = *reinterpret_cast<const float4*>(sB1 + c0 + c);
+        const float4 bh = *reinterpret_cast<const float4*>(sB1 + c0 + c + 4);
+        const uint4 pk = make_uint4(pack_relu_bf16(v[c], v[c + 1], bl.x, bl.y),
+                                    pack_relu_bf16(v[c + 2], v[c + 3], bl.z, bl.w),
+                                    pack_relu_bf16(v[c + 4], v[c + 5], bh.x, bh.y),
+                                    pack_relu_bf16(v[c + 6], v[c + 7], bh.z, bh.w));
+        *reinterpret_cast<uint4*>(a2 + (c0 / 8 + g) * L.a2_plane + grow * 16) = pk;
+      }
+    };
     for (int k = 0; k < my_tiles; ++k) {
       const int b = k & 1;
       const uint32_t u = static_cast<uint32_t>(k >> 1) & 1u;
-      mbar_sleep_wait(&c1_full[b], u);
-      mbar_sleep_wait(&a2_empty[b], u ^ 1u);
-      if (ta == 0) TRACE(k, 6);
-      tc_fence_after();
       uint8_t* a2 = sA2 + b * L.a2_bytes;
-      const int rows = L.T * G2;
-      for (int mb = 0; mb < L.mb1; ++mb) {
-        const int r = mb * 128 + q * 32 + lane;
-        const int n = r / G2, p = r % G2, i = p / L.G, j = p % L.G;
-        const int grow = kMargin + n * P2 + (i + 1) * L.R + j;  // column G is the border
-        for (int c0 = cbeg; c0 < cbeg + cpw; c0 += 32) {
-          uint32_t v[32];
-          if (args.debug & 1) {
+      if (SPLIT) {
+        // One conv1 buffer: pull this warp's 2 x 32 values into registers,
+        // release the TMEM, then convert and store.
+        mbar_sleep_wait(&c1_full[0], static_cast<uint32_t>(k) & 1u);
+        mbar_sleep_wait(&a2_empty[b], u ^ 1u);
+        if (ta == 0) TRACE(k, 6);
+        tc_fence_after();
+        uint32_t v0[32], v1[32];
+        tmem_ld32_raw(tmem_base + lane_field + static_cast<uint32_t>(cbeg), v0);
+        if (L.mb1 > 1) tmem_ld32_raw(tmem_base + lane_field + static_cast<uint32_t>(L.c1 + cbeg), v1);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&c1_empty[0]);
+        emit(a2, 0, cbeg, v0);
+        if (L.mb1 > 1) emit(a2, 1, cbeg, v1);
+      } else {
+        mbar_sleep_wait(&c1_full[b], u);
+        mbar_sleep_wait(&a2_empty[b], u ^ 1u);
+        if (ta == 0) TRACE(k, 6);
+        tc_fence_after();
+        for (int mb = 0; mb < L.mb1; ++mb)
+          for (int c0 = 0; c0 < L.c1; c0 += 32) {
+            uint32_t v[32];
+            if (args.debug & 1) {
 #pragma unroll
-            for (int c = 0; c < 32; ++c) v[c] = static_cast<uint32_t>(c);
-          } else {
-            tmem_ld32_raw(tmem_base + lane_field + static_cast<uint32_t>(b * L.tmem_c1 + mb * L.c1 + c0), v);
-            tmem_ld_wait();
-          }
-          if (r < rows && !(args.debug & 2)) {
-#pragma unroll
-            for (int g = 0; g < 4; ++g) {
-              const int c = g * 8;
-              const float4 bl = *reinterpret_cast<const float4*>(sB1 + c0 + c);
-              const float4 bh = *reinterpret_cast<const float4*>(sB1 + c0 + c + 4);
-              const uint4 pk = make_uint4(pack_relu_bf16(v[c], v[c + 1], bl.x, bl.y),
-                                          pack_relu_bf16(v[c + 2], v[c + 3], bl.z, bl.w),
-                                          pack_relu_bf16(v[c + 4], v[c + 5], bh.x, bh.y),
-                                          pack_relu_bf16(v[c + 6], v[c + 7], bh.z, bh.w));
-              *reinterpret_cast<uint4*>(a2 + (c0 / 8 + g) * L.a2_plane + grow * 16) = pk;
+              for (int c = 0; c < 32; ++c) v[c] = static_cast<uint32_t>(c);
+            } else {
+              tmem_ld32_raw(tmem_base + lane_field + static_cast<uint32_t>(b * L.tmem_c1 + mb * L.c1 + c0), v);
+              tmem_ld_wait();
             }
+            emit(a2, mb, c0, v);
           }
-        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&c1_empty[b]);
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&c1_empty[b]);
       fence_proxy_async_smem();
       mbar_arrive(&a2_full[b]);
       if (ta == 0) TRACE(k, 7);
@@ -389,8 +385,27 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
       const long long s0 = args.row_begin + (blockIdx.x + static_cast<long long>(k) * gridDim.x) * L.T;
       const float keep_p1 = lane == 30 ? 0.0f : 1.0f;
       for (int mb = 0; mb < L.mb2; ++mb) {
-        const int blk = k * L.mb2 + mb, sl = blk & 1;
-        mbar_sleep_wait(&c2_full[sl], static_cast<uint32_t>(blk >> 1) & 1u);
+        const int blk = k * L.mb2 + mb, sl = blk % 3;
+        const uint32_t ph = static_cast<uint32_t>(blk / 3) & 1u;
+        // tcgen05.shift is not ordered behind in-flight UMMAs on the same
+        // columns (measured: shifting right after the UMMAs reads partial
+        // sums), so the shifts wait for the block's UMMA commit -- issued here,
+        // by one epilogue warp, so the UMMA warp never waits on its own work.
+        if (warp == 10) {
+          mbar_sleep_wait(&mma_done[sl], ph);
+          tc_fence_after();
+          const uint32_t d = tmem_base + static_cast<uint32_t>(L.tmem_c1 + sl * L.n2);
+          // out[q] = D'[q][dw=-1] + D'[q+1][dw=0] + D'[q+2][dw=+1]: pull the
+          // dw=0 columns one lane, the dw=+1 columns two lanes toward lane 0.
+          for (int c = 0; c < L.c2; c += 8) {
+            if (elect_one()) tmem_shift_down(d + static_cast<uint32_t>(L.c2 + c));
+            if (elect_one()) tmem_shift_down(d + static_cast<uint32_t>(2 * L.c2 + c));
+            if (elect_one()) tmem_shift_down(d + static_cast<uint32_t>(2 * L.c2 + c));
+          }
+          if (elect_one()) umma_commit(&c2_full[sl]);
+          __syncwarp();
+        }
+        mbar_sleep_wait(&c2_full[sl], ph);
         if (warp == 10 && lane == 0 && mb == 0) TRACE(k, 8);
         tc_fence_after();
         const int r = mb * 128 + q * 32 + lane;  // grid row of the tile
@@ -398,7 +413,7 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
         const bool valid = r < L.T * P2 && h >= 1 && w < L.G && s0 + n < args.row_end;
         uint8_t* dst = static_cast<uint8_t*>(args.out) + (s0 + n) * row_bytes +
                        ((h - 1) * L.G + w) * L.c2 * 2;
-        const uint32_t col = tmem_base + lane_field + static_cast<uint32_t>(2 * L.tmem_c1 + sl * L.n2);
+        const uint32_t col = tmem_base + lane_field + static_cast<uint32_t>(L.tmem_c1 + sl * L.n2);
         for (int c0 = 0; c0 < L.c2; c0 += 16) {
           uint32_t r0[16], r1[16], r2[16];
           if (args.debug & 4) {
@@ -511,10 +526,12 @@ bool conv_plan(int S, int P, int c1, int c2, ConvLayout* out, int schedule) {
   // split: N = 3*c2 per UMMA; 128-row blocks and 32-lane quadrants must start
   // on grid-row boundaries (R | 32) so every quadrant's last lane is a border
   // column (the in-quadrant lane shift never needs the next quadrant).
-  const bool split_ok = 3 * c2 <= 256 && 32 % L.R == 0 && c1 % 64 == 0;
+  const bool split_ok = 3 * c2 <= 256 && 32 % L.R == 0 && c1 == 64;
   if (schedule == 2 && !split_ok) return false;
-  // Measured on B200 (tools/trace_conv.cu, 2^20 CNN-s samples): split 3.49 ms
-  // (8 conv1-epilogue warps, 4 for the lane-local conv2 epilogue), tap 3.84 ms.
+  // Measured on B200 (tools/trace_conv.cu, 2^20 CNN-s samples): split 3.16 ms
+  // (one conv1 TMEM buffer + a 3-slot conv2 ring, shifts issued by an
+  // epilogue warp after the block's UMMA commit, 8 conv1-epilogue warps),
+  // tap 3.84 ms.
   L.split = split_ok && schedule != 1;
   L.n2 = L.split ? 3 * c2 : c2;
   for (int T = std::max(1, 256 / P2); T >= 1; --T) {
@@ -526,7 +543,8 @@ bool conv_plan(int S, int P, int c1, int c2, ConvLayout* out, int schedule) {
     // split: one N = 3*c2 slot per 128-row block, two slots; tap: a
     // double-buffered [mb2][c2] accumulator per tile.
     L.tmem_c2 = L.split ? L.n2 : L.mb2 * c2;
-    const int cols = 2 * (L.tmem_c1 + L.tmem_c2);
+    // split: one conv1 buffer + a ring of 3 conv2 slots; tap: 2 + 2.
+    const int cols = L.split ? L.tmem_c1 + 3 * L.tmem_c2 : 2 * (L.tmem_c1 + L.tmem_c2);
     if (cols > 512) continue;
     int tc = 32;
     while (tc < cols) tc <<= 1;
@@ -548,7 +566,7 @@ bool conv_plan(int S, int P, int c1, int c2, ConvLayout* out, int schedule) {
     L.off_rows = align_up(L.off_b2 + static_cast<uint32_t>(c2 * 4), 16);
     L.off_xch = align_up(L.off_rows + static_cast<uint32_t>(T * G2 * 4), 16);
     L.off_bar = align_up(L.off_xch, 8);
-    const uint32_t bars = static_cast<uint32_t>(2 * L.raw_stages + 18) * 8u + 16u;
+    const uint32_t bars = static_cast<uint32_t>(2 * L.raw_stages + 21) * 8u + 16u;
     L.smem_bytes = L.off_bar + bars + 1024u;  // + alignment slack of the dynamic base
     if (L.smem_bytes > kSmemBudget) continue;
     *out = L;
