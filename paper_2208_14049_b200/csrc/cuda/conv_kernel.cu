@@ -64,6 +64,8 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
   float* sB1 = reinterpret_cast<float*>(smem + L.off_b1);
   float* sB2 = reinterpret_cast<float*>(smem + L.off_b2);
   int* sRowOff = reinterpret_cast<int*>(smem + L.off_rows);  // im2col source offset per row
+  int* sGrow = sRowOff + L.T * L.G * L.G;  // conv1 output row -> grid row
+  int* sOut = sGrow + L.T * L.G * L.G;     // grid row -> (sample << 24 | byte offset), -1 = border
   uint64_t* raw_full = reinterpret_cast<uint64_t*>(smem + L.off_bar);
   uint64_t* a1_full = raw_full + 2 * L.raw_stages;  // every pair below: one per buffer
   uint64_t* a1_empty = a1_full + 2;
@@ -128,6 +130,11 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
     for (int r = threadIdx.x; r < L.T * L.G * L.G; r += threads_for<SPLIT>()) {
       const int G2r = L.G * L.G, n = r / G2r, p = r % G2r, i = p / L.G, j = p % L.G;
       sRowOff[r] = (n * L.S * L.S + (4 * i) * L.S + 4 * j) * 2;  // patch (i, j) of sample n
+      sGrow[r] = kMargin + n * L.R * L.R + (i + 1) * L.R + j;     // column G is the border
+    }
+    for (int r = threadIdx.x; r < L.mb2 * 128; r += threads_for<SPLIT>()) {
+      const int P2r = L.R * L.R, n = r / P2r, rr = r % P2r, h = rr / L.R, w = rr % L.R;
+      sOut[r] = (r < L.T * P2r && h >= 1 && w < L.G) ? (n << 24) | (((h - 1) * L.G + w) * L.c2 * 2) : -1;
     }
     for (int i = threadIdx.x; i < L.c1; i += threads_for<SPLIT>()) sB1[i] = args.b1[i];
     for (int i = threadIdx.x; i < L.c2; i += threads_for<SPLIT>()) sB2[i] = args.b2[i];
@@ -308,24 +315,33 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
     const int cbeg = SPLIT ? ((warp - 2) >> 2) * (L.c1 / 2) : 0;  // split: c1 = 64, 32 per warp
     const uint32_t lane_field = static_cast<uint32_t>(q * 32) << 16;
     const int rows = L.T * G2;
-    // relu(acc + b1) as bf16 into grid buffer a2 for 32 channels from c0.
-    auto emit = [&](uint8_t* a2, int mb, int c0, const uint32_t (&v)[32]) {
+    // relu(acc + bias) as bf16 into grid buffer a2 for the 32 channels from c0.
+    auto emit = [&](uint8_t* a2, int mb, int c0, const uint32_t (&v)[32], const float (&bias)[32]) {
       const int r = mb * 128 + q * 32 + lane;
       if (r >= rows || (args.debug & 2)) return;
-      const int n = r / G2, p = r % G2, i = p / L.G, j = p % L.G;
-      const int grow = kMargin + n * P2 + (i + 1) * L.R + j;  // column G is the border
+      const int grow = sGrow[r];
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
         const int c = g * 8;
-        const float4 bl = *reinterpret_cast<const float4*>(sB1 + c0 + c);
-        const float4 bh = *reinterpret_cast<const float4*>(sB1 + c0 + c + 4);
-        const uint4 pk = make_uint4(pack_relu_bf16(v[c], v[c + 1], bl.x, bl.y),
-                                    pack_relu_bf16(v[c + 2], v[c + 3], bl.z, bl.w),
-                                    pack_relu_bf16(v[c + 4], v[c + 5], bh.x, bh.y),
-                                    pack_relu_bf16(v[c + 6], v[c + 7], bh.z, bh.w));
+        const uint4 pk = make_uint4(pack_relu_bf16(v[c], v[c + 1], bias[c], bias[c + 1]),
+                                    pack_relu_bf16(v[c + 2], v[c + 3], bias[c + 2], bias[c + 3]),
+                                    pack_relu_bf16(v[c + 4], v[c + 5], bias[c + 4], bias[c + 5]),
+                                    pack_relu_bf16(v[c + 6], v[c + 7], bias[c + 6], bias[c + 7]));
         *reinterpret_cast<uint4*>(a2 + (c0 / 8 + g) * L.a2_plane + grow * 16) = pk;
       }
     };
+    auto load_bias = [&](int c0, float (&bias)[32]) {
+#pragma unroll
+      for (int c = 0; c < 32; c += 4) {
+        const float4 b4 = *reinterpret_cast<const float4*>(sB1 + c0 + c);
+        bias[c] = b4.x;
+        bias[c + 1] = b4.y;
+        bias[c + 2] = b4.z;
+        bias[c + 3] = b4.w;
+      }
+    };
+    float bias_w[32];  // split: this warp's 32 channels, loaded once
+    if (SPLIT) load_bias(cbeg, bias_w);
     for (int k = 0; k < my_tiles; ++k) {
       const int b = k & 1;
       const uint32_t u = static_cast<uint32_t>(k >> 1) & 1u;
@@ -344,8 +360,8 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&c1_empty[0]);
-        emit(a2, 0, cbeg, v0);
-        if (L.mb1 > 1) emit(a2, 1, cbeg, v1);
+        emit(a2, 0, cbeg, v0, bias_w);
+        if (L.mb1 > 1) emit(a2, 1, cbeg, v1, bias_w);
       } else {
         mbar_sleep_wait(&c1_full[b], u);
         mbar_sleep_wait(&a2_empty[b], u ^ 1u);
@@ -361,7 +377,9 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
               tmem_ld32_raw(tmem_base + lane_field + static_cast<uint32_t>(b * L.tmem_c1 + mb * L.c1 + c0), v);
               tmem_ld_wait();
             }
-            emit(a2, mb, c0, v);
+            float bias[32];
+            load_bias(c0, bias);
+            emit(a2, mb, c0, v, bias);
           }
         tc_fence_before();
         __syncwarp();
@@ -409,10 +427,10 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
         if (warp == 10 && lane == 0 && mb == 0) TRACE(k, 8);
         tc_fence_after();
         const int r = mb * 128 + q * 32 + lane;  // grid row of the tile
-        const int n = r / P2, rr = r % P2, h = rr / L.R, w = rr % L.R;
-        const bool valid = r < L.T * P2 && h >= 1 && w < L.G && s0 + n < args.row_end;
-        uint8_t* dst = static_cast<uint8_t*>(args.out) + (s0 + n) * row_bytes +
-                       ((h - 1) * L.G + w) * L.c2 * 2;
+        const int oo = sOut[r];
+        const int n = oo >> 24;
+        const bool valid = oo >= 0 && s0 + n < args.row_end;
+        uint8_t* dst = static_cast<uint8_t*>(args.out) + (s0 + n) * row_bytes + (oo & 0xFFFFFF);
         const uint32_t col = tmem_base + lane_field + static_cast<uint32_t>(L.tmem_c1 + sl * L.n2);
         for (int c0 = 0; c0 < L.c2; c0 += 16) {
           uint32_t r0[16], r1[16], r2[16];
@@ -463,10 +481,10 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
       const long long s0 = args.row_begin + (blockIdx.x + static_cast<long long>(k) * gridDim.x) * L.T;
       for (int mb = 0; mb < L.mb2; ++mb) {
         const int r = mb * 128 + q * 32 + lane;  // grid row of the tile
-        const int n = r / P2, rr = r % P2, h = rr / L.R, w = rr % L.R;
-        const bool valid = r < L.T * P2 && h >= 1 && w < L.G && s0 + n < args.row_end;
-        uint8_t* dst = static_cast<uint8_t*>(args.out) + (s0 + n) * row_bytes +
-                       ((h - 1) * L.G + w) * L.c2 * 2;
+        const int oo = sOut[r];
+        const int n = oo >> 24;
+        const bool valid = oo >= 0 && s0 + n < args.row_end;
+        uint8_t* dst = static_cast<uint8_t*>(args.out) + (s0 + n) * row_bytes + (oo & 0xFFFFFF);
         for (int c0 = 0; c0 < L.c2; c0 += 32) {
           uint32_t v[32];
           tmem_ld32_raw(tmem_base + lane_field +
@@ -528,10 +546,10 @@ bool conv_plan(int S, int P, int c1, int c2, ConvLayout* out, int schedule) {
   // column (the in-quadrant lane shift never needs the next quadrant).
   const bool split_ok = 3 * c2 <= 256 && 32 % L.R == 0 && c1 == 64;
   if (schedule == 2 && !split_ok) return false;
-  // Measured on B200 (tools/trace_conv.cu, 2^20 CNN-s samples): split 3.16 ms
+  // Measured on B200 (tools/trace_conv.cu, 2^20 CNN-s samples): split 2.99 ms
   // (one conv1 TMEM buffer + a 3-slot conv2 ring, shifts issued by an
-  // epilogue warp after the block's UMMA commit, 8 conv1-epilogue warps),
-  // tap 3.84 ms.
+  // epilogue warp after the block's UMMA commit, 8 conv1-epilogue warps,
+  // row-address tables instead of divisions), tap 3.77 ms.
   L.split = split_ok && schedule != 1;
   L.n2 = L.split ? 3 * c2 : c2;
   for (int T = std::max(1, 256 / P2); T >= 1; --T) {
@@ -564,7 +582,7 @@ bool conv_plan(int S, int P, int c1, int c2, ConvLayout* out, int schedule) {
     L.off_b1 = align_up(L.off_w2 + static_cast<uint32_t>(9 * c1 * c2 * 2), 16);
     L.off_b2 = align_up(L.off_b1 + static_cast<uint32_t>(c1 * 4), 16);
     L.off_rows = align_up(L.off_b2 + static_cast<uint32_t>(c2 * 4), 16);
-    L.off_xch = align_up(L.off_rows + static_cast<uint32_t>(T * G2 * 4), 16);
+    L.off_xch = align_up(L.off_rows + static_cast<uint32_t>((2 * T * G2 + L.mb2 * 128) * 4), 16);
     L.off_bar = align_up(L.off_xch, 8);
     const uint32_t bars = static_cast<uint32_t>(2 * L.raw_stages + 21) * 8u + 16u;
     L.smem_bytes = L.off_bar + bars + 1024u;  // + alignment slack of the dynamic base

@@ -282,7 +282,75 @@ __global__ void __launch_bounds__(128, 1) rate_split(int N, int reps, int shift_
   if (threadIdx.x < 32) tmem_dealloc(tmem, 512);
 }
 
+__device__ __forceinline__ void tshift(uint32_t taddr) {
+  asm volatile("tcgen05.shift.cta_group::1.down [%0];" ::"r"(taddr) : "memory");
+}
+
+// The conv kernel's split pipeline: per block 12 UMMAs (N = 96) into a ring
+// slot, then 12 tcgen05.shift on an older slot (nshift = 0: UMMAs only).
+__global__ void __launch_bounds__(128, 1) rate_mix(int reps, int nshift, unsigned long long* out) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align_smem_1024(smem_raw);
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  for (int i = threadIdx.x; i < 96 * 1024 / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  if (threadIdx.x < 32) tmem_alloc(&slot, 512);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
+  if (warp == 0) {
+    const uint32_t a = smem_u32(smem), b = smem_u32(smem + 40 * 1024);
+    const uint32_t idesc = idesc_bf16_f32(128, 96);
+    const uint64_t ad0 = sdesc_planar(a + 16 * 16, 4608), bd0 = sdesc_planar(b, 96 * 16);
+    const long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+      const uint32_t d = tmem + 128u + static_cast<uint32_t>((r % 3) * 96);
+#pragma unroll
+      for (int dhi = 0; dhi < 3; ++dhi)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint64_t ad = ad0 + static_cast<uint64_t>((dhi - 1) * 8 - 1 + j * 576);
+          const uint64_t bd = bd0 + static_cast<uint64_t>((dhi * 4 + j) * 2 * 96);
+          if (elect_one()) umma_bf16(d, ad, bd, idesc, (dhi | j) != 0);
+        }
+      const uint32_t ds = tmem + 128u + static_cast<uint32_t>(((r + 2) % 3) * 96);
+      for (int c = 0; c < 32 && nshift; c += 8) {
+        if (elect_one()) tshift(ds + 32u + c);
+        if (elect_one()) tshift(ds + 64u + c);
+        if (elect_one()) tshift(ds + 64u + c);
+      }
+    }
+    if (elect_one()) umma_commit(&bar);
+    __syncwarp();
+    mbar_wait(&bar, 0);
+    if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = static_cast<unsigned long long>(clock64() - t0);
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) tmem_dealloc(tmem, 512);
+}
+
 int main() {
+  {
+    unsigned long long* d;
+    cudaMalloc(&d, 8);
+    cudaFuncSetAttribute(rate_mix, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    for (int ns = 0; ns < 2; ++ns) {
+      rate_mix<<<148, 128, 100 * 1024>>>(60, ns, d);
+      unsigned long long c = 0;
+      cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
+      std::printf("mix shifts=%d: %.1f clk per block (12 UMMA N=96%s) %s\n", ns, double(c) / 60,
+                  ns ? " + 12 shifts" : "", cudaGetErrorString(cudaGetLastError()));
+    }
+    cudaFree(d);
+  }
   {
     unsigned long long* d;
     cudaMalloc(&d, 8);
