@@ -184,6 +184,14 @@ class Dist:
         self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
         return float(t.item())
 
+    def broadcast_object(self, obj):
+        """rank 0's picklable object on every rank."""
+        if not self.pg:
+            return obj
+        box = [obj]
+        self.pg.broadcast_object_list(box, src=0)
+        return box[0]
+
     def gather(self, values: list) -> list:
         """All ranks' lists of ints (for the exactly-once check)."""
         if not self.pg:
@@ -388,10 +396,18 @@ def run_b200(args, dist: Dist) -> dict | None:
         choice = {"A1": es.worst_fit_decreasing(cluster, cluster.min_batch()), "A2": A,
                   "A1_score": 0.0, "A2_score": 0.0, "bench_calls": 0,
                   "bbs": {"applicable": False, "reason": "matrix given on the command line"}}
-    elif multirow and dist.rank != 0:
-        choice = None
+    elif dist.rank != 0:
+        choice = None  # rank 0 optimizes; single-row configs take its matrix below
     else:
         choice = choose_matrix(es, cluster, cfg, device_map, args.calib_nb, args.seed)
+    if not multirow and dist.world > 1:
+        # Every rank must run the SAME matrix (one cluster, N device rows):
+        # rank 0's greedy result is broadcast.
+        cells = dist.broadcast_object(choice["A2"].cells.tolist() if choice else None)
+        if choice is None:
+            A0 = es.AllocationMatrix.from_array(cells)
+            choice = {"A1": A0, "A2": A0, "A1_score": 0.0, "A2_score": 0.0, "bench_calls": 0,
+                      "bbs": {"applicable": False, "reason": "rank 0 optimizes"}}
     rule = es.CombinationRule.averaging(softmax=cfg["softmax"])
     active = not multirow or dist.rank == 0
     local_nb = 0

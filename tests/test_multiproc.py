@@ -33,8 +33,10 @@ def _worker(rank: int, world: int, port: int, q):
         r0, r1, shares = bench.rank_shard(es, world, rank, [64, 64, 128, 128], nb_per_gpu)
         rows = dist.gather([r0, r1])
         t = dist.max(float(rank + 1) * 0.5)
+        # bench.py: rank 0's optimized matrix reaches every rank.
+        cells = dist.broadcast_object([[128, 64, 128, 32]] if rank == 0 else None)
         dist.barrier()
-        q.put((rank, rows, t, shares))
+        q.put((rank, rows, t, shares, cells))
     finally:
         dist.close()
 
@@ -52,8 +54,9 @@ def test_rank_shards_cover_every_segment_once_and_max_time(world):
         p.join(timeout=60)
         assert p.exitcode == 0
     total = world * 1037
-    for rank, rows, t, shares in results:
+    for rank, rows, t, shares, cells in results:
         assert t == pytest.approx(world * 0.5)  # max over ranks
+        assert cells == [[128, 64, 128, 32]]
         spans = sorted(tuple(r) for r in rows)
         assert spans[0][0] == 0 and spans[-1][1] == total
         for (a0, a1), (b0, b1) in zip(spans, spans[1:]):
