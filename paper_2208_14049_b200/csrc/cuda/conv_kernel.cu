@@ -23,7 +23,7 @@ namespace {
 constexpr int kThreads = 320;
 // split schedule: four more conv2-epilogue warps (10-13), see epi2_split.
 template <bool SPLIT>
-constexpr int threads_for() { return SPLIT ? 448 : kThreads; }
+constexpr int threads_for() { return SPLIT ? 480 : kThreads; }  // split: + warp 14, the conv2 issuer
 constexpr uint32_t kSmemBudget = 232448;
 constexpr int kMargin = 16;  // zero rows before/after the tile's grids; taps reach R+1 rows
 
@@ -155,6 +155,7 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
     // writes conv1's im2col rows of tile k (one row per output pixel: the
     // 4x4 patch as two 16-byte K planes), then refills the freed stage.
     // Source offsets per row come from a table, so the loop is loads/stores.
+    // (A second builder warp measured no faster.)
     const uint64_t pol = l2_policy_evict_first();
     const int rows16 = L.S * L.S / 16;  // the map views x as [rows * S*S/16][16]
     auto load = [&](int k) {
@@ -194,7 +195,7 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
       }
       __syncwarp();
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 || (SPLIT && warp == 14)) {
     // ------------------------------------------------------------ UMMA issuer
     // The whole warp walks the schedule (uniform descriptor arithmetic); one
     // elected lane issues.  Descriptors advance by adding 16-byte units to
@@ -231,6 +232,29 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
       }
       __syncwarp();
     };
+    // split: warp 14 issues conv2's UMMAs AND its lane shifts.  tcgen05.shift
+    // is not ordered behind in-flight UMMAs on the same columns (measured:
+    // shifting right after the UMMAs reads partial sums), so a block's shifts
+    // go out after the NEXT block's UMMAs are queued, once its own UMMA commit
+    // has landed -- the pipe never drains, and UMMAs + shifts come from one
+    // issuer (two issuers cost ~25 %, tools/umma_rate.cu).  Warp 1 issues only
+    // the few conv1 UMMAs.
+    int pend_blk = -1;
+    auto shift_block = [&](int blk) {
+      const int sl = blk % 3;
+      mbar_sleep_wait(&mma_done[sl], static_cast<uint32_t>(blk / 3) & 1u);
+      tc_fence_after();
+      const uint32_t d = tbase + static_cast<uint32_t>(L.tmem_c1 + sl * L.n2);
+      // out[q] = D'[q][dw=-1] + D'[q+1][dw=0] + D'[q+2][dw=+1]: pull the dw=0
+      // columns one lane, the dw=+1 columns two lanes toward lane 0.
+      for (int c = 0; c < L.c2; c += 8) {
+        if (elect_one()) tmem_shift_down(d + static_cast<uint32_t>(L.c2 + c));
+        if (elect_one()) tmem_shift_down(d + static_cast<uint32_t>(2 * L.c2 + c));
+        if (elect_one()) tmem_shift_down(d + static_cast<uint32_t>(2 * L.c2 + c));
+      }
+      if (elect_one()) umma_commit(&c2_full[sl]);
+      __syncwarp();
+    };
     auto conv2_split = [&](int k) {
       // One accumulator slot per 128-row block, alternating over the running
       // block count: the epilogue of block i overlaps the UMMAs of block i+1.
@@ -262,6 +286,8 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
         }
         __syncwarp();
         TRACE(k, 11 + 3 * mb);
+        if (pend_blk >= 0) shift_block(pend_blk);
+        pend_blk = blk;
       }
       TRACE(k, 3);
     };
@@ -299,13 +325,22 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
       __syncwarp();
       TRACE(k, 3);
     };
-    // conv1 runs one tile ahead of conv2 (conv2 of tile k waits for the
-    // conv1 epilogue of tile k, which overlaps conv1 of tile k+1).
-    for (int k = 0; k < my_tiles; ++k) {
-      conv1(k);
-      if (k > 0) conv2(k - 1);
+    if (SPLIT) {
+      if (warp == 1) {
+        for (int k = 0; k < my_tiles; ++k) conv1(k);
+      } else {
+        for (int k = 0; k < my_tiles; ++k) conv2(k);
+        if (pend_blk >= 0) shift_block(pend_blk);
+      }
+    } else {
+      // conv1 runs one tile ahead of conv2 (conv2 of tile k waits for the
+      // conv1 epilogue of tile k, which overlaps conv1 of tile k+1).
+      for (int k = 0; k < my_tiles; ++k) {
+        conv1(k);
+        if (k > 0) conv2(k - 1);
+      }
+      if (my_tiles > 0) conv2(my_tiles - 1);
     }
-    if (my_tiles > 0) conv2(my_tiles - 1);
   } else if (warp < (SPLIT ? 10 : 6)) {
     // ------------------------------------------------------- conv1 epilogue
     // tap: warps 2-5, all c1 channels; split: warps 2-9, two channel halves
@@ -405,24 +440,6 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
       for (int mb = 0; mb < L.mb2; ++mb) {
         const int blk = k * L.mb2 + mb, sl = blk % 3;
         const uint32_t ph = static_cast<uint32_t>(blk / 3) & 1u;
-        // tcgen05.shift is not ordered behind in-flight UMMAs on the same
-        // columns (measured: shifting right after the UMMAs reads partial
-        // sums), so the shifts wait for the block's UMMA commit -- issued here,
-        // by one epilogue warp, so the UMMA warp never waits on its own work.
-        if (warp == 10) {
-          mbar_sleep_wait(&mma_done[sl], ph);
-          tc_fence_after();
-          const uint32_t d = tmem_base + static_cast<uint32_t>(L.tmem_c1 + sl * L.n2);
-          // out[q] = D'[q][dw=-1] + D'[q+1][dw=0] + D'[q+2][dw=+1]: pull the
-          // dw=0 columns one lane, the dw=+1 columns two lanes toward lane 0.
-          for (int c = 0; c < L.c2; c += 8) {
-            if (elect_one()) tmem_shift_down(d + static_cast<uint32_t>(L.c2 + c));
-            if (elect_one()) tmem_shift_down(d + static_cast<uint32_t>(2 * L.c2 + c));
-            if (elect_one()) tmem_shift_down(d + static_cast<uint32_t>(2 * L.c2 + c));
-          }
-          if (elect_one()) umma_commit(&c2_full[sl]);
-          __syncwarp();
-        }
         mbar_sleep_wait(&c2_full[sl], ph);
         if (warp == 10 && lane == 0 && mb == 0) TRACE(k, 8);
         tc_fence_after();
@@ -546,9 +563,9 @@ bool conv_plan(int S, int P, int c1, int c2, ConvLayout* out, int schedule) {
   // column (the in-quadrant lane shift never needs the next quadrant).
   const bool split_ok = 3 * c2 <= 256 && 32 % L.R == 0 && c1 == 64;
   if (schedule == 2 && !split_ok) return false;
-  // Measured on B200 (tools/trace_conv.cu, 2^20 CNN-s samples): split 2.99 ms
-  // (one conv1 TMEM buffer + a 3-slot conv2 ring, shifts issued by an
-  // epilogue warp after the block's UMMA commit, 8 conv1-epilogue warps,
+  // Measured on B200 (tools/trace_conv.cu, 2^20 CNN-s samples): split 2.63 ms
+  // (one conv1 TMEM buffer + a 3-slot conv2 ring, conv2 UMMAs and shifts from
+  // one issuer warp with the shifts one block behind, 8 conv1-epilogue warps,
   // row-address tables instead of divisions), tap 3.77 ms.
   L.split = split_ok && schedule != 1;
   L.n2 = L.split ? 3 * c2 : c2;
