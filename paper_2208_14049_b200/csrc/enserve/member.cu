@@ -252,7 +252,6 @@ int DeviceMember::forward(const void* x, long long nb, int seg_size, long long s
     c.w2 = base + I.w_off[1];
     c.b2 = reinterpret_cast<const float*>(base + I.b_off[1]);
     c.out = I.act[0];
-    if (const char* dbg = std::getenv("ES_CONV_DEBUG")) c.debug = std::atoi(dbg);  // design evidence only
     M_LAUNCH(es::conv_launch(c, cur, nb, grid, stream));
     mark(launches++);
     cur = I.act[0];
