@@ -143,10 +143,11 @@ bool DeviceMember::load(int device, const ModelSpec& model, int batch) {
   const std::string want = pick ? pick : "";
   const bool pair_ok = (want.empty() || want == "pair") && es::mlpp_plan(K, H, C, batch, &I.plan_pair);
   const bool tmem_ok = (want.empty() || want == "tmem") && es::mlpt_plan(K, H, C, batch, &I.plan_tmem);
-  // Measured on B200 (profiles/): SM pairs win from H = 384 up (half the W1
-  // ingress per SM); below, the single-SM schedule's shorter barrier round
-  // trips win.
-  if (pair_ok && (!tmem_ok || !want.empty() || H >= 384))
+  // Measured on B200 (tools/time_members.py, 4M samples): the single-SM TMEM
+  // schedule wins up to H = 384 (784-384-10: 2.64 vs 2.73 ms; 784-256-10:
+  // 1.75 vs 1.76 ms; 1568-128-10: 2.29 vs 2.79 ms); SM pairs (half the W1
+  // ingress per SM) from H = 512 up, and they alone cover hidden passes.
+  if (pair_ok && (!tmem_ok || !want.empty() || H >= 512))
     I.head = Impl::Head::Pair;
   else if (tmem_ok)
     I.head = Impl::Head::Tmem;
