@@ -6,7 +6,7 @@
 //   * MLP widths[0] -> ... -> widths[L]: the first L-2 layers run as tcgen05
 //     dense layers (bias + ReLU fused, bf16 activations in HBM), the last two
 //     as one fused member kernel (hidden layer never leaves the SM): the
-//     SM-pair schedule for hidden >= 384, the single-SM TMEM schedule below,
+//     SM-pair schedule for hidden >= 512, the single-SM TMEM schedule below,
 //     the swap-AB schedule when neither fits.
 #pragma once
 
