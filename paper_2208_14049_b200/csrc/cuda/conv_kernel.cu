@@ -547,6 +547,9 @@ uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
 }  // namespace
 
 bool conv_plan(int S, int P, int c1, int c2, ConvLayout* out, int schedule) {
+  // Default: split where a plan exists (shape allowed AND it fits TMEM/smem),
+  // else tap.
+  if (schedule == 0) return conv_plan(S, P, c1, c2, out, 2) || conv_plan(S, P, c1, c2, out, 1);
   if (P != 4 || S < P || S % P != 0 || (S * S) % 16 != 0) return false;
   if ((c1 != 32 && c1 != 64 && c1 != 128) || c2 < 32 || c2 % 32 != 0 || c2 > 256) return false;
   ConvLayout L;

@@ -118,6 +118,7 @@ bool DeviceMember::load(int device, const ModelSpec& model, int batch) {
     I.cnn = true;
     const char* cs = std::getenv("ES_CONV_SCHEDULE");  // tests: "tap" | "split"
     const int sched = cs && std::strcmp(cs, "tap") == 0 ? 1 : cs && std::strcmp(cs, "split") == 0 ? 2 : 0;
+    // ES_CONV_SCHEDULE=split falls back to tap where the shape has no split plan.
     if (!es::conv_plan(a.widths[0], a.widths[1], a.widths[2], a.widths[3], &I.conv, sched) &&
         !(sched == 2 && es::conv_plan(a.widths[0], a.widths[1], a.widths[2], a.widths[3], &I.conv, 1)))
       throw SpecError(model.name + ": CNN shape has no tile plan (patch 4, image side a "

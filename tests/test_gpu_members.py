@@ -74,8 +74,10 @@ def test_heterogeneous_depths_in_one_ensemble_match_reference_pipeline():
 
 
 # ------------------------------------------------------------------ K2 CNN
+# (28,4,64,32): split; (12,4,64,32): split on a 3x3 grid (R = 4);
+# (28,4,64,64): split allowed but no TMEM plan -> tap; the rest: tap.
 CNN_SHAPES = [(28, 4, 64, 32, 128, 10), (28, 4, 32, 64, 256, 10), (16, 4, 64, 32, 128, 10),
-              (28, 4, 128, 32, 1024, 10)]
+              (28, 4, 128, 32, 1024, 10), (12, 4, 64, 32, 128, 10), (28, 4, 64, 64, 128, 10)]
 
 
 @pytest.mark.parametrize("shape", CNN_SHAPES)
