@@ -404,7 +404,75 @@ __global__ void __launch_bounds__(128, 1) rate_two_issuers(int reps, int shifts_
   if (threadIdx.x < 32) tmem_dealloc(tmem, 512);
 }
 
+// The conv kernel's conv2 issuer: UMMAs of block r, then (after waiting for
+// block r-1's commit) block r-1's 12 shifts, one warp.
+__global__ void __launch_bounds__(128, 1) rate_issuer(int reps, unsigned long long* out) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align_smem_1024(smem_raw);
+  __shared__ uint64_t done[3];
+  __shared__ uint32_t slot;
+  for (int i = threadIdx.x; i < 96 * 1024 / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 3; ++i) mbar_init(&done[i], 1);
+    fence_barrier_init();
+  }
+  if (threadIdx.x < 32) tmem_alloc(&slot, 512);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
+  if (warp == 0) {
+    const uint32_t a = smem_u32(smem), b = smem_u32(smem + 40 * 1024);
+    const uint32_t idesc = idesc_bf16_f32(128, 96);
+    const uint64_t ad0 = sdesc_planar(a + 16 * 16, 4608), bd0 = sdesc_planar(b, 96 * 16);
+    const long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+      const int sl = r % 3;
+      const uint32_t d = tmem + 128u + static_cast<uint32_t>(sl * 96);
+#pragma unroll
+      for (int dhi = 0; dhi < 3; ++dhi)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint64_t ad = ad0 + static_cast<uint64_t>((dhi - 1) * 8 - 1 + j * 576);
+          const uint64_t bd = bd0 + static_cast<uint64_t>((dhi * 4 + j) * 2 * 96);
+          if (elect_one()) umma_bf16(d, ad, bd, idesc, (dhi | j) != 0);
+        }
+      if (elect_one()) umma_commit(&done[sl]);
+      __syncwarp();
+      if (r > 0) {
+        const int ps = (r - 1) % 3;
+        mbar_wait(&done[ps], static_cast<uint32_t>((r - 1) / 3) & 1u);
+        tc_fence_after();
+        const uint32_t dp = tmem + 128u + static_cast<uint32_t>(ps * 96);
+        for (int c = 0; c < 32; c += 8) {
+          if (elect_one()) tshift(dp + 32u + c);
+          if (elect_one()) tshift(dp + 64u + c);
+          if (elect_one()) tshift(dp + 64u + c);
+        }
+      }
+    }
+    mbar_wait(&done[(reps - 1) % 3], static_cast<uint32_t>((reps - 1) / 3) & 1u);
+    if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = static_cast<unsigned long long>(clock64() - t0);
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) tmem_dealloc(tmem, 512);
+}
+
 int main() {
+  {
+    unsigned long long* d;
+    cudaMalloc(&d, 8);
+    cudaFuncSetAttribute(rate_issuer, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    rate_issuer<<<148, 128, 100 * 1024>>>(60, d);
+    unsigned long long c = 0;
+    cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
+    std::printf("conv2 issuer pattern: %.1f clk per block %s\n", double(c) / 60,
+                cudaGetErrorString(cudaGetLastError()));
+    cudaFree(d);
+  }
   {
     unsigned long long* d;
     cudaMalloc(&d, 8);
