@@ -36,7 +36,8 @@ typedef enum es_status {
   ES_ERR_PROTOCOL = 7,         /* ProtocolError */
   ES_ERR_CUDA = 8,             /* CUDA failure other than out-of-memory */
   ES_ERR_INTERNAL = 9,
-  ES_ERR_BUFFER = 10           /* caller buffer too small */
+  ES_ERR_BUFFER = 10,          /* caller buffer too small */
+  ES_ERR_NOT_READY = 11        /* NotReadyError: service still loading or stopped (HTTP 503) */
 } es_status;
 
 /* DeviceSpec (types.hpp:17-26); ids are the array positions. */
@@ -334,6 +335,47 @@ es_status es_calibrate_cost_model(const es_cluster_desc* c, int device, size_t c
  * program name.  Report on stdout, errors on stderr; returns the exit code
  * (0 ok, 1 error, 2 allocation error). */
 int es_cli_main(int argc, const char* const* argv);
+
+/* ------------------------------------------------------------ deploy-mode service */
+/* The serving core of the reference's PredictionServer (src/server/server.cpp,
+ * SURVEY.md §8-F F1) without the HTTP listener: requests are buffered and
+ * flushed into one device run when a full segment is waiting or the oldest
+ * request has waited flush_timeout_ms (server.cpp:227-273); each request gets
+ * its own rows of the combined output back.  A caller's HTTP front end maps
+ * POST /v1/predict -> es_service_submit + es_request_wait and GET /v1/stats
+ * -> es_service_stats. */
+typedef struct es_service es_service;
+typedef struct es_request es_request;
+
+typedef struct es_service_info {
+  int ready;
+  uint64_t requests_served;
+  uint64_t samples_served;
+  uint64_t flushes;
+  double last_flush_throughput; /* samples/s over the last flush's device window */
+  size_t pending_requests;
+  size_t pending_samples;
+  double uptime_s;
+} es_service_info;
+
+/* Validates A (ES_ERR_SPEC if invalid, server.cpp:30-31) and starts building
+ * the device pool on a background thread (init_pool, server.cpp:37-52). */
+es_status es_service_create(const es_cluster_desc* c, const int* A, const es_rule_desc* rule,
+                            const es_pool_opts* opts, int flush_timeout_ms, size_t input_width,
+                            es_service** out);
+/* ready = 1 once the pool is up; error receives the startup error (if any). */
+es_status es_service_wait_ready(es_service* s, int timeout_ms, int* ready, char* error,
+                                size_t error_len);
+/* X: rows x input_width fp32 (copied before return).  rows = 0 completes at once. */
+es_status es_service_submit(es_service* s, const float* X, size_t rows, es_request** out);
+/* Blocks until the request's flush ran; Y: rows x output_width, winners: rows
+ * (either may be NULL).  ES_ERR_STARTUP if the pool failed, an error status
+ * with "server shutting down" if the service stopped first. */
+es_status es_request_wait(es_request* r, float* Y, int32_t* winners);
+void es_request_destroy(es_request* r);
+es_status es_service_stats(es_service* s, es_service_info* out);
+/* Stops the dispatcher (buffered requests fail) and releases the pool. */
+void es_service_destroy(es_service* s);
 
 #ifdef __cplusplus
 }

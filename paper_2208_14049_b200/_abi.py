@@ -52,6 +52,13 @@ class RunStats(C.Structure):
                 ("data_messages", C.c_size_t), ("elapsed_s", C.c_double)]
 
 
+class ServiceStatsC(C.Structure):
+    _fields_ = [("ready", C.c_int), ("requests_served", C.c_uint64),
+                ("samples_served", C.c_uint64), ("flushes", C.c_uint64),
+                ("last_flush_throughput", C.c_double), ("pending_requests", C.c_size_t),
+                ("pending_samples", C.c_size_t), ("uptime_s", C.c_double)]
+
+
 class BenchResultC(C.Structure):
     _fields_ = [("throughput", C.c_double), ("elapsed_s", C.c_double),
                 ("nb_samples", C.c_size_t), ("n_runs", C.c_int), ("runs", C.c_double * 64),
@@ -159,6 +166,16 @@ _SIGS = {
     "es_member_destroy": (None, [C.c_void_p]),
     "es_combine": (C.c_int, [C.POINTER(RuleDesc), C.c_int, C.c_int, C.c_size_t,
                              C.POINTER(c_float_p), c_float_p, c_int32_p]),
+    "es_service_create": (C.c_int, [C.POINTER(ClusterDesc), c_int_p, C.POINTER(RuleDesc),
+                                    C.POINTER(PoolOpts), C.c_int, C.c_size_t,
+                                    C.POINTER(C.c_void_p)]),
+    "es_service_wait_ready": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int), C.c_char_p,
+                                        C.c_size_t]),
+    "es_service_submit": (C.c_int, [C.c_void_p, c_float_p, C.c_size_t, C.POINTER(C.c_void_p)]),
+    "es_request_wait": (C.c_int, [C.c_void_p, c_float_p, c_int32_p]),
+    "es_request_destroy": (None, [C.c_void_p]),
+    "es_service_stats": (C.c_int, [C.c_void_p, C.POINTER(ServiceStatsC)]),
+    "es_service_destroy": (None, [C.c_void_p]),
 }
 
 EXPORTED = tuple(_SIGS)

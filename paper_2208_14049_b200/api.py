@@ -55,13 +55,17 @@ class DeviceError(EnserveError):
     """CUDA failure other than out-of-memory (no reference counterpart)."""
 
 
+class NotReadyError(EnserveError):
+    """The service is still loading or has stopped (the reference server's 503)."""
+
+
 class InvalidArgument(ValueError):
     """std::invalid_argument / std::out_of_range thrown by the reference."""
 
 
 _STATUS = {1: InvalidArgument, 2: SpecError, 3: AllocationError, 4: StartupError,
            5: BaselineError, 6: CapExceededError, 7: ProtocolError, 8: DeviceError,
-           9: EnserveError, 10: EnserveError}
+           9: EnserveError, 10: EnserveError, 11: NotReadyError}
 
 
 def _check(status: int) -> None:
@@ -812,6 +816,118 @@ def bench(A: AllocationMatrix, calib: SampleStore, cluster: ClusterSpec, repeats
         _check(lib().es_bench(d.ptr, A.ptr(), calib._h if calib is not None else None, repeats,
                               C.byref(_pool_opts(keep, **pool)), C.byref(r)))
     return BenchResult(r.throughput, r.elapsed_s, r.nb_samples, list(r.runs)[: r.n_runs], r.rsd)
+
+
+
+@dataclass
+class ServiceStats:
+    """GET /v1/stats (server.cpp:88-107)."""
+    ready: bool
+    requests_served: int
+    samples_served: int
+    flushes: int
+    last_flush_throughput: float
+    pending_requests: int
+    pending_samples: int
+    uptime_s: float
+
+
+class PendingPrediction:
+    """One POST /v1/predict in flight; result() blocks until its flush ran."""
+
+    def __init__(self, handle, rows: int, width: int):
+        self._h = handle
+        self.rows = rows
+        self._C = width
+        self._out = None
+
+    def result(self) -> tuple:
+        """(combined [rows, C] fp32, winners [rows] int32); raises the flush's error."""
+        if self._out is None:
+            Y = np.zeros((self.rows, self._C), dtype=np.float32)
+            W = np.zeros(self.rows, dtype=np.int32)
+            try:
+                _check(lib().es_request_wait(self._h, Y.ctypes.data_as(_abi.c_float_p),
+                                             W.ctypes.data_as(_abi.c_int32_p)))
+            finally:
+                lib().es_request_destroy(self._h)
+                self._h = None
+            self._out = (Y, W)
+        return self._out
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().es_request_destroy(self._h)
+            self._h = None
+
+
+class PredictionService:
+    """Deploy-mode serving core of PredictionServer (server.hpp:28-60,
+    server.cpp:65-288) without the HTTP listener.
+
+    Requests are buffered and flushed into one device run when a full segment is
+    waiting or the oldest request has waited `flush_timeout_ms`; each request
+    receives its own rows of the combined output."""
+
+    def __init__(self, cluster: ClusterSpec, A: AllocationMatrix,
+                 rule: CombinationRule = None, flush_timeout_ms: int = 50,
+                 input_width: int = None, **pool):
+        keep: list = []
+        rule = rule or CombinationRule.averaging()
+        self.input_width = int(input_width or cluster.models[0].input_width)
+        self.C = cluster.models[0].output_width
+        h = C.c_void_p()
+        with _Desc(cluster) as d:
+            _check(lib().es_service_create(d.ptr, A.ptr(), C.byref(rule._desc(keep)),
+                                           C.byref(_pool_opts(keep, **pool)),
+                                           int(flush_timeout_ms), self.input_width, C.byref(h)))
+        self._h = h
+
+    def wait_ready(self, timeout_s: float = 60.0) -> bool:
+        ready = C.c_int()
+        err = C.create_string_buffer(512)
+        _check(lib().es_service_wait_ready(self._h, int(timeout_s * 1000), C.byref(ready), err,
+                                           len(err)))
+        self.startup_error = err.value.decode() or None
+        return bool(ready.value)
+
+    def submit(self, samples: np.ndarray) -> PendingPrediction:
+        x = np.ascontiguousarray(samples, dtype=np.float32)
+        if x.size == 0:
+            x = x.reshape(0, self.input_width)
+        if x.ndim != 2 or x.shape[1] != self.input_width:  # server.cpp:118-135 -> 400
+            raise InvalidArgument(f"expected rows of {self.input_width} features, got shape "
+                                  f"{x.shape}")
+        r = C.c_void_p()
+        _check(lib().es_service_submit(self._h, x.ctypes.data_as(_abi.c_float_p), x.shape[0],
+                                       C.byref(r)))
+        return PendingPrediction(r, x.shape[0], self.C)
+
+    def predict(self, samples: np.ndarray) -> tuple:
+        """Blocking POST /v1/predict."""
+        return self.submit(samples).result()
+
+    def stats(self) -> ServiceStats:
+        st = _abi.ServiceStatsC()
+        _check(lib().es_service_stats(self._h, C.byref(st)))
+        return ServiceStats(bool(st.ready), st.requests_served, st.samples_served, st.flushes,
+                            st.last_flush_throughput, st.pending_requests, st.pending_samples,
+                            st.uptime_s)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib().es_service_destroy(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+        return False
+
+    def __del__(self):
+        self.close()
 
 
 class Member:

@@ -15,6 +15,7 @@
 #include "enserve/spec_io.hpp"
 #include "enserve/commands.hpp"
 #include "enserve/calibrate.hpp"
+#include "enserve/service.hpp"
 #include "enserve/placement.hpp"
 #include "enserve/rng.hpp"
 #include "enserve/runtime.hpp"
@@ -33,6 +34,16 @@ struct es_system {
 
 struct es_member {
   std::unique_ptr<B200Predictor> predictor;
+};
+
+struct es_service {
+  std::unique_ptr<enserve::PredictionService> svc;
+  int C = 0;
+};
+
+struct es_request {
+  std::future<enserve::RunOutput> fut;
+  std::size_t rows = 0;
 };
 
 // A parsed spec document: the ClusterSpec plus the C views es_spec_describe
@@ -69,6 +80,9 @@ es_status guard(F&& body) {
   } catch (const ProtocolError& e) {
     g_last_error = e.what();
     return ES_ERR_PROTOCOL;
+  } catch (const NotReadyError& e) {
+    g_last_error = e.what();
+    return ES_ERR_NOT_READY;
   } catch (const DeviceError& e) {
     g_last_error = e.what();
     return ES_ERR_CUDA;
@@ -907,6 +921,90 @@ es_status es_calibrate_cost_model(const es_cluster_desc* c, int device, size_t c
       for (std::size_t i = 0; i < meas.size(); ++i) measured_out[i] = meas[i].throughput;
     return ES_OK;
   });
+}
+
+
+// ------------------------------------------------------------ deploy-mode service
+es_status es_service_create(const es_cluster_desc* c, const int* A, const es_rule_desc* rule,
+                            const es_pool_opts* opts, int flush_timeout_ms, size_t input_width,
+                            es_service** out) {
+  return guard([&] {
+    need(out != nullptr, "out is NULL");
+    ClusterSpec cl = to_cluster(c);
+    ServiceConfig cfg;
+    cfg.flush_timeout_ms = flush_timeout_ms;
+    cfg.input_width = input_width;
+    cfg.rule = to_rule(rule, cl.model_count());
+    cfg.pool = to_opts(opts);
+    auto* s = new es_service();
+    s->C = cl.models.empty() ? 0 : cl.models[0].output_width;
+    try {
+      s->svc = std::make_unique<PredictionService>(cl, to_matrix(A, c->n_devices, c->n_models), cfg);
+    } catch (...) {
+      delete s;
+      throw;
+    }
+    *out = s;
+    return ES_OK;
+  });
+}
+
+es_status es_service_wait_ready(es_service* s, int timeout_ms, int* ready, char* error, size_t len) {
+  return guard([&] {
+    need(s != nullptr && ready != nullptr, "NULL argument");
+    *ready = s->svc->wait_ready(std::chrono::milliseconds(timeout_ms)) ? 1 : 0;
+    if (error && len) std::snprintf(error, len, "%s", s->svc->startup_error().c_str());
+    return ES_OK;
+  });
+}
+
+es_status es_service_submit(es_service* s, const float* X, size_t rows, es_request** out) {
+  return guard([&] {
+    need(s != nullptr && out != nullptr && (X != nullptr || rows == 0), "NULL argument");
+    auto* r = new es_request();
+    r->rows = rows;
+    r->fut = s->svc->submit(X, rows);
+    *out = r;
+    return ES_OK;
+  });
+}
+
+es_status es_request_wait(es_request* r, float* Y, int32_t* winners) {
+  return guard([&] {
+    need(r != nullptr, "NULL handle");
+    RunOutput out = r->fut.get();  // rethrows StartupError / Error
+    if (Y) std::memcpy(Y, out.combined.data(), out.combined.size() * sizeof(float));
+    if (winners)
+      for (std::size_t i = 0; i < out.winners.size(); ++i) winners[i] = out.winners[i];
+    return ES_OK;
+  });
+}
+
+void es_request_destroy(es_request* r) { delete r; }
+
+es_status es_service_stats(es_service* s, es_service_info* out) {
+  return guard([&] {
+    need(s != nullptr && out != nullptr, "NULL argument");
+    const ServiceStats st = s->svc->stats();
+    out->ready = st.ready ? 1 : 0;
+    out->requests_served = st.requests_served;
+    out->samples_served = st.samples_served;
+    out->flushes = st.flushes;
+    out->last_flush_throughput = st.last_flush_throughput;
+    out->pending_requests = st.pending_requests;
+    out->pending_samples = st.pending_samples;
+    out->uptime_s = st.uptime_s;
+    return ES_OK;
+  });
+}
+
+void es_service_destroy(es_service* s) {
+  if (!s) return;
+  try {
+    s->svc->stop();
+  } catch (...) {
+  }
+  delete s;
 }
 
 }  // extern "C"

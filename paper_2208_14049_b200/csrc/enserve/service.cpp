@@ -1,0 +1,159 @@
+// Deploy-mode prediction service (design in service.hpp).
+#include "enserve/service.hpp"
+
+#include <cstring>
+
+namespace enserve {
+
+PredictionService::PredictionService(ClusterSpec cluster, AllocationMatrix matrix,
+                                     ServiceConfig config)
+    : cluster_(std::move(cluster)), matrix_(std::move(matrix)), config_(std::move(config)) {
+  if (!validate_matrix(matrix_, cluster_).ok) throw SpecError("cannot serve an invalid matrix");
+  if (config_.input_width == 0) throw SpecError("input width must be positive");
+  started_at_ = std::chrono::steady_clock::now();
+  config_.pool.copy_outputs = true;
+  init_thread_ = std::thread([this] { init_pool(); });
+  dispatcher_ = std::thread([this] { dispatcher_loop(); });
+}
+
+PredictionService::~PredictionService() { stop(); }
+
+void PredictionService::init_pool() {
+  try {
+    system_ = std::make_unique<InferenceSystem>(matrix_, cluster_, config_.rule, config_.pool);
+    ready_.store(true);
+  } catch (const std::exception& e) {
+    std::lock_guard<std::mutex> lock(init_mutex_);
+    init_error_ = e.what();
+  }
+  {
+    std::lock_guard<std::mutex> lock(init_mutex_);
+    init_done_ = true;
+  }
+  init_cv_.notify_all();
+  buffer_cv_.notify_all();
+}
+
+bool PredictionService::wait_ready(std::chrono::milliseconds timeout) {
+  std::unique_lock<std::mutex> lock(init_mutex_);
+  init_cv_.wait_for(lock, timeout, [&] { return init_done_; });
+  return ready_.load();
+}
+
+std::string PredictionService::startup_error() const {
+  std::lock_guard<std::mutex> lock(init_mutex_);
+  return init_error_;
+}
+
+std::future<RunOutput> PredictionService::submit(const float* samples, std::size_t rows) {
+  auto p = std::make_shared<Pending>();
+  std::future<RunOutput> fut = p->promise.get_future();
+  if (rows == 0) {  // POST [] -> [] (server.cpp:124-127)
+    RunOutput empty;
+    empty.output_width = cluster_.models.empty() ? 0 : cluster_.models[0].output_width;
+    p->promise.set_value(std::move(empty));
+    return fut;
+  }
+  if (!ready_.load()) throw NotReadyError("service not ready");
+  p->rows = rows;
+  p->samples.assign(samples, samples + rows * config_.input_width);
+  {
+    std::lock_guard<std::mutex> lock(buffer_mutex_);
+    // Checked under the buffer lock: the dispatcher fails whatever it finds
+    // buffered after stopping_ flips, so an accepted request never hangs.
+    if (stopping_.load()) throw NotReadyError("server shutting down");
+    p->arrived = std::chrono::steady_clock::now();
+    buffer_.push_back(p);
+    buffered_samples_ += rows;
+  }
+  buffer_cv_.notify_all();
+  return fut;
+}
+
+void PredictionService::flush_locked(std::unique_lock<std::mutex>& lock) {
+  std::vector<std::shared_ptr<Pending>> batch(buffer_.begin(), buffer_.end());
+  buffer_.clear();
+  buffered_samples_ = 0;
+  lock.unlock();
+  std::size_t total = 0;
+  for (const auto& r : batch) total += r->rows;
+  std::vector<float> data;
+  data.reserve(total * config_.input_width);
+  for (const auto& r : batch) data.insert(data.end(), r->samples.begin(), r->samples.end());
+  try {
+    auto store = std::make_shared<SampleStore>(std::move(data), total, config_.input_width);
+    RunOutput out = system_->run(store);
+    if (out.stats.elapsed_s > 0) last_flush_throughput_.store(total / out.stats.elapsed_s);
+    samples_served_.fetch_add(total);
+    flushes_.fetch_add(1);
+    const std::size_t w = static_cast<std::size_t>(out.output_width);
+    std::size_t row = 0;
+    for (const auto& r : batch) {
+      RunOutput piece;
+      piece.output_width = out.output_width;
+      piece.combined.assign(out.combined.begin() + row * w, out.combined.begin() + (row + r->rows) * w);
+      if (!out.winners.empty())
+        piece.winners.assign(out.winners.begin() + row, out.winners.begin() + row + r->rows);
+      piece.stats = out.stats;
+      r->promise.set_value(std::move(piece));
+      requests_served_.fetch_add(1);
+      row += r->rows;
+    }
+  } catch (...) {
+    for (const auto& r : batch) r->promise.set_exception(std::current_exception());
+  }
+  lock.lock();
+}
+
+void PredictionService::dispatcher_loop() {
+  std::unique_lock<std::mutex> lock(buffer_mutex_);
+  while (!stopping_.load()) {
+    if (buffer_.empty()) {
+      buffer_cv_.wait(lock, [&] { return stopping_.load() || !buffer_.empty(); });
+      continue;
+    }
+    const auto deadline = buffer_.front()->arrived + std::chrono::milliseconds(config_.flush_timeout_ms);
+    const bool full = buffered_samples_ >= static_cast<std::size_t>(cluster_.segment_size);
+    if (!full && std::chrono::steady_clock::now() < deadline) {
+      buffer_cv_.wait_until(lock, deadline, [&] {
+        return stopping_.load() ||
+               buffered_samples_ >= static_cast<std::size_t>(cluster_.segment_size);
+      });
+      continue;
+    }
+    flush_locked(lock);
+  }
+  for (const auto& r : buffer_)  // so no client hangs
+    r->promise.set_exception(std::make_exception_ptr(NotReadyError("server shutting down")));
+  buffer_.clear();
+  buffered_samples_ = 0;
+}
+
+ServiceStats PredictionService::stats() const {
+  ServiceStats s;
+  s.ready = ready_.load();
+  s.requests_served = requests_served_.load();
+  s.samples_served = samples_served_.load();
+  s.flushes = flushes_.load();
+  s.last_flush_throughput = last_flush_throughput_.load();
+  {
+    std::lock_guard<std::mutex> lock(buffer_mutex_);
+    s.pending_requests = buffer_.size();
+    s.pending_samples = buffered_samples_;
+  }
+  s.uptime_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - started_at_).count();
+  return s;
+}
+
+void PredictionService::stop() {
+  bool expected = false;
+  if (!stopping_.compare_exchange_strong(expected, true)) return;
+  ready_.store(false);
+  { std::lock_guard<std::mutex> lock(buffer_mutex_); }  // no lost wake-up
+  buffer_cv_.notify_all();
+  if (dispatcher_.joinable()) dispatcher_.join();
+  if (init_thread_.joinable()) init_thread_.join();
+  if (system_) system_->shutdown();
+}
+
+}  // namespace enserve

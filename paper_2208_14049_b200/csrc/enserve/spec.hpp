@@ -43,6 +43,11 @@ struct StartupError : Error {
 struct ProtocolError : Error {
   using Error::Error;
 };
+// The deploy-mode service is not (or no longer) accepting requests: the
+// reference server's 503 (server.cpp:112-116, 281-287).
+struct NotReadyError : Error {
+  using Error::Error;
+};
 // A CUDA runtime failure other than out-of-memory (never swallowed by bench).
 struct DeviceError : Error {
   using Error::Error;
