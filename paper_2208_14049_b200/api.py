@@ -874,7 +874,12 @@ class PredictionService:
                  input_width: int = None, **pool):
         keep: list = []
         rule = rule or CombinationRule.averaging()
-        self.input_width = int(input_width or cluster.models[0].input_width)
+        if input_width is None:  # real members define it; synthetic ones need it given
+            arch = cluster.models[0].arch
+            if arch is None or arch.kind == "synthetic":
+                raise InvalidArgument("input_width is required for synthetic members")
+            input_width = arch.input_width()
+        self.input_width = int(input_width)
         self.C = cluster.models[0].output_width
         h = C.c_void_p()
         with _Desc(cluster) as d:

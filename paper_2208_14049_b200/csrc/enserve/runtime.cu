@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <mutex>
 
 #include "../cuda/aux_kernels.cuh"
@@ -364,6 +365,12 @@ void InferenceSystem::assign_shares(std::size_t nb) {
   }
 }
 
+bool InferenceSystem::single_device() const {
+  for (const auto& w : workers_)
+    if (w->phys != combine_dev_) return false;
+  return true;
+}
+
 std::vector<int> InferenceSystem::workers_per_model() const {
   std::vector<int> n(cluster_.model_count(), 0);
   for (const auto& w : workers_) ++n[w->model];
@@ -552,6 +559,68 @@ double InferenceSystem::last_combine_ms() const {
 // host conversion, which no CUDA event can see).
 double InferenceSystem::run_host(const float* X, std::size_t nb, std::size_t width, float* Y_out,
                                  std::int32_t* labels_out) {
+  // Chunk routes (DESIGN.md §e2e): "convert" = host threads write bf16 into a
+  // pinned slot, 2 B/feature cross PCIe; "direct" = DMA straight from the
+  // caller's pinned fp32 buffer, converted on the device (no host-memory
+  // pass).  Alternating them balances host-memory bandwidth against PCIe.
+  cudaPointerAttributes pa{};
+  const bool pinned_input =
+      cudaPointerGetAttributes(&pa, X) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+  cudaGetLastError();
+  const int mode = options_.e2e_host_convert ? (pinned_input ? 0 : 1) : (pinned_input ? 2 : 1);
+  const std::size_t k8 = static_cast<std::size_t>(std::clamp(options_.e2e_convert_eighths, 0, 8));
+  return run_host_core(nb, width, Y_out, labels_out,
+                       [&](std::size_t i, std::uint16_t* pinned, std::size_t r0,
+                           std::size_t rows) -> const float* {
+                         const bool convert =
+                             mode == 1 || (mode == 0 && (i + 1) * k8 / 8 > i * k8 / 8);
+                         if (!convert) return X + r0 * width;
+                         convert_f32_to_bf16_host(X + r0 * width, pinned, rows * width,
+                                                  *impl_->pool);
+                         return nullptr;
+                       });
+}
+
+double InferenceSystem::run_host_blocks(const std::vector<HostRowBlock>& blocks, std::size_t width,
+                                        float* Y_out, std::int32_t* labels_out) {
+  std::size_t nb = 0;
+  for (const HostRowBlock& b : blocks) nb += b.rows;
+  std::vector<std::size_t> first(blocks.size() + 1, 0);  // first row of every block
+  for (std::size_t k = 0; k < blocks.size(); ++k) first[k + 1] = first[k] + blocks[k].rows;
+  return run_host_core(nb, width, Y_out, labels_out,
+                       [&](std::size_t, std::uint16_t* pinned, std::size_t r0,
+                           std::size_t rows) -> const float* {
+                         // Gather rows [r0, r0 + rows) from the blocks, split over the pool.
+                         const std::function<void(int, int)> job = [&](int part, int parts) {
+                           const std::size_t per = (rows + parts - 1) / parts;
+                           const std::size_t a = r0 + std::min(rows, part * per);
+                           const std::size_t e = r0 + std::min(rows, (part + 1) * per);
+                           std::size_t k = std::upper_bound(first.begin(), first.end(), a) -
+                                           first.begin() - 1;
+                           for (std::size_t r = a; r < e; ++k) {
+                             const std::size_t take = std::min(e, first[k + 1]) - r;
+                             std::memcpy(pinned + (r - r0) * width,
+                                         blocks[k].bf16 + (r - first[k]) * width,
+                                         take * width * sizeof(std::uint16_t));
+                             r += take;
+                           }
+                         };
+                         impl_->pool->run(job);
+                         return nullptr;
+                       });
+}
+
+// End to end from host memory, pipelined over chunks of whole segments:
+//   host threads: fill(i) puts chunk i into a pinned slot as bf16 (2 B/feature
+//                 on the wire) — or returns a pinned fp32 source that is DMA'd
+//                 as is and converted on the device;
+//   copy stream:  H2D of chunk i while chunk i-1 computes;
+//   main stream:  member kernels + combine of chunk i into slot buffers;
+//   d2h stream:   combined probabilities + labels of chunk i back to the caller.
+// The returned time is host wall-clock around the whole call (it includes the
+// host conversion, which no CUDA event can see).
+double InferenceSystem::run_host_core(std::size_t nb, std::size_t width, float* Y_out,
+                                      std::int32_t* labels_out, const HostFill& fill) {
   for (const auto& w : workers_)
     if (w->phys != combine_dev_) throw SpecError("run_host needs every worker on one GPU");
   if (run_open_) throw Error("previous run still open");
@@ -565,15 +634,6 @@ double InferenceSystem::run_host(const float* X, std::size_t nb, std::size_t wid
   const int M = cluster_.model_count();
   const std::size_t seg = static_cast<std::size_t>(cluster_.segment_size);
   const std::size_t chunk = std::max<std::size_t>(seg, (options_.e2e_chunk_rows / seg) * seg);
-  // Chunk routes (DESIGN.md §e2e): "convert" = host threads write bf16 into a
-  // pinned slot, 2 B/feature cross PCIe; "direct" = DMA straight from the
-  // caller's pinned fp32 buffer, converted on the device (no host-memory
-  // pass).  Alternating them balances host-memory bandwidth against PCIe.
-  cudaPointerAttributes pa{};
-  const bool pinned_input =
-      cudaPointerGetAttributes(&pa, X) == cudaSuccess && pa.type == cudaMemoryTypeHost;
-  cudaGetLastError();
-  const int mode = options_.e2e_host_convert ? (pinned_input ? 0 : 1) : (pinned_input ? 2 : 1);
   constexpr int kSlots = 3;
   if (chunk * width > I.e2e_chunk_elems) {
     I.free_e2e();
@@ -606,23 +666,19 @@ double InferenceSystem::run_host(const float* X, std::size_t nb, std::size_t wid
     const std::size_t r0 = i * chunk;
     const std::size_t rows = std::min(chunk, nb - r0);
     const std::size_t elems = rows * width;
-    const std::size_t k8 = static_cast<std::size_t>(std::clamp(options_.e2e_convert_eighths, 0, 8));
-    const bool convert = mode == 1 || (mode == 0 && (i + 1) * k8 / 8 > i * k8 / 8);
     if (i >= kSlots) ES_CUDA(cudaEventSynchronize(sl.h2d_done));  // pinned slot reusable
-    if (convert)
-      convert_f32_to_bf16_host(X + r0 * width, static_cast<std::uint16_t*>(sl.pinned), elems,
-                               *I.pool);
+    const float* direct = fill(i, static_cast<std::uint16_t*>(sl.pinned), r0, rows);
     if (i >= kSlots) ES_CUDA(cudaStreamWaitEvent(I.copy, sl.d2h_done, 0));  // slot buffers free
-    h2d_bytes_ += elems * (convert ? 2 : sizeof(float));
+    h2d_bytes_ += elems * (direct ? sizeof(float) : 2);
     d2h_bytes_ += (Y_out ? rows * C * sizeof(float) : 0) + (labels_out ? rows * sizeof(int32_t) : 0);
-    if (convert)
+    if (!direct)
       ES_CUDA(cudaMemcpyAsync(sl.x16, sl.pinned, elems * 2, cudaMemcpyHostToDevice, I.copy));
     else
-      ES_CUDA(cudaMemcpyAsync(sl.x32, X + r0 * width, elems * sizeof(float),
-                              cudaMemcpyHostToDevice, I.copy));
+      ES_CUDA(cudaMemcpyAsync(sl.x32, direct, elems * sizeof(float), cudaMemcpyHostToDevice,
+                              I.copy));
     ES_CUDA(cudaEventRecord(sl.h2d_done, I.copy));
     ES_CUDA(cudaStreamWaitEvent(I.main, sl.h2d_done, 0));
-    if (!convert) {
+    if (direct) {
       ES_LAUNCH(es::convert_f32_to_bf16(sl.x32, static_cast<__nv_bfloat16*>(sl.x16), elems, I.main));
       ++launches_;
     }

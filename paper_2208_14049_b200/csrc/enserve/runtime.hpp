@@ -16,6 +16,7 @@
 #pragma once
 
 #include <cstdint>
+#include <functional>
 #include <memory>
 #include <optional>
 #include <string>
@@ -152,6 +153,17 @@ class InferenceSystem {
   // physical GPU only.
   double run_host(const float* X, std::size_t nb, std::size_t width, float* Y_out,
                   std::int32_t* labels_out);
+  // The same pipeline over rows already converted to bf16 and held in several
+  // host blocks (the deploy-mode service's buffered requests): each chunk is
+  // gathered into a pinned slot by the host pool, 2 B/feature cross PCIe.
+  struct HostRowBlock {
+    const std::uint16_t* bf16 = nullptr;  // rows x width
+    std::size_t rows = 0;
+  };
+  double run_host_blocks(const std::vector<HostRowBlock>& blocks, std::size_t width,
+                         float* Y_out, std::int32_t* labels_out);
+  // Every worker on one physical GPU (run_host / run_host_blocks apply).
+  bool single_device() const;
 
   int worker_count() const { return static_cast<int>(workers_.size()); }
   std::vector<int> workers_per_model() const;
@@ -173,6 +185,11 @@ class InferenceSystem {
 
  private:
   struct Worker;
+  // fill(chunk, pinned, first_row, rows): stage the chunk's bf16 rows in the
+  // pinned slot and return nullptr, or return a pinned fp32 source to DMA.
+  using HostFill = std::function<const float*(std::size_t, std::uint16_t*, std::size_t, std::size_t)>;
+  double run_host_core(std::size_t nb, std::size_t width, float* Y_out, std::int32_t* labels_out,
+                       const HostFill& fill);
   struct Impl;
   void assign_shares(std::size_t nb);
   AllocationMatrix matrix_;

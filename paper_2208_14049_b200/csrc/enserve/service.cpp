@@ -3,6 +3,8 @@
 
 #include <cstring>
 
+#include "enserve/host_convert.hpp"
+
 namespace enserve {
 
 PredictionService::PredictionService(ClusterSpec cluster, AllocationMatrix matrix,
@@ -21,6 +23,10 @@ PredictionService::~PredictionService() { stop(); }
 void PredictionService::init_pool() {
   try {
     system_ = std::make_unique<InferenceSystem>(matrix_, cluster_, config_.rule, config_.pool);
+    host_blocks_ = system_->single_device();
+    // Pinned slots, streams and the host pool up front (and the input width
+    // checked against the members), so the first flush pays none of it.
+    if (host_blocks_) system_->run_host_blocks({}, config_.input_width, nullptr, nullptr);
     ready_.store(true);
   } catch (const std::exception& e) {
     std::lock_guard<std::mutex> lock(init_mutex_);
@@ -56,7 +62,15 @@ std::future<RunOutput> PredictionService::submit(const float* samples, std::size
   }
   if (!ready_.load()) throw NotReadyError("service not ready");
   p->rows = rows;
-  p->samples.assign(samples, samples + rows * config_.input_width);
+  // The copy the request needs anyway doubles as the fp32 -> bf16 conversion
+  // (on the caller's thread, so it scales with the clients), halving what the
+  // flush gathers and sends over PCIe.
+  if (host_blocks_) {
+    p->bf16.resize(rows * config_.input_width);
+    convert_f32_to_bf16_range(samples, p->bf16.data(), p->bf16.size());
+  } else {
+    p->samples.assign(samples, samples + rows * config_.input_width);
+  }
   {
     std::lock_guard<std::mutex> lock(buffer_mutex_);
     // Checked under the buffer lock: the dispatcher fails whatever it finds
@@ -77,12 +91,29 @@ void PredictionService::flush_locked(std::unique_lock<std::mutex>& lock) {
   lock.unlock();
   std::size_t total = 0;
   for (const auto& r : batch) total += r->rows;
-  std::vector<float> data;
-  data.reserve(total * config_.input_width);
-  for (const auto& r : batch) data.insert(data.end(), r->samples.begin(), r->samples.end());
   try {
-    auto store = std::make_shared<SampleStore>(std::move(data), total, config_.input_width);
-    RunOutput out = system_->run(store);
+    RunOutput out;
+    if (host_blocks_) {
+      std::vector<InferenceSystem::HostRowBlock> blocks;
+      blocks.reserve(batch.size());
+      for (const auto& r : batch) blocks.push_back({r->bf16.data(), r->rows});
+      const int C = cluster_.models[0].output_width;
+      out.output_width = C;
+      out.combined.resize(total * static_cast<std::size_t>(C));
+      out.winners.resize(total);
+      static_assert(sizeof(int) == sizeof(std::int32_t), "winners are int32 on the wire");
+      out.stats.elapsed_s = system_->run_host_blocks(
+          blocks, config_.input_width, out.combined.data(),
+          reinterpret_cast<std::int32_t*>(out.winners.data()));
+      out.stats.nb_samples = total;
+      out.stats.segments = num_segments(total, cluster_.segment_size);
+    } else {
+      std::vector<float> data;
+      data.reserve(total * config_.input_width);
+      for (const auto& r : batch) data.insert(data.end(), r->samples.begin(), r->samples.end());
+      auto store = std::make_shared<SampleStore>(std::move(data), total, config_.input_width);
+      out = system_->run(store);
+    }
     if (out.stats.elapsed_s > 0) last_flush_throughput_.store(total / out.stats.elapsed_s);
     samples_served_.fetch_add(total);
     flushes_.fetch_add(1);

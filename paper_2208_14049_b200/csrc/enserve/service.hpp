@@ -62,7 +62,8 @@ class PredictionService {
 
  private:
   struct Pending {
-    std::vector<float> samples;
+    std::vector<float> samples;          // multi-GPU pools: fp32 rows for a SampleStore
+    std::vector<std::uint16_t> bf16;     // one-GPU pools: rows converted by the caller
     std::size_t rows = 0;
     std::chrono::steady_clock::time_point arrived;
     std::promise<RunOutput> promise;
@@ -76,6 +77,7 @@ class PredictionService {
   ServiceConfig config_;
   std::unique_ptr<InferenceSystem> system_;
   std::atomic<bool> ready_{false};
+  bool host_blocks_ = false;  // pool on one GPU: flush through run_host_blocks
   std::atomic<bool> stopping_{false};
   mutable std::mutex init_mutex_;
   std::condition_variable init_cv_;

@@ -34,7 +34,7 @@ def main():
     cluster = bench.make_cluster(es, cfg)
     # The matrix bench.py's greedy picks for cfg2 (profiles/r1i_bench.json).
     A = es.AllocationMatrix.from_array([[int(b) for b in args.matrix.split(",")]])
-    W = cluster.models[0].input_width
+    W = cluster.models[0].arch.input_width()
     rng = np.random.default_rng(0)
     pool = [rng.random((args.rows, W), dtype=np.float32) for _ in range(4)]
     lat: list = []
