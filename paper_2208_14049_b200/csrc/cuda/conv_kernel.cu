@@ -22,9 +22,10 @@ namespace {
 // issue loop down (measured with tools/trace_conv.cu).
 constexpr int kThreads = 320;
 // split schedule: four more conv2-epilogue warps (10-13), see epi2_split.
-template <bool SPLIT>
+template <int SPLIT>
 constexpr int threads_for() { return SPLIT ? 480 : kThreads; }  // split: + warp 14, the conv2 issuer
 constexpr uint32_t kSmemBudget = 232448;
+constexpr int kShiftPipe = 0, kShiftShfl = 1, kShiftHybrid = 2;  // ConvArgs::shifts
 constexpr int kMargin = 16;  // zero rows before/after the tile's grids; taps reach R+1 rows
 
 // bf16x2 {relu(a + ba), relu(b + bb)} (a in the low half), one cvt.relu.
@@ -49,8 +50,11 @@ __device__ __forceinline__ unsigned long long global_ns() {
   } while (0)
 
 // KP2 = c1 / 16: K steps per tap, unrolled so the issue loop is pure uniform
-// adds (tools/umma_rate.cu).  SPLIT: the conv2 schedule (conv_kernel.cuh).
-template <int KP2, bool SPLIT>
+// adds (tools/umma_rate.cu).  SPLIT: 0 = tap schedule, else the split
+// schedule with ConvArgs::shifts = SPLIT - 1 (conv_kernel.cuh), a template
+// argument because a runtime switch in the issue and epilogue loops measured
+// 50 % slower.
+template <int KP2, int SPLIT>
 __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
     conv_stack_sm100(const __grid_constant__ CUtensorMap tm_x, const ConvArgs args) {
   extern __shared__ uint8_t smem_raw[];
@@ -62,7 +66,6 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
   uint8_t* sW1 = smem + L.off_w1;
   uint8_t* sW2 = smem + L.off_w2;
   float* sB1 = reinterpret_cast<float*>(smem + L.off_b1);
-  float* sB2 = reinterpret_cast<float*>(smem + L.off_b2);
   int* sRowOff = reinterpret_cast<int*>(smem + L.off_rows);  // im2col source offset per row
   int* sGrow = sRowOff + L.T * L.G * L.G;  // conv1 output row -> grid row
   int* sOut = sGrow + L.T * L.G * L.G;     // grid row -> (sample << 24 | byte offset), -1 = border
@@ -137,7 +140,6 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
       sOut[r] = (r < L.T * P2r && h >= 1 && w < L.G) ? (n << 24) | (((h - 1) * L.G + w) * L.c2 * 2) : -1;
     }
     for (int i = threadIdx.x; i < L.c1; i += threads_for<SPLIT>()) sB1[i] = args.b1[i];
-    for (int i = threadIdx.x; i < L.c2; i += threads_for<SPLIT>()) sB2[i] = args.b2[i];
     uint4* z = reinterpret_cast<uint4*>(sA2);
     for (int i = threadIdx.x; i < static_cast<int>(2 * L.a2_bytes / 16); i += threads_for<SPLIT>())
       z[i] = make_uint4(0, 0, 0, 0);
@@ -232,25 +234,26 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
       }
       __syncwarp();
     };
-    // split: warp 14 issues conv2's UMMAs AND its lane shifts.  tcgen05.shift
-    // is not ordered behind in-flight UMMAs on the same columns (measured:
-    // shifting right after the UMMAs reads partial sums), so a block's shifts
-    // go out after the NEXT block's UMMAs are queued, once its own UMMA commit
-    // has landed -- the pipe never drains, and UMMAs + shifts come from one
-    // issuer (two issuers cost ~25 %, tools/umma_rate.cu).  Warp 1 issues only
-    // the few conv1 UMMAs.
+    // split: warp 14 issues conv2's UMMAs and the tensor-pipe lane shifts of
+    // args.shifts (conv_kernel.cuh).  tcgen05.shift is not ordered behind
+    // in-flight UMMAs on the same columns (measured: shifting right after the
+    // UMMAs reads partial sums), so a block's shifts go out after the NEXT
+    // block's UMMAs are queued, once its own UMMA commit has landed -- the
+    // pipe never drains, and UMMAs + shifts come from one issuer (two issuers
+    // cost ~25 %, tools/umma_rate.cu).  Warp 1 issues only the conv1 UMMAs.
+    constexpr int shifts = SPLIT - 1;
     int pend_blk = -1;
     auto shift_block = [&](int blk) {
       const int sl = blk % 3;
       mbar_sleep_wait(&mma_done[sl], static_cast<uint32_t>(blk / 3) & 1u);
       tc_fence_after();
       const uint32_t d = tbase + static_cast<uint32_t>(L.tmem_c1 + sl * L.n2);
-      // out[q] = D'[q][dw=-1] + D'[q+1][dw=0] + D'[q+2][dw=+1]: pull the dw=0
-      // columns one lane, the dw=+1 columns two lanes toward lane 0.
       for (int c = 0; c < L.c2; c += 8) {
-        if (elect_one()) tmem_shift_down(d + static_cast<uint32_t>(L.c2 + c));
+        if constexpr (shifts == kShiftPipe)
+          if (elect_one()) tmem_shift_down(d + static_cast<uint32_t>(L.c2 + c));
         if (elect_one()) tmem_shift_down(d + static_cast<uint32_t>(2 * L.c2 + c));
-        if (elect_one()) tmem_shift_down(d + static_cast<uint32_t>(2 * L.c2 + c));
+        if constexpr (shifts == kShiftPipe)
+          if (elect_one()) tmem_shift_down(d + static_cast<uint32_t>(2 * L.c2 + c));
       }
       if (elect_one()) umma_commit(&c2_full[sl]);
       __syncwarp();
@@ -281,13 +284,15 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
             if (elect_one()) umma_bf16(d, ad, bd, id2, (dhi | j) != 0);
           }
         if (elect_one()) {
-          umma_commit(&mma_done[sl]);
+          umma_commit(shifts == kShiftShfl ? &c2_full[sl] : &mma_done[sl]);
           if (mb == L.mb2 - 1) umma_commit(&a2_empty[b]);
         }
         __syncwarp();
         TRACE(k, 11 + 3 * mb);
-        if (pend_blk >= 0) shift_block(pend_blk);
-        pend_blk = blk;
+        if constexpr (shifts != kShiftShfl) {
+          if (pend_blk >= 0) shift_block(pend_blk);
+          pend_blk = blk;
+        }
       }
       TRACE(k, 3);
     };
@@ -429,14 +434,17 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
     const int q = warp & 3;
     const uint32_t lane_field = static_cast<uint32_t>(q * 32) << 16;
     const int row_bytes = G2 * L.c2 * 2;
-    // split: the tensor pipe already moved the dw = 0 / +1 partials onto the
-    // output's lane (conv_kernel.cuh), so out = g(-1) + g(0) + g(+1) per lane.
-    // Lane 30 of a quadrant needs lane 32's dw=+1 partial, which the in-quadrant
-    // shift cannot fetch: that partial is zero (it reads the border column).
-    // Warps 10-13, every channel, 16 at a time.
+    // split: out[q] = D'[q][-1] + D'[q+1][0] + D'[q+2][+1] (conv_kernel.cuh),
+    // the lane moves split between the tensor pipe and shuffles by
+    // args.shifts.  Lane 30 would need lane 32's dw=+1 partial, which lies in
+    // the next quadrant: it is zero (it reads the border column); lane 31 is
+    // itself a border pixel and is not stored.  Warps 10-13, every channel,
+    // 16 at a time.
     auto epi2_split = [&](int k) {
       const long long s0 = args.row_begin + (blockIdx.x + static_cast<long long>(k) * gridDim.x) * L.T;
+      constexpr int shifts = SPLIT - 1;
       const float keep_p1 = lane == 30 ? 0.0f : 1.0f;
+      const float keep_31 = lane == 31 ? 0.0f : 1.0f;  // kShiftHybrid: u[31] takes no dw=+1 term
       for (int mb = 0; mb < L.mb2; ++mb) {
         const int blk = k * L.mb2 + mb, sl = blk % 3;
         const uint32_t ph = static_cast<uint32_t>(blk / 3) & 1u;
@@ -462,14 +470,26 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
           }
           float v[16];
 #pragma unroll
-          for (int c = 0; c < 16; ++c)
-            v[c] = __uint_as_float(r0[c]) + __uint_as_float(r1[c]) + keep_p1 * __uint_as_float(r2[c]);
+          for (int c = 0; c < 16; ++c) {
+            if constexpr (shifts == kShiftPipe) {  // both partials already on this lane
+              v[c] = __uint_as_float(r0[c]) + __uint_as_float(r1[c]) + keep_p1 * __uint_as_float(r2[c]);
+            } else if constexpr (shifts == kShiftShfl) {
+              const uint32_t g0 = __shfl_down_sync(0xffffffffu, r1[c], 1);
+              const uint32_t g1 = __shfl_down_sync(0xffffffffu, r2[c], 2);
+              v[c] = __uint_as_float(r0[c]) + __uint_as_float(g0) + keep_p1 * __uint_as_float(g1);
+            } else {  // dw=+1 moved one lane by the pipe: u[p] = D'[p][0] + D'[p+1][+1]
+              const float u = __uint_as_float(r1[c]) + keep_31 * __uint_as_float(r2[c]);
+              v[c] = __uint_as_float(r0[c]) + __shfl_down_sync(0xffffffffu, u, 1);
+            }
+          }
           if (valid && !(args.debug & 16)) {
 #pragma unroll
             for (int g = 0; g < 2; ++g) {
               const int c = g * 8;
-              const float4 bl = *reinterpret_cast<const float4*>(sB2 + c0 + c);
-              const float4 bh = *reinterpret_cast<const float4*>(sB2 + c0 + c + 4);
+              const float4 bl = make_float4(args.b2c[c0 + c], args.b2c[c0 + c + 1],
+                                            args.b2c[c0 + c + 2], args.b2c[c0 + c + 3]);
+              const float4 bh = make_float4(args.b2c[c0 + c + 4], args.b2c[c0 + c + 5],
+                                            args.b2c[c0 + c + 6], args.b2c[c0 + c + 7]);
               const uint4 pk = make_uint4(
                   pack_relu_bf16(__float_as_uint(v[c]), __float_as_uint(v[c + 1]), bl.x, bl.y),
                   pack_relu_bf16(__float_as_uint(v[c + 2]), __float_as_uint(v[c + 3]), bl.z, bl.w),
@@ -512,8 +532,10 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
 #pragma unroll
             for (int g = 0; g < 4; ++g) {
               const int c = g * 8;
-              const float4 bl = *reinterpret_cast<const float4*>(sB2 + c0 + c);
-              const float4 bh = *reinterpret_cast<const float4*>(sB2 + c0 + c + 4);
+              const float4 bl = make_float4(args.b2c[c0 + c], args.b2c[c0 + c + 1],
+                                            args.b2c[c0 + c + 2], args.b2c[c0 + c + 3]);
+              const float4 bh = make_float4(args.b2c[c0 + c + 4], args.b2c[c0 + c + 5],
+                                            args.b2c[c0 + c + 6], args.b2c[c0 + c + 7]);
               const uint4 pk = make_uint4(pack_relu_bf16(v[c], v[c + 1], bl.x, bl.y),
                                           pack_relu_bf16(v[c + 2], v[c + 3], bl.z, bl.w),
                                           pack_relu_bf16(v[c + 4], v[c + 5], bh.x, bh.y),
@@ -567,8 +589,8 @@ bool conv_plan(int S, int P, int c1, int c2, ConvLayout* out, int schedule) {
   const bool split_ok = 3 * c2 <= 256 && 32 % L.R == 0 && c1 == 64;
   if (schedule == 2 && !split_ok) return false;
   // Measured on B200 (tools/trace_conv.cu, 2^20 CNN-s samples): split 2.63 ms
-  // (one conv1 TMEM buffer + a 3-slot conv2 ring, conv2 UMMAs and shifts from
-  // one issuer warp with the shifts one block behind, 8 conv1-epilogue warps,
+  // (one conv1 TMEM buffer + a 3-slot conv2 ring, conv2 UMMAs from one
+  // issuer warp, lane shifts as epilogue shuffles, 8 conv1-epilogue warps,
   // row-address tables instead of divisions), tap 3.77 ms.
   L.split = split_ok && schedule != 1;
   L.n2 = L.split ? 3 * c2 : c2;
@@ -630,13 +652,19 @@ int conv_launch(const ConvArgs& args, const void* x, long long x_rows, int grid,
                                                                                                 args);
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
   };
-  switch (L.c1 * 2 + (L.split ? 1 : 0)) {
-    case 64: return go(conv_stack_sm100<2, false>);
-    case 65: return go(conv_stack_sm100<2, true>);
-    case 128: return go(conv_stack_sm100<4, false>);
-    case 129: return go(conv_stack_sm100<4, true>);
-    case 256: return go(conv_stack_sm100<8, false>);
-    case 257: return go(conv_stack_sm100<8, true>);
+  if (L.split) {  // split plans have c1 = 64 (conv_plan)
+    if (L.c1 != 64) return -1;
+    switch (args.shifts) {
+      case kShiftPipe: return go(conv_stack_sm100<4, 1 + kShiftPipe>);
+      case kShiftShfl: return go(conv_stack_sm100<4, 1 + kShiftShfl>);
+      case kShiftHybrid: return go(conv_stack_sm100<4, 1 + kShiftHybrid>);
+      default: return -1;
+    }
+  }
+  switch (L.c1) {
+    case 32: return go(conv_stack_sm100<2, 0>);
+    case 64: return go(conv_stack_sm100<4, 0>);
+    case 128: return go(conv_stack_sm100<8, 0>);
     default: return -1;
   }
 }

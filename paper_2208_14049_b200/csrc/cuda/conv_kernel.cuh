@@ -35,13 +35,13 @@
 //     per block instead of 36 of N = 32.  Column group dw of accumulator row
 //     p then holds D'[p][dw] = sum_dh X[p - 1 + dh*R] W(dh, dw), and
 //         out[q] = D'[q][-1] + D'[q+1][0] + D'[q+2][+1],
-//     a lane shift the tensor pipe does itself: tcgen05.shift moves the dw=0
-//     columns one lane and the dw=+1 columns two lanes toward lane 0 (within
-//     each 32-lane quadrant).  With the grid's border column LAST in a row
-//     (w = G), a quadrant's lane 31 is a border pixel and lane 30's missing
-//     dw=+1 partial (lane 32's) reads only the border column, i.e. is zero --
-//     so the epilogue is a lane-local sum.  The default where the shape
-//     allows it (measured faster than tap, conv_plan).
+//     a lane shift within each 32-lane quadrant (ConvArgs::shifts: by
+//     tcgen05.shift in the tensor pipe, by warp shuffles in the epilogue
+//     warp that reads the quadrant, or split between the two).  With the
+//     grid's border column LAST in a row (w = G), a quadrant's lane 31 is a
+//     border pixel and lane 30's missing dw=+1 partial (lane 32's) reads only
+//     the border column, i.e. is zero.  The default where the shape allows
+//     it (measured faster than tap, conv_plan).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -75,6 +75,18 @@ struct ConvArgs {
   const float* b1 = nullptr;
   const void* w2 = nullptr;  // bf16 [c2][9*c1], K index = tap*c1 + channel, tap = 3*(dh+1)+(dw+1)
   const float* b2 = nullptr;
+  // conv2 bias by value (kernel parameter space = constant cache): the conv2
+  // epilogue's per-channel bias reads are uniform across lanes, and shared
+  // memory reads queue behind the UMMAs' operand reads (tools/umma_contention.cu).
+  float b2c[256] = {};
+  // split: who moves the dw partials onto the output's lane -- 0: the tensor
+  // pipe (tcgen05.shift: dw=0 one lane, dw=+1 two lanes, 12 ops per block);
+  // 1: the epilogue (two shuffles per value); 2: both (dw=+1 one lane in the
+  // pipe, then one shuffle of D'[p][0] + D'[p+1][+1]).  Measured on B200
+  // (tools/trace_conv.cu, 2^20 samples): 2.67 / 2.92 / 2.62 ms.  The conv2
+  // epilogue (4 warps, ~0.6 us per 128-row block) gates the issuer through
+  // the 3-slot TMEM ring in every mode; the tensor pipe is ~55 % busy.
+  int shifts = 2;
   void* out = nullptr;  // bf16 [rows][G*G*c2]
   // Design evidence (tools/trace_conv.cu): globaltimer stamps of CTA 0's
   // first 32 tiles, [tile][16]; nullptr in the product.

@@ -76,6 +76,7 @@ struct DeviceMember::Impl {
   es::ConvLayout conv{};  // CNN: the convolution stack (layers 0 and 1)
   void* weights = nullptr;
   std::vector<std::size_t> w_off, b_off;  // per layer
+  std::vector<float> conv_b2;               // CNN: conv2 bias, host copy
   // Outputs of the leading layers, bf16 [rows][width], indexed like X.
   std::vector<void*> act;
   std::vector<int> act_width;
@@ -196,6 +197,11 @@ bool DeviceMember::load(int device, const ModelSpec& model, int batch) {
   I.act.assign(I.act_width.size(), nullptr);
   I.act_rows.assign(I.act_width.size(), 0);
   M_CUDA(cudaDeviceSynchronize());
+  if (I.cnn) {  // conv2 bias travels by value in the launch parameters (conv_kernel.cuh)
+    I.conv_b2.resize(static_cast<std::size_t>(I.dims[1].second));
+    M_CUDA(cudaMemcpy(I.conv_b2.data(), base + I.b_off[1], I.conv_b2.size() * sizeof(float),
+                      cudaMemcpyDeviceToHost));
+  }
   return true;
 }
 
@@ -253,6 +259,7 @@ int DeviceMember::forward(const void* x, long long nb, int seg_size, long long s
     c.b1 = reinterpret_cast<const float*>(base + I.b_off[0]);
     c.w2 = base + I.w_off[1];
     c.b2 = reinterpret_cast<const float*>(base + I.b_off[1]);
+    std::copy(I.conv_b2.begin(), I.conv_b2.end(), c.b2c);
     c.out = I.act[0];
     M_LAUNCH(es::conv_launch(c, cur, nb, grid, stream));
     mark(launches++);

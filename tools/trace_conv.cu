@@ -19,6 +19,7 @@ int main(int argc, char** argv) {
   const int c2 = argc > 2 ? std::atoi(argv[2]) : 32;
   const int sched = argc > 3 ? std::atoi(argv[3]) : 0;  // conv_plan schedule
   const int debug = argc > 4 ? std::atoi(argv[4]) : 0;  // ConvArgs::debug bits
+  const int shifts = argc > 5 ? std::atoi(argv[5]) : -1;  // ConvArgs::shifts (-1 = default)
   const long long nb = 1 << 20;
   const int S = 28, P = 4, G = 7;
   __nv_bfloat16 *x, *w1, *w2, *y;
@@ -48,6 +49,9 @@ int main(int argc, char** argv) {
   a.b1 = b1;
   a.w2 = w2;
   a.b2 = b2;
+  if (shifts >= 0) a.shifts = shifts;
+  cudaDeviceSynchronize();
+  cudaMemcpy(a.b2c, b2, c2 * sizeof(float), cudaMemcpyDeviceToHost);
   a.out = y;
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
