@@ -97,6 +97,9 @@ typedef struct es_pool_opts {
                             0 = every chunk DMA'd as fp32 (pinned X) */
   int e2e_convert_eighths; /* with e2e_host_convert and pinned X: chunks in 8 the
                               host converts (0 = default 6) */
+  int dp_equal_split;      /* 0 = a model's data-parallel workers split its segments in
+                              runs proportional to their probed rows/s (SURVEY.md §8-E
+                              static fallback of the shared FIFO); 1 = equal runs */
 } es_pool_opts;
 
 /* RunStats (pipeline.hpp:19-25). */
@@ -141,6 +144,12 @@ es_status es_segment_bounds(int segment_id, int segment_size, size_t nb, size_t*
  * split): out[4*i..] = {device, model, first segment, end segment}. */
 es_status es_segment_shares(const int* A, int devices, int models, size_t nb, int segment_size,
                             long long* out, int cap, int* n);
+/* The same with each model's runs proportional to weight[w] (one per worker,
+ * row-major cells, > 0): what InferenceSystem uses with probed rows/s
+ * (SURVEY.md §8-E static fallback).  Equal weights give es_segment_shares. */
+es_status es_segment_shares_weighted(const int* A, int devices, int models, size_t nb,
+                                     int segment_size, const double* weight, long long* out,
+                                     int cap, int* n);
 /* fit_mem (src/memory/memory_model.cpp:22-32); used_mib[D]. */
 es_status es_fit_mem(const es_cluster_desc* c, const int* A, double* used_mib, int* fits);
 /* more_remaining_memory (memory_model.cpp:34-50); *device = -1 when none. */
@@ -237,6 +246,11 @@ es_status es_system_info(es_system* s, int* workers, int* workers_per_model, int
                          int* combine_device);
 /* Device time of each worker's member kernel and of the combine, last run. */
 es_status es_system_timing(es_system* s, double* member_ms, double* combine_ms);
+/* Segment runs of every worker (row-major cells) in the last run:
+ * shares[2w] = begin, shares[2w+1] = end; rates[w] = probed rows/s of a
+ * data-parallel worker (1.0 for a model's only worker, or before any run).
+ * Either array may be NULL; each holds the worker count of es_system_info. */
+es_status es_system_shares(es_system* s, int64_t* shares, double* rates);
 /* Host<->device bytes the last es_system_run_host moved. */
 es_status es_system_last_transfer(es_system* s, size_t* h2d_bytes, size_t* d2h_bytes);
 /* Per-launch device time of one worker's member kernels in the last run

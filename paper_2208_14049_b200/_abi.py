@@ -44,7 +44,8 @@ class PoolOpts(C.Structure):
     _fields_ = [("device_map", c_int_p), ("n_device_map", C.c_int), ("copy_outputs", C.c_int),
                 ("warmup", C.c_int), ("sms_per_worker", C.c_int),
                 ("overlap_colocated", C.c_int), ("e2e_chunk_rows", C.c_size_t),
-                ("e2e_host_convert", C.c_int), ("e2e_convert_eighths", C.c_int)]
+                ("e2e_host_convert", C.c_int), ("e2e_convert_eighths", C.c_int),
+                ("dp_equal_split", C.c_int)]
 
 
 class RunStats(C.Structure):
@@ -114,6 +115,9 @@ _SIGS = {
     "es_segment_bounds": (C.c_int, [C.c_int, C.c_int, C.c_size_t, c_size_t_p, c_size_t_p]),
     "es_segment_shares": (C.c_int, [c_int_p, C.c_int, C.c_int, C.c_size_t, C.c_int,
                                     C.POINTER(C.c_longlong), C.c_int, c_int_p]),
+    "es_segment_shares_weighted": (C.c_int, [c_int_p, C.c_int, C.c_int, C.c_size_t, C.c_int,
+                                             c_double_p, C.POINTER(C.c_longlong), C.c_int,
+                                             c_int_p]),
     "es_fit_mem": (C.c_int, [C.POINTER(ClusterDesc), c_int_p, c_double_p, c_int_p]),
     "es_more_remaining_memory": (C.c_int, [C.POINTER(ClusterDesc), c_int_p, C.c_int, c_int_p]),
     "es_predict_ensemble_throughput": (C.c_int, [C.POINTER(ClusterDesc), c_int_p, c_double_p]),
@@ -166,6 +170,7 @@ _SIGS = {
     "es_member_destroy": (None, [C.c_void_p]),
     "es_combine": (C.c_int, [C.POINTER(RuleDesc), C.c_int, C.c_int, C.c_size_t,
                              C.POINTER(c_float_p), c_float_p, c_int32_p]),
+    "es_system_shares": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64), c_double_p]),
     "es_service_create": (C.c_int, [C.POINTER(ClusterDesc), c_int_p, C.POINTER(RuleDesc),
                                     C.POINTER(PoolOpts), C.c_int, C.c_size_t,
                                     C.POINTER(C.c_void_p)]),

@@ -339,13 +339,19 @@ def segment_bounds(segment_id: int, segment_size: int, nb: int) -> tuple:
     return s.value, e.value
 
 
-def segment_shares(A: AllocationMatrix, nb: int, segment_size: int) -> list:
-    """[(device, model, first_segment, end_segment)] per worker, row-major."""
+def segment_shares(A: AllocationMatrix, nb: int, segment_size: int, weights=None) -> list:
+    """[(device, model, first_segment, end_segment)] per worker, row-major;
+    with `weights` (one per worker) a model's runs are proportional to them."""
     cap = max(A.worker_count(), 1)
     out = (C.c_longlong * (4 * cap))()
     n = C.c_int()
-    _check(lib().es_segment_shares(A.ptr(), A.device_count(), A.model_count(), nb, segment_size,
-                                   out, cap, C.byref(n)))
+    if weights is None:
+        _check(lib().es_segment_shares(A.ptr(), A.device_count(), A.model_count(), nb,
+                                       segment_size, out, cap, C.byref(n)))
+    else:
+        w = (C.c_double * cap)(*[float(x) for x in weights])
+        _check(lib().es_segment_shares_weighted(A.ptr(), A.device_count(), A.model_count(), nb,
+                                                segment_size, w, out, cap, C.byref(n)))
     return [tuple(out[4 * i: 4 * i + 4]) for i in range(n.value)]
 
 
@@ -591,7 +597,8 @@ class CombinationRule:
 
 def _pool_opts(keep: list, device_map=None, copy_outputs=True, warmup=True,
                sms_per_worker=0, overlap_colocated=False, e2e_chunk_rows=0,
-               e2e_host_convert=True, e2e_convert_eighths=0) -> _abi.PoolOpts:
+               e2e_host_convert=True, e2e_convert_eighths=0,
+               dp_equal_split=False) -> _abi.PoolOpts:
     """PoolOptions (runtime.hpp)."""
     dm = None
     n = 0
@@ -601,7 +608,8 @@ def _pool_opts(keep: list, device_map=None, copy_outputs=True, warmup=True,
         n = len(device_map)
     o = _abi.PoolOpts(C.cast(dm, _abi.c_int_p) if dm is not None else None, n, int(copy_outputs),
                       int(warmup), int(sms_per_worker), int(overlap_colocated),
-                      int(e2e_chunk_rows), int(e2e_host_convert), int(e2e_convert_eighths))
+                      int(e2e_chunk_rows), int(e2e_host_convert), int(e2e_convert_eighths),
+                      int(dp_equal_split))
     keep.append(o)
     return o
 
@@ -705,6 +713,15 @@ class InferenceSystem:
         cm = C.c_double()
         _check(lib().es_system_timing(self._h, ms, C.byref(cm)))
         return list(ms)[:w], cm.value
+
+    def shares(self) -> tuple:
+        """([(begin, end)] segment runs per worker in the last run, [rows/s]
+        probed per data-parallel worker; 1.0 for single workers)."""
+        w = self.worker_count()
+        sh = (C.c_int64 * max(2 * w, 1))()
+        r = (C.c_double * max(w, 1))()
+        _check(lib().es_system_shares(self._h, sh, r))
+        return [(sh[2 * i], sh[2 * i + 1]) for i in range(w)], list(r)[:w]
 
     def last_transfer(self) -> tuple:
         """(h2d_bytes, d2h_bytes) moved by the last run_host."""

@@ -179,6 +179,7 @@ PoolOptions to_opts(const es_pool_opts* o) {
   if (o->e2e_chunk_rows > 0) p.e2e_chunk_rows = o->e2e_chunk_rows;
   p.e2e_host_convert = o->e2e_host_convert != 0;
   if (o->e2e_convert_eighths > 0) p.e2e_convert_eighths = o->e2e_convert_eighths;
+  p.dp_equal_split = o->dp_equal_split != 0;
   return p;
 }
 
@@ -277,6 +278,25 @@ es_status es_segment_shares(const int* A, int devices, int models, size_t nb, in
                             long long* out, int cap, int* n) {
   return guard([&] {
     std::vector<SegmentShare> s = segment_shares(to_matrix(A, devices, models), nb, segment_size);
+    *n = static_cast<int>(s.size());
+    for (int i = 0; out && i < *n && i < cap; ++i) {
+      out[4 * i + 0] = s[i].device;
+      out[4 * i + 1] = s[i].model;
+      out[4 * i + 2] = s[i].begin;
+      out[4 * i + 3] = s[i].end;
+    }
+    return ES_OK;
+  });
+}
+
+es_status es_segment_shares_weighted(const int* A, int devices, int models, size_t nb,
+                                     int segment_size, const double* weight, long long* out,
+                                     int cap, int* n) {
+  return guard([&] {
+    need(weight != nullptr, "NULL weights");
+    const AllocationMatrix M = to_matrix(A, devices, models);
+    std::vector<double> w(weight, weight + M.worker_count());
+    std::vector<SegmentShare> s = segment_shares_weighted(M, nb, segment_size, w);
     *n = static_cast<int>(s.size());
     for (int i = 0; out && i < *n && i < cap; ++i) {
       out[4 * i + 0] = s[i].device;
@@ -583,6 +603,22 @@ es_status es_system_info(es_system* s, int* workers, int* workers_per_model, int
     }
     if (launches) *launches = s->sys->launches_last_run();
     if (combine_device) *combine_device = s->sys->combine_device();
+    return ES_OK;
+  });
+}
+
+es_status es_system_shares(es_system* s, int64_t* shares, double* rates) {
+  return guard([&] {
+    need(s != nullptr, "NULL handle");
+    const auto sh = s->sys->last_shares();
+    const auto& r = s->sys->worker_rates();
+    for (std::size_t w = 0; w < sh.size(); ++w) {
+      if (shares) {
+        shares[2 * w] = sh[w].first;
+        shares[2 * w + 1] = sh[w].second;
+      }
+      if (rates) rates[w] = r.empty() ? 1.0 : r[w];
+    }
     return ES_OK;
   });
 }

@@ -4,6 +4,9 @@
 // /root/reference/proj/src/opt/optimizer.cpp:26-64.
 #include "enserve/placement.hpp"
 
+#include <cmath>
+#include <stdexcept>
+
 #include <algorithm>
 #include <limits>
 #include <numeric>
@@ -101,6 +104,39 @@ std::vector<SegmentShare> segment_shares(const AllocationMatrix& A, std::size_t 
       const long long k = seen[m]++, n = A.column_worker_count(m);
       out.push_back({d, m, S * k / n, S * (k + 1) / n});
     }
+  return out;
+}
+
+std::vector<SegmentShare> segment_shares_weighted(const AllocationMatrix& A,
+                                                  std::size_t nb_samples, int segment_size,
+                                                  const std::vector<double>& weight) {
+  std::vector<SegmentShare> out = segment_shares(A, nb_samples, segment_size);
+  if (weight.size() != out.size()) throw std::invalid_argument("one weight per worker");
+  const long long S = static_cast<long long>(num_segments(nb_samples, segment_size));
+  for (int m = 0; m < A.model_count(); ++m) {
+    std::vector<std::size_t> ws;
+    double total = 0.0;
+    bool equal = true;
+    for (std::size_t i = 0; i < out.size(); ++i)
+      if (out[i].model == m) {
+        if (!(weight[i] > 0.0) || !std::isfinite(weight[i]))
+          throw std::invalid_argument("worker weights must be positive");
+        if (!ws.empty() && weight[i] != weight[ws[0]]) equal = false;
+        ws.push_back(i);
+        total += weight[i];
+      }
+    if (ws.size() < 2 || equal) continue;  // keep the equal split bit for bit
+    double cum = 0.0;
+    long long prev = 0;
+    for (std::size_t k = 0; k < ws.size(); ++k) {
+      cum += weight[ws[k]];
+      const long long end =
+          k + 1 == ws.size() ? S : std::max(prev, std::llround(static_cast<double>(S) * cum / total));
+      out[ws[k]].begin = prev;
+      out[ws[k]].end = end;
+      prev = end;
+    }
+  }
   return out;
 }
 

@@ -66,5 +66,13 @@ struct SegmentShare {
 };
 std::vector<SegmentShare> segment_shares(const AllocationMatrix& A, std::size_t nb_samples,
                                          int segment_size);
+// The same split with a model's runs proportional to `weight` (one entry per
+// worker, row-major cell order; e.g. measured rows/s): the static fallback of
+// SURVEY.md §8-E for the reference's shared FIFO, where a faster
+// data-parallel worker pulls more segments.  Contiguous, exactly once; equal
+// weights give segment_shares' split exactly.
+std::vector<SegmentShare> segment_shares_weighted(const AllocationMatrix& A,
+                                                  std::size_t nb_samples, int segment_size,
+                                                  const std::vector<double>& weight);
 
 }  // namespace enserve

@@ -358,11 +358,55 @@ void InferenceSystem::shutdown() {
 }
 
 void InferenceSystem::assign_shares(std::size_t nb) {
-  std::vector<SegmentShare> shares = segment_shares(matrix_, nb, cluster_.segment_size);
+  std::vector<SegmentShare> shares =
+      rates_.empty() ? segment_shares(matrix_, nb, cluster_.segment_size)
+                     : segment_shares_weighted(matrix_, nb, cluster_.segment_size, rates_);
   for (std::size_t i = 0; i < workers_.size(); ++i) {  // both in row-major cell order
     workers_[i]->seg_begin = shares[i].begin;
     workers_[i]->seg_end = shares[i].end;
   }
+}
+
+std::vector<std::pair<long long, long long>> InferenceSystem::last_shares() const {
+  std::vector<std::pair<long long, long long>> out;
+  for (const auto& w : workers_) out.emplace_back(w->seg_begin, w->seg_end);
+  return out;
+}
+
+// Rows/s of every data-parallel worker running alone over one wave of its
+// tiles (grid x batch rows, whole segments) of this run's store: untimed, like
+// the upload in begin_run.  The second of two launches counts.
+void InferenceSystem::probe_rates(const SampleStore& X) {
+  const std::vector<int> per_model = workers_per_model();
+  bool any = false;
+  for (const auto& w : workers_) any = any || per_model[w->model] > 1;
+  if (!any) return;
+  const long long nb = static_cast<long long>(X.nb_samples());
+  const long long S = static_cast<long long>(num_segments(X.nb_samples(), cluster_.segment_size));
+  std::vector<double> rates(workers_.size(), 1.0);
+  for (std::size_t i = 0; i < workers_.size(); ++i) {
+    Worker& w = *workers_[i];
+    if (per_model[w.model] < 2) continue;
+    OnDevice on(w.phys);
+    int grid = es::num_sms(w.phys);
+    if (options_.sms_per_worker > 0) grid = std::min(grid, options_.sms_per_worker);
+    const long long want = (static_cast<long long>(grid) * w.batch + cluster_.segment_size - 1) /
+                           cluster_.segment_size;
+    const long long segs = std::max<long long>(1, std::min(S, want));
+    float* out = w.phys != combine_dev_ ? w.staging : impl_->logits[w.model];
+    float ms = 0.0f;
+    for (int rep = 0; rep < 2; ++rep) {
+      ES_CUDA(cudaEventRecord(w.ev_begin, w.stream));
+      w.member->forward(X.device_replica(w.phys), nb, cluster_.segment_size, 0, segs, out, grid,
+                        w.stream, nullptr);
+      ES_CUDA(cudaEventRecord(w.ev_done, w.stream));
+      ES_CUDA(cudaEventSynchronize(w.ev_done));
+      ES_CUDA(cudaEventElapsedTime(&ms, w.ev_begin, w.ev_done));
+    }
+    const double rows = static_cast<double>(std::min(nb, segs * cluster_.segment_size));
+    rates[i] = rows / std::max(static_cast<double>(ms) * 1e-3, 1e-9);
+  }
+  rates_ = std::move(rates);
 }
 
 bool InferenceSystem::single_device() const {
@@ -412,7 +456,6 @@ void InferenceSystem::begin_run(std::shared_ptr<const SampleStore> X, Combinatio
     }
   }
   const std::size_t S = num_segments(nb, cluster_.segment_size);
-  assign_shares(nb);
   for (auto& w : workers_) {
     if (w->phys != combine_dev_ && w->staging_rows < nb) {
       OnDevice on(w->phys);
@@ -421,6 +464,8 @@ void InferenceSystem::begin_run(std::shared_ptr<const SampleStore> X, Combinatio
       w->staging_rows = nb;
     }
   }
+  if (!options_.dp_equal_split && rates_.empty() && nb > 0) probe_rates(*X);
+  assign_shares(nb);
   impl_->store = std::move(X);
   impl_->rule = std::move(rule);
   impl_->segments = S;
@@ -682,7 +727,9 @@ double InferenceSystem::run_host_core(std::size_t nb, std::size_t width, float* 
       ES_LAUNCH(es::convert_f32_to_bf16(sl.x32, static_cast<__nv_bfloat16*>(sl.x16), elems, I.main));
       ++launches_;
     }
-    std::vector<SegmentShare> shares = segment_shares(matrix_, rows, cluster_.segment_size);
+    std::vector<SegmentShare> shares =
+        rates_.empty() ? segment_shares(matrix_, rows, cluster_.segment_size)
+                       : segment_shares_weighted(matrix_, rows, cluster_.segment_size, rates_);
     for (std::size_t w = 0; w < workers_.size(); ++w)
       launches_ += workers_[w]->member->forward(sl.x16, static_cast<long long>(rows),
                                                 cluster_.segment_size, shares[w].begin,

@@ -127,6 +127,11 @@ struct PoolOptions {
   // boxes (tools/e2e_sweep.py, cfg2: 4/8 2.03e7, 6/8 2.17e7, 8/8 1.98e7
   // samples/s): both legs saturate the host's memory bandwidth.
   int e2e_convert_eighths = 6;
+  // Data-parallel split of a model's segments: runs
+  // proportional to each worker's probed rows/s (the static stand-in for the
+  // reference's shared FIFO, where faster workers pull more segments), or
+  // equal runs.
+  bool dp_equal_split = false;
 };
 
 // Per-model executable member on one GPU (the Predictor of backend.hpp:25-34).
@@ -182,12 +187,18 @@ class InferenceSystem {
   std::vector<double> last_kernel_ms(int worker) const;
   std::vector<std::string> kernel_names(int worker) const;
   int combine_device() const { return combine_dev_; }
+  // Segment runs [begin, end) of every worker in the last run, and the rows/s
+  // each data-parallel worker measured when probed (1.0 for single workers).
+  std::vector<std::pair<long long, long long>> last_shares() const;
+  const std::vector<double>& worker_rates() const { return rates_; }
 
  private:
   struct Worker;
   // fill(chunk, pinned, first_row, rows): stage the chunk's bf16 rows in the
   // pinned slot and return nullptr, or return a pinned fp32 source to DMA.
   using HostFill = std::function<const float*(std::size_t, std::uint16_t*, std::size_t, std::size_t)>;
+  void probe_rates(const SampleStore& X);
+  std::vector<double> rates_;  // per worker, probed on the first run with a DP column
   double run_host_core(std::size_t nb, std::size_t width, float* Y_out, std::int32_t* labels_out,
                        const HostFill& fill);
   struct Impl;

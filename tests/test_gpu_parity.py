@@ -335,3 +335,26 @@ def test_pipelined_run_host_equals_resident_run(host_convert, pinned):
         assert t > 0
     np.testing.assert_array_equal(Y, resident.combined)
     np.testing.assert_array_equal(lab, resident.winners)
+
+
+def test_data_parallel_split_follows_probed_rates():
+    """a model's data-parallel workers split its segments in
+    proportion to their probed rows/s (static stand-in for the reference's
+    shared FIFO); results do not depend on the split."""
+    c = mlp_cluster([256], [128], devices=2)
+    A = es.AllocationMatrix.from_array([[128], [8]])  # a fast and a slow worker, both on GPU 0
+    X = es.SampleStore(synthetic_seed=5, nb=1 << 16, width=784, device=0)
+    with es.InferenceSystem(A, c, device_map=[0, 0]) as s:
+        out = s.run(X)
+        shares, rates = s.shares()
+    assert rates[0] > 2 * rates[1]  # 128-row tiles vs 8-row tiles
+    n0, n1 = shares[0][1] - shares[0][0], shares[1][1] - shares[1][0]
+    assert shares[0][0] == 0 and shares[0][1] == shares[1][0] and shares[1][1] == 512
+    assert n0 > 2 * n1
+    assert abs(n0 / 512 - rates[0] / (rates[0] + rates[1])) < 0.01
+    with es.InferenceSystem(A, c, device_map=[0, 0], dp_equal_split=True) as s:
+        eq = s.run(X)
+        shares_eq, _ = s.shares()
+    assert shares_eq == [(0, 256), (256, 512)]
+    np.testing.assert_array_equal(out.combined, eq.combined)
+    np.testing.assert_array_equal(out.winners, eq.winners)

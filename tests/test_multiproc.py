@@ -76,3 +76,30 @@ def test_segment_shares_exactly_once_for_mixed_layouts():
             if mm == m:
                 covered += list(range(b, e))
         assert sorted(covered) == list(range(16))
+
+
+def test_weighted_segment_shares_proportional_and_exactly_once():
+    """SURVEY.md §8-E static fallback of the shared per-model FIFO: a model's
+    data-parallel workers take contiguous runs proportional to their rates."""
+    sys.path.insert(0, str(REPO))
+    import paper_2208_14049_b200 as es
+    A = es.AllocationMatrix.from_array([[16, 0], [32, 8], [0, 64], [128, 0]])
+    S = 100  # 12800 rows / 128
+    equal = es.segment_shares(A, 12800, 128)
+    assert es.segment_shares(A, 12800, 128, [2.0] * 5) == equal  # equal weights: same split
+    w = [1.0, 3.0, 5.0, 1.0, 4.0]  # workers (0,0) (1,0) (1,1) (2,1) (3,0)
+    shares = es.segment_shares(A, 12800, 128, w)
+    assert [(d, m) for d, m, _, _ in shares] == [(0, 0), (1, 0), (1, 1), (2, 1), (3, 0)]
+    for m in (0, 1):
+        mine = [(b, e, w[i]) for i, (d, mm, b, e) in enumerate(shares) if mm == m]
+        assert mine[0][0] == 0 and mine[-1][1] == S
+        for (a0, a1, _), (b0, b1, _) in zip(mine, mine[1:]):
+            assert a1 == b0  # contiguous, exactly once, worker order kept
+        tot = sum(x for _, _, x in mine)
+        for b, e, x in mine:
+            assert abs((e - b) - S * x / tot) <= 1.0
+    # model 0: weights 1, 3, 4 of 8 -> cumulative 12.5, 50, 100 segments (half rounds up)
+    assert [(b, e) for d, m, b, e in shares if m == 0] == [(0, 13), (13, 50), (50, 100)]
+    import pytest
+    with pytest.raises(es.InvalidArgument):
+        es.segment_shares(A, 12800, 128, [1.0, 0.0, 1.0, 1.0, 1.0])
