@@ -63,28 +63,42 @@ inline std::uint16_t bf16_rn(float f) {
 __attribute__((target("avx512f,avx512bf16"))) void convert_avx512bf16(const float* x,
                                                                       std::uint16_t* y,
                                                                       std::size_t n) {
+  // Non-temporal stores once y is 64-byte aligned: the destination (a pinned
+  // staging slot the DMA engine reads next) is not read for ownership first,
+  // which saves a third of the host-memory traffic of a converted chunk.
   std::size_t i = 0;
+  for (; i < n && (reinterpret_cast<std::uintptr_t>(y + i) & 63u); ++i) y[i] = bf16_rn(x[i]);
   for (; i + 32 <= n; i += 32) {
     __m512 a = _mm512_loadu_ps(x + i);
     __m512 b = _mm512_loadu_ps(x + i + 16);
     __m512bh p = _mm512_cvtne2ps_pbh(b, a);  // low half from a
-    _mm512_storeu_si512(reinterpret_cast<void*>(y + i), reinterpret_cast<__m512i>(p));
+    _mm512_stream_si512(reinterpret_cast<__m512i*>(y + i), reinterpret_cast<__m512i>(p));
   }
+  _mm_sfence();
   for (; i < n; ++i) y[i] = bf16_rn(x[i]);
 }
 
 __attribute__((target("avx2"))) void convert_avx2(const float* x, std::uint16_t* y,
                                                   std::size_t n) {
   std::size_t i = 0;
+  for (; i < n && (reinterpret_cast<std::uintptr_t>(y + i) & 15u); ++i) y[i] = bf16_rn(x[i]);
   const __m256i one = _mm256_set1_epi32(1), bias = _mm256_set1_epi32(0x7fff);
   for (; i + 8 <= n; i += 8) {
     __m256i u = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(x + i));
+    // NaN inputs take the scalar path's quiet-NaN rule below
+    const __m256i expo = _mm256_and_si256(u, _mm256_set1_epi32(0x7f800000));
+    if (!_mm256_testz_si256(_mm256_cmpeq_epi32(expo, _mm256_set1_epi32(0x7f800000)),
+                            _mm256_set1_epi32(-1))) {
+      for (std::size_t j = i; j < i + 8; ++j) y[j] = bf16_rn(x[j]);
+      continue;
+    }
     __m256i lsb = _mm256_and_si256(_mm256_srli_epi32(u, 16), one);
     __m256i r = _mm256_srli_epi32(_mm256_add_epi32(_mm256_add_epi32(u, bias), lsb), 16);
     // pack 8 x u32 (values < 2^16) into 8 x u16
     __m128i lo = _mm256_castsi256_si128(r), hi = _mm256_extracti128_si256(r, 1);
-    _mm_storeu_si128(reinterpret_cast<__m128i*>(y + i), _mm_packus_epi32(lo, hi));
+    _mm_stream_si128(reinterpret_cast<__m128i*>(y + i), _mm_packus_epi32(lo, hi));  // see above
   }
+  _mm_sfence();
   for (; i < n; ++i) y[i] = bf16_rn(x[i]);
 }
 
@@ -106,7 +120,7 @@ void convert_f32_to_bf16_range(const float* x, std::uint16_t* y, std::size_t n) 
 
 void convert_f32_to_bf16_host(const float* x, std::uint16_t* y, std::size_t n, ThreadPool& pool) {
   const std::function<void(int, int)> job = [&](int part, int parts) {
-    const std::size_t per = (n / parts + 63) / 64 * 64;
+    const std::size_t per = ((n + parts - 1) / parts + 63) / 64 * 64;  // > 0 for any n
     const std::size_t a = std::min(n, static_cast<std::size_t>(part) * per);
     const std::size_t b = std::min(n, a + per);
     if (b > a) convert_f32_to_bf16_range(x + a, y + a, b - a);

@@ -83,3 +83,19 @@ def test_host_bf16_converter_rounds_to_nearest_even():
     y = es.host_convert_bf16(x)
     want = (round_bf16(x).view(np.uint32) >> 16).astype(np.uint16)
     np.testing.assert_array_equal(y, want)
+
+
+def test_host_bf16_converter_special_values_and_odd_lengths():
+    # Inf keeps its sign, NaN stays a (quiet) NaN, on the vector and scalar paths alike
+    for n in (7, 8, 33, 1000):
+        x = np.linspace(-3, 3, n).astype(np.float32)
+        x[n // 2] = np.inf
+        x[0] = -np.inf
+        x[-1] = np.nan
+        y = es.host_convert_bf16(x)
+        assert y[n // 2] == 0x7F80 and y[0] == 0xFF80
+        assert (y[-1] & 0x7F80) == 0x7F80 and (y[-1] & 0x007F) != 0
+        from oracle.refcpu import round_bf16
+        finite = np.isfinite(x)
+        want = (round_bf16(x[finite]).view(np.uint32) >> 16).astype(np.uint16)
+        np.testing.assert_array_equal(y[finite], want)
