@@ -124,8 +124,9 @@ struct PoolOptions {
   // Pinned input with host conversion on: how many chunks in 8 the host
   // converts (the rest are DMA'd as fp32 and converted on the device) --
   // balances host-memory bandwidth against PCIe.  6 measured best on B200
-  // boxes (tools/e2e_sweep.py, cfg2: 4/8 2.03e7, 6/8 2.17e7, 8/8 1.98e7
-  // samples/s): both legs saturate the host's memory bandwidth.
+  // boxes (tools/e2e_sweep.py, cfg2, non-temporal stores into the pinned
+  // slots: 4/8 2.19e7, 6/8 2.56e7, 7/8 2.53e7, 8/8 2.26e7 samples/s): both
+  // legs saturate the host's memory bandwidth.
   int e2e_convert_eighths = 6;
   // Data-parallel split of a model's segments: runs
   // proportional to each worker's probed rows/s (the static stand-in for the
