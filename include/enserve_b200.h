@@ -374,9 +374,12 @@ typedef struct es_service_info {
 
 /* Validates A (ES_ERR_SPEC if invalid, server.cpp:30-31) and starts building
  * the device pool on a background thread (init_pool, server.cpp:37-52). */
+/* arena_rows: rows per page-locked staging arena of a one-GPU pool (two
+ * arenas; submits convert to bf16 straight into them), < 0 = default 131072,
+ * 0 = none (requests staged in private buffers and gathered per flush). */
 es_status es_service_create(const es_cluster_desc* c, const int* A, const es_rule_desc* rule,
                             const es_pool_opts* opts, int flush_timeout_ms, size_t input_width,
-                            es_service** out);
+                            long long arena_rows, es_service** out);
 /* ready = 1 once the pool is up; error receives the startup error (if any). */
 es_status es_service_wait_ready(es_service* s, int timeout_ms, int* ready, char* error,
                                 size_t error_len);

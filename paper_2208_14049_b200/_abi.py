@@ -172,7 +172,7 @@ _SIGS = {
                              C.POINTER(c_float_p), c_float_p, c_int32_p]),
     "es_system_shares": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64), c_double_p]),
     "es_service_create": (C.c_int, [C.POINTER(ClusterDesc), c_int_p, C.POINTER(RuleDesc),
-                                    C.POINTER(PoolOpts), C.c_int, C.c_size_t,
+                                    C.POINTER(PoolOpts), C.c_int, C.c_size_t, C.c_longlong,
                                     C.POINTER(C.c_void_p)]),
     "es_service_wait_ready": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int), C.c_char_p,
                                         C.c_size_t]),

@@ -888,7 +888,7 @@ class PredictionService:
 
     def __init__(self, cluster: ClusterSpec, A: AllocationMatrix,
                  rule: CombinationRule = None, flush_timeout_ms: int = 50,
-                 input_width: int = None, **pool):
+                 input_width: int = None, arena_rows: int = -1, **pool):
         keep: list = []
         rule = rule or CombinationRule.averaging()
         if input_width is None:  # real members define it; synthetic ones need it given
@@ -902,7 +902,8 @@ class PredictionService:
         with _Desc(cluster) as d:
             _check(lib().es_service_create(d.ptr, A.ptr(), C.byref(rule._desc(keep)),
                                            C.byref(_pool_opts(keep, **pool)),
-                                           int(flush_timeout_ms), self.input_width, C.byref(h)))
+                                           int(flush_timeout_ms), self.input_width,
+                                           int(arena_rows), C.byref(h)))
         self._h = h
 
     def wait_ready(self, timeout_s: float = 60.0) -> bool:

@@ -963,7 +963,7 @@ es_status es_calibrate_cost_model(const es_cluster_desc* c, int device, size_t c
 // ------------------------------------------------------------ deploy-mode service
 es_status es_service_create(const es_cluster_desc* c, const int* A, const es_rule_desc* rule,
                             const es_pool_opts* opts, int flush_timeout_ms, size_t input_width,
-                            es_service** out) {
+                            long long arena_rows, es_service** out) {
   return guard([&] {
     need(out != nullptr, "out is NULL");
     ClusterSpec cl = to_cluster(c);
@@ -972,6 +972,7 @@ es_status es_service_create(const es_cluster_desc* c, const int* A, const es_rul
     cfg.input_width = input_width;
     cfg.rule = to_rule(rule, cl.model_count());
     cfg.pool = to_opts(opts);
+    if (arena_rows >= 0) cfg.arena_rows = static_cast<std::size_t>(arena_rows);
     auto* s = new es_service();
     s->C = cl.models.empty() ? 0 : cl.models[0].output_width;
     try {

@@ -616,13 +616,13 @@ double InferenceSystem::run_host(const float* X, std::size_t nb, std::size_t wid
   const std::size_t k8 = static_cast<std::size_t>(std::clamp(options_.e2e_convert_eighths, 0, 8));
   return run_host_core(nb, width, Y_out, labels_out,
                        [&](std::size_t i, std::uint16_t* pinned, std::size_t r0,
-                           std::size_t rows) -> const float* {
+                           std::size_t rows) -> HostChunk {
                          const bool convert =
                              mode == 1 || (mode == 0 && (i + 1) * k8 / 8 > i * k8 / 8);
-                         if (!convert) return X + r0 * width;
+                         if (!convert) return {X + r0 * width, true};
                          convert_f32_to_bf16_host(X + r0 * width, pinned, rows * width,
                                                   *impl_->pool);
-                         return nullptr;
+                         return {};
                        });
 }
 
@@ -634,7 +634,12 @@ double InferenceSystem::run_host_blocks(const std::vector<HostRowBlock>& blocks,
   for (std::size_t k = 0; k < blocks.size(); ++k) first[k + 1] = first[k] + blocks[k].rows;
   return run_host_core(nb, width, Y_out, labels_out,
                        [&](std::size_t, std::uint16_t* pinned, std::size_t r0,
-                           std::size_t rows) -> const float* {
+                           std::size_t rows) -> HostChunk {
+                         // A chunk inside one page-locked block goes straight to the DMA.
+                         const std::size_t k0 =
+                             std::upper_bound(first.begin(), first.end(), r0) - first.begin() - 1;
+                         if (blocks[k0].pinned && r0 + rows <= first[k0 + 1])
+                           return {blocks[k0].bf16 + (r0 - first[k0]) * width, false};
                          // Gather rows [r0, r0 + rows) from the blocks, split over the pool.
                          const std::function<void(int, int)> job = [&](int part, int parts) {
                            const std::size_t per = (rows + parts - 1) / parts;
@@ -651,7 +656,7 @@ double InferenceSystem::run_host_blocks(const std::vector<HostRowBlock>& blocks,
                            }
                          };
                          impl_->pool->run(job);
-                         return nullptr;
+                         return {};
                        });
 }
 
@@ -712,12 +717,14 @@ double InferenceSystem::run_host_core(std::size_t nb, std::size_t width, float* 
     const std::size_t rows = std::min(chunk, nb - r0);
     const std::size_t elems = rows * width;
     if (i >= kSlots) ES_CUDA(cudaEventSynchronize(sl.h2d_done));  // pinned slot reusable
-    const float* direct = fill(i, static_cast<std::uint16_t*>(sl.pinned), r0, rows);
+    const HostChunk src = fill(i, static_cast<std::uint16_t*>(sl.pinned), r0, rows);
+    const float* direct = src.fp32 ? static_cast<const float*>(src.src) : nullptr;
     if (i >= kSlots) ES_CUDA(cudaStreamWaitEvent(I.copy, sl.d2h_done, 0));  // slot buffers free
     h2d_bytes_ += elems * (direct ? sizeof(float) : 2);
     d2h_bytes_ += (Y_out ? rows * C * sizeof(float) : 0) + (labels_out ? rows * sizeof(int32_t) : 0);
     if (!direct)
-      ES_CUDA(cudaMemcpyAsync(sl.x16, sl.pinned, elems * 2, cudaMemcpyHostToDevice, I.copy));
+      ES_CUDA(cudaMemcpyAsync(sl.x16, src.src ? src.src : sl.pinned, elems * 2,
+                              cudaMemcpyHostToDevice, I.copy));
     else
       ES_CUDA(cudaMemcpyAsync(sl.x32, direct, elems * sizeof(float), cudaMemcpyHostToDevice,
                               I.copy));

@@ -165,6 +165,7 @@ class InferenceSystem {
   struct HostRowBlock {
     const std::uint16_t* bf16 = nullptr;  // rows x width
     std::size_t rows = 0;
+    bool pinned = false;  // page-locked: a chunk inside it is DMA'd with no gather
   };
   double run_host_blocks(const std::vector<HostRowBlock>& blocks, std::size_t width,
                          float* Y_out, std::int32_t* labels_out);
@@ -196,8 +197,13 @@ class InferenceSystem {
  private:
   struct Worker;
   // fill(chunk, pinned, first_row, rows): stage the chunk's bf16 rows in the
-  // pinned slot and return nullptr, or return a pinned fp32 source to DMA.
-  using HostFill = std::function<const float*(std::size_t, std::uint16_t*, std::size_t, std::size_t)>;
+  // pinned slot and return {}, or name a page-locked source to DMA as is
+  // (fp32, converted on the device, or bf16).
+  struct HostChunk {
+    const void* src = nullptr;
+    bool fp32 = false;
+  };
+  using HostFill = std::function<HostChunk(std::size_t, std::uint16_t*, std::size_t, std::size_t)>;
   void probe_rates(const SampleStore& X);
   std::vector<double> rates_;  // per worker, probed on the first run with a DP column
   double run_host_core(std::size_t nb, std::size_t width, float* Y_out, std::int32_t* labels_out,

@@ -1,6 +1,8 @@
 // Deploy-mode prediction service (design in service.hpp).
 #include "enserve/service.hpp"
 
+#include <cuda_runtime.h>
+
 #include <cstring>
 
 #include "enserve/host_convert.hpp"
@@ -18,7 +20,11 @@ PredictionService::PredictionService(ClusterSpec cluster, AllocationMatrix matri
   dispatcher_ = std::thread([this] { dispatcher_loop(); });
 }
 
-PredictionService::~PredictionService() { stop(); }
+PredictionService::~PredictionService() {
+  stop();
+  for (Arena& a : arena_)
+    if (a.rows) cudaFreeHost(a.rows);
+}
 
 void PredictionService::init_pool() {
   try {
@@ -27,6 +33,16 @@ void PredictionService::init_pool() {
     // Pinned slots, streams and the host pool up front (and the input width
     // checked against the members), so the first flush pays none of it.
     if (host_blocks_) system_->run_host_blocks({}, config_.input_width, nullptr, nullptr);
+    if (host_blocks_ && config_.arena_rows > 0)
+      for (Arena& a : arena_) {
+        void* p = nullptr;
+        if (cudaHostAlloc(&p, config_.arena_rows * config_.input_width * 2, cudaHostAllocDefault) !=
+            cudaSuccess) {
+          cudaGetLastError();
+          throw StartupError("cannot allocate the service's page-locked arenas");
+        }
+        a.rows = static_cast<std::uint16_t*>(p);
+      }
     ready_.store(true);
   } catch (const std::exception& e) {
     std::lock_guard<std::mutex> lock(init_mutex_);
@@ -62,14 +78,44 @@ std::future<RunOutput> PredictionService::submit(const float* samples, std::size
   }
   if (!ready_.load()) throw NotReadyError("service not ready");
   p->rows = rows;
+  const std::size_t elems = rows * config_.input_width;
+  if (host_blocks_ && arena_[0].rows) {
+    // Reserve rows in the open arena (in buffer order), convert into them
+    // outside the lock; the flush waits for the arena's writers.
+    std::uint16_t* dst = nullptr;
+    {
+      std::lock_guard<std::mutex> lock(buffer_mutex_);
+      if (stopping_.load()) throw NotReadyError("server shutting down");
+      Arena& a = arena_[open_];
+      if (a.used + rows <= config_.arena_rows) {
+        dst = a.rows + a.used * config_.input_width;
+        a.used += rows;
+        ++a.writers;
+        p->staged = dst;
+        p->arena = open_;
+        p->arrived = std::chrono::steady_clock::now();
+        buffer_.push_back(p);
+        buffered_samples_ += rows;
+      }
+    }
+    if (dst) {
+      convert_f32_to_bf16_range(samples, dst, elems);
+      {
+        std::lock_guard<std::mutex> lock(buffer_mutex_);
+        --arena_[p->arena].writers;
+      }
+      buffer_cv_.notify_all();
+      return fut;
+    }
+  }
   // The copy the request needs anyway doubles as the fp32 -> bf16 conversion
   // (on the caller's thread, so it scales with the clients), halving what the
   // flush gathers and sends over PCIe.
-  if (host_blocks_) {
-    p->bf16.resize(rows * config_.input_width);
-    convert_f32_to_bf16_range(samples, p->bf16.data(), p->bf16.size());
+  if (host_blocks_) {  // arena full or too small for this request
+    p->bf16.resize(elems);
+    convert_f32_to_bf16_range(samples, p->bf16.data(), elems);
   } else {
-    p->samples.assign(samples, samples + rows * config_.input_width);
+    p->samples.assign(samples, samples + elems);
   }
   {
     std::lock_guard<std::mutex> lock(buffer_mutex_);
@@ -85,6 +131,13 @@ std::future<RunOutput> PredictionService::submit(const float* samples, std::size
 }
 
 void PredictionService::flush_locked(std::unique_lock<std::mutex>& lock) {
+  if (arena_[0].rows) {
+    // Every reserved row of the open arena converted, then submits move to
+    // the other arena (free: the previous flush from it has completed).
+    buffer_cv_.wait(lock, [&] { return arena_[open_].writers == 0; });
+    open_ ^= 1;
+    arena_[open_].used = 0;
+  }
   std::vector<std::shared_ptr<Pending>> batch(buffer_.begin(), buffer_.end());
   buffer_.clear();
   buffered_samples_ = 0;
@@ -96,7 +149,16 @@ void PredictionService::flush_locked(std::unique_lock<std::mutex>& lock) {
     if (host_blocks_) {
       std::vector<InferenceSystem::HostRowBlock> blocks;
       blocks.reserve(batch.size());
-      for (const auto& r : batch) blocks.push_back({r->bf16.data(), r->rows});
+      for (const auto& r : batch) {
+        const std::uint16_t* src = r->staged ? r->staged : r->bf16.data();
+        InferenceSystem::HostRowBlock& last = blocks.empty() ? blocks.emplace_back() : blocks.back();
+        if (r->staged && last.pinned && last.bf16 + last.rows * config_.input_width == src)
+          last.rows += r->rows;  // consecutive arena rows: one page-locked block
+        else if (blocks.size() == 1 && last.rows == 0)
+          last = {src, r->rows, r->staged != nullptr};
+        else
+          blocks.push_back({src, r->rows, r->staged != nullptr});
+      }
       const int C = cluster_.models[0].output_width;
       out.output_width = C;
       out.combined.resize(total * static_cast<std::size_t>(C));
@@ -184,6 +246,10 @@ void PredictionService::stop() {
   buffer_cv_.notify_all();
   if (dispatcher_.joinable()) dispatcher_.join();
   if (init_thread_.joinable()) init_thread_.join();
+  {  // submits still converting into an arena finish before it can be freed
+    std::unique_lock<std::mutex> lock(buffer_mutex_);
+    buffer_cv_.wait(lock, [&] { return arena_[0].writers == 0 && arena_[1].writers == 0; });
+  }
   if (system_) system_->shutdown();
 }
 

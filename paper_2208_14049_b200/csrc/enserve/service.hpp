@@ -25,6 +25,10 @@ struct ServiceConfig {  // ServeConfig (server.hpp:19-26), minus bind host / por
   std::size_t input_width = 16;
   CombinationRule rule = CombinationRule::averaging();
   PoolOptions pool;
+  // One-GPU pools: rows per page-locked arena (two: one filling while the
+  // other flushes).  Requests are converted to bf16 straight into the open
+  // arena by the submitting thread and DMA'd from there; 0 = no arenas.
+  std::size_t arena_rows = 131072;
 };
 
 struct ServiceStats {  // GET /v1/stats (server.cpp:88-107)
@@ -64,6 +68,8 @@ class PredictionService {
   struct Pending {
     std::vector<float> samples;          // multi-GPU pools: fp32 rows for a SampleStore
     std::vector<std::uint16_t> bf16;     // one-GPU pools: rows converted by the caller
+    const std::uint16_t* staged = nullptr;  // ... or their place in a pinned arena
+    int arena = -1;
     std::size_t rows = 0;
     std::chrono::steady_clock::time_point arrived;
     std::promise<RunOutput> promise;
@@ -78,6 +84,13 @@ class PredictionService {
   std::unique_ptr<InferenceSystem> system_;
   std::atomic<bool> ready_{false};
   bool host_blocks_ = false;  // pool on one GPU: flush through run_host_blocks
+  struct Arena {
+    std::uint16_t* rows = nullptr;  // page-locked, arena_rows x input_width bf16
+    std::size_t used = 0;           // rows handed out
+    int writers = 0;                // submits still converting into it
+  };
+  Arena arena_[2];
+  int open_ = 0;  // the arena submits fill; the other one is flushed
   std::atomic<bool> stopping_{false};
   mutable std::mutex init_mutex_;
   std::condition_variable init_cv_;

@@ -158,3 +158,19 @@ def test_startup_oom_reported_by_wait_ready():
         assert not svc.stats().ready
         with pytest.raises(es.NotReadyError):
             svc.submit(np.zeros((1, 4), np.float32))
+
+
+@pytest.mark.parametrize("arena_rows", [0, 256, 131072])
+def test_arena_sizes_give_identical_answers(arena_rows):
+    """Requests staged in the page-locked arenas, spilled to private buffers
+    (arena full or too small), or mixed in one flush answer identically."""
+    c, A = mlp_cluster(), es.AllocationMatrix.from_array([[64, 32]])
+    rng = np.random.default_rng(11)
+    reqs = [rng.random((int(n), 784), dtype=np.float32) for n in rng.integers(1, 400, 40)]
+    with es.PredictionService(c, A, flush_timeout_ms=3, input_width=784,
+                              arena_rows=arena_rows) as svc:
+        assert svc.wait_ready(30.0)
+        got = [p.result() for p in [svc.submit(x) for x in reqs]]
+    ref = offline(np.concatenate(reqs), A, c)
+    np.testing.assert_array_equal(np.concatenate([g[0] for g in got]), ref.combined)
+    np.testing.assert_array_equal(np.concatenate([g[1] for g in got]), ref.winners)
