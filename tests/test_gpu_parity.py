@@ -358,3 +358,35 @@ def test_data_parallel_split_follows_probed_rates():
     assert shares_eq == [(0, 256), (256, 512)]
     np.testing.assert_array_equal(out.combined, eq.combined)
     np.testing.assert_array_equal(out.winners, eq.winners)
+
+
+def test_member_handles_used_concurrently_from_worker_threads():
+    """SURVEY.md §8-B threading contract: each worker thread owns its Predictor
+    (load + every predict on that thread); different handles run concurrently.
+    Results equal the single-threaded ones bit for bit."""
+    import threading
+    models = [es.mlp_model(0, "a", [784, 256, 10], 31), es.mlp_model(1, "b", [784, 1024, 10], 32),
+              es.cnn_model(2, "c", 33)]
+    rng = np.random.default_rng(21)
+    X = rng.random((3000, 784), dtype=np.float32)
+    want = [es.Member(m, 64).predict(X, first_index=100) for m in models]
+    got = [None] * len(models)
+    errors = []
+
+    def worker(i):
+        try:
+            mem = es.Member(models[i], 64)  # load() on the worker's own thread
+            outs = [mem.predict(X, first_index=100) for _ in range(3)]
+            got[i] = outs
+        except Exception as e:  # noqa: BLE001
+            errors.append(e)
+
+    ts = [threading.Thread(target=worker, args=(i,)) for i in range(len(models))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
+    for i in range(len(models)):
+        for o in got[i]:
+            np.testing.assert_array_equal(o, want[i])
