@@ -144,6 +144,12 @@ es_status es_segment_bounds(int segment_id, int segment_size, size_t nb, size_t*
  * split): out[4*i..] = {device, model, first segment, end segment}. */
 es_status es_segment_shares(const int* A, int devices, int models, size_t nb, int segment_size,
                             long long* out, int cap, int* n);
+/* The batcher (src/runtime/pipeline.cpp:143-166) as the member kernels run
+ * it: segments [seg_begin, seg_end) of nb rows become tiles of `batch` rows
+ * per segment, the last of each segment the remainder.  row0[i], rows[i] for
+ * up to cap tiles; *n = the tile count. */
+es_status es_batch_rows(size_t nb, int segment_size, long long seg_begin, long long seg_end,
+                        int batch, long long* row0, int* rows, int cap, int* n);
 /* The same with each model's runs proportional to weight[w] (one per worker,
  * row-major cells, > 0): what InferenceSystem uses with probed rows/s
  * (SURVEY.md §8-E static fallback).  Equal weights give es_segment_shares. */

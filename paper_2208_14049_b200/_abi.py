@@ -115,6 +115,8 @@ _SIGS = {
     "es_segment_bounds": (C.c_int, [C.c_int, C.c_int, C.c_size_t, c_size_t_p, c_size_t_p]),
     "es_segment_shares": (C.c_int, [c_int_p, C.c_int, C.c_int, C.c_size_t, C.c_int,
                                     C.POINTER(C.c_longlong), C.c_int, c_int_p]),
+    "es_batch_rows": (C.c_int, [C.c_size_t, C.c_int, C.c_longlong, C.c_longlong, C.c_int,
+                                C.POINTER(C.c_longlong), c_int_p, C.c_int, c_int_p]),
     "es_segment_shares_weighted": (C.c_int, [c_int_p, C.c_int, C.c_int, C.c_size_t, C.c_int,
                                              c_double_p, C.POINTER(C.c_longlong), C.c_int,
                                              c_int_p]),

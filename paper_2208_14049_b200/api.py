@@ -339,6 +339,22 @@ def segment_bounds(segment_id: int, segment_size: int, nb: int) -> tuple:
     return s.value, e.value
 
 
+def batch_rows(nb: int, segment_size: int, batch: int, seg_begin: int = 0,
+               seg_end: int = None) -> list:
+    """[(first_row, rows)] of the member kernels' tiles over segments
+    [seg_begin, seg_end): the reference batcher (pipeline.cpp:143-166)."""
+    if seg_end is None:
+        seg_end = num_segments(nb, segment_size)
+    n = C.c_int()
+    _check(lib().es_batch_rows(nb, segment_size, seg_begin, seg_end, batch, None, None, 0,
+                               C.byref(n)))
+    r0 = (C.c_longlong * max(n.value, 1))()
+    rows = (C.c_int * max(n.value, 1))()
+    _check(lib().es_batch_rows(nb, segment_size, seg_begin, seg_end, batch, r0, rows, n.value,
+                               C.byref(n)))
+    return [(r0[i], rows[i]) for i in range(n.value)]
+
+
 def segment_shares(A: AllocationMatrix, nb: int, segment_size: int, weights=None) -> list:
     """[(device, model, first_segment, end_segment)] per worker, row-major;
     with `weights` (one per worker) a model's runs are proportional to them."""

@@ -16,6 +16,7 @@
 #include "enserve/commands.hpp"
 #include "enserve/calibrate.hpp"
 #include "enserve/service.hpp"
+#include "cuda/batching.cuh"
 #include "enserve/placement.hpp"
 #include "enserve/rng.hpp"
 #include "enserve/runtime.hpp"
@@ -284,6 +285,27 @@ es_status es_segment_shares(const int* A, int devices, int models, size_t nb, in
       out[4 * i + 1] = s[i].model;
       out[4 * i + 2] = s[i].begin;
       out[4 * i + 3] = s[i].end;
+    }
+    return ES_OK;
+  });
+}
+
+es_status es_batch_rows(size_t nb, int segment_size, long long seg_begin, long long seg_end,
+                        int batch, long long* row0, int* rows, int cap, int* n) {
+  return guard([&] {
+    need(n != nullptr && segment_size > 0 && batch > 0 && seg_begin >= 0 && seg_end >= seg_begin,
+         "invalid batching arguments");
+    const long long S = static_cast<long long>(num_segments(nb, segment_size));
+    need(seg_end <= S, "segment range past the store");
+    const es::BatchTiles ts =
+        es::batch_tiles(seg_begin, seg_end, segment_size, static_cast<long long>(nb), batch);
+    *n = static_cast<int>(ts.total);
+    for (long long t = 0; t < ts.total && t < cap; ++t) {
+      int r = 0;
+      const long long r0 =
+          es::batch_tile(ts, t, seg_begin, segment_size, static_cast<long long>(nb), batch, &r);
+      if (row0) row0[t] = r0;
+      if (rows) rows[t] = r;
     }
     return ES_OK;
   });

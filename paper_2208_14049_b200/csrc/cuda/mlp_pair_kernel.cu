@@ -5,6 +5,7 @@
 #include <algorithm>
 
 #include "mlp_pair_kernel.cuh"
+#include "batching.cuh"
 #include "epilogue.cuh"
 #include "tma_host.hpp"
 
@@ -21,19 +22,10 @@ constexpr uint32_t kMinSmem = 120 * 1024;
 constexpr int kMaxT = 2;
 constexpr uint16_t kBoth = 0b11;
 
-struct Tiles {
-  long long per_seg = 1, total = 0;
-};
+using Tiles = BatchTiles;
 
 __device__ __forceinline__ Tiles tile_space(const MlpPArgs& a) {
-  Tiles t;
-  t.per_seg = (a.seg_size + a.b - 1) / a.b;
-  const long long nseg = a.seg_end - a.seg_begin;
-  if (nseg <= 0) return t;
-  const long long last = a.seg_end - 1;
-  const long long last_len = min((long long)a.seg_size, a.nb - last * a.seg_size);
-  t.total = (nseg - 1) * t.per_seg + (last_len + a.b - 1) / a.b;
-  return t;
+  return batch_tiles(a.seg_begin, a.seg_end, a.seg_size, a.nb, a.b);
 }
 
 // Group g of this pair: pair-tile tp = pair + (g*T + k) * pairs covers tiles
@@ -49,11 +41,7 @@ __device__ __forceinline__ int group_tiles(const MlpPArgs& a, const Tiles& ts, i
     if (2 * tp >= ts.total) break;
     const long long t = 2 * tp + rank;
     if (t < ts.total) {
-      const long long seg = a.seg_begin + t / ts.per_seg;
-      const long long s1 = min(seg * a.seg_size + a.seg_size, a.nb);
-      const long long r0 = seg * a.seg_size + (t % ts.per_seg) * a.b;
-      row0[k] = r0;
-      rows[k] = static_cast<int>(min((long long)a.b, s1 - r0));
+      row0[k] = batch_tile(ts, t, a.seg_begin, a.seg_size, a.nb, a.b, &rows[k]);
     } else {
       row0[k] = 0;  // load something valid; nothing is written back
       rows[k] = 0;

@@ -6,6 +6,7 @@
 #include <algorithm>
 
 #include "mlp_tmem_kernel.cuh"
+#include "batching.cuh"
 #include "epilogue.cuh"
 #include "tma_host.hpp"
 
@@ -21,19 +22,10 @@ constexpr uint32_t kSmemBudget = 232448;  // 227 KB
 constexpr uint32_t kMinSmem = 120 * 1024; // one CTA per SM: TMEM is allocated whole
 constexpr int kMaxT = 4;
 
-struct Tiles {
-  long long per_seg = 1, total = 0;
-};
+using Tiles = BatchTiles;
 
 __device__ __forceinline__ Tiles tile_space(const MlpTArgs& a) {
-  Tiles t;
-  t.per_seg = (a.seg_size + a.b - 1) / a.b;
-  const long long nseg = a.seg_end - a.seg_begin;
-  if (nseg <= 0) return t;
-  const long long last = a.seg_end - 1;
-  const long long last_len = min((long long)a.seg_size, a.nb - last * a.seg_size);
-  t.total = (nseg - 1) * t.per_seg + (last_len + a.b - 1) / a.b;
-  return t;
+  return batch_tiles(a.seg_begin, a.seg_end, a.seg_size, a.nb, a.b);
 }
 
 // Tiles of group g for this CTA: returns how many (<= T) exist.
@@ -43,11 +35,7 @@ __device__ __forceinline__ int group_tiles(const MlpTArgs& a, const Tiles& ts, i
   for (int k = 0; k < a.L.T; ++k) {
     const long long t = blockIdx.x + static_cast<long long>(g * a.L.T + k) * gridDim.x;
     if (t >= ts.total) break;
-    const long long seg = a.seg_begin + t / ts.per_seg;
-    const long long s1 = min(seg * a.seg_size + a.seg_size, a.nb);
-    const long long r0 = seg * a.seg_size + (t % ts.per_seg) * a.b;
-    row0[k] = r0;
-    rows[k] = static_cast<int>(min((long long)a.b, s1 - r0));
+    row0[k] = batch_tile(ts, t, a.seg_begin, a.seg_size, a.nb, a.b, &rows[k]);
     ++n;
   }
   return n;

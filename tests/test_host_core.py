@@ -322,3 +322,31 @@ def test_bbs_matches_reference():
     got = es.bbs_baseline(c)
     np.testing.assert_array_equal(got.matrix.cells, want["matrix"])
     assert got.chosen_batches == want["chosen"] and got.bench_calls == want["calls"]
+
+
+def test_batcher_splits_segments_into_full_batches_plus_remainder():
+    """test_runtime.cpp:315-332: 300 rows (segments 128, 128, 44) at b = 32 ->
+    nine batches of 32 and one of 12; es.batch_rows is the tile space the
+    fused-head kernels run (csrc/cuda/batching.cuh)."""
+    import collections
+    tiles = es.batch_rows(300, 128, 32)
+    assert collections.Counter(r for _, r in tiles) == {32: 9, 12: 1}
+    # every row once, in order, no tile crossing a segment boundary
+    covered = [r0 + i for r0, r in tiles for i in range(r)]
+    assert covered == list(range(300))
+    for r0, r in tiles:
+        assert r0 // 128 == (r0 + r - 1) // 128
+    # a share of segments, odd batch and segment sizes, against a plain restatement
+    rng = np.random.default_rng(4)
+    for _ in range(50):
+        seg = int(rng.integers(1, 300))
+        nb = int(rng.integers(1, 5000))
+        b = int(rng.integers(1, 129))
+        S = (nb + seg - 1) // seg
+        s0 = int(rng.integers(0, S))
+        s1 = int(rng.integers(s0, S + 1))
+        want = []
+        for s in range(s0, s1):
+            lo, hi = s * seg, min((s + 1) * seg, nb)
+            want += [(r, min(b, hi - r)) for r in range(lo, hi, b)]
+        assert es.batch_rows(nb, seg, b, s0, s1) == want
