@@ -100,6 +100,11 @@ typedef struct es_pool_opts {
   int dp_equal_split;      /* 0 = a model's data-parallel workers split its segments in
                               runs proportional to their probed rows/s (SURVEY.md §8-E
                               static fallback of the shared FIFO); 1 = equal runs */
+  int row_partials;        /* 1 = fast gather: each device row folds its
+                              members into a partial on its GPU, only partials travel,
+                              summed in row order (fp32 order differs from the
+                              reference fold; votes exact; pure model placement only);
+                              0 = parity gather (bit-identical fold) */
 } es_pool_opts;
 
 /* RunStats (pipeline.hpp:19-25). */

@@ -45,7 +45,7 @@ class PoolOpts(C.Structure):
                 ("warmup", C.c_int), ("sms_per_worker", C.c_int),
                 ("overlap_colocated", C.c_int), ("e2e_chunk_rows", C.c_size_t),
                 ("e2e_host_convert", C.c_int), ("e2e_convert_eighths", C.c_int),
-                ("dp_equal_split", C.c_int)]
+                ("dp_equal_split", C.c_int), ("row_partials", C.c_int)]
 
 
 class RunStats(C.Structure):

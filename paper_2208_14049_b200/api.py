@@ -614,7 +614,7 @@ class CombinationRule:
 def _pool_opts(keep: list, device_map=None, copy_outputs=True, warmup=True,
                sms_per_worker=0, overlap_colocated=False, e2e_chunk_rows=0,
                e2e_host_convert=True, e2e_convert_eighths=0,
-               dp_equal_split=False) -> _abi.PoolOpts:
+               dp_equal_split=False, row_partials=False) -> _abi.PoolOpts:
     """PoolOptions (runtime.hpp)."""
     dm = None
     n = 0
@@ -625,7 +625,7 @@ def _pool_opts(keep: list, device_map=None, copy_outputs=True, warmup=True,
     o = _abi.PoolOpts(C.cast(dm, _abi.c_int_p) if dm is not None else None, n, int(copy_outputs),
                       int(warmup), int(sms_per_worker), int(overlap_colocated),
                       int(e2e_chunk_rows), int(e2e_host_convert), int(e2e_convert_eighths),
-                      int(dp_equal_split))
+                      int(dp_equal_split), int(row_partials))
     keep.append(o)
     return o
 

@@ -181,6 +181,7 @@ PoolOptions to_opts(const es_pool_opts* o) {
   p.e2e_host_convert = o->e2e_host_convert != 0;
   if (o->e2e_convert_eighths > 0) p.e2e_convert_eighths = o->e2e_convert_eighths;
   p.dp_equal_split = o->dp_equal_split != 0;
+  p.row_partials = o->row_partials != 0;
   return p;
 }
 

@@ -196,6 +196,17 @@ struct InferenceSystem::Impl {
   float* y = nullptr;
   int32_t* labels = nullptr;
   std::size_t cap_rows = 0;
+  // row_partials: per device row, its partial on its GPU and (remote rows)
+  // the copy on the combining GPU; rows without workers stay empty.
+  struct RowPartial {
+    int phys = 0;
+    float* local = nullptr;
+    float* at_combine = nullptr;  // == local when phys is the combining GPU
+    std::size_t rows = 0;
+    cudaEvent_t done = nullptr;
+  };
+  std::vector<RowPartial> partials;
+  bool partial_mode = false;
   // run_host pipeline (slots of whole-segment chunks)
   struct Slot {
     void* pinned = nullptr;
@@ -349,6 +360,13 @@ void InferenceSystem::shutdown() {
     cudaFree(impl_->y);
     cudaFree(impl_->labels);
     impl_->free_e2e();
+    for (Impl::RowPartial& p : impl_->partials) {
+      if (p.at_combine != p.local) cudaFree(p.at_combine);
+      cudaSetDevice(p.phys);
+      cudaFree(p.local);
+      if (p.done) cudaEventDestroy(p.done);
+      cudaSetDevice(combine_dev_);
+    }
     cudaEventDestroy(impl_->start);
     cudaEventDestroy(impl_->combine_begin);
     cudaEventDestroy(impl_->end);
@@ -466,6 +484,40 @@ void InferenceSystem::begin_run(std::shared_ptr<const SampleStore> X, Combinatio
   }
   if (!options_.dp_equal_split && rates_.empty() && nb > 0) probe_rates(*X);
   assign_shares(nb);
+  // Fast gather: one partial per device row (pure model placement only).
+  impl_->partial_mode = false;
+  if (options_.row_partials) {
+    const std::vector<int> per_model = workers_per_model();
+    bool single = true;
+    for (int n : per_model) single = single && n == 1;
+    impl_->partial_mode = single;
+  }
+  if (impl_->partial_mode) {
+    impl_->partials.resize(static_cast<std::size_t>(cluster_.device_count()));
+    for (auto& w : workers_) {
+      Impl::RowPartial& p = impl_->partials[static_cast<std::size_t>(w->row)];
+      p.phys = w->phys;
+      if (p.rows < nb) {
+        OnDevice on(p.phys);
+        if (p.at_combine != p.local) {
+          OnDevice oc(combine_dev_);
+          cudaFree(p.at_combine);
+        }
+        cudaFree(p.local);
+        ES_CUDA(cudaMalloc(&p.local, std::max<std::size_t>(nb, 1) * C * sizeof(float)));
+        p.at_combine = p.local;
+        if (p.phys != combine_dev_) {
+          OnDevice oc(combine_dev_);
+          ES_CUDA(cudaMalloc(&p.at_combine, std::max<std::size_t>(nb, 1) * C * sizeof(float)));
+        }
+        p.rows = nb;
+      }
+      if (!p.done) {
+        OnDevice on(p.phys);
+        ES_CUDA(cudaEventCreateWithFlags(&p.done, cudaEventDisableTiming));
+      }
+    }
+  }
   impl_->store = std::move(X);
   impl_->rule = std::move(rule);
   impl_->segments = S;
@@ -493,7 +545,7 @@ std::size_t InferenceSystem::broadcast() {
     launches_ += w->member->forward(X.device_replica(w->phys), nb, cluster_.segment_size,
                                     w->seg_begin, w->seg_end, out, grid, w->stream,
                                     w->marks.empty() ? nullptr : w->marks.data());
-    if (remote && w->seg_end > w->seg_begin) {
+    if (remote && w->seg_end > w->seg_begin && !impl_->partial_mode) {
       const long long r0 = w->seg_begin * cluster_.segment_size;
       const long long r1 = std::min<long long>(w->seg_end * cluster_.segment_size, nb);
       ES_CUDA(cudaMemcpyPeerAsync(impl_->logits[w->model] + r0 * C, combine_dev_,
@@ -502,6 +554,7 @@ std::size_t InferenceSystem::broadcast() {
     }
     ES_CUDA(cudaEventRecord(w->ev_done, w->stream));
   }
+  if (impl_->partial_mode && nb > 0) return broadcast_partials(nb);
   OnDevice on(combine_dev_);
   for (auto& w : workers_) ES_CUDA(cudaStreamWaitEvent(impl_->main, w->ev_done, 0));
   ES_CUDA(cudaEventRecord(impl_->combine_begin, impl_->main));
@@ -511,6 +564,72 @@ std::size_t InferenceSystem::broadcast() {
     ES_LAUNCH(es::combine_launch(ca, impl_->main));
     ++launches_;
   }
+  ES_CUDA(cudaEventRecord(impl_->end, impl_->main));
+  return impl_->segments;
+}
+
+// Fast gather (PoolOptions::row_partials): every device row folds its own
+// members on its GPU -- the same K3 kernel over the row's members with the
+// rule's per-member factor (avg: 1/M of the whole ensemble, wavg: w_m; vote:
+// tallies) -- and the combining GPU sums the partials in row order with factor
+// 1 (exact for tallies) and takes the argmax.
+std::size_t InferenceSystem::broadcast_partials(long long nb) {
+  const int C = output_width_;
+  const int M = cluster_.model_count();
+  const CombinationRule& rule = impl_->rule;
+  const bool vote = rule.kind == CombinationRule::Kind::majority_vote;
+  std::vector<float*> finals;
+  for (std::size_t d = 0; d < impl_->partials.size(); ++d) {
+    Impl::RowPartial& p = impl_->partials[d];
+    es::CombineArgs ca;
+    ca.C = C;
+    ca.rows = nb;
+    ca.y = p.local;
+    ca.argmax = nullptr;
+    ca.softmax = rule.member_softmax ? 1 : 0;
+    ca.rule = vote ? es::kVote : es::kWeighted;
+    Worker* last = nullptr;
+    for (auto& w : workers_) {
+      if (w->row != static_cast<int>(d)) continue;
+      ca.logits[ca.M] = w->phys != combine_dev_ ? w->staging : impl_->logits[w->model];
+      ca.weight[ca.M] = rule.kind == CombinationRule::Kind::weighted_averaging
+                            ? static_cast<float>(rule.weights[w->model])
+                            : 1.0f / static_cast<float>(M);
+      ++ca.M;
+      last = w.get();
+    }
+    if (!last) continue;
+    OnDevice on(p.phys);
+    for (auto& w : workers_)  // the row's workers may run on other streams
+      if (w->row == static_cast<int>(d) && w.get() != last)
+        ES_CUDA(cudaStreamWaitEvent(last->stream, w->ev_done, 0));
+    ES_LAUNCH(es::combine_launch(ca, last->stream));
+    ++launches_;
+    if (p.at_combine != p.local)
+      ES_CUDA(cudaMemcpyPeerAsync(p.at_combine, combine_dev_, p.local, p.phys,
+                                  static_cast<std::size_t>(nb) * C * sizeof(float), last->stream));
+    ES_CUDA(cudaEventRecord(p.done, last->stream));
+    finals.push_back(p.at_combine);
+  }
+  OnDevice on(combine_dev_);
+  for (auto& w : workers_) ES_CUDA(cudaStreamWaitEvent(impl_->main, w->ev_done, 0));
+  for (const Impl::RowPartial& p : impl_->partials)
+    if (p.done && p.rows) ES_CUDA(cudaStreamWaitEvent(impl_->main, p.done, 0));
+  ES_CUDA(cudaEventRecord(impl_->combine_begin, impl_->main));
+  es::CombineArgs fa;
+  fa.M = static_cast<int>(finals.size());
+  fa.C = C;
+  fa.rows = nb;
+  fa.y = impl_->y;
+  fa.argmax = impl_->labels;
+  fa.softmax = 0;
+  fa.rule = es::kWeighted;
+  for (int i = 0; i < fa.M; ++i) {
+    fa.logits[i] = finals[static_cast<std::size_t>(i)];
+    fa.weight[i] = 1.0f;
+  }
+  ES_LAUNCH(es::combine_launch(fa, impl_->main));
+  ++launches_;
   ES_CUDA(cudaEventRecord(impl_->end, impl_->main));
   return impl_->segments;
 }

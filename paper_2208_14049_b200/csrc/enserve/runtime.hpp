@@ -133,6 +133,14 @@ struct PoolOptions {
   // reference's shared FIFO, where faster workers pull more segments), or
   // equal runs.
   bool dp_equal_split = false;
+  // Gather: false = parity mode, every member's logits go
+  // to the combining GPU and one fold runs in model order (bit-identical to
+  // the reference); true = fast mode, each device row folds its own members
+  // into a partial [nb][C] (avg/wavg: sum of weighted (softmax) outputs;
+  // vote: tallies) and only the partials travel, summed in row order -- C
+  // floats per sample per row instead of per member.  fp32 sums in another
+  // order (votes stay exact); applies when no model is data-parallel.
+  bool row_partials = false;
 };
 
 // Per-model executable member on one GPU (the Predictor of backend.hpp:25-34).
@@ -205,6 +213,7 @@ class InferenceSystem {
   };
   using HostFill = std::function<HostChunk(std::size_t, std::uint16_t*, std::size_t, std::size_t)>;
   void probe_rates(const SampleStore& X);
+  std::size_t broadcast_partials(long long nb);
   std::vector<double> rates_;  // per worker, probed on the first run with a DP column
   double run_host_core(std::size_t nb, std::size_t width, float* Y_out, std::int32_t* labels_out,
                        const HostFill& fill);

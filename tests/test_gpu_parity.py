@@ -390,3 +390,33 @@ def test_member_handles_used_concurrently_from_worker_threads():
     for i in range(len(models)):
         for o in got[i]:
             np.testing.assert_array_equal(o, want[i])
+
+
+@pytest.mark.parametrize("rule", ["avg", "avg_softmax", "wavg", "vote"])
+def test_row_partial_gather_matches_parity_gather(rule):
+    """SURVEY.md §8-E fast mode: each device row folds its members into a
+    partial and only partials are summed on the combining GPU.  Votes are
+    exact; probability sums differ from the model-order fold only by fp32
+    rounding."""
+    c = mlp_cluster([256, 128, 384, 256, 128], [128] * 5, devices=3)
+    A = es.AllocationMatrix.from_array([[128, 0, 64, 0, 0], [0, 32, 0, 0, 128],
+                                        [0, 0, 0, 128, 0]])
+    r = {"avg": es.CombinationRule.averaging(),
+         "avg_softmax": es.CombinationRule.averaging(softmax=True),
+         "wavg": es.CombinationRule.weighted([0.3, 0.1, 0.2, 0.25, 0.15]),
+         "vote": es.CombinationRule.majority_vote()}[rule]
+    X = es.SampleStore(synthetic_seed=9, nb=5000, width=784, device=0)
+    with es.InferenceSystem(A, c, r, device_map=[0, 0, 0]) as s:
+        ref = s.run(X)
+    with es.InferenceSystem(A, c, r, device_map=[0, 0, 0], row_partials=True) as s:
+        got = s.run(X)
+        assert s.launches_last_run() > 0
+    if rule == "vote":
+        np.testing.assert_array_equal(got.combined, ref.combined)
+        np.testing.assert_array_equal(got.winners, ref.winners)
+    else:
+        scale = np.abs(ref.combined).max(axis=1, keepdims=True) + 1e-30
+        assert (np.abs(got.combined - ref.combined) / scale).max() < 1e-5
+        srt = np.sort(ref.combined, axis=1)
+        clear = (srt[:, -1] - srt[:, -2]) > 1e-4 * scale[:, 0]
+        np.testing.assert_array_equal(got.winners[clear], ref.winners[clear])
