@@ -91,3 +91,35 @@ def test_text_report_and_error_exit_codes(tmp_path):
     bad.write_text(json.dumps(doc))
     rc, _, err = cli("--cluster", str(bad), "--bench-mode", "analytic", "optimize")
     assert rc == 2 and "enserve:" in err
+
+
+@pytest.mark.gpu
+def test_measured_optimize_and_bench_on_the_b200_backend(tmp_path):
+    """`optimize` / `bench` with --bench-mode measured run the device-timed
+    bench (es_bench) as the greedy's ScoreFn (commands.cpp:132-150) on the
+    members the spec's "arch" objects describe."""
+    sys.path.insert(0, str(ROOT))
+    import paper_2208_14049_b200 as es
+    c = es.ClusterSpec([es.DeviceSpec(0, es.GPU, 160000.0, 1e9, 0.0)],
+                       [es.mlp_model(0, "a", [784, 256, 10], 5), es.mlp_model(1, "b", [784, 128, 10], 6)],
+                       [8, 32, 128], 128)
+    spec = tmp_path / "cluster.json"
+    spec.write_text(es.cluster_to_json(c, with_arch=True))
+    rc, out, err = cli("--cluster", str(spec), "--bench-mode", "measured", "--backend", "b200",
+                       "--calib-samples", "8192", "--input-width", "784", "--max-iter", "3",
+                       "--json", "optimize")
+    assert rc == 0, err
+    rep = json.loads(out)
+    assert rep["bench_calls"] > 1 and rep["score"] > 0
+    best = rep["best_matrix"]
+    rc, out, err = cli("--cluster", str(spec), "--bench-mode", "measured", "--backend", "b200",
+                       "--calib-samples", "8192", "--input-width", "784", "--json", "bench",
+                       "--matrix", str(_write_matrix(tmp_path, best)))
+    assert rc == 0, err
+    assert json.loads(out)["throughput"] > 0
+
+
+def _write_matrix(tmp_path, best):
+    p = tmp_path / "matrix.json"
+    p.write_text(json.dumps(best) if isinstance(best, dict) else json.dumps({"entries": best}))
+    return p
