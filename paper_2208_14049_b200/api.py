@@ -863,6 +863,7 @@ class ServiceStats:
     pending_requests: int
     pending_samples: int
     uptime_s: float
+    matrix: list = None  # the allocation matrix being served (server.cpp:88-107 "matrix")
 
 
 class PendingPrediction:
@@ -914,6 +915,7 @@ class PredictionService:
             input_width = arch.input_width()
         self.input_width = int(input_width)
         self.C = cluster.models[0].output_width
+        self.matrix = A.cells.tolist()
         h = C.c_void_p()
         with _Desc(cluster) as d:
             _check(lib().es_service_create(d.ptr, A.ptr(), C.byref(rule._desc(keep)),
@@ -951,7 +953,7 @@ class PredictionService:
         _check(lib().es_service_stats(self._h, C.byref(st)))
         return ServiceStats(bool(st.ready), st.requests_served, st.samples_served, st.flushes,
                             st.last_flush_throughput, st.pending_requests, st.pending_samples,
-                            st.uptime_s)
+                            st.uptime_s, self.matrix)
 
     def close(self) -> None:
         if getattr(self, "_h", None):

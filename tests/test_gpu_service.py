@@ -58,6 +58,7 @@ def test_predictions_identical_to_offline_runtime(kind):
         st = svc.stats()
         assert st.ready and st.samples_served >= 5 and st.requests_served >= 1
         assert st.pending_requests == 0 and st.flushes >= 1 and st.uptime_s > 0
+        assert st.matrix == A.cells.tolist()  # test_server.cpp:210-217
 
 
 def test_full_segment_flushes_immediately_single_sample_waits_timer():
