@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--matrix", default="128,128,128,128")
     ap.add_argument("--chunk", type=int, default=0, help="e2e_chunk_rows (0 = pool default)")
+    ap.add_argument("--arena", type=int, default=-1, help="arena_rows (-1 = default)")
     args = ap.parse_args()
     cfg = bench.CONFIGS[args.config]
     cluster = bench.make_cluster(es, cfg)
@@ -42,7 +43,7 @@ def main():
     lock = threading.Lock()
     stop_at = [0.0]
     with es.PredictionService(cluster, A, flush_timeout_ms=args.flush_ms, input_width=W,
-                              e2e_chunk_rows=args.chunk) as svc:
+                              e2e_chunk_rows=args.chunk, arena_rows=args.arena) as svc:
         assert svc.wait_ready(120.0), svc.startup_error
         svc.predict(pool[0])  # warm-up
 
@@ -70,7 +71,7 @@ def main():
     lat_ms = np.array(lat) * 1e3
     print(json.dumps({
         "config": args.config, "matrix": A.cells.tolist(),
-        "clients": args.clients, "chunk_rows": args.chunk, "rows_per_request": args.rows, "flush_timeout_ms": args.flush_ms,
+        "clients": args.clients, "chunk_rows": args.chunk, "arena_rows": args.arena, "rows_per_request": args.rows, "flush_timeout_ms": args.flush_ms,
         "samples_per_s": served / wall, "requests_per_s": len(lat) / wall,
         "flushes": st.flushes - base.flushes,
         "samples_per_flush": served / max(st.flushes - base.flushes, 1),
