@@ -386,7 +386,7 @@ typedef struct es_service_info {
 /* Validates A (ES_ERR_SPEC if invalid, server.cpp:30-31) and starts building
  * the device pool on a background thread (init_pool, server.cpp:37-52). */
 /* arena_rows: rows per page-locked staging arena of a one-GPU pool (two
- * arenas; submits convert to bf16 straight into them), < 0 = default 131072,
+ * arenas; submits convert to bf16 straight into them), < 0 = default 262144,
  * 0 = none (requests staged in private buffers and gathered per flush). */
 es_status es_service_create(const es_cluster_desc* c, const int* A, const es_rule_desc* rule,
                             const es_pool_opts* opts, int flush_timeout_ms, size_t input_width,

@@ -28,7 +28,9 @@ struct ServiceConfig {  // ServeConfig (server.hpp:19-26), minus bind host / por
   // One-GPU pools: rows per page-locked arena (two: one filling while the
   // other flushes).  Requests are converted to bf16 straight into the open
   // arena by the submitting thread and DMA'd from there; 0 = no arenas.
-  std::size_t arena_rows = 131072;
+  // 262144 rows of 784 features = 2 x 411 MB page-locked (profiles/
+  // r1j_service_load.md: requests that overflow an arena take the gather path).
+  std::size_t arena_rows = 262144;
 };
 
 struct ServiceStats {  // GET /v1/stats (server.cpp:88-107)
