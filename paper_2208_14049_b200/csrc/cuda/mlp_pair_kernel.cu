@@ -127,6 +127,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       // ------------------------------------------------------------ TMA (both SMs)
       const uint64_t pol_stream = l2_policy_evict_first();
       const uint64_t pol_keep = l2_policy_evict_last();
+      // Hidden passes re-read the same X tiles right away: every pass but the
+      // last keeps them in L2 (evict_last), the last lets them go.
+      const uint64_t pol_reread = l2_policy_evict_last();
       if (leader) mbar_arrive_expect_tx(w2_full, 2u * static_cast<uint32_t>(H / 64) * 1024u);
       for (int kc = 0; kc < H / 64; ++kc)
         tma_load_2d_pair(sW2 + kc * 1024, &tm_w2, w2_full, kc * 64, static_cast<int32_t>(rank) * 8,
@@ -149,7 +152,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                                                         static_cast<uint32_t>(HP) * 64u));
             for (int k = 0; k < n; ++k)
               tma_load_2d_pair(st + k * 16384, &tm_x, &full[stage], kc * 64,
-                               static_cast<int32_t>(row0[k]), pol_stream);
+                               static_cast<int32_t>(row0[k]),
+                               hp + 1 < L.passes ? pol_reread : pol_stream);
             uint8_t* sw = st + L.T * 16384;
             for (int h = 0; h < L.nh; ++h)
               tma_load_2d_pair(sw + h * half_w * 128u, &tm_w1, &full[stage], kc * 64,
