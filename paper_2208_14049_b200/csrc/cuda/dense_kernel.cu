@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      const uint64_t pol_stream = l2_policy_evict_first();
+      const uint64_t pol_stream = l2_policy_evict_normal();  // evict_first on X cost the weights their L2 residency
       const uint64_t pol_keep = l2_policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;

@@ -113,7 +113,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------------------ TMA (both SMs)
-      const uint64_t pol_stream = l2_policy_evict_first();
+      const uint64_t pol_stream = l2_policy_evict_normal();  // evict_first on X cost the weights their L2 residency
       const uint64_t pol_keep = l2_policy_evict_last();
       const uint32_t half_w = static_cast<uint32_t>(L.NH / 2);
       int stage = 0;

@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------ TMA producer
-      const uint64_t pol_stream = l2_policy_evict_first();  // X: read once
+      const uint64_t pol_stream = l2_policy_evict_normal();  // X: read once; evict_first cost W its L2 residency
       const uint64_t pol_keep = l2_policy_evict_last();     // weights: every CTA re-reads
       mbar_arrive_expect_tx(w2_full, static_cast<uint32_t>(kc2n) * 2048u);
       for (int kc = 0; kc < kc2n; ++kc)

@@ -125,7 +125,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------------------ TMA (both SMs)
-      const uint64_t pol_stream = l2_policy_evict_first();
+      const uint64_t pol_stream = l2_policy_evict_normal();  // evict_first on X cost the weights their L2 residency
       const uint64_t pol_keep = l2_policy_evict_last();
       // Hidden passes re-read the same X tiles right away: every pass but the
       // last keeps them in L2 (evict_last), the last lets them go.

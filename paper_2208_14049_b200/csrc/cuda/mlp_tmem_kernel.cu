@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------------------ TMA producer
-      const uint64_t pol_stream = l2_policy_evict_first();
+      const uint64_t pol_stream = l2_policy_evict_normal();  // evict_first on X cost the weights their L2 residency
       const uint64_t pol_keep = l2_policy_evict_last();
       mbar_arrive_expect_tx(w2_full, static_cast<uint32_t>(H / 64) * 2048u);
       for (int kc = 0; kc < H / 64; ++kc)
