@@ -55,7 +55,7 @@ CONFIGS = {
              "workload": "cfg1: 2-member MLP ensemble (784-256-10 x 2), batch 32, averaging rule, "
                          "1 device, as run by the CPU reference"},
     "cfg2": {"roster": ROSTER, "devices": 1, "device_mib": 183359.0, "matrix": "greedy",
-             "softmax": True,
+             "softmax": True, "ref_matrix": [[128, 128, 128, 128]],
              "workload": "cfg2: 4 heterogeneous MLP/CNN members (784-256-10, 784-512-512-10, "
                          "784-1024-10, CNN-s 28x28-c4x4/4:64-c3x3:32-128-10) co-located on 1 B200, "
                          "batches from bounded greedy over calib_data; avg of softmax + argmax"},
@@ -64,11 +64,16 @@ CONFIGS = {
                          "dozen memory spec) worst-fit-decreasing packed into 4 device rows; avg of "
                          "softmax + argmax"},
     "cfg4": {"roster": [("mlp2048x2", "mlp", [784, 2048, 2048, 10], 41)], "devices": 1,
-             "device_mib": 183359.0, "matrix": "greedy", "softmax": True,
+             "device_mib": 183359.0, "matrix": "greedy", "softmax": True, "ref_matrix": [[128]],
              "workload": "cfg4: single DNN (MLP 784-2048-2048-10) data-parallel, per-GPU batch "
                          "slices; batch from bounded greedy (batch-size-only baseline applies)"},
     "cfg5": {"roster": DOZEN, "devices": 8, "device_mib": 16000.0, "matrix": "greedy",
              "softmax": True,
+             # the device greedy's result on B200 (profiles/r1k_configs.json)
+             "ref_matrix": [[8, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0], [0, 64, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0],
+                            [0, 0, 64, 0, 0, 0, 128, 0, 0, 0, 0, 0], [0, 0, 0, 8, 0, 0, 0, 0, 0, 0, 0, 0],
+                            [0, 0, 0, 0, 64, 128, 0, 0, 0, 0, 0, 8], [0, 0, 0, 0, 0, 8, 0, 128, 0, 0, 128, 0],
+                            [128, 0, 0, 0, 0, 0, 8, 0, 0, 8, 0, 0], [0, 0, 0, 128, 0, 0, 0, 8, 64, 0, 0, 0]],
              "workload": "cfg5: full allocation optimizer sweep (worst-fit-decreasing + bounded "
                          "greedy, device-timed bench) for the 12-member ensemble on 8 device rows"},
 }
@@ -340,39 +345,120 @@ def roofline_for(es, cluster, A, kernels: list, nb: int, pk: dict) -> dict:
             "per_kernel": per_kernel}
 
 
-def cpu_baseline(cluster, A_cells: np.ndarray, budget_s: float = 12.0, softmax: bool = True) -> dict:
-    """The reference InferenceSystem (compiled from /root/reference by
-    oracle/Makefile) with the oracle CPU member, on this box's host cores:
-    every model data-parallel over floor(cores / M) CPU 'devices' (batch =
-    its largest batch in A) so all cores compute.  Bounded sample; returns
-    samples/s."""
+# ------------------------------------------------------------------ CPU reference (no product)
+class _Ns:
+    def __init__(self, **kw):
+        self.__dict__.update(kw)
+
+
+def _arch_footprint(kind: str, w: list) -> tuple:
+    """(weight_mib, act_mib_per_sample, cost_per_sample) of a member shape —
+    the product's derive_footprint (spec.cpp parameter_count /
+    activation_elems / flops_per_sample) restated so the reference arm
+    imports nothing from the product."""
+    if kind == "cnn":
+        S, P, c1, c2, hidden, Cn = w
+        G2 = (S // P) ** 2
+        dims = [(P * P, c1), (9 * c1, c2), (G2 * c2, hidden), (hidden, Cn)]
+        flops = 2.0 * (G2 * dims[0][0] * dims[0][1] + G2 * dims[1][0] * dims[1][1] +
+                       dims[2][0] * dims[2][1] + dims[3][0] * dims[3][1])
+        act = S * S + G2 * (c1 + c2) + hidden + Cn
+    else:
+        dims = list(zip(w[:-1], w[1:]))
+        flops = float(sum(2.0 * a * b for a, b in dims))
+        act = float(sum(w))
+    params = sum(a * b + b for a, b in dims)
+    mib = 1024.0 * 1024.0
+    return params * 2.0 / mib, act * 2.0 / mib, flops
+
+
+def plain_cluster(cfg: dict, devices: int = 0, kind: str = "GPU"):
+    """The config's cluster as plain Python objects (duck-typed for
+    oracle/refcpu): the reference arm must not load the product."""
+    models = []
+    for i, r in enumerate(cfg["roster"]):
+        name, k, w, seed = r[:4]
+        wm, am, cost = _arch_footprint(k, list(w))
+        if len(r) >= 6:
+            wm, am = r[4], r[5]
+        models.append(_Ns(id=i, name=name, weight_mib=wm, act_mib_per_sample=am,
+                          cost_per_sample=cost, output_width=list(w)[-1],
+                          arch=_Ns(kind=k, widths=tuple(w), weight_seed=seed)))
+    n = devices or cfg["devices"]
+    devs = [_Ns(id=d, kind=kind, memory_mib=cfg["device_mib"] if kind == "GPU" else 1e9,
+                compute_rate=1e15 if kind == "GPU" else 1.0, batch_overhead_s=0.0)
+            for d in range(n)]
+    return _Ns(devices=devs, models=models, batch_menu=list(MENU), segment_size=128)
+
+
+def reference_matrix(cfg: dict) -> list:
+    """The matrix both arms run: the config's fixed batches, WFD (reference's
+    own worst_fit_decreasing from oracle/_ref), or the matrix the device
+    greedy reaches on B200 (recorded per config)."""
     from oracle import refcpu
-    import paper_2208_14049_b200 as es
-    cores = refcpu.host_cores()
-    M = cluster.model_count()
-    D = max(1, cores // M)
-    cpu_cluster = es.ClusterSpec([es.DeviceSpec(d, es.CPU, 1e9, 1.0, 0.0) for d in range(D)],
-                                 cluster.models, list(MENU), cluster.segment_size)
-    A = np.tile(np.asarray(A_cells).max(axis=0), (D, 1)).astype(np.int32)
-    sysr = refcpu.RefSystem(cpu_cluster, A, softmax=softmax)
-    nb = 512 * D
-    X = refcpu.features(5, nb, 784)
-    el, _ = sysr.run(X)  # warm-up + size the sample to the budget
-    per_sample = el / nb
-    nb = int(min(max(nb, budget_s / 3 / max(per_sample, 1e-9)), 1 << 20))
+    if cfg["matrix"] == "fixed":
+        return [list(cfg["batches"])]
+    if cfg["matrix"] == "wfd":
+        return refcpu.ref_wfd(plain_cluster(cfg), MENU[0]).tolist()
+    return [list(r) for r in cfg["ref_matrix"]]
+
+
+def _timed_ref_runs(sysr, nb: int, budget_s: float, seed: int, steps: int = 3) -> tuple:
+    """Size nb to ~budget_s / steps per run (one probe run), then time `steps`
+    runs of the reference InferenceSystem; returns (nb, [samples/s])."""
+    from oracle import refcpu
+    X = refcpu.features(seed, nb, 784)
+    el, _ = sysr.run(X)
+    per = el / nb
+    nb = int(min(max(nb, budget_s / steps / max(per, 1e-9)), 1 << 20))
     nb = max(128, nb // 128 * 128)
-    X = refcpu.features(6, nb, 784)
+    X = refcpu.features(seed + 1, nb, 784)
     runs = []
-    for _ in range(3):
+    for _ in range(steps):
         el, _ = sysr.run(X)
         runs.append(nb / el)
+    return nb, runs
+
+
+def cpu_baseline(cfg: dict, A_cells, budget_s: float = 12.0, faithful_budget_s: float = 4.0) -> dict:
+    """The reference InferenceSystem (compiled from /root/reference by
+    oracle/Makefile) with the oracle CPU member, on this box's host cores
+    (BASELINE.md §4):
+      (ii) all-cores — every model data-parallel over floor(cores / M) CPU
+           device rows (batch = its largest batch in A), the headline figure;
+      (i)  matrix-faithful — exactly A (one CPU device per row of A), one
+           compute thread per nonzero cell, as the reference would run it.
+    Bounded samples; samples/s medians."""
+    from oracle import refcpu
+    cores = refcpu.host_cores()
+    M = len(cfg["roster"])
+    A = np.asarray(A_cells, dtype=np.int32)
+    D = max(1, cores // M)
+    allc = np.tile(A.max(axis=0), (D, 1)).astype(np.int32)
+    sysr = refcpu.RefSystem(plain_cluster(cfg, D, "CPU"), allc, softmax=cfg["softmax"])
+    nb, runs = _timed_ref_runs(sysr, 512 * D, budget_s, 5)
     sysr.close()
     return {"value": round(statistics.median(runs), 1), "unit": "samples/s", "cores": D * M,
             "kind": "reference",
             "sample": f"{nb} samples x 3 runs (median) of the reference InferenceSystem "
                       f"(pipeline.cpp, -O3) with the oracle CPU member (AVX2 fp32, bf16-quantised "
-                      f"operands), matrix {A.tolist()} over {D} CPU rows x {M} members "
-                      f"= {D * M} compute threads on {cores} host cores"}
+                      f"operands), matrix {allc.tolist()} over {D} CPU rows x {M} members "
+                      f"= {D * M} compute threads on {cores} host cores",
+            "matrix_faithful": cpu_matrix_faithful(cfg, A, faithful_budget_s)}
+
+
+def cpu_matrix_faithful(cfg: dict, A_cells, budget_s: float = 4.0) -> dict:
+    """BASELINE.md §4 figure (i): the reference InferenceSystem on exactly A
+    (one CPU device per row of A, one compute thread per nonzero cell)."""
+    from oracle import refcpu
+    A = np.asarray(A_cells, dtype=np.int32)
+    sysf = refcpu.RefSystem(plain_cluster(cfg, A.shape[0], "CPU"), A, softmax=cfg["softmax"])
+    nbf, runs_f = _timed_ref_runs(sysf, 512, budget_s, 7)
+    sysf.close()
+    return {"value": round(statistics.median(runs_f), 1), "unit": "samples/s",
+            "matrix": A.tolist(), "compute_threads": int((A > 0).sum()),
+            "sample": f"{nbf} samples x 3 runs (median), one CPU device per row of A, one "
+                      f"compute thread per worker"}
 
 
 # ------------------------------------------------------------------ arms
@@ -537,38 +623,65 @@ def run_b200(args, dist: Dist) -> dict | None:
         "clocks": clocks.summary(),
         "host_wall_s": round(wall, 4),
     }
+    result["config"]["same_config"] = (cfg["matrix"] == "wfd" or
+                                       A.cells.tolist() == reference_matrix(cfg))
     if args.cpu_baseline and n == 1:
-        result["cpu_baseline"] = cpu_baseline(cluster, A.cells, softmax=cfg["softmax"])
+        result["cpu_baseline"] = cpu_baseline(cfg, A.cells)
     return result
 
 
 def run_reference(args, dist: Dist) -> dict | None:
     """The reference's own CPU implementation of the path on this box's host
     cores: its InferenceSystem (compiled from /root/reference sources into
-    oracle/_ref) with the oracle CPU member — same config, metric and unit."""
+    oracle/_ref) with the oracle CPU member — same config, matrix, metric and
+    unit as the b200 arm; nothing from the product is imported.  W warm-up
+    and K timed steps, each a bounded sample (all cores busy)."""
     if dist.rank != 0:
         return None
-    import paper_2208_14049_b200 as es
     from oracle import refcpu
     cfg = CONFIGS[args.config]
-    cluster = make_cluster(es, cfg)
-    # The reference cannot time a GPU bench: take the b200 arm's matrix shape
-    # with the batch sizes WFD gives (A1), which is what the reference's
-    # optimizer starts from (cfg1: its fixed batch 32).
-    A1 = es.worst_fit_decreasing(cluster, 32 if cfg["matrix"] != "fixed" else cfg["batches"][0])
-    base = cpu_baseline(cluster, A1.cells, budget_s=max(4.0, 2.0 * args.steps),
-                        softmax=cfg["softmax"])
-    value = base["value"]
+    A = np.asarray(reference_matrix(cfg), dtype=np.int32)
+    cores = refcpu.host_cores()
+    M = len(cfg["roster"])
+    D = max(1, cores // M)
+    allc = np.tile(A.max(axis=0), (D, 1)).astype(np.int32)
+    sysr = refcpu.RefSystem(plain_cluster(cfg, D, "CPU"), allc, softmax=cfg["softmax"])
+    # step size: the whole W + K run within ~args.ref_budget_s seconds
+    per_step = max(0.5, args.ref_budget_s / max(1, args.steps + args.warmup))
+    X = refcpu.features(5, 512 * D, 784)
+    el, _ = sysr.run(X)
+    nb = int(min(max(128, per_step / max(el / len(X), 1e-9)), 1 << 20)) // 128 * 128
+    nb = max(128, nb)
+    X = refcpu.features(6, nb, 784)
+    for _ in range(args.warmup):
+        sysr.run(X)
+    times = []
+    for _ in range(args.steps):
+        el, _ = sysr.run(X)
+        times.append(el)
+    sysr.close()
+    total = float(sum(times))
+    value = nb * args.steps / total
+    faithful = cpu_matrix_faithful(cfg, A) if args.ref_faithful else None
     return {
         "impl": "reference",
         "metric": "ensemble samples/sec at 1/2/4/8 B200 vs batch-only baseline and CPU ref",
-        "value": value, "unit": "samples/s", "n_gpus": dist.world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32 (bf16-quantised operands)",
-        "data": "synthetic", "config": {"workload": cfg["workload"] + " -- on host cores (reference runtime)",
-                                       "config": args.config},
-        "cpu_baseline": base,
-        "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
+        "value": round(value, 1), "unit": "samples/s", "n_gpus": dist.world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(total / args.steps * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32 (bf16-quantised operands)", "data": "synthetic (U[0,1) features; Glorot-uniform weights)",
+        "config": {"workload": cfg["workload"] + " -- on host cores (reference runtime)",
+                   "config": args.config, "matrix": A.tolist(), "same_config": True,
+                   "samples_per_step": nb,
+                   "note": "same roster, weights, matrix and rule as the b200 arm; each step a "
+                           "bounded sample (the b200 arm runs 2^22 samples per step)"},
+        "cpu_baseline": {"value": round(value, 1), "unit": "samples/s", "cores": D * M,
+                         "kind": "reference",
+                         "sample": f"{args.steps} steps x {nb} samples of the reference "
+                                   f"InferenceSystem, matrix {allc.tolist()} ({D} CPU rows x "
+                                   f"{M} members, {cores} host cores)",
+                         "matrix_faithful": faithful},
+        "e2e": {"value": round(value, 1), "unit": "samples/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
 
@@ -591,6 +704,10 @@ def main():
     ap.add_argument("--matrix", default="",
                     help="profiling: batch per member, rows separated by ';' (e.g. 64,64,128,128), "
                          "skips the greedy")
+    ap.add_argument("--ref-budget-s", type=float, default=120.0,
+                    help="--impl reference: seconds for the whole warm-up + timed run")
+    ap.add_argument("--no-ref-faithful", dest="ref_faithful", action="store_false",
+                    help="--impl reference: skip the matrix-faithful figure")
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS),
                     help="BASELINE.json config (default cfg2, the metric's config)")
     args = ap.parse_args()

@@ -74,6 +74,23 @@ def _check(status: int) -> None:
         raise _STATUS.get(status, EnserveError)(msg)
 
 
+# K3 combine limits (csrc/cuda/aux_kernels.cuh kMaxMembers / kMaxClasses).
+MAX_MEMBERS = 32
+MAX_CLASSES = 16
+
+
+def _require_out(a, dtype, shape: tuple, what: str) -> None:
+    """An output array the C side writes rows * C elements into: it must have
+    exactly that dtype, shape and C-contiguous layout (None = not wanted)."""
+    if a is None:
+        return
+    if not isinstance(a, np.ndarray) or a.dtype != dtype or a.shape != shape or \
+            not a.flags.c_contiguous or not a.flags.writeable:
+        got = (a.dtype, a.shape) if isinstance(a, np.ndarray) else type(a).__name__
+        raise InvalidArgument(f"{what} must be a writable C-contiguous {np.dtype(dtype).name} "
+                              f"array of shape {shape}, got {got}")
+
+
 # ------------------------------------------------------------------ specs
 GPU, CPU = "GPU", "CPU"
 
@@ -783,9 +800,17 @@ class InferenceSystem:
         return self.await_run(copy)
 
     def run_host(self, X: np.ndarray, Y: np.ndarray = None, labels: np.ndarray = None) -> float:
-        """End-to-end from host memory; returns the CUDA-event seconds."""
+        """End-to-end from host memory: X (nb, width) fp32 in, the combined
+        output into Y (nb, C) float32 and the argmax into labels (nb,) int32
+        (each optional, C-contiguous, written in place).  Returns the host
+        wall-clock seconds of the whole pipelined call (host conversion,
+        copies and kernels)."""
         X = np.ascontiguousarray(X, dtype=np.float32)
+        if X.ndim != 2:
+            raise InvalidArgument(f"run_host: X must be 2-D (nb, width), got shape {X.shape}")
         nb, width = X.shape
+        _require_out(Y, np.float32, (nb, self.C), "Y")
+        _require_out(labels, np.int32, (nb,), "labels")
         el = C.c_double()
         _check(lib().es_system_run_host(
             self._h, X.ctypes.data_as(_abi.c_float_p), nb, width,
@@ -988,6 +1013,8 @@ class Member:
 
     def predict(self, features: np.ndarray, first_index: int = 0) -> np.ndarray:
         f = np.ascontiguousarray(features, dtype=np.float32)
+        if f.ndim != 2:
+            raise InvalidArgument(f"predict: features must be 2-D (rows, width), got shape {f.shape}")
         out = np.zeros((f.shape[0], self.C), dtype=np.float32)
         _check(lib().es_member_predict(self._h, f.ctypes.data_as(_abi.c_float_p), first_index,
                                        f.shape[0], f.shape[1], out.ctypes.data_as(_abi.c_float_p)))
@@ -1003,7 +1030,20 @@ def combine(rule: CombinationRule, blocks: Sequence[np.ndarray]) -> tuple:
     """Device fold of per-model blocks (combine.cpp:93-136) -> (Y, winners)."""
     keep: list = []
     arrs = [np.ascontiguousarray(b, dtype=np.float32) for b in blocks]
+    if not arrs:
+        raise InvalidArgument("combine: no member blocks")
+    if len(arrs) > MAX_MEMBERS:
+        raise InvalidArgument(f"combine: at most {MAX_MEMBERS} member blocks, got {len(arrs)}")
+    # PredictionAccumulator::add rejects a block of the wrong shape
+    # (combine.cpp:63-77): every block must be rows x C like the first.
+    if arrs[0].ndim != 2:
+        raise ProtocolError(f"combine: block 0 must be 2-D (rows, C), got shape {arrs[0].shape}")
     rows, Cw = arrs[0].shape
+    if Cw > MAX_CLASSES:
+        raise InvalidArgument(f"combine: at most {MAX_CLASSES} classes, got {Cw}")
+    for m, a in enumerate(arrs):
+        if a.shape != (rows, Cw):
+            raise ProtocolError(f"combine: block {m} has shape {a.shape}, expected {(rows, Cw)}")
     ptrs = (_abi.c_float_p * len(arrs))(*[a.ctypes.data_as(_abi.c_float_p) for a in arrs])
     Y = np.zeros((rows, Cw), dtype=np.float32)
     W = np.zeros(rows, dtype=np.int32)

@@ -22,6 +22,9 @@ ThreadPool::~ThreadPool() {
 }
 
 void ThreadPool::run(const std::function<void(int, int)>& fn) {
+  // One job at a time: a second caller (another thread sharing the pool)
+  // waits here instead of overwriting job_/pending_ of the running one.
+  std::lock_guard<std::mutex> serial(run_mu_);
   std::unique_lock<std::mutex> lock(mu_);
   job_ = &fn;
   pending_ = size();
@@ -68,9 +71,22 @@ __attribute__((target("avx512f,avx512bf16"))) void convert_avx512bf16(const floa
   // which saves a third of the host-memory traffic of a converted chunk.
   std::size_t i = 0;
   for (; i < n && (reinterpret_cast<std::uintptr_t>(y + i) & 63u); ++i) y[i] = bf16_rn(x[i]);
+  const __m512i expo = _mm512_set1_epi32(0x7f800000), mant = _mm512_set1_epi32(0x007fffff);
   for (; i + 32 <= n; i += 32) {
     __m512 a = _mm512_loadu_ps(x + i);
     __m512 b = _mm512_loadu_ps(x + i + 16);
+    // VCVTNE2PS2BF16 flushes fp32 subnormals to zero; bf16_rn (and the
+    // device's __float2bfloat16_rn) keeps them as bf16 subnormals, so a
+    // vector holding one takes the scalar rule.
+    const __m512i ua = _mm512_castps_si512(a), ub = _mm512_castps_si512(b);
+    const __mmask16 sa = _mm512_testn_epi32_mask(ua, expo) & _mm512_test_epi32_mask(ua, mant);
+    const __mmask16 sb = _mm512_testn_epi32_mask(ub, expo) & _mm512_test_epi32_mask(ub, mant);
+    if (sa | sb) {
+      alignas(64) std::uint16_t tmp[32];
+      for (int j = 0; j < 32; ++j) tmp[j] = bf16_rn(x[i + j]);
+      _mm512_stream_si512(reinterpret_cast<__m512i*>(y + i), _mm512_load_si512(tmp));
+      continue;
+    }
     __m512bh p = _mm512_cvtne2ps_pbh(b, a);  // low half from a
     _mm512_stream_si512(reinterpret_cast<__m512i*>(y + i), reinterpret_cast<__m512i>(p));
   }

@@ -29,6 +29,7 @@ class ThreadPool {
   void loop(int index);
   std::vector<std::thread> workers_;
   std::mutex mu_;
+  std::mutex run_mu_;  // serialises run() across callers
   std::condition_variable cv_, done_cv_;
   const std::function<void(int, int)>* job_ = nullptr;
   std::uint64_t generation_ = 0;

@@ -1004,6 +1004,12 @@ void B200Predictor::predict(const float* features, std::size_t first_index, std:
                             std::size_t width, float* out) {
   if (!s_->member) throw Error("predict before a successful load()");
   const int C = s_->model.output_width;
+  // The member kernels' TMA maps are [rows][input_width]: a narrower row
+  // would make them read past the staging buffer (begin_run checks the same).
+  if (s_->model.arch.kind != MemberArch::Kind::Synthetic &&
+      width != static_cast<std::size_t>(s_->model.arch.input_width()))
+    throw SpecError(s_->model.name + ": input width " + std::to_string(s_->model.arch.input_width()) +
+                    " differs from the batch's " + std::to_string(width));
   if (rows == 0) return;
   OnDevice on(s_->device);
   const std::size_t n = rows * width;

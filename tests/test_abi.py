@@ -99,3 +99,40 @@ def test_host_bf16_converter_special_values_and_odd_lengths():
         finite = np.isfinite(x)
         want = (round_bf16(x[finite]).view(np.uint32) >> 16).astype(np.uint16)
         np.testing.assert_array_equal(y[finite], want)
+
+
+def test_host_bf16_converter_keeps_subnormals_on_every_path():
+    """fp32 subnormals become bf16 subnormals (RNE), as on the device, also
+    inside the 32-wide vector loop (VCVTNE2PS2BF16 would flush them)."""
+    from oracle.refcpu import round_bf16
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal(4096).astype(np.float32)
+    sub = (rng.random(4096) < 0.05)
+    x[sub] = (rng.standard_normal(int(sub.sum())) * 1e-39).astype(np.float32)
+    for off in (0, 1, 17):
+        y = es.host_convert_bf16(x[off:])
+        want = (round_bf16(x[off:]).view(np.uint32) >> 16).astype(np.uint16)
+        np.testing.assert_array_equal(y, want)
+
+
+def test_host_bf16_converter_concurrent_callers():
+    """One process-wide pool, many Python threads (ctypes drops the GIL):
+    every caller gets its whole array converted."""
+    import threading
+    from oracle.refcpu import round_bf16
+    rng = np.random.default_rng(6)
+    xs = [rng.standard_normal(200_000 + 37 * k).astype(np.float32) for k in range(8)]
+    out = [None] * len(xs)
+
+    def work(k):
+        for _ in range(5):
+            out[k] = es.host_convert_bf16(xs[k])
+
+    ts = [threading.Thread(target=work, args=(k,)) for k in range(len(xs))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for k, x in enumerate(xs):
+        want = (round_bf16(x).view(np.uint32) >> 16).astype(np.uint16)
+        np.testing.assert_array_equal(out[k], want)

@@ -60,3 +60,37 @@ def test_every_baseline_config_builds_a_valid_cluster_and_start_matrix():
     dozen = bench.make_cluster(es, bench.CONFIGS["cfg3"])
     A = es.worst_fit_decreasing(dozen, 8)
     assert all(A.row_worker_count(d) == 3 for d in range(4))  # acceptance.cpp:217-232
+
+
+def test_plain_cluster_footprints_equal_the_products():
+    """The reference arm's product-free cluster derives the same footprints
+    (spec.cpp derive_footprint), so WFD and memory checks agree."""
+    for name, cfg in bench.CONFIGS.items():
+        a = bench.make_cluster(es, cfg)
+        b = bench.plain_cluster(cfg)
+        for ma, mb in zip(a.models, b.models):
+            assert (ma.weight_mib, ma.act_mib_per_sample, ma.cost_per_sample) == \
+                pytest.approx((mb.weight_mib, mb.act_mib_per_sample, mb.cost_per_sample), rel=1e-12)
+        from oracle import refcpu
+        assert refcpu.ref_wfd(b, 8).tolist() == es.worst_fit_decreasing(a, 8).cells.tolist()
+
+
+def test_reference_arm_runs_the_same_matrix_without_loading_the_product():
+    """bench.py --impl reference: the reference InferenceSystem on host cores
+    with the b200 arm's matrix; the product library never loads."""
+    import json
+    import subprocess
+    repo = Path(__file__).resolve().parents[1]
+    code = ("import runpy, sys; sys.argv = ['bench.py', '--impl', 'reference', '--steps', '2', "
+            "'--warmup', '1', '--ref-budget-s', '2', '--no-ref-faithful']; "
+            "runpy.run_path('bench.py', run_name='__main__'); "
+            "maps = open('/proc/self/maps').read(); "
+            "assert 'libenserve_b200' not in maps, 'product library loaded'; "
+            "assert 'paper_2208_14049_b200' not in sys.modules")
+    out = subprocess.run([sys.executable, "-c", code], cwd=repo, capture_output=True, text=True,
+                         timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["config"]["same_config"]
+    assert line["config"]["matrix"] == bench.CONFIGS["cfg2"]["ref_matrix"]
+    assert line["value"] > 0 and line["ms_per_step"] > 0 and line["steps"] == 2

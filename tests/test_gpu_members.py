@@ -28,9 +28,7 @@ def test_deep_mlp_member_matches_cpu_oracle(widths, b, dense, monkeypatch):
     got = es.Member(model, b).predict(X)
     cpu = refcpu.CpuMlp(widths, 4242)
     want = cpu.forward(X)
-    # Every bf16-rounded activation layer brings its own rounding-flip budget
-    # (DESIGN.md §Tolerances): rtol scales with the number of hidden layers.
-    assert_logits_close(got, want, cpu.logit_scale(X), rtol=RTOL_BF16 * (len(widths) - 2))
+    assert_logits_close(got, want, cpu.logit_scale(X), rtol=RTOL_BF16)
     np.testing.assert_array_equal(np.argmax(got, 1), np.argmax(want, 1))
 
 
@@ -46,7 +44,7 @@ def test_wide_mlp_member_matches_cpu_oracle(widths):
     got = es.Member(model, 64).predict(X)
     cpu = refcpu.CpuMlp(widths, 4343)
     want = cpu.forward(X)
-    assert_logits_close(got, want, cpu.logit_scale(X), rtol=RTOL_BF16 * (len(widths) - 2))
+    assert_logits_close(got, want, cpu.logit_scale(X), rtol=RTOL_BF16)
     np.testing.assert_array_equal(np.argmax(got, 1), np.argmax(want, 1))
 
 
@@ -63,14 +61,7 @@ def test_heterogeneous_depths_in_one_ensemble_match_reference_pipeline():
     out = es.run_inference(es.SampleStore(X), A, c, es.CombinationRule.averaging(softmax=True))
     Yr, _, _ = refcpu.ref_run_ensemble(c, A.cells, X, rule=0, softmax=True)
     np.testing.assert_allclose(out.combined, Yr, rtol=0, atol=1e-3)
-    # Winners agree wherever the reference's top two probabilities are further
-    # apart than the two tolerances; inside that band either may win, but the
-    # winner must still be one of the reference's top two.
-    top = np.argsort(Yr, axis=1)[:, -2:]
-    gap = np.take_along_axis(Yr, top[:, 1:], 1)[:, 0] - np.take_along_axis(Yr, top[:, :1], 1)[:, 0]
-    clear = gap > 2e-3
-    np.testing.assert_array_equal(out.winners[clear], top[clear, 1])
-    assert np.all((out.winners == top[:, 1]) | (out.winners == top[:, 0]))
+    np.testing.assert_array_equal(out.winners, np.argmax(Yr, 1))
 
 
 # ------------------------------------------------------------------ K2 CNN
@@ -96,8 +87,7 @@ def test_cnn_member_matches_cpu_oracle(shape, b, schedule, monkeypatch):
     got = es.Member(model, b).predict(X)
     cpu = refcpu.CpuCnn(shape, 77)
     want = cpu.forward(X)
-    # Three bf16-rounded activation layers (conv1, conv2, hidden).
-    assert_logits_close(got, want, cpu.logit_scale(X), rtol=RTOL_BF16 * 3)
+    assert_logits_close(got, want, cpu.logit_scale(X), rtol=RTOL_BF16)
     np.testing.assert_array_equal(np.argmax(got, 1), np.argmax(want, 1))
 
 
@@ -129,7 +119,4 @@ def test_cnn_in_data_parallel_ensemble_matches_reference_pipeline():
     out = es.run_inference(es.SampleStore(X), A, c, es.CombinationRule.averaging(softmax=True))
     Yr, _, _ = refcpu.ref_run_ensemble(c, A.cells, X, rule=0, softmax=True)
     np.testing.assert_allclose(out.combined, Yr, rtol=0, atol=1e-3)
-    top = np.argsort(Yr, axis=1)[:, -2:]
-    gap = np.take_along_axis(Yr, top[:, 1:], 1)[:, 0] - np.take_along_axis(Yr, top[:, :1], 1)[:, 0]
-    clear = gap > 2e-3
-    np.testing.assert_array_equal(out.winners[clear], top[clear, 1])
+    np.testing.assert_array_equal(out.winners, np.argmax(Yr, 1))
