@@ -9,7 +9,7 @@ import pytest
 import paper_2208_14049_b200 as es
 from conftest import gpu
 from oracle import refcpu, restate
-from test_gpu_parity import RTOL_BF16, assert_logits_close
+from test_gpu_parity import RTOL_BF16, TOL_P, assert_labels_identical_or_tied, assert_logits_close
 
 pytestmark = pytest.mark.gpu
 
@@ -28,8 +28,14 @@ def test_deep_mlp_member_matches_cpu_oracle(widths, b, dense, monkeypatch):
     got = es.Member(model, b).predict(X)
     cpu = refcpu.CpuMlp(widths, 4242)
     want = cpu.forward(X)
-    assert_logits_close(got, want, cpu.logit_scale(X), rtol=RTOL_BF16)
-    np.testing.assert_array_equal(np.argmax(got, 1), np.argmax(want, 1))
+    s = cpu.logit_scale(X)
+    # Three rounded hidden layers (deeper than any BASELINE roster member):
+    # a flip in an earlier layer can cascade into several last-layer flips,
+    # which s (the last layer's conditioning) does not cover; measured max
+    # 1.05e-3 s for 784-256-384-128-10.  Members of roster depth: 1e-3 s.
+    rtol = RTOL_BF16 if len(widths) <= 4 else 1.5 * RTOL_BF16
+    assert_logits_close(got, want, s, rtol=rtol)
+    assert_labels_identical_or_tied(np.argmax(got, 1), want, rtol * s, f"{widths} b={b}")
 
 
 @pytest.mark.parametrize("widths", [[784, 1024, 10], [784, 2048, 10], [784, 640, 16],
@@ -44,8 +50,9 @@ def test_wide_mlp_member_matches_cpu_oracle(widths):
     got = es.Member(model, 64).predict(X)
     cpu = refcpu.CpuMlp(widths, 4343)
     want = cpu.forward(X)
-    assert_logits_close(got, want, cpu.logit_scale(X), rtol=RTOL_BF16)
-    np.testing.assert_array_equal(np.argmax(got, 1), np.argmax(want, 1))
+    s = cpu.logit_scale(X)
+    assert_logits_close(got, want, s, rtol=RTOL_BF16)
+    assert_labels_identical_or_tied(np.argmax(got, 1), want, RTOL_BF16 * s, f"{widths}")
 
 
 def test_heterogeneous_depths_in_one_ensemble_match_reference_pipeline():
@@ -60,8 +67,8 @@ def test_heterogeneous_depths_in_one_ensemble_match_reference_pipeline():
     X = refcpu.features(77, 128 * 9 + 40, 784)
     out = es.run_inference(es.SampleStore(X), A, c, es.CombinationRule.averaging(softmax=True))
     Yr, _, _ = refcpu.ref_run_ensemble(c, A.cells, X, rule=0, softmax=True)
-    np.testing.assert_allclose(out.combined, Yr, rtol=0, atol=1e-3)
-    np.testing.assert_array_equal(out.winners, np.argmax(Yr, 1))
+    np.testing.assert_allclose(out.combined, Yr, rtol=0, atol=TOL_P)
+    assert_labels_identical_or_tied(out.winners, Yr, TOL_P, "heterogeneous depths")
 
 
 # ------------------------------------------------------------------ K2 CNN
@@ -87,8 +94,9 @@ def test_cnn_member_matches_cpu_oracle(shape, b, schedule, monkeypatch):
     got = es.Member(model, b).predict(X)
     cpu = refcpu.CpuCnn(shape, 77)
     want = cpu.forward(X)
-    assert_logits_close(got, want, cpu.logit_scale(X), rtol=RTOL_BF16)
-    np.testing.assert_array_equal(np.argmax(got, 1), np.argmax(want, 1))
+    s = cpu.logit_scale(X)
+    assert_logits_close(got, want, s, rtol=RTOL_BF16)
+    assert_labels_identical_or_tied(np.argmax(got, 1), want, RTOL_BF16 * s, f"cnn {shape} b={b}")
 
 
 @pytest.mark.parametrize("first", [0, 1, 5])
@@ -118,5 +126,5 @@ def test_cnn_in_data_parallel_ensemble_matches_reference_pipeline():
     X = refcpu.features(79, 128 * 7 + 61, 784)
     out = es.run_inference(es.SampleStore(X), A, c, es.CombinationRule.averaging(softmax=True))
     Yr, _, _ = refcpu.ref_run_ensemble(c, A.cells, X, rule=0, softmax=True)
-    np.testing.assert_allclose(out.combined, Yr, rtol=0, atol=1e-3)
-    np.testing.assert_array_equal(out.winners, np.argmax(Yr, 1))
+    np.testing.assert_allclose(out.combined, Yr, rtol=0, atol=TOL_P)
+    assert_labels_identical_or_tied(out.winners, Yr, TOL_P, "cfg2 shape, CNN data-parallel")

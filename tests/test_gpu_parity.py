@@ -33,6 +33,34 @@ def assert_logits_close(got, want, scale, rtol=RTOL_BF16):
     return err.max()
 
 
+# Averaged probabilities: the north_star contract is 1e-3; every softmax
+# ensemble here stays within 2.5e-4 (max observed 2.0e-4 over 16384 rows of
+# every roster, profiles/r2a_label_probe_16k.jsonl), asserted as achieved.
+TOL_P = 2.5e-4
+
+
+def assert_labels_identical_or_tied(got_labels, ref_scores, band, what=""):
+    """Predicted classes identical on every row, except where the two
+    competing classes are a certified tie: the reference's score gap between
+    its winner a and the device's winner b is within `band[row, a] +
+    band[row, b]` (each score's a-priori tolerance).  Prints the mismatch
+    count and gaps.  band: scalar or [rows, C] array."""
+    ref = np.argmax(ref_scores, 1)
+    rows = np.nonzero(got_labels != ref)[0]
+    bnd = np.broadcast_to(np.asarray(band, dtype=np.float64), ref_scores.shape)
+    a, b = ref[rows], got_labels[rows]
+    gap = ref_scores[rows, a].astype(np.float64) - ref_scores[rows, b]
+    lim = bnd[rows, a] + bnd[rows, b]
+    srt = np.sort(ref_scores, axis=1)
+    in_band = int(((srt[:, -1] - srt[:, -2]) <= bnd.max(axis=1) * 2).sum())
+    print(f"{what}: label mismatches = {len(rows)} / {len(ref)} "
+          f"(rows inside the tie band: {in_band}); mismatch gaps {gap.tolist()} "
+          f"vs tie bounds {lim.tolist()}")
+    assert np.all(gap <= lim), "a label differs outside the tie band"
+    assert len(rows) <= max(2, len(ref) // 500), "too many label differences"
+    return len(rows)
+
+
 def top2_margin(z):
     s = np.sort(z, axis=1)
     return (s[:, -1] - s[:, -2]) / np.maximum(np.abs(z).max(axis=1), 1e-6)
@@ -177,8 +205,9 @@ def test_member_kernel_matches_cpu_oracle(H, b, mlp_kernel):
     got = member.predict(X)
     cpu = refcpu.CpuMlp([784, H, 10], 1234 + H)
     want = cpu.forward(X)
-    assert_logits_close(got, want, cpu.logit_scale(X))
-    np.testing.assert_array_equal(np.argmax(got, 1), np.argmax(want, 1))
+    sc = cpu.logit_scale(X)
+    assert_logits_close(got, want, sc)
+    assert_labels_identical_or_tied(np.argmax(got, 1), want, RTOL_BF16 * sc, f"H={H} b={b}")
 
 
 @pytest.mark.parametrize("H,b", [(512, 128), (256, 128), (128, 64), (384, 32)])
@@ -215,8 +244,9 @@ def test_member_kernel_single_sample_and_large_batch_rows():
         X = refcpu.features(nb, nb, 784)
         got = es.Member(model, 32).predict(X)
         want = cpu.forward(X)
-        assert_logits_close(got, want, cpu.logit_scale(X))
-        np.testing.assert_array_equal(np.argmax(got, 1), np.argmax(want, 1))
+        sc = cpu.logit_scale(X)
+        assert_logits_close(got, want, sc)
+        assert_labels_identical_or_tied(np.argmax(got, 1), want, RTOL_BF16 * sc, f"nb={nb}")
 
 
 # ------------------------------------------------------------------ ensemble system
@@ -231,10 +261,8 @@ def test_cfg1_ensemble_matches_reference_pipeline_with_cpu_member():
     X = refcpu.features(21, nb, 784)
     out = es.run_inference(es.SampleStore(X), A, c, es.CombinationRule.averaging(softmax=True))
     Yr, _, _ = refcpu.ref_run_ensemble(c, A.cells, X, rule=0, softmax=True)
-    np.testing.assert_allclose(out.combined, Yr, rtol=0, atol=RTOL_BF16)
-    np.testing.assert_array_equal(out.winners, np.argmax(Yr, 1))
-    print(f"min top-2 margin of the reference's averaged probabilities: "
-          f"{top2_margin(Yr).min():.3e}")
+    np.testing.assert_allclose(out.combined, Yr, rtol=0, atol=TOL_P)
+    assert_labels_identical_or_tied(out.winners, Yr, TOL_P, "cfg1 softmax ensemble")
 
 
 @need_ref
@@ -245,8 +273,8 @@ def test_heterogeneous_ensemble_vote_and_wavg_match_reference():
     w = [0.4, 0.3, 0.2, 0.1]
     out = es.run_inference(es.SampleStore(X), A, c, es.CombinationRule.weighted(w, softmax=True))
     Yr, _, _ = refcpu.ref_run_ensemble(c, A.cells, X, rule=2, weights=w, softmax=True)
-    np.testing.assert_allclose(out.combined, Yr, rtol=0, atol=RTOL_BF16)
-    np.testing.assert_array_equal(out.winners, np.argmax(Yr, 1))
+    np.testing.assert_allclose(out.combined, Yr, rtol=0, atol=TOL_P)
+    assert_labels_identical_or_tied(out.winners, Yr, TOL_P, "wavg ensemble")
     out = es.run_inference(es.SampleStore(X), A, c, es.CombinationRule.majority_vote())
     Yr, Wr, _ = refcpu.ref_run_ensemble(c, A.cells, X, rule=1)
     np.testing.assert_array_equal(out.winners, Wr)
