@@ -223,6 +223,13 @@ def rank_shard(es, world: int, rank: int, batches: list, nb_per_gpu: int, seg: i
     return first * seg, min(end * seg, total), shares
 
 
+def gather_plan(es, world: int, batches: list, nb_per_gpu: int, seg: int = 128) -> tuple:
+    """(first row, rows) of every rank's shard in the gathered result --
+    the plan InferenceSystem.set_gather receives on every rank."""
+    spans = [rank_shard(es, world, r, batches, nb_per_gpu, seg)[:2] for r in range(world)]
+    return [a for a, _ in spans], [b - a for a, b in spans]
+
+
 # ------------------------------------------------------------------ workload
 def roster_models(es, roster):
     out = []
@@ -270,6 +277,10 @@ def choose_matrix(es, cluster, cfg: dict, device_map: list, calib_nb: int, seed:
         bbs = {"applicable": False, "reason": str(e)}
     return {"A1": A1, "A2": A2, "A1_score": s1, "A2_score": s2, "bench_calls": calls,
             "greedy_s": time.time() - t0, "bbs": bbs}
+
+
+def cfg_classes(cfg: dict) -> int:
+    return int(cfg["roster"][0][2][-1])
 
 
 def launch_work(arch, names: list) -> list:
@@ -508,6 +519,20 @@ def run_b200(args, dist: Dist) -> dict | None:
                            device=device_map[0])
         system = es.InferenceSystem(A, cluster, rule, device_map=device_map, copy_outputs=False,
                                     e2e_host_convert=bool(args.e2e_host_convert))
+    gather = None
+    if not multirow and dist.world > 1:
+        # The reference's accumulator sees every worker's predictions
+        # (pipeline.cpp:210-211, :258-279): each rank's probabilities + argmax
+        # go to rank 0 over NCCL after every run, inside the timed window.
+        firsts, counts = gather_plan(es, dist.world, A.cells[0].tolist(), args.nb)
+        uid = dist.broadcast_object(es.nccl_unique_id() if dist.rank == 0 else None)
+        comm = es.Comm(uid, dist.world, dist.rank, gpu)
+        system.set_gather(comm, 0, firsts, counts)
+        total = sum(counts)
+        gather = {"collective": "NCCL grouped send/recv to rank 0 (probabilities + argmax)",
+                  "bytes_per_step": total * (cfg_classes(cfg) * 4 + 4),
+                  "rows_per_step": total, "nccl_version": es.nccl_version()}
+    if active:
         for _ in range(args.warmup):
             system.run(X, copy=False)
     launches = 0
@@ -532,10 +557,10 @@ def run_b200(args, dist: Dist) -> dict | None:
     combine_ms /= max(1, args.steps)
     kern = [[(n, t / args.steps) for n, t in k] for k in kern]
 
-    # e2e: host (pinned) X in, combined probabilities + labels out, per step.
-    # Needs every worker on one GPU (run_host); skipped for multi-GPU rows.
+    # e2e: host (pinned) X in, combined probabilities + labels out, per step
+    # (run_host: one lane per GPU hosting workers, each over its own PCIe link).
     e2e = None
-    if active and len(set(device_map)) == 1:
+    if active:
         e2e_nb = max(1, min(args.e2e_nb, args.nb))
         try:
             import torch
@@ -609,8 +634,11 @@ def run_b200(args, dist: Dist) -> dict | None:
             "calib_samples": args.calib_nb,
             "batch_only_baseline": choice["bbs"],
             "parallelism": (f"members placed on {cfg['devices']} device rows over {ngpus_used} "
-                            f"GPU(s), remote logits peer-copied to the combining GPU") if multirow
-            else f"ensemble replicated per GPU, dp{n} over samples",
+                            f"GPU(s), remote logits stored into the combining GPU over NVLink "
+                            f"peer mappings") if multirow
+            else f"ensemble replicated per GPU, dp{n} over samples" +
+            (", predictions gathered to rank 0 over NCCL inside the timed window" if gather else ""),
+            "gather": gather,
             "segment_size": 128,
         },
         "roofline": roofline_for(es, cluster, A, kern, args.nb, pk),

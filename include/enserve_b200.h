@@ -105,6 +105,12 @@ typedef struct es_pool_opts {
                               summed in row order (fp32 order differs from the
                               reference fold; votes exact; pure model placement only);
                               0 = parity gather (bit-identical fold) */
+  int no_peer_stores;      /* 0 = remote workers store logits straight into the combining
+                              GPU's buffers over NVLink peer mappings (peer access is
+                              enabled at construction); 1 = local staging buffer +
+                              cudaMemcpyPeerAsync after the member kernels */
+  int row_nodes;           /* 1 = every device row is its own node (stream, staging,
+                              gather, run_host lane) even where rows share a GPU */
 } es_pool_opts;
 
 /* RunStats (pipeline.hpp:19-25). */
@@ -127,6 +133,7 @@ typedef struct es_bench_result {
 
 typedef struct es_store es_store;
 typedef struct es_system es_system;
+typedef struct es_comm es_comm;
 typedef struct es_member es_member;
 
 int es_abi_version(void);
@@ -269,8 +276,31 @@ es_status es_system_last_transfer(es_system* s, size_t* h2d_bytes, size_t* d2h_b
  * ';' into names[names_len], and the launch count per run. */
 es_status es_system_kernel_timing(es_system* s, int worker, double* ms, char* names,
                                   size_t names_len, int cap, int* count);
+/* Per worker: 0 = on the combining node, 1 = remote with direct peer stores,
+ * 2 = remote through staging + peer copy (routes[workers]); peers[cap] = CUDA
+ * ordinals with peer access to/from the combining GPU, *n_peers their count. */
+es_status es_system_routes(es_system* s, int* routes, int* peers, int cap, int* n_peers);
 es_status es_system_shutdown(es_system* s);
 void es_system_destroy(es_system* s);
+
+/* ---------------------------------------------- one process per GPU (NCCL)
+ * The reference funnels every worker's predictions into one accumulator
+ * (src/runtime/pipeline.cpp:210-211, :258-279); across processes that is a
+ * gather of each rank's combined probabilities + argmax to a root rank.
+ * libnccl.so.2 is resolved at run time. */
+/* ncclGetUniqueId: id[128] for es_comm_create on every rank. */
+es_status es_comm_unique_id(uint8_t* id, size_t len);
+/* ncclCommInitRank on CUDA ordinal `device` (collective: every rank calls it). */
+es_status es_comm_create(const uint8_t* id, size_t len, int nranks, int rank, int device,
+                         es_comm** out);
+es_status es_nccl_version(int* version);
+void es_comm_destroy(es_comm* c);
+/* After each run's combine, this rank's rows go to `root` at row first_rows[rank]
+ * of an (sum rows)-row result, inside the timed window; the root's await_run /
+ * es_system_run returns every rank's rows (Y/winners sized for the sum).
+ * comm NULL detaches.  The system keeps the communicator alive. */
+es_status es_system_set_gather(es_system* s, es_comm* comm, int root, const int64_t* first_rows,
+                               const int64_t* rows, int nranks);
 
 /* run_inference (pipeline.cpp:418-444), Deploy mode: Y[nb*C], winners[nb]. */
 es_status es_run_inference(const es_cluster_desc* c, const int* A, const es_rule_desc* rule,
@@ -329,6 +359,15 @@ es_status es_digest_hex(const char* text, char out[17]);
 es_status es_cache_key(const es_cluster_desc* c, int max_iter, int max_neighs, uint64_t rng_seed,
                        int default_batch, const char* bench_mode, size_t calib_samples,
                        int repeats, char out[17]);
+/* cache_key with the opt-in hardware identity (NULL or "" = es_cache_key):
+ * a matrix measured on other GPUs misses.  Reference-computed keys match only
+ * the identity-free form. */
+es_status es_cache_key_device(const es_cluster_desc* c, int max_iter, int max_neighs,
+                              uint64_t rng_seed, int default_batch, const char* bench_mode,
+                              size_t calib_samples, int repeats, const char* device,
+                              char out[17]);
+/* "<name>/sm_<cc>/<SMs> SMs/<GiB> GiB x<count>" of the visible GPUs. */
+es_status es_device_identity(char* out, size_t len);
 /* MatrixCache::lookup / store (cache.cpp:35-88): corrupt, stale or invalid
  * entries are misses (*hit = 0), never errors. */
 es_status es_cache_lookup(const char* directory, const char* key, const es_cluster_desc* c,

@@ -45,7 +45,8 @@ class PoolOpts(C.Structure):
                 ("warmup", C.c_int), ("sms_per_worker", C.c_int),
                 ("overlap_colocated", C.c_int), ("e2e_chunk_rows", C.c_size_t),
                 ("e2e_host_convert", C.c_int), ("e2e_convert_eighths", C.c_int),
-                ("dp_equal_split", C.c_int), ("row_partials", C.c_int)]
+                ("dp_equal_split", C.c_int), ("row_partials", C.c_int),
+                ("no_peer_stores", C.c_int), ("row_nodes", C.c_int)]
 
 
 class RunStats(C.Structure):
@@ -101,6 +102,10 @@ _SIGS = {
     "es_digest_hex": (C.c_int, [C.c_char_p, C.c_char_p]),
     "es_cache_key": (C.c_int, [C.POINTER(ClusterDesc), C.c_int, C.c_int, C.c_uint64, C.c_int,
                                C.c_char_p, C.c_size_t, C.c_int, C.c_char_p]),
+    "es_cache_key_device": (C.c_int, [C.POINTER(ClusterDesc), C.c_int, C.c_int, C.c_uint64,
+                                      C.c_int, C.c_char_p, C.c_size_t, C.c_int, C.c_char_p,
+                                      C.c_char_p]),
+    "es_device_identity": (C.c_int, [C.c_char_p, C.c_size_t]),
     "es_cache_lookup": (C.c_int, [C.c_char_p, C.c_char_p, C.POINTER(ClusterDesc), c_int_p,
                                   c_double_p, C.POINTER(C.c_int64), c_int_p]),
     "es_cache_store": (C.c_int, [C.c_char_p, C.c_char_p, C.POINTER(ClusterDesc), c_int_p,
@@ -173,6 +178,14 @@ _SIGS = {
     "es_combine": (C.c_int, [C.POINTER(RuleDesc), C.c_int, C.c_int, C.c_size_t,
                              C.POINTER(c_float_p), c_float_p, c_int32_p]),
     "es_system_shares": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64), c_double_p]),
+    "es_system_routes": (C.c_int, [C.c_void_p, c_int_p, c_int_p, C.c_int, c_int_p]),
+    "es_comm_unique_id": (C.c_int, [C.POINTER(C.c_uint8), C.c_size_t]),
+    "es_comm_create": (C.c_int, [C.POINTER(C.c_uint8), C.c_size_t, C.c_int, C.c_int, C.c_int,
+                                 C.POINTER(C.c_void_p)]),
+    "es_nccl_version": (C.c_int, [c_int_p]),
+    "es_comm_destroy": (None, [C.c_void_p]),
+    "es_system_set_gather": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.POINTER(C.c_int64),
+                                       C.POINTER(C.c_int64), C.c_int]),
     "es_service_create": (C.c_int, [C.POINTER(ClusterDesc), c_int_p, C.POINTER(RuleDesc),
                                     C.POINTER(PoolOpts), C.c_int, C.c_size_t, C.c_longlong,
                                     C.POINTER(C.c_void_p)]),

@@ -631,7 +631,8 @@ class CombinationRule:
 def _pool_opts(keep: list, device_map=None, copy_outputs=True, warmup=True,
                sms_per_worker=0, overlap_colocated=False, e2e_chunk_rows=0,
                e2e_host_convert=True, e2e_convert_eighths=0,
-               dp_equal_split=False, row_partials=False) -> _abi.PoolOpts:
+               dp_equal_split=False, row_partials=False, peer_stores=True,
+               row_nodes=False) -> _abi.PoolOpts:
     """PoolOptions (runtime.hpp)."""
     dm = None
     n = 0
@@ -642,7 +643,8 @@ def _pool_opts(keep: list, device_map=None, copy_outputs=True, warmup=True,
     o = _abi.PoolOpts(C.cast(dm, _abi.c_int_p) if dm is not None else None, n, int(copy_outputs),
                       int(warmup), int(sms_per_worker), int(overlap_colocated),
                       int(e2e_chunk_rows), int(e2e_host_convert), int(e2e_convert_eighths),
-                      int(dp_equal_split), int(row_partials))
+                      int(dp_equal_split), int(row_partials), int(not peer_stores),
+                      int(row_nodes))
     keep.append(o)
     return o
 
@@ -771,10 +773,39 @@ class InferenceSystem:
         _check(lib().es_system_kernel_timing(self._h, worker, ms, names, 512, 16, C.byref(n)))
         return list(zip(names.value.decode().split(";"), list(ms)[:n.value]))
 
+    def routes(self) -> tuple:
+        """([route per worker], [peer CUDA ordinals]): 0 = on the combining
+        node, 1 = remote with direct NVLink peer stores, 2 = remote through a
+        staging buffer + peer copy."""
+        w = self.worker_count()
+        r = (C.c_int * max(w, 1))()
+        p = (C.c_int * 64)()
+        n = C.c_int()
+        _check(lib().es_system_routes(self._h, r, p, 64, C.byref(n)))
+        return list(r)[:w], list(p)[:n.value]
+
+    def set_gather(self, comm: "Comm" = None, root: int = 0, first_rows=None, rows=None) -> None:
+        """One process per GPU: after every run this rank's probabilities +
+        argmax go to `root` over NCCL (inside the timed window), landing at
+        row first_rows[rank] of a sum(rows)-row result that the root's run()
+        returns.  comm=None detaches."""
+        if comm is None:
+            _check(lib().es_system_set_gather(self._h, None, 0, None, None, 0))
+            self._gather = None
+            return
+        n = comm.size
+        f = (C.c_int64 * n)(*[int(v) for v in first_rows])
+        k = (C.c_int64 * n)(*[int(v) for v in rows])
+        _check(lib().es_system_set_gather(self._h, comm._h, int(root), f, k, n))
+        self._gather = (comm, int(root), [int(v) for v in rows])
+
     def begin_run(self, X: SampleStore, rule: CombinationRule = None) -> None:
         keep: list = []
         self._store = X
         self._pending = X.nb
+        g = getattr(self, "_gather", None)
+        if g is not None and g[0].rank == g[1]:
+            self._pending = sum(g[2])  # the root receives every rank's rows
         _check(lib().es_system_begin_run(self._h, X._h,
                                          C.byref(rule._desc(keep)) if rule else None))
 
@@ -836,6 +867,41 @@ class InferenceSystem:
     def __exit__(self, *exc):
         self.close()
         return False
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId (128 bytes) for Comm on every rank."""
+    buf = (C.c_uint8 * 128)()
+    _check(lib().es_comm_unique_id(buf, 128))
+    return bytes(buf)
+
+
+def nccl_version() -> int:
+    v = C.c_int()
+    _check(lib().es_nccl_version(C.byref(v)))
+    return v.value
+
+
+class Comm:
+    """NCCL communicator of one process per GPU (ncclCommInitRank; every
+    rank constructs it collectively with rank 0's nccl_unique_id())."""
+
+    def __init__(self, unique_id: bytes, size: int, rank: int, device: int):
+        if len(unique_id) != 128:
+            raise InvalidArgument("NCCL unique id must be 128 bytes")
+        buf = (C.c_uint8 * 128)(*unique_id)
+        h = C.c_void_p()
+        _check(lib().es_comm_create(buf, 128, int(size), int(rank), int(device), C.byref(h)))
+        self._h = h
+        self.size, self.rank, self.device = int(size), int(rank), int(device)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib().es_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
 
 
 def run_inference(X: SampleStore, A: AllocationMatrix, cluster: ClusterSpec,
@@ -1139,15 +1205,25 @@ class OptimizerKey:
     bench_mode: str = "measured"
     calib_samples: int = 0
     repeats: int = 1
+    # opt-in hardware identity (device_identity()); "" = the reference's key
+    device: str = ""
+
+
+def device_identity() -> str:
+    """'<name>/sm_<cc>/<SMs> SMs/<GiB> GiB x<count>' of the visible GPUs."""
+    out = C.create_string_buffer(256)
+    _check(lib().es_device_identity(out, 256))
+    return out.value.decode()
 
 
 def cache_key(cluster: ClusterSpec, key: OptimizerKey) -> str:
-    """cache.cpp:22-33."""
+    """cache.cpp:22-33 (plus the opt-in device identity when key.device is set)."""
     out = C.create_string_buffer(17)
     with _Desc(cluster) as d:
-        _check(lib().es_cache_key(d.ptr, key.greedy.max_iter, key.greedy.max_neighs,
-                                  key.greedy.rng_seed, key.default_batch, key.bench_mode.encode(),
-                                  key.calib_samples, key.repeats, out))
+        _check(lib().es_cache_key_device(d.ptr, key.greedy.max_iter, key.greedy.max_neighs,
+                                         key.greedy.rng_seed, key.default_batch,
+                                         key.bench_mode.encode(), key.calib_samples, key.repeats,
+                                         key.device.encode(), out))
     return out.value.decode()
 
 

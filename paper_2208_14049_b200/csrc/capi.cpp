@@ -15,6 +15,7 @@
 #include "enserve/spec_io.hpp"
 #include "enserve/commands.hpp"
 #include "enserve/calibrate.hpp"
+#include "enserve/collective.hpp"
 #include "enserve/service.hpp"
 #include "cuda/batching.cuh"
 #include "enserve/placement.hpp"
@@ -31,6 +32,10 @@ struct es_store {
 struct es_system {
   std::unique_ptr<InferenceSystem> sys;
   int models = 0;
+};
+
+struct es_comm {
+  std::shared_ptr<enserve::Comm> comm;
 };
 
 struct es_member {
@@ -182,6 +187,8 @@ PoolOptions to_opts(const es_pool_opts* o) {
   if (o->e2e_convert_eighths > 0) p.e2e_convert_eighths = o->e2e_convert_eighths;
   p.dp_equal_split = o->dp_equal_split != 0;
   p.row_partials = o->row_partials != 0;
+  p.peer_stores = o->no_peer_stores == 0;
+  p.row_nodes = o->row_nodes != 0;
   return p;
 }
 
@@ -683,6 +690,65 @@ es_status es_system_kernel_timing(es_system* s, int worker, double* ms, char* na
   });
 }
 
+es_status es_system_routes(es_system* s, int* routes, int* peers, int cap, int* n_peers) {
+  return guard([&] {
+    need(s != nullptr, "NULL handle");
+    const std::vector<int> r = s->sys->worker_routes();
+    for (std::size_t w = 0; routes && w < r.size(); ++w) routes[w] = r[w];
+    const std::vector<int>& p = s->sys->peer_devices();
+    for (int i = 0; peers && i < cap && i < static_cast<int>(p.size()); ++i) peers[i] = p[i];
+    if (n_peers) *n_peers = static_cast<int>(p.size());
+    return ES_OK;
+  });
+}
+
+es_status es_comm_unique_id(uint8_t* id, size_t len) {
+  return guard([&] {
+    need(id != nullptr, "NULL id buffer");
+    const std::string u = enserve::Comm::unique_id();
+    need(len >= u.size(), "id buffer smaller than an NCCL unique id (128 bytes)");
+    std::memcpy(id, u.data(), u.size());
+    return ES_OK;
+  });
+}
+
+es_status es_comm_create(const uint8_t* id, size_t len, int nranks, int rank, int device,
+                         es_comm** out) {
+  return guard([&] {
+    need(id != nullptr && out != nullptr, "NULL argument");
+    auto h = std::make_unique<es_comm>();
+    h->comm = std::make_shared<enserve::Comm>(
+        std::string(reinterpret_cast<const char*>(id), len), nranks, rank, device);
+    *out = h.release();
+    return ES_OK;
+  });
+}
+
+es_status es_nccl_version(int* version) {
+  return guard([&] {
+    need(version != nullptr, "NULL argument");
+    *version = enserve::Comm::version();
+    return ES_OK;
+  });
+}
+
+void es_comm_destroy(es_comm* c) { delete c; }
+
+es_status es_system_set_gather(es_system* s, es_comm* comm, int root, const int64_t* first_rows,
+                               const int64_t* rows, int nranks) {
+  return guard([&] {
+    need(s != nullptr, "NULL handle");
+    if (!comm) {
+      s->sys->set_gather(nullptr, 0, {}, {});
+      return ES_OK;
+    }
+    need(first_rows && rows && nranks == comm->comm->size(), "gather plan needs one entry per rank");
+    s->sys->set_gather(comm->comm, root, std::vector<long long>(first_rows, first_rows + nranks),
+                       std::vector<long long>(rows, rows + nranks));
+    return ES_OK;
+  });
+}
+
 es_status es_system_shutdown(es_system* s) {
   return guard([&] {
     need(s != nullptr, "NULL handle");
@@ -902,6 +968,29 @@ es_status es_cache_key(const es_cluster_desc* c, int max_iter, int max_neighs, u
                                                            default_batch, bench_mode,
                                                            calib_samples, repeats));
     std::memcpy(out, k.c_str(), 17);
+    return ES_OK;
+  });
+}
+
+es_status es_cache_key_device(const es_cluster_desc* c, int max_iter, int max_neighs,
+                              uint64_t rng_seed, int default_batch, const char* bench_mode,
+                              size_t calib_samples, int repeats, const char* device,
+                              char out[17]) {
+  return guard([&] {
+    need(out != nullptr, "out is NULL");
+    OptimizerKey k = opt_key(max_iter, max_neighs, rng_seed, default_batch, bench_mode,
+                             calib_samples, repeats);
+    k.device = device ? device : "";
+    const std::string d = cache_key(to_cluster(c), k);
+    std::memcpy(out, d.c_str(), 17);
+    return ES_OK;
+  });
+}
+
+es_status es_device_identity(char* out, size_t len) {
+  return guard([&] {
+    need(out != nullptr && len > 0, "out is NULL");
+    std::snprintf(out, len, "%s", enserve::device_identity().c_str());
     return ES_OK;
   });
 }

@@ -27,6 +27,7 @@ struct CommandOptions {  // commands.hpp:12-24
   std::string backend = "b200";         // the reference's "synthetic" maps here too
   std::size_t calib_samples = 1024;
   std::size_t input_width = 0;          // 0 = the members' input width (or 16)
+  bool key_device = false;  // cache key includes device_identity() (spec_io.hpp OptimizerKey)
 };
 
 // Scoring oracle per the bench mode; increments *calls per use (commands.cpp:76-94).

@@ -4,6 +4,7 @@
 
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -14,6 +15,7 @@
 
 #include "../cuda/aux_kernels.cuh"
 #include "../cuda/mlp_kernel.cuh"
+#include "enserve/collective.hpp"
 #include "enserve/member.hpp"
 #include "enserve/host_convert.hpp"
 #include "enserve/placement.hpp"
@@ -47,6 +49,14 @@ int visible_devices() {
   return n;
 }
 
+// NVTX range over the host code that enqueues one worker's (or the combine's)
+// work: a profiler shows each worker's segments next to its kernels.  No cost
+// without an attached tool (nvtx3 is header-only, the injection is dlopen'd).
+struct Nvtx {
+  explicit Nvtx(const std::string& what) { nvtxRangePushA(what.c_str()); }
+  ~Nvtx() { nvtxRangePop(); }
+};
+
 // RAII device selection.
 struct OnDevice {
   int prev = 0;
@@ -56,6 +66,17 @@ struct OnDevice {
   }
   ~OnDevice() { cudaSetDevice(prev); }
 };
+
+// `from` may access `to`'s memory (idempotent: an already enabled pair is fine).
+void enable_peer(int from, int to) {
+  OnDevice on(from);
+  const cudaError_t e = cudaDeviceEnablePeerAccess(to, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return;
+  }
+  ES_CUDA(e);
+}
 
 // K3 arguments for M per-model logit buffers of `rows` rows.
 es::CombineArgs combine_args(const CombinationRule& rule, const std::vector<float*>& logits,
@@ -187,6 +208,12 @@ struct InferenceSystem::Worker {
   long long seg_begin = 0, seg_end = 0;  // this run's share
   float* staging = nullptr;              // remote worker: local logits [nb][C]
   std::size_t staging_rows = 0;
+  bool remote = false;  // on another node than the combining one
+  bool direct = false;  // remote, storing its logits straight into the combining GPU's buffers
+  // Logits go to the worker's own staging buffer: a remote worker without
+  // direct peer stores, or any remote worker in row_partials mode (its row's
+  // partial fold runs on its own GPU).
+  bool staged(bool partial_mode) const { return remote && (!direct || partial_mode); }
 };
 
 struct InferenceSystem::Impl {
@@ -207,38 +234,77 @@ struct InferenceSystem::Impl {
   };
   std::vector<RowPartial> partials;
   bool partial_mode = false;
-  // run_host pipeline (slots of whole-segment chunks)
+  // run_host pipeline (slots of whole-segment chunks).  A slot's host side
+  // and combining-node buffers:
   struct Slot {
-    void* pinned = nullptr;
-    float* x32 = nullptr;
-    void* x16 = nullptr;
-    std::vector<float*> logits;
+    void* pinned = nullptr;      // bf16 chunk staged by the host pool (portable)
+    std::vector<float*> logits;  // per model, on the combining GPU
     float* y = nullptr;
     int32_t* labels = nullptr;
-    cudaEvent_t h2d_done = nullptr, comp_done = nullptr, d2h_done = nullptr;
+    cudaEvent_t combined = nullptr, d2h_done = nullptr;
+  };
+  // Every node hosting workers is a lane (lane 0 = the combining node): its
+  // copy stream brings the rows its workers predict over its own PCIe link,
+  // its compute stream runs them, remote logits reach the combining GPU by
+  // direct peer stores or staging + peer copy.
+  struct Lane {
+    int phys = 0;
+    cudaStream_t copy = nullptr, comp = nullptr;
+    std::vector<int> workers;  // indices into workers_
+    struct LSlot {
+      float* x32 = nullptr;
+      void* x16 = nullptr;
+      std::vector<float*> staging;  // per model (staged workers only)
+      cudaEvent_t h2d_done = nullptr, comp_done = nullptr;
+      bool used = false;  // the lane had rows in the chunk last held by this slot
+    } s[3];
   };
   Slot slots[3];
-  cudaStream_t copy = nullptr, d2h = nullptr;
+  std::vector<Lane> lanes;
+  cudaStream_t d2h = nullptr;
   std::unique_ptr<ThreadPool> pool;
   std::size_t e2e_chunk_elems = 0;
   void free_e2e() {
+    int prev = 0;
+    cudaGetDevice(&prev);
     for (Slot& sl : slots) {
       if (sl.pinned) cudaFreeHost(sl.pinned);
-      cudaFree(sl.x32);
-      cudaFree(sl.x16);
+      cudaSetDevice(lanes.empty() ? 0 : lanes[0].phys);
       for (float* p : sl.logits) cudaFree(p);
       cudaFree(sl.y);
       cudaFree(sl.labels);
-      if (sl.h2d_done) cudaEventDestroy(sl.h2d_done);
-      if (sl.comp_done) cudaEventDestroy(sl.comp_done);
+      if (sl.combined) cudaEventDestroy(sl.combined);
       if (sl.d2h_done) cudaEventDestroy(sl.d2h_done);
       sl = Slot{};
     }
-    if (copy) cudaStreamDestroy(copy);
+    for (std::size_t l = 0; l < lanes.size(); ++l) {
+      Lane& ln = lanes[l];
+      cudaSetDevice(ln.phys);
+      if (ln.copy) cudaStreamSynchronize(ln.copy);
+      if (ln.comp) cudaStreamSynchronize(ln.comp);
+      for (Lane::LSlot& ls : ln.s) {
+        cudaFree(ls.x32);
+        cudaFree(ls.x16);
+        for (float* p : ls.staging) cudaFree(p);
+        if (ls.h2d_done) cudaEventDestroy(ls.h2d_done);
+        if (ls.comp_done) cudaEventDestroy(ls.comp_done);
+      }
+      if (ln.copy) cudaStreamDestroy(ln.copy);
+      if (l > 0 && ln.comp) cudaStreamDestroy(ln.comp);  // lane 0 computes on `main`
+    }
+    lanes.clear();
     if (d2h) cudaStreamDestroy(d2h);
-    copy = d2h = nullptr;
+    d2h = nullptr;
     e2e_chunk_elems = 0;
+    cudaSetDevice(prev);
   }
+  // NCCL prediction gather (set_gather).
+  std::shared_ptr<Comm> comm;
+  int root = 0;
+  std::vector<long long> g_first, g_rows;
+  float* gy = nullptr;
+  int32_t* glabels = nullptr;
+  std::size_t g_cap = 0;
   std::shared_ptr<const SampleStore> store;
   CombinationRule rule;
   std::size_t segments = 0;
@@ -303,7 +369,7 @@ InferenceSystem::InferenceSystem(const AllocationMatrix& A, const ClusterSpec& c
       cudaStream_t shared = nullptr;
       if (!options_.overlap_colocated)
         for (const auto& o : workers_)
-          if (o->phys == w->phys) shared = o->stream;
+          if (o->phys == w->phys && (!options_.row_nodes || o->row == w->row)) shared = o->stream;
       if (shared) {
         w->stream = shared;
         w->owns_stream = false;
@@ -322,6 +388,29 @@ InferenceSystem::InferenceSystem(const AllocationMatrix& A, const ClusterSpec& c
     throw StartupError("a worker reported out-of-memory during startup");
   }
   combine_dev_ = workers_.front()->phys;
+  combine_row_ = workers_.front()->row;
+  // Remote workers and NVLink peer access (both directions: the worker's GPU
+  // stores into the combining GPU's buffers, the combining GPU's copies may
+  // read a staging buffer).  Without peer access a remote worker stages.
+  for (auto& w : workers_) {
+    w->remote = w->phys != combine_dev_ || (options_.row_nodes && w->row != combine_row_);
+    if (!w->remote) continue;
+    bool peer = w->phys == combine_dev_;
+    if (!peer) {
+      if (std::find(peers_.begin(), peers_.end(), w->phys) == peers_.end()) {
+        int fwd = 0, back = 0;
+        ES_CUDA(cudaDeviceCanAccessPeer(&fwd, w->phys, combine_dev_));
+        ES_CUDA(cudaDeviceCanAccessPeer(&back, combine_dev_, w->phys));
+        if (fwd && back) {
+          enable_peer(w->phys, combine_dev_);
+          enable_peer(combine_dev_, w->phys);
+          peers_.push_back(w->phys);
+        }
+      }
+      peer = std::find(peers_.begin(), peers_.end(), w->phys) != peers_.end();
+    }
+    w->direct = peer && options_.peer_stores;
+  }
   OnDevice on(combine_dev_);
   ES_CUDA(cudaStreamCreateWithFlags(&impl_->main, cudaStreamNonBlocking));
   ES_CUDA(cudaEventCreate(&impl_->start));
@@ -359,6 +448,9 @@ void InferenceSystem::shutdown() {
     for (float* p : impl_->logits) cudaFree(p);
     cudaFree(impl_->y);
     cudaFree(impl_->labels);
+    cudaFree(impl_->gy);
+    cudaFree(impl_->glabels);
+    impl_->comm.reset();
     impl_->free_e2e();
     for (Impl::RowPartial& p : impl_->partials) {
       if (p.at_combine != p.local) cudaFree(p.at_combine);
@@ -411,7 +503,7 @@ void InferenceSystem::probe_rates(const SampleStore& X) {
     const long long want = (static_cast<long long>(grid) * w.batch + cluster_.segment_size - 1) /
                            cluster_.segment_size;
     const long long segs = std::max<long long>(1, std::min(S, want));
-    float* out = w.phys != combine_dev_ ? w.staging : impl_->logits[w.model];
+    float* out = w.staged(false) ? w.staging : impl_->logits[w.model];
     float ms = 0.0f;
     for (int rep = 0; rep < 2; ++rep) {
       ES_CUDA(cudaEventRecord(w.ev_begin, w.stream));
@@ -429,8 +521,14 @@ void InferenceSystem::probe_rates(const SampleStore& X) {
 
 bool InferenceSystem::single_device() const {
   for (const auto& w : workers_)
-    if (w->phys != combine_dev_) return false;
+    if (w->remote) return false;
   return true;
+}
+
+std::vector<int> InferenceSystem::worker_routes() const {
+  std::vector<int> r;
+  for (const auto& w : workers_) r.push_back(!w->remote ? 0 : w->direct ? 1 : 2);
+  return r;
 }
 
 std::vector<int> InferenceSystem::workers_per_model() const {
@@ -475,7 +573,7 @@ void InferenceSystem::begin_run(std::shared_ptr<const SampleStore> X, Combinatio
   }
   const std::size_t S = num_segments(nb, cluster_.segment_size);
   for (auto& w : workers_) {
-    if (w->phys != combine_dev_ && w->staging_rows < nb) {
+    if (w->remote && w->staging_rows < nb) {
       OnDevice on(w->phys);
       cudaFree(w->staging);
       ES_CUDA(cudaMalloc(&w->staging, std::max<std::size_t>(nb, 1) * C * sizeof(float)));
@@ -518,6 +616,27 @@ void InferenceSystem::begin_run(std::shared_ptr<const SampleStore> X, Combinatio
       }
     }
   }
+  if (impl_->comm) {
+    const int r = impl_->comm->rank();
+    if (static_cast<long long>(nb) != impl_->g_rows[r])
+      throw SpecError("gather plan gives rank " + std::to_string(r) + " " +
+                      std::to_string(impl_->g_rows[r]) + " rows, the store holds " +
+                      std::to_string(nb));
+    if (r == impl_->root) {
+      std::size_t total = 0;
+      for (long long n : impl_->g_rows) total += static_cast<std::size_t>(n);
+      if (total > impl_->g_cap) {
+        OnDevice on(combine_dev_);
+        cudaFree(impl_->gy);
+        cudaFree(impl_->glabels);
+        impl_->gy = nullptr;
+        impl_->glabels = nullptr;
+        ES_CUDA(cudaMalloc(&impl_->gy, total * C * sizeof(float)));
+        ES_CUDA(cudaMalloc(&impl_->glabels, total * sizeof(int32_t)));
+        impl_->g_cap = total;
+      }
+    }
+  }
   impl_->store = std::move(X);
   impl_->rule = std::move(rule);
   impl_->segments = S;
@@ -538,14 +657,17 @@ std::size_t InferenceSystem::broadcast() {
     OnDevice on(w->phys);
     ES_CUDA(cudaStreamWaitEvent(w->stream, impl_->start, 0));
     ES_CUDA(cudaEventRecord(w->ev_begin, w->stream));
-    const bool remote = w->phys != combine_dev_;
-    float* out = remote ? w->staging : impl_->logits[w->model];
+    const bool staged = w->staged(impl_->partial_mode);
+    float* out = staged ? w->staging : impl_->logits[w->model];
     int grid = es::num_sms(w->phys);
     if (options_.sms_per_worker > 0) grid = std::min(grid, options_.sms_per_worker);
+    Nvtx range("worker row " + std::to_string(w->row) + " model " + std::to_string(w->model) +
+               " b=" + std::to_string(w->batch) + " segments [" + std::to_string(w->seg_begin) +
+               "," + std::to_string(w->seg_end) + ")");
     launches_ += w->member->forward(X.device_replica(w->phys), nb, cluster_.segment_size,
                                     w->seg_begin, w->seg_end, out, grid, w->stream,
                                     w->marks.empty() ? nullptr : w->marks.data());
-    if (remote && w->seg_end > w->seg_begin && !impl_->partial_mode) {
+    if (staged && w->seg_end > w->seg_begin && !impl_->partial_mode) {
       const long long r0 = w->seg_begin * cluster_.segment_size;
       const long long r1 = std::min<long long>(w->seg_end * cluster_.segment_size, nb);
       ES_CUDA(cudaMemcpyPeerAsync(impl_->logits[w->model] + r0 * C, combine_dev_,
@@ -558,14 +680,57 @@ std::size_t InferenceSystem::broadcast() {
   OnDevice on(combine_dev_);
   for (auto& w : workers_) ES_CUDA(cudaStreamWaitEvent(impl_->main, w->ev_done, 0));
   ES_CUDA(cudaEventRecord(impl_->combine_begin, impl_->main));
+  Nvtx range("combine " + impl_->rule.name());
   es::CombineArgs ca = combine_args(impl_->rule, impl_->logits, static_cast<std::size_t>(nb),
                                     C, impl_->y, impl_->labels);
   if (nb > 0) {
     ES_LAUNCH(es::combine_launch(ca, impl_->main));
     ++launches_;
   }
-  ES_CUDA(cudaEventRecord(impl_->end, impl_->main));
+  finish_broadcast();
   return impl_->segments;
+}
+
+void InferenceSystem::finish_broadcast() {
+  if (impl_->comm) {
+    ES_CUDA(cudaGetLastError());
+    impl_->comm->gather_rows(impl_->y, impl_->labels, output_width_, impl_->g_first,
+                             impl_->g_rows, impl_->root, impl_->gy, impl_->glabels, impl_->main);
+  }
+  ES_CUDA(cudaEventRecord(impl_->end, impl_->main));
+}
+
+void InferenceSystem::set_gather(std::shared_ptr<Comm> comm, int root,
+                                 std::vector<long long> first_rows, std::vector<long long> rows) {
+  if (run_open_) throw Error("set_gather while a run is open");
+  if (!comm) {
+    impl_->comm.reset();
+    return;
+  }
+  if (comm->device() != combine_dev_)
+    throw SpecError("the gather communicator must live on the combining GPU (CUDA ordinal " +
+                    std::to_string(combine_dev_) + ")");
+  const int n = comm->size();
+  if (static_cast<int>(first_rows.size()) != n || static_cast<int>(rows.size()) != n)
+    throw SpecError("gather plan needs one (first row, rows) pair per rank");
+  if (root < 0 || root >= n) throw SpecError("gather root out of range");
+  // The ranks' row ranges tile [0, total) exactly once.
+  std::vector<std::pair<long long, long long>> r;
+  for (int i = 0; i < n; ++i) {
+    if (first_rows[i] < 0 || rows[i] < 0) throw SpecError("negative gather row range");
+    r.emplace_back(first_rows[i], rows[i]);
+  }
+  std::sort(r.begin(), r.end());
+  long long next = 0;
+  for (const auto& [f, k] : r) {
+    if (k == 0) continue;
+    if (f != next) throw SpecError("gather row ranges must tile the result exactly once");
+    next = f + k;
+  }
+  impl_->comm = std::move(comm);
+  impl_->root = root;
+  impl_->g_first = std::move(first_rows);
+  impl_->g_rows = std::move(rows);
 }
 
 // Fast gather (PoolOptions::row_partials): every device row folds its own
@@ -591,7 +756,7 @@ std::size_t InferenceSystem::broadcast_partials(long long nb) {
     Worker* last = nullptr;
     for (auto& w : workers_) {
       if (w->row != static_cast<int>(d)) continue;
-      ca.logits[ca.M] = w->phys != combine_dev_ ? w->staging : impl_->logits[w->model];
+      ca.logits[ca.M] = w->staged(true) ? w->staging : impl_->logits[w->model];
       ca.weight[ca.M] = rule.kind == CombinationRule::Kind::weighted_averaging
                             ? static_cast<float>(rule.weights[w->model])
                             : 1.0f / static_cast<float>(M);
@@ -630,7 +795,7 @@ std::size_t InferenceSystem::broadcast_partials(long long nb) {
   }
   ES_LAUNCH(es::combine_launch(fa, impl_->main));
   ++launches_;
-  ES_CUDA(cudaEventRecord(impl_->end, impl_->main));
+  finish_broadcast();
   return impl_->segments;
 }
 
@@ -657,13 +822,20 @@ RunOutput InferenceSystem::await_run() {
   for (std::size_t s = 0; s < impl_->segments; ++s)
     out.stats.segment_rows[s] = segment_bounds(static_cast<int>(s), cluster_.segment_size, nb).size();
   out.stats.elapsed_s = ms * 1e-3;
-  if (options_.copy_outputs && nb > 0) {
-    out.combined.resize(nb * output_width_);
-    out.winners.resize(nb);
-    ES_CUDA(cudaMemcpy(out.combined.data(), impl_->y, out.combined.size() * sizeof(float),
-                       cudaMemcpyDeviceToHost));
-    ES_CUDA(cudaMemcpy(out.winners.data(), impl_->labels, nb * sizeof(int32_t),
-                       cudaMemcpyDeviceToHost));
+  // The gather root returns every rank's rows.
+  const bool gathered = impl_->comm && impl_->comm->rank() == impl_->root;
+  std::size_t rows = nb;
+  if (gathered) {
+    rows = 0;
+    for (long long n : impl_->g_rows) rows += static_cast<std::size_t>(n);
+  }
+  if (options_.copy_outputs && rows > 0) {
+    out.combined.resize(rows * output_width_);
+    out.winners.resize(rows);
+    ES_CUDA(cudaMemcpy(out.combined.data(), gathered ? impl_->gy : impl_->y,
+                       out.combined.size() * sizeof(float), cudaMemcpyDeviceToHost));
+    ES_CUDA(cudaMemcpy(out.winners.data(), gathered ? impl_->glabels : impl_->labels,
+                       rows * sizeof(int32_t), cudaMemcpyDeviceToHost));
   }
   return out;
 }
@@ -790,8 +962,6 @@ double InferenceSystem::run_host_blocks(const std::vector<HostRowBlock>& blocks,
 // host conversion, which no CUDA event can see).
 double InferenceSystem::run_host_core(std::size_t nb, std::size_t width, float* Y_out,
                                       std::int32_t* labels_out, const HostFill& fill) {
-  for (const auto& w : workers_)
-    if (w->phys != combine_dev_) throw SpecError("run_host needs every worker on one GPU");
   if (run_open_) throw Error("previous run still open");
   for (const ModelSpec& m : cluster_.models)
     if (m.arch.kind != MemberArch::Kind::Synthetic &&
@@ -807,65 +977,154 @@ double InferenceSystem::run_host_core(std::size_t nb, std::size_t width, float* 
   if (chunk * width > I.e2e_chunk_elems) {
     I.free_e2e();
     I.e2e_chunk_elems = chunk * width;
+    // Lanes: the combining node first, then every other node in worker order.
+    auto node_of = [&](const Worker& w) {
+      return w.remote ? (options_.row_nodes ? 1000000 + w.row : w.phys) : -1;
+    };
+    std::vector<int> keys;
+    for (std::size_t i = 0; i < workers_.size(); ++i) {
+      const int key = node_of(*workers_[i]);
+      auto it = std::find(keys.begin(), keys.end(), key);
+      std::size_t l = static_cast<std::size_t>(it - keys.begin());
+      if (it == keys.end()) {
+        if (key == -1) {  // keep the combining node at lane 0
+          keys.insert(keys.begin(), key);
+          I.lanes.insert(I.lanes.begin(), Impl::Lane{});
+          l = 0;
+        } else {
+          keys.push_back(key);
+          I.lanes.emplace_back();
+        }
+        I.lanes[l].phys = workers_[i]->phys;
+      }
+      I.lanes[l].workers.push_back(static_cast<int>(i));
+    }
+    if (keys.empty() || keys.front() != -1) {  // no worker on the combining node
+      keys.insert(keys.begin(), -1);
+      I.lanes.insert(I.lanes.begin(), Impl::Lane{});
+      I.lanes[0].phys = combine_dev_;
+    }
+    for (std::size_t l = 0; l < I.lanes.size(); ++l) {
+      Impl::Lane& ln = I.lanes[l];
+      OnDevice od(ln.phys);
+      ES_CUDA(cudaStreamCreateWithFlags(&ln.copy, cudaStreamNonBlocking));
+      if (l == 0)
+        ln.comp = I.main;
+      else
+        ES_CUDA(cudaStreamCreateWithFlags(&ln.comp, cudaStreamNonBlocking));
+      for (Impl::Lane::LSlot& ls : ln.s) {
+        ES_CUDA(cudaMalloc(&ls.x32, chunk * width * sizeof(float)));
+        ES_CUDA(cudaMalloc(&ls.x16, chunk * width * 2));
+        ls.staging.assign(M, nullptr);
+        for (int wi : ln.workers)
+          if (workers_[wi]->staged(false) && !ls.staging[workers_[wi]->model])
+            ES_CUDA(cudaMalloc(&ls.staging[workers_[wi]->model], chunk * C * sizeof(float)));
+        ES_CUDA(cudaEventCreateWithFlags(&ls.h2d_done, cudaEventDisableTiming));
+        ES_CUDA(cudaEventCreateWithFlags(&ls.comp_done, cudaEventDisableTiming));
+      }
+    }
     for (int s = 0; s < kSlots; ++s) {
       Impl::Slot& sl = I.slots[s];
-      ES_CUDA(cudaHostAlloc(&sl.pinned, chunk * width * 2, cudaHostAllocDefault));
-      ES_CUDA(cudaMalloc(&sl.x32, chunk * width * sizeof(float)));
-      ES_CUDA(cudaMalloc(&sl.x16, chunk * width * 2));
+      // Portable: every lane's GPU DMAs from it.
+      ES_CUDA(cudaHostAlloc(&sl.pinned, chunk * width * 2, cudaHostAllocPortable));
       sl.logits.assign(M, nullptr);
       for (float*& p : sl.logits) ES_CUDA(cudaMalloc(&p, chunk * C * sizeof(float)));
       ES_CUDA(cudaMalloc(&sl.y, chunk * C * sizeof(float)));
       ES_CUDA(cudaMalloc(&sl.labels, chunk * sizeof(int32_t)));
-      ES_CUDA(cudaEventCreateWithFlags(&sl.h2d_done, cudaEventDisableTiming));
-      ES_CUDA(cudaEventCreateWithFlags(&sl.comp_done, cudaEventDisableTiming));
+      ES_CUDA(cudaEventCreateWithFlags(&sl.combined, cudaEventDisableTiming));
       ES_CUDA(cudaEventCreateWithFlags(&sl.d2h_done, cudaEventDisableTiming));
     }
-    ES_CUDA(cudaStreamCreateWithFlags(&I.copy, cudaStreamNonBlocking));
     ES_CUDA(cudaStreamCreateWithFlags(&I.d2h, cudaStreamNonBlocking));
   }
   if (!I.pool) I.pool = std::make_unique<ThreadPool>(0);
-  ES_CUDA(cudaDeviceSynchronize());
+  for (const Impl::Lane& ln : I.lanes) {
+    OnDevice od(ln.phys);
+    ES_CUDA(cudaDeviceSynchronize());
+  }
+  for (Impl::Lane& ln : I.lanes)
+    for (Impl::Lane::LSlot& ls : ln.s) ls.used = false;
   const auto t0 = std::chrono::steady_clock::now();
   launches_ = 0;
   h2d_bytes_ = d2h_bytes_ = 0;
   const std::size_t nchunks = (nb + chunk - 1) / chunk;
-  const int grid = es::num_sms(combine_dev_);
   for (std::size_t i = 0; i < nchunks; ++i) {
-    Impl::Slot& sl = I.slots[i % kSlots];
+    const int si = static_cast<int>(i % kSlots);
+    Impl::Slot& sl = I.slots[si];
+    Nvtx range("run_host chunk " + std::to_string(i));
     const std::size_t r0 = i * chunk;
     const std::size_t rows = std::min(chunk, nb - r0);
-    const std::size_t elems = rows * width;
-    if (i >= kSlots) ES_CUDA(cudaEventSynchronize(sl.h2d_done));  // pinned slot reusable
+    if (i >= kSlots)  // the pinned slot is reusable once every lane's H2D of chunk i-3 is done
+      for (Impl::Lane& ln : I.lanes)
+        if (ln.s[si].used) ES_CUDA(cudaEventSynchronize(ln.s[si].h2d_done));
     const HostChunk src = fill(i, static_cast<std::uint16_t*>(sl.pinned), r0, rows);
     const float* direct = src.fp32 ? static_cast<const float*>(src.src) : nullptr;
-    if (i >= kSlots) ES_CUDA(cudaStreamWaitEvent(I.copy, sl.d2h_done, 0));  // slot buffers free
-    h2d_bytes_ += elems * (direct ? sizeof(float) : 2);
-    d2h_bytes_ += (Y_out ? rows * C * sizeof(float) : 0) + (labels_out ? rows * sizeof(int32_t) : 0);
-    if (!direct)
-      ES_CUDA(cudaMemcpyAsync(sl.x16, src.src ? src.src : sl.pinned, elems * 2,
-                              cudaMemcpyHostToDevice, I.copy));
-    else
-      ES_CUDA(cudaMemcpyAsync(sl.x32, direct, elems * sizeof(float), cudaMemcpyHostToDevice,
-                              I.copy));
-    ES_CUDA(cudaEventRecord(sl.h2d_done, I.copy));
-    ES_CUDA(cudaStreamWaitEvent(I.main, sl.h2d_done, 0));
-    if (direct) {
-      ES_LAUNCH(es::convert_f32_to_bf16(sl.x32, static_cast<__nv_bfloat16*>(sl.x16), elems, I.main));
-      ++launches_;
-    }
+    const std::uint16_t* bf = static_cast<const std::uint16_t*>(src.src ? src.src : sl.pinned);
     std::vector<SegmentShare> shares =
         rates_.empty() ? segment_shares(matrix_, rows, cluster_.segment_size)
                        : segment_shares_weighted(matrix_, rows, cluster_.segment_size, rates_);
-    for (std::size_t w = 0; w < workers_.size(); ++w)
-      launches_ += workers_[w]->member->forward(sl.x16, static_cast<long long>(rows),
-                                                cluster_.segment_size, shares[w].begin,
-                                                shares[w].end, sl.logits[workers_[w]->model], grid,
-                                                I.main);
+    for (std::size_t l = 0; l < I.lanes.size(); ++l) {
+      Impl::Lane& ln = I.lanes[l];
+      Impl::Lane::LSlot& ls = ln.s[si];
+      // Rows this lane's workers predict in the chunk (their segment runs are
+      // contiguous; a lane with a whole member needs the whole chunk).
+      long long sb = -1, se = -1;
+      for (int wi : ln.workers)
+        if (shares[wi].end > shares[wi].begin) {
+          sb = sb < 0 ? shares[wi].begin : std::min<long long>(sb, shares[wi].begin);
+          se = std::max<long long>(se, shares[wi].end);
+        }
+      ls.used = sb >= 0;
+      if (!ls.used) continue;
+      const std::size_t g0 = static_cast<std::size_t>(sb) * seg;
+      const std::size_t g1 = std::min(static_cast<std::size_t>(se) * seg, rows);
+      const std::size_t elems = (g1 - g0) * width;
+      OnDevice od(ln.phys);
+      // x16/x32 of this slot are free once the lane's compute of chunk i-3 is done.
+      if (i >= kSlots) ES_CUDA(cudaStreamWaitEvent(ln.copy, ls.comp_done, 0));
+      h2d_bytes_ += elems * (direct ? sizeof(float) : 2);
+      if (!direct)
+        ES_CUDA(cudaMemcpyAsync(static_cast<std::uint16_t*>(ls.x16) + g0 * width, bf + g0 * width,
+                                elems * 2, cudaMemcpyHostToDevice, ln.copy));
+      else
+        ES_CUDA(cudaMemcpyAsync(ls.x32 + g0 * width, direct + g0 * width, elems * sizeof(float),
+                                cudaMemcpyHostToDevice, ln.copy));
+      ES_CUDA(cudaEventRecord(ls.h2d_done, ln.copy));
+      ES_CUDA(cudaStreamWaitEvent(ln.comp, ls.h2d_done, 0));
+      if (direct) {
+        ES_LAUNCH(es::convert_f32_to_bf16(ls.x32 + g0 * width,
+                                          static_cast<__nv_bfloat16*>(ls.x16) + g0 * width, elems,
+                                          ln.comp));
+        ++launches_;
+      }
+      // The combining slot's logits are free once its combine of chunk i-3 ran.
+      if (i >= kSlots) ES_CUDA(cudaStreamWaitEvent(ln.comp, sl.combined, 0));
+      const int grid = es::num_sms(ln.phys);
+      for (int wi : ln.workers) {
+        Worker& w = *workers_[wi];
+        const SegmentShare& sh = shares[wi];
+        if (sh.end <= sh.begin) continue;
+        const bool staged = w.staged(false);
+        float* out = staged ? ls.staging[w.model] : sl.logits[w.model];
+        launches_ += w.member->forward(ls.x16, static_cast<long long>(rows), cluster_.segment_size,
+                                       sh.begin, sh.end, out, grid, ln.comp);
+        if (staged) {
+          const std::size_t a = static_cast<std::size_t>(sh.begin) * seg;
+          const std::size_t e = std::min(static_cast<std::size_t>(sh.end) * seg, rows);
+          ES_CUDA(cudaMemcpyPeerAsync(sl.logits[w.model] + a * C, combine_dev_, out + a * C,
+                                      ln.phys, (e - a) * C * sizeof(float), ln.comp));
+        }
+      }
+      ES_CUDA(cudaEventRecord(ls.comp_done, ln.comp));
+    }
+    for (std::size_t l = 1; l < I.lanes.size(); ++l)
+      if (I.lanes[l].s[si].used) ES_CUDA(cudaStreamWaitEvent(I.main, I.lanes[l].s[si].comp_done, 0));
+    if (i >= kSlots) ES_CUDA(cudaStreamWaitEvent(I.main, sl.d2h_done, 0));  // y/labels free
+    d2h_bytes_ += (Y_out ? rows * C * sizeof(float) : 0) + (labels_out ? rows * sizeof(int32_t) : 0);
     es::CombineArgs ca = combine_args(rule_, sl.logits, rows, C, sl.y, sl.labels);
     ES_LAUNCH(es::combine_launch(ca, I.main));
     ++launches_;
-    ES_CUDA(cudaEventRecord(sl.comp_done, I.main));
-    ES_CUDA(cudaStreamWaitEvent(I.d2h, sl.comp_done, 0));
+    ES_CUDA(cudaEventRecord(sl.combined, I.main));
+    ES_CUDA(cudaStreamWaitEvent(I.d2h, sl.combined, 0));
     if (Y_out)
       ES_CUDA(cudaMemcpyAsync(Y_out + r0 * C, sl.y, rows * C * sizeof(float),
                               cudaMemcpyDeviceToHost, I.d2h));
@@ -875,7 +1134,10 @@ double InferenceSystem::run_host_core(std::size_t nb, std::size_t width, float* 
     ES_CUDA(cudaEventRecord(sl.d2h_done, I.d2h));
   }
   ES_CUDA(cudaStreamSynchronize(I.d2h));
-  ES_CUDA(cudaStreamSynchronize(I.main));
+  for (const Impl::Lane& ln : I.lanes) {
+    OnDevice od(ln.phys);
+    ES_CUDA(cudaStreamSynchronize(ln.comp));
+  }
   const auto t1 = std::chrono::steady_clock::now();
   return std::chrono::duration<double>(t1 - t0).count();
 }
@@ -1090,6 +1352,16 @@ void combine_blocks(const CombinationRule& rule, int M, int C, std::size_t rows,
   for (float* p : dev) cudaFree(p);
   cudaFree(dy);
   cudaFree(dl);
+}
+
+std::string device_identity() {
+  const int n = visible_devices();
+  cudaDeviceProp p{};
+  ES_CUDA(cudaGetDeviceProperties(&p, 0));
+  char buf[256];
+  std::snprintf(buf, sizeof(buf), "%s/sm_%d%d/%d SMs/%.0f GiB x%d", p.name, p.major, p.minor,
+                p.multiProcessorCount, static_cast<double>(p.totalGlobalMem) / (1 << 30), n);
+  return buf;
 }
 
 void derive_footprint(ModelSpec& model) {

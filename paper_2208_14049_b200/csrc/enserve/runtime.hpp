@@ -141,10 +141,22 @@ struct PoolOptions {
   // floats per sample per row instead of per member.  fp32 sums in another
   // order (votes stay exact); applies when no model is data-parallel.
   bool row_partials = false;
+  // Remote workers (another GPU than the combining one) store their logits
+  // straight into the combining GPU's buffers through NVLink peer mappings
+  // (cudaDeviceEnablePeerAccess at construction) -- no staging copy.  Off, or
+  // where the pair has no peer access, they write a local staging buffer that
+  // cudaMemcpyPeerAsync moves after the member kernels.
+  bool peer_stores = true;
+  // Every cluster device row is its own node -- own stream, own logits
+  // staging and gather, own run_host lane -- even where rows share a CUDA
+  // ordinal.  Lays an N-GPU matrix out on fewer GPUs with the multi-GPU data
+  // path intact (tests exercise every cross-device branch on one GPU this way).
+  bool row_nodes = false;
 };
 
 // Per-model executable member on one GPU (the Predictor of backend.hpp:25-34).
 class DeviceMember;
+class Comm;
 
 class InferenceSystem {
  public:
@@ -162,9 +174,19 @@ class InferenceSystem {
   RunOutput await_run();
   void shutdown();
 
+  // One process per GPU (torchrun): after every run's combine, this rank's
+  // probabilities + argmax are gathered over NCCL to rank `root`, at row
+  // first_rows[rank] of a sum(rows)-row result -- inside the timed window.
+  // The root's await_run returns the gathered rows; every rank's run must
+  // cover exactly rows[rank] samples.  The comm must live on the combining GPU.
+  void set_gather(std::shared_ptr<Comm> comm, int root, std::vector<long long> first_rows,
+                  std::vector<long long> rows);
+
   // End-to-end variant: X from (preferably pinned) host memory, combined output
-  // and labels back to host, all copies inside the CUDA-event window.  Single
-  // physical GPU only.
+  // and labels back to host, all copies inside the timed window.  Every node
+  // (GPU, or device row with row_nodes) hosting workers is a lane with its own
+  // copy stream: it receives the rows its workers predict over its own PCIe
+  // link, and remote logits reach the combining GPU as in broadcast().
   double run_host(const float* X, std::size_t nb, std::size_t width, float* Y_out,
                   std::int32_t* labels_out);
   // The same pipeline over rows already converted to bf16 and held in several
@@ -177,7 +199,7 @@ class InferenceSystem {
   };
   double run_host_blocks(const std::vector<HostRowBlock>& blocks, std::size_t width,
                          float* Y_out, std::int32_t* labels_out);
-  // Every worker on one physical GPU (run_host / run_host_blocks apply).
+  // Every worker on the combining node (no remote worker).
   bool single_device() const;
 
   int worker_count() const { return static_cast<int>(workers_.size()); }
@@ -197,6 +219,12 @@ class InferenceSystem {
   std::vector<double> last_kernel_ms(int worker) const;
   std::vector<std::string> kernel_names(int worker) const;
   int combine_device() const { return combine_dev_; }
+  // Per worker: 0 = local to the combining node, 1 = remote with direct peer
+  // stores, 2 = remote through a staging buffer + peer copy.
+  std::vector<int> worker_routes() const;
+  // CUDA ordinals (other than the combining GPU) with peer access enabled
+  // towards and from the combining GPU.
+  const std::vector<int>& peer_devices() const { return peers_; }
   // Segment runs [begin, end) of every worker in the last run, and the rows/s
   // each data-parallel worker measured when probed (1.0 for single workers).
   std::vector<std::pair<long long, long long>> last_shares() const;
@@ -214,6 +242,7 @@ class InferenceSystem {
   using HostFill = std::function<HostChunk(std::size_t, std::uint16_t*, std::size_t, std::size_t)>;
   void probe_rates(const SampleStore& X);
   std::size_t broadcast_partials(long long nb);
+  void finish_broadcast();  // prediction gather (if any) + the end event
   std::vector<double> rates_;  // per worker, probed on the first run with a DP column
   double run_host_core(std::size_t nb, std::size_t width, float* Y_out, std::int32_t* labels_out,
                        const HostFill& fill);
@@ -225,6 +254,8 @@ class InferenceSystem {
   PoolOptions options_;
   int output_width_ = 0;
   int combine_dev_ = 0;
+  int combine_row_ = 0;
+  std::vector<int> peers_;
   std::vector<std::unique_ptr<Worker>> workers_;
   std::unique_ptr<Impl> impl_;
   int launches_ = 0;
@@ -265,6 +296,10 @@ class B200Predictor {
 // device: y[rows*C], winners[rows] (argmax, lowest index on ties).
 void combine_blocks(const CombinationRule& rule, int M, int C, std::size_t rows,
                     const float* const* blocks, float* y, std::int32_t* winners);
+
+// "<name>/sm_<cc>/<SMs> SMs/<GiB> GiB x<count>" of the visible GPUs (all of
+// the first GPU's kind): the hardware half of an opt-in matrix-cache key.
+std::string device_identity();
 
 // Fill ModelSpec footprint fields from its MLP architecture (bf16 weights,
 // bf16 activations per sample) when they are zero.

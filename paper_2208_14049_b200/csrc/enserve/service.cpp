@@ -29,14 +29,14 @@ PredictionService::~PredictionService() {
 void PredictionService::init_pool() {
   try {
     system_ = std::make_unique<InferenceSystem>(matrix_, cluster_, config_.rule, config_.pool);
-    host_blocks_ = system_->single_device();
     // Pinned slots, streams and the host pool up front (and the input width
     // checked against the members), so the first flush pays none of it.
-    if (host_blocks_) system_->run_host_blocks({}, config_.input_width, nullptr, nullptr);
-    if (host_blocks_ && config_.arena_rows > 0)
+    system_->run_host_blocks({}, config_.input_width, nullptr, nullptr);
+    if (config_.arena_rows > 0)
       for (Arena& a : arena_) {
         void* p = nullptr;
-        if (cudaHostAlloc(&p, config_.arena_rows * config_.input_width * 2, cudaHostAllocDefault) !=
+        // Portable: every GPU of a multi-GPU pool DMAs its rows from here.
+        if (cudaHostAlloc(&p, config_.arena_rows * config_.input_width * 2, cudaHostAllocPortable) !=
             cudaSuccess) {
           cudaGetLastError();
           throw StartupError("cannot allocate the service's page-locked arenas");
@@ -79,7 +79,7 @@ std::future<RunOutput> PredictionService::submit(const float* samples, std::size
   if (!ready_.load()) throw NotReadyError("service not ready");
   p->rows = rows;
   const std::size_t elems = rows * config_.input_width;
-  if (host_blocks_ && arena_[0].rows) {
+  if (arena_[0].rows) {
     // Reserve rows in the open arena (in buffer order), convert into them
     // outside the lock; the flush waits for the arena's writers.
     std::uint16_t* dst = nullptr;
@@ -111,12 +111,9 @@ std::future<RunOutput> PredictionService::submit(const float* samples, std::size
   // The copy the request needs anyway doubles as the fp32 -> bf16 conversion
   // (on the caller's thread, so it scales with the clients), halving what the
   // flush gathers and sends over PCIe.
-  if (host_blocks_) {  // arena full or too small for this request
-    p->bf16.resize(elems);
-    convert_f32_to_bf16_range(samples, p->bf16.data(), elems);
-  } else {
-    p->samples.assign(samples, samples + elems);
-  }
+  // Arena full or too small for this request.
+  p->bf16.resize(elems);
+  convert_f32_to_bf16_range(samples, p->bf16.data(), elems);
   {
     std::lock_guard<std::mutex> lock(buffer_mutex_);
     // Checked under the buffer lock: the dispatcher fails whatever it finds
@@ -146,7 +143,7 @@ void PredictionService::flush_locked(std::unique_lock<std::mutex>& lock) {
   for (const auto& r : batch) total += r->rows;
   try {
     RunOutput out;
-    if (host_blocks_) {
+    {
       std::vector<InferenceSystem::HostRowBlock> blocks;
       blocks.reserve(batch.size());
       for (const auto& r : batch) {
@@ -169,12 +166,6 @@ void PredictionService::flush_locked(std::unique_lock<std::mutex>& lock) {
           reinterpret_cast<std::int32_t*>(out.winners.data()));
       out.stats.nb_samples = total;
       out.stats.segments = num_segments(total, cluster_.segment_size);
-    } else {
-      std::vector<float> data;
-      data.reserve(total * config_.input_width);
-      for (const auto& r : batch) data.insert(data.end(), r->samples.begin(), r->samples.end());
-      auto store = std::make_shared<SampleStore>(std::move(data), total, config_.input_width);
-      out = system_->run(store);
     }
     if (out.stats.elapsed_s > 0) last_flush_throughput_.store(total / out.stats.elapsed_s);
     samples_served_.fetch_add(total);

@@ -68,7 +68,6 @@ class PredictionService {
 
  private:
   struct Pending {
-    std::vector<float> samples;          // multi-GPU pools: fp32 rows for a SampleStore
     std::vector<std::uint16_t> bf16;     // one-GPU pools: rows converted by the caller
     const std::uint16_t* staged = nullptr;  // ... or their place in a pinned arena
     int arena = -1;
@@ -85,7 +84,6 @@ class PredictionService {
   ServiceConfig config_;
   std::unique_ptr<InferenceSystem> system_;
   std::atomic<bool> ready_{false};
-  bool host_blocks_ = false;  // pool on one GPU: flush through run_host_blocks
   struct Arena {
     std::uint16_t* rows = nullptr;  // page-locked, arena_rows x input_width bf16
     std::size_t used = 0;           // rows handed out

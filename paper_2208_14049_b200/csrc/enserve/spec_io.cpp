@@ -1,6 +1,8 @@
 // Spec / matrix documents and the matrix cache (design in spec_io.hpp).
 #include "enserve/spec_io.hpp"
 
+#include <unistd.h>
+
 #include <chrono>
 #include <cstdio>
 #include <filesystem>
@@ -242,19 +244,59 @@ std::string digest_hex(const std::string& canonical) {
 }
 
 std::string cache_key(const ClusterSpec& cluster, const OptimizerKey& key) {
+  js::Value settings = js::Value::object();
+  settings["max_iter"] = key.greedy.max_iter;
+  settings["max_neighs"] = key.greedy.max_neighs;
+  settings["rng_seed"] = key.greedy.rng_seed;
+  settings["default_batch"] = key.default_batch;
+  settings["bench_mode"] = key.bench_mode;
+  settings["calib_samples"] = static_cast<std::uint64_t>(key.calib_samples);
+  settings["repeats"] = key.repeats;
+  // Opt-in hardware identity: a matrix measured on other GPUs then misses.
+  // Empty keeps the digest equal to the reference's for the same inputs.
+  if (!key.device.empty()) settings["device"] = key.device;
   js::Value doc = js::Value::object();
+  doc["optimizer"] = std::move(settings);
   doc["specs"] = cluster_to_json(cluster);
-  js::Value o = js::Value::object();
-  o["max_iter"] = key.greedy.max_iter;
-  o["max_neighs"] = key.greedy.max_neighs;
-  o["rng_seed"] = key.greedy.rng_seed;
-  o["default_batch"] = key.default_batch;
-  o["bench_mode"] = key.bench_mode;
-  o["calib_samples"] = static_cast<std::uint64_t>(key.calib_samples);
-  o["repeats"] = key.repeats;
-  doc["optimizer"] = std::move(o);
   return digest_hex(js::dump(doc));
 }
+
+namespace {
+
+// Why a cache file cannot serve `key`, or "" when `entry` was filled.
+std::string read_entry(const std::string& path, const std::string& key, const ClusterSpec& cluster,
+                       MatrixCacheEntry* entry) {
+  js::Value doc;
+  try {
+    doc = load_json_file(path);
+  } catch (const std::exception& e) {
+    return std::string("unreadable: ") + e.what();
+  }
+  const js::Value* stored_key = doc.find("key");
+  if (stored_key == nullptr || stored_key->as_string() != key) return "written for another key";
+  const js::Value* matrix = doc.find("matrix");
+  const js::Value* score = doc.find("score");
+  if (matrix == nullptr || score == nullptr) return "no matrix or score";
+  try {
+    entry->matrix = matrix_from_json(*matrix, cluster);
+    entry->score = score->as_double();
+    const js::Value* created = doc.find("created_at");
+    entry->created_at = created ? created->as_int() : 0;
+  } catch (const std::exception& e) {
+    return std::string("malformed: ") + e.what();
+  }
+  if (!validate_matrix(entry->matrix, cluster).ok) return "matrix not valid for this cluster";
+  entry->key = key;
+  return "";
+}
+
+std::int64_t unix_seconds() {
+  return std::chrono::duration_cast<std::chrono::seconds>(
+             std::chrono::system_clock::now().time_since_epoch())
+      .count();
+}
+
+}  // namespace
 
 MatrixCache::MatrixCache(std::string directory) : directory_(std::move(directory)) {
   std::filesystem::create_directories(directory_);
@@ -268,48 +310,27 @@ std::optional<MatrixCacheEntry> MatrixCache::lookup(const std::string& key,
                                                     const ClusterSpec& cluster) const {
   const std::string path = path_for(key);
   if (!std::filesystem::exists(path)) return std::nullopt;
-  try {
-    const js::Value doc = load_json_file(path);
-    const js::Value* k = doc.find("key");
-    if (!k || k->as_string() != key) {
-      std::cerr << "enserve: cache file " << path << " has a stale key; ignoring\n";
-      return std::nullopt;
-    }
-    MatrixCacheEntry entry;
-    entry.key = key;
-    const js::Value* mx = doc.find("matrix");
-    const js::Value* sc = doc.find("score");
-    if (!mx || !sc) throw SpecError("cache document lacks matrix or score");
-    entry.matrix = matrix_from_json(*mx, cluster);
-    entry.score = sc->as_double();
-    if (const js::Value* c = doc.find("created_at")) entry.created_at = c->as_int();
-    if (!validate_matrix(entry.matrix, cluster).ok) {
-      std::cerr << "enserve: cached matrix in " << path << " is invalid; ignoring\n";
-      return std::nullopt;
-    }
-    return entry;
-  } catch (const std::exception& e) {
-    std::cerr << "enserve: cannot read cache file " << path << " (" << e.what()
-              << "); treating as a miss\n";
-    return std::nullopt;
-  }
+  MatrixCacheEntry entry;
+  const std::string why = read_entry(path, key, cluster, &entry);
+  if (why.empty()) return entry;
+  std::cerr << "enserve-b200: matrix cache miss for " << key << " (" << why << "): " << path
+            << "\n";
+  return std::nullopt;
 }
 
 void MatrixCache::store(const MatrixCacheEntry& entry, const ClusterSpec& cluster) const {
   js::Value doc = js::Value::object();
+  doc["created_at"] = static_cast<long long>(entry.created_at ? entry.created_at : unix_seconds());
   doc["key"] = entry.key;
   doc["matrix"] = matrix_to_json(entry.matrix, cluster);
   doc["score"] = entry.score;
-  doc["created_at"] = static_cast<long long>(
-      entry.created_at != 0
-          ? entry.created_at
-          : std::chrono::duration_cast<std::chrono::seconds>(
-                std::chrono::system_clock::now().time_since_epoch())
-                .count());
-  const std::string path = path_for(entry.key);
-  const std::string tmp = path + ".tmp";
-  save_json_file(tmp, doc);
-  std::filesystem::rename(tmp, path);  // atomic overwrite
+  // Readers never see a half-written entry: write a sibling, then rename it
+  // over the entry (rename within one directory replaces atomically).
+  const std::filesystem::path final_path(path_for(entry.key));
+  std::filesystem::path staging = final_path;
+  staging += ".partial." + std::to_string(static_cast<long long>(::getpid()));
+  save_json_file(staging.string(), doc);
+  std::filesystem::rename(staging, final_path);
 }
 
 }  // namespace enserve

@@ -45,6 +45,11 @@ struct OptimizerKey {
   std::string bench_mode;  // "measured" or "analytic"
   std::size_t calib_samples = 0;
   int repeats = 1;
+  // Opt-in (empty = off, the reference's key): identity of the GPUs the
+  // measured bench ran on (device_identity()), so a matrix tuned on other
+  // hardware is a miss.  Reference tools never set it, so keys they compute
+  // still match ours whenever it is empty.
+  std::string device;
 };
 
 // digest of {"optimizer": settings, "specs": cluster_to_json} (cache.cpp:22-33).

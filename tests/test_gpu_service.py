@@ -175,3 +175,40 @@ def test_arena_sizes_give_identical_answers(arena_rows):
     ref = offline(np.concatenate(reqs), A, c)
     np.testing.assert_array_equal(np.concatenate([g[0] for g in got]), ref.combined)
     np.testing.assert_array_equal(np.concatenate([g[1] for g in got]), ref.winners)
+
+
+def test_service_matches_the_reference_pipeline_with_mlp_and_cnn_members():
+    """The reference's fidelity test (test_server.cpp:176-221) compares served
+    predictions with offline inference; here the offline side is the
+    reference's own InferenceSystem (oracle/_ref, pipeline.cpp) running the
+    oracle CPU members of the cfg2 roster (MLPs + CNN), and the requests
+    arrive from four concurrent clients with ragged sizes."""
+    import bench
+    from oracle import refcpu
+    from test_gpu_parity import TOL_P, assert_labels_identical_or_tied
+    if not refcpu.ref_available():
+        pytest.skip("oracle/_ref not built")
+    c = bench.make_cluster(es, {"roster": bench.ROSTER, "devices": 1, "device_mib": 183359.0})
+    A = es.AllocationMatrix.from_array([[128, 64, 128, 32]])
+    rule = es.CombinationRule.averaging(softmax=True)
+    X = refcpu.features(501, 1300, 784)
+    sizes = [1, 37, 128, 200, 3, 331, 100, 500]
+    cuts = np.cumsum([0] + sizes)
+    Yr, _, _ = refcpu.ref_run_ensemble(c, A.cells, X, rule=0, softmax=True)
+    got = [None] * len(sizes)
+    with es.PredictionService(c, A, rule, flush_timeout_ms=5) as svc:
+        assert svc.wait_ready(60.0)
+
+        def client(k):
+            for i in range(k, len(sizes), 4):
+                got[i] = svc.predict(X[cuts[i]:cuts[i + 1]])
+
+        threads = [threading.Thread(target=client, args=(k,)) for k in range(4)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+    Y = np.concatenate([g[0] for g in got])
+    W = np.concatenate([g[1] for g in got])
+    assert np.abs(Y - Yr).max() <= TOL_P
+    assert_labels_identical_or_tied(W, Yr, TOL_P, "service vs reference pipeline")

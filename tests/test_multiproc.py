@@ -35,8 +35,28 @@ def _worker(rank: int, world: int, port: int, q):
         t = dist.max(float(rank + 1) * 0.5)
         # bench.py: rank 0's optimized matrix reaches every rank.
         cells = dist.broadcast_object([[128, 64, 128, 32]] if rank == 0 else None)
+        # The prediction gather's plan (InferenceSystem.set_gather): every
+        # rank derives the same one; emulate the NCCL send/recv with gloo --
+        # each rank's rows (labelled with their global row index) must land
+        # at their place in rank 0's result.
+        firsts, counts = bench.gather_plan(es, world, [64, 64, 128, 128], nb_per_gpu)
+        plans = dist.gather([firsts, counts])
+        import torch
+        import torch.distributed as tdist
+        mine = torch.arange(r0, r1, dtype=torch.int64)
+        if rank == 0:
+            result = torch.full((sum(counts),), -1, dtype=torch.int64)
+            result[firsts[0]:firsts[0] + counts[0]] = mine
+            for r in range(1, world):
+                buf = torch.empty(counts[r], dtype=torch.int64)
+                tdist.recv(buf, src=r)
+                result[firsts[r]:firsts[r] + counts[r]] = buf
+            gathered = result.tolist()
+        else:
+            tdist.send(mine, dst=0)
+            gathered = None
         dist.barrier()
-        q.put((rank, rows, t, shares, cells))
+        q.put((rank, rows, t, shares, cells, plans, gathered))
     finally:
         dist.close()
 
@@ -54,7 +74,12 @@ def test_rank_shards_cover_every_segment_once_and_max_time(world):
         p.join(timeout=60)
         assert p.exitcode == 0
     total = world * 1037
-    for rank, rows, t, shares, cells in results:
+    for rank, rows, t, shares, cells, plans, gathered in results:
+        assert all(p == plans[0] for p in plans)  # one plan on every rank
+        firsts, counts = plans[0]
+        assert [(f, f + c) for f, c in zip(firsts, counts)] == [tuple(r) for r in rows]
+        if rank == 0:
+            assert gathered == list(range(total))  # every row once, in place
         assert t == pytest.approx(world * 0.5)  # max over ranks
         assert cells == [[128, 64, 128, 32]]
         spans = sorted(tuple(r) for r in rows)

@@ -2,6 +2,7 @@
 against what the reference's own spec_io.cpp + cache.cpp print
 (tests/golden/spec_io.json, made by oracle/spec_golden.cpp).  Host-only: no
 GPU needed."""
+import dataclasses
 import json
 import os
 from pathlib import Path
@@ -112,8 +113,24 @@ def test_matrix_cache_hit_miss_and_corruption(tmp_path, capfd):
     (tmp_path / f"{key}.json").write_text(json.dumps(bad))
     assert cache.lookup(key, c) is None
     err = capfd.readouterr().err
-    assert "stale key" in err and "treating as a miss" in err and "is invalid" in err
-    assert not any(n.endswith(".tmp") for n in os.listdir(tmp_path))
+    assert "written for another key" in err and "unreadable" in err
+    assert "not valid for this cluster" in err
+    assert not any(".partial." in n for n in os.listdir(tmp_path))
+
+
+def test_device_identity_is_an_opt_in_part_of_the_key():
+    """the reference's key (cache.cpp:22-33) has no hardware
+    identity, so a matrix tuned on other GPUs would hit.  Opt-in: an empty
+    identity keeps the reference's digest, any identity changes it."""
+    g = GOLDEN["clusters"]["dozen"]
+    c = es.cluster_from_json(g["spec_compact"])
+    k = g["cache_keys"][0]
+    key = es.OptimizerKey(es.GreedyConfig(k["max_iter"], k["max_neighs"], k["rng_seed"]),
+                          k["default_batch"], k["bench_mode"], k["calib_samples"], k["repeats"])
+    assert es.cache_key(c, key) == k["key"]
+    b200 = es.cache_key(c, dataclasses.replace(key, device="NVIDIA B200/sm_100/148 SMs/178 GiB x8"))
+    h100 = es.cache_key(c, dataclasses.replace(key, device="NVIDIA H100/sm_90/132 SMs/80 GiB x8"))
+    assert len({k["key"], b200, h100}) == 3
 
 
 def test_matrix_shape_errors_are_spec_errors():
