@@ -61,6 +61,8 @@ typedef struct es_model_desc {
                                    conv PxP/P -> c1, conv 3x3 -> c2, dense -> hidden -> classes) */
   int widths[ES_MAX_WIDTHS];
   uint64_t weight_seed;
+  double b200_cost_s;     /* B200 calibration (extension; 0 = none): 1 / throughput(b) = */
+  double b200_overhead_s; /* b200_cost_s + b200_overhead_s / b, member alone on one GPU  */
 } es_model_desc;
 
 /* ClusterSpec (types.hpp:38-52). */
@@ -201,7 +203,9 @@ typedef double (*es_score_fn)(const int* A, int devices, int models, void* user)
 typedef enum es_bench_mode {
   ES_BENCH_ANALYTIC = 0, /* predict_ensemble_throughput */
   ES_BENCH_DEVICE = 1,   /* bench() on the GPUs, CUDA-event timed */
-  ES_BENCH_CALLBACK = 2  /* caller's es_score_fn */
+  ES_BENCH_CALLBACK = 2, /* caller's es_score_fn */
+  ES_BENCH_CALIBRATED = 3 /* calibrated_throughput (per-member B200 fit; opts->device_map,
+                             when given, groups rows sharing a GPU) */
 } es_bench_mode;
 
 typedef struct es_bench_cfg {
@@ -230,6 +234,12 @@ typedef struct es_greedy_trace {
 es_status es_bounded_greedy(const es_cluster_desc* c, const int* A0, int max_iter, int max_neighs,
                             uint64_t seed, const es_bench_cfg* bench, int* A_out,
                             es_greedy_trace* trace);
+/* bounded_greedy with a pre-screen: each iteration's sampled
+ * neighbours are ranked by `screen` (e.g. ES_BENCH_CALIBRATED) and only the top_k
+ * are scored by `bench`; trace->bench_calls counts the bench calls. */
+es_status es_screened_greedy(const es_cluster_desc* c, const int* A0, int max_iter,
+                             int max_neighs, uint64_t seed, int top_k, const es_bench_cfg* bench,
+                             const es_bench_cfg* screen, int* A_out, es_greedy_trace* trace);
 /* bbs_baseline (optimizer.cpp:229-269); chosen[M]. */
 es_status es_bbs_baseline(const es_cluster_desc* c, const es_bench_cfg* bench, int* A_out,
                           int* chosen, int* calls);
@@ -381,15 +391,25 @@ es_status es_cache_store(const char* directory, const char* key, const es_cluste
  * 1/throughput(m, b) = c_m + o/b is fitted by least squares in relative error
  * (cost_out[n_models] = c_m in seconds per sample, *overhead_out = o >= 0,
  * *rms_out = relative RMS misfit). */
+/* member_cost_out / member_overhead_out [n_models] (may be NULL) receive the
+ * per-member fit 1/throughput(m, b) = c'_m + o_m/b and *member_rms_out its misfit. */
 es_status es_fit_cost_model(const int* model, const int* batch, const double* throughput, int n,
-                            int n_models, double* cost_out, double* overhead_out, double* rms_out);
+                            int n_models, double* cost_out, double* overhead_out, double* rms_out,
+                            double* member_cost_out, double* member_overhead_out,
+                            double* member_rms_out);
 /* Benches every model of c alone on CUDA device `device` at every menu batch
  * (device-timed bench over calib_nb synthetic samples, median of repeats)
  * and fits; measured_out[n_models * menu_size] (may be NULL) receives the
  * throughputs, model-major. */
 es_status es_calibrate_cost_model(const es_cluster_desc* c, int device, size_t calib_nb,
                                   int repeats, double* cost_out, double* overhead_out,
-                                  double* rms_out, double* measured_out);
+                                  double* rms_out, double* measured_out, double* member_cost_out,
+                                  double* member_overhead_out, double* member_rms_out);
+/* calibrated_throughput (calibrate.hpp): A scored with the models' b200_cost_s /
+ * b200_overhead_s as the device runs it; row_gpu[n_devices] (may be NULL) maps
+ * rows to GPUs (rows sharing one time-share it). */
+es_status es_calibrated_throughput(const es_cluster_desc* c, const int* A, const int* row_gpu,
+                                   double* out);
 
 /* ------------------------------------------------------------ operator commands */
 /* tools/enserve_cli.cpp main() + src/cli/commands.cpp:

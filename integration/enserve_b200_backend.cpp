@@ -5,6 +5,7 @@
 #include <cstring>
 #include <stdexcept>
 
+#include "enserve/opt/optimizer.hpp"
 #include "enserve/runtime/pipeline.hpp"
 
 namespace enserve {
@@ -101,39 +102,91 @@ ScoreFn make_b200_score(const ClusterSpec& cluster, std::vector<es_model_desc> m
 }  // namespace enserve
 
 // ---------------------------------------------------------------------------
-// Test entry (ctypes): the reference's own run_inference with the b200 backend.
-// The cluster arrives as the es_cluster_desc of include/enserve_b200.h.
+// Test entries (ctypes): the reference's own run_inference and bounded_greedy
+// with the b200 backend / score.  The cluster arrives as the es_cluster_desc
+// of include/enserve_b200.h.
+namespace {
+
+enserve::ClusterSpec cluster_of(const es_cluster_desc* c) {
+  using namespace enserve;
+  ClusterSpec cluster;
+  for (int d = 0; d < c->n_devices; ++d)
+    cluster.devices.push_back({d, c->devices[d].kind == 0 ? DeviceKind::CPU : DeviceKind::GPU,
+                               c->devices[d].memory_mib, c->devices[d].compute_rate,
+                               c->devices[d].batch_overhead_s});
+  for (int m = 0; m < c->n_models; ++m) {
+    const es_model_desc& md = c->models[m];
+    cluster.models.push_back({m, md.name ? md.name : "m", md.weight_mib, md.act_mib_per_sample,
+                              md.cost_per_sample, md.output_width});
+  }
+  cluster.batch_menu.assign(c->batch_menu, c->batch_menu + c->menu_size);
+  cluster.segment_size = c->segment_size;
+  return cluster;
+}
+
+enserve::AllocationMatrix matrix_of(const int* cells, int D, int M) {
+  enserve::AllocationMatrix A(D, M);
+  for (int d = 0; d < D; ++d)
+    for (int m = 0; m < M; ++m) A.set(d, m, cells[d * M + m]);
+  return A;
+}
+
+}  // namespace
+
+// run_inference (pipeline.cpp:418-444) through B200Backend; *elapsed_s (may be
+// NULL) = the reference's own timing window (broadcast -> last fold).
 extern "C" int ref_b200_run(const es_cluster_desc* c, const int* cells, int rule,
                             const float* X, std::size_t nb, std::size_t width, float* Y,
-                            int* winners) {
+                            int* winners, double* elapsed_s) {
   using namespace enserve;
   try {
-    ClusterSpec cluster;
-    for (int d = 0; d < c->n_devices; ++d)
-      cluster.devices.push_back({d, c->devices[d].kind == 0 ? DeviceKind::CPU : DeviceKind::GPU,
-                                 c->devices[d].memory_mib, c->devices[d].compute_rate,
-                                 c->devices[d].batch_overhead_s});
-    for (int m = 0; m < c->n_models; ++m) {
-      const es_model_desc& md = c->models[m];
-      cluster.models.push_back({m, md.name ? md.name : "m", md.weight_mib, md.act_mib_per_sample,
-                                md.cost_per_sample, md.output_width});
-    }
-    cluster.batch_menu.assign(c->batch_menu, c->batch_menu + c->menu_size);
-    cluster.segment_size = c->segment_size;
-    const int D = cluster.device_count(), M = cluster.model_count();
-    AllocationMatrix A(D, M);
-    for (int d = 0; d < D; ++d)
-      for (int m = 0; m < M; ++m) A.set(d, m, cells[d * M + m]);
-    B200Backend backend(std::vector<es_model_desc>(c->models, c->models + M));
+    ClusterSpec cluster = cluster_of(c);
+    const AllocationMatrix A = matrix_of(cells, cluster.device_count(), cluster.model_count());
+    B200Backend backend(std::vector<es_model_desc>(c->models, c->models + c->n_models));
     auto store = std::make_shared<SampleStore>(std::vector<float>(X, X + nb * width), nb, width);
     CombinationRule r = rule == 1 ? CombinationRule::majority_vote() : CombinationRule::averaging();
     InferenceResult out = run_inference(store, A, cluster, backend, r, Mode::Deploy);
     std::memcpy(Y, out.output->combined.data(), out.output->combined.size() * sizeof(float));
     if (winners && !out.output->winners.empty())
       std::memcpy(winners, out.output->winners.data(), out.output->winners.size() * sizeof(int));
+    if (elapsed_s) *elapsed_s = out.output->stats.elapsed_s;
     return 0;
   } catch (const StartupError&) {
     return 3;
+  } catch (const std::exception&) {
+    return 1;
+  }
+}
+
+// The reference's bounded_greedy (optimizer.cpp:178-227) scoring every matrix
+// with make_b200_score (the device-timed bench behind the C ABI) over calib
+// rows X[nb][width]: A_out[D*M], *final_score, *calls (bench calls).
+extern "C" int ref_b200_greedy(const es_cluster_desc* c, const int* A0_cells, int max_iter,
+                               int max_neighs, std::uint64_t seed, const float* X, std::size_t nb,
+                               std::size_t width, int repeats, int* A_out, double* final_score,
+                               int* calls) {
+  using namespace enserve;
+  try {
+    ClusterSpec cluster = cluster_of(c);
+    const int D = cluster.device_count(), M = cluster.model_count();
+    auto calib = std::make_shared<SampleStore>(std::vector<float>(X, X + nb * width), nb, width);
+    ScoreFn inner = make_b200_score(cluster, std::vector<es_model_desc>(c->models, c->models + M),
+                                    calib, repeats);
+    int n = 0;
+    ScoreFn counted = [&](const AllocationMatrix& A) {
+      ++n;
+      return inner(A);
+    };
+    GreedyConfig cfg;
+    cfg.max_iter = max_iter;
+    cfg.max_neighs = max_neighs;
+    cfg.rng_seed = seed;
+    GreedyResult g = bounded_greedy(matrix_of(A0_cells, D, M), cluster, counted, cfg);
+    for (int d = 0; d < D; ++d)
+      for (int m = 0; m < M; ++m) A_out[d * M + m] = g.matrix.at(d, m);
+    *final_score = g.trace.final_score;
+    *calls = n;
+    return 0;
   } catch (const std::exception&) {
     return 1;
   }

@@ -27,7 +27,8 @@ class ModelDesc(C.Structure):
     _fields_ = [("name", C.c_char_p), ("weight_mib", C.c_double),
                 ("act_mib_per_sample", C.c_double), ("cost_per_sample", C.c_double),
                 ("output_width", C.c_int), ("arch", C.c_int), ("n_widths", C.c_int),
-                ("widths", C.c_int * MAX_WIDTHS), ("weight_seed", C.c_uint64)]
+                ("widths", C.c_int * MAX_WIDTHS), ("weight_seed", C.c_uint64),
+                ("b200_cost_s", C.c_double), ("b200_overhead_s", C.c_double)]
 
 
 class ClusterDesc(C.Structure):
@@ -85,9 +86,14 @@ class GreedyTrace(C.Structure):
 # name -> (restype, argtypes)
 _SIGS = {
     "es_fit_cost_model": (C.c_int, [c_int_p, c_int_p, c_double_p, C.c_int, C.c_int, c_double_p,
-                                    c_double_p, c_double_p]),
+                                    c_double_p, c_double_p, c_double_p, c_double_p, c_double_p]),
     "es_calibrate_cost_model": (C.c_int, [C.POINTER(ClusterDesc), C.c_int, C.c_size_t, C.c_int,
-                                          c_double_p, c_double_p, c_double_p, c_double_p]),
+                                          c_double_p, c_double_p, c_double_p, c_double_p,
+                                          c_double_p, c_double_p, c_double_p]),
+    "es_calibrated_throughput": (C.c_int, [C.POINTER(ClusterDesc), c_int_p, c_int_p, c_double_p]),
+    "es_screened_greedy": (C.c_int, [C.POINTER(ClusterDesc), c_int_p, C.c_int, C.c_int, C.c_uint64,
+                                     C.c_int, C.POINTER(BenchCfg), C.POINTER(BenchCfg), c_int_p,
+                                     C.POINTER(GreedyTrace)]),
     "es_cli_main": (C.c_int, [C.c_int, C.POINTER(C.c_char_p)]),
     "es_cluster_to_json": (C.c_int, [C.POINTER(ClusterDesc), C.c_int, C.c_int, C.c_char_p,
                                      C.c_size_t, c_size_t_p]),

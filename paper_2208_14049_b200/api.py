@@ -161,6 +161,9 @@ class ModelSpec:
     cost_per_sample: float = 0.0
     output_width: int = 1
     arch: MemberArch = field(default_factory=MemberArch)
+    # B200 calibration (extension): 1/throughput(b) = b200_cost_s + b200_overhead_s/b
+    b200_cost_s: float = 0.0
+    b200_overhead_s: float = 0.0
 
 
 def mlp_model(id: int, name: str, widths: Sequence[int], seed: int, *,
@@ -244,6 +247,8 @@ class _Desc:
             for j, w in enumerate(m.arch.widths):
                 md.widths[j] = int(w)
             md.weight_seed = int(m.arch.weight_seed)
+            md.b200_cost_s = m.b200_cost_s
+            md.b200_overhead_s = m.b200_overhead_s
         self.menu = (C.c_int * max(len(c.batch_menu), 1))(*c.batch_menu)
         self.desc = _abi.ClusterDesc(self.devs, nd, self.models, nm, self.menu,
                                      len(c.batch_menu), c.segment_size)
@@ -531,10 +536,23 @@ class DeviceBench:
         self.calib, self.repeats, self.pool = calib, repeats, pool
 
 
+class CalibratedBench:
+    """calibrated_throughput as a ScoreFn: the per-member B200 fit
+    (ModelSpec.b200_cost_s / b200_overhead_s); device_map groups rows that
+    share a GPU."""
+
+    def __init__(self, device_map=None):
+        self.device_map = list(device_map) if device_map else None
+
+
 def _bench_cfg(bench, keep: list):
     cfg = _abi.BenchCfg()
     if bench is None or bench == "analytic":
         cfg.mode = 0
+    elif isinstance(bench, CalibratedBench):
+        cfg.mode = 3
+        opts = _pool_opts(keep, device_map=bench.device_map)
+        cfg.opts = C.pointer(opts)
     elif isinstance(bench, DeviceBench):
         cfg.mode = 1
         cfg.calib = bench.calib._h
@@ -573,6 +591,38 @@ def bounded_greedy(A0: AllocationMatrix, cluster: ClusterSpec, bench=None,
     trace = OptimizationTrace(its, tr.start_score, tr.final_score,
                               "local_optimum" if tr.stop_reason == 0 else "iter_cap", tr.bench_calls)
     return GreedyResult(out, trace)
+
+
+def screened_greedy(A0: AllocationMatrix, cluster: ClusterSpec, bench, screen,
+                    config: GreedyConfig = GreedyConfig(), top_k: int = 4) -> GreedyResult:
+    """bounded_greedy whose iterations bench only the `top_k` sampled
+    neighbours `screen` ranks best (search.hpp screened_greedy)."""
+    keep: list = []
+    cfg = _bench_cfg(bench, keep)
+    scfg = _bench_cfg(screen, keep)
+    out = AllocationMatrix(A0.device_count(), A0.model_count())
+    cap = effective_max_iter(cluster.device_count(), cluster.model_count(), config.max_iter) + 1
+    nbr = (C.c_int * cap)()
+    best = (C.c_double * cap)()
+    acc = (C.c_int * cap)()
+    tr = _abi.GreedyTrace(0, 0, 0, 0, 0, cap, nbr, best, acc)
+    with _Desc(cluster) as d:
+        _check(lib().es_screened_greedy(d.ptr, A0.ptr(), config.max_iter, config.max_neighs,
+                                        config.rng_seed, int(top_k), C.byref(cfg), C.byref(scfg),
+                                        out.ptr(), C.byref(tr)))
+    its = [GreedyIteration(i, nbr[i], best[i], bool(acc[i])) for i in range(tr.n_iters)]
+    trace = OptimizationTrace(its, tr.start_score, tr.final_score,
+                              "local_optimum" if tr.stop_reason == 0 else "iter_cap", tr.bench_calls)
+    return GreedyResult(out, trace)
+
+
+def calibrated_throughput(A: AllocationMatrix, cluster: ClusterSpec, row_gpu=None) -> float:
+    """calibrate.hpp calibrated_throughput (per-member B200 fit)."""
+    out = C.c_double()
+    rg = (C.c_int * len(row_gpu))(*row_gpu) if row_gpu else None
+    with _Desc(cluster) as d:
+        _check(lib().es_calibrated_throughput(d.ptr, A.ptr(), rg, C.byref(out)))
+    return out.value
 
 
 @dataclass
@@ -1138,7 +1188,8 @@ def _cluster_from_desc(d: "_abi.ClusterDesc") -> ClusterSpec:
         kind = {1: "mlp", 2: "cnn"}.get(m.arch, "synthetic")
         arch = MemberArch(kind, tuple(m.widths[j] for j in range(m.n_widths)), int(m.weight_seed))
         models.append(ModelSpec(i, m.name.decode(), m.weight_mib, m.act_mib_per_sample,
-                                m.cost_per_sample, m.output_width, arch))
+                                m.cost_per_sample, m.output_width, arch, m.b200_cost_s,
+                                m.b200_overhead_s))
     return ClusterSpec(devs, models, [d.batch_menu[i] for i in range(d.menu_size)], d.segment_size)
 
 
@@ -1263,6 +1314,10 @@ class CostFit:
     batch_overhead_s: float
     rms_rel_error: float
     measured: Optional[list] = None  # [(model, batch, samples/s)] when benched here
+    # per-member form 1/throughput = member_cost_s[m] + member_overhead_s[m] / b
+    member_cost_s: Optional[list] = None
+    member_overhead_s: Optional[list] = None
+    member_rms_rel_error: float = 0.0
 
 
 def fit_cost_model(samples: Sequence[tuple], n_models: int) -> CostFit:
@@ -1273,9 +1328,11 @@ def fit_cost_model(samples: Sequence[tuple], n_models: int) -> CostFit:
     bi = (C.c_int * max(n, 1))(*[int(s[1]) for s in samples])
     th = (C.c_double * max(n, 1))(*[float(s[2]) for s in samples])
     cost = (C.c_double * n_models)()
-    o, rms = C.c_double(), C.c_double()
-    _check(lib().es_fit_cost_model(mi, bi, th, n, n_models, cost, C.byref(o), C.byref(rms)))
-    return CostFit(list(cost), o.value, rms.value)
+    mc, mo = (C.c_double * n_models)(), (C.c_double * n_models)()
+    o, rms, mrms = C.c_double(), C.c_double(), C.c_double()
+    _check(lib().es_fit_cost_model(mi, bi, th, n, n_models, cost, C.byref(o), C.byref(rms),
+                                   mc, mo, C.byref(mrms)))
+    return CostFit(list(cost), o.value, rms.value, None, list(mc), list(mo), mrms.value)
 
 
 def calibrate_cost_model(cluster: ClusterSpec, device: int = 0, calib_nb: int = 65536,
@@ -1284,12 +1341,13 @@ def calibrate_cost_model(cluster: ClusterSpec, device: int = 0, calib_nb: int = 
     M, B = cluster.model_count(), len(cluster.batch_menu)
     cost = (C.c_double * M)()
     meas = (C.c_double * (M * B))()
-    o, rms = C.c_double(), C.c_double()
+    mc, mo = (C.c_double * M)(), (C.c_double * M)()
+    o, rms, mrms = C.c_double(), C.c_double(), C.c_double()
     with _Desc(cluster) as d:
         _check(lib().es_calibrate_cost_model(d.ptr, device, calib_nb, repeats, cost, C.byref(o),
-                                             C.byref(rms), meas))
+                                             C.byref(rms), meas, mc, mo, C.byref(mrms)))
     samples = [(m, cluster.batch_menu[j], meas[m * B + j]) for m in range(M) for j in range(B)]
-    return CostFit(list(cost), o.value, rms.value, samples)
+    return CostFit(list(cost), o.value, rms.value, samples, list(mc), list(mo), mrms.value)
 
 
 def apply_cost_fit(cluster: ClusterSpec, fit: CostFit) -> ClusterSpec:
@@ -1299,6 +1357,8 @@ def apply_cost_fit(cluster: ClusterSpec, fit: CostFit) -> ClusterSpec:
     for d in out.devices:
         if d.kind == GPU:
             d.compute_rate, d.batch_overhead_s = 1.0, fit.batch_overhead_s
-    for m, c in zip(out.models, fit.cost_per_sample):
+    for i, (m, c) in enumerate(zip(out.models, fit.cost_per_sample)):
         m.cost_per_sample = c
+        if fit.member_cost_s:
+            m.b200_cost_s, m.b200_overhead_s = fit.member_cost_s[i], fit.member_overhead_s[i]
     return out

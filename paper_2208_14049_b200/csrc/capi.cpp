@@ -119,6 +119,8 @@ ModelSpec to_model(const es_model_desc& d, int id) {
   m.act_mib_per_sample = d.act_mib_per_sample;
   m.cost_per_sample = d.cost_per_sample;
   m.output_width = d.output_width;
+  m.b200_cost_s = d.b200_cost_s;
+  m.b200_overhead_s = d.b200_overhead_s;
   if (d.arch == 1) {
     need(d.n_widths >= 2 && d.n_widths <= ES_MAX_WIDTHS, "MLP needs 2..9 widths");
     m.arch.kind = MemberArch::Kind::MLP;
@@ -202,6 +204,12 @@ ScoreFn make_score(const ClusterSpec& cluster, const es_bench_cfg* cfg) {
       return cfg->fn(A.cells().data(), A.device_count(), A.model_count(), cfg->user);
     };
   }
+  if (mode == ES_BENCH_CALIBRATED) {
+    const std::vector<int> row_gpu = to_opts(cfg->opts).device_map;
+    return [&cluster, row_gpu](const AllocationMatrix& A) {
+      return calibrated_throughput(A, cluster, row_gpu);
+    };
+  }
   need(cfg->calib != nullptr, "device bench needs a calibration store");
   PoolOptions opts = to_opts(cfg->opts);
   std::shared_ptr<const SampleStore> calib = cfg->calib->store;
@@ -209,6 +217,21 @@ ScoreFn make_score(const ClusterSpec& cluster, const es_bench_cfg* cfg) {
   return [&cluster, calib, repeats, opts](const AllocationMatrix& A) {
     return bench(A, calib, cluster, repeats, opts).throughput;
   };
+}
+
+void export_trace(const GreedyResult& r, int calls, es_greedy_trace* trace) {
+  if (!trace) return;
+  trace->start_score = r.trace.start_score;
+  trace->final_score = r.trace.final_score;
+  trace->stop_reason = r.trace.stop_reason == StopReason::local_optimum ? 0 : 1;
+  trace->n_iters = static_cast<int>(r.trace.iterations.size());
+  trace->bench_calls = calls;
+  for (int i = 0; i < trace->n_iters && i < trace->iter_cap; ++i) {
+    const GreedyIteration& it = r.trace.iterations[i];
+    if (trace->iter_neighbors) trace->iter_neighbors[i] = it.neighbors_evaluated;
+    if (trace->iter_best) trace->iter_best[i] = it.best_score;
+    if (trace->iter_accepted) trace->iter_accepted[i] = it.accepted ? 1 : 0;
+  }
 }
 
 }  // namespace
@@ -455,19 +478,27 @@ es_status es_bounded_greedy(const es_cluster_desc* c, const int* A0, int max_ite
     GreedyResult r = bounded_greedy(to_matrix(A0, c->n_devices, c->n_models), s, counted,
                                     {max_iter, max_neighs, seed});
     write_matrix(r.matrix, A_out);
-    if (trace) {
-      trace->start_score = r.trace.start_score;
-      trace->final_score = r.trace.final_score;
-      trace->stop_reason = r.trace.stop_reason == StopReason::local_optimum ? 0 : 1;
-      trace->n_iters = static_cast<int>(r.trace.iterations.size());
-      trace->bench_calls = calls;
-      for (int i = 0; i < trace->n_iters && i < trace->iter_cap; ++i) {
-        const GreedyIteration& it = r.trace.iterations[i];
-        if (trace->iter_neighbors) trace->iter_neighbors[i] = it.neighbors_evaluated;
-        if (trace->iter_best) trace->iter_best[i] = it.best_score;
-        if (trace->iter_accepted) trace->iter_accepted[i] = it.accepted ? 1 : 0;
-      }
-    }
+    export_trace(r, calls, trace);
+    return ES_OK;
+  });
+}
+
+es_status es_screened_greedy(const es_cluster_desc* c, const int* A0, int max_iter,
+                             int max_neighs, uint64_t seed, int top_k, const es_bench_cfg* bcfg,
+                             const es_bench_cfg* scfg, int* A_out, es_greedy_trace* trace) {
+  return guard([&] {
+    ClusterSpec s = to_cluster(c);
+    int calls = 0;
+    ScoreFn inner = make_score(s, bcfg);
+    ScoreFn counted = [&](const AllocationMatrix& A) {
+      ++calls;
+      return inner(A);
+    };
+    ScoreFn screen = make_score(s, scfg);
+    GreedyResult r = screened_greedy(to_matrix(A0, c->n_devices, c->n_models), s, counted, screen,
+                                     {max_iter, max_neighs, seed}, top_k);
+    write_matrix(r.matrix, A_out);
+    export_trace(r, calls, trace);
     return ES_OK;
   });
 }
@@ -853,6 +884,8 @@ es_spec* make_spec(ClusterSpec c) {
     x.n_widths = static_cast<int>(std::min<std::size_t>(m.arch.widths.size(), ES_MAX_WIDTHS));
     for (int i = 0; i < x.n_widths; ++i) x.widths[i] = m.arch.widths[i];
     x.weight_seed = m.arch.weight_seed;
+    x.b200_cost_s = m.b200_cost_s;
+    x.b200_overhead_s = m.b200_overhead_s;
     s->models.push_back(x);
   }
   return s;
@@ -1040,8 +1073,18 @@ int es_cli_main(int argc, const char* const* argv) {
 
 
 // ------------------------------------------------------------ calibrated cost model
+namespace {
+void export_member_fit(const CostFit& f, int M, double* c, double* o, double* rms) {
+  for (int m = 0; c && m < M; ++m) c[m] = f.member_cost_s[m];
+  for (int m = 0; o && m < M; ++m) o[m] = f.member_overhead_s[m];
+  if (rms) *rms = f.member_rms_rel_error;
+}
+}  // namespace
+
 es_status es_fit_cost_model(const int* model, const int* batch, const double* throughput, int n,
-                            int n_models, double* cost_out, double* overhead_out, double* rms_out) {
+                            int n_models, double* cost_out, double* overhead_out, double* rms_out,
+                            double* member_cost_out, double* member_overhead_out,
+                            double* member_rms_out) {
   return guard([&] {
     need(n >= 0 && n_models > 0 && cost_out != nullptr, "bad arguments");
     std::vector<CostSample> s;
@@ -1050,13 +1093,15 @@ es_status es_fit_cost_model(const int* model, const int* batch, const double* th
     for (int m = 0; m < n_models; ++m) cost_out[m] = f.cost_per_sample[m];
     if (overhead_out) *overhead_out = f.batch_overhead_s;
     if (rms_out) *rms_out = f.rms_rel_error;
+    export_member_fit(f, n_models, member_cost_out, member_overhead_out, member_rms_out);
     return ES_OK;
   });
 }
 
 es_status es_calibrate_cost_model(const es_cluster_desc* c, int device, size_t calib_nb,
                                   int repeats, double* cost_out, double* overhead_out,
-                                  double* rms_out, double* measured_out) {
+                                  double* rms_out, double* measured_out, double* member_cost_out,
+                                  double* member_overhead_out, double* member_rms_out) {
   return guard([&] {
     need(cost_out != nullptr, "cost_out is NULL");
     const ClusterSpec s = to_cluster(c);
@@ -1067,6 +1112,18 @@ es_status es_calibrate_cost_model(const es_cluster_desc* c, int device, size_t c
     if (rms_out) *rms_out = f.rms_rel_error;
     if (measured_out)
       for (std::size_t i = 0; i < meas.size(); ++i) measured_out[i] = meas[i].throughput;
+    export_member_fit(f, s.model_count(), member_cost_out, member_overhead_out, member_rms_out);
+    return ES_OK;
+  });
+}
+
+es_status es_calibrated_throughput(const es_cluster_desc* c, const int* A, const int* row_gpu,
+                                   double* out) {
+  return guard([&] {
+    need(c != nullptr && out != nullptr, "NULL argument");
+    std::vector<int> rg;
+    if (row_gpu) rg.assign(row_gpu, row_gpu + c->n_devices);
+    *out = calibrated_throughput(to_matrix(A, c->n_devices, c->n_models), to_cluster(c), rg);
     return ES_OK;
   });
 }

@@ -28,6 +28,9 @@ struct CommandOptions {  // commands.hpp:12-24
   std::size_t calib_samples = 1024;
   std::size_t input_width = 0;          // 0 = the members' input width (or 16)
   bool key_device = false;  // cache key includes device_identity() (spec_io.hpp OptimizerKey)
+  // optimize: rank each greedy neighbourhood by the calibrated model and bench
+  // only its top `prescreen` (0 = the reference's bounded_greedy)
+  int prescreen = 0;
 };
 
 // Scoring oracle per the bench mode; increments *calls per use (commands.cpp:76-94).

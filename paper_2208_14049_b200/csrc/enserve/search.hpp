@@ -71,6 +71,17 @@ struct GreedyResult {
 GreedyResult bounded_greedy(const AllocationMatrix& A0, const ClusterSpec& cluster,
                             const ScoreFn& bench, const GreedyConfig& config);
 
+// bounded_greedy with a pre-screen: the same start,
+// neighbourhood, seeded subsample and acceptance rule (optimizer.cpp:178-227),
+// but each iteration ranks its sampled neighbours by `screen` (the calibrated
+// analytic model: no device time) and benches only the best `top_k` of them
+// (ties keep neighbourhood order; neighbours the screen scores 0 -- invalid or
+// over memory -- are never benched).  top_k >= max_neighs is bounded_greedy.
+// trace.iterations[i].neighbors_evaluated counts the benched neighbours.
+GreedyResult screened_greedy(const AllocationMatrix& A0, const ClusterSpec& cluster,
+                             const ScoreFn& bench, const ScoreFn& screen,
+                             const GreedyConfig& config, int top_k);
+
 struct BaselineResult {
   AllocationMatrix matrix;
   int bench_calls = 0;

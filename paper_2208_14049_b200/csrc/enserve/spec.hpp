@@ -102,6 +102,13 @@ struct ModelSpec {
   double cost_per_sample = 0.0;
   int output_width = 1;
   MemberArch arch;
+  // B200 calibration (extension, calibrate.hpp; 0 = uncalibrated): seconds
+  // per sample and per batch of this member alone on one GPU at R = 1, i.e.
+  // 1 / throughput(b) = b200_cost_s + b200_overhead_s / b.  The reference's
+  // analytic model has one overhead per device (cost_model.cpp:13-20) and
+  // ignores these.
+  double b200_cost_s = 0.0;
+  double b200_overhead_s = 0.0;
 };
 
 struct ClusterSpec {

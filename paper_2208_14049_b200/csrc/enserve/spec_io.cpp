@@ -102,6 +102,12 @@ js::Value cluster_to_json(const ClusterSpec& cluster, bool with_arch) {
       a["weight_seed"] = m.arch.weight_seed;
       e["arch"] = std::move(a);
     }
+    if (with_arch && m.b200_cost_s > 0.0) {  // calibration extension, never in a cache key
+      js::Value b = js::Value::object();
+      b["per_sample_s"] = m.b200_cost_s;
+      b["per_batch_s"] = m.b200_overhead_s;
+      e["b200_cost"] = std::move(b);
+    }
     models.push_back(std::move(e));
   }
   doc["models"] = std::move(models);
@@ -137,6 +143,10 @@ ClusterSpec cluster_from_json(const js::Value& doc) {
         m.cost_per_sample = req_double(jm, "cost_per_sample", "model");
         m.output_width = req_int(jm, "output_width", "model");
         if (const js::Value* a = jm.find("arch")) m.arch = arch_from_json(*a, "model " + m.name);
+        if (const js::Value* b = jm.find("b200_cost")) {
+          m.b200_cost_s = req_double(*b, "per_sample_s", "b200_cost");
+          m.b200_overhead_s = opt_double(*b, "per_batch_s", 0.0, "b200_cost");
+        }
         cluster.models.push_back(m);
       }
     }
@@ -255,6 +265,7 @@ std::string cache_key(const ClusterSpec& cluster, const OptimizerKey& key) {
   // Opt-in hardware identity: a matrix measured on other GPUs then misses.
   // Empty keeps the digest equal to the reference's for the same inputs.
   if (!key.device.empty()) settings["device"] = key.device;
+  if (key.prescreen > 0) settings["prescreen"] = key.prescreen;
   js::Value doc = js::Value::object();
   doc["optimizer"] = std::move(settings);
   doc["specs"] = cluster_to_json(cluster);

@@ -50,6 +50,7 @@ struct OptimizerKey {
   // hardware is a miss.  Reference tools never set it, so keys they compute
   // still match ours whenever it is empty.
   std::string device;
+  int prescreen = 0;  // screened_greedy's top_k (0 = bounded_greedy, not in the key)
 };
 
 // digest of {"optimizer": settings, "specs": cluster_to_json} (cache.cpp:22-33).
