@@ -113,6 +113,12 @@ typedef struct es_pool_opts {
                               cudaMemcpyPeerAsync after the member kernels */
   int row_nodes;           /* 1 = every device row is its own node (stream, staging,
                               gather, run_host lane) even where rows share a GPU */
+  int dp_claim;            /* device FIFO (the reference's shared per-model queue,
+                              pipeline.cpp:44-51): a data-parallel model's workers pop
+                              chunks of segments off one device counter.  0 = auto (models
+                              whose workers sit on distinct GPUs), 1 = always, -1 = off
+                              (the static split, dp_equal_split) */
+  int64_t claim_chunk;     /* segments per claim (0 = auto) */
 } es_pool_opts;
 
 /* RunStats (pipeline.hpp:19-25). */
@@ -290,6 +296,12 @@ es_status es_system_kernel_timing(es_system* s, int worker, double* ms, char* na
  * 2 = remote through staging + peer copy (routes[workers]); peers[cap] = CUDA
  * ordinals with peer access to/from the combining GPU, *n_peers their count. */
 es_status es_system_routes(es_system* s, int* routes, int* peers, int cap, int* n_peers);
+/* Device FIFO of the last run for model m: owner[segments] = the worker index
+ * (row-major cells) that claimed each segment; *n = segments (0 when the model
+ * has no queue).  owner may be NULL to query n. */
+es_status es_system_claims(es_system* s, int model, int* owner, size_t cap, size_t* n);
+/* Models whose data-parallel workers claim from a device queue: models[cap], *n. */
+es_status es_system_claim_models(es_system* s, int* models, int cap, int* n);
 es_status es_system_shutdown(es_system* s);
 void es_system_destroy(es_system* s);
 

@@ -47,7 +47,8 @@ class PoolOpts(C.Structure):
                 ("overlap_colocated", C.c_int), ("e2e_chunk_rows", C.c_size_t),
                 ("e2e_host_convert", C.c_int), ("e2e_convert_eighths", C.c_int),
                 ("dp_equal_split", C.c_int), ("row_partials", C.c_int),
-                ("no_peer_stores", C.c_int), ("row_nodes", C.c_int)]
+                ("no_peer_stores", C.c_int), ("row_nodes", C.c_int),
+                ("dp_claim", C.c_int), ("claim_chunk", C.c_int64)]
 
 
 class RunStats(C.Structure):
@@ -185,6 +186,8 @@ _SIGS = {
                              C.POINTER(c_float_p), c_float_p, c_int32_p]),
     "es_system_shares": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64), c_double_p]),
     "es_system_routes": (C.c_int, [C.c_void_p, c_int_p, c_int_p, C.c_int, c_int_p]),
+    "es_system_claims": (C.c_int, [C.c_void_p, C.c_int, c_int_p, C.c_size_t, c_size_t_p]),
+    "es_system_claim_models": (C.c_int, [C.c_void_p, c_int_p, C.c_int, c_int_p]),
     "es_comm_unique_id": (C.c_int, [C.POINTER(C.c_uint8), C.c_size_t]),
     "es_comm_create": (C.c_int, [C.POINTER(C.c_uint8), C.c_size_t, C.c_int, C.c_int, C.c_int,
                                  C.POINTER(C.c_void_p)]),

@@ -682,7 +682,7 @@ def _pool_opts(keep: list, device_map=None, copy_outputs=True, warmup=True,
                sms_per_worker=0, overlap_colocated=False, e2e_chunk_rows=0,
                e2e_host_convert=True, e2e_convert_eighths=0,
                dp_equal_split=False, row_partials=False, peer_stores=True,
-               row_nodes=False) -> _abi.PoolOpts:
+               row_nodes=False, dp_claim="auto", claim_chunk=0) -> _abi.PoolOpts:
     """PoolOptions (runtime.hpp)."""
     dm = None
     n = 0
@@ -694,7 +694,8 @@ def _pool_opts(keep: list, device_map=None, copy_outputs=True, warmup=True,
                       int(warmup), int(sms_per_worker), int(overlap_colocated),
                       int(e2e_chunk_rows), int(e2e_host_convert), int(e2e_convert_eighths),
                       int(dp_equal_split), int(row_partials), int(not peer_stores),
-                      int(row_nodes))
+                      int(row_nodes), {"auto": 0, True: 1, False: -1}[dp_claim],
+                      int(claim_chunk))
     keep.append(o)
     return o
 
@@ -833,6 +834,25 @@ class InferenceSystem:
         n = C.c_int()
         _check(lib().es_system_routes(self._h, r, p, 64, C.byref(n)))
         return list(r)[:w], list(p)[:n.value]
+
+    def claim_models(self) -> list:
+        """Models whose data-parallel workers pop a device queue."""
+        out = (C.c_int * 64)()
+        n = C.c_int()
+        _check(lib().es_system_claim_models(self._h, out, 64, C.byref(n)))
+        return list(out)[:n.value]
+
+    def claims(self, model: int) -> Optional[np.ndarray]:
+        """Device FIFO of the last run for `model`: the worker index (row-major
+        cells) that claimed each segment, or None if the model has no queue."""
+        n = C.c_size_t()
+        _check(lib().es_system_claims(self._h, int(model), None, 0, C.byref(n)))
+        if n.value == 0:
+            return None
+        out = np.zeros(n.value, dtype=np.int32)
+        _check(lib().es_system_claims(self._h, int(model), out.ctypes.data_as(_abi.c_int_p),
+                                      n.value, C.byref(n)))
+        return out
 
     def set_gather(self, comm: "Comm" = None, root: int = 0, first_rows=None, rows=None) -> None:
         """One process per GPU: after every run this rank's probabilities +

@@ -191,6 +191,9 @@ PoolOptions to_opts(const es_pool_opts* o) {
   p.row_partials = o->row_partials != 0;
   p.peer_stores = o->no_peer_stores == 0;
   p.row_nodes = o->row_nodes != 0;
+  p.dp_claim = o->dp_claim < 0 ? PoolOptions::kClaimOff
+               : o->dp_claim > 0 ? PoolOptions::kClaimAlways : PoolOptions::kClaimAuto;
+  p.claim_chunk = o->claim_chunk;
   return p;
 }
 
@@ -729,6 +732,28 @@ es_status es_system_routes(es_system* s, int* routes, int* peers, int cap, int* 
     const std::vector<int>& p = s->sys->peer_devices();
     for (int i = 0; peers && i < cap && i < static_cast<int>(p.size()); ++i) peers[i] = p[i];
     if (n_peers) *n_peers = static_cast<int>(p.size());
+    return ES_OK;
+  });
+}
+
+es_status es_system_claims(es_system* s, int model, int* owner, size_t cap, size_t* n) {
+  return guard([&] {
+    need(s != nullptr && n != nullptr, "NULL argument");
+    const auto all = s->sys->last_claims();
+    need(model >= 0 && model < static_cast<int>(all.size()), "model out of range");
+    const std::vector<int>& o = all[model];
+    *n = o.size();
+    if (owner) std::memcpy(owner, o.data(), std::min(cap, o.size()) * sizeof(int));
+    return ES_OK;
+  });
+}
+
+es_status es_system_claim_models(es_system* s, int* models, int cap, int* n) {
+  return guard([&] {
+    need(s != nullptr && n != nullptr, "NULL argument");
+    const std::vector<int> m = s->sys->claim_models();
+    *n = static_cast<int>(m.size());
+    for (int i = 0; models && i < cap && i < *n; ++i) models[i] = m[i];
     return ES_OK;
   });
 }

@@ -192,7 +192,12 @@ __global__ void mlp2_simt_kernel(const __nv_bfloat16* __restrict__ x, int K,
 }
 
 __global__ void synthetic_member_kernel(int model_id, int C, long long row_begin,
-                                        long long row_end, float* __restrict__ out) {
+                                        long long row_end, float* __restrict__ out,
+                                        const ClaimedRun* claim) {
+  if (claim) {
+    row_begin = claim->row_begin;
+    row_end = claim->row_end;
+  }
   const uint64_t km = splitmix64(static_cast<uint64_t>(model_id) + 1);
   const long long n = (row_end - row_begin) * C;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
@@ -212,6 +217,24 @@ __global__ void features_kernel(uint64_t seed, size_t n, __nv_bfloat16* __restri
     const uint64_t h = splitmix64(base + i);
     y[i] = __float2bfloat16_rn(__fdiv_rn(static_cast<float>(h >> 40), 16777216.0f));
   }
+}
+
+__global__ void __launch_bounds__(256) claim_kernel(unsigned long long* counter, long long segments,
+                                                    long long chunk, int seg_size, long long nb,
+                                                    ClaimedRun* out, int* owner, int worker) {
+  __shared__ long long run[2];
+  if (threadIdx.x == 0) {
+    const long long first = static_cast<long long>(atomicAdd(counter, static_cast<unsigned long long>(chunk)));
+    const long long b = first < segments ? first : segments;
+    const long long e = first + chunk < segments ? first + chunk : segments;
+    run[0] = b;
+    run[1] = e;
+    const long long r1 = e * seg_size < nb ? e * seg_size : nb;
+    *out = ClaimedRun{b, e, b * seg_size, b < e ? r1 : b * seg_size};
+  }
+  __syncthreads();
+  if (owner)
+    for (long long s = run[0] + threadIdx.x; s < run[1]; s += blockDim.x) owner[s] = worker;
 }
 
 int grid_for(size_t n, int threads) {
@@ -244,13 +267,20 @@ int generate_dense_layer_f32(uint64_t seed, int layer, int fan_in, int fan_out, 
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
+int claim_launch(unsigned long long* counter, long long segments, long long chunk, int seg_size,
+                 long long nb, ClaimedRun* out, int* owner, int worker, cudaStream_t s) {
+  claim_kernel<<<1, 256, 0, s>>>(counter, segments, chunk, seg_size, nb, out, owner, worker);
+  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+
 int synthetic_member_launch(int model_id, int C, int seg_size, long long seg_begin,
-                            long long seg_end, long long nb, float* out, cudaStream_t s) {
+                            long long seg_end, long long nb, float* out, cudaStream_t s,
+                            const ClaimedRun* claim) {
   const long long r0 = seg_begin * seg_size;
   const long long r1 = seg_end * static_cast<long long>(seg_size) < nb ? seg_end * seg_size : nb;
   if (r1 <= r0) return 0;
   synthetic_member_kernel<<<grid_for(static_cast<size_t>((r1 - r0) * C), 256), 256, 0, s>>>(
-      model_id, C, r0, r1, out);
+      model_id, C, r0, r1, out, claim);
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 

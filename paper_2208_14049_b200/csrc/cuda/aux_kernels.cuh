@@ -6,6 +6,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include "batching.cuh"
+
 namespace es {
 
 // y[i] = bf16_rn(x[i]).
@@ -44,8 +46,20 @@ int combine_launch(const CombineArgs& a, cudaStream_t s);
 
 // Synthetic member: out[r][c] = synthetic_prediction(model_id, r, c) for rows
 // of the segments [seg_begin, seg_end) (reference src/runtime/backend.cpp:21-29).
+// claim (may be null): rows of a data-parallel worker's claimed run instead.
 int synthetic_member_launch(int model_id, int C, int seg_size, long long seg_begin,
-                            long long seg_end, long long nb, float* out, cudaStream_t s);
+                            long long seg_end, long long nb, float* out, cudaStream_t s,
+                            const ClaimedRun* claim = nullptr);
+
+// Device FIFO of a data-parallel model (the reference's
+// shared per-model segment queue, pipeline.cpp:44-51, :103-104): pop the next
+// `chunk` segments of [0, segments) off *counter (atomicAdd; the counter may
+// live on a peer GPU), store the run and its rows [.., min(end * seg_size, nb))
+// in *out for the worker's member launches, and stamp owner[s] = worker for
+// every popped segment (exactly-once evidence; may be null).  An exhausted
+// queue stores an empty run.
+int claim_launch(unsigned long long* counter, long long segments, long long chunk, int seg_size,
+                 long long nb, ClaimedRun* out, int* owner, int worker, cudaStream_t s);
 
 // Synthetic features straight into the bf16 device replica:
 // x[i] = bf16_rn(U24(splitmix64(seed * 0x2545f4914f6cdd1d + i))).

@@ -9,14 +9,26 @@
 namespace es {
 
 struct BatchTiles {
-  long long per_seg = 1;  // tiles of a full segment
-  long long total = 0;    // tiles of segments [seg_begin, seg_end)
+  long long per_seg = 1;    // tiles of a full segment
+  long long total = 0;      // tiles of segments [seg_begin, seg_end)
+  long long seg_begin = 0;  // first segment of the launch
+};
+
+// A data-parallel worker's claimed run (SURVEY.md §8-E device FIFO): the
+// claim kernel (aux_kernels.cu) pops [seg_begin, seg_end) off its model's
+// shared counter and stores it here, with the matching rows; every launch of
+// the worker's member chain reads it at kernel start (stream order makes the
+// claim visible), so all of a member's launches -- and every warp role inside
+// them -- walk the same segments.
+struct ClaimedRun {
+  long long seg_begin, seg_end, row_begin, row_end;
 };
 
 __host__ __device__ __forceinline__ BatchTiles batch_tiles(long long seg_begin, long long seg_end,
                                                           int seg_size, long long nb, int b) {
   BatchTiles t;
   t.per_seg = (seg_size + b - 1) / b;
+  t.seg_begin = seg_begin;
   const long long nseg = seg_end - seg_begin;
   if (nseg <= 0) return t;
   const long long last = seg_end - 1;

@@ -83,7 +83,10 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
 
   const int warp = warp_uniform_id();
   const int lane = threadIdx.x & 31;
-  const long long tiles = (args.row_end - args.row_begin + L.T - 1) / L.T;
+  // Rows of this launch: its static range, or the data-parallel claim.
+  const long long row_begin = args.claim ? args.claim->row_begin : args.row_begin;
+  const long long row_end = args.claim ? args.claim->row_end : args.row_end;
+  const long long tiles = (row_end - row_begin + L.T - 1) / L.T;
   const int my_tiles =
       blockIdx.x < tiles ? static_cast<int>((tiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
   const int kp = L.c1 / 8;  // 16-byte planes of conv2's K per tap
@@ -162,7 +165,7 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
     const int rows16 = L.S * L.S / 16;  // the map views x as [rows * S*S/16][16]
     auto load = [&](int k) {
       const int st = k % L.raw_stages;
-      const long long s0 = args.row_begin + (blockIdx.x + static_cast<long long>(k) * gridDim.x) * L.T;
+      const long long s0 = row_begin + (blockIdx.x + static_cast<long long>(k) * gridDim.x) * L.T;
       mbar_arrive_expect_tx(&raw_full[st], static_cast<uint32_t>(L.T * L.S * L.S * 2));
       tma_load_2d(sRaw + st * L.raw_stride, &tm_x, &raw_full[st], 0,
                   static_cast<int32_t>(s0 * rows16), pol);
@@ -441,7 +444,7 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
     // itself a border pixel and is not stored.  Warps 10-13, every channel,
     // 16 at a time.
     auto epi2_split = [&](int k) {
-      const long long s0 = args.row_begin + (blockIdx.x + static_cast<long long>(k) * gridDim.x) * L.T;
+      const long long s0 = row_begin + (blockIdx.x + static_cast<long long>(k) * gridDim.x) * L.T;
       constexpr int shifts = SPLIT - 1;
       const float keep_p1 = lane == 30 ? 0.0f : 1.0f;
       const float keep_31 = lane == 31 ? 0.0f : 1.0f;  // kShiftHybrid: u[31] takes no dw=+1 term
@@ -454,7 +457,7 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
         const int r = mb * 128 + q * 32 + lane;  // grid row of the tile
         const int oo = sOut[r];
         const int n = oo >> 24;
-        const bool valid = oo >= 0 && s0 + n < args.row_end;
+        const bool valid = oo >= 0 && s0 + n < row_end;
         uint8_t* dst = static_cast<uint8_t*>(args.out) + (s0 + n) * row_bytes + (oo & 0xFFFFFF);
         const uint32_t col = tmem_base + lane_field + static_cast<uint32_t>(L.tmem_c1 + sl * L.n2);
         for (int c0 = 0; c0 < L.c2; c0 += 16) {
@@ -515,12 +518,12 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
       mbar_sleep_wait(&c2_full[b], u);
       if (warp == 6 && lane == 0) TRACE(k, 8);
       tc_fence_after();
-      const long long s0 = args.row_begin + (blockIdx.x + static_cast<long long>(k) * gridDim.x) * L.T;
+      const long long s0 = row_begin + (blockIdx.x + static_cast<long long>(k) * gridDim.x) * L.T;
       for (int mb = 0; mb < L.mb2; ++mb) {
         const int r = mb * 128 + q * 32 + lane;  // grid row of the tile
         const int oo = sOut[r];
         const int n = oo >> 24;
-        const bool valid = oo >= 0 && s0 + n < args.row_end;
+        const bool valid = oo >= 0 && s0 + n < row_end;
         uint8_t* dst = static_cast<uint8_t*>(args.out) + (s0 + n) * row_bytes + (oo & 0xFFFFFF);
         for (int c0 = 0; c0 < L.c2; c0 += 32) {
           uint32_t v[32];

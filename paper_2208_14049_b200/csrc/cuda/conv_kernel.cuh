@@ -48,6 +48,8 @@
 
 #include <cstdint>
 
+#include "batching.cuh"
+
 namespace es {
 
 struct ConvLayout {
@@ -71,6 +73,7 @@ struct ConvLayout {
 struct ConvArgs {
   ConvLayout L;
   long long row_begin = 0, row_end = 0;  // samples handled by this launch
+  const ClaimedRun* claim = nullptr;      // set: the rows stored there instead
   const void* w1 = nullptr;              // bf16 [c1][P*P]
   const float* b1 = nullptr;
   const void* w2 = nullptr;  // bf16 [c2][9*c1], K index = tap*c1 + channel, tap = 3*(dh+1)+(dw+1)

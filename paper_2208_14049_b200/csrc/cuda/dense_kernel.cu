@@ -21,8 +21,16 @@ constexpr int kMaxT = 4;
 // The CTA's i-th work unit: T consecutive 128-row tiles x one column block.
 // Consecutive units of a row group walk its column blocks, so the X tiles are
 // re-read from L2 while hot.  Returns the number of tiles (0 = no more work).
+__device__ __forceinline__ long long rows_begin(const DenseArgs& a) {
+  return a.claim ? a.claim->row_begin : a.row_begin;
+}
+__device__ __forceinline__ long long rows_end(const DenseArgs& a) {
+  return a.claim ? a.claim->row_end : a.row_end;
+}
+
 __device__ __forceinline__ int unit_rows(const DenseArgs& a, int i, int* cb, long long (&row0)[kMaxT]) {
-  const long long tiles = (a.row_end - a.row_begin + 127) / 128;
+  const long long rb = rows_begin(a);
+  const long long tiles = (rows_end(a) - rb + 127) / 128;
   const long long groups = (tiles + a.L.T - 1) / a.L.T;
   const long long u = blockIdx.x + static_cast<long long>(i) * gridDim.x;
   if (u >= groups * a.L.ncb) return 0;
@@ -32,7 +40,7 @@ __device__ __forceinline__ int unit_rows(const DenseArgs& a, int i, int* cb, lon
   for (int k = 0; k < a.L.T; ++k) {
     const long long t = g * a.L.T + k;
     if (t >= tiles) break;
-    row0[k] = a.row_begin + t * 128;
+    row0[k] = rb + t * 128;
     ++n;
   }
   return n;
@@ -184,7 +192,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tmem_ld16(tmem_base + lane_field + static_cast<uint32_t>(buf * L.group_cols + k * 16), v);
             tmem_ld_wait();
             const long long r = row0[k] + row;
-            if (r < args.row_end) {
+            if (r < rows_end(args)) {
               float* o = static_cast<float*>(args.logits) + r * L.C;
               for (int c = 0; c < L.C; ++c) o[c] = v[c] + sBias[c];
             }

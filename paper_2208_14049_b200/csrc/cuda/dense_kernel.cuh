@@ -16,6 +16,7 @@
 
 #include <cstdint>
 
+#include "batching.cuh"
 #include "sm100.cuh"
 
 namespace es {
@@ -34,6 +35,7 @@ struct DenseLayout {
 struct DenseArgs {
   DenseLayout L;
   long long row_begin = 0, row_end = 0;  // rows of X / Y handled by this launch
+  const ClaimedRun* claim = nullptr;      // set: the rows stored there instead
   const float* bias = nullptr;
   float* logits = nullptr;  // logits mode: fp32 [rows][C]
 };

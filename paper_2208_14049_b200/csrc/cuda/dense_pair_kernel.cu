@@ -40,7 +40,8 @@ constexpr uint16_t kBoth = 0b11;
 // (it still loads valid rows so the leader's byte count holds).
 __device__ __forceinline__ int pair_unit(const DenseArgs& a, int i, uint32_t rank, int* cb,
                                          long long (&row0)[kMaxT], bool (&present)[kMaxT]) {
-  const long long tiles = (a.row_end - a.row_begin + 127) / 128;
+  const long long rb = a.claim ? a.claim->row_begin : a.row_begin;
+  const long long tiles = ((a.claim ? a.claim->row_end : a.row_end) - rb + 127) / 128;
   const long long ptiles = (tiles + 1) / 2;
   const long long groups = (ptiles + a.L.T - 1) / a.L.T;
   const long long pair = blockIdx.x >> 1, pairs = gridDim.x >> 1;
@@ -54,7 +55,7 @@ __device__ __forceinline__ int pair_unit(const DenseArgs& a, int i, uint32_t ran
     if (tp >= ptiles) break;
     const long long t = 2 * tp + rank;
     present[k] = t < tiles;
-    row0[k] = a.row_begin + (present[k] ? t : 2 * tp) * 128;
+    row0[k] = rb + (present[k] ? t : 2 * tp) * 128;
     ++n;
   }
   return n;

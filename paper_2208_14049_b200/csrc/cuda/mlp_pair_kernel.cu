@@ -25,6 +25,7 @@ constexpr uint16_t kBoth = 0b11;
 using Tiles = BatchTiles;
 
 __device__ __forceinline__ Tiles tile_space(const MlpPArgs& a) {
+  if (a.claim) return batch_tiles(a.claim->seg_begin, a.claim->seg_end, a.seg_size, a.nb, a.b);
   return batch_tiles(a.seg_begin, a.seg_end, a.seg_size, a.nb, a.b);
 }
 
@@ -41,7 +42,7 @@ __device__ __forceinline__ int group_tiles(const MlpPArgs& a, const Tiles& ts, i
     if (2 * tp >= ts.total) break;
     const long long t = 2 * tp + rank;
     if (t < ts.total) {
-      row0[k] = batch_tile(ts, t, a.seg_begin, a.seg_size, a.nb, a.b, &rows[k]);
+      row0[k] = batch_tile(ts, t, ts.seg_begin, a.seg_size, a.nb, a.b, &rows[k]);
     } else {
       row0[k] = 0;  // load something valid; nothing is written back
       rows[k] = 0;

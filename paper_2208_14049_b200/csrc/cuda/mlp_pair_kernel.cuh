@@ -21,6 +21,7 @@
 
 #include <cstdint>
 
+#include "batching.cuh"
 #include "sm100.cuh"
 
 namespace es {
@@ -52,6 +53,9 @@ struct MlpPArgs {
   const float* bias1 = nullptr;
   const float* bias2 = nullptr;
   float* out = nullptr;
+  // Dynamic claim (batching.cuh ClaimedRun): when set, the launch walks the
+  // segments stored there instead of [seg_begin, seg_end).
+  const ClaimedRun* claim = nullptr;
   // Optional timeline of CTA 0 (globaltimer ns): [group][8] for groups < 32,
   // see the TRACE() points in the kernel.  nullptr = off.
   unsigned long long* trace = nullptr;

@@ -25,6 +25,7 @@ constexpr int kMaxT = 4;
 using Tiles = BatchTiles;
 
 __device__ __forceinline__ Tiles tile_space(const MlpTArgs& a) {
+  if (a.claim) return batch_tiles(a.claim->seg_begin, a.claim->seg_end, a.seg_size, a.nb, a.b);
   return batch_tiles(a.seg_begin, a.seg_end, a.seg_size, a.nb, a.b);
 }
 
@@ -35,7 +36,7 @@ __device__ __forceinline__ int group_tiles(const MlpTArgs& a, const Tiles& ts, i
   for (int k = 0; k < a.L.T; ++k) {
     const long long t = blockIdx.x + static_cast<long long>(g * a.L.T + k) * gridDim.x;
     if (t >= ts.total) break;
-    row0[k] = batch_tile(ts, t, a.seg_begin, a.seg_size, a.nb, a.b, &rows[k]);
+    row0[k] = batch_tile(ts, t, ts.seg_begin, a.seg_size, a.nb, a.b, &rows[k]);
     ++n;
   }
   return n;

@@ -25,6 +25,7 @@
 
 #include <cstdint>
 
+#include "batching.cuh"
 #include "sm100.cuh"
 
 namespace es {
@@ -55,6 +56,9 @@ struct MlpTArgs {
   const float* bias1 = nullptr;
   const float* bias2 = nullptr;
   float* out = nullptr;
+  // Dynamic claim (batching.cuh ClaimedRun): when set, the launch walks the
+  // segments stored there instead of [seg_begin, seg_end).
+  const ClaimedRun* claim = nullptr;
 };
 
 bool mlpt_plan(int K, int H, int C, int b, MlpTLayout* out);

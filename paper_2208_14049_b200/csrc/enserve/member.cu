@@ -225,15 +225,23 @@ std::vector<std::string> DeviceMember::kernel_names() const {
   return n;
 }
 
+bool DeviceMember::supports_claim() const {
+  if (!impl_) return false;
+  if (env_is("ES_MEMBER_KERNEL", "simt")) return false;
+  return impl_->head != Impl::Head::SwapAB;
+}
+
 int DeviceMember::forward(const void* x, long long nb, int seg_size, long long s0, long long s1,
-                          float* out, int grid, cudaStream_t stream, const cudaEvent_t* marks) {
+                          float* out, int grid, cudaStream_t stream, const cudaEvent_t* marks,
+                          const es::ClaimedRun* claim) {
   Impl& I = *impl_;
   if (s1 <= s0 || nb == 0) return 0;
+  if (claim && !supports_claim()) throw Error(I.model.name + ": schedule cannot follow a claim");
   auto mark = [&](int i) {
     if (marks) M_CUDA(cudaEventRecord(marks[i], stream));
   };
   if (I.head == Impl::Head::Synthetic) {
-    M_LAUNCH(es::synthetic_member_launch(I.model.id, I.C, seg_size, s0, s1, nb, out, stream));
+    M_LAUNCH(es::synthetic_member_launch(I.model.id, I.C, seg_size, s0, s1, nb, out, stream, claim));
     mark(0);
     return 1;
   }
@@ -255,6 +263,7 @@ int DeviceMember::forward(const void* x, long long nb, int seg_size, long long s
     c.L = I.conv;
     c.row_begin = r0;
     c.row_end = r1;
+    c.claim = claim;
     c.w1 = base + I.w_off[0];
     c.b1 = reinterpret_cast<const float*>(base + I.b_off[0]);
     c.w2 = base + I.w_off[1];
@@ -272,6 +281,7 @@ int DeviceMember::forward(const void* x, long long nb, int seg_size, long long s
     d.L = I.dense[i];
     d.row_begin = r0;
     d.row_end = r1;
+    d.claim = claim;
     d.bias = reinterpret_cast<const float*>(base + I.b_off[l]);
     M_LAUNCH(d.L.pair ? es::dense_pair_launch(d, cur, nb, base + I.w_off[l], y, grid, stream)
                       : es::dense_launch(d, cur, nb, base + I.w_off[l], y, grid, stream));
@@ -283,6 +293,7 @@ int DeviceMember::forward(const void* x, long long nb, int seg_size, long long s
     d.L = I.logits;
     d.row_begin = r0;
     d.row_end = r1;
+    d.claim = claim;
     d.bias = reinterpret_cast<const float*>(base + I.b_off[L - 1]);
     d.logits = out;
     M_LAUNCH(es::dense_launch(d, cur, nb, base + I.w_off[L - 1], nullptr, grid, stream));
@@ -314,6 +325,7 @@ int DeviceMember::forward(const void* x, long long nb, int seg_size, long long s
       p.bias1 = b1;
       p.bias2 = b2;
       p.out = out;
+      p.claim = claim;
       M_LAUNCH(es::mlpp_launch(p, cur, w1, w2, grid, stream));
       break;
     }
@@ -328,6 +340,7 @@ int DeviceMember::forward(const void* x, long long nb, int seg_size, long long s
       t.bias1 = b1;
       t.bias2 = b2;
       t.out = out;
+      t.claim = claim;
       M_LAUNCH(es::mlpt_launch(t, cur, w1, w2, grid, stream));
       break;
     }

@@ -12,6 +12,8 @@
 
 #include <cuda_runtime.h>
 
+#include "../cuda/batching.cuh"
+
 #include <cstddef>
 #include <string>
 #include <vector>
@@ -36,8 +38,16 @@ class DeviceMember {
   // `marks` (optional, >= max_launches() events): marks[i] is recorded on
   // `stream` right after launch i, so launch i's device time is the interval
   // from the previous mark (or the caller's start event) to marks[i].
+  // `claim` (optional, device memory): a data-parallel worker's claimed run
+  // (cuda/batching.cuh ClaimedRun, written by es::claim_launch earlier on
+  // `stream`); every launch then walks the rows stored there, and [s0, s1)
+  // only bounds the grid.
   int forward(const void* x, long long nb, int seg_size, long long s0, long long s1, float* out,
-              int grid, cudaStream_t stream, const cudaEvent_t* marks = nullptr);
+              int grid, cudaStream_t stream, const cudaEvent_t* marks = nullptr,
+              const es::ClaimedRun* claim = nullptr);
+  // Whether every launch of this member honours a claim (the swap-AB and
+  // SIMT schedules do not; their workers keep the static split).
+  bool supports_claim() const;
 
   // Kernel names forward() launches, in order (one per launch).
   std::vector<std::string> kernel_names() const;

@@ -209,6 +209,8 @@ struct InferenceSystem::Worker {
   float* staging = nullptr;              // remote worker: local logits [nb][C]
   std::size_t staging_rows = 0;
   bool remote = false;  // on another node than the combining one
+  bool peer = false;    // may access the combining GPU's memory (same GPU or peer access)
+  es::ClaimedRun* claim = nullptr;  // device FIFO: this worker's claimed run (on its GPU)
   bool direct = false;  // remote, storing its logits straight into the combining GPU's buffers
   // Logits go to the worker's own staging buffer: a remote worker without
   // direct peer stores, or any remote worker in row_partials mode (its row's
@@ -234,6 +236,15 @@ struct InferenceSystem::Impl {
   };
   std::vector<RowPartial> partials;
   bool partial_mode = false;
+  // Device FIFO per data-parallel model (PoolOptions::dp_claim).
+  struct Queue {
+    bool on = false;
+    unsigned long long* counter = nullptr;  // on the combining GPU
+    int* owner = nullptr;                   // [segments] claiming worker (evidence)
+    std::size_t owner_cap = 0;
+    long long segments = 0, chunk = 1, rounds = 0;
+  };
+  std::vector<Queue> queues;
   // run_host pipeline (slots of whole-segment chunks).  A slot's host side
   // and combining-node buffers:
   struct Slot {
@@ -410,6 +421,39 @@ InferenceSystem::InferenceSystem(const AllocationMatrix& A, const ClusterSpec& c
       peer = std::find(peers_.begin(), peers_.end(), w->phys) != peers_.end();
     }
     w->direct = peer && options_.peer_stores;
+    w->peer = peer;
+  }
+  for (auto& w : workers_)
+    if (!w->remote) w->peer = true;
+  // Device FIFO: models with several workers that can all follow a claim and
+  // store straight into the combining GPU's logits.
+  impl_->queues.assign(cluster.model_count(), Impl::Queue{});
+  if (options_.dp_claim != PoolOptions::kClaimOff) {
+    const std::vector<int> per_model = workers_per_model();
+    for (int m = 0; m < cluster.model_count(); ++m) {
+      if (per_model[m] < 2) continue;
+      bool ok = true;
+      std::vector<int> gpus;
+      for (const auto& w : workers_)
+        if (w->model == m) {
+          ok = ok && w->member->supports_claim() && w->peer && (!w->remote || w->direct);
+          ok = ok && (options_.dp_claim == PoolOptions::kClaimAlways ||
+                      std::find(gpus.begin(), gpus.end(), w->phys) == gpus.end());
+          gpus.push_back(w->phys);
+        }
+      if (!ok) continue;
+      Impl::Queue& q = impl_->queues[m];
+      {
+        OnDevice oc(combine_dev_);
+        ES_CUDA(cudaMalloc(&q.counter, sizeof(unsigned long long)));
+      }
+      for (auto& w : workers_)
+        if (w->model == m) {
+          OnDevice ow(w->phys);
+          ES_CUDA(cudaMalloc(&w->claim, sizeof(es::ClaimedRun)));
+        }
+      q.on = true;
+    }
   }
   OnDevice on(combine_dev_);
   ES_CUDA(cudaStreamCreateWithFlags(&impl_->main, cudaStreamNonBlocking));
@@ -436,6 +480,7 @@ void InferenceSystem::shutdown() {
   for (auto& w : workers_) {
     cudaSetDevice(w->phys);
     if (w->staging) cudaFree(w->staging);
+    if (w->claim) cudaFree(w->claim);
     if (w->stream && w->owns_stream) cudaStreamDestroy(w->stream);
     if (w->ev_begin) cudaEventDestroy(w->ev_begin);
     if (w->ev_done) cudaEventDestroy(w->ev_done);
@@ -450,6 +495,11 @@ void InferenceSystem::shutdown() {
     cudaFree(impl_->labels);
     cudaFree(impl_->gy);
     cudaFree(impl_->glabels);
+    for (Impl::Queue& q : impl_->queues) {
+      cudaFree(q.counter);
+      cudaFree(q.owner);
+    }
+    impl_->queues.clear();
     impl_->comm.reset();
     impl_->free_e2e();
     for (Impl::RowPartial& p : impl_->partials) {
@@ -525,6 +575,26 @@ bool InferenceSystem::single_device() const {
   return true;
 }
 
+std::vector<std::vector<int>> InferenceSystem::last_claims() const {
+  std::vector<std::vector<int>> out(impl_->queues.size());
+  OnDevice on(combine_dev_);
+  ES_CUDA(cudaStreamSynchronize(impl_->main));
+  for (std::size_t m = 0; m < impl_->queues.size(); ++m) {
+    const Impl::Queue& q = impl_->queues[m];
+    if (!q.on || q.segments == 0) continue;
+    out[m].resize(static_cast<std::size_t>(q.segments));
+    ES_CUDA(cudaMemcpy(out[m].data(), q.owner, out[m].size() * sizeof(int), cudaMemcpyDeviceToHost));
+  }
+  return out;
+}
+
+std::vector<int> InferenceSystem::claim_models() const {
+  std::vector<int> out;
+  for (std::size_t m = 0; m < impl_->queues.size(); ++m)
+    if (impl_->queues[m].on) out.push_back(static_cast<int>(m));
+  return out;
+}
+
 std::vector<int> InferenceSystem::worker_routes() const {
   std::vector<int> r;
   for (const auto& w : workers_) r.push_back(!w->remote ? 0 : w->direct ? 1 : 2);
@@ -582,6 +652,33 @@ void InferenceSystem::begin_run(std::shared_ptr<const SampleStore> X, Combinatio
   }
   if (!options_.dp_equal_split && rates_.empty() && nb > 0) probe_rates(*X);
   assign_shares(nb);
+  // Device FIFO sizing: chunks of about S / (4 W) segments, at least two
+  // waves of 128-row tiles on the smallest worker GPU, so every claimed round
+  // still fills the machine; enough rounds per worker to drain the queue alone.
+  {
+    const std::vector<int> per_model = workers_per_model();
+    for (int m = 0; m < cluster_.model_count(); ++m) {
+      Impl::Queue& q = impl_->queues[m];
+      if (!q.on) continue;
+      q.segments = static_cast<long long>(S);
+      int sms = 1 << 30;
+      for (const auto& w : workers_)
+        if (w->model == m) sms = std::min(sms, es::num_sms(w->phys));
+      long long chunk = options_.claim_chunk;
+      if (chunk <= 0)
+        chunk = std::max<long long>(2LL * sms, (q.segments + 4LL * per_model[m] - 1) /
+                                                   (4LL * per_model[m]));
+      q.chunk = std::max<long long>(1, chunk);
+      q.rounds = q.segments > 0 ? (q.segments + q.chunk - 1) / q.chunk : 0;
+      if (static_cast<std::size_t>(q.segments) > q.owner_cap) {
+        OnDevice oc(combine_dev_);
+        cudaFree(q.owner);
+        q.owner = nullptr;
+        ES_CUDA(cudaMalloc(&q.owner, std::max<std::size_t>(S, 1) * sizeof(int)));
+        q.owner_cap = S;
+      }
+    }
+  }
   // Fast gather: one partial per device row (pure model placement only).
   impl_->partial_mode = false;
   if (options_.row_partials) {
@@ -651,6 +748,13 @@ std::size_t InferenceSystem::broadcast() {
   launches_ = 0;
   {
     OnDevice on(combine_dev_);
+    // Fresh queues: every segment of a data-parallel model once more.
+    for (const Impl::Queue& q : impl_->queues)
+      if (q.on && q.segments > 0) {
+        ES_CUDA(cudaMemsetAsync(q.counter, 0, sizeof(unsigned long long), impl_->main));
+        ES_CUDA(cudaMemsetAsync(q.owner, 0xff, static_cast<std::size_t>(q.segments) * sizeof(int),
+                                impl_->main));
+      }
     ES_CUDA(cudaEventRecord(impl_->start, impl_->main));
   }
   for (auto& w : workers_) {
@@ -664,10 +768,25 @@ std::size_t InferenceSystem::broadcast() {
     Nvtx range("worker row " + std::to_string(w->row) + " model " + std::to_string(w->model) +
                " b=" + std::to_string(w->batch) + " segments [" + std::to_string(w->seg_begin) +
                "," + std::to_string(w->seg_end) + ")");
-    launches_ += w->member->forward(X.device_replica(w->phys), nb, cluster_.segment_size,
-                                    w->seg_begin, w->seg_end, out, grid, w->stream,
-                                    w->marks.empty() ? nullptr : w->marks.data());
-    if (staged && w->seg_end > w->seg_begin && !impl_->partial_mode) {
+    const Impl::Queue& q = impl_->queues[w->model];
+    if (q.on) {
+      // Device FIFO: pop a chunk, run the member chain over it, repeat; a
+      // round after the queue ran dry claims an empty run and its launches
+      // exit at once.  The worker's launch marks all land after its rounds.
+      const int index = static_cast<int>(&w - workers_.data());
+      for (long long r = 0; r < q.rounds; ++r) {
+        ES_LAUNCH(es::claim_launch(q.counter, q.segments, q.chunk, cluster_.segment_size, nb,
+                                   w->claim, q.owner, index, w->stream));
+        launches_ += 1 + w->member->forward(X.device_replica(w->phys), nb, cluster_.segment_size,
+                                            0, q.segments, out, grid, w->stream, nullptr, w->claim);
+      }
+      for (cudaEvent_t e : w->marks) ES_CUDA(cudaEventRecord(e, w->stream));
+    } else {
+      launches_ += w->member->forward(X.device_replica(w->phys), nb, cluster_.segment_size,
+                                      w->seg_begin, w->seg_end, out, grid, w->stream,
+                                      w->marks.empty() ? nullptr : w->marks.data());
+    }
+    if (!q.on && staged && w->seg_end > w->seg_begin && !impl_->partial_mode) {
       const long long r0 = w->seg_begin * cluster_.segment_size;
       const long long r1 = std::min<long long>(w->seg_end * cluster_.segment_size, nb);
       ES_CUDA(cudaMemcpyPeerAsync(impl_->logits[w->model] + r0 * C, combine_dev_,

@@ -133,6 +133,24 @@ struct PoolOptions {
   // reference's shared FIFO, where faster workers pull more segments), or
   // equal runs.
   bool dp_equal_split = false;
+  // The device FIFO (the reference's shared per-model queue,
+  // pipeline.cpp:44-51, :103-104): a data-parallel model's workers pop chunks
+  // of `claim_chunk` segments (0 = auto: about four per worker, at least two
+  // waves of tiles) off one device counter on the combining GPU -- remote
+  // workers through their NVLink peer mapping -- so a faster worker takes more
+  // of the model's segments.  Applies when every worker of the model can
+  // follow a claim and reach the combining GPU directly; otherwise (or off)
+  // the static split above.  run_host keeps the static split.
+  //   kClaimAuto: only where the model's workers sit on distinct GPUs -- they
+  //     run side by side, so the faster GPU pulls more.  Workers sharing a GPU
+  //     time-share its SMs; whoever claims, the GPU does the same work, and a
+  //     worker with a small batch (slow per segment) claiming much costs more
+  //     than the probed split, which gives it little (measured, tools/
+  //     claim_probe.py: 10.9 vs 4.6 ms on one B200).
+  //   kClaimAlways: every eligible model (tests; SM-partitioned workers).
+  enum ClaimMode { kClaimOff = 0, kClaimAuto = 1, kClaimAlways = 2 };
+  int dp_claim = kClaimAuto;
+  long long claim_chunk = 0;
   // Gather: false = parity mode, every member's logits go
   // to the combining GPU and one fold runs in model order (bit-identical to
   // the reference); true = fast mode, each device row folds its own members
@@ -228,6 +246,12 @@ class InferenceSystem {
   // Segment runs [begin, end) of every worker in the last run, and the rows/s
   // each data-parallel worker measured when probed (1.0 for single workers).
   std::vector<std::pair<long long, long long>> last_shares() const;
+  // Device FIFO of the last run: per model, the worker index (into the
+  // row-major worker list) that claimed each segment; empty for models
+  // without a queue.  Synchronises with the device.
+  std::vector<std::vector<int>> last_claims() const;
+  // Models whose data-parallel workers claim from a device queue.
+  std::vector<int> claim_models() const;
   const std::vector<double>& worker_rates() const { return rates_; }
 
  private:
