@@ -310,7 +310,7 @@ def launch_work(arch, names: list) -> list:
     return out
 
 
-def roofline_for(es, cluster, A, kernels: list, nb: int, pk: dict) -> dict:
+def roofline_for(es, cluster, A, kernels: list, nb: int, pk: dict, pack: bool = False) -> dict:
     """Dominant kernel = the member launch with the largest device time.
     kernels: per worker [(name, ms)] averaged over the timed steps."""
     workers = [(d, m) for d in range(A.device_count()) for m in range(A.model_count())
@@ -336,6 +336,11 @@ def roofline_for(es, cluster, A, kernels: list, nb: int, pk: dict) -> dict:
                    "hbm_gbs": round(gbs, 1), "hbm_frac": round(gbs / peak_b, 3),
                    "flop_per_sample": f, "bytes_per_sample": b, "bound": bound,
                    "frac": round(frac, 4)}
+            # A b-row batch is one M = 128 UMMA tile (the batcher's split), so
+            # the fused heads' tensor ceiling at batch b is b/128 of peak.
+            bt = A.at(d, mm) if not pack else 128
+            if name.startswith("member_mlp2") and bt < 128:
+                row["b_ceiling_frac"] = round(tf / (peak_t * bt / 128.0), 4)
             per_kernel.append(row)
             if best is None or ms > best["ms"]:
                 best = row
@@ -518,7 +523,8 @@ def run_b200(args, dist: Dist) -> dict | None:
         X = es.SampleStore(synthetic_seed=args.seed + dist.rank * 7919, nb=local_nb, width=784,
                            device=device_map[0])
         system = es.InferenceSystem(A, cluster, rule, device_map=device_map, copy_outputs=False,
-                                    e2e_host_convert=bool(args.e2e_host_convert))
+                                    e2e_host_convert=bool(args.e2e_host_convert),
+                                    pack_batches=args.pack_batches)
     gather = None
     if not multirow and dist.world > 1:
         # The reference's accumulator sees every worker's predictions
@@ -640,8 +646,10 @@ def run_b200(args, dist: Dist) -> dict | None:
             (", predictions gathered to rank 0 over NCCL inside the timed window" if gather else ""),
             "gather": gather,
             "segment_size": 128,
+            "tiles": "whole segments (pack_batches)" if args.pack_batches
+            else "one b-row batch per UMMA tile (the reference batcher's split)",
         },
-        "roofline": roofline_for(es, cluster, A, kern, args.nb, pk),
+        "roofline": roofline_for(es, cluster, A, kern, args.nb, pk, args.pack_batches),
         "member_ms": [round(sum(t for _, t in k), 4) for k in kern],
         "combine_ms": round(combine_ms, 4),
         "combine_hbm_gbs": round(args.nb * (len(cfg["roster"]) * 40 + 44) / (combine_ms * 1e-3) / 1e9, 1)
@@ -736,6 +744,8 @@ def main():
                     help="--impl reference: seconds for the whole warm-up + timed run")
     ap.add_argument("--no-ref-faithful", dest="ref_faithful", action="store_false",
                     help="--impl reference: skip the matrix-faithful figure")
+    ap.add_argument("--pack-batches", action="store_true",
+                    help="tiles pack whole segments whatever the batch (PoolOptions.pack_batches)")
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS),
                     help="BASELINE.json config (default cfg2, the metric's config)")
     args = ap.parse_args()

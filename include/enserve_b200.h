@@ -119,6 +119,9 @@ typedef struct es_pool_opts {
                               whose workers sit on distinct GPUs), 1 = always, -1 = off
                               (the static split, dp_equal_split) */
   int64_t claim_chunk;     /* segments per claim (0 = auto) */
+  int pack_batches;        /* 1 = every tile packs a whole segment whatever the batch
+                              (bit-identical logits; b then stops mattering on B200);
+                              0 = a b-row batch is one tile (the reference batcher) */
 } es_pool_opts;
 
 /* RunStats (pipeline.hpp:19-25). */

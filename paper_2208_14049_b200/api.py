@@ -682,7 +682,8 @@ def _pool_opts(keep: list, device_map=None, copy_outputs=True, warmup=True,
                sms_per_worker=0, overlap_colocated=False, e2e_chunk_rows=0,
                e2e_host_convert=True, e2e_convert_eighths=0,
                dp_equal_split=False, row_partials=False, peer_stores=True,
-               row_nodes=False, dp_claim="auto", claim_chunk=0) -> _abi.PoolOpts:
+               row_nodes=False, dp_claim="auto", claim_chunk=0,
+               pack_batches=False) -> _abi.PoolOpts:
     """PoolOptions (runtime.hpp)."""
     dm = None
     n = 0
@@ -695,7 +696,7 @@ def _pool_opts(keep: list, device_map=None, copy_outputs=True, warmup=True,
                       int(e2e_chunk_rows), int(e2e_host_convert), int(e2e_convert_eighths),
                       int(dp_equal_split), int(row_partials), int(not peer_stores),
                       int(row_nodes), {"auto": 0, True: 1, False: -1}[dp_claim],
-                      int(claim_chunk))
+                      int(claim_chunk), int(pack_batches))
     keep.append(o)
     return o
 

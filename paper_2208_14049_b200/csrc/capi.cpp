@@ -194,6 +194,7 @@ PoolOptions to_opts(const es_pool_opts* o) {
   p.dp_claim = o->dp_claim < 0 ? PoolOptions::kClaimOff
                : o->dp_claim > 0 ? PoolOptions::kClaimAlways : PoolOptions::kClaimAuto;
   p.claim_chunk = o->claim_chunk;
+  p.pack_batches = o->pack_batches != 0;
   return p;
 }
 

@@ -369,7 +369,8 @@ InferenceSystem::InferenceSystem(const AllocationMatrix& A, const ClusterSpec& c
       // backend's rule, backend.cpp:41), and the real device must host it.
       w->member = std::make_unique<DeviceMember>();
       if (load > cluster_.devices[d].memory_mib ||
-          !w->member->load(w->phys, cluster_.models[m], b)) {
+          !w->member->load(w->phys, cluster_.models[m],
+                           options_.pack_batches ? std::max(b, cluster_.segment_size) : b)) {
         oom = true;
         break;
       }

@@ -151,6 +151,15 @@ struct PoolOptions {
   enum ClaimMode { kClaimOff = 0, kClaimAuto = 1, kClaimAlways = 2 };
   int dp_claim = kClaimAuto;
   long long claim_chunk = 0;
+  // A worker's batch b is its tile height: each b-row batch of a segment is
+  // one M = 128 UMMA tile (the reference batcher's split, pipeline.cpp:155-162,
+  // kept observable).  A tcgen05 MMA costs the same for 8 or 128 rows (and
+  // swap-AB with N = b the same for N <= 92), so on B200 a batch of b rows
+  // runs at b/128 of the tensor rate (profiles/r2m_small_batch.txt).  On,
+  // every tile packs a whole segment whatever b (rows are independent, the
+  // logits are bit-identical): the batch size then stops mattering on the
+  // device.  Off by default so the optimizer still sees the batch dimension.
+  bool pack_batches = false;
   // Gather: false = parity mode, every member's logits go
   // to the combining GPU and one fold runs in model order (bit-identical to
   // the reference); true = fast mode, each device row folds its own members

@@ -448,3 +448,18 @@ def test_row_partial_gather_matches_parity_gather(rule):
         srt = np.sort(ref.combined, axis=1)
         clear = (srt[:, -1] - srt[:, -2]) > 1e-4 * scale[:, 0]
         np.testing.assert_array_equal(got.winners[clear], ref.winners[clear])
+
+
+def test_packed_batches_are_bit_identical_to_batch_tiles():
+    """PoolOptions.pack_batches (a tile packs a whole segment whatever the
+    batch) changes only the device schedule: every member's logits, and so
+    the fold, are bit-identical to one b-row tile per batch."""
+    import bench
+    c = bench.make_cluster(es, {"roster": bench.ROSTER, "devices": 1, "device_mib": 183359.0})
+    A = es.AllocationMatrix.from_array([[8, 32, 16, 64]])
+    X = es.SampleStore(refcpu.features(81, 128 * 13 + 77, 784))
+    rule = es.CombinationRule.averaging(softmax=True)
+    tiles = es.run_inference(X, A, c, rule)
+    packed = es.run_inference(X, A, c, rule, pack_batches=True)
+    np.testing.assert_array_equal(tiles.combined, packed.combined)
+    np.testing.assert_array_equal(tiles.winners, packed.winners)
