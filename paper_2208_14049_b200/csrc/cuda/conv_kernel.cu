@@ -282,8 +282,7 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
 #pragma unroll
           for (int j = 0; j < KP2; ++j) {
             const uint64_t ad =
-                adm + static_cast<uint64_t>((dhi - 1) * L.R - ((args.debug & 32) ? 0 : 1) +
-                                            j * static_cast<int>(a2_step));
+                adm + static_cast<uint64_t>((dhi - 1) * L.R - 1 + j * static_cast<int>(a2_step));
             const uint64_t bd = w2d + static_cast<uint64_t>((dhi * KP2 + j) * 2 * L.n2);
             if (elect_one()) umma_bf16(d, ad, bd, id2, (dhi | j) != 0);
           }
