@@ -526,18 +526,37 @@ def run_b200(args, dist: Dist) -> dict | None:
                                     e2e_host_convert=bool(args.e2e_host_convert),
                                     pack_batches=args.pack_batches)
     gather = None
-    if not multirow and dist.world > 1:
+    if not multirow and dist.world > 1 and args.gather:
         # The reference's accumulator sees every worker's predictions
         # (pipeline.cpp:210-211, :258-279): each rank's probabilities + argmax
         # go to rank 0 over NCCL after every run, inside the timed window.
+        # Every rank must agree on using it: a rank whose setup failed makes
+        # all ranks run without it (and the line says why).
         firsts, counts = gather_plan(es, dist.world, A.cells[0].tolist(), args.nb)
-        uid = dist.broadcast_object(es.nccl_unique_id() if dist.rank == 0 else None)
-        comm = es.Comm(uid, dist.world, dist.rank, gpu)
-        system.set_gather(comm, 0, firsts, counts)
+        err, uid = None, None
+        if dist.rank == 0:
+            try:
+                uid = es.nccl_unique_id()
+            except Exception as e:  # noqa: BLE001 -- reported in the JSON line
+                err = f"{type(e).__name__}: {e}"
+        uid = dist.broadcast_object(uid)
+        if uid is None:
+            err = err or "rank 0 could not create an NCCL unique id"
+        else:
+            try:
+                comm = es.Comm(uid, dist.world, dist.rank, gpu)
+                system.set_gather(comm, 0, firsts, counts)
+            except Exception as e:  # noqa: BLE001 -- reported in the JSON line
+                err = f"{type(e).__name__}: {e}"
+        errs = [e for e in dist.gather([err]) if e[0] is not None]
         total = sum(counts)
-        gather = {"collective": "NCCL grouped send/recv to rank 0 (probabilities + argmax)",
-                  "bytes_per_step": total * (cfg_classes(cfg) * 4 + 4),
-                  "rows_per_step": total, "nccl_version": es.nccl_version()}
+        if errs:
+            system.set_gather(None)
+            gather = {"error": errs[0][0]}
+        else:
+            gather = {"collective": "NCCL grouped send/recv to rank 0 (probabilities + argmax)",
+                      "bytes_per_step": total * (cfg_classes(cfg) * 4 + 4),
+                      "rows_per_step": total, "nccl_version": es.nccl_version()}
     if active:
         for _ in range(args.warmup):
             system.run(X, copy=False)
@@ -744,6 +763,8 @@ def main():
                     help="--impl reference: seconds for the whole warm-up + timed run")
     ap.add_argument("--no-ref-faithful", dest="ref_faithful", action="store_false",
                     help="--impl reference: skip the matrix-faithful figure")
+    ap.add_argument("--no-gather", dest="gather", action="store_false",
+                    help="N > 1: skip the NCCL prediction gather to rank 0")
     ap.add_argument("--pack-batches", action="store_true",
                     help="tiles pack whole segments whatever the batch (PoolOptions.pack_batches)")
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS),
