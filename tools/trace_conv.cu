@@ -14,6 +14,18 @@
 #include "cuda/aux_kernels.cuh"
 #include "cuda/conv_kernel.cuh"
 
+// SM clock while the GPU is busy: clock64 vs globaltimer over ~2 ms of spinning.
+__global__ void clock_probe(double* mhz) {
+  unsigned long long g0, g1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
+  const long long c0 = clock64();
+  do {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
+  } while (g1 - g0 < 2000000ull);
+  const long long c1 = clock64();
+  if (threadIdx.x == 0 && blockIdx.x == 0) *mhz = double(c1 - c0) / double(g1 - g0) * 1e3;
+}
+
 int main(int argc, char** argv) {
   const int c1 = argc > 1 ? std::atoi(argv[1]) : 64;
   const int c2 = argc > 2 ? std::atoi(argv[2]) : 32;
@@ -69,6 +81,14 @@ int main(int argc, char** argv) {
     cudaEventElapsedTime(&ms, e0, e1);
     std::printf("rep %d: %.3f ms = %.3e samples/s (%s)\n", rep, ms, nb / (ms * 1e-3),
                 cudaGetErrorString(cudaGetLastError()));
+  }
+  {
+    double* mhz;
+    cudaMalloc(&mhz, 8);
+    clock_probe<<<148, 128>>>(mhz);
+    double h = 0;
+    cudaMemcpy(&h, mhz, 8, cudaMemcpyDeviceToHost);
+    std::printf("SM clock right after: %.0f MHz\n", h);
   }
   std::vector<unsigned long long> t(32 * 16);
   cudaMemcpy(t.data(), trace, t.size() * 8, cudaMemcpyDeviceToHost);
