@@ -122,6 +122,9 @@ typedef struct es_pool_opts {
   int pack_batches;        /* 1 = every tile packs a whole segment whatever the batch
                               (bit-identical logits; b then stops mattering on B200);
                               0 = a b-row batch is one tile (the reference batcher) */
+  int fp32;                /* 1 = fp32-accurate members (fp32 X, weights, activations and
+                              accumulation on the CUDA cores; 1e-5 parity mode);
+                              0 = bf16 operands on the tensor cores */
 } es_pool_opts;
 
 /* RunStats (pipeline.hpp:19-25). */

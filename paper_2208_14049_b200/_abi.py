@@ -48,7 +48,8 @@ class PoolOpts(C.Structure):
                 ("e2e_host_convert", C.c_int), ("e2e_convert_eighths", C.c_int),
                 ("dp_equal_split", C.c_int), ("row_partials", C.c_int),
                 ("no_peer_stores", C.c_int), ("row_nodes", C.c_int),
-                ("dp_claim", C.c_int), ("claim_chunk", C.c_int64), ("pack_batches", C.c_int)]
+                ("dp_claim", C.c_int), ("claim_chunk", C.c_int64), ("pack_batches", C.c_int),
+                ("fp32", C.c_int)]
 
 
 class RunStats(C.Structure):

@@ -683,7 +683,7 @@ def _pool_opts(keep: list, device_map=None, copy_outputs=True, warmup=True,
                e2e_host_convert=True, e2e_convert_eighths=0,
                dp_equal_split=False, row_partials=False, peer_stores=True,
                row_nodes=False, dp_claim="auto", claim_chunk=0,
-               pack_batches=False) -> _abi.PoolOpts:
+               pack_batches=False, fp32=False) -> _abi.PoolOpts:
     """PoolOptions (runtime.hpp)."""
     dm = None
     n = 0
@@ -696,7 +696,7 @@ def _pool_opts(keep: list, device_map=None, copy_outputs=True, warmup=True,
                       int(e2e_chunk_rows), int(e2e_host_convert), int(e2e_convert_eighths),
                       int(dp_equal_split), int(row_partials), int(not peer_stores),
                       int(row_nodes), {"auto": 0, True: 1, False: -1}[dp_claim],
-                      int(claim_chunk), int(pack_batches))
+                      int(claim_chunk), int(pack_batches), int(fp32))
     keep.append(o)
     return o
 

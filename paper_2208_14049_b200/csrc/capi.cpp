@@ -195,6 +195,7 @@ PoolOptions to_opts(const es_pool_opts* o) {
                : o->dp_claim > 0 ? PoolOptions::kClaimAlways : PoolOptions::kClaimAuto;
   p.claim_chunk = o->claim_chunk;
   p.pack_batches = o->pack_batches != 0;
+  p.fp32 = o->fp32 != 0;
   return p;
 }
 

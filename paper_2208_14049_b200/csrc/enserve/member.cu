@@ -11,6 +11,7 @@
 #include "../cuda/aux_kernels.cuh"
 #include "../cuda/conv_kernel.cuh"
 #include "../cuda/dense_kernel.cuh"
+#include "../cuda/fp32_kernels.cuh"
 #include "../cuda/mlp_kernel.cuh"
 #include "../cuda/mlp_pair_kernel.cuh"
 #include "../cuda/mlp_tmem_kernel.cuh"
@@ -65,7 +66,7 @@ struct DeviceMember::Impl {
   std::vector<std::pair<int, int>> dims;  // (fan_in, fan_out) per weight matrix
   // Dense: too wide for a fused head -- the hidden layer through the dense
   // kernel, the last layer in its logits mode.
-  enum class Head { Synthetic, SwapAB, Tmem, Pair, Dense } head = Head::Synthetic;
+  enum class Head { Synthetic, SwapAB, Tmem, Pair, Dense, Fp32 } head = Head::Synthetic;
   es::Mlp2Layout plan_swapab{};
   es::MlpTLayout plan_tmem{};
   es::MlpPLayout plan_pair{};
@@ -81,6 +82,7 @@ struct DeviceMember::Impl {
   std::vector<void*> act;
   std::vector<int> act_width;
   std::vector<std::size_t> act_rows;
+  int act_elem = 2;  // bytes per activation: bf16, or fp32 (Head::Fp32)
 };
 
 DeviceMember::~DeviceMember() {
@@ -98,11 +100,14 @@ std::string DeviceMember::schedule() const {
     case Impl::Head::Tmem: return "tmem";
     case Impl::Head::SwapAB: return "swapab";
     case Impl::Head::Dense: return "dense";
+    case Impl::Head::Fp32: return "fp32";
     default: return "synthetic";
   }
 }
 
-bool DeviceMember::load(int device, const ModelSpec& model, int batch) {
+bool DeviceMember::fp32() const { return impl_ && impl_->head == Impl::Head::Fp32; }
+
+bool DeviceMember::load(int device, const ModelSpec& model, int batch, bool fp32) {
   device_ = device;
   impl_ = new Impl();
   Impl& I = *impl_;
@@ -114,6 +119,7 @@ bool DeviceMember::load(int device, const ModelSpec& model, int batch) {
   I.dims = a.layer_dims();
   const int L = static_cast<int>(I.dims.size());
   if (L < 2) throw SpecError(model.name + ": a member needs at least two layers");
+  if (fp32) return load_fp32(device);
   if (a.kind == MemberArch::Kind::CNN) {
     // Leading layers: the fused convolution stack, bf16 [(S/P)^2 * c2] rows out.
     I.cnn = true;
@@ -210,6 +216,11 @@ std::vector<std::string> DeviceMember::kernel_names() const {
   if (!impl_) return n;
   const Impl& I = *impl_;
   if (I.head == Impl::Head::Synthetic) return {"synthetic_member_kernel"};
+  if (I.head == Impl::Head::Fp32) {
+    if (I.cnn) n.push_back("f32_conv_kernel");
+    for (std::size_t l = I.cnn ? 2 : 0; l < I.dims.size(); ++l) n.push_back("f32_dense_kernel");
+    return n;
+  }
   if (I.cnn) n.push_back(I.conv.split ? "conv_stack_sm100[split]" : "conv_stack_sm100[tap]");
   for (const auto& d : I.dense) n.push_back(d.pair ? "dense_pair_sm100" : "dense_sm100");
   if (env_is("ES_MEMBER_KERNEL", "simt") && I.head != Impl::Head::Dense) {
@@ -254,10 +265,12 @@ int DeviceMember::forward(const void* x, long long nb, int seg_size, long long s
     if (I.act_rows[l] < static_cast<std::size_t>(nb)) {
       cudaFree(I.act[l]);
       I.act[l] = nullptr;
-      M_CUDA(cudaMalloc(&I.act[l], static_cast<std::size_t>(nb) * I.act_width[l] * 2));
+      M_CUDA(cudaMalloc(&I.act[l], static_cast<std::size_t>(nb) * I.act_width[l] * I.act_elem));
       I.act_rows[l] = static_cast<std::size_t>(nb);
     }
   }
+  if (I.head == Impl::Head::Fp32)
+    return forward_fp32(static_cast<const float*>(x), nb, r0, r1, out, grid, stream, marks, claim);
   if (I.cnn) {
     es::ConvArgs c;
     c.L = I.conv;
@@ -361,6 +374,107 @@ int DeviceMember::forward(const void* x, long long nb, int seg_size, long long s
   }
   mark(launches);
   return launches + 1;
+}
+
+bool DeviceMember::load_fp32(int device) {
+  Impl& I = *impl_;
+  const MemberArch& a = I.model.arch;
+  const int L = static_cast<int>(I.dims.size());
+  I.head = Impl::Head::Fp32;
+  I.act_elem = 4;
+  if (a.kind == MemberArch::Kind::CNN) {
+    I.cnn = true;
+    if (!es::f32_conv_supported(a.widths[0], a.widths[1], a.widths[2], a.widths[3]))
+      throw SpecError(I.model.name + ": CNN shape too large for the fp32 convolution kernel");
+    for (int l = 2; l < L - 1; ++l) I.act_width.push_back(I.dims[l].first);
+    I.act_width.push_back(I.dims[L - 1].first);
+  } else {
+    for (int l = 0; l < L - 1; ++l) I.act_width.push_back(I.dims[l].second);
+  }
+  OnDev on(device);
+  auto up = [](std::size_t x) { return (x + 255) / 256 * 256; };
+  std::size_t off = 0;
+  for (int l = 0; l < L; ++l) {
+    I.w_off.push_back(off);
+    off += up(static_cast<std::size_t>(I.dims[l].first) * I.dims[l].second * 4);
+    I.b_off.push_back(off);
+    off += up(static_cast<std::size_t>(I.dims[l].second) * 4);
+  }
+  bytes_ = off;
+  cudaError_t e = cudaMalloc(&I.weights, bytes_);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    I.weights = nullptr;
+    return false;
+  }
+  M_CUDA(e);
+  uint8_t* base = static_cast<uint8_t*>(I.weights);
+  for (int l = 0; l < L; ++l) {
+    const int fi = I.dims[l].first, fo = I.dims[l].second;
+    const float limit = static_cast<float>(std::sqrt(6.0 / static_cast<double>(fi + fo)));
+    M_LAUNCH(es::generate_dense_layer_f32(a.weight_seed, l, fi, fo, limit,
+                                          reinterpret_cast<float*>(base + I.w_off[l]),
+                                          reinterpret_cast<float*>(base + I.b_off[l]), 0));
+  }
+  I.act.assign(I.act_width.size(), nullptr);
+  I.act_rows.assign(I.act_width.size(), 0);
+  M_CUDA(cudaDeviceSynchronize());
+  return true;
+}
+
+// fp32 chain: [conv stack] then every dense layer (ReLU but the last), the
+// last writing fp32 logits at the rows' offsets.
+int DeviceMember::forward_fp32(const float* x, long long nb, long long r0, long long r1, float* out,
+                               int grid, cudaStream_t stream, const cudaEvent_t* marks,
+                               const es::ClaimedRun* claim) {
+  Impl& I = *impl_;
+  const uint8_t* base = static_cast<const uint8_t*>(I.weights);
+  const int L = static_cast<int>(I.dims.size());
+  auto W = [&](int l) { return reinterpret_cast<const float*>(base + I.w_off[l]); };
+  auto B = [&](int l) { return reinterpret_cast<const float*>(base + I.b_off[l]); };
+  int launches = 0;
+  const float* cur = x;
+  int l = 0;
+  if (I.cnn) {
+    const MemberArch& a = I.model.arch;
+    es::F32ConvArgs c;
+    c.x = x;
+    c.w1 = W(0);
+    c.b1 = B(0);
+    c.w2 = W(1);
+    c.b2 = B(1);
+    c.out = static_cast<float*>(I.act[0]);
+    c.S = a.widths[0];
+    c.P = a.widths[1];
+    c.c1 = a.widths[2];
+    c.c2 = a.widths[3];
+    c.row_begin = r0;
+    c.row_end = r1;
+    c.claim = claim;
+    M_LAUNCH(es::f32_conv_launch(c, grid, stream));
+    if (marks) M_CUDA(cudaEventRecord(marks[launches], stream));
+    ++launches;
+    cur = c.out;
+    l = 2;
+  }
+  for (; l < L; ++l) {
+    es::F32DenseArgs d;
+    d.x = cur;
+    d.w = W(l);
+    d.b = B(l);
+    d.K = I.dims[l].first;
+    d.N = I.dims[l].second;
+    d.relu = l < L - 1;
+    d.y = l == L - 1 ? out : static_cast<float*>(I.act[I.cnn ? l - 1 : l]);
+    d.row_begin = r0;
+    d.row_end = r1;
+    d.claim = claim;
+    M_LAUNCH(es::f32_dense_launch(d, grid, stream));
+    if (marks) M_CUDA(cudaEventRecord(marks[launches], stream));
+    ++launches;
+    cur = d.y;
+  }
+  return launches;
 }
 
 }  // namespace enserve

@@ -8,6 +8,9 @@
 //     as one fused member kernel (hidden layer never leaves the SM): the
 //     SM-pair schedule for hidden >= 512, the single-SM TMEM schedule below,
 //     the swap-AB schedule when neither fits.
+//   * fp32 (load(..., fp32 = true)): the same layers with fp32 X, weights,
+//     activations and accumulation on the CUDA cores (cuda/fp32_kernels.cuh),
+//     for the 1e-5 fp32 parity mode; forward() then reads an fp32 X.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -31,7 +34,8 @@ class DeviceMember {
 
   // Predictor::load(): false = out of memory (a tile plan does not fit an SM,
   // or a device allocation failed); other failures throw.
-  bool load(int device, const ModelSpec& model, int batch);
+  bool load(int device, const ModelSpec& model, int batch, bool fp32 = false);
+  bool fp32() const;
 
   // Logits of every row of segments [s0, s1) of x (bf16 [nb][width], rows
   // indexed globally) into out ([nb][C] fp32).  Returns kernel launches.
@@ -63,6 +67,9 @@ class DeviceMember {
   Impl* impl_ = nullptr;
   int device_ = 0;
   std::size_t bytes_ = 0;
+  bool load_fp32(int device);
+  int forward_fp32(const float* x, long long nb, long long r0, long long r1, float* out, int grid,
+                   cudaStream_t stream, const cudaEvent_t* marks, const es::ClaimedRun* claim);
 };
 
 }  // namespace enserve

@@ -14,6 +14,7 @@
 #include <mutex>
 
 #include "../cuda/aux_kernels.cuh"
+#include "../cuda/fp32_kernels.cuh"
 #include "../cuda/mlp_kernel.cuh"
 #include "enserve/collective.hpp"
 #include "enserve/member.hpp"
@@ -164,6 +165,27 @@ SampleStore::~SampleStore() {
       cudaSetDevice(static_cast<int>(d));
       cudaFree(replicas_[d]);
     }
+  for (std::size_t d = 0; d < replicas32_.size(); ++d)
+    if (replicas32_[d]) {
+      cudaSetDevice(static_cast<int>(d));
+      cudaFree(replicas32_[d]);
+    }
+}
+
+const float* SampleStore::device_replica_f32(int device) const {
+  if (replicas32_.size() <= static_cast<std::size_t>(device)) replicas32_.resize(device + 1, nullptr);
+  if (replicas32_[device]) return replicas32_[device];
+  OnDevice on(device);
+  const std::size_t n = nb_ * width_;
+  float* x = nullptr;
+  ES_CUDA(cudaMalloc(&x, std::max<std::size_t>(n, 1) * sizeof(float)));
+  if (synthetic_)
+    ES_LAUNCH(es::generate_features_f32(synthetic_seed_, n, x, 0));
+  else if (n > 0)
+    ES_CUDA(cudaMemcpy(x, host_, n * sizeof(float), cudaMemcpyHostToDevice));
+  ES_CUDA(cudaDeviceSynchronize());
+  replicas32_[device] = x;
+  return x;
 }
 
 const void* SampleStore::device_replica(int device) const {
@@ -370,7 +392,8 @@ InferenceSystem::InferenceSystem(const AllocationMatrix& A, const ClusterSpec& c
       w->member = std::make_unique<DeviceMember>();
       if (load > cluster_.devices[d].memory_mib ||
           !w->member->load(w->phys, cluster_.models[m],
-                           options_.pack_batches ? std::max(b, cluster_.segment_size) : b)) {
+                           options_.pack_batches ? std::max(b, cluster_.segment_size) : b,
+                           options_.fp32)) {
         oom = true;
         break;
       }
@@ -558,7 +581,7 @@ void InferenceSystem::probe_rates(const SampleStore& X) {
     float ms = 0.0f;
     for (int rep = 0; rep < 2; ++rep) {
       ES_CUDA(cudaEventRecord(w.ev_begin, w.stream));
-      w.member->forward(X.device_replica(w.phys), nb, cluster_.segment_size, 0, segs, out, grid,
+      w.member->forward(x_on(X, w.phys), nb, cluster_.segment_size, 0, segs, out, grid,
                         w.stream, nullptr);
       ES_CUDA(cudaEventRecord(w.ev_done, w.stream));
       ES_CUDA(cudaEventSynchronize(w.ev_done));
@@ -568,6 +591,11 @@ void InferenceSystem::probe_rates(const SampleStore& X) {
     rates[i] = rows / std::max(static_cast<double>(ms) * 1e-3, 1e-9);
   }
   rates_ = std::move(rates);
+}
+
+const void* InferenceSystem::x_on(const SampleStore& X, int phys) const {
+  if (options_.fp32) return X.device_replica_f32(phys);
+  return X.device_replica(phys);
 }
 
 bool InferenceSystem::single_device() const {
@@ -625,7 +653,7 @@ void InferenceSystem::begin_run(std::shared_ptr<const SampleStore> X, Combinatio
   const std::size_t nb = X->nb_samples();
   const int C = output_width_;
   // Device replicas (untimed, like the reference's begin_run).
-  for (const auto& w : workers_) X->device_replica(w->phys);
+  for (const auto& w : workers_) x_on(*X, w->phys);
   {
     OnDevice on(combine_dev_);
     if (nb > impl_->cap_rows) {
@@ -778,12 +806,12 @@ std::size_t InferenceSystem::broadcast() {
       for (long long r = 0; r < q.rounds; ++r) {
         ES_LAUNCH(es::claim_launch(q.counter, q.segments, q.chunk, cluster_.segment_size, nb,
                                    w->claim, q.owner, index, w->stream));
-        launches_ += 1 + w->member->forward(X.device_replica(w->phys), nb, cluster_.segment_size,
+        launches_ += 1 + w->member->forward(x_on(X, w->phys), nb, cluster_.segment_size,
                                             0, q.segments, out, grid, w->stream, nullptr, w->claim);
       }
       for (cudaEvent_t e : w->marks) ES_CUDA(cudaEventRecord(e, w->stream));
     } else {
-      launches_ += w->member->forward(X.device_replica(w->phys), nb, cluster_.segment_size,
+      launches_ += w->member->forward(x_on(X, w->phys), nb, cluster_.segment_size,
                                       w->seg_begin, w->seg_end, out, grid, w->stream,
                                       w->marks.empty() ? nullptr : w->marks.data());
     }
@@ -1023,13 +1051,15 @@ double InferenceSystem::run_host(const float* X, std::size_t nb, std::size_t wid
   const bool pinned_input =
       cudaPointerGetAttributes(&pa, X) == cudaSuccess && pa.type == cudaMemoryTypeHost;
   cudaGetLastError();
-  const int mode = options_.e2e_host_convert ? (pinned_input ? 0 : 1) : (pinned_input ? 2 : 1);
+  // fp32 members read fp32 rows: every chunk is DMA'd as is (mode 3).
+  const int mode = options_.fp32 ? 3
+                   : options_.e2e_host_convert ? (pinned_input ? 0 : 1)
+                                               : (pinned_input ? 2 : 1);
   const std::size_t k8 = static_cast<std::size_t>(std::clamp(options_.e2e_convert_eighths, 0, 8));
   return run_host_core(nb, width, Y_out, labels_out,
                        [&](std::size_t i, std::uint16_t* pinned, std::size_t r0,
                            std::size_t rows) -> HostChunk {
-                         const bool convert =
-                             mode == 1 || (mode == 0 && (i + 1) * k8 / 8 > i * k8 / 8);
+                         const bool convert = mode != 3 && (mode == 1 || (mode == 0 && (i + 1) * k8 / 8 > i * k8 / 8));
                          if (!convert) return {X + r0 * width, true};
                          convert_f32_to_bf16_host(X + r0 * width, pinned, rows * width,
                                                   *impl_->pool);
@@ -1039,6 +1069,8 @@ double InferenceSystem::run_host(const float* X, std::size_t nb, std::size_t wid
 
 double InferenceSystem::run_host_blocks(const std::vector<HostRowBlock>& blocks, std::size_t width,
                                         float* Y_out, std::int32_t* labels_out) {
+  if (options_.fp32)
+    throw SpecError("fp32 members read fp32 rows; host row blocks carry bf16 (use run_host)");
   std::size_t nb = 0;
   for (const HostRowBlock& b : blocks) nb += b.rows;
   std::vector<std::size_t> first(blocks.size() + 1, 0);  // first row of every block
@@ -1210,12 +1242,13 @@ double InferenceSystem::run_host_core(std::size_t nb, std::size_t width, float* 
                                 cudaMemcpyHostToDevice, ln.copy));
       ES_CUDA(cudaEventRecord(ls.h2d_done, ln.copy));
       ES_CUDA(cudaStreamWaitEvent(ln.comp, ls.h2d_done, 0));
-      if (direct) {
+      if (direct && !options_.fp32) {
         ES_LAUNCH(es::convert_f32_to_bf16(ls.x32 + g0 * width,
                                           static_cast<__nv_bfloat16*>(ls.x16) + g0 * width, elems,
                                           ln.comp));
         ++launches_;
       }
+      const void* xin = options_.fp32 ? static_cast<const void*>(ls.x32) : ls.x16;
       // The combining slot's logits are free once its combine of chunk i-3 ran.
       if (i >= kSlots) ES_CUDA(cudaStreamWaitEvent(ln.comp, sl.combined, 0));
       const int grid = es::num_sms(ln.phys);
@@ -1225,7 +1258,7 @@ double InferenceSystem::run_host_core(std::size_t nb, std::size_t width, float* 
         if (sh.end <= sh.begin) continue;
         const bool staged = w.staged(false);
         float* out = staged ? ls.staging[w.model] : sl.logits[w.model];
-        launches_ += w.member->forward(ls.x16, static_cast<long long>(rows), cluster_.segment_size,
+        launches_ += w.member->forward(xin, static_cast<long long>(rows), cluster_.segment_size,
                                        sh.begin, sh.end, out, grid, ln.comp);
         if (staged) {
           const std::size_t a = static_cast<std::size_t>(sh.begin) * seg;

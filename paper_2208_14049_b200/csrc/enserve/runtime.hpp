@@ -66,6 +66,8 @@ class SampleStore {
   const float* host_data() const { return host_; }
   // bf16 [nb][width] on `device` (uploads + converts on first call).
   const void* device_replica(int device) const;
+  // fp32 [nb][width] on `device` (the fp32 member mode), created on first call.
+  const float* device_replica_f32(int device) const;
 
  private:
   SampleStore() = default;
@@ -76,6 +78,7 @@ class SampleStore {
   std::uint64_t synthetic_seed_ = 0;
   bool synthetic_ = false;
   mutable std::vector<void*> replicas_;  // indexed by CUDA ordinal
+  mutable std::vector<float*> replicas32_;
 };
 
 // ---- run bookkeeping (pipeline.hpp:17-53) -----------------------------------
@@ -160,6 +163,11 @@ struct PoolOptions {
   // logits are bit-identical): the batch size then stops mattering on the
   // device.  Off by default so the optimizer still sees the batch dimension.
   bool pack_batches = false;
+  // fp32-accurate members (north_star's 1e-5 fp32 tolerance): X, weights,
+  // activations and accumulation in fp32 on the CUDA cores
+  // (cuda/fp32_kernels.cuh) instead of bf16 operands on the tensor cores.
+  // run_host then moves fp32 rows (4 B/feature) and converts nothing.
+  bool fp32 = false;
   // Gather: false = parity mode, every member's logits go
   // to the combining GPU and one fold runs in model order (bit-identical to
   // the reference); true = fast mode, each device row folds its own members
@@ -274,6 +282,8 @@ class InferenceSystem {
   };
   using HostFill = std::function<HostChunk(std::size_t, std::uint16_t*, std::size_t, std::size_t)>;
   void probe_rates(const SampleStore& X);
+  // X as the members read it on CUDA ordinal `phys`: bf16, or fp32 (PoolOptions::fp32).
+  const void* x_on(const SampleStore& X, int phys) const;
   std::size_t broadcast_partials(long long nb);
   void finish_broadcast();  // prediction gather (if any) + the end event
   std::vector<double> rates_;  // per worker, probed on the first run with a DP column
