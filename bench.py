@@ -301,7 +301,7 @@ def launch_work(arch, names: list) -> list:
     out, l = [], 0
     for n in names:
         take = 2 if n.startswith("conv_stack") or n.startswith("member_mlp2") or \
-            n.startswith("mlp2_simt") else 1
+            n.startswith("mlp2_simt") or n.startswith("f32_conv") else 1
         f = float(sum(flops[l:l + take]))
         last = l + take == L
         b = widths[l] * 2 + widths[l + take] * (4 if last else 2)
@@ -310,12 +310,20 @@ def launch_work(arch, names: list) -> list:
     return out
 
 
-def roofline_for(es, cluster, A, kernels: list, nb: int, pk: dict, pack: bool = False) -> dict:
+# fp32 mode runs on the CUDA cores: nominal FP32 FMA rate of this part
+# (148 SMs x 128 lanes x 2 FLOP x 1.965 GHz), no measured figure exists.
+FP32_SIMT_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
+
+
+def roofline_for(es, cluster, A, kernels: list, nb: int, pk: dict, pack: bool = False,
+                 fp32: bool = False) -> dict:
     """Dominant kernel = the member launch with the largest device time.
     kernels: per worker [(name, ms)] averaged over the timed steps."""
     workers = [(d, m) for d in range(A.device_count()) for m in range(A.model_count())
                if A.at(d, m)]
     peak_t, peak_b = pk["bf16_tflops_sustained"], pk["hbm_gbs"]
+    if fp32:
+        peak_t = FP32_SIMT_TFLOPS
     ridge = peak_t * 1e12 / (peak_b * 1e9)
     traffic_db = {}
     try:
@@ -326,6 +334,8 @@ def roofline_for(es, cluster, A, kernels: list, nb: int, pk: dict, pack: bool = 
     for j, (d, mm) in enumerate(workers):
         model = cluster.models[mm]
         work = launch_work(model.arch, [n for n, _ in kernels[j]])
+        if fp32:  # 4-byte activations and inputs
+            work = [(f, 2.0 * b) for f, b in work]
         for (name, ms), (f, b) in zip(kernels[j], work):
             tf = f * nb / (ms * 1e-3) / 1e12
             gbs = b * nb / (ms * 1e-3) / 1e9
@@ -356,8 +366,10 @@ def roofline_for(es, cluster, A, kernels: list, nb: int, pk: dict, pack: bool = 
                                        "flop_per_sample": best["flop_per_sample"],
                                        "bytes_per_sample": best["bytes_per_sample"],
                                        "samples": nb},
-            "peak_source": f"{pk['source']} " + ("bf16 dense, sustained (kernel timed inside a "
-                                                 "long step)" if tensor else "HBM copy"),
+            "peak_source": ("nominal fp32 CUDA-core FMA rate (148 SMs x 128 lanes x 2 x 1.965 "
+                            "GHz)" if fp32 and tensor else
+                            f"{pk['source']} " + ("bf16 dense, sustained (kernel timed inside a "
+                                                  "long step)" if tensor else "HBM copy")),
             "per_kernel": per_kernel}
 
 
@@ -524,7 +536,7 @@ def run_b200(args, dist: Dist) -> dict | None:
                            device=device_map[0])
         system = es.InferenceSystem(A, cluster, rule, device_map=device_map, copy_outputs=False,
                                     e2e_host_convert=bool(args.e2e_host_convert),
-                                    pack_batches=args.pack_batches)
+                                    pack_batches=args.pack_batches, fp32=args.fp32)
     gather = None
     if not multirow and dist.world > 1 and args.gather:
         # The reference's accumulator sees every worker's predictions
@@ -638,7 +650,7 @@ def run_b200(args, dist: Dist) -> dict | None:
         "higher_is_better": True,
         "scaling": "strong" if multirow else "weak",
         "vs_baseline": None,
-        "dtype": "bf16",
+        "dtype": "f32" if args.fp32 else "bf16",
         "data": "synthetic (U[0,1) features generated on device; Glorot-uniform synthetic weights)",
         "config": {
             "workload": cfg["workload"],
@@ -668,7 +680,7 @@ def run_b200(args, dist: Dist) -> dict | None:
             "tiles": "whole segments (pack_batches)" if args.pack_batches
             else "one b-row batch per UMMA tile (the reference batcher's split)",
         },
-        "roofline": roofline_for(es, cluster, A, kern, args.nb, pk, args.pack_batches),
+        "roofline": roofline_for(es, cluster, A, kern, args.nb, pk, args.pack_batches, args.fp32),
         "member_ms": [round(sum(t for _, t in k), 4) for k in kern],
         "combine_ms": round(combine_ms, 4),
         "combine_hbm_gbs": round(args.nb * (len(cfg["roster"]) * 40 + 44) / (combine_ms * 1e-3) / 1e9, 1)
@@ -765,6 +777,8 @@ def main():
                     help="--impl reference: skip the matrix-faithful figure")
     ap.add_argument("--no-gather", dest="gather", action="store_false",
                     help="N > 1: skip the NCCL prediction gather to rank 0")
+    ap.add_argument("--fp32", action="store_true",
+                    help="fp32-accurate members on the CUDA cores (PoolOptions.fp32)")
     ap.add_argument("--pack-batches", action="store_true",
                     help="tiles pack whole segments whatever the batch (PoolOptions.pack_batches)")
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS),
