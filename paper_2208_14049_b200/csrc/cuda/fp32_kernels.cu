@@ -70,16 +70,25 @@ __global__ void __launch_bounds__(kThreads) f32_dense_kernel(const F32DenseArgs 
   }
 }
 
-// One sample at a time per CTA: the image and conv1's output (with a zero
-// border) in shared memory, conv2 outputs spread over the threads.
+// One sample at a time per CTA, conv2's weights resident in shared memory
+// (row stride 9*c1 + 1 floats: threads of a warp read different output
+// channels of one K index without bank conflicts).  The image and conv1's
+// output (with a zero border) are staged per sample.  conv2: thread t owns
+// channel t % c2 of positions t / c2, t / c2 + groups, ...; the positions'
+// activations are warp-uniform (broadcast reads).  Every output is one fmaf
+// chain in K order (tap-major, then input channel), like the oracle.
 __global__ void __launch_bounds__(kThreads) f32_conv_kernel(const F32ConvArgs a) {
   extern __shared__ float smem[];
   const int S = a.S, P = a.P, G = S / P, GP = G + 2, c1 = a.c1, c2 = a.c2;
-  float* img = smem;                // [S*S]
-  float* a1 = smem + S * S;         // [(G+2)*(G+2)][c1], border zero
+  const int K2 = 9 * c1, ws = K2 + 1;
+  float* w2 = smem;                 // [c2][9*c1 + 1]
+  float* img = w2 + c2 * ws;        // [S*S]
+  float* a1 = img + S * S;          // [(G+2)*(G+2)][c1], border zero
   const long long rb = a.claim ? a.claim->row_begin : a.row_begin;
   const long long re = a.claim ? a.claim->row_end : a.row_end;
+  for (int i = threadIdx.x; i < c2 * K2; i += kThreads) w2[(i / K2) * ws + i % K2] = a.w2[i];
   for (int i = threadIdx.x; i < GP * GP * c1; i += kThreads) a1[i] = 0.0f;
+  const int groups = kThreads / c2;  // c2 divides 256 or groups = 0 (handled below)
   for (long long s = rb + blockIdx.x; s < re; s += gridDim.x) {
     __syncthreads();  // the previous sample's a1 / img reads are done
     for (int i = threadIdx.x; i < S * S; i += kThreads) img[i] = a.x[s * S * S + i];
@@ -94,16 +103,46 @@ __global__ void __launch_bounds__(kThreads) f32_conv_kernel(const F32ConvArgs a)
     }
     __syncthreads();
     float* dst = a.out + s * static_cast<long long>(G * G * c2);
-    for (int o = threadIdx.x; o < G * G * c2; o += kThreads) {
-      const int co = o % c2, p = o / c2, pi = p / G, pj = p % G;
-      const float* w = a.w2 + static_cast<long long>(co) * 9 * c1;
-      float acc = 0.0f;
-      for (int tap = 0; tap < 9; ++tap) {
-        const float* src = a1 + ((pi + 1 + tap / 3 - 1) * GP + pj + 1 + tap % 3 - 1) * c1;
-        const float* wt = w + tap * c1;
-        for (int ci = 0; ci < c1; ++ci) acc = fmaf(src[ci], __ldg(wt + ci), acc);
+    if (groups > 0 && threadIdx.x < groups * c2) {
+      constexpr int kPos = 8;  // positions per pass of a thread
+      const int co = threadIdx.x % c2, pg = threadIdx.x / c2;
+      const float* w = w2 + co * ws;
+      const float bias = __ldg(a.b2 + co);
+      for (int p0 = pg; p0 < G * G; p0 += groups * kPos) {
+        float acc[kPos];
+        int base[kPos];
+#pragma unroll
+        for (int q = 0; q < kPos; ++q) {
+          acc[q] = 0.0f;
+          const int p = min(p0 + q * groups, G * G - 1);
+          base[q] = ((p / G) * GP + p % G) * c1;  // a1 row of tap (dh, dw) = (-1, -1)
+        }
+        for (int tap = 0; tap < 9; ++tap) {
+          const int toff = ((tap / 3) * GP + tap % 3) * c1;
+          const float* wt = w + tap * c1;
+          for (int ci = 0; ci < c1; ++ci) {
+            const float wv = wt[ci];
+#pragma unroll
+            for (int q = 0; q < kPos; ++q) acc[q] = fmaf(a1[base[q] + toff + ci], wv, acc[q]);
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < kPos; ++q) {
+          const int p = p0 + q * groups;
+          if (p < G * G) dst[p * c2 + co] = fmaxf(acc[q] + bias, 0.0f);
+        }
       }
-      dst[p * c2 + co] = fmaxf(acc + __ldg(a.b2 + co), 0.0f);
+    } else if (groups == 0) {  // c2 > 256: one output at a time
+      for (int o = threadIdx.x; o < G * G * c2; o += kThreads) {
+        const int co = o % c2, p = o / c2;
+        const float* w = w2 + co * ws;
+        const int b0 = ((p / G) * GP + p % G) * c1;
+        float acc = 0.0f;
+        for (int tap = 0; tap < 9; ++tap)
+          for (int ci = 0; ci < c1; ++ci)
+            acc = fmaf(a1[b0 + ((tap / 3) * GP + tap % 3) * c1 + ci], w[tap * c1 + ci], acc);
+        dst[p * c2 + co] = fmaxf(acc + __ldg(a.b2 + co), 0.0f);
+      }
     }
   }
 }
@@ -115,9 +154,9 @@ __global__ void features_f32_kernel(uint64_t seed, size_t n, float* __restrict__
     y[i] = __fdiv_rn(static_cast<float>(mix64(base + i) >> 40), 16777216.0f);
 }
 
-size_t conv_smem(int S, int P, int c1) {
+size_t conv_smem(int S, int P, int c1, int c2) {
   const int G = S / P;
-  return static_cast<size_t>(S * S + (G + 2) * (G + 2) * c1) * sizeof(float);
+  return static_cast<size_t>(c2 * (9 * c1 + 1) + S * S + (G + 2) * (G + 2) * c1) * sizeof(float);
 }
 
 }  // namespace
@@ -132,14 +171,14 @@ int f32_dense_launch(const F32DenseArgs& a, int grid, cudaStream_t s) {
 }
 
 bool f32_conv_supported(int S, int P, int c1, int c2) {
-  return P >= 1 && S >= P && S % P == 0 && c1 >= 1 && c2 >= 1 && conv_smem(S, P, c1) <= 200 * 1024;
+  return P >= 1 && S >= P && S % P == 0 && c1 >= 1 && c2 >= 1 && conv_smem(S, P, c1, c2) <= 200 * 1024;
 }
 
 int f32_conv_launch(const F32ConvArgs& a, int grid, cudaStream_t s) {
   if (!f32_conv_supported(a.S, a.P, a.c1, a.c2)) return -1;
   const long long rows = a.row_end - a.row_begin;
   if (rows <= 0) return 0;
-  const size_t smem = conv_smem(a.S, a.P, a.c1);
+  const size_t smem = conv_smem(a.S, a.P, a.c1, a.c2);
   if (smem > 48 * 1024 &&
       cudaFuncSetAttribute(f32_conv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(smem)) != cudaSuccess)
