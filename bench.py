@@ -537,7 +537,7 @@ def run_b200(args, dist: Dist) -> dict | None:
         system = es.InferenceSystem(A, cluster, rule, device_map=device_map, copy_outputs=False,
                                     e2e_host_convert=bool(args.e2e_host_convert),
                                     pack_batches=args.pack_batches, fp32=args.fp32)
-    gather = None
+    gather, comm = None, None
     if not multirow and dist.world > 1 and args.gather:
         # The reference's accumulator sees every worker's predictions
         # (pipeline.cpp:210-211, :258-279): each rank's probabilities + argmax
@@ -633,6 +633,8 @@ def run_b200(args, dist: Dist) -> dict | None:
                "samples_per_step": e2e_nb}
     if active:
         system.close()
+    if comm is not None:
+        comm.close()  # after the system (which holds its own reference)
 
     if dist.rank != 0:
         return None
