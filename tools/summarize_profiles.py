@@ -15,7 +15,7 @@ from pathlib import Path
 
 REPO = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(REPO / "tools"))
-from ncu_summary import summarize  # noqa: E402
+from ncu_summary import summarise  # noqa: E402
 
 tag = sys.argv[1]
 key = sys.argv[2] if len(sys.argv) > 2 else None
@@ -42,7 +42,7 @@ shares = {k: {"launches": n[k], "total_us": round(v, 1),
           for k, v in sorted(t.items(), key=lambda kv: -kv[1])}
 (dst / f"{tag}_launch_shares.json").write_text(json.dumps(shares, indent=1) + "\n")
 
-top = summarize(str(src / f"{tag}_top.ncu-rep"))
+top = summarise(src / f"{tag}_top.ncu-rep")
 (dst / f"{tag}_top_ncu.json").write_text(json.dumps(top, indent=1) + "\n")
 if key and top:
     d = top[0]
