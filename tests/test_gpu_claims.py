@@ -136,3 +136,30 @@ def test_auto_queue_across_two_physical_gpus():
     single = es.run_inference(X, es.AllocationMatrix.from_array([[128, 64, 128, 32]]), cluster(1),
                               RULE)
     np.testing.assert_array_equal(out.combined, single.combined)
+
+
+@pytest.mark.parametrize("nb", [0, 1, 127, 129])
+def test_tiny_and_empty_stores_through_every_new_path(nb):
+    """Edge sizes the reference handles (an empty store Deploys to nothing,
+    test_runtime.cpp): claims, row nodes with peer-store and staged routes,
+    run_host lanes and fp32 all agree with the one-node bf16 layout."""
+    A = es.AllocationMatrix.from_array([[128, 64, 0, 32], [64, 128, 128, 128]])
+    c = cluster(2)
+    X = refcpu.features(74, nb, 784) if nb else np.zeros((0, 784), np.float32)
+    rule = RULE
+    ref = es.run_inference(es.SampleStore(X), A, c, rule, device_map=[0, 0])
+    for opts in ({"row_nodes": True, "dp_claim": True, "claim_chunk": 1},
+                 {"row_nodes": True, "peer_stores": False},
+                 {"dp_claim": False}):
+        with es.InferenceSystem(A, c, rule, device_map=[0, 0], **opts) as s:
+            out = s.run(es.SampleStore(X))
+            Y = np.zeros((nb, 10), np.float32)
+            L = np.zeros(nb, np.int32)
+            s.run_host(X, Y, L)
+        np.testing.assert_array_equal(out.combined, ref.combined)
+        np.testing.assert_array_equal(Y, ref.combined)
+        np.testing.assert_array_equal(L, ref.winners)
+    fp = es.run_inference(es.SampleStore(X), A, c, rule, device_map=[0, 0], fp32=True)
+    assert fp.combined.shape == (nb, 10)
+    if nb:
+        assert np.abs(fp.combined - ref.combined).max() < 2e-3  # bf16 vs fp32 members
