@@ -237,15 +237,29 @@ __global__ void __launch_bounds__(128, 1) rate_ta(int N, int reps, unsigned long
 
 // The conv kernel's split conv2 block: 3 dw shifts x 4 K steps, A planar
 // (plane 4608 B, start moved by -1/0/+1 rows), B planar N = 96.
+// rand_fill: operands filled with random bf16 in (-1, 1) instead of zeros
+// (the tensor pipe's rate on real data, not on all-zero operands).
 __global__ void __launch_bounds__(128, 1) rate_split(int N, int reps, int shift_on,
                                                      unsigned long long* out, int dcol = 0,
-                                                     int boff = 0) {
+                                                     int boff = 0, int rand_fill = 0) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align_smem_1024(smem_raw);
   __shared__ uint64_t bar;
   __shared__ uint32_t slot;
-  for (int i = threadIdx.x; i < 96 * 1024 / 16; i += blockDim.x)
-    reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+  for (int i = threadIdx.x; i < 96 * 1024 / 4; i += blockDim.x) {
+    uint32_t v = 0;
+    if (rand_fill) {
+      uint32_t h = (i + 1) * 2654435761u;
+      h ^= h >> 15;
+      h *= 2246822519u;
+      h ^= h >> 13;
+      // two bf16 with sign, exponent 0x7E or 0x7D (|x| in [0.25, 1)), random mantissa
+      const uint32_t lo = ((h & 1u) << 15) | ((0x7Du + ((h >> 1) & 1u)) << 7) | ((h >> 2) & 0x7Fu);
+      const uint32_t hi = (((h >> 9) & 1u) << 15) | ((0x7Du + ((h >> 10) & 1u)) << 7) | ((h >> 11) & 0x7Fu);
+      v = lo | (hi << 16);
+    }
+    reinterpret_cast<uint32_t*>(smem)[i] = v;
+  }
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     fence_barrier_init();
@@ -510,6 +524,14 @@ int main() {
         cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
         std::printf("split pattern N=%d shifts=%d: %6.1f clk/MMA %s\n", N, sh, double(c) / 504,
                     cudaGetErrorString(cudaGetLastError()));
+      }
+    for (int N : {32, 96, 128})
+      for (int rf = 0; rf < 2; ++rf) {
+        rate_split<<<148, 128, 100 * 1024>>>(N, 504, 1, d, 0, 0, rf);
+        unsigned long long c = 0;
+        cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
+        std::printf("split pattern N=%d operands=%s: %6.1f clk/MMA %s\n", N, rf ? "random" : "zero",
+                    double(c) / 504, cudaGetErrorString(cudaGetLastError()));
       }
     for (int dcol : {0, 96, 256, 352})
       for (int boff : {0, 128, 512}) {
