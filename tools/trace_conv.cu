@@ -32,6 +32,7 @@ int main(int argc, char** argv) {
   const int sched = argc > 3 ? std::atoi(argv[3]) : 0;  // conv_plan schedule
   const int debug = argc > 4 ? std::atoi(argv[4]) : 0;  // ConvArgs::debug bits
   const int shifts = argc > 5 ? std::atoi(argv[5]) : -1;  // ConvArgs::shifts (-1 = default)
+  const int grid_div = argc > 6 ? std::atoi(argv[6]) : 1;  // run on sms / grid_div CTAs
   const long long nb = 1 << 20;
   const int S = 28, P = 4, G = 7;
   __nv_bfloat16 *x, *w1, *w2, *y;
@@ -74,7 +75,7 @@ int main(int argc, char** argv) {
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    es::conv_launch(a, x, nb, sms, 0);
+    es::conv_launch(a, x, nb, sms / grid_div, 0);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
