@@ -239,9 +239,10 @@ __global__ void __launch_bounds__(128, 1) rate_ta(int N, int reps, unsigned long
 // (plane 4608 B, start moved by -1/0/+1 rows), B planar N = 96.
 // rand_fill: operands filled with random bf16 in (-1, 1) instead of zeros
 // (the tensor pipe's rate on real data, not on all-zero operands).
-__global__ void __launch_bounds__(128, 1) rate_split(int N, int reps, int shift_on,
+__global__ void __launch_bounds__(512, 1) rate_split(int N, int reps, int shift_on,
                                                      unsigned long long* out, int dcol = 0,
-                                                     int boff = 0, int rand_fill = 0) {
+                                                     int boff = 0, int rand_fill = 0,
+                                                     int idle_mode = 0) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align_smem_1024(smem_raw);
   __shared__ uint64_t bar;
@@ -271,6 +272,16 @@ __global__ void __launch_bounds__(128, 1) rate_split(int N, int reps, int shift_
   tc_fence_after();
   const uint32_t tmem = slot;
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
+  __shared__ uint64_t idle_bar;
+  if (threadIdx.x == 0) {
+    mbar_init(&idle_bar, 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (warp >= 4) {  // idle warps: 1 = suspended try_wait, 2 = spinning try_wait
+    if (idle_mode == 1) mbar_sleep_wait(&idle_bar, 0);
+    if (idle_mode == 2) mbar_wait(&idle_bar, 0);
+  }
   if (warp == 0) {
     const uint32_t a = smem_u32(smem), b = smem_u32(smem + 40 * 1024 + boff);
     const uint32_t idesc = idesc_bf16_f32(128, N);
@@ -278,19 +289,101 @@ __global__ void __launch_bounds__(128, 1) rate_split(int N, int reps, int shift_
     const uint32_t dt = tmem + static_cast<uint32_t>(dcol);
     const long long t0 = clock64();
     for (int r = 0; r < reps; r += 12) {
+      // rotate (idle_mode >= 3): each block reads another 8 KB window of A,
+      // as the kernel does (a new grid block every time), not the same bytes
+      const uint64_t rot = idle_mode >= 3 ? static_cast<uint64_t>(((r / 12) % 4) * 128) : 0;
 #pragma unroll
       for (int dwi = 0; dwi < 3; ++dwi)
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const uint64_t ad = ad0 + static_cast<uint64_t>((dwi - 1) * 8 * shift_on - shift_on + j * 576);
+          const uint64_t ad = ad0 + rot + static_cast<uint64_t>((dwi - 1) * 8 * shift_on - shift_on + j * 576);
           const uint64_t bd = bd0 + static_cast<uint64_t>((dwi * 4 + j) * 2 * N);
-          if (elect_one()) umma_bf16(dt, ad, bd, idesc, (r | dwi | j) != 0);
+          // idle_mode 4: the kernel's ring -- every block starts a fresh
+          // accumulation in the next of 3 slots; 5: plus a commit per block
+          const uint32_t dslot = idle_mode >= 4 ? dt + static_cast<uint32_t>(((r / 12) % 3) * 96) : dt;
+          const uint32_t acc = idle_mode >= 4 ? ((dwi | j) != 0) : ((r | dwi | j) != 0);
+          if (elect_one()) umma_bf16(dslot, ad, bd, idesc, acc);
         }
+      if (idle_mode == 5 && elect_one()) umma_commit(&idle_bar);
     }
     if (elect_one()) umma_commit(&bar);
     __syncwarp();
     mbar_wait(&bar, 0);
     if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = static_cast<unsigned long long>(clock64() - t0);
+    if (threadIdx.x == 0) mbar_arrive(&idle_bar);
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) tmem_dealloc(tmem, 512);
+}
+
+// The conv kernel's slot protocol without its data flow: warp 0 issues the
+// split pattern into a ring of `slots` TMEM slots, committing c2_full[s] per
+// block and waiting c2_empty[s] before reusing a slot; warp 1 (the
+// "epilogue") waits c2_full[s] and arrives c2_empty[s] (optionally after a
+// tcgen05.ld of the slot).
+__global__ void __launch_bounds__(128, 1) rate_ring(int reps, int slots, int epi_ld,
+                                                    unsigned long long* out) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align_smem_1024(smem_raw);
+  __shared__ uint64_t full[4], empty[4], done;
+  __shared__ uint32_t slot;
+  for (int i = threadIdx.x; i < 96 * 1024 / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(&done, 1);
+    fence_barrier_init();
+  }
+  if (threadIdx.x < 32) tmem_alloc(&slot, 512);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
+  const int blocks = reps / 12;
+  if (warp == 0) {
+    const uint32_t a = smem_u32(smem), b = smem_u32(smem + 40 * 1024);
+    const uint32_t idesc = idesc_bf16_f32(128, 96);
+    const uint64_t ad0 = sdesc_planar(a + 16 * 16, 4608), bd0 = sdesc_planar(b, 96 * 16);
+    const long long t0 = clock64();
+    for (int blk = 0; blk < blocks; ++blk) {
+      const int sl = blk % slots;
+      mbar_wait(&empty[sl], (static_cast<uint32_t>(blk / slots) & 1u) ^ 1u);
+      tc_fence_after();
+      const uint32_t d = tmem + 128u + static_cast<uint32_t>(sl * 96);
+#pragma unroll
+      for (int dwi = 0; dwi < 3; ++dwi)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint64_t ad = ad0 + static_cast<uint64_t>((dwi - 1) * 8 - 1 + j * 576);
+          const uint64_t bd = bd0 + static_cast<uint64_t>((dwi * 4 + j) * 2 * 96);
+          if (elect_one()) umma_bf16(d, ad, bd, idesc, (dwi | j) != 0);
+        }
+      if (elect_one()) umma_commit(&full[sl]);
+      __syncwarp();
+    }
+    mbar_wait(&done, 0);
+    if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = static_cast<unsigned long long>(clock64() - t0);
+  } else if (warp == 1) {
+    for (int blk = 0; blk < blocks; ++blk) {
+      const int sl = blk % slots;
+      mbar_wait(&full[sl], static_cast<uint32_t>(blk / slots) & 1u);
+      tc_fence_after();
+      if (epi_ld) {
+        uint32_t r[32];
+        tmem_ld32_raw(tmem + 128u + static_cast<uint32_t>(sl * 96), r);
+        tmem_ld_wait();
+        if (r[0] == 0x12345678u && r[31] == 7u) out[1] = r[1];  // keep the load
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (threadIdx.x == 32) mbar_arrive(&empty[sl]);
+    }
+    if (threadIdx.x == 32) mbar_arrive(&done);
   }
   __syncthreads();
   if (threadIdx.x < 32) tmem_dealloc(tmem, 512);
@@ -532,6 +625,28 @@ int main() {
         cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
         std::printf("split pattern N=%d operands=%s: %6.1f clk/MMA %s\n", N, rf ? "random" : "zero",
                     double(c) / 504, cudaGetErrorString(cudaGetLastError()));
+      }
+    cudaFuncSetAttribute(rate_ring, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    for (int slots : {2, 3, 4})
+      for (int ld = 0; ld < 2; ++ld) {
+        unsigned long long* d2;
+        cudaMalloc(&d2, 16);
+        rate_ring<<<148, 128, 100 * 1024>>>(1200, slots, ld, d2);
+        unsigned long long c = 0;
+        cudaMemcpy(&c, d2, 8, cudaMemcpyDeviceToHost);
+        std::printf("ring slots=%d epilogue_ld=%d: %6.1f clk/MMA %s\n", slots, ld, double(c) / 1200,
+                    cudaGetErrorString(cudaGetLastError()));
+        cudaFree(d2);
+      }
+    for (int threads : {128, 480})
+      for (int idle = 0; idle < 6; ++idle) {
+        if (threads == 128 && idle && idle < 3) continue;
+        rate_split<<<148, threads, 100 * 1024>>>(96, 504, 1, d, 0, 0, 1, idle);
+        unsigned long long c = 0;
+        cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
+        std::printf("split N=96 threads=%d idle=%s: %6.1f clk/MMA %s\n", threads,
+                    idle == 0 ? "exit" : idle == 1 ? "sleep-wait" : idle == 2 ? "spin-wait" : idle == 3 ? "rotating A" : idle == 4 ? "slot ring" : "ring+commit", double(c) / 504,
+                    cudaGetErrorString(cudaGetLastError()));
       }
     for (int dcol : {0, 96, 256, 352})
       for (int boff : {0, 128, 512}) {
