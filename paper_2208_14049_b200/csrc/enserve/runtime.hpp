@@ -6,10 +6,16 @@
 // by device work:
 //   * one persistent member kernel per nonzero cell (worker), on its own CUDA
 //     stream, walking its share of the segments tile by tile (tile = the
-//     worker's batch b, the batcher split of pipeline.cpp:155-162);
+//     worker's batch b, the batcher split of pipeline.cpp:155-162); a
+//     data-parallel model's workers pop their segments off one device
+//     counter (the per-model queue of pipeline.cpp:44-51) or split them
+//     statically;
 //   * per-model logits land directly at their row offset in a [nb x C] buffer on
-//     the combining device (peer copy when the worker sits on another GPU);
-//   * one K3 combine launch folds all members in model-id order.
+//     the combining device (a remote worker's kernels store them over NVLink
+//     peer mappings, or stage + peer-copy);
+//   * one K3 combine launch folds all members in model-id order; with one
+//     process per GPU, an NCCL gather then brings every rank's rows to the
+//     root (the single accumulator of pipeline.cpp:258-279).
 // The timed window is the reference's (broadcast -> last fold,
 // pipeline.cpp:309 / :268-269), measured with CUDA events on the combining
 // device; X upload happens in begin_run, untimed, as in pipeline.cpp:285-302.
