@@ -163,3 +163,34 @@ def test_tiny_and_empty_stores_through_every_new_path(nb):
     assert fp.combined.shape == (nb, 10)
     if nb:
         assert np.abs(fp.combined - ref.combined).max() < 2e-3  # bf16 vs fp32 members
+
+
+@pytest.mark.parametrize("single", [False, True], ids=["dense_pair", "dense_single"])
+def test_wide_member_dense_head_follows_claims(single, monkeypatch):
+    """The dense schedules -- a hidden layer too wide for a fused head
+    (784 -> 4096 -> 10: dense hidden layer + dense logits layer), on SM pairs
+    or, with ES_DENSE_KERNEL=single, one SM -- also follow a claimed run:
+    data-parallel over two rows they give the one-worker bits."""
+    if single:
+        monkeypatch.setenv("ES_DENSE_KERNEL", "single")
+    roster = [("wide", "mlp", [784, 4096, 10], 91), ("mlp256", "mlp", [784, 256, 10], 92)]
+    c1 = bench.make_cluster(es, {"roster": roster, "devices": 1, "device_mib": 183359.0})
+    c2 = bench.make_cluster(es, {"roster": roster, "devices": 2, "device_mib": 183359.0})
+    X = es.SampleStore(refcpu.features(75, 128 * 37 + 9, 784))
+    single_out = es.run_inference(X, es.AllocationMatrix.from_array([[128, 128]]), c1, RULE)
+    A = es.AllocationMatrix.from_array([[128, 128], [64, 32]])
+    with es.InferenceSystem(A, c2, RULE, device_map=[0, 0], row_nodes=True, dp_claim=True,
+                            claim_chunk=3) as s:
+        out = s.run(X)
+        assert s.claim_models() == [0, 1]
+        assert_exactly_once(s.claims(0), workers_of(A, 0), 38)
+    np.testing.assert_array_equal(out.combined, single_out.combined)
+    cpu = refcpu.CpuMlp([784, 4096, 10], 91)
+    Xh = refcpu.features(75, 128 * 37 + 9, 784)
+    z = es.run_inference(es.SampleStore(Xh), es.AllocationMatrix.from_array([[128]]),
+                         bench.make_cluster(es, {"roster": roster[:1], "devices": 1,
+                                                 "device_mib": 183359.0}),
+                         es.CombinationRule.averaging()).combined
+    want = cpu.forward(Xh)
+    s_ = cpu.logit_scale(Xh)
+    assert (np.abs(z - want) / np.maximum(s_, 1e-6)).max() <= 1e-3
