@@ -389,6 +389,140 @@ __global__ void __launch_bounds__(128, 1) rate_ring(int reps, int slots, int epi
   if (threadIdx.x < 32) tmem_dealloc(tmem, 512);
 }
 
+// The conv kernel's two-chain structure without its data: per tile, warp 1
+// issues conv1 (2 UMMAs M=128 N=64) into ONE TMEM buffer (c1_full commit,
+// waits c1_empty); an "epi1" warp waits c1_full, arrives c1_empty at once,
+// waits a2_empty[t % nbuf_a2] and arrives a2_full[t % nbuf_a2]; warp 0
+// (conv2) waits a2_full, issues 2 blocks x 12 UMMAs (N=96) into a 3-slot ring
+// (c2_full per block, commits a2_empty after the tile); an "epi2" warp
+// releases the slots.  mode bit 0: conv1 issued by warp 0 right before
+// conv2 of the previous tile instead of by warp 1.
+__global__ void __launch_bounds__(384, 1) rate_chain(int tiles, int mode, unsigned long long* out) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align_smem_1024(smem_raw);
+  __shared__ uint64_t c1f, c1e, c1e8, a2f[2], a2e[2], c2f[3], c2e[3], done;
+  __shared__ uint32_t slot;
+  for (int i = threadIdx.x; i < 96 * 1024 / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+  if (threadIdx.x == 0) {
+    mbar_init(&c1f, 1);
+    mbar_init(&c1e, 1);
+    mbar_init(&c1e8, 8);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&a2f[i], 1);
+      mbar_init(&a2e[i], 1);
+    }
+    for (int i = 0; i < 3; ++i) {
+      mbar_init(&c2f[i], 1);
+      mbar_init(&c2e[i], 1);
+    }
+    mbar_init(&done, 1);
+    fence_barrier_init();
+  }
+  if (threadIdx.x < 32) tmem_alloc(&slot, 512);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
+  const uint32_t a = smem_u32(smem), b = smem_u32(smem + 40 * 1024);
+  const uint32_t id1 = idesc_bf16_f32(128, 64), id2 = idesc_bf16_f32(128, 96);
+  const uint64_t ad0 = sdesc_planar(a + 16 * 16, 4608), bd0 = sdesc_planar(b, 96 * 16);
+  const uint64_t a1d = sdesc_planar(a + 60 * 1024, 4096), w1d = sdesc_planar(b + 40 * 1024, 64 * 16);
+  const bool fused = mode & 1;
+  auto conv1 = [&](int t) {
+    mbar_wait(&c1e, (static_cast<uint32_t>(t) & 1u) ^ 1u);
+    tc_fence_after();
+    for (int mb = 0; mb < 2; ++mb)
+      if (elect_one()) umma_bf16(tmem + static_cast<uint32_t>(mb * 64), a1d + mb * 128, w1d, id1, 0);
+    if (elect_one()) umma_commit(&c1f);
+    __syncwarp();
+  };
+  if (warp == 0) {
+    const long long t0 = clock64();
+    if (fused) conv1(0);
+    for (int t = 0; t < tiles; ++t) {
+      if (fused && t + 1 < tiles) conv1(t + 1);
+      const int ab = t & 1;
+      mbar_wait(&a2f[ab], static_cast<uint32_t>(t >> 1) & 1u);
+      tc_fence_after();
+      for (int mb = 0; mb < 2; ++mb) {
+        const int blk = t * 2 + mb, sl = blk % 3;
+        mbar_wait(&c2e[sl], (static_cast<uint32_t>(blk / 3) & 1u) ^ 1u);
+        tc_fence_after();
+        const uint32_t d = tmem + 128u + static_cast<uint32_t>(sl * 96);
+#pragma unroll
+        for (int dwi = 0; dwi < 3; ++dwi)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint64_t ad = ad0 + static_cast<uint64_t>(mb * 128 + (dwi - 1) * 8 - 1 + j * 576);
+            const uint64_t bd = bd0 + static_cast<uint64_t>((dwi * 4 + j) * 2 * 96);
+            if (elect_one()) umma_bf16(d, ad, bd, id2, (dwi | j) != 0);
+          }
+        if (elect_one()) {
+          umma_commit(&c2f[sl]);
+          if (mb == 1) umma_commit(&a2e[ab]);
+        }
+        __syncwarp();
+      }
+    }
+    mbar_wait(&done, 0);
+    if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = static_cast<unsigned long long>(clock64() - t0);
+  } else if (warp == 1) {
+    if (!fused)
+      for (int t = 0; t < tiles; ++t) conv1(t);
+  } else if (warp == 2 || warp >= 4) {  // epi1 (mode bit 2: 8 warps that tcgen05.ld conv1's TMEM)
+    const bool ld = mode & 4;
+    if (warp >= 4 && !ld) {
+      // idle
+    } else {
+    for (int t = 0; t < tiles; ++t) {
+      mbar_wait(&c1f, static_cast<uint32_t>(t) & 1u);
+      tc_fence_after();
+      if (ld && warp >= 4) {
+        const int ew = warp - 4, q = warp & 3;
+        uint32_t v0[32], v1[32];
+        const uint32_t base = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>((ew >> 2) * 32);
+        tmem_ld32_raw(base, v0);
+        tmem_ld32_raw(base + 64u, v1);
+        tmem_ld_wait();
+        if (v0[3] == 0x7fffffffu && v1[5] == 3u) out[1] = v0[0];
+      }
+      tc_fence_before();
+      if (ld) {
+        // c1 buffer released by the 8 loading warps (count 8 via lane 0 of each)
+        if (warp >= 4 && (threadIdx.x & 31) == 0) mbar_arrive(&c1e8);
+      } else if (threadIdx.x == 64) {
+        mbar_arrive(&c1e);
+      }
+      if (warp >= 4) continue;
+      const int ab = t & 1;
+      mbar_wait(&a2e[ab], (static_cast<uint32_t>(t >> 1) & 1u) ^ 1u);
+      if (ld) mbar_wait(&c1e8, static_cast<uint32_t>(t) & 1u);  // the loads are done
+      if (mode & 2) {  // the kernel's generic -> async proxy fence before the hand-off
+        reinterpret_cast<volatile uint32_t*>(smem + 60 * 1024)[threadIdx.x] = t;
+        fence_proxy_async_smem();
+      }
+      if (threadIdx.x == 64) {
+        if (ld) mbar_arrive(&c1e);
+        mbar_arrive(&a2f[ab]);
+      }
+    }
+    }
+  } else if (warp == 3) {  // epi2
+    for (int blk = 0; blk < 2 * tiles; ++blk) {
+      const int sl = blk % 3;
+      mbar_wait(&c2f[sl], static_cast<uint32_t>(blk / 3) & 1u);
+      tc_fence_before();
+      if (threadIdx.x == 96) mbar_arrive(&c2e[sl]);
+    }
+    if (threadIdx.x == 96) mbar_arrive(&done);
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) tmem_dealloc(tmem, 512);
+}
+
 __device__ __forceinline__ void tshift(uint32_t taddr) {
   asm volatile("tcgen05.shift.cta_group::1.down [%0];" ::"r"(taddr) : "memory");
 }
@@ -626,6 +760,19 @@ int main() {
         std::printf("split pattern N=%d operands=%s: %6.1f clk/MMA %s\n", N, rf ? "random" : "zero",
                     double(c) / 504, cudaGetErrorString(cudaGetLastError()));
       }
+    cudaFuncSetAttribute(rate_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    for (int mode : {0, 1, 4, 5}) {
+      unsigned long long* d3;
+      cudaMalloc(&d3, 16);
+      rate_chain<<<148, 384, 100 * 1024>>>(200, mode, d3);
+      unsigned long long c = 0;
+      cudaMemcpy(&c, d3, 8, cudaMemcpyDeviceToHost);
+      std::printf("chain mode=%d (%s%s): %6.1f clk per tile (%5.1f per conv2 UMMA) %s\n", mode,
+                  (mode & 1) ? "conv1 from the conv2 issuer" : "conv1 from its own warp",
+                  (mode & 4) ? ", 8 epi1 warps tcgen05.ld conv1" : "", double(c) / 200,
+                  double(c) / 200 / 24, cudaGetErrorString(cudaGetLastError()));
+      cudaFree(d3);
+    }
     cudaFuncSetAttribute(rate_ring, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
     for (int slots : {2, 3, 4})
       for (int ld = 0; ld < 2; ++ld) {
