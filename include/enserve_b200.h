@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define ES_ABI_VERSION 1
+#define ES_ABI_VERSION 2  /* 2: es_pool_opts and es_model_desc grew (multi-GPU, device FIFO, fp32, B200 cost fit) */
 #define ES_MAX_WIDTHS 9
 
 /* Error classes of include/enserve/core/errors.hpp:9-51, plus device errors. */

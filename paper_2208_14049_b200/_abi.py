@@ -18,6 +18,10 @@ c_int32_p = C.POINTER(C.c_int32)
 c_size_t_p = C.POINTER(C.c_size_t)
 
 
+# include/enserve_b200.h ES_ABI_VERSION: the struct layouts below.
+ABI_VERSION = 2
+
+
 class DeviceDesc(C.Structure):
     _fields_ = [("kind", C.c_int), ("memory_mib", C.c_double), ("compute_rate", C.c_double),
                 ("batch_overhead_s", C.c_double)]
@@ -226,7 +230,7 @@ def lib() -> C.CDLL:
             fn = getattr(handle, name)
             fn.restype = res
             fn.argtypes = args
-        if handle.es_abi_version() != 1:
+        if handle.es_abi_version() != ABI_VERSION:
             raise ImportError("libenserve_b200.so ABI version mismatch")
         _lib = handle
     return _lib
