@@ -46,7 +46,7 @@ def test_library_is_built_for_sm100a_with_tcgen05_and_tma():
 
 def test_abi_version_and_status_names():
     lib = es.lib()
-    assert lib.es_abi_version() == 1
+    assert lib.es_abi_version() == es._abi.ABI_VERSION == 2
     assert lib.es_status_name(4) == b"ES_ERR_STARTUP"
 
 
