@@ -67,6 +67,12 @@ __device__ __forceinline__ void epi_barrier() {
   asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
 }
 
+// HPC: the hidden units per pass as a compile-time constant (0 = runtime
+// L.HP).  Layer 2's 2 * HP/32 UMMAs then issue from a fully unrolled loop
+// with constant TMEM / descriptor offsets: with runtime offsets the issuing
+// thread, not the tensor pipe, paced them (tools/umma_contention.cu
+// layer2_rate: ~230 vs ~100 clk per N = 16 UMMA).
+template <int HPC>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     member_mlp2_pair_sm100(const __grid_constant__ CUtensorMap tm_x,
                            const __grid_constant__ CUtensorMap tm_w1,
@@ -90,7 +96,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int warp = warp_uniform_id();
   const int lane = threadIdx.x & 31;
   const int H = L.H;    // all hidden units (W2 columns, biases)
-  const int HP = L.HP;  // hidden units per pass (TMEM-resident at a time)
+  const int HP = HPC ? HPC : L.HP;  // hidden units per pass (TMEM-resident at a time)
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
   const Tiles ts = tile_space(args);
@@ -199,14 +205,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         // bases keep the single issuing thread at a few ALU ops per UMMA.
         const uint64_t w2d = sdesc_k128(sW2_addr);
         const uint32_t pmask = static_cast<uint32_t>(L.d2_parts - 1);  // parts: 1 or 4
-        uint32_t step = 0;
-        for (int hh = 0; hh < 2; ++hh)
-          for (int kk = 0; kk < HP / 32; ++kk, ++step) {  // 16 hidden units per step
-            const uint32_t h0 = static_cast<uint32_t>(pend_hp * HP + hh * (HP / 2) + kk * 16);
-            const uint32_t a = tile + static_cast<uint32_t>(hh * (HP / 2) + kk * 8);
-            const uint64_t b = w2d + (h0 >> 6) * 64u + (h0 & 63u) / 8u;
-            if (elect_one()) umma_bf16_pair_ta(d2 + 16u * (step & pmask), a, b, idesc2, step > pmask);
+        if constexpr (HPC != 0) {
+          // pend_hp * HPC is a multiple of 64 hidden units: one runtime add.
+          const uint64_t w2p = w2d + static_cast<uint64_t>(pend_hp * HPC / 64) * 64u;
+#pragma unroll
+          for (int step = 0; step < HPC / 16; ++step) {  // 16 hidden units per step
+            const int hh = step / (HPC / 32), kk = step % (HPC / 32);
+            const uint32_t h0 = static_cast<uint32_t>(hh * (HPC / 2) + kk * 16);
+            const uint32_t a = tile + static_cast<uint32_t>(hh * (HPC / 2) + kk * 8);
+            const uint64_t b = w2p + (h0 >> 6) * 64u + (h0 & 63u) / 8u;
+            if (elect_one())
+              umma_bf16_pair_ta(d2 + 16u * (static_cast<uint32_t>(step) & pmask), a, b, idesc2,
+                                static_cast<uint32_t>(step) > pmask);
           }
+        } else {
+          uint32_t step = 0;
+          for (int hh = 0; hh < 2; ++hh)
+            for (int kk = 0; kk < HP / 32; ++kk, ++step) {  // 16 hidden units per step
+              const uint32_t h0 = static_cast<uint32_t>(pend_hp * HP + hh * (HP / 2) + kk * 16);
+              const uint32_t a = tile + static_cast<uint32_t>(hh * (HP / 2) + kk * 8);
+              const uint64_t b = w2d + (h0 >> 6) * 64u + (h0 & 63u) / 8u;
+              if (elect_one()) umma_bf16_pair_ta(d2 + 16u * (step & pmask), a, b, idesc2, step > pmask);
+            }
+        }
         if (elect_one()) umma_commit_pair(&acc2_full[k], kBoth);
         if (k == 0) TRACE(pend_g, 9);
       };
@@ -440,14 +461,20 @@ int mlpp_launch(const MlpPArgs& args, const void* x, const void* w1, const void*
     return -1;
   if (make_bf16_map(&mw2, w2, static_cast<uint64_t>(L.H), static_cast<uint64_t>(L.C), 8) != 0)
     return -1;
-  if (ensure_smem_attr(member_mlp2_pair_sm100, static_cast<int>(kSmemBudget)) != 0) return -4;
+  auto kernel = L.HP == 128   ? member_mlp2_pair_sm100<128>
+                : L.HP == 256 ? member_mlp2_pair_sm100<256>
+                : L.HP == 384 ? member_mlp2_pair_sm100<384>
+                : L.HP == 512 ? member_mlp2_pair_sm100<512>
+                              : member_mlp2_pair_sm100<0>;
+  if (std::getenv("ES_PAIR_RUNTIME_HP")) kernel = member_mlp2_pair_sm100<0>;  // A/B probe
+  if (ensure_smem_attr(kernel, static_cast<int>(kSmemBudget)) != 0) return -4;
   const long long per_seg = (args.seg_size + args.b - 1) / args.b;
   const long long tiles = (args.seg_end - args.seg_begin) * per_seg;
   if (tiles <= 0) return 0;
   const long long pair_groups = (tiles + 2LL * L.T - 1) / (2LL * L.T);
   grid = static_cast<int>(std::min<long long>(grid / 2, pair_groups)) * 2;
   if (grid < 2) grid = 2;
-  member_mlp2_pair_sm100<<<grid, kThreads, L.smem_bytes, stream>>>(mx, mw1, mw2, args);
+  kernel<<<grid, kThreads, L.smem_bytes, stream>>>(mx, mw1, mw2, args);
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 

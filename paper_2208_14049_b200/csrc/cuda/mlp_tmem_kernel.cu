@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "mlp_tmem_kernel.cuh"
 #include "batching.cuh"
@@ -46,6 +47,10 @@ __device__ __forceinline__ void epi_barrier() {
   asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
 }
 
+// HC: the hidden width as a compile-time constant (0 = runtime L.H), so
+// layer 2's H/16 UMMAs issue from a fully unrolled loop with constant
+// offsets (mlp_pair_kernel.cu: the issuing thread, not the pipe, paced them).
+template <int HC>
 __global__ void __launch_bounds__(kThreads, 1)
     member_mlp2_tmem_sm100(const __grid_constant__ CUtensorMap tm_x,
                            const __grid_constant__ CUtensorMap tm_w1,
@@ -68,7 +73,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = warp_uniform_id();
   const int lane = threadIdx.x & 31;
-  const int H = L.H;
+  const int H = HC ? HC : L.H;
   const Tiles ts = tile_space(args);
 
   if (threadIdx.x == 0) {
@@ -164,14 +169,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         // bases keep the single issuing thread at a few ALU ops per UMMA.
         const uint64_t w2d = sdesc_k128(sW2_addr);
         const uint32_t pmask = static_cast<uint32_t>(L.d2_parts - 1);  // parts: 1 or 4
-        uint32_t step = 0;
-        for (int hh = 0; hh < 2; ++hh)
-          for (int kk = 0; kk < H / 32; ++kk, ++step) {  // 16 hidden units per step
-            const uint32_t h0 = static_cast<uint32_t>(hh * (H / 2) + kk * 16);
-            const uint32_t a = tile + static_cast<uint32_t>(hh * (H / 2) + kk * 8);
+        if constexpr (HC != 0) {
+#pragma unroll
+          for (int step = 0; step < HC / 16; ++step) {  // 16 hidden units per step
+            const int hh = step / (HC / 32), kk = step % (HC / 32);
+            const uint32_t h0 = static_cast<uint32_t>(hh * (HC / 2) + kk * 16);
+            const uint32_t a = tile + static_cast<uint32_t>(hh * (HC / 2) + kk * 8);
             const uint64_t b = w2d + (h0 >> 6) * 128u + (h0 & 63u) / 8u;
-            if (elect_one()) umma_bf16_ta(d2 + 16u * (step & pmask), a, b, idesc2, step > pmask);
+            if (elect_one())
+              umma_bf16_ta(d2 + 16u * (static_cast<uint32_t>(step) & pmask), a, b, idesc2,
+                           static_cast<uint32_t>(step) > pmask);
           }
+        } else {
+          uint32_t step = 0;
+          for (int hh = 0; hh < 2; ++hh)
+            for (int kk = 0; kk < H / 32; ++kk, ++step) {  // 16 hidden units per step
+              const uint32_t h0 = static_cast<uint32_t>(hh * (H / 2) + kk * 16);
+              const uint32_t a = tile + static_cast<uint32_t>(hh * (H / 2) + kk * 8);
+              const uint64_t b = w2d + (h0 >> 6) * 128u + (h0 & 63u) / 8u;
+              if (elect_one()) umma_bf16_ta(d2 + 16u * (step & pmask), a, b, idesc2, step > pmask);
+            }
+        }
         if (elect_one()) umma_commit(&acc2_full[k]);
       };
       auto drain_pending = [&]() {
@@ -383,12 +401,18 @@ int mlpt_launch(const MlpTArgs& args, const void* x, const void* w1, const void*
     return -1;
   if (make_bf16_map(&mw2, w2, static_cast<uint64_t>(L.H), static_cast<uint64_t>(L.C), 16) != 0)
     return -1;
-  if (ensure_smem_attr(member_mlp2_tmem_sm100, static_cast<int>(kSmemBudget)) != 0) return -4;
+  auto kernel = L.H == 128   ? member_mlp2_tmem_sm100<128>
+                : L.H == 256 ? member_mlp2_tmem_sm100<256>
+                : L.H == 384 ? member_mlp2_tmem_sm100<384>
+                : L.H == 512 ? member_mlp2_tmem_sm100<512>
+                             : member_mlp2_tmem_sm100<0>;
+  if (std::getenv("ES_TMEM_RUNTIME_H")) kernel = member_mlp2_tmem_sm100<0>;  // A/B probe
+  if (ensure_smem_attr(kernel, static_cast<int>(kSmemBudget)) != 0) return -4;
   const long long per_seg = (args.seg_size + args.b - 1) / args.b;
   const long long tiles = (args.seg_end - args.seg_begin) * per_seg;
   if (tiles <= 0) return 0;
   grid = static_cast<int>(std::min<long long>(grid, (tiles + L.T - 1) / L.T));
-  member_mlp2_tmem_sm100<<<grid, kThreads, L.smem_bytes, stream>>>(mx, mw1, mw2, args);
+  kernel<<<grid, kThreads, L.smem_bytes, stream>>>(mx, mw1, mw2, args);
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 

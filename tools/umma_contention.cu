@@ -145,6 +145,82 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
   if (threadIdx.x < 32) tmem_dealloc_pair(tmem, 256);
 }
 
+// Layer 2 of the pair head: M = 256 over the pair, A (bf16 hidden) from
+// TMEM, N = 16, one dependent chain (or `parts` independent chains) -- vs the
+// same UMMAs issued per CTA with cta_group::1 (M = 128 each, both SMs in
+// parallel).
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
+    layer2_rate(int pair_mode, int parts, int reps, unsigned long long* out) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align_smem_1024(smem_raw);
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  for (int i = threadIdx.x; i < 96 * 1024 / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  if (threadIdx.x < 32) {
+    if (pair_mode) tmem_alloc_pair(&slot, 512);
+    else tmem_alloc(&slot, 512);
+  }
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  const bool issuer = pair_mode ? (cluster_ctarank() == 0 && threadIdx.x < 32) : threadIdx.x < 32;
+  if (issuer) {
+    const uint32_t b = smem_u32(smem + 64 * 1024);
+    const uint32_t idesc = idesc_bf16_f32(pair_mode ? 256 : 128, 16);
+    const uint64_t bd = sdesc_k128(b);
+    const long long t0 = clock64();
+    if (parts == 0) {
+      // unrolled: 32 UMMAs per round with compile-time offsets (4 chains)
+      for (int r = 0; r < reps; r += 32) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const uint32_t a = tmem + static_cast<uint32_t>(i * 8);
+          const uint32_t d = tmem + 256u + 16u * static_cast<uint32_t>(i & 3);
+          if (elect_one()) {
+            if (pair_mode) umma_bf16_pair_ta(d, a, bd + (i % 8) * 2, idesc, (r | (i >> 2)) != 0);
+            else umma_bf16_ta(d, a, bd + (i % 8) * 2, idesc, (r | (i >> 2)) != 0);
+          }
+        }
+      }
+    } else {
+      for (int r = 0; r < reps; ++r) {
+        const uint32_t a = tmem + static_cast<uint32_t>((r % 32) * 8);
+        const uint32_t d = tmem + 256u + 16u * static_cast<uint32_t>(r % parts);
+        if (elect_one()) {
+          if (pair_mode) umma_bf16_pair_ta(d, a, bd + (r % 8) * 2, idesc, r >= parts);
+          else umma_bf16_ta(d, a, bd + (r % 8) * 2, idesc, r >= parts);
+        }
+      }
+    }
+    if (elect_one()) {
+      if (pair_mode) umma_commit_pair(&bar, 3);
+      else umma_commit(&bar);
+    }
+    __syncwarp();
+    mbar_wait(&bar, 0);
+    const long long t1 = clock64();
+    if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = static_cast<unsigned long long>(t1 - t0);
+  } else if (pair_mode && threadIdx.x == 0) {
+    mbar_wait_cluster(&bar, 0);
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  if (threadIdx.x < 32) {
+    if (pair_mode) tmem_dealloc_pair(tmem, 512);
+    else tmem_dealloc(tmem, 512);
+  }
+}
+
 int main() {
   unsigned long long* d;
   cudaMalloc(&d, 16);
@@ -166,6 +242,16 @@ int main() {
                     (128.0 * 32 + N * 32.0) * reps / double(h[0]), double(h[1]) / double(kWindow),
                     cudaGetErrorString(cudaGetLastError()));
       }
+  cudaFuncSetAttribute(layer2_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  for (int pm = 0; pm < 2; ++pm)
+    for (int parts : {0, 1, 4}) {
+      layer2_rate<<<148, 128, 100 * 1024>>>(pm, parts, 512, d);
+      unsigned long long c = 0;
+      cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
+      std::printf("layer2 %s N=16 A=tmem parts=%d (0 = unrolled, constant offsets): %6.1f clk/MMA %s\n",
+                  pm ? "pair M=256 (cta_group::2)" : "per CTA M=128 (cta_group::1)", parts,
+                  double(c) / 512, cudaGetErrorString(cudaGetLastError()));
+    }
   cudaFuncSetAttribute(pair_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
   for (int N : {64, 96, 128, 192, 256}) {
     pair_rate<<<148, 128, 100 * 1024>>>(N, reps, d);
