@@ -1,0 +1,596 @@
+// Samples-in-M CNN-s convolution stack (design in conv_rows_kernel.cuh).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+
+#include "conv_rows_kernel.cuh"
+#include "sm100.cuh"
+#include "tma_host.hpp"
+
+namespace es {
+
+using namespace sm100;
+
+namespace {
+
+constexpr int kS = 28, kG = 7, kC1 = 64, kC2 = 32, kTile = 128;
+constexpr int kOutRow = kG * kG * kC2;  // bf16 elements per output sample
+constexpr int kThreads = 480;           // 15 warps: 2 im2col builders (warp 0 also TMA),
+                                        // the UMMA issuer, 2 x 4 conv1 epilogue,
+                                        // 4 output drain
+constexpr int kBuilders = 2;
+constexpr int kLead = 2;  // conv1 of a position is issued kLead windows before its first use
+
+// Production order of a strip's positions (builder, conv1, epilogue): input
+// rows 0 and 1 interleaved by column, then rows 2..6 -- so the window that
+// first needs a position is non-decreasing along it.  Window index (within
+// the tile: strip A windows 0..34, strip B 35..62) that first reads the
+// position at local index i (strip A 0..34, strip B 35..62):
+__host__ __device__ constexpr int first_window(int i) {
+  return i < 35 ? (i < 10 ? i / 2 : i - 5) : (i < 43 ? 35 + (i - 35) / 2 : i - 4);
+}
+// (input row, strip column) of local position i.
+__host__ __device__ constexpr int pos_row(int i) {
+  return i < 35 ? (i < 10 ? i & 1 : 2 + (i - 10) / 5) : (i < 43 ? (i - 35) & 1 : 2 + (i - 43) / 4);
+}
+__host__ __device__ constexpr int pos_col(int i) {
+  return i < 35 ? (i < 10 ? i / 2 : (i - 10) % 5) : (i < 43 ? (i - 35) / 2 : (i - 43) % 4);
+}
+
+// Shared memory (offsets from the 1024-aligned base).
+constexpr uint32_t kSlotBytes = 16384;  // A2 smem slot: [128 samples][64 ch] bf16, SW128
+constexpr int kSmemSlots = 7;
+constexpr uint32_t kOffW2 = kSmemSlots * kSlotBytes;  // [dh][ks][plane][96 rows][16 B]
+constexpr uint32_t kW2Plane = 96 * 16;
+constexpr uint32_t kOffW1 = kOffW2 + 3 * 4 * 2 * kW2Plane;  // [plane][64 c][16 B]
+constexpr uint32_t kOffA1 = kOffW1 + 2 * 64 * 16;           // im2col ring: [2 planes][128][16 B]
+constexpr uint32_t kA1Bytes = 2 * 128 * 16;
+constexpr int kA1Stages = 3;
+// x staging: half patch rows (image rows 4 ih + 2 h, +1 = 56 contiguous
+// pixels) of the tile's 128 samples, one TMA box each (112-byte runs).
+constexpr uint32_t kOffX = kOffA1 + kA1Stages * kA1Bytes;
+constexpr uint32_t kXHalf = 128 * 56 * 2;
+constexpr int kXRows = 2;  // patch rows in flight (the next one loads while this one is built)
+constexpr uint32_t kOffBar = kOffX + kXRows * 2 * kXHalf;
+constexpr int kNumBars = 2 * kXRows + kA1Stages * 2 + 2 + 2 + 15 + 15 + 4 + 4;
+constexpr uint32_t kSmemBytes = kOffBar + kNumBars * 8 + 16 + 1024;
+
+// TMEM columns: output-row accumulator O (4 blocks of 32), two conv1
+// accumulators of 64, eight A2 slots of 32 (64 bf16 channels packed in pairs).
+constexpr uint32_t kTmO = 0, kTmD1 = 128, kTmA2 = 256;
+
+// A2 slot of (strip column j = iw - first column, input-row phase p).  A UMMA
+// reading A from smem costs max(N/2, (4096 + 32 N)/128) clk and takes the
+// smem bandwidth the builder and epilogue also need; from TMEM N/2
+// (tools/conv_probe.cu).  TMEM holds 8 of the 15 slots: columns 0 and 3
+// (narrow windows) and column 4 (N = 32, strip A only) at phases 0 and 1;
+// shared memory the rest.  Slot id (barriers) = 3 j + p.
+__host__ __device__ constexpr bool slot_tmem(int j, int p) { return j == 0 || j == 3 || (j == 4 && p < 2); }
+__host__ __device__ constexpr int slot_index(int j, int p) {  // within its memory
+  return slot_tmem(j, p) ? (j == 0 ? p : j == 3 ? 3 + p : 6 + p) : (j == 1 ? p : j == 2 ? 3 + p : 6);
+}
+
+// bf16x2 {relu(a + ba), relu(b + bb)} (a in the low half), one cvt.relu.
+__device__ __forceinline__ uint32_t pack_relu_bf16(uint32_t a, uint32_t b, float ba, float bb) {
+  const float lo = __uint_as_float(a) + ba;
+  const float hi = __uint_as_float(b) + bb;
+  uint32_t d;
+  asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+  return d;
+}
+
+// Stamp event `kind` number i (CTA 0 only, tools/trace_rows.cu).
+#define TRACE(kind, i)                                                                      \
+  do {                                                                                      \
+    if (trace && (i) < 256) trace[(kind) * 256 + (i)] = static_cast<unsigned long long>(clock64()); \
+  } while (0)
+
+struct Bars {
+  uint64_t* x_full;    // [kXRows] TMA -> im2col builders (one patch row, both halves)
+  uint64_t* x_empty;   // [kXRows] builders -> TMA
+  uint64_t* a1_full;   // [3] builder -> conv1 issuer
+  uint64_t* a1_empty;  // [3]
+  uint64_t* c1_full;   // [2] conv1 issuer -> epilogue group of that D slot
+  uint64_t* c1_empty;  // [2]
+  uint64_t* a2_full;   // [15] conv1 epilogue -> conv2 issuer
+  uint64_t* a2_empty;  // [15]
+  uint64_t* o_full;    // [4] conv2 issuer -> drain
+  uint64_t* o_empty;   // [4]
+};
+
+// ------------------------------------------------------------ conv2 issuer
+struct IssueCtx {
+  uint32_t tbase;
+  uint64_t a2d;  // SW128 descriptor of A2 smem slot 0
+  uint64_t w2d;  // planar descriptor of W2
+  Bars b;
+  uint32_t a2par;  // per slot id: parity of the next fill to wait for
+  uint32_t ouse;   // per O block: parity of its first-touch count
+  unsigned long long* trace;
+  long long w;  // running window index
+  // conv1 feed: next position, total, operand bases
+  long long c1n, npos;
+  uint32_t a1_base;
+  uint64_t w1d;
+};
+
+// Issue conv1 for every position whose first window is <= w + kLead, in
+// production order; ahead of need only if its operand and accumulator are
+// already free (never stall the conv2 stream for work not due yet).
+__device__ __forceinline__ void feed_conv1(IssueCtx& c) {
+  constexpr uint32_t id1 = idesc_bf16_f32(128, kC1);
+  while (c.c1n < c.npos) {
+    const long long n = c.c1n;
+    const long long due = (n / 63) * 63 + first_window(static_cast<int>(n % 63));
+    if (due > c.w + kLead) break;
+    const int sl = static_cast<int>(n % kA1Stages), dsl = static_cast<int>(n & 1);
+    const uint32_t pa = static_cast<uint32_t>(n / kA1Stages) & 1u;
+    const uint32_t pd = (static_cast<uint32_t>(n >> 1) & 1u) ^ 1u;
+    if (due > c.w) {
+      if (!mbar_test(&c.b.a1_full[sl], pa) || !mbar_test(&c.b.c1_empty[dsl], pd)) break;
+    } else {
+      mbar_sleep_wait(&c.b.a1_full[sl], pa);
+      mbar_sleep_wait(&c.b.c1_empty[dsl], pd);
+    }
+    tc_fence_after();
+    if (elect_one()) {
+      umma_bf16(c.tbase + kTmD1 + 64u * dsl, sdesc_planar(c.a1_base + sl * kA1Bytes, 2048), c.w1d,
+                id1, 0);
+      umma_commit(&c.b.c1_full[dsl]);
+      umma_commit(&c.b.a1_empty[sl]);
+    }
+    __syncwarp();
+    ++c.c1n;
+  }
+}
+
+// D (+)= A2(slot of column J, phase p) x W2(dh, ks, blocks jlo..jlo+n-1).
+template <int J, int NB, int P>
+__device__ __forceinline__ void mma2(const IssueCtx& c, uint32_t d, int dh, int ks, int jlo,
+                                     uint32_t acc) {
+  constexpr uint32_t p = P;
+  constexpr uint32_t idesc = idesc_bf16_f32(128, 32 * NB);
+  const uint64_t bd = c.w2d + static_cast<uint64_t>(((dh * 4 + ks) * 2 * kW2Plane + jlo * 32 * 16) >> 4);
+  auto tm = [&](uint32_t t) {
+    if (elect_one()) umma_bf16_ta(d, c.tbase + kTmA2 + 32u * t + 8u * ks, bd, idesc, acc);
+  };
+  auto sm = [&](uint32_t t) {
+    if (elect_one())
+      umma_bf16(d, c.a2d + static_cast<uint64_t>(t * (kSlotBytes >> 4) + 2u * ks), bd, idesc, acc);
+  };
+  if constexpr (J == 0 || J == 3) {
+    tm((J == 0 ? 0u : 3u) + p);
+  } else if constexpr (J == 4) {
+    if constexpr (P < 2) tm(6u + p);
+    else sm(6u);
+  } else {
+    sm((J == 1 ? 0u : 3u) + p);
+  }
+}
+
+__device__ __forceinline__ void wait_slot(IssueCtx& c, uint32_t sid) {
+  mbar_sleep_wait(&c.b.a2_full[sid], (c.a2par >> sid) & 1u);
+  c.a2par ^= 1u << sid;
+}
+
+// Window IW of strip ST for output row oh, whose input row has phase P1: the
+// phases (slot addresses) are template arguments, so every operand address is
+// a constant offset from a uniform base (a run-time phase cost an R2UR per UMMA
+// and ~40 clk of issue each).
+template <int ST, int IW, int P1>
+__device__ __forceinline__ void window(IssueCtx& c, int oh) {
+  constexpr uint32_t p1 = P1, p0 = (P1 + 2) % 3, p2 = (P1 + 1) % 3;
+  constexpr int c0 = ST ? 3 : 0, ow0 = ST ? 4 : 0, nout = ST ? 3 : 4, iwl = ST ? 6 : 4;
+  constexpr int J = IW - c0;
+  constexpr int owlo = IW - 1 > ow0 ? IW - 1 : ow0;
+  constexpr int owhi = IW + 1 < ow0 + nout - 1 ? IW + 1 : ow0 + nout - 1;
+  constexpr int jlo = owlo - IW + 1, NB = owhi - owlo + 1, dblk = owlo - ow0;
+  constexpr bool all_new = IW == c0;
+  constexpr bool last_new = !all_new && owhi == IW + 1;
+  unsigned long long* trace = c.trace;
+  TRACE(6, static_cast<int>(c.w));
+  feed_conv1(c);
+  // new input positions: (0, IW) and (1, IW) at the first row, else (oh+1, IW)
+  if (oh == 0) wait_slot(c, 3u * J + p1);
+  if (oh < kG - 1) wait_slot(c, 3u * J + p2);
+  // first touches of O blocks in this output row
+#pragma unroll
+  for (int b = dblk; b < dblk + NB; ++b)
+    if (all_new || (last_new && b == dblk + NB - 1)) {
+      mbar_sleep_wait(&c.b.o_empty[b], ((c.ouse >> b) & 1u) ^ 1u);
+      c.ouse ^= 1u << b;
+    }
+  tc_fence_after();
+  TRACE(7, static_cast<int>(c.w));
+  // Opaque per-window copies of the bases: otherwise the compiler hoists all
+  // 36 B descriptors of the strip into uniform registers and spills them.
+  IssueCtx cw = c;
+  asm volatile("" : "+l"(cw.w2d), "+l"(cw.a2d), "+r"(cw.tbase));
+  const uint32_t d = cw.tbase + kTmO + 32u * dblk;
+  // dh = 1 (always valid) first: its K step 0 starts the new blocks.
+  if constexpr (last_new) {  // old blocks accumulate, the new (last) one starts
+    mma2<J, NB - 1, p1>(cw, d, 1, 0, jlo, 1u);
+    mma2<J, 1, p1>(cw, d + 32u * (NB - 1), 1, 0, jlo + NB - 1, 0u);
+  } else {
+    mma2<J, NB, p1>(cw, d, 1, 0, jlo, all_new ? 0u : 1u);
+  }
+#pragma unroll
+  for (int ks = 1; ks < 4; ++ks) mma2<J, NB, p1>(cw, d, 1, ks, jlo, 1u);
+  if (oh > 0) {
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) mma2<J, NB, p0>(cw, d, 0, ks, jlo, 1u);
+  }
+  if (oh < kG - 1) {
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) mma2<J, NB, p2>(cw, d, 2, ks, jlo, 1u);
+  }
+  // releases: input (oh-1, IW) is dead; at the last row (oh, IW) too
+  if (oh > 0 && elect_one()) umma_commit(&c.b.a2_empty[3u * J + p0]);
+  if (oh == kG - 1 && elect_one()) umma_commit(&c.b.a2_empty[3u * J + p1]);
+  // output blocks completed by this window
+  if constexpr (IW - 1 >= ow0 && IW - 1 < ow0 + nout)
+    if (elect_one()) umma_commit(&c.b.o_full[IW - 1 - ow0]);
+  if constexpr (IW == iwl && IW < ow0 + nout)
+    if (elect_one()) umma_commit(&c.b.o_full[IW - ow0]);
+  __syncwarp();
+  TRACE(8, static_cast<int>(c.w));
+  ++c.w;
+}
+
+template <int P>
+__device__ __forceinline__ void strip_a(IssueCtx& c, int oh) {
+  window<0, 0, P>(c, oh);
+  window<0, 1, P>(c, oh);
+  window<0, 2, P>(c, oh);
+  window<0, 3, P>(c, oh);
+  window<0, 4, P>(c, oh);
+}
+template <int P>
+__device__ __forceinline__ void strip_b(IssueCtx& c, int oh) {
+  window<1, 3, P>(c, oh);
+  window<1, 4, P>(c, oh);
+  window<1, 5, P>(c, oh);
+  window<1, 6, P>(c, oh);
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    conv_rows_sm100(const __grid_constant__ CUtensorMap tm_x, const ConvRowsArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align_smem_1024(smem_raw);
+  uint64_t* bar0 = reinterpret_cast<uint64_t*>(smem + kOffBar);
+  Bars B;
+  B.x_full = bar0;
+  B.x_empty = B.x_full + kXRows;
+  B.a1_full = B.x_empty + kXRows;
+  B.a1_empty = B.a1_full + kA1Stages;
+  B.c1_full = B.a1_empty + kA1Stages;
+  B.c1_empty = B.c1_full + 2;
+  B.a2_full = B.c1_empty + 2;
+  B.a2_empty = B.a2_full + 15;
+  B.o_full = B.a2_empty + 15;
+  B.o_empty = B.o_full + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(B.o_empty + 4);
+
+  const int warp = warp_uniform_id();
+  const int lane = threadIdx.x & 31;
+  unsigned long long* const trace = blockIdx.x == 0 ? args.trace : nullptr;
+  const long long row_begin = args.claim ? args.claim->row_begin : args.row_begin;
+  const long long row_end = args.claim ? args.claim->row_end : args.row_end;
+  const long long tiles = (row_end - row_begin + kTile - 1) / kTile;
+  const int my_tiles =
+      blockIdx.x < tiles ? static_cast<int>((tiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kXRows; ++i) {
+      mbar_init(&B.x_full[i], 1);
+      mbar_init(&B.x_empty[i], kBuilders);
+    }
+    for (int i = 0; i < kA1Stages; ++i) {
+      mbar_init(&B.a1_full[i], kBuilders);
+      mbar_init(&B.a1_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) mbar_init(&B.c1_full[i], 1);
+    for (int i = 0; i < 2; ++i) mbar_init(&B.c1_empty[i], 4);
+    for (int i = 0; i < 15; ++i) {
+      mbar_init(&B.a2_full[i], 4);
+      mbar_init(&B.a2_empty[i], 1);
+    }
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&B.o_full[i], 1);
+      mbar_init(&B.o_empty[i], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) tma_prefetch(&tm_x);
+  if (warp == 0) tmem_alloc(tmem_slot, 512);
+
+  // Resident weights.  W2 -> [dh][ks][plane][n = 32 j + co][8 ci] with
+  // j = 2 - dw (window column block j is output iw - 1 + j, read through
+  // tap dw = 2 - j).  W1 -> [plane][c][8]: K = 4 r + px, plane p = rows
+  // 2p, 2p + 1 (the im2col order below).
+  {
+    const uint4* w2 = static_cast<const uint4*>(args.w2);  // [32][72 chunks of 8]
+    for (int i = threadIdx.x; i < kC2 * 72; i += kThreads) {
+      const int co = i / 72, ch = i % 72, tap = ch >> 3, rem = ch & 7;
+      const int ks = rem >> 1, pl = rem & 1, dh = tap / 3, dw = tap % 3, j = 2 - dw;
+      *reinterpret_cast<uint4*>(smem + kOffW2 + ((dh * 4 + ks) * 2 + pl) * kW2Plane +
+                                (j * 32 + co) * 16) = w2[i];
+    }
+    const uint4* w1 = static_cast<const uint4*>(args.w1);  // [64][2 chunks of 8]
+    for (int i = threadIdx.x; i < 2 * 64; i += kThreads) {
+      const int c = i >> 1, pl = i & 1;
+      *reinterpret_cast<uint4*>(smem + kOffW1 + (pl * 64 + c) * 16) = w1[i];
+    }
+  }
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+
+  if (warp < kBuilders) {
+    // ------------------------------------------- TMA producer + im2col builders
+    // Per patch row: two TMA boxes of [128 samples][56 px] (image rows
+    // 4 ih .. 4 ih + 3; 112-byte runs -- boxes of single 16-byte patch rows ran
+    // the TMA unit at a fraction of this), then the warp writes each
+    // position's K = 16 im2col operand: plane p = rows 2p, 2p + 1 x 4 pixels.
+    const uint64_t pol = l2_policy_evict_normal();
+    // Patch rows in order q = 14 k + 7 strip + ih, kXRows in flight.
+    const int nrows = my_tiles * 14;
+    auto load_row = [&](int q) {
+      if (q >= nrows) return;
+      const int k = q / 14, ih = q % 7;
+      const long long s0 = row_begin + (blockIdx.x + static_cast<long long>(k) * gridDim.x) * kTile;
+      uint64_t* bar = &B.x_full[q % kXRows];
+      mbar_arrive_expect_tx(bar, 2 * kXHalf);
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        tma_load_2d(smem + kOffX + ((q % kXRows) * 2 + h) * kXHalf, &tm_x, bar, 112 * ih + 56 * h,
+                    static_cast<int32_t>(s0), pol);
+      TRACE(0, q);
+    };
+    if (warp == 0 && lane == 0)
+      for (int q = 0; q < kXRows; ++q) load_row(q);
+    // Builder warp w writes samples 32 w + 64 i + lane (i = 0, 1) of every
+    // operand; positions in production order (first_window above).
+    long long n = 0;
+    auto release_row = [&](int q) {  // this warp is done reading patch row q
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&B.x_empty[q % kXRows]);
+      if (warp == 0 && lane == 0) {  // its buffer takes row q + kXRows
+        mbar_sleep_wait(&B.x_empty[q % kXRows], static_cast<uint32_t>(q / kXRows) & 1u);
+        load_row(q + kXRows);
+      }
+    };
+    for (int k = 0; k < my_tiles; ++k)
+      for (int st = 0; st < 2; ++st) {
+        const int q0 = k * 14 + st * 7, J = st ? 4 : 5;
+        for (int i = 0; i < 7 * J; ++i, ++n) {
+          const int li = (st ? 35 : 0) + i;
+          const int ih = pos_row(li), c = (st ? 3 : 0) + pos_col(li);
+          const int q = q0 + ih;
+          if (i == 0 || i >= 2 * J) {  // first use of row q (rows 0 and 1 both at i = 0)
+            if (i == 0) mbar_sleep_wait(&B.x_full[q0 % kXRows], static_cast<uint32_t>(q0 / kXRows) & 1u);
+            if (i == 0) mbar_sleep_wait(&B.x_full[(q0 + 1) % kXRows], static_cast<uint32_t>((q0 + 1) / kXRows) & 1u);
+            if (i >= 2 * J && pos_col(li) == 0) {
+              if (ih == 2) {  // rows 0 and 1 are done
+                release_row(q0);
+                release_row(q0 + 1);
+              } else {
+                release_row(q - 1);
+              }
+              mbar_sleep_wait(&B.x_full[q % kXRows], static_cast<uint32_t>(q / kXRows) & 1u);
+            }
+          }
+          const int sl = static_cast<int>(n % kA1Stages);
+          mbar_sleep_wait(&B.a1_empty[sl], (static_cast<uint32_t>(n / kA1Stages) & 1u) ^ 1u);
+          const uint8_t* xs = smem + kOffX + (q % kXRows) * 2 * kXHalf + 8 * c;
+#pragma unroll
+          for (int t = 0; t < 2; ++t) {
+            const int smp = warp * 32 + 64 * t + lane;
+            uint8_t* a1 = smem + kOffA1 + sl * kA1Bytes + smp * 16;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const uint8_t* src = xs + h * kXHalf + smp * 112;
+              uint2 lo = make_uint2(0, 0), hi = make_uint2(0, 0);
+              if (!(args.debug & 2)) {  // timing probe: no x reads
+                lo = *reinterpret_cast<const uint2*>(src);
+                hi = *reinterpret_cast<const uint2*>(src + 56);
+              }
+              *reinterpret_cast<uint4*>(a1 + h * 2048) = make_uint4(lo.x, lo.y, hi.x, hi.y);
+            }
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive(&B.a1_full[sl]);
+            if (warp == 0) TRACE(1, static_cast<int>(n));
+          }
+        }
+        release_row(q0 + 6);
+      }
+  } else if (warp == kBuilders) {
+    // ----------------------------------------------------- UMMA issuer
+    // conv2 windows in order, conv1 of each position fed in kLead windows
+    // ahead (one in-order tensor pipe: a conv1 issued from another warp
+    // queued behind the conv2 stream and came back thousands of clocks late).
+    IssueCtx c;
+    c.tbase = __shfl_sync(0xffffffffu, tmem_base, 0);
+    c.a2d = sdesc_k128(__shfl_sync(0xffffffffu, smem_u32(smem), 0));
+    c.w2d = sdesc_planar(__shfl_sync(0xffffffffu, smem_u32(smem + kOffW2), 0), kW2Plane);
+    c.b = B;
+    c.a2par = 0;
+    c.ouse = 0;
+    c.trace = trace;
+    c.w = 0;
+    c.c1n = 0;
+    c.npos = static_cast<long long>(my_tiles) * 63;
+    c.a1_base = __shfl_sync(0xffffffffu, smem_u32(smem + kOffA1), 0);
+    c.w1d = sdesc_planar(__shfl_sync(0xffffffffu, smem_u32(smem + kOffW1), 0), 1024);
+    for (int k = 0; k < my_tiles; ++k) {
+      const int g0 = (k * 14) % 3;  // row-phase origin of this tile
+      for (int oh = 0; oh < kG; ++oh) {
+        switch ((g0 + oh) % 3) {
+          case 0: strip_a<0>(c, oh); break;
+          case 1: strip_a<1>(c, oh); break;
+          default: strip_a<2>(c, oh); break;
+        }
+      }
+      for (int oh = 0; oh < kG; ++oh) {
+        switch ((g0 + 7 + oh) % 3) {
+          case 0: strip_b<0>(c, oh); break;
+          case 1: strip_b<1>(c, oh); break;
+          default: strip_b<2>(c, oh); break;
+        }
+      }
+    }
+  } else if (warp < kBuilders + 9) {
+    // ------------------------------------------------- conv1 epilogue
+    // Two groups of four warps (one per TMEM lane quadrant), group g owns
+    // conv1 accumulator g and takes positions n = g mod 2; each walks every
+    // position to keep the slot parities.
+    const int g = (warp - kBuilders - 1) >> 2, qd = warp & 3;
+    const uint32_t lane_field = static_cast<uint32_t>(qd * 32) << 16;
+    const int row = qd * 32 + lane;  // sample within the tile
+    uint32_t a2par = 0;              // per slot id: parity of the next empty-wait
+    long long n = 0;
+    for (int k = 0; k < my_tiles; ++k) {
+      const int g0 = (k * 14) % 3;
+      for (int li = 0; li < 63; ++li, ++n) {  // production order
+        {
+          const int st = li < 35 ? 0 : 1, ih = pos_row(li), j = pos_col(li);
+          {
+            const uint32_t ph = static_cast<uint32_t>((g0 + 7 * st + ih) % 3);
+            const uint32_t sid = 3u * j + ph;
+            const uint32_t par = (a2par >> sid) & 1u;
+            a2par ^= 1u << sid;
+            const int dsl = static_cast<int>(n & 1);  // this group's D slot
+            if (dsl != g) continue;
+            mbar_sleep_wait(&B.c1_full[dsl], static_cast<uint32_t>(n >> 1) & 1u);
+            if (qd == 0 && lane == 0) TRACE(3, n);
+            tc_fence_after();
+            uint32_t v0[32], v1[32];
+            const uint32_t src = tmem_base + lane_field + kTmD1 + 64u * dsl;
+            tmem_ld32_raw(src, v0);
+            tmem_ld32_raw(src + 32u, v1);
+            tmem_ld_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&B.c1_empty[dsl]);
+            uint32_t pk[32];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              pk[i] = pack_relu_bf16(v0[2 * i], v0[2 * i + 1], args.b1c[2 * i], args.b1c[2 * i + 1]);
+              pk[16 + i] = pack_relu_bf16(v1[2 * i], v1[2 * i + 1], args.b1c[32 + 2 * i],
+                                          args.b1c[33 + 2 * i]);
+            }
+            mbar_sleep_wait(&B.a2_empty[sid], par ^ 1u);
+            if (qd == 0 && lane == 0) TRACE(4, n);
+            if (slot_tmem(j, static_cast<int>(ph))) {
+              tc_fence_after();
+              tmem_st32(tmem_base + lane_field + kTmA2 + 32u * slot_index(j, static_cast<int>(ph)), pk);
+              tmem_st_wait();
+              tc_fence_before();
+            } else {
+              uint8_t* dst = smem + slot_index(j, static_cast<int>(ph)) * kSlotBytes + row * 128;
+              if (!(args.debug & 4))  // timing probe: no A2 smem stores
+#pragma unroll
+              for (int cc = 0; cc < 8; ++cc)
+                *reinterpret_cast<uint4*>(dst + ((cc ^ (row & 7)) << 4)) =
+                    make_uint4(pk[4 * cc], pk[4 * cc + 1], pk[4 * cc + 2], pk[4 * cc + 3]);
+              fence_proxy_async_smem();
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&B.a2_full[sid]);
+            if (qd == 0 && lane == 0) TRACE(5, n);
+          }
+        }
+      }
+    }
+  } else {
+    // ----------------------------------------------------- output drain
+    const int qd = warp & 3;
+    const uint32_t lane_field = static_cast<uint32_t>(qd * 32) << 16;
+    const int row = qd * 32 + lane;
+    uint32_t opar = 0;
+    int nblk = 0;
+    for (int k = 0; k < my_tiles; ++k) {
+      const long long s = row_begin + (blockIdx.x + static_cast<long long>(k) * gridDim.x) * kTile + row;
+      uint8_t* dst_row = static_cast<uint8_t*>(args.out) + s * (kOutRow * 2);
+      const bool valid = s < row_end;
+      for (int st = 0; st < 2; ++st)
+        for (int oh = 0; oh < kG; ++oh)
+          for (int b = 0; b < (st ? 3 : 4); ++b) {
+            mbar_sleep_wait(&B.o_full[b], (opar >> b) & 1u);
+            opar ^= 1u << b;
+            if (qd == 0 && lane == 0) TRACE(9, nblk);
+            ++nblk;
+            tc_fence_after();
+            uint32_t v[32];
+            tmem_ld32_raw(tmem_base + lane_field + kTmO + 32u * b, v);
+            tmem_ld_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&B.o_empty[b]);
+            if (valid) {
+              const int ow = (st ? 4 : 0) + b;
+              uint4* dst = reinterpret_cast<uint4*>(dst_row + (oh * kG + ow) * kC2 * 2);
+#pragma unroll
+              for (int c = 0; c < 4; ++c)
+                dst[c] = make_uint4(
+                    pack_relu_bf16(v[8 * c], v[8 * c + 1], args.b2c[8 * c], args.b2c[8 * c + 1]),
+                    pack_relu_bf16(v[8 * c + 2], v[8 * c + 3], args.b2c[8 * c + 2], args.b2c[8 * c + 3]),
+                    pack_relu_bf16(v[8 * c + 4], v[8 * c + 5], args.b2c[8 * c + 4], args.b2c[8 * c + 5]),
+                    pack_relu_bf16(v[8 * c + 6], v[8 * c + 7], args.b2c[8 * c + 6], args.b2c[8 * c + 7]));
+            }
+          }
+    }
+  }
+
+  __syncthreads();
+  if (warp == 0) {
+    __syncwarp();
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 512);
+  }
+}
+
+}  // namespace
+
+bool conv_rows_supported(int S, int P, int c1, int c2) {
+  return S == kS && P == 4 && c1 == kC1 && c2 == kC2;
+}
+
+int conv_rows_launch(const ConvRowsArgs& args, const void* x, long long x_rows, int grid,
+                     cudaStream_t stream) {
+  if (x_rows > INT_MAX) return -1;
+  EncodeTiledFn fn = encode_tiled_fn();
+  if (!fn) return -1;
+  // x as [x_rows][784] bf16; box = 56 pixels (half a patch row) x 128
+  // samples, no swizzle.
+  CUtensorMap mx;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(kS * kS), static_cast<cuuint64_t>(x_rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(kS * kS * 2)};
+  cuuint32_t box[2] = {56, kTile};
+  cuuint32_t estr[2] = {1, 1};
+  if (fn(&mx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(x), dims, strides, box, estr,
+         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return -2;
+  // with a claim, [row_begin, row_end) is the worker's whole range (the grid
+  // covers any run the claim can hold), as for conv_launch
+  const long long tiles = (args.row_end - args.row_begin + kTile - 1) / kTile;
+  if (tiles <= 0) return 0;
+  grid = static_cast<int>(std::min<long long>(grid, tiles));
+  if (ensure_smem_attr(conv_rows_sm100, static_cast<int>(kSmemBytes)) != 0) return -4;
+  ConvRowsArgs a = args;
+  a.x = x;
+  a.x_rows = x_rows;
+  conv_rows_sm100<<<grid, kThreads, kSmemBytes, stream>>>(mx, a);
+  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+
+}  // namespace es

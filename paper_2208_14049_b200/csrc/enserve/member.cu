@@ -10,6 +10,7 @@
 
 #include "../cuda/aux_kernels.cuh"
 #include "../cuda/conv_kernel.cuh"
+#include "../cuda/conv_rows_kernel.cuh"
 #include "../cuda/dense_kernel.cuh"
 #include "../cuda/fp32_kernels.cuh"
 #include "../cuda/mlp_kernel.cuh"
@@ -75,9 +76,10 @@ struct DeviceMember::Impl {
   es::DenseLayout logits{};            // Head::Dense: the last layer
   bool cnn = false;
   es::ConvLayout conv{};  // CNN: the convolution stack (layers 0 and 1)
+  bool conv_rows = false;  // CNN-s shape: the samples-in-M kernel (conv_rows_kernel.cuh)
   void* weights = nullptr;
   std::vector<std::size_t> w_off, b_off;  // per layer
-  std::vector<float> conv_b2;               // CNN: conv2 bias, host copy
+  std::vector<float> conv_b1, conv_b2;      // CNN: conv biases, host copies
   // Outputs of the leading layers, bf16 [rows][width], indexed like X.
   std::vector<void*> act;
   std::vector<int> act_width;
@@ -125,6 +127,9 @@ bool DeviceMember::load(int device, const ModelSpec& model, int batch, bool fp32
     I.cnn = true;
     const char* cs = std::getenv("ES_CONV_SCHEDULE");  // tests: "tap" | "split"
     const int sched = cs && std::strcmp(cs, "tap") == 0 ? 1 : cs && std::strcmp(cs, "split") == 0 ? 2 : 0;
+    // Default for the CNN-s shape: samples in M (measured on B200);
+    // "tap" / "split" select the positions-in-M kernel for comparison.
+    I.conv_rows = !cs && es::conv_rows_supported(a.widths[0], a.widths[1], a.widths[2], a.widths[3]);
     // ES_CONV_SCHEDULE=split falls back to tap where the shape has no split plan.
     if (!es::conv_plan(a.widths[0], a.widths[1], a.widths[2], a.widths[3], &I.conv, sched) &&
         !(sched == 2 && es::conv_plan(a.widths[0], a.widths[1], a.widths[2], a.widths[3], &I.conv, 1)))
@@ -207,6 +212,9 @@ bool DeviceMember::load(int device, const ModelSpec& model, int batch, bool fp32
     I.conv_b2.resize(static_cast<std::size_t>(I.dims[1].second));
     M_CUDA(cudaMemcpy(I.conv_b2.data(), base + I.b_off[1], I.conv_b2.size() * sizeof(float),
                       cudaMemcpyDeviceToHost));
+    I.conv_b1.resize(static_cast<std::size_t>(I.dims[0].second));
+    M_CUDA(cudaMemcpy(I.conv_b1.data(), base + I.b_off[0], I.conv_b1.size() * sizeof(float),
+                      cudaMemcpyDeviceToHost));
   }
   return true;
 }
@@ -221,7 +229,8 @@ std::vector<std::string> DeviceMember::kernel_names() const {
     for (std::size_t l = I.cnn ? 2 : 0; l < I.dims.size(); ++l) n.push_back("f32_dense_kernel");
     return n;
   }
-  if (I.cnn) n.push_back(I.conv.split ? "conv_stack_sm100[split]" : "conv_stack_sm100[tap]");
+  if (I.cnn)
+    n.push_back(I.conv_rows ? "conv_rows_sm100" : I.conv.split ? "conv_stack_sm100[split]" : "conv_stack_sm100[tap]");
   for (const auto& d : I.dense) n.push_back(d.pair ? "dense_pair_sm100" : "dense_sm100");
   if (env_is("ES_MEMBER_KERNEL", "simt") && I.head != Impl::Head::Dense) {
     n.push_back("mlp2_simt_kernel");
@@ -271,7 +280,20 @@ int DeviceMember::forward(const void* x, long long nb, int seg_size, long long s
   }
   if (I.head == Impl::Head::Fp32)
     return forward_fp32(static_cast<const float*>(x), nb, r0, r1, out, grid, stream, marks, claim);
-  if (I.cnn) {
+  if (I.cnn && I.conv_rows) {
+    es::ConvRowsArgs c;
+    c.row_begin = r0;
+    c.row_end = r1;
+    c.claim = claim;
+    c.w1 = base + I.w_off[0];
+    c.w2 = base + I.w_off[1];
+    std::copy(I.conv_b1.begin(), I.conv_b1.end(), c.b1c);
+    std::copy(I.conv_b2.begin(), I.conv_b2.end(), c.b2c);
+    c.out = I.act[0];
+    M_LAUNCH(es::conv_rows_launch(c, cur, nb, grid, stream));
+    mark(launches++);
+    cur = I.act[0];
+  } else if (I.cnn) {
     es::ConvArgs c;
     c.L = I.conv;
     c.row_begin = r0;

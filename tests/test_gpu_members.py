@@ -80,7 +80,7 @@ CNN_SHAPES = [(28, 4, 64, 32, 128, 10), (28, 4, 32, 64, 256, 10), (16, 4, 64, 32
 
 @pytest.mark.parametrize("shape", CNN_SHAPES)
 @pytest.mark.parametrize("b", [32, 128])
-@pytest.mark.parametrize("schedule", ["auto", "tap"])
+@pytest.mark.parametrize("schedule", ["auto", "tap", "split"])
 def test_cnn_member_matches_cpu_oracle(shape, b, schedule, monkeypatch):
     """Both conv2 schedules (conv_kernel.cuh): "auto" takes the split
     schedule where the shape allows it (R | 32, c1 % 64 == 0), "tap" forces
