@@ -8,7 +8,7 @@
 
 #include "conv_rows_kernel.cuh"
 #include "sm100.cuh"
-#include "tma_host.hpp"
+#include "tma_host.hpp"  // ensure_smem_attr
 
 namespace es {
 
@@ -18,28 +18,10 @@ namespace {
 
 constexpr int kS = 28, kG = 7, kC1 = 64, kC2 = 32, kTile = 128;
 constexpr int kOutRow = kG * kG * kC2;  // bf16 elements per output sample
-constexpr int kThreads = 480;           // 15 warps: 2 im2col builders (warp 0 also TMA),
-                                        // the UMMA issuer, 2 x 4 conv1 epilogue,
-                                        // 4 output drain
-constexpr int kBuilders = 2;
-constexpr int kLead = 2;  // conv1 of a position is issued kLead windows before its first use
-
-// Production order of a strip's positions (builder, conv1, epilogue): input
-// rows 0 and 1 interleaved by column, then rows 2..6 -- so the window that
-// first needs a position is non-decreasing along it.  Window index (within
-// the tile: strip A windows 0..34, strip B 35..62) that first reads the
-// position at local index i (strip A 0..34, strip B 35..62):
-__host__ __device__ constexpr int first_window(int i) {
-  return i < 35 ? (i < 10 ? i / 2 : i - 5) : (i < 43 ? 35 + (i - 35) / 2 : i - 4);
-}
-// (input row, strip column) of local position i.
-__host__ __device__ constexpr int pos_row(int i) {
-  return i < 35 ? (i < 10 ? i & 1 : 2 + (i - 10) / 5) : (i < 43 ? (i - 35) & 1 : 2 + (i - 43) / 4);
-}
-__host__ __device__ constexpr int pos_col(int i) {
-  return i < 35 ? (i < 10 ? i / 2 : (i - 10) % 5) : (i < 43 ? (i - 35) / 2 : (i - 43) % 4);
-}
-
+constexpr int kBuilders = 2;            // im2col builder warps (kSampPerLane samples per lane)
+constexpr int kSampPerLane = 128 / (32 * kBuilders);
+constexpr int kThreads = 32 * (kBuilders + 14);  // + conv1 issuer, conv2 issuer, 2 x 4 conv1
+                                                 // epilogue, 4 output drain
 // Shared memory (offsets from the 1024-aligned base).
 constexpr uint32_t kSlotBytes = 16384;  // A2 smem slot: [128 samples][64 ch] bf16, SW128
 constexpr int kSmemSlots = 7;
@@ -48,14 +30,9 @@ constexpr uint32_t kW2Plane = 96 * 16;
 constexpr uint32_t kOffW1 = kOffW2 + 3 * 4 * 2 * kW2Plane;  // [plane][64 c][16 B]
 constexpr uint32_t kOffA1 = kOffW1 + 2 * 64 * 16;           // im2col ring: [2 planes][128][16 B]
 constexpr uint32_t kA1Bytes = 2 * 128 * 16;
-constexpr int kA1Stages = 3;
-// x staging: half patch rows (image rows 4 ih + 2 h, +1 = 56 contiguous
-// pixels) of the tile's 128 samples, one TMA box each (112-byte runs).
-constexpr uint32_t kOffX = kOffA1 + kA1Stages * kA1Bytes;
-constexpr uint32_t kXHalf = 128 * 56 * 2;
-constexpr int kXRows = 2;  // patch rows in flight (the next one loads while this one is built)
-constexpr uint32_t kOffBar = kOffX + kXRows * 2 * kXHalf;
-constexpr int kNumBars = 2 * kXRows + kA1Stages * 2 + 2 + 2 + 15 + 15 + 4 + 4;
+constexpr int kA1Stages = 10;  // two patch rows of im2col operands
+constexpr uint32_t kOffBar = kOffA1 + kA1Stages * kA1Bytes;
+constexpr int kNumBars = kA1Stages * 2 + 2 + 2 + 15 + 15 + 4 + 4;
 constexpr uint32_t kSmemBytes = kOffBar + kNumBars * 8 + 16 + 1024;
 
 // TMEM columns: output-row accumulator O (4 blocks of 32), two conv1
@@ -89,10 +66,8 @@ __device__ __forceinline__ uint32_t pack_relu_bf16(uint32_t a, uint32_t b, float
   } while (0)
 
 struct Bars {
-  uint64_t* x_full;    // [kXRows] TMA -> im2col builders (one patch row, both halves)
-  uint64_t* x_empty;   // [kXRows] builders -> TMA
-  uint64_t* a1_full;   // [3] builder -> conv1 issuer
-  uint64_t* a1_empty;  // [3]
+  uint64_t* a1_full;   // [kA1Stages] builders -> conv1 issuer
+  uint64_t* a1_empty;  // [kA1Stages]
   uint64_t* c1_full;   // [2] conv1 issuer -> epilogue group of that D slot
   uint64_t* c1_empty;  // [2]
   uint64_t* a2_full;   // [15] conv1 epilogue -> conv2 issuer
@@ -110,42 +85,8 @@ struct IssueCtx {
   uint32_t a2par;  // per slot id: parity of the next fill to wait for
   uint32_t ouse;   // per O block: parity of its first-touch count
   unsigned long long* trace;
-  long long w;  // running window index
-  // conv1 feed: next position, total, operand bases
-  long long c1n, npos;
-  uint32_t a1_base;
-  uint64_t w1d;
+  int w;  // running window index (trace)
 };
-
-// Issue conv1 for every position whose first window is <= w + kLead, in
-// production order; ahead of need only if its operand and accumulator are
-// already free (never stall the conv2 stream for work not due yet).
-__device__ __forceinline__ void feed_conv1(IssueCtx& c) {
-  constexpr uint32_t id1 = idesc_bf16_f32(128, kC1);
-  while (c.c1n < c.npos) {
-    const long long n = c.c1n;
-    const long long due = (n / 63) * 63 + first_window(static_cast<int>(n % 63));
-    if (due > c.w + kLead) break;
-    const int sl = static_cast<int>(n % kA1Stages), dsl = static_cast<int>(n & 1);
-    const uint32_t pa = static_cast<uint32_t>(n / kA1Stages) & 1u;
-    const uint32_t pd = (static_cast<uint32_t>(n >> 1) & 1u) ^ 1u;
-    if (due > c.w) {
-      if (!mbar_test(&c.b.a1_full[sl], pa) || !mbar_test(&c.b.c1_empty[dsl], pd)) break;
-    } else {
-      mbar_sleep_wait(&c.b.a1_full[sl], pa);
-      mbar_sleep_wait(&c.b.c1_empty[dsl], pd);
-    }
-    tc_fence_after();
-    if (elect_one()) {
-      umma_bf16(c.tbase + kTmD1 + 64u * dsl, sdesc_planar(c.a1_base + sl * kA1Bytes, 2048), c.w1d,
-                id1, 0);
-      umma_commit(&c.b.c1_full[dsl]);
-      umma_commit(&c.b.a1_empty[sl]);
-    }
-    __syncwarp();
-    ++c.c1n;
-  }
-}
 
 // D (+)= A2(slot of column J, phase p) x W2(dh, ks, blocks jlo..jlo+n-1).
 template <int J, int NB, int P>
@@ -172,7 +113,7 @@ __device__ __forceinline__ void mma2(const IssueCtx& c, uint32_t d, int dh, int 
 }
 
 __device__ __forceinline__ void wait_slot(IssueCtx& c, uint32_t sid) {
-  mbar_sleep_wait(&c.b.a2_full[sid], (c.a2par >> sid) & 1u);
+  mbar_wait(&c.b.a2_full[sid], (c.a2par >> sid) & 1u);
   c.a2par ^= 1u << sid;
 }
 
@@ -191,8 +132,7 @@ __device__ __forceinline__ void window(IssueCtx& c, int oh) {
   constexpr bool all_new = IW == c0;
   constexpr bool last_new = !all_new && owhi == IW + 1;
   unsigned long long* trace = c.trace;
-  TRACE(6, static_cast<int>(c.w));
-  feed_conv1(c);
+  TRACE(6, c.w);
   // new input positions: (0, IW) and (1, IW) at the first row, else (oh+1, IW)
   if (oh == 0) wait_slot(c, 3u * J + p1);
   if (oh < kG - 1) wait_slot(c, 3u * J + p2);
@@ -200,11 +140,11 @@ __device__ __forceinline__ void window(IssueCtx& c, int oh) {
 #pragma unroll
   for (int b = dblk; b < dblk + NB; ++b)
     if (all_new || (last_new && b == dblk + NB - 1)) {
-      mbar_sleep_wait(&c.b.o_empty[b], ((c.ouse >> b) & 1u) ^ 1u);
+      mbar_wait(&c.b.o_empty[b], ((c.ouse >> b) & 1u) ^ 1u);
       c.ouse ^= 1u << b;
     }
   tc_fence_after();
-  TRACE(7, static_cast<int>(c.w));
+  TRACE(7, c.w);
   // Opaque per-window copies of the bases: otherwise the compiler hoists all
   // 36 B descriptors of the strip into uniform registers and spills them.
   IssueCtx cw = c;
@@ -236,8 +176,61 @@ __device__ __forceinline__ void window(IssueCtx& c, int oh) {
   if constexpr (IW == iwl && IW < ow0 + nout)
     if (elect_one()) umma_commit(&c.b.o_full[IW - ow0]);
   __syncwarp();
-  TRACE(8, static_cast<int>(c.w));
+  TRACE(8, c.w);
   ++c.w;
+}
+
+// Patch row ih of strip ST for this lane's two samples; positions n0 .. n0+J-1.
+template <int ST>
+__device__ __forceinline__ void build_row(const ConvRowsArgs& args, uint8_t* smem, const Bars& B,
+                                          long long s0, int ih, int warp, int lane, int n0) {
+  constexpr int J = ST ? 4 : 5, c0 = ST ? 3 : 0;
+#pragma unroll
+  for (int t = 0; t < kSampPerLane; ++t) {
+    const int smp = warp * 32 * kSampPerLane + t * 32 + lane;
+    const long long s = s0 + smp;
+    uint4 ch[4][3];
+    const uint8_t* xrow = static_cast<const uint8_t*>(args.x) + s * (kS * kS * 2);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      // first pixel of the aligned 24-pixel window of image row y = 4 ih + r
+      const int y = 4 * ih + r;
+      const int x0 = ST ? 28 * y + 12 - 4 * ((r + 1) & 1) : 28 * y - 4 * (r & 1);
+#pragma unroll
+      for (int m = 0; m < 3; ++m)
+        ch[r][m] = s < args.x_rows
+                       ? __ldg(reinterpret_cast<const uint4*>(xrow + 2 * (x0 + 8 * m)))
+                       : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const int n = n0 + j;
+      const int sl = static_cast<int>(n % kA1Stages);
+      if (t == 0) mbar_sleep_wait(&B.a1_empty[sl], (static_cast<uint32_t>(n / kA1Stages) & 1u) ^ 1u);
+      uint32_t w[4][2];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        // pixel offset of the position's 4 pixels inside the window
+        const int c = c0 + j;
+        const int o = ST ? 4 * c - 12 + 4 * ((r + 1) & 1) : 4 * c + 4 * (r & 1);
+        const uint4 q = ch[r][o / 8];
+        const bool hi = (o % 8) != 0;
+        w[r][0] = hi ? q.z : q.x;
+        w[r][1] = hi ? q.w : q.y;
+      }
+      uint8_t* a1 = smem + kOffA1 + sl * kA1Bytes + smp * 16;
+      *reinterpret_cast<uint4*>(a1) = make_uint4(w[0][0], w[0][1], w[1][0], w[1][1]);
+      *reinterpret_cast<uint4*>(a1 + 2048) = make_uint4(w[2][0], w[2][1], w[3][0], w[3][1]);
+    }
+  }
+  fence_proxy_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+#pragma unroll
+    for (int j = 0; j < J; ++j) mbar_arrive(&B.a1_full[(n0 + j) % kA1Stages]);
+    unsigned long long* trace = blockIdx.x == 0 && warp == 0 ? args.trace : nullptr;
+    TRACE(1, static_cast<int>(n0));
+  }
 }
 
 template <int P>
@@ -257,14 +250,12 @@ __device__ __forceinline__ void strip_b(IssueCtx& c, int oh) {
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
-    conv_rows_sm100(const __grid_constant__ CUtensorMap tm_x, const ConvRowsArgs args) {
+    conv_rows_sm100(const ConvRowsArgs args) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align_smem_1024(smem_raw);
   uint64_t* bar0 = reinterpret_cast<uint64_t*>(smem + kOffBar);
   Bars B;
-  B.x_full = bar0;
-  B.x_empty = B.x_full + kXRows;
-  B.a1_full = B.x_empty + kXRows;
+  B.a1_full = bar0;
   B.a1_empty = B.a1_full + kA1Stages;
   B.c1_full = B.a1_empty + kA1Stages;
   B.c1_empty = B.c1_full + 2;
@@ -284,10 +275,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       blockIdx.x < tiles ? static_cast<int>((tiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kXRows; ++i) {
-      mbar_init(&B.x_full[i], 1);
-      mbar_init(&B.x_empty[i], kBuilders);
-    }
     for (int i = 0; i < kA1Stages; ++i) {
       mbar_init(&B.a1_full[i], kBuilders);
       mbar_init(&B.a1_empty[i], 1);
@@ -304,7 +291,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     fence_barrier_init();
   }
-  if (warp == 0 && lane == 0) tma_prefetch(&tm_x);
   if (warp == 0) tmem_alloc(tmem_slot, 512);
 
   // Resident weights.  W2 -> [dh][ks][plane][n = 32 j + co][8 ci] with
@@ -332,91 +318,55 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);
 
   if (warp < kBuilders) {
-    // ------------------------------------------- TMA producer + im2col builders
-    // Per patch row: two TMA boxes of [128 samples][56 px] (image rows
-    // 4 ih .. 4 ih + 3; 112-byte runs -- boxes of single 16-byte patch rows ran
-    // the TMA unit at a fraction of this), then the warp writes each
-    // position's K = 16 im2col operand: plane p = rows 2p, 2p + 1 x 4 pixels.
-    const uint64_t pol = l2_policy_evict_normal();
-    // Patch rows in order q = 14 k + 7 strip + ih, kXRows in flight.
-    const int nrows = my_tiles * 14;
-    auto load_row = [&](int q) {
-      if (q >= nrows) return;
-      const int k = q / 14, ih = q % 7;
+    // ------------------------------------------------------ im2col builders
+    // Each lane owns samples 64 w + 32 t + lane (t = 0, 1).  Per patch row it
+    // loads, straight from x (L2; no smem staging, whose loads queued behind
+    // the UMMA operand reads), the 16-byte-aligned chunks covering the
+    // strip's pixels of the 4 image rows, then writes every position's K = 16
+    // operand: plane p = rows 2p, 2p + 1 x the position's 4 pixels.
+    int n = 0;
+    for (int k = 0; k < my_tiles; ++k) {
       const long long s0 = row_begin + (blockIdx.x + static_cast<long long>(k) * gridDim.x) * kTile;
-      uint64_t* bar = &B.x_full[q % kXRows];
-      mbar_arrive_expect_tx(bar, 2 * kXHalf);
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-        tma_load_2d(smem + kOffX + ((q % kXRows) * 2 + h) * kXHalf, &tm_x, bar, 112 * ih + 56 * h,
-                    static_cast<int32_t>(s0), pol);
-      TRACE(0, q);
-    };
-    if (warp == 0 && lane == 0)
-      for (int q = 0; q < kXRows; ++q) load_row(q);
-    // Builder warp w writes samples 32 w + 64 i + lane (i = 0, 1) of every
-    // operand; positions in production order (first_window above).
-    long long n = 0;
-    auto release_row = [&](int q) {  // this warp is done reading patch row q
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&B.x_empty[q % kXRows]);
-      if (warp == 0 && lane == 0) {  // its buffer takes row q + kXRows
-        mbar_sleep_wait(&B.x_empty[q % kXRows], static_cast<uint32_t>(q / kXRows) & 1u);
-        load_row(q + kXRows);
+      for (int ih = 0; ih < kG; ++ih) {
+        build_row<0>(args, smem, B, s0, ih, warp, lane, n);
+        n += 5;
       }
-    };
-    for (int k = 0; k < my_tiles; ++k)
-      for (int st = 0; st < 2; ++st) {
-        const int q0 = k * 14 + st * 7, J = st ? 4 : 5;
-        for (int i = 0; i < 7 * J; ++i, ++n) {
-          const int li = (st ? 35 : 0) + i;
-          const int ih = pos_row(li), c = (st ? 3 : 0) + pos_col(li);
-          const int q = q0 + ih;
-          if (i == 0 || i >= 2 * J) {  // first use of row q (rows 0 and 1 both at i = 0)
-            if (i == 0) mbar_sleep_wait(&B.x_full[q0 % kXRows], static_cast<uint32_t>(q0 / kXRows) & 1u);
-            if (i == 0) mbar_sleep_wait(&B.x_full[(q0 + 1) % kXRows], static_cast<uint32_t>((q0 + 1) / kXRows) & 1u);
-            if (i >= 2 * J && pos_col(li) == 0) {
-              if (ih == 2) {  // rows 0 and 1 are done
-                release_row(q0);
-                release_row(q0 + 1);
-              } else {
-                release_row(q - 1);
-              }
-              mbar_sleep_wait(&B.x_full[q % kXRows], static_cast<uint32_t>(q / kXRows) & 1u);
-            }
-          }
-          const int sl = static_cast<int>(n % kA1Stages);
-          mbar_sleep_wait(&B.a1_empty[sl], (static_cast<uint32_t>(n / kA1Stages) & 1u) ^ 1u);
-          const uint8_t* xs = smem + kOffX + (q % kXRows) * 2 * kXHalf + 8 * c;
-#pragma unroll
-          for (int t = 0; t < 2; ++t) {
-            const int smp = warp * 32 + 64 * t + lane;
-            uint8_t* a1 = smem + kOffA1 + sl * kA1Bytes + smp * 16;
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const uint8_t* src = xs + h * kXHalf + smp * 112;
-              uint2 lo = make_uint2(0, 0), hi = make_uint2(0, 0);
-              if (!(args.debug & 2)) {  // timing probe: no x reads
-                lo = *reinterpret_cast<const uint2*>(src);
-                hi = *reinterpret_cast<const uint2*>(src + 56);
-              }
-              *reinterpret_cast<uint4*>(a1 + h * 2048) = make_uint4(lo.x, lo.y, hi.x, hi.y);
-            }
-          }
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            mbar_arrive(&B.a1_full[sl]);
-            if (warp == 0) TRACE(1, static_cast<int>(n));
-          }
-        }
-        release_row(q0 + 6);
+      for (int ih = 0; ih < kG; ++ih) {
+        build_row<1>(args, smem, B, s0, ih, warp, lane, n);
+        n += 4;
       }
+    }
   } else if (warp == kBuilders) {
-    // ----------------------------------------------------- UMMA issuer
-    // conv2 windows in order, conv1 of each position fed in kLead windows
-    // ahead (one in-order tensor pipe: a conv1 issued from another warp
-    // queued behind the conv2 stream and came back thousands of clocks late).
+    // ----------------------------------------------------- conv1 issuer
+    // One K = 16 UMMA (N = 64) per position, in production order, as soon as
+    // its operand is built and an accumulator is free.  (Feeding conv1 from
+    // the conv2 issuer's own stream cost ~800 clk of issue overhead a window.)
+    const uint32_t tbase = __shfl_sync(0xffffffffu, tmem_base, 0);
+    const uint32_t a1_base = __shfl_sync(0xffffffffu, smem_u32(smem + kOffA1), 0);
+    const uint64_t w1d = sdesc_planar(__shfl_sync(0xffffffffu, smem_u32(smem + kOffW1), 0), 1024);
+    constexpr uint32_t id1 = idesc_bf16_f32(128, kC1);
+    const int npos = my_tiles * 63;
+    int sl = 0;
+    uint32_t slpar = 0;
+    for (int n = 0; n < npos; ++n) {
+      mbar_sleep_wait(&B.a1_full[sl], slpar);
+      const int dsl = n & 1;
+      mbar_sleep_wait(&B.c1_empty[dsl], (static_cast<uint32_t>(n >> 1) & 1u) ^ 1u);
+      if (lane == 0) TRACE(2, n);
+      tc_fence_after();
+      if (elect_one()) {
+        umma_bf16(tbase + kTmD1 + 64u * dsl, sdesc_planar(a1_base + sl * kA1Bytes, 2048), w1d, id1, 0);
+        umma_commit(&B.c1_full[dsl]);
+        umma_commit(&B.a1_empty[sl]);
+      }
+      __syncwarp();
+      if (++sl == kA1Stages) {
+        sl = 0;
+        slpar ^= 1u;
+      }
+    }
+  } else if (warp == kBuilders + 1) {
+    // ----------------------------------------------------- conv2 issuer
     IssueCtx c;
     c.tbase = __shfl_sync(0xffffffffu, tmem_base, 0);
     c.a2d = sdesc_k128(__shfl_sync(0xffffffffu, smem_u32(smem), 0));
@@ -426,10 +376,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     c.ouse = 0;
     c.trace = trace;
     c.w = 0;
-    c.c1n = 0;
-    c.npos = static_cast<long long>(my_tiles) * 63;
-    c.a1_base = __shfl_sync(0xffffffffu, smem_u32(smem + kOffA1), 0);
-    c.w1d = sdesc_planar(__shfl_sync(0xffffffffu, smem_u32(smem + kOffW1), 0), 1024);
+
     for (int k = 0; k < my_tiles; ++k) {
       const int g0 = (k * 14) % 3;  // row-phase origin of this tile
       for (int oh = 0; oh < kG; ++oh) {
@@ -447,21 +394,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp < kBuilders + 9) {
+  } else if (warp < kBuilders + 10) {
     // ------------------------------------------------- conv1 epilogue
     // Two groups of four warps (one per TMEM lane quadrant), group g owns
     // conv1 accumulator g and takes positions n = g mod 2; each walks every
     // position to keep the slot parities.
-    const int g = (warp - kBuilders - 1) >> 2, qd = warp & 3;
+    const int g = (warp - kBuilders - 2) >> 2, qd = warp & 3;
     const uint32_t lane_field = static_cast<uint32_t>(qd * 32) << 16;
     const int row = qd * 32 + lane;  // sample within the tile
     uint32_t a2par = 0;              // per slot id: parity of the next empty-wait
-    long long n = 0;
+    int n = 0;
     for (int k = 0; k < my_tiles; ++k) {
       const int g0 = (k * 14) % 3;
       for (int li = 0; li < 63; ++li, ++n) {  // production order
         {
-          const int st = li < 35 ? 0 : 1, ih = pos_row(li), j = pos_col(li);
+          const int st = li < 35 ? 0 : 1, ih = st ? (li - 35) / 4 : li / 5, j = st ? (li - 35) % 4 : li % 5;
           {
             const uint32_t ph = static_cast<uint32_t>((g0 + 7 * st + ih) % 3);
             const uint32_t sid = 3u * j + ph;
@@ -567,19 +514,6 @@ bool conv_rows_supported(int S, int P, int c1, int c2) {
 int conv_rows_launch(const ConvRowsArgs& args, const void* x, long long x_rows, int grid,
                      cudaStream_t stream) {
   if (x_rows > INT_MAX) return -1;
-  EncodeTiledFn fn = encode_tiled_fn();
-  if (!fn) return -1;
-  // x as [x_rows][784] bf16; box = 56 pixels (half a patch row) x 128
-  // samples, no swizzle.
-  CUtensorMap mx;
-  cuuint64_t dims[2] = {static_cast<cuuint64_t>(kS * kS), static_cast<cuuint64_t>(x_rows)};
-  cuuint64_t strides[1] = {static_cast<cuuint64_t>(kS * kS * 2)};
-  cuuint32_t box[2] = {56, kTile};
-  cuuint32_t estr[2] = {1, 1};
-  if (fn(&mx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(x), dims, strides, box, estr,
-         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-    return -2;
   // with a claim, [row_begin, row_end) is the worker's whole range (the grid
   // covers any run the claim can hold), as for conv_launch
   const long long tiles = (args.row_end - args.row_begin + kTile - 1) / kTile;
@@ -589,7 +523,7 @@ int conv_rows_launch(const ConvRowsArgs& args, const void* x, long long x_rows, 
   ConvRowsArgs a = args;
   a.x = x;
   a.x_rows = x_rows;
-  conv_rows_sm100<<<grid, kThreads, kSmemBytes, stream>>>(mx, a);
+  conv_rows_sm100<<<grid, kThreads, kSmemBytes, stream>>>(a);
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 

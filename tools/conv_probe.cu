@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(128, 1) fixed_rate(int reps, unsigned long lon
   __shared__ uint64_t bar;
   __shared__ uint32_t slot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int i = threadIdx.x; i < 16384 / 16; i += 128) reinterpret_cast<uint4*>(sm)[i] = make_uint4(0, 0, 0, 0);
+  for (int i = threadIdx.x; i < 49152 / 16; i += 128) reinterpret_cast<uint4*>(sm)[i] = make_uint4(0, 0, 0, 0);
   fence_proxy_async_smem();
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
@@ -188,13 +188,19 @@ __global__ void __launch_bounds__(128, 1) fixed_rate(int reps, unsigned long lon
     const uint32_t td0 = __shfl_sync(0xffffffffu, slot, 0);
     const uint64_t ad = sdesc_planar(__shfl_sync(0xffffffffu, smem_u32(sm), 0), 2048);
     const uint64_t bd = sdesc_planar(__shfl_sync(0xffffffffu, smem_u32(sm + 4096), 0), 4096);
+    const uint64_t ad128 = sdesc_k128(__shfl_sync(0xffffffffu, smem_u32(sm), 0));
+    const uint64_t bd128 = sdesc_k128(__shfl_sync(0xffffffffu, smem_u32(sm + 16384), 0));
     constexpr uint32_t id = idesc_bf16_f32(128, N);
     const long long t0 = clock64();
     for (int r = 0; r < reps; ++r) {
 #pragma unroll
       for (int i = 0; i < 84; ++i) {
-        if constexpr (TA) {
+        if constexpr (TA == 1) {
           if (elect_one()) umma_bf16_ta(td0, td0 + 256u + 8u * (i & 3), bd, id, 1);
+        } else if constexpr (TA == 2) {  // A: K-major SW128 [128][64], K step = +32 B
+          if (elect_one()) umma_bf16(td0, ad128 + 2u * (i & 3), bd, id, 1);
+        } else if constexpr (TA == 3) {  // A SW128, B SW128 [N][64]
+          if (elect_one()) umma_bf16(td0, ad128 + 2u * (i & 3), bd128 + 2u * (i & 3), id, 1);
         } else {
           if (elect_one()) umma_bf16(td0, ad + 2u * (i & 3), bd, id, 1);
         }
@@ -212,12 +218,153 @@ __global__ void __launch_bounds__(128, 1) fixed_rate(int reps, unsigned long lon
 
 template <int N, int TA>
 static void run_fixed(unsigned long long* clk) {
-  cudaFuncSetAttribute(fixed_rate<N, TA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 40000);
-  fixed_rate<N, TA><<<148, 128, 40000>>>(100, clk);
+  cudaFuncSetAttribute(fixed_rate<N, TA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 60000);
+  fixed_rate<N, TA><<<148, 128, 60000>>>(100, clk);
   cudaDeviceSynchronize();
   unsigned long long c;
   cudaMemcpy(&c, clk, 8, cudaMemcpyDeviceToHost);
-  printf("fixed N=%3d A from %s: %.1f clk/UMMA\n", N, TA ? "TMEM" : "smem", double(c) / (100.0 * 84));
+  printf("fixed N=%3d A from %s: %.1f clk/UMMA\n", N, TA == 1 ? "TMEM" : TA == 2 ? "smem SW128 (B planar)" : TA == 3 ? "smem SW128 (B SW128)" : "smem planar", double(c) / (100.0 * 84));
+}
+
+// Commit cost: 96 UMMAs (N = 96, A from TMEM) per rep, a tcgen05.commit to a
+// dummy mbarrier after every `every` UMMAs (0 = none).
+template <int EVERY>
+__global__ void __launch_bounds__(128, 1) commit_rate(int reps, unsigned long long* clk) {
+  extern __shared__ uint8_t raw[];
+  uint8_t* sm = align_smem_1024(raw);
+  __shared__ uint64_t bar, dummy;
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < 16384 / 16; i += 128) reinterpret_cast<uint4*>(sm)[i] = make_uint4(0, 0, 0, 0);
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_init(&dummy, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc(&slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) {
+    const uint32_t td0 = __shfl_sync(0xffffffffu, slot, 0);
+    const uint64_t bd = sdesc_planar(__shfl_sync(0xffffffffu, smem_u32(sm + 4096), 0), 4096);
+    constexpr uint32_t id = idesc_bf16_f32(128, 96);
+    const long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+#pragma unroll
+      for (int i = 0; i < 96; ++i) {
+        if (elect_one()) umma_bf16_ta(td0, td0 + 256u + 8u * (i & 3), bd, id, 1);
+        if constexpr (EVERY > 0)
+          if ((i + 1) % EVERY == 0 && elect_one()) umma_commit(&dummy);
+        if constexpr (EVERY < 0)
+          if ((i + 1) % (-EVERY) == 0) tc_fence_after();
+      }
+    }
+    if (elect_one()) umma_commit(&bar);
+    __syncwarp();
+    mbar_wait(&bar, 0);
+    if (lane == 0 && blockIdx.x == 0) clk[0] = static_cast<unsigned long long>(clock64() - t0);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(slot, 512);
+}
+
+template <int EVERY>
+static void run_commit(unsigned long long* clk) {
+  cudaFuncSetAttribute(commit_rate<EVERY>, cudaFuncAttributeMaxDynamicSharedMemorySize, 40000);
+  commit_rate<EVERY><<<148, 128, 40000>>>(50, clk);
+  cudaDeviceSynchronize();
+  unsigned long long c;
+  cudaMemcpy(&c, clk, 8, cudaMemcpyDeviceToHost);
+  printf("%s every %2d UMMAs (N=96, TMEM A): %.1f clk/UMMA\n", EVERY < 0 ? "fence::after_thread_sync" : "commit", EVERY < 0 ? -EVERY : EVERY, double(c) / (50.0 * 96));
+}
+
+// Mixed stream: per rep 12 TMEM-A N=64 then 12 smem-A (SW128) N=96 UMMAs
+// (MODE bit 0), optionally with warps 1-3 + 4-7 streaming tcgen05.ld (bit 1)
+// or tcgen05.st (bit 2) on other columns, and warps streaming STS (bit 3).
+template <int MODE>
+__global__ void __launch_bounds__(256, 1) mixed_rate(int reps, unsigned long long* clk) {
+  extern __shared__ uint8_t raw[];
+  uint8_t* sm = align_smem_1024(raw);
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  __shared__ volatile int stop;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < 65536 / 16; i += 256) reinterpret_cast<uint4*>(sm)[i] = make_uint4(0, 0, 0, 0);
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+    stop = 0;
+  }
+  if (warp == 0) tmem_alloc(&slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = slot;
+  if (warp == 0) {
+    const uint32_t td0 = __shfl_sync(0xffffffffu, tm, 0);
+    const uint64_t bd = sdesc_planar(__shfl_sync(0xffffffffu, smem_u32(sm + 16384), 0), 1536);
+    const uint64_t ad128 = sdesc_k128(__shfl_sync(0xffffffffu, smem_u32(sm), 0));
+    constexpr uint32_t id64 = idesc_bf16_f32(128, 64), id96 = idesc_bf16_f32(128, 96);
+    const long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+#pragma unroll
+      for (int i = 0; i < 12; ++i)
+        if (elect_one()) umma_bf16_ta(td0 + 32u * (i & 1), td0 + 256u + 8u * (i & 3), bd, id64, 1);
+      if constexpr (MODE & 1) {
+#pragma unroll
+        for (int i = 0; i < 12; ++i)
+          if (elect_one()) umma_bf16(td0 + 32u * (i & 1), ad128 + 2u * (i & 3), bd, id96, 1);
+      }
+    }
+    if (elect_one()) umma_commit(&bar);
+    __syncwarp();
+    mbar_wait(&bar, 0);
+    if (lane == 0 && blockIdx.x == 0) clk[0] = static_cast<unsigned long long>(clock64() - t0);
+    if (lane == 0) stop = 1;
+  } else if (warp >= 4) {
+    const uint32_t lf = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    uint32_t v[32];
+    for (int c = 0; c < 32; ++c) v[c] = c;
+    float acc = 0.f;
+    while (!stop) {
+      if constexpr (MODE & 2) {
+        tmem_ld32_raw(tm + lf + 320u, v);
+        tmem_ld32_raw(tm + lf + 352u, v);
+        tmem_ld_wait();
+        acc += __uint_as_float(v[3]);
+      }
+      if constexpr (MODE & 4) {
+        tmem_st32(tm + lf + 384u, v);
+        tmem_st_wait();
+      }
+      if constexpr (MODE & 8) {
+        uint4* d = reinterpret_cast<uint4*>(sm + 40960 + (warp - 4) * 4096);
+        for (int k = 0; k < 8; ++k) d[k * 32 + lane] = make_uint4(k, lane, 1, 2);
+      }
+      if constexpr (MODE < 2) break;
+    }
+    if (acc == 1234.f) clk[1] = 1;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tm, 512);
+}
+
+template <int MODE>
+static void run_mixed(unsigned long long* clk) {
+  cudaFuncSetAttribute(mixed_rate<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 70000);
+  mixed_rate<MODE><<<148, 256, 70000>>>(100, clk);
+  cudaDeviceSynchronize();
+  unsigned long long c;
+  cudaMemcpy(&c, clk, 8, cudaMemcpyDeviceToHost);
+  const double ideal = (MODE & 1) ? 12 * 32 + 12 * 56 : 12 * 32;
+  printf("mixed mode %2d (%s%s%s%s): %.0f clk per rep (isolated-rate sum %.0f)\n", MODE,
+         (MODE & 1) ? "TMEM-A N64 + smem-A N96" : "TMEM-A N64 only", (MODE & 2) ? ", +tcgen05.ld" : "",
+         (MODE & 4) ? ", +tcgen05.st" : "", (MODE & 8) ? ", +STS" : "", double(c) / 100.0, ideal);
 }
 
 static uint16_t f2bf(float f) {
@@ -289,6 +436,8 @@ int main() {
            mode == 0 ? "sliding windows, smem A" : mode == 1 ? "one D, smem A" : "sliding, TMEM A",
            static_cast<double>(c) / n);
   }
+  run_commit<0>(clk); run_commit<12>(clk); run_commit<-12>(clk); run_commit<-4>(clk);
+  run_mixed<0>(clk); run_mixed<1>(clk); run_mixed<2>(clk); run_mixed<3>(clk); run_mixed<4>(clk); run_mixed<5>(clk); run_mixed<8>(clk); run_mixed<9>(clk); run_mixed<15>(clk);
   run_fixed<16, 1>(clk); run_fixed<32, 1>(clk); run_fixed<48, 1>(clk); run_fixed<64, 1>(clk);
   run_fixed<96, 1>(clk); run_fixed<128, 1>(clk); run_fixed<32, 0>(clk); run_fixed<64, 0>(clk); run_fixed<96, 0>(clk);
   for (int st : {0, 1})

@@ -28,7 +28,7 @@ int main(int argc, char** argv) {
   cudaMalloc(&b1, c1 * 4);
   cudaMalloc(&b2, c2 * 4);
   cudaMalloc(&y, nb * G * G * c2 * 2);
-  cudaMalloc(&trace, 10 * 256 * 8);
+  cudaMalloc(&trace, 16 * 256 * 8);
   es::generate_features_bf16(1, nb * S * S, x, 0);
   es::generate_dense_layer(7, 0, 16, c1, std::sqrt(6.0f / (16 + c1)), w1, b1, 0);
   es::generate_dense_layer(7, 1, 9 * c1, c2, std::sqrt(6.0f / (9 * c1 + c2)), w2, b2, 0);
@@ -45,7 +45,7 @@ int main(int argc, char** argv) {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   for (int rep = 0; rep < 4; ++rep) {
-    cudaMemset(trace, 0, 10 * 256 * 8);
+    cudaMemset(trace, 0, 16 * 256 * 8);
     a.trace = rep == 3 ? trace : nullptr;
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
@@ -60,18 +60,21 @@ int main(int argc, char** argv) {
     std::printf("rep %d rc %d: %.3f ms = %.3e samples/s, %.0f ns per tile per CTA (%s)\n", rep, rc, ms,
                 nb / (ms * 1e-3), ms * 1e6 / tiles, cudaGetErrorString(cudaGetLastError()));
   }
-  std::vector<unsigned long long> t(10 * 256);
+  std::vector<unsigned long long> t(16 * 256);
   cudaMemcpy(t.data(), trace, t.size() * 8, cudaMemcpyDeviceToHost);
   unsigned long long t0 = ~0ull;
   for (auto v : t)
     if (v && v < t0) t0 = v;
   auto r = [&](int k, int i) { return t[k * 256 + i] ? (long long)(t[k * 256 + i] - t0) : -1ll; };
-  std::printf("pos   tma  c1_a1  c1_iss  epi_c1  epi_a2e  epi_done\n");
+  std::printf("pos   tma  c1_a1  c1_iss  epi_c1  epi_a2e  epi_done c1_issued\n");
   for (int n = 0; n < 130; ++n)
-    std::printf("%3d %7lld %7lld %7lld %7lld %7lld %7lld\n", n, r(0, n), r(1, n), r(2, n), r(3, n),
-                r(4, n), r(5, n));
-  std::printf("win  start  waited  issued\n");
-  for (int w = 0; w < 130; ++w) std::printf("%3d %7lld %7lld %7lld\n", w, r(6, w), r(7, w), r(8, w));
+    std::printf("%3d %7lld %7lld %7lld %7lld %7lld %7lld %7lld %7lld\n", n, r(0, n), r(1, n), r(2, n), r(3, n),
+                r(4, n), r(5, n), r(14, n), r(15, n));
+  std::printf("win  start  fed  waited  issued\n");
+  for (int w = 0; w < 130; ++w) std::printf("%3d %7lld %7lld %7lld %7lld\n", w, r(6, w), r(10, w), r(7, w), r(8, w));
+  std::printf("feed-block  pos  start  a1_ok  c1e_ok\n");
+  for (int n = 0; n < 130; ++n)
+    if (r(11, n) >= 0) std::printf("%3d %7lld %7lld %7lld\n", n, r(11, n), r(12, n), r(13, n));
   std::printf("blk  o_full\n");
   for (int b = 0; b < 100; ++b) std::printf("%3d %7lld\n", b, r(9, b));
   return 0;
