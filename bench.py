@@ -300,7 +300,7 @@ def launch_work(arch, names: list) -> list:
     L = len(dims)
     out, l = [], 0
     for n in names:
-        take = 2 if n.startswith(("conv_stack", "conv_rows")) or n.startswith("member_mlp2") or \
+        take = 2 if n.startswith(("conv_stack", "conv_rows", "conv_sweep")) or n.startswith("member_mlp2") or \
             n.startswith("mlp2_simt") or n.startswith("f32_conv") else 1
         f = float(sum(flops[l:l + take]))
         last = l + take == L

@@ -181,13 +181,14 @@ __device__ __forceinline__ void window(IssueCtx& c, int oh) {
 }
 
 // Patch row ih of strip ST for this lane's two samples; positions n0 .. n0+J-1.
-template <int ST>
+template <int ST, int SPL = kSampPerLane>
 __device__ __forceinline__ void build_row(const ConvRowsArgs& args, uint8_t* smem, const Bars& B,
-                                          long long s0, int ih, int warp, int lane, int n0) {
+                                          long long s0, int ih, int warp, int lane, int n0,
+                                          uint32_t off_a1 = kOffA1) {
   constexpr int J = ST ? 4 : 5, c0 = ST ? 3 : 0;
 #pragma unroll
-  for (int t = 0; t < kSampPerLane; ++t) {
-    const int smp = warp * 32 * kSampPerLane + t * 32 + lane;
+  for (int t = 0; t < SPL; ++t) {
+    const int smp = warp * 32 * SPL + t * 32 + lane;
     const long long s = s0 + smp;
     uint4 ch[4][3];
     const uint8_t* xrow = static_cast<const uint8_t*>(args.x) + s * (kS * kS * 2);
@@ -218,7 +219,7 @@ __device__ __forceinline__ void build_row(const ConvRowsArgs& args, uint8_t* sme
         w[r][0] = hi ? q.z : q.x;
         w[r][1] = hi ? q.w : q.y;
       }
-      uint8_t* a1 = smem + kOffA1 + sl * kA1Bytes + smp * 16;
+      uint8_t* a1 = smem + off_a1 + sl * kA1Bytes + smp * 16;
       *reinterpret_cast<uint4*>(a1) = make_uint4(w[0][0], w[0][1], w[1][0], w[1][1]);
       *reinterpret_cast<uint4*>(a1 + 2048) = make_uint4(w[2][0], w[2][1], w[3][0], w[3][1]);
     }
@@ -505,6 +506,465 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ====================================================================
+// conv_sweep_sm100: the input-sweep schedule (conv_rows_kernel.cuh).
+//
+// Each conv1 output A2(ih, iw) is consumed as soon as it exists: ONE set of
+// UMMAs with A read from TMEM adds it to all nine outputs it feeds.  The
+// output accumulator O holds three output rows of the strip, laid out
+// [j = ow - ow0][r = (oh + 1) mod 3] x 32 channels, so the nine taps of an
+// input are 9 CONTIGUOUS 32-column blocks (j = 2 - dw, r from dh); the B
+// operand is W2 with its tap blocks in that order, one copy per input-row
+// phase q = ih mod 3 (dh = (q + 2 - r) mod 3).  Interior inputs issue
+// N = 160 + 128 per K step (all 288 columns), strip-edge inputs N = 192 or
+// 96, and the image's top / bottom input rows one N = 64 UMMA per output
+// column (the two valid rows).  Every UMMA accumulates: the drain zeroes a
+// block after reading it, so the row that next uses the block starts at 0.
+namespace sweep {
+
+constexpr int kBuilders = 4;       // one sample per lane: one load round trip per patch row
+// kDrain drain warps: kDrain / 4 per TMEM lane quadrant
+template <int kDrain>
+__host__ __device__ constexpr int threads() { return 32 * (kBuilders + 10 + kDrain); }  // + conv1 issuer,
+                                                                     // conv2 issuer, 8 conv1 epilogue
+constexpr uint32_t kQBytes = 4 * 2 * 288 * 16;  // one W2 copy: [ks][plane][288 rows][16 B]
+constexpr uint32_t kOffW2 = 0;
+constexpr uint32_t kOffW1 = kOffW2 + 3 * kQBytes;
+constexpr uint32_t kOffA1 = kOffW1 + 2 * 64 * 16;
+// drain staging: per drain warp a ring of kOutStages boxes [32 samples][64 B]
+// (one O block of its lane quadrant), 64-byte swizzled, stored by TMA
+constexpr int kOutStages = 4;
+constexpr uint32_t kOutBox = 32 * 64;
+constexpr uint32_t kOffOut = kOffA1 + kA1Stages * kA1Bytes;
+constexpr uint32_t kOffBar = kOffOut + 4 * kOutStages * kOutBox;  // 4 drain warps
+constexpr int kNumBars = 2 * kA1Stages + 2 + 4 + 24;
+constexpr uint32_t kSmemBytes = kOffBar + kNumBars * 8 + 16 + 1024;
+// TMEM: O [0, 384), conv1 accumulator D1 [384, 448), two A2 slots [448, 512).
+constexpr uint32_t kTmO = 0, kTmD1 = 384, kTmA2 = 448;
+
+struct Bars {
+  uint64_t* a1_full;   // [kA1Stages] builders -> conv1 issuer
+  uint64_t* a1_empty;  // [kA1Stages]
+  uint64_t* c1_full;   // conv1 issuer -> epilogue
+  uint64_t* c1_empty;  // epilogue (8 warps) -> conv1 issuer
+  uint64_t* a2_full;   // [2] epilogue -> conv2 issuer
+  uint64_t* a2_empty;  // [2]
+  uint64_t* o_full;    // [12] block b = 3 j + r: conv2 issuer -> drain
+  uint64_t* o_empty;   // [12] drain (4 warps) -> conv2 issuer
+};
+
+// Strip geometry: strip 0 = output columns 0-3 from input columns 0-4,
+// strip 1 = output columns 4-6 from input columns 3-6.
+__host__ __device__ constexpr int c0(int st) { return st ? 3 : 0; }     // first input column
+__host__ __device__ constexpr int clast(int st) { return st ? 6 : 4; }  // last input column
+__host__ __device__ constexpr int ow0(int st) { return st ? 4 : 0; }    // first output column
+__host__ __device__ constexpr int nw(int st) { return st ? 3 : 4; }     // output columns
+__host__ __device__ constexpr int slot_r(int oh) { return (oh + 1) % 3; }
+__host__ __device__ constexpr int block(int st, int oh, int ow) { return 3 * (ow - ow0(st)) + slot_r(oh); }
+__host__ __device__ constexpr bool in_strip(int st, int ow) { return ow >= ow0(st) && ow < ow0(st) + nw(st); }
+// (oh, ow) is first touched by input (max(oh - 1, 0), max(ow - 1, c0)) and
+// complete after input (min(oh + 1, 6), min(ow + 1, clast)) -- row-major order.
+__host__ __device__ constexpr bool first_at(int st, int ih, int iw, int oh, int ow) {
+  return in_strip(st, ow) && oh >= 0 && oh < kG && (oh - 1 > 0 ? oh - 1 : 0) == ih &&
+         (ow - 1 > c0(st) ? ow - 1 : c0(st)) == iw;
+}
+__host__ __device__ constexpr bool last_at(int st, int ih, int iw, int oh, int ow) {
+  return in_strip(st, ow) && oh >= 0 && oh < kG && (oh + 1 < kG - 1 ? oh + 1 : kG - 1) == ih &&
+         (ow + 1 < clast(st) ? ow + 1 : clast(st)) == iw;
+}
+
+struct Ctx {
+  uint32_t tbase;
+  uint64_t w2d;  // planar descriptor of W2 copy 0, K step 0
+  Bars b;
+  uint32_t ouse;  // per O block: parity of its next empty-wait
+  unsigned long long* trace;
+  int debug;
+};
+
+template <int N>
+__device__ __forceinline__ void mma(uint32_t d, uint32_t a, uint64_t b) {
+  umma_bf16_ta(d, a, b, idesc_bf16_f32(128, N), 1u);
+}
+
+// Input (IH, IW) of strip ST: A2 slot `slot` into every output it feeds.
+template <int ST, int IH, int IW>
+__device__ __forceinline__ void sweep_input(Ctx& c, uint32_t n) {
+  constexpr int q = IH % 3;
+  constexpr int jlo = ow0(ST) - (IW - 1) > 0 ? ow0(ST) - (IW - 1) : 0;
+  constexpr int jhi = ow0(ST) + nw(ST) - IW < 2 ? ow0(ST) + nw(ST) - IW : 2;
+  constexpr int nj = jhi - jlo + 1;
+  constexpr int rlo = IH == 0 ? 1 : 0;             // row -1 does not exist
+  constexpr int nr = IH == 0 || IH == kG - 1 ? 2 : 3;  // nor row 7
+  const uint32_t slot = n & 1u;
+  unsigned long long* trace = c.trace;
+  TRACE(6, static_cast<int>(n));
+  const bool pipe_only = (c.debug & 1024) != 0;  // timing probe: the UMMA stream alone
+  if (!pipe_only) mbar_wait(&c.b.a2_full[slot], (n >> 1) & 1u);
+#pragma unroll
+  for (int oh = 0; oh < kG; ++oh)
+#pragma unroll
+    for (int ow = 0; ow < kG; ++ow)
+      if (first_at(ST, IH, IW, oh, ow) && !pipe_only) {
+        const int b = block(ST, oh, ow);
+        mbar_wait(&c.b.o_empty[b], ((c.ouse >> b) & 1u) ^ 1u);
+        c.ouse ^= 1u << b;
+      }
+  tc_fence_after();
+  TRACE(7, static_cast<int>(n));
+  Ctx cw = c;
+  asm volatile("" : "+l"(cw.w2d), "+r"(cw.tbase));
+  const uint32_t a = cw.tbase + kTmA2 + 32u * slot;
+  const uint32_t d0 = cw.tbase + kTmO + 96u * (IW - 1 + jlo - ow0(ST));
+  const uint64_t b0 = cw.w2d + (q * kQBytes >> 4) + 32u * 3u * jlo;
+  if (elect_one()) {
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      const uint64_t bk = b0 + ((ks * 2 * 288 * 16) >> 4);
+      const uint32_t ak = a + 8u * ks;
+      if constexpr (nr == 3) {
+        if constexpr (nj == 3) {
+          mma<160>(d0, ak, bk);
+          mma<128>(d0 + 160u, ak, bk + 160u);
+        } else {
+          mma<96 * nj>(d0, ak, bk);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < nj; ++j) mma<64>(d0 + 96u * j + 32u * rlo, ak, bk + 96u * j + 32u * rlo);
+      }
+    }
+    if (!pipe_only) {
+      umma_commit(&c.b.a2_empty[slot]);
+#pragma unroll
+      for (int oh = 0; oh < kG; ++oh)
+#pragma unroll
+        for (int ow = 0; ow < kG; ++ow)
+          if (last_at(ST, IH, IW, oh, ow)) umma_commit(&c.b.o_full[block(ST, oh, ow)]);
+    }
+  }
+  __syncwarp();
+  TRACE(8, static_cast<int>(n));
+}
+
+template <int ST, int IH>
+__device__ __forceinline__ void sweep_row(Ctx& c, uint32_t& n) {
+  sweep_input<ST, IH, c0(ST)>(c, n++);
+  sweep_input<ST, IH, c0(ST) + 1>(c, n++);
+  sweep_input<ST, IH, c0(ST) + 2>(c, n++);
+  sweep_input<ST, IH, c0(ST) + 3>(c, n++);
+  if constexpr (ST == 0) sweep_input<ST, IH, 4>(c, n++);
+}
+
+template <int ST>
+__device__ __forceinline__ void sweep_strip(Ctx& c, uint32_t& n) {
+  sweep_row<ST, 0>(c, n);
+  sweep_row<ST, 1>(c, n);
+  sweep_row<ST, 2>(c, n);
+  sweep_row<ST, 3>(c, n);
+  sweep_row<ST, 4>(c, n);
+  sweep_row<ST, 5>(c, n);
+  sweep_row<ST, 6>(c, n);
+}
+
+template <int kDrain>
+__global__ void __launch_bounds__(threads<kDrain>(), 1)
+    conv_sweep_sm100(const __grid_constant__ CUtensorMap tm_out, const ConvRowsArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align_smem_1024(smem_raw);
+  uint64_t* bar0 = reinterpret_cast<uint64_t*>(smem + kOffBar);
+  Bars B;
+  B.a1_full = bar0;
+  B.a1_empty = B.a1_full + kA1Stages;
+  B.c1_full = B.a1_empty + kA1Stages;
+  B.c1_empty = B.c1_full + 1;
+  B.a2_full = B.c1_empty + 1;
+  B.a2_empty = B.a2_full + 2;
+  B.o_full = B.a2_empty + 2;
+  B.o_empty = B.o_full + 12;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(B.o_empty + 12);
+  es::Bars rb;  // the builders' view (a1 ring only)
+  rb.a1_full = B.a1_full;
+  rb.a1_empty = B.a1_empty;
+
+  const int warp = warp_uniform_id();
+  const int lane = threadIdx.x & 31;
+  unsigned long long* const trace = blockIdx.x == 0 ? args.trace : nullptr;
+  const long long row_begin = args.claim ? args.claim->row_begin : args.row_begin;
+  const long long row_end = args.claim ? args.claim->row_end : args.row_end;
+  const long long tiles = (row_end - row_begin + kTile - 1) / kTile;
+  const int my_tiles =
+      blockIdx.x < tiles ? static_cast<int>((tiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kA1Stages; ++i) {
+      mbar_init(&B.a1_full[i], kBuilders);
+      mbar_init(&B.a1_empty[i], 1);
+    }
+    mbar_init(B.c1_full, 1);
+    mbar_init(B.c1_empty, 8);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&B.a2_full[i], 8);
+      mbar_init(&B.a2_empty[i], 1);
+    }
+    for (int i = 0; i < 12; ++i) {
+      mbar_init(&B.o_full[i], 1);
+      mbar_init(&B.o_empty[i], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc(tmem_slot, 512);
+
+  // Resident weights.  W2 copy q -> [ks][plane][row = 32 k + co][8 ci], block
+  // k = 3 j + r holding tap (dh = (q + 2 - r) mod 3, dw = 2 - j).  W1 as in
+  // conv_rows_sm100.
+  {
+    const uint4* w2 = static_cast<const uint4*>(args.w2);  // [32][72 chunks of 8]
+    for (int i = threadIdx.x; i < 3 * 288 * 8; i += threads<kDrain>()) {
+      const int q = i / 2304, rem = i % 2304, row = rem >> 3, ch = rem & 7;
+      const int ks = ch >> 1, pl = ch & 1, k = row >> 5, co = row & 31;
+      const int j = k / 3, r = k % 3, dh = (q + 2 - r) % 3, dw = 2 - j;
+      *reinterpret_cast<uint4*>(smem + kOffW2 + q * kQBytes + (ks * 2 + pl) * (288 * 16) + row * 16) =
+          w2[co * 72 + (3 * dh + dw) * 8 + ch];
+    }
+    const uint4* w1 = static_cast<const uint4*>(args.w1);  // [64][2 chunks of 8]
+    for (int i = threadIdx.x; i < 2 * 64; i += threads<kDrain>()) {
+      const int cc = i >> 1, pl = i & 1;
+      *reinterpret_cast<uint4*>(smem + kOffW1 + (pl * 64 + cc) * 16) = w1[i];
+    }
+  }
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+  if (warp >= kBuilders + 10) {  // O starts at zero (every UMMA accumulates)
+    uint32_t z[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) z[i] = 0u;
+    const uint32_t lf = static_cast<uint32_t>((warp & 3) * 32) << 16;
+#pragma unroll
+    for (int cb = 0; cb < 12; ++cb) tmem_st32(tmem_base + lf + kTmO + 32u * cb, z);
+    tmem_st_wait();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+
+  if (args.debug & 1024) {  // timing probe: the conv2 UMMA stream alone, no data
+    if (warp == kBuilders + 1) {
+      Ctx c;
+      c.tbase = __shfl_sync(0xffffffffu, tmem_base, 0);
+      c.w2d = sdesc_planar(__shfl_sync(0xffffffffu, smem_u32(smem + kOffW2), 0), 288 * 16);
+      c.b = B;
+      c.ouse = 0;
+      c.trace = trace;
+      c.debug = args.debug;
+      uint32_t n = 0;
+      for (int k = 0; k < my_tiles; ++k) {
+        sweep_strip<0>(c, n);
+        sweep_strip<1>(c, n);
+      }
+      if (elect_one()) umma_commit(B.c1_full);
+      __syncwarp();
+      mbar_wait(B.c1_full, 0);
+    }
+  } else if (warp < kBuilders) {
+    // --------------------------------------------- im2col builders (as conv_rows)
+    int n = 0;
+    for (int k = 0; k < my_tiles; ++k) {
+      const long long s0 = row_begin + (blockIdx.x + static_cast<long long>(k) * gridDim.x) * kTile;
+      // the next tile's images (contiguous rows of x) into L2 while this one is built
+      const long long s1 = s0 + static_cast<long long>(gridDim.x) * kTile;
+      if (warp == 0 && lane == 0 && k + 1 < my_tiles) {
+        const long long e1 = s1 + kTile < args.x_rows ? s1 + kTile : args.x_rows;
+        if (e1 > s1)
+          prefetch_l2_bulk(static_cast<const uint8_t*>(args.x) + s1 * (kS * kS * 2),
+                           static_cast<uint32_t>((e1 - s1) * (kS * kS * 2)));
+      }
+      for (int ih = 0; ih < kG; ++ih) {
+        build_row<0, 1>(args, smem, rb, s0, ih, warp, lane, n, kOffA1);
+        n += 5;
+      }
+      for (int ih = 0; ih < kG; ++ih) {
+        build_row<1, 1>(args, smem, rb, s0, ih, warp, lane, n, kOffA1);
+        n += 4;
+      }
+    }
+  } else if (warp == kBuilders) {
+    // ------------------------------------------------------- conv1 issuer
+    const uint32_t tbase = __shfl_sync(0xffffffffu, tmem_base, 0);
+    const uint32_t a1_base = __shfl_sync(0xffffffffu, smem_u32(smem + kOffA1), 0);
+    const uint64_t w1d = sdesc_planar(__shfl_sync(0xffffffffu, smem_u32(smem + kOffW1), 0), 1024);
+    constexpr uint32_t id1 = idesc_bf16_f32(128, kC1);
+    const int npos = my_tiles * 63;
+    int sl = 0;
+    uint32_t slpar = 0;
+    for (int n = 0; n < npos; ++n) {
+      mbar_wait(&B.a1_full[sl], slpar);
+      mbar_wait(B.c1_empty, (static_cast<uint32_t>(n) & 1u) ^ 1u);
+      tc_fence_after();
+      if (elect_one()) {
+        umma_bf16(tbase + kTmD1, sdesc_planar(a1_base + sl * kA1Bytes, 2048), w1d, id1, 0);
+        umma_commit(B.c1_full);
+        umma_commit(&B.a1_empty[sl]);
+      }
+      __syncwarp();
+      if (++sl == kA1Stages) {
+        sl = 0;
+        slpar ^= 1u;
+      }
+    }
+  } else if (warp == kBuilders + 1) {
+    // ------------------------------------------------------- conv2 issuer
+    Ctx c;
+    c.tbase = __shfl_sync(0xffffffffu, tmem_base, 0);
+    c.w2d = sdesc_planar(__shfl_sync(0xffffffffu, smem_u32(smem + kOffW2), 0), 288 * 16);
+    c.b = B;
+    c.ouse = 0;
+    c.trace = trace;
+    c.debug = args.debug;
+    uint32_t n = 0;
+    for (int k = 0; k < my_tiles; ++k) {
+      sweep_strip<0>(c, n);
+      sweep_strip<1>(c, n);
+    }
+  } else if (warp < kBuilders + 10) {
+    // ---------------------------------------------------- conv1 epilogue
+    // Eight warps: lane quadrant warp & 3, channel half h.  relu(D1 + b1) as
+    // bf16 pairs into A2 slot n & 1 (the conv2 UMMAs read A from TMEM).
+    const int e = warp - kBuilders - 2, h = e >> 2;
+    const uint32_t lf = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const int npos = my_tiles * 63;
+    for (int n = 0; n < npos; ++n) {
+      mbar_wait(B.c1_full, static_cast<uint32_t>(n) & 1u);
+      const uint32_t slot = static_cast<uint32_t>(n) & 1u;
+      if (args.debug & 16) {  // timing probe (results wrong): no TMEM traffic
+        __syncwarp();
+        if (lane == 0) mbar_arrive(B.c1_empty);
+        mbar_wait(&B.a2_empty[slot], ((static_cast<uint32_t>(n) >> 1) & 1u) ^ 1u);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&B.a2_full[slot]);
+        continue;
+      }
+      tc_fence_after();
+      uint32_t v[32];
+      tmem_ld32_raw(tmem_base + lf + kTmD1 + 32u * h, v);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(B.c1_empty);
+      uint32_t pk[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        pk[i] = pack_relu_bf16(v[2 * i], v[2 * i + 1], args.b1c[32 * h + 2 * i], args.b1c[32 * h + 2 * i + 1]);
+      mbar_wait(&B.a2_empty[slot], ((static_cast<uint32_t>(n) >> 1) & 1u) ^ 1u);
+      tc_fence_after();
+      tmem_st16(tmem_base + lf + kTmA2 + 32u * slot + 16u * h, pk);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&B.a2_full[slot]);
+    }
+  } else {
+    // ---------------------------------------------------------- output drain
+    // Blocks in completion order: read, zero (the block's next row starts at
+    // 0), release, then bias + ReLU + bf16 into a swizzled staging box that
+    // one TMA store writes as 32 rows x 64 B (per-lane 16-byte stores to rows
+    // 3136 B apart were LSU-bound: the drain, not the tensor pipe, set the
+    // kernel's pace).  A partial last tile takes per-lane stores of its valid
+    // rows instead (a claimed run must not write past its rows).
+    // Drain warp dw: lane quadrant dw & 3; the two warps of a quadrant take
+    // alternate blocks of the completion order.
+    const int dw = warp - kBuilders - 10, qd = warp & 3, grp = dw >> 2;
+    const uint32_t lf = static_cast<uint32_t>(qd * 32) << 16;
+    const int row = qd * 32 + lane;
+    uint8_t* const ring = smem + kOffOut + dw * (kOutStages * kOutBox);
+    int seq = 0;
+    uint32_t z[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) z[i] = 0u;
+    uint32_t opar = 0, nst = 0;
+    for (int k = 0; k < my_tiles; ++k) {
+      const long long s0 = row_begin + (blockIdx.x + static_cast<long long>(k) * gridDim.x) * kTile;
+      const long long s = s0 + row;
+      uint8_t* dst_row = static_cast<uint8_t*>(args.out) + s * (kOutRow * 2);
+      const bool valid = s < row_end;
+      const bool full = s0 + kTile <= row_end;
+      for (int st = 0; st < 2; ++st)
+        for (int ih = 0; ih < kG; ++ih)
+          for (int iw = c0(st); iw <= clast(st); ++iw)
+            for (int oh = ih - 1; oh <= ih; ++oh)
+              for (int ow = iw - 1; ow <= iw; ++ow) {
+                if (!last_at(st, ih, iw, oh, ow)) continue;
+                const int b = block(st, oh, ow);
+                const uint32_t par = (opar >> b) & 1u;
+                opar ^= 1u << b;
+                ++seq;
+                if (kDrain > 4 && (seq & 1) != grp) continue;
+                mbar_wait(&B.o_full[b], par);
+                unsigned long long* const tr = qd == 0 && grp == 0 && lane == 0 ? trace : nullptr;
+                { unsigned long long* trace = tr; TRACE(9, seq >> (kDrain > 4)); }
+                tc_fence_after();
+                uint32_t v[32];
+                const uint32_t src = tmem_base + lf + kTmO + 32u * b;
+                tmem_ld32_raw(src, v);
+                tmem_ld_wait();
+                if (!(args.debug & 128)) {  // bit 128: timing probe, no zeroing (results wrong)
+                  tmem_st32(src, z);
+                  tmem_st_wait();
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&B.o_empty[b]);
+                { unsigned long long* trace = tr; TRACE(10, seq >> (kDrain > 4)); }
+                if (args.debug & 32) continue;  // timing probe: no output stores
+                uint4 q[4];
+#pragma unroll
+                for (int cc = 0; cc < 4; ++cc)
+                  q[cc] = make_uint4(
+                      pack_relu_bf16(v[8 * cc], v[8 * cc + 1], args.b2c[8 * cc], args.b2c[8 * cc + 1]),
+                      pack_relu_bf16(v[8 * cc + 2], v[8 * cc + 3], args.b2c[8 * cc + 2], args.b2c[8 * cc + 3]),
+                      pack_relu_bf16(v[8 * cc + 4], v[8 * cc + 5], args.b2c[8 * cc + 4], args.b2c[8 * cc + 5]),
+                      pack_relu_bf16(v[8 * cc + 6], v[8 * cc + 7], args.b2c[8 * cc + 6], args.b2c[8 * cc + 7]));
+                if (full) {
+                  uint8_t* box = ring + (nst % kOutStages) * kOutBox;
+                  if (lane == 0) tma_store_wait_read<kOutStages - 1>();  // the box's last store read it
+                  __syncwarp();
+                  if (!(args.debug & 512)) {  // bit 512: timing probe, no staging stores
+#pragma unroll
+                    for (int cc = 0; cc < 4; ++cc)
+                      *reinterpret_cast<uint4*>(box + lane * 64 + ((cc ^ ((lane >> 1) & 3)) << 4)) = q[cc];
+                    fence_proxy_async_smem();
+                  }
+                  __syncwarp();
+                  if (lane == 0 && !(args.debug & 256)) {  // bit 256: timing probe, no TMA store
+                    tma_store_2d(&tm_out, box, (oh * kG + ow) * kC2, static_cast<int32_t>(s0 + qd * 32));
+                    tma_store_commit();
+                  }
+                  ++nst;
+                  { unsigned long long* trace = tr; TRACE(11, seq >> (kDrain > 4)); }
+                } else if (valid) {
+                  uint4* dst = reinterpret_cast<uint4*>(dst_row + (oh * kG + ow) * kC2 * 2);
+#pragma unroll
+                  for (int cc = 0; cc < 4; ++cc) dst[cc] = q[cc];
+                }
+              }
+    }
+    if (lane == 0) tma_store_wait_all<0>();
+    __syncwarp();
+  }
+
+  __syncthreads();
+  if (warp == 0) {
+    __syncwarp();
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 512);
+  }
+}
+
+}  // namespace sweep
+
 }  // namespace
 
 bool conv_rows_supported(int S, int P, int c1, int c2) {
@@ -524,6 +984,26 @@ int conv_rows_launch(const ConvRowsArgs& args, const void* x, long long x_rows, 
   a.x = x;
   a.x_rows = x_rows;
   conv_rows_sm100<<<grid, kThreads, kSmemBytes, stream>>>(a);
+  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+
+int conv_sweep_launch(const ConvRowsArgs& args, const void* x, long long x_rows, int grid,
+                      cudaStream_t stream) {
+  if (x_rows > INT_MAX) return -1;
+  const long long tiles = (args.row_end - args.row_begin + kTile - 1) / kTile;
+  if (tiles <= 0) return 0;
+  grid = static_cast<int>(std::min<long long>(grid, tiles));
+  if (ensure_smem_attr(sweep::conv_sweep_sm100<4>, static_cast<int>(sweep::kSmemBytes)) != 0)
+    return -4;
+  // output rows [0, row_end): TMA stores only ever cover whole tiles inside it
+  CUtensorMap tm_out;
+  if (make_bf16_map_box(&tm_out, args.out, kOutRow, static_cast<uint64_t>(args.row_end), 32, 32,
+                        CU_TENSOR_MAP_SWIZZLE_64B) != 0)
+    return -2;
+  ConvRowsArgs a = args;
+  a.x = x;
+  a.x_rows = x_rows;
+  sweep::conv_sweep_sm100<4><<<grid, sweep::threads<4>(), sweep::kSmemBytes, stream>>>(tm_out, a);
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 

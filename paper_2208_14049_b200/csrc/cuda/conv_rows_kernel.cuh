@@ -67,5 +67,10 @@ bool conv_rows_supported(int S, int P, int c1, int c2);
 // x: bf16 [x_rows][784].
 int conv_rows_launch(const ConvRowsArgs& args, const void* x, long long x_rows, int grid,
                      cudaStream_t stream);
+// The input-sweep schedule of the same stack (conv_rows_kernel.cu, namespace
+// sweep): each conv1 output feeds all nine of its outputs at once, every conv2
+// UMMA reads A from TMEM.
+int conv_sweep_launch(const ConvRowsArgs& args, const void* x, long long x_rows, int grid,
+                      cudaStream_t stream);
 
 }  // namespace es

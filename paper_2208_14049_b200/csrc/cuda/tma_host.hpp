@@ -63,6 +63,22 @@ inline int make_bf16_map_plain(CUtensorMap* map, const void* base, uint64_t inne
   return r == CUDA_SUCCESS ? 0 : -2;
 }
 
+// bf16 [rows][inner] row-major, box = box_inner x box_rows with the given
+// shared-memory swizzle (box_inner * 2 bytes must match the swizzle span).
+inline int make_bf16_map_box(CUtensorMap* map, const void* base, uint64_t inner, uint64_t rows,
+                             uint32_t box_inner, uint32_t box_rows, CUtensorMapSwizzle swizzle) {
+  EncodeTiledFn fn = encode_tiled_fn();
+  if (!fn) return -1;
+  cuuint64_t dims[2] = {inner, rows};
+  cuuint64_t strides[1] = {inner * 2};
+  cuuint32_t box[2] = {box_inner, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -2;
+}
+
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device).
 template <typename Kernel>
 int ensure_smem_attr(Kernel kernel, int bytes) {

@@ -76,7 +76,9 @@ struct DeviceMember::Impl {
   es::DenseLayout logits{};            // Head::Dense: the last layer
   bool cnn = false;
   es::ConvLayout conv{};  // CNN: the convolution stack (layers 0 and 1)
-  bool conv_rows = false;  // CNN-s shape: the samples-in-M kernel (conv_rows_kernel.cuh)
+  // CNN-s shape: a samples-in-M kernel (conv_rows_kernel.cuh): 2 = the input
+  // sweep (default), 1 = the row windows (ES_CONV_SCHEDULE=rows), 0 = neither.
+  int conv_rows = 0;
   void* weights = nullptr;
   std::vector<std::size_t> w_off, b_off;  // per layer
   std::vector<float> conv_b1, conv_b2;      // CNN: conv biases, host copies
@@ -125,11 +127,15 @@ bool DeviceMember::load(int device, const ModelSpec& model, int batch, bool fp32
   if (a.kind == MemberArch::Kind::CNN) {
     // Leading layers: the fused convolution stack, bf16 [(S/P)^2 * c2] rows out.
     I.cnn = true;
-    const char* cs = std::getenv("ES_CONV_SCHEDULE");  // tests: "tap" | "split"
+    const char* cs = std::getenv("ES_CONV_SCHEDULE");  // tests: "tap" | "split" | "rows"
+    const bool rows = cs && std::strcmp(cs, "rows") == 0;
+    if (rows) cs = nullptr;
     const int sched = cs && std::strcmp(cs, "tap") == 0 ? 1 : cs && std::strcmp(cs, "split") == 0 ? 2 : 0;
     // Default for the CNN-s shape: samples in M (measured on B200);
     // "tap" / "split" select the positions-in-M kernel for comparison.
-    I.conv_rows = !cs && es::conv_rows_supported(a.widths[0], a.widths[1], a.widths[2], a.widths[3]);
+    I.conv_rows = !cs && es::conv_rows_supported(a.widths[0], a.widths[1], a.widths[2], a.widths[3])
+                      ? (rows ? 1 : 2)
+                      : 0;
     // ES_CONV_SCHEDULE=split falls back to tap where the shape has no split plan.
     if (!es::conv_plan(a.widths[0], a.widths[1], a.widths[2], a.widths[3], &I.conv, sched) &&
         !(sched == 2 && es::conv_plan(a.widths[0], a.widths[1], a.widths[2], a.widths[3], &I.conv, 1)))
@@ -230,7 +236,7 @@ std::vector<std::string> DeviceMember::kernel_names() const {
     return n;
   }
   if (I.cnn)
-    n.push_back(I.conv_rows ? "conv_rows_sm100" : I.conv.split ? "conv_stack_sm100[split]" : "conv_stack_sm100[tap]");
+    n.push_back(I.conv_rows == 2 ? "conv_sweep_sm100" : I.conv_rows ? "conv_rows_sm100" : I.conv.split ? "conv_stack_sm100[split]" : "conv_stack_sm100[tap]");
   for (const auto& d : I.dense) n.push_back(d.pair ? "dense_pair_sm100" : "dense_sm100");
   if (env_is("ES_MEMBER_KERNEL", "simt") && I.head != Impl::Head::Dense) {
     n.push_back("mlp2_simt_kernel");
@@ -290,7 +296,8 @@ int DeviceMember::forward(const void* x, long long nb, int seg_size, long long s
     std::copy(I.conv_b1.begin(), I.conv_b1.end(), c.b1c);
     std::copy(I.conv_b2.begin(), I.conv_b2.end(), c.b2c);
     c.out = I.act[0];
-    M_LAUNCH(es::conv_rows_launch(c, cur, nb, grid, stream));
+    M_LAUNCH(I.conv_rows == 2 ? es::conv_sweep_launch(c, cur, nb, grid, stream)
+                              : es::conv_rows_launch(c, cur, nb, grid, stream));
     mark(launches++);
     cur = I.act[0];
   } else if (I.cnn) {

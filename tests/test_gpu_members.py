@@ -80,11 +80,12 @@ CNN_SHAPES = [(28, 4, 64, 32, 128, 10), (28, 4, 32, 64, 256, 10), (16, 4, 64, 32
 
 @pytest.mark.parametrize("shape", CNN_SHAPES)
 @pytest.mark.parametrize("b", [32, 128])
-@pytest.mark.parametrize("schedule", ["auto", "tap", "split"])
+@pytest.mark.parametrize("schedule", ["auto", "tap", "split", "rows"])
 def test_cnn_member_matches_cpu_oracle(shape, b, schedule, monkeypatch):
-    """Both conv2 schedules (conv_kernel.cuh): "auto" takes the split
-    schedule where the shape allows it (R | 32, c1 % 64 == 0), "tap" forces
-    the tap-by-tap one."""
+    """Every conv2 schedule: "auto" takes the input sweep (conv_rows_kernel.cuh)
+    for the CNN-s shape and otherwise the split schedule of conv_kernel.cuh
+    where the shape allows it (R | 32, c1 % 64 == 0); "tap" forces the
+    tap-by-tap one, "rows" the row-window samples-in-M kernel."""
     if schedule != "auto":
         monkeypatch.setenv("ES_CONV_SCHEDULE", schedule)
     S = shape[0]

@@ -18,6 +18,7 @@ int main(int argc, char** argv) {
   const long long nb = argc > 1 ? std::atoll(argv[1]) : (1 << 20);
   const int grid_div = argc > 2 ? std::atoi(argv[2]) : 1;
   const int debug = argc > 3 ? std::atoi(argv[3]) : 0;
+  const bool sweep = argc > 4 && std::atoi(argv[4]) != 0;  // conv_sweep_sm100
   const int S = 28, G = 7, c1 = 64, c2 = 32;
   __nv_bfloat16 *x, *w1, *w2, *y;
   float *b1, *b2;
@@ -51,7 +52,8 @@ int main(int argc, char** argv) {
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    const int rc = es::conv_rows_launch(a, x, nb, sms / grid_div, 0);
+    const int rc = sweep ? es::conv_sweep_launch(a, x, nb, sms / grid_div, 0)
+                         : es::conv_rows_launch(a, x, nb, sms / grid_div, 0);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
@@ -75,7 +77,7 @@ int main(int argc, char** argv) {
   std::printf("feed-block  pos  start  a1_ok  c1e_ok\n");
   for (int n = 0; n < 130; ++n)
     if (r(11, n) >= 0) std::printf("%3d %7lld %7lld %7lld\n", n, r(11, n), r(12, n), r(13, n));
-  std::printf("blk  o_full\n");
-  for (int b = 0; b < 100; ++b) std::printf("%3d %7lld\n", b, r(9, b));
+  std::printf("blk  o_full  released  stored\n");
+  for (int b = 0; b < 256; ++b) std::printf("%3d %7lld %7lld %7lld\n", b, r(9, b), r(10, b), r(11, b));
   return 0;
 }
