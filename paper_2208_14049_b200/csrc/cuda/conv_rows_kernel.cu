@@ -523,9 +523,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 namespace sweep {
 
 constexpr int kBuilders = 4;       // one sample per lane: one load round trip per patch row
-// kDrain drain warps: kDrain / 4 per TMEM lane quadrant
-template <int kDrain>
-__host__ __device__ constexpr int threads() { return 32 * (kBuilders + 10 + kDrain); }  // + conv1 issuer,
+// Warp roles: kBuilders im2col builders, the conv1 issuer, the conv2 issuer,
+// kEpi conv1-epilogue warps (one per TMEM lane quadrant, all 64 channels;
+// eight warps of 32 channels measured the same), kDrain drain warps, and a
+// watcher that only runs under tools/trace_rows.cu.
+constexpr int kEpi = 4;
+constexpr int kDrain = 4;
+constexpr int kThreads = 32 * (kBuilders + 2 + kEpi + kDrain + 1);  // + conv1 issuer,
                                                                      // conv2 issuer, 8 conv1 epilogue
 constexpr uint32_t kQBytes = 4 * 2 * 288 * 16;  // one W2 copy: [ks][plane][288 rows][16 B]
 constexpr uint32_t kOffW2 = 0;
@@ -537,7 +541,7 @@ constexpr int kOutStages = 4;
 constexpr uint32_t kOutBox = 32 * 64;
 constexpr uint32_t kOffOut = kOffA1 + kA1Stages * kA1Bytes;
 constexpr uint32_t kOffBar = kOffOut + 4 * kOutStages * kOutBox;  // 4 drain warps
-constexpr int kNumBars = 2 * kA1Stages + 2 + 4 + 24;
+constexpr int kNumBars = 2 * kA1Stages + 2 + 4 + 24 + 1;
 constexpr uint32_t kSmemBytes = kOffBar + kNumBars * 8 + 16 + 1024;
 // TMEM: O [0, 384), conv1 accumulator D1 [384, 448), two A2 slots [448, 512).
 constexpr uint32_t kTmO = 0, kTmD1 = 384, kTmA2 = 448;
@@ -573,13 +577,38 @@ __host__ __device__ constexpr bool last_at(int st, int ih, int iw, int oh, int o
          (ow + 1 < clast(st) ? ow + 1 : clast(st)) == iw;
 }
 
+// The drain's walk: O blocks of one tile in completion order (block id and
+// output position oh * 7 + ow), a compile-time table so the drain's control
+// flow is one constant-bank load per block (the nested loop with run-time
+// last_at() tests cost ~600 clk per block of dependent integer issue).
+struct DrainSeq {
+  uint8_t blk[kG * kG];
+  uint8_t pos[kG * kG];
+};
+__host__ __device__ constexpr DrainSeq make_drain_seq() {
+  DrainSeq d{};
+  int k = 0;
+  for (int st = 0; st < 2; ++st)
+    for (int ih = 0; ih < kG; ++ih)
+      for (int iw = c0(st); iw <= clast(st); ++iw)
+        for (int oh = ih - 1; oh <= ih; ++oh)
+          for (int ow = iw - 1; ow <= iw; ++ow)
+            if (last_at(st, ih, iw, oh, ow)) {
+              d.blk[k] = static_cast<uint8_t>(block(st, oh, ow));
+              d.pos[k] = static_cast<uint8_t>(oh * kG + ow);
+              ++k;
+            }
+  return d;
+}
+__constant__ DrainSeq kDrainSeq = make_drain_seq();
+
 struct Ctx {
   uint32_t tbase;
   uint64_t w2d;  // planar descriptor of W2 copy 0, K step 0
   Bars b;
   uint32_t ouse;  // per O block: parity of its next empty-wait
   unsigned long long* trace;
-  int debug;
+  uint64_t* done;  // trace only: a commit per input, watched by the last warp
 };
 
 template <int N>
@@ -599,13 +628,12 @@ __device__ __forceinline__ void sweep_input(Ctx& c, uint32_t n) {
   const uint32_t slot = n & 1u;
   unsigned long long* trace = c.trace;
   TRACE(6, static_cast<int>(n));
-  const bool pipe_only = (c.debug & 1024) != 0;  // timing probe: the UMMA stream alone
-  if (!pipe_only) mbar_wait(&c.b.a2_full[slot], (n >> 1) & 1u);
+  mbar_wait(&c.b.a2_full[slot], (n >> 1) & 1u);
 #pragma unroll
   for (int oh = 0; oh < kG; ++oh)
 #pragma unroll
     for (int ow = 0; ow < kG; ++ow)
-      if (first_at(ST, IH, IW, oh, ow) && !pipe_only) {
+      if (first_at(ST, IH, IW, oh, ow)) {
         const int b = block(ST, oh, ow);
         mbar_wait(&c.b.o_empty[b], ((c.ouse >> b) & 1u) ^ 1u);
         c.ouse ^= 1u << b;
@@ -634,14 +662,13 @@ __device__ __forceinline__ void sweep_input(Ctx& c, uint32_t n) {
         for (int j = 0; j < nj; ++j) mma<64>(d0 + 96u * j + 32u * rlo, ak, bk + 96u * j + 32u * rlo);
       }
     }
-    if (!pipe_only) {
-      umma_commit(&c.b.a2_empty[slot]);
+    umma_commit(&c.b.a2_empty[slot]);
+    if (c.trace) umma_commit(c.done);
 #pragma unroll
-      for (int oh = 0; oh < kG; ++oh)
+    for (int oh = 0; oh < kG; ++oh)
 #pragma unroll
-        for (int ow = 0; ow < kG; ++ow)
-          if (last_at(ST, IH, IW, oh, ow)) umma_commit(&c.b.o_full[block(ST, oh, ow)]);
-    }
+      for (int ow = 0; ow < kG; ++ow)
+        if (last_at(ST, IH, IW, oh, ow)) umma_commit(&c.b.o_full[block(ST, oh, ow)]);
   }
   __syncwarp();
   TRACE(8, static_cast<int>(n));
@@ -667,8 +694,7 @@ __device__ __forceinline__ void sweep_strip(Ctx& c, uint32_t& n) {
   sweep_row<ST, 6>(c, n);
 }
 
-template <int kDrain>
-__global__ void __launch_bounds__(threads<kDrain>(), 1)
+__global__ void __launch_bounds__(kThreads, 1)
     conv_sweep_sm100(const __grid_constant__ CUtensorMap tm_out, const ConvRowsArgs args) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align_smem_1024(smem_raw);
@@ -682,7 +708,8 @@ __global__ void __launch_bounds__(threads<kDrain>(), 1)
   B.a2_empty = B.a2_full + 2;
   B.o_full = B.a2_empty + 2;
   B.o_empty = B.o_full + 12;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(B.o_empty + 12);
+  uint64_t* const done_bar = B.o_empty + 12;  // trace only: conv2 input completions
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done_bar + 1);
   es::Bars rb;  // the builders' view (a1 ring only)
   rb.a1_full = B.a1_full;
   rb.a1_empty = B.a1_empty;
@@ -702,15 +729,16 @@ __global__ void __launch_bounds__(threads<kDrain>(), 1)
       mbar_init(&B.a1_empty[i], 1);
     }
     mbar_init(B.c1_full, 1);
-    mbar_init(B.c1_empty, 8);
+    mbar_init(B.c1_empty, kEpi);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&B.a2_full[i], 8);
+      mbar_init(&B.a2_full[i], kEpi);
       mbar_init(&B.a2_empty[i], 1);
     }
     for (int i = 0; i < 12; ++i) {
       mbar_init(&B.o_full[i], 1);
       mbar_init(&B.o_empty[i], 4);
     }
+    mbar_init(done_bar, 1);
     fence_barrier_init();
   }
   if (warp == 0) tmem_alloc(tmem_slot, 512);
@@ -720,7 +748,7 @@ __global__ void __launch_bounds__(threads<kDrain>(), 1)
   // conv_rows_sm100.
   {
     const uint4* w2 = static_cast<const uint4*>(args.w2);  // [32][72 chunks of 8]
-    for (int i = threadIdx.x; i < 3 * 288 * 8; i += threads<kDrain>()) {
+    for (int i = threadIdx.x; i < 3 * 288 * 8; i += kThreads) {
       const int q = i / 2304, rem = i % 2304, row = rem >> 3, ch = rem & 7;
       const int ks = ch >> 1, pl = ch & 1, k = row >> 5, co = row & 31;
       const int j = k / 3, r = k % 3, dh = (q + 2 - r) % 3, dw = 2 - j;
@@ -728,7 +756,7 @@ __global__ void __launch_bounds__(threads<kDrain>(), 1)
           w2[co * 72 + (3 * dh + dw) * 8 + ch];
     }
     const uint4* w1 = static_cast<const uint4*>(args.w1);  // [64][2 chunks of 8]
-    for (int i = threadIdx.x; i < 2 * 64; i += threads<kDrain>()) {
+    for (int i = threadIdx.x; i < 2 * 64; i += kThreads) {
       const int cc = i >> 1, pl = i & 1;
       *reinterpret_cast<uint4*>(smem + kOffW1 + (pl * 64 + cc) * 16) = w1[i];
     }
@@ -738,7 +766,8 @@ __global__ void __launch_bounds__(threads<kDrain>(), 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);
-  if (warp >= kBuilders + 10) {  // O starts at zero (every UMMA accumulates)
+  const int drain0 = kBuilders + 2 + kEpi;  // first drain warp
+  if (warp >= drain0 && warp < drain0 + kDrain) {  // O starts at zero (every UMMA accumulates)
     uint32_t z[32];
 #pragma unroll
     for (int i = 0; i < 32; ++i) z[i] = 0u;
@@ -751,25 +780,7 @@ __global__ void __launch_bounds__(threads<kDrain>(), 1)
   __syncthreads();
   tc_fence_after();
 
-  if (args.debug & 1024) {  // timing probe: the conv2 UMMA stream alone, no data
-    if (warp == kBuilders + 1) {
-      Ctx c;
-      c.tbase = __shfl_sync(0xffffffffu, tmem_base, 0);
-      c.w2d = sdesc_planar(__shfl_sync(0xffffffffu, smem_u32(smem + kOffW2), 0), 288 * 16);
-      c.b = B;
-      c.ouse = 0;
-      c.trace = trace;
-      c.debug = args.debug;
-      uint32_t n = 0;
-      for (int k = 0; k < my_tiles; ++k) {
-        sweep_strip<0>(c, n);
-        sweep_strip<1>(c, n);
-      }
-      if (elect_one()) umma_commit(B.c1_full);
-      __syncwarp();
-      mbar_wait(B.c1_full, 0);
-    }
-  } else if (warp < kBuilders) {
+  if (warp < kBuilders) {
     // --------------------------------------------- im2col builders (as conv_rows)
     int n = 0;
     for (int k = 0; k < my_tiles; ++k) {
@@ -802,7 +813,9 @@ __global__ void __launch_bounds__(threads<kDrain>(), 1)
     uint32_t slpar = 0;
     for (int n = 0; n < npos; ++n) {
       mbar_wait(&B.a1_full[sl], slpar);
+      if (lane == 0) TRACE(2, n);
       mbar_wait(B.c1_empty, (static_cast<uint32_t>(n) & 1u) ^ 1u);
+      if (lane == 0) TRACE(12, n);
       tc_fence_after();
       if (elect_one()) {
         umma_bf16(tbase + kTmD1, sdesc_planar(a1_base + sl * kA1Bytes, 2048), w1d, id1, 0);
@@ -823,48 +836,56 @@ __global__ void __launch_bounds__(threads<kDrain>(), 1)
     c.b = B;
     c.ouse = 0;
     c.trace = trace;
-    c.debug = args.debug;
+    c.done = done_bar;
     uint32_t n = 0;
     for (int k = 0; k < my_tiles; ++k) {
       sweep_strip<0>(c, n);
       sweep_strip<1>(c, n);
     }
-  } else if (warp < kBuilders + 10) {
+  } else if (warp == drain0 + kDrain) {
+    // trace only: completion time of every conv2 input (CTA 0)
+    if (trace && lane == 0) {
+      const int npos = my_tiles * 63;
+      for (int n = 0; n < npos && n < 256; ++n) {
+        mbar_wait(done_bar, static_cast<uint32_t>(n) & 1u);
+        TRACE(13, n);
+      }
+    }
+  } else if (warp < drain0) {
     // ---------------------------------------------------- conv1 epilogue
-    // Eight warps: lane quadrant warp & 3, channel half h.  relu(D1 + b1) as
-    // bf16 pairs into A2 slot n & 1 (the conv2 UMMAs read A from TMEM).
-    const int e = warp - kBuilders - 2, h = e >> 2;
+    // One warp per lane quadrant: relu(D1 + b1) of its 32 samples' 64
+    // channels as bf16 pairs into A2 slot n & 1 (the conv2 UMMAs read A from
+    // TMEM).
+    const int e = warp - kBuilders - 2;
+    constexpr int kCh = 64, h = 0;
     const uint32_t lf = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const int npos = my_tiles * 63;
     for (int n = 0; n < npos; ++n) {
       mbar_wait(B.c1_full, static_cast<uint32_t>(n) & 1u);
+      if (e == 0 && lane == 0) TRACE(3, n);
       const uint32_t slot = static_cast<uint32_t>(n) & 1u;
-      if (args.debug & 16) {  // timing probe (results wrong): no TMEM traffic
-        __syncwarp();
-        if (lane == 0) mbar_arrive(B.c1_empty);
-        mbar_wait(&B.a2_empty[slot], ((static_cast<uint32_t>(n) >> 1) & 1u) ^ 1u);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&B.a2_full[slot]);
-        continue;
-      }
       tc_fence_after();
-      uint32_t v[32];
-      tmem_ld32_raw(tmem_base + lf + kTmD1 + 32u * h, v);
+      uint32_t v[kCh];
+#pragma unroll
+      for (int c = 0; c < kCh / 32; ++c)
+        tmem_ld32_raw(tmem_base + lf + kTmD1 + 32u * (h + c), *reinterpret_cast<uint32_t(*)[32]>(v + 32 * c));
       tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(B.c1_empty);
-      uint32_t pk[16];
+      uint32_t pk[kCh / 2];
 #pragma unroll
-      for (int i = 0; i < 16; ++i)
+      for (int i = 0; i < kCh / 2; ++i)
         pk[i] = pack_relu_bf16(v[2 * i], v[2 * i + 1], args.b1c[32 * h + 2 * i], args.b1c[32 * h + 2 * i + 1]);
       mbar_wait(&B.a2_empty[slot], ((static_cast<uint32_t>(n) >> 1) & 1u) ^ 1u);
+      if (e == 0 && lane == 0) TRACE(4, n);
       tc_fence_after();
-      tmem_st16(tmem_base + lf + kTmA2 + 32u * slot + 16u * h, pk);
+      tmem_st32(tmem_base + lf + kTmA2 + 32u * slot, pk);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&B.a2_full[slot]);
+      if (e == 0 && lane == 0) TRACE(5, n);
     }
   } else {
     // ---------------------------------------------------------- output drain
@@ -874,9 +895,7 @@ __global__ void __launch_bounds__(threads<kDrain>(), 1)
     // 3136 B apart were LSU-bound: the drain, not the tensor pipe, set the
     // kernel's pace).  A partial last tile takes per-lane stores of its valid
     // rows instead (a claimed run must not write past its rows).
-    // Drain warp dw: lane quadrant dw & 3; the two warps of a quadrant take
-    // alternate blocks of the completion order.
-    const int dw = warp - kBuilders - 10, qd = warp & 3, grp = dw >> 2;
+    const int dw = warp - drain0, qd = warp & 3;
     const uint32_t lf = static_cast<uint32_t>(qd * 32) << 16;
     const int row = qd * 32 + lane;
     uint8_t* const ring = smem + kOffOut + dw * (kOutStages * kOutBox);
@@ -891,65 +910,55 @@ __global__ void __launch_bounds__(threads<kDrain>(), 1)
       uint8_t* dst_row = static_cast<uint8_t*>(args.out) + s * (kOutRow * 2);
       const bool valid = s < row_end;
       const bool full = s0 + kTile <= row_end;
-      for (int st = 0; st < 2; ++st)
-        for (int ih = 0; ih < kG; ++ih)
-          for (int iw = c0(st); iw <= clast(st); ++iw)
-            for (int oh = ih - 1; oh <= ih; ++oh)
-              for (int ow = iw - 1; ow <= iw; ++ow) {
-                if (!last_at(st, ih, iw, oh, ow)) continue;
-                const int b = block(st, oh, ow);
-                const uint32_t par = (opar >> b) & 1u;
-                opar ^= 1u << b;
-                ++seq;
-                if (kDrain > 4 && (seq & 1) != grp) continue;
-                mbar_wait(&B.o_full[b], par);
-                unsigned long long* const tr = qd == 0 && grp == 0 && lane == 0 ? trace : nullptr;
-                { unsigned long long* trace = tr; TRACE(9, seq >> (kDrain > 4)); }
-                tc_fence_after();
-                uint32_t v[32];
-                const uint32_t src = tmem_base + lf + kTmO + 32u * b;
-                tmem_ld32_raw(src, v);
-                tmem_ld_wait();
-                if (!(args.debug & 128)) {  // bit 128: timing probe, no zeroing (results wrong)
-                  tmem_st32(src, z);
-                  tmem_st_wait();
-                }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&B.o_empty[b]);
-                { unsigned long long* trace = tr; TRACE(10, seq >> (kDrain > 4)); }
-                if (args.debug & 32) continue;  // timing probe: no output stores
-                uint4 q[4];
+#pragma unroll 1
+      for (int i = 0; i < kG * kG; ++i) {
+        const int b = kDrainSeq.blk[i], p = kDrainSeq.pos[i];
+        const uint32_t par = (opar >> b) & 1u;
+        opar ^= 1u << b;
+        ++seq;
+        mbar_wait(&B.o_full[b], par);
+        unsigned long long* const tr = qd == 0 && lane == 0 ? trace : nullptr;
+        { unsigned long long* trace = tr; TRACE(9, seq); }
+        tc_fence_after();
+        uint32_t v[32];
+        const uint32_t src = tmem_base + lf + kTmO + 32u * b;
+        tmem_ld32_raw(src, v);
+        tmem_ld_wait();
+        tmem_st32(src, z);
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&B.o_empty[b]);
+        { unsigned long long* trace = tr; TRACE(10, seq); }
+        uint4 q[4];
 #pragma unroll
-                for (int cc = 0; cc < 4; ++cc)
-                  q[cc] = make_uint4(
-                      pack_relu_bf16(v[8 * cc], v[8 * cc + 1], args.b2c[8 * cc], args.b2c[8 * cc + 1]),
-                      pack_relu_bf16(v[8 * cc + 2], v[8 * cc + 3], args.b2c[8 * cc + 2], args.b2c[8 * cc + 3]),
-                      pack_relu_bf16(v[8 * cc + 4], v[8 * cc + 5], args.b2c[8 * cc + 4], args.b2c[8 * cc + 5]),
-                      pack_relu_bf16(v[8 * cc + 6], v[8 * cc + 7], args.b2c[8 * cc + 6], args.b2c[8 * cc + 7]));
-                if (full) {
-                  uint8_t* box = ring + (nst % kOutStages) * kOutBox;
-                  if (lane == 0) tma_store_wait_read<kOutStages - 1>();  // the box's last store read it
-                  __syncwarp();
-                  if (!(args.debug & 512)) {  // bit 512: timing probe, no staging stores
+        for (int cc = 0; cc < 4; ++cc)
+          q[cc] = make_uint4(
+              pack_relu_bf16(v[8 * cc], v[8 * cc + 1], args.b2c[8 * cc], args.b2c[8 * cc + 1]),
+              pack_relu_bf16(v[8 * cc + 2], v[8 * cc + 3], args.b2c[8 * cc + 2], args.b2c[8 * cc + 3]),
+              pack_relu_bf16(v[8 * cc + 4], v[8 * cc + 5], args.b2c[8 * cc + 4], args.b2c[8 * cc + 5]),
+              pack_relu_bf16(v[8 * cc + 6], v[8 * cc + 7], args.b2c[8 * cc + 6], args.b2c[8 * cc + 7]));
+        if (full) {
+          uint8_t* box = ring + (nst % kOutStages) * kOutBox;
+          if (lane == 0) tma_store_wait_read<kOutStages - 1>();  // the box's last store read it
+          __syncwarp();
 #pragma unroll
-                    for (int cc = 0; cc < 4; ++cc)
-                      *reinterpret_cast<uint4*>(box + lane * 64 + ((cc ^ ((lane >> 1) & 3)) << 4)) = q[cc];
-                    fence_proxy_async_smem();
-                  }
-                  __syncwarp();
-                  if (lane == 0 && !(args.debug & 256)) {  // bit 256: timing probe, no TMA store
-                    tma_store_2d(&tm_out, box, (oh * kG + ow) * kC2, static_cast<int32_t>(s0 + qd * 32));
-                    tma_store_commit();
-                  }
-                  ++nst;
-                  { unsigned long long* trace = tr; TRACE(11, seq >> (kDrain > 4)); }
-                } else if (valid) {
-                  uint4* dst = reinterpret_cast<uint4*>(dst_row + (oh * kG + ow) * kC2 * 2);
+          for (int cc = 0; cc < 4; ++cc)
+            *reinterpret_cast<uint4*>(box + lane * 64 + ((cc ^ ((lane >> 1) & 3)) << 4)) = q[cc];
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tm_out, box, p * kC2, static_cast<int32_t>(s0 + qd * 32));
+            tma_store_commit();
+          }
+          ++nst;
+        } else if (valid) {
+          uint4* dst = reinterpret_cast<uint4*>(dst_row + p * kC2 * 2);
 #pragma unroll
-                  for (int cc = 0; cc < 4; ++cc) dst[cc] = q[cc];
-                }
-              }
+          for (int cc = 0; cc < 4; ++cc) dst[cc] = q[cc];
+        }
+        { unsigned long long* trace = tr; TRACE(11, seq); }
+      }
     }
     if (lane == 0) tma_store_wait_all<0>();
     __syncwarp();
@@ -993,8 +1002,7 @@ int conv_sweep_launch(const ConvRowsArgs& args, const void* x, long long x_rows,
   const long long tiles = (args.row_end - args.row_begin + kTile - 1) / kTile;
   if (tiles <= 0) return 0;
   grid = static_cast<int>(std::min<long long>(grid, tiles));
-  if (ensure_smem_attr(sweep::conv_sweep_sm100<4>, static_cast<int>(sweep::kSmemBytes)) != 0)
-    return -4;
+  if (ensure_smem_attr(sweep::conv_sweep_sm100, static_cast<int>(sweep::kSmemBytes)) != 0) return -4;
   // output rows [0, row_end): TMA stores only ever cover whole tiles inside it
   CUtensorMap tm_out;
   if (make_bf16_map_box(&tm_out, args.out, kOutRow, static_cast<uint64_t>(args.row_end), 32, 32,
@@ -1003,7 +1011,7 @@ int conv_sweep_launch(const ConvRowsArgs& args, const void* x, long long x_rows,
   ConvRowsArgs a = args;
   a.x = x;
   a.x_rows = x_rows;
-  sweep::conv_sweep_sm100<4><<<grid, sweep::threads<4>(), sweep::kSmemBytes, stream>>>(tm_out, a);
+  sweep::conv_sweep_sm100<<<grid, sweep::kThreads, sweep::kSmemBytes, stream>>>(tm_out, a);
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 

@@ -71,9 +71,9 @@ int main(int argc, char** argv) {
   std::printf("pos   tma  c1_a1  c1_iss  epi_c1  epi_a2e  epi_done c1_issued\n");
   for (int n = 0; n < 130; ++n)
     std::printf("%3d %7lld %7lld %7lld %7lld %7lld %7lld %7lld %7lld\n", n, r(0, n), r(1, n), r(2, n), r(3, n),
-                r(4, n), r(5, n), r(14, n), r(15, n));
-  std::printf("win  start  fed  waited  issued\n");
-  for (int w = 0; w < 130; ++w) std::printf("%3d %7lld %7lld %7lld %7lld\n", w, r(6, w), r(10, w), r(7, w), r(8, w));
+                r(4, n), r(5, n), r(12, n), r(15, n));
+  std::printf("win  start  done  waited  issued\n");
+  for (int w = 0; w < 130; ++w) std::printf("%3d %7lld %7lld %7lld %7lld\n", w, r(6, w), r(13, w), r(7, w), r(8, w));
   std::printf("feed-block  pos  start  a1_ok  c1e_ok\n");
   for (int n = 0; n < 130; ++n)
     if (r(11, n) >= 0) std::printf("%3d %7lld %7lld %7lld\n", n, r(11, n), r(12, n), r(13, n));
