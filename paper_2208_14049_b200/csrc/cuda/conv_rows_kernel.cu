@@ -602,6 +602,68 @@ __host__ __device__ constexpr DrainSeq make_drain_seq() {
 }
 __constant__ DrainSeq kDrainSeq = make_drain_seq();
 
+// Patch row ih of strip ST for this lane's sample (builder warps own 32
+// samples each), positions n0 .. n0 + J - 1.  Each position is published as
+// soon as it is written (conv1 of the row's first position does not wait for
+// the whole row), waits spin (a suspended builder woke late at row starts),
+// and the next patch row's image lines are prefetched into L1 before this
+// row's operands are written.
+__device__ __forceinline__ uint4 ld_hint(const void* p, uint64_t pol) {
+  uint4 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p), "l"(pol));
+  return v;
+}
+
+// Strip 0 reads an image band first (evict_last: strip 1 reads it again
+// half a tile later), strip 1 last (evict_first).
+template <int ST>
+__device__ __forceinline__ void build_row_sweep(const ConvRowsArgs& args, uint8_t* smem, const es::Bars& B,
+                                                long long s, int ih, int smp, int lane, int n0,
+                                                const uint8_t* next_row) {
+  const uint64_t pol = ST ? l2_policy_evict_first() : l2_policy_evict_last();
+  constexpr int J = ST ? 4 : 5, cs = ST ? 3 : 0;
+  uint4 ch[4][3];
+  const uint8_t* xrow = static_cast<const uint8_t*>(args.x) + s * (kS * kS * 2);
+  const bool in = s < args.x_rows;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int y = 4 * ih + r;
+    const int x0 = ST ? 28 * y + 12 - 4 * ((r + 1) & 1) : 28 * y - 4 * (r & 1);
+#pragma unroll
+    for (int m = 0; m < 3; ++m)
+      ch[r][m] = in ? ld_hint(xrow + 2 * (x0 + 8 * m), pol) : make_uint4(0, 0, 0, 0);
+  }
+  if (next_row) {  // the next patch row's 224 bytes (up to three 128-byte lines)
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(next_row));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(next_row + 112));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(next_row + 223));
+  }
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const int n = n0 + j;
+    const int sl = n % kA1Stages;
+    mbar_wait(&B.a1_empty[sl], (static_cast<uint32_t>(n / kA1Stages) & 1u) ^ 1u);
+    uint32_t w[4][2];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int c = cs + j;
+      const int o = ST ? 4 * c - 12 + 4 * ((r + 1) & 1) : 4 * c + 4 * (r & 1);
+      const uint4 q = ch[r][o / 8];
+      const bool hi = (o % 8) != 0;
+      w[r][0] = hi ? q.z : q.x;
+      w[r][1] = hi ? q.w : q.y;
+    }
+    uint8_t* a1 = smem + kOffA1 + sl * kA1Bytes + smp * 16;
+    *reinterpret_cast<uint4*>(a1) = make_uint4(w[0][0], w[0][1], w[1][0], w[1][1]);
+    *reinterpret_cast<uint4*>(a1 + 2048) = make_uint4(w[2][0], w[2][1], w[3][0], w[3][1]);
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&B.a1_full[sl]);
+  }
+}
+
 struct Ctx {
   uint32_t tbase;
   uint64_t w2d;  // planar descriptor of W2 copy 0, K step 0
@@ -790,15 +852,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (warp == 0 && lane == 0 && k + 1 < my_tiles) {
         const long long e1 = s1 + kTile < args.x_rows ? s1 + kTile : args.x_rows;
         if (e1 > s1)
-          prefetch_l2_bulk(static_cast<const uint8_t*>(args.x) + s1 * (kS * kS * 2),
-                           static_cast<uint32_t>((e1 - s1) * (kS * kS * 2)));
+          // evict_last: the drain's output stream (2x the image bytes) passes
+          // through L2 before this tile is built and evicted the plain prefetch
+          prefetch_l2_bulk_hint(static_cast<const uint8_t*>(args.x) + s1 * (kS * kS * 2),
+                                static_cast<uint32_t>((e1 - s1) * (kS * kS * 2)), l2_policy_evict_last());
       }
+      const int smp = warp * 32 + lane;
+      const long long s = s0 + smp;
+      const uint8_t* xs = static_cast<const uint8_t*>(args.x) + s * (kS * kS * 2);
+      const uint8_t* xn = s + static_cast<long long>(gridDim.x) * kTile < args.x_rows && k + 1 < my_tiles
+                              ? xs + static_cast<long long>(gridDim.x) * kTile * (kS * kS * 2)
+                              : nullptr;  // the next tile's first patch row
+      const bool in = s < args.x_rows;
       for (int ih = 0; ih < kG; ++ih) {
-        build_row<0, 1>(args, smem, rb, s0, ih, warp, lane, n, kOffA1);
+        build_row_sweep<0>(args, smem, rb, s, ih, smp, lane, n,
+                           !in ? nullptr : ih + 1 < kG ? xs + 224 * (ih + 1) : xs);
+        if (warp == 0 && lane == 0) TRACE(1, n);
         n += 5;
       }
       for (int ih = 0; ih < kG; ++ih) {
-        build_row<1, 1>(args, smem, rb, s0, ih, warp, lane, n, kOffA1);
+        build_row_sweep<1>(args, smem, rb, s, ih, smp, lane, n,
+                           !in ? nullptr : ih + 1 < kG ? xs + 224 * (ih + 1) : xn);
+        if (warp == 0 && lane == 0) TRACE(1, n);
         n += 4;
       }
     }
@@ -904,6 +979,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
     for (int i = 0; i < 32; ++i) z[i] = 0u;
     uint32_t opar = 0, nst = 0;
+    const uint64_t out_policy = l2_policy_evict_first();  // read back by the next launch only
     for (int k = 0; k < my_tiles; ++k) {
       const long long s0 = row_begin + (blockIdx.x + static_cast<long long>(k) * gridDim.x) * kTile;
       const long long s = s0 + row;
@@ -948,7 +1024,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&tm_out, box, p * kC2, static_cast<int32_t>(s0 + qd * 32));
+            tma_store_2d_hint(&tm_out, box, p * kC2, static_cast<int32_t>(s0 + qd * 32), out_policy);
             tma_store_commit();
           }
           ++nst;
