@@ -679,7 +679,43 @@ __device__ __forceinline__ void mma(uint32_t d, uint32_t a, uint64_t b) {
 }
 
 // Input (IH, IW) of strip ST: A2 slot `slot` into every output it feeds.
+// 64-bit smem descriptor from a 32-bit low word (start address, LBO) and the
+// constant high word: one add per operand instead of a 64-bit add chain.
+__device__ __forceinline__ uint64_t desc64(uint32_t lo, uint32_t hi) {
+  return (static_cast<uint64_t>(hi) << 32) | lo;
+}
+
+// kTr: the tools/trace_rows.cu build (clock stamps, completion commits); the
+// product instantiation carries no trace code on the issuer's path (the
+// tensor pipe queues only ~2 UMMAs, so every instruction between two inputs'
+// bursts can idle it).
+// O blocks first touched by input (ST, IH, IW): their o_empty waits.
 template <int ST, int IH, int IW>
+__host__ __device__ constexpr uint32_t new_blocks() {
+  uint32_t m = 0;
+  for (int oh = 0; oh < kG; ++oh)
+    for (int ow = 0; ow < kG; ++ow)
+      if (first_at(ST, IH, IW, oh, ow)) m |= 1u << block(ST, oh, ow);
+  return m;
+}
+
+// Everything input n needs before its UMMAs: its A2 slot filled, and the
+// previous occupants of the O blocks it touches first drained.  `ouse` holds
+// the blocks' use parities BEFORE this input's first touches.
+template <int ST, int IH, int IW>
+__device__ __forceinline__ void wait_input(const Ctx& c, uint32_t n, uint32_t ouse) {
+  mbar_wait(&c.b.a2_full[n & 1u], (n >> 1) & 1u);
+  constexpr uint32_t m = new_blocks<ST, IH, IW>();
+#pragma unroll
+  for (int b = 0; b < 12; ++b)
+    if (m & (1u << b)) mbar_wait(&c.b.o_empty[b], ((ouse >> b) & 1u) ^ 1u);
+  tc_fence_after();
+}
+
+// Input (IH, IW) of strip ST: A2 slot n & 1 into every output it feeds.
+// (Measured and dropped: running the NEXT input's waits inside this input's
+// UMMA burst -- blocking there costs 20 %, a non-blocking test gains nothing.)
+template <bool kTr, int ST, int IH, int IW>
 __device__ __forceinline__ void sweep_input(Ctx& c, uint32_t n) {
   constexpr int q = IH % 3;
   constexpr int jlo = ow0(ST) - (IW - 1) > 0 ? ow0(ST) - (IW - 1) : 0;
@@ -689,43 +725,37 @@ __device__ __forceinline__ void sweep_input(Ctx& c, uint32_t n) {
   constexpr int nr = IH == 0 || IH == kG - 1 ? 2 : 3;  // nor row 7
   const uint32_t slot = n & 1u;
   unsigned long long* trace = c.trace;
-  TRACE(6, static_cast<int>(n));
-  mbar_wait(&c.b.a2_full[slot], (n >> 1) & 1u);
-#pragma unroll
-  for (int oh = 0; oh < kG; ++oh)
-#pragma unroll
-    for (int ow = 0; ow < kG; ++ow)
-      if (first_at(ST, IH, IW, oh, ow)) {
-        const int b = block(ST, oh, ow);
-        mbar_wait(&c.b.o_empty[b], ((c.ouse >> b) & 1u) ^ 1u);
-        c.ouse ^= 1u << b;
-      }
-  tc_fence_after();
-  TRACE(7, static_cast<int>(n));
+  if constexpr (kTr) TRACE(6, static_cast<int>(n));
+  wait_input<ST, IH, IW>(c, n, c.ouse);
+  c.ouse ^= new_blocks<ST, IH, IW>();
+  if constexpr (kTr) TRACE(7, static_cast<int>(n));
   Ctx cw = c;
   asm volatile("" : "+l"(cw.w2d), "+r"(cw.tbase));
   const uint32_t a = cw.tbase + kTmA2 + 32u * slot;
   const uint32_t d0 = cw.tbase + kTmO + 96u * (IW - 1 + jlo - ow0(ST));
-  const uint64_t b0 = cw.w2d + (q * kQBytes >> 4) + 32u * 3u * jlo;
+  const uint32_t blo = static_cast<uint32_t>(cw.w2d) + (q * kQBytes >> 4) + 32u * 3u * jlo;
+  const uint32_t bhi = static_cast<uint32_t>(cw.w2d >> 32);
   if (elect_one()) {
 #pragma unroll
     for (int ks = 0; ks < 4; ++ks) {
-      const uint64_t bk = b0 + ((ks * 2 * 288 * 16) >> 4);
+      const uint32_t bk = blo + ((ks * 2 * 288 * 16) >> 4);
       const uint32_t ak = a + 8u * ks;
       if constexpr (nr == 3) {
         if constexpr (nj == 3) {
-          mma<160>(d0, ak, bk);
-          mma<128>(d0 + 160u, ak, bk + 160u);
+          mma<160>(d0, ak, desc64(bk, bhi));
+          mma<128>(d0 + 160u, ak, desc64(bk + 160u, bhi));
         } else {
-          mma<96 * nj>(d0, ak, bk);
+          mma<96 * nj>(d0, ak, desc64(bk, bhi));
         }
       } else {
 #pragma unroll
-        for (int j = 0; j < nj; ++j) mma<64>(d0 + 96u * j + 32u * rlo, ak, bk + 96u * j + 32u * rlo);
+        for (int j = 0; j < nj; ++j)
+          mma<64>(d0 + 96u * j + 32u * rlo, ak, desc64(bk + 96u * j + 32u * rlo, bhi));
       }
     }
     umma_commit(&c.b.a2_empty[slot]);
-    if (c.trace) umma_commit(c.done);
+    if constexpr (kTr)
+      if (c.trace) umma_commit(c.done);
 #pragma unroll
     for (int oh = 0; oh < kG; ++oh)
 #pragma unroll
@@ -733,29 +763,30 @@ __device__ __forceinline__ void sweep_input(Ctx& c, uint32_t n) {
         if (last_at(ST, IH, IW, oh, ow)) umma_commit(&c.b.o_full[block(ST, oh, ow)]);
   }
   __syncwarp();
-  TRACE(8, static_cast<int>(n));
+  if constexpr (kTr) TRACE(8, static_cast<int>(n));
 }
 
-template <int ST, int IH>
+template <bool kTr, int ST, int IH>
 __device__ __forceinline__ void sweep_row(Ctx& c, uint32_t& n) {
-  sweep_input<ST, IH, c0(ST)>(c, n++);
-  sweep_input<ST, IH, c0(ST) + 1>(c, n++);
-  sweep_input<ST, IH, c0(ST) + 2>(c, n++);
-  sweep_input<ST, IH, c0(ST) + 3>(c, n++);
-  if constexpr (ST == 0) sweep_input<ST, IH, 4>(c, n++);
+  sweep_input<kTr, ST, IH, c0(ST)>(c, n++);
+  sweep_input<kTr, ST, IH, c0(ST) + 1>(c, n++);
+  sweep_input<kTr, ST, IH, c0(ST) + 2>(c, n++);
+  sweep_input<kTr, ST, IH, c0(ST) + 3>(c, n++);
+  if constexpr (ST == 0) sweep_input<kTr, ST, IH, 4>(c, n++);
 }
 
-template <int ST>
+template <bool kTr, int ST>
 __device__ __forceinline__ void sweep_strip(Ctx& c, uint32_t& n) {
-  sweep_row<ST, 0>(c, n);
-  sweep_row<ST, 1>(c, n);
-  sweep_row<ST, 2>(c, n);
-  sweep_row<ST, 3>(c, n);
-  sweep_row<ST, 4>(c, n);
-  sweep_row<ST, 5>(c, n);
-  sweep_row<ST, 6>(c, n);
+  sweep_row<kTr, ST, 0>(c, n);
+  sweep_row<kTr, ST, 1>(c, n);
+  sweep_row<kTr, ST, 2>(c, n);
+  sweep_row<kTr, ST, 3>(c, n);
+  sweep_row<kTr, ST, 4>(c, n);
+  sweep_row<kTr, ST, 5>(c, n);
+  sweep_row<kTr, ST, 6>(c, n);
 }
 
+template <bool kTr>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_sweep_sm100(const __grid_constant__ CUtensorMap tm_out, const ConvRowsArgs args) {
   extern __shared__ uint8_t smem_raw[];
@@ -778,7 +809,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = warp_uniform_id();
   const int lane = threadIdx.x & 31;
-  unsigned long long* const trace = blockIdx.x == 0 ? args.trace : nullptr;
+  unsigned long long* const trace = kTr && blockIdx.x == 0 ? args.trace : nullptr;
   const long long row_begin = args.claim ? args.claim->row_begin : args.row_begin;
   const long long row_end = args.claim ? args.claim->row_end : args.row_end;
   const long long tiles = (row_end - row_begin + kTile - 1) / kTile;
@@ -914,12 +945,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     c.done = done_bar;
     uint32_t n = 0;
     for (int k = 0; k < my_tiles; ++k) {
-      sweep_strip<0>(c, n);
-      sweep_strip<1>(c, n);
+      sweep_strip<kTr, 0>(c, n);
+      sweep_strip<kTr, 1>(c, n);
     }
   } else if (warp == drain0 + kDrain) {
     // trace only: completion time of every conv2 input (CTA 0)
-    if (trace && lane == 0) {
+    if (kTr && trace && lane == 0) {
       const int npos = my_tiles * 63;
       for (int n = 0; n < npos && n < 256; ++n) {
         mbar_wait(done_bar, static_cast<uint32_t>(n) & 1u);
@@ -1078,7 +1109,9 @@ int conv_sweep_launch(const ConvRowsArgs& args, const void* x, long long x_rows,
   const long long tiles = (args.row_end - args.row_begin + kTile - 1) / kTile;
   if (tiles <= 0) return 0;
   grid = static_cast<int>(std::min<long long>(grid, tiles));
-  if (ensure_smem_attr(sweep::conv_sweep_sm100, static_cast<int>(sweep::kSmemBytes)) != 0) return -4;
+  if (ensure_smem_attr(sweep::conv_sweep_sm100<false>, static_cast<int>(sweep::kSmemBytes)) != 0 ||
+      ensure_smem_attr(sweep::conv_sweep_sm100<true>, static_cast<int>(sweep::kSmemBytes)) != 0)
+    return -4;
   // output rows [0, row_end): TMA stores only ever cover whole tiles inside it
   CUtensorMap tm_out;
   if (make_bf16_map_box(&tm_out, args.out, kOutRow, static_cast<uint64_t>(args.row_end), 32, 32,
@@ -1087,7 +1120,10 @@ int conv_sweep_launch(const ConvRowsArgs& args, const void* x, long long x_rows,
   ConvRowsArgs a = args;
   a.x = x;
   a.x_rows = x_rows;
-  sweep::conv_sweep_sm100<<<grid, sweep::kThreads, sweep::kSmemBytes, stream>>>(tm_out, a);
+  if (a.trace)
+    sweep::conv_sweep_sm100<true><<<grid, sweep::kThreads, sweep::kSmemBytes, stream>>>(tm_out, a);
+  else
+    sweep::conv_sweep_sm100<false><<<grid, sweep::kThreads, sweep::kSmemBytes, stream>>>(tm_out, a);
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 
