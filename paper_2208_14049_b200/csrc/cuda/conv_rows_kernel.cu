@@ -528,6 +528,10 @@ constexpr int kBuilders = 4;       // one sample per lane: one load round trip p
 // eight warps of 32 channels measured the same), kDrain drain warps, and a
 // watcher that only runs under tools/trace_rows.cu.
 constexpr int kEpi = 4;
+#ifndef ES_SWEEP_DIRECT
+#define ES_SWEEP_DIRECT 0
+#endif
+constexpr bool kDirectStores = ES_SWEEP_DIRECT;  // A/B build switch (design probe)
 constexpr int kDrain = 4;
 constexpr int kThreads = 32 * (kBuilders + 2 + kEpi + kDrain + 1);  // + conv1 issuer,
                                                                      // conv2 issuer, 8 conv1 epilogue
@@ -1045,7 +1049,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               pack_relu_bf16(v[8 * cc + 2], v[8 * cc + 3], args.b2c[8 * cc + 2], args.b2c[8 * cc + 3]),
               pack_relu_bf16(v[8 * cc + 4], v[8 * cc + 5], args.b2c[8 * cc + 4], args.b2c[8 * cc + 5]),
               pack_relu_bf16(v[8 * cc + 6], v[8 * cc + 7], args.b2c[8 * cc + 6], args.b2c[8 * cc + 7]));
-        if (full) {
+        if (full && !kDirectStores) {
           uint8_t* box = ring + (nst % kOutStages) * kOutBox;
           if (lane == 0) tma_store_wait_read<kOutStages - 1>();  // the box's last store read it
           __syncwarp();
@@ -1059,7 +1063,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_store_commit();
           }
           ++nst;
-        } else if (valid) {
+        } else if (valid) {  // partial tile (or kDirectStores): per-lane 64-byte stores
           uint4* dst = reinterpret_cast<uint4*>(dst_row + p * kC2 * 2);
 #pragma unroll
           for (int cc = 0; cc < 4; ++cc) dst[cc] = q[cc];
