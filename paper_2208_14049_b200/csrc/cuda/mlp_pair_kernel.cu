@@ -152,7 +152,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int hp = 0; hp < L.passes; ++hp)  // hidden passes re-stream the X tiles
           for (int kc = 0; kc < L.kchunks; ++kc) {
             mbar_wait(&empty[stage], phase ^ 1u);
-            if (kc == 0 && hp == 0) TRACE(g, 7);
+            if (kc == 0) TRACE(g * L.passes + hp, 7);
             uint8_t* st = smem + static_cast<size_t>(stage) * L.stage_bytes;
             if (leader)
               mbar_arrive_expect_tx(&full[stage], 2u * (static_cast<uint32_t>(n) * 16384u +
@@ -191,7 +191,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           w2_ready = true;
         }
         if (!waited) mbar_wait_cluster(&a_full[k], (a_par >> k) & 1u);
-        if (k == 0) TRACE(pend_g, 8);
+        if (k == 0) TRACE(pend_g * L.passes + pend_hp, 8);
         a_par ^= 1u << k;
         tc_fence_after();
         const uint32_t tile = tmem_base + static_cast<uint32_t>(buf * L.group_cols + k * HP);
@@ -229,7 +229,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
         }
         if (elect_one()) umma_commit_pair(&acc2_full[k], kBoth);
-        if (k == 0) TRACE(pend_g, 9);
+        if (k == 0) TRACE(pend_g * L.passes + pend_hp, 9);
       };
       auto drain_pending = [&]() {
         for (; pend_next < pend_n; ++pend_next) layer2(pend_buf, pend_next, false);
@@ -244,9 +244,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int buf = v % L.nbuf;
         const uint32_t use = static_cast<uint32_t>(v / L.nbuf);
         if (pend_buf == buf) drain_pending();
-        TRACE(g, 0);
+        TRACE(v, 0);
         mbar_wait_cluster(&acc_empty[buf], (use & 1u) ^ 1u);
-        TRACE(g, 1);
+        TRACE(v, 1);
         tc_fence_after();
         const uint32_t d0 = tmem_base + static_cast<uint32_t>(buf * L.group_cols);
         for (int kc = 0; kc < L.kchunks; ++kc) {
@@ -277,7 +277,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (pend_buf >= 0 && pend_next == pend_n) pend_buf = -1;
         }
         if (elect_one()) umma_commit_pair(&acc_full[buf], kBoth);
-        TRACE(g, 2);
+        TRACE(v, 2);
         if (pend_buf >= 0) drain_pending();
         pend_buf = buf;
         pend_n = n;
@@ -310,14 +310,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int buf = v % L.nbuf;
       const uint32_t use = static_cast<uint32_t>(v / L.nbuf);
       mbar_wait(&acc_full[buf], use & 1u);
-      if (warp == 2 && lane == 0) TRACE(g, 3);
+      if (warp == 2 && lane == 0) TRACE(v, 3);
       tc_fence_after();
       for (int k = 0; k < n; ++k) {
         const uint32_t col0 = static_cast<uint32_t>(buf * L.group_cols + k * HP + half * hw);
         const float* bias = sBias + hp * HP + half * hw;
         hidden_to_bf16(tmem_base + lane_field + col0, bias, hw);
-        if (warp == 2 && lane == 0 && k == 0) TRACE(g, 4);
-        if (warp == 9 && lane == 0 && k == 0) TRACE(g, 10);
+        if (warp == 2 && lane == 0 && k == 0) TRACE(v, 4);
+        if (warp == 9 && lane == 0 && k == 0) TRACE(v, 10);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&a_full[k]), 0));
@@ -331,7 +331,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int k = 0; k < kMaxT; ++k) {
           if (k >= n) continue;
           mbar_wait(&acc2_full[k], (acc2_par >> k) & 1u);
-          if (warp == 2 && lane == 0 && k == 0) TRACE(g, 5);
+          if (warp == 2 && lane == 0 && k == 0) TRACE(v, 5);
           acc2_par ^= 1u << k;
           tc_fence_after();
           const uint32_t d2col =
@@ -360,7 +360,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int c = 0; c < 16; ++c)
             if (c < L.C) o[c] = zs[k][c] + b2[c];
         }
-        if (warp == 2 && lane == 0) TRACE(g, 6);
+        if (warp == 2 && lane == 0) TRACE(v, 6);
       }
     }
   }
