@@ -533,7 +533,35 @@ constexpr int kEpi = 4;
 #endif
 constexpr bool kDirectStores = ES_SWEEP_DIRECT;  // A/B build switch (design probe)
 constexpr int kDrain = 4;
-constexpr int kThreads = 32 * (kBuilders + 2 + kEpi + kDrain + 1);  // + conv1 issuer,
+constexpr int kThreads = 32 * (kBuilders + 2 + kEpi + kDrain + 1);
+// Warp -> role.  A warp issues on sub-partition warp % 4, and the epilogue and
+// drain warps of TMEM lane quadrant q must sit on sub-partition q; the conv2
+// issuer gets sub-partition 1 with no builder beside it (its per-input
+// instructions compete for that sub-partition's issue slots, and the tensor
+// pipe queues only ~2 UMMAs).
+enum Role : int { kRBuild, kRConv1, kRConv2, kREpi, kRDrain, kRWatch };
+constexpr int kRoles[kThreads / 32] = {kRBuild, kRConv2, kRBuild, kRBuild, kRBuild, kREpi,   kRConv1, kREpi,
+                                       kREpi,   kRDrain, kREpi,   kRDrain, kRDrain, kRWatch, kRDrain};
+__host__ __device__ constexpr uint64_t pack_roles() {  // 3 bits per warp: no local-memory table
+  uint64_t v = 0;
+  for (int w = 0; w < kThreads / 32; ++w) v |= static_cast<uint64_t>(kRoles[w]) << (3 * w);
+  return v;
+}
+__host__ __device__ constexpr uint64_t pack_role_idx() {  // 4 bits per warp: index within its role
+  uint64_t v = 0;
+  for (int w = 0; w < kThreads / 32; ++w) {
+    int k = 0;
+    for (int i = 0; i < w; ++i) k += kRoles[i] == kRoles[w];
+    v |= static_cast<uint64_t>(k) << (4 * w);
+  }
+  return v;
+}
+__host__ __device__ __forceinline__ int role_of(int w) {
+  return static_cast<int>((pack_roles() >> (3 * w)) & 7u);
+}
+__host__ __device__ __forceinline__ int role_idx(int w) {
+  return static_cast<int>((pack_role_idx() >> (4 * w)) & 15u);
+}  // + conv1 issuer,
                                                                      // conv2 issuer, 8 conv1 epilogue
 constexpr uint32_t kQBytes = 4 * 2 * 288 * 16;  // one W2 copy: [ks][plane][288 rows][16 B]
 constexpr uint32_t kOffW2 = 0;
@@ -863,8 +891,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);
-  const int drain0 = kBuilders + 2 + kEpi;  // first drain warp
-  if (warp >= drain0 && warp < drain0 + kDrain) {  // O starts at zero (every UMMA accumulates)
+  const int role = role_of(warp);
+  if (role == kRDrain) {  // O starts at zero (every UMMA accumulates)
     uint32_t z[32];
 #pragma unroll
     for (int i = 0; i < 32; ++i) z[i] = 0u;
@@ -877,7 +905,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
 
-  if (warp < kBuilders) {
+  if (role == kRBuild) {
     // --------------------------------------------- im2col builders (as conv_rows)
     int n = 0;
     for (int k = 0; k < my_tiles; ++k) {
@@ -892,7 +920,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           prefetch_l2_bulk_hint(static_cast<const uint8_t*>(args.x) + s1 * (kS * kS * 2),
                                 static_cast<uint32_t>((e1 - s1) * (kS * kS * 2)), l2_policy_evict_last());
       }
-      const int smp = warp * 32 + lane;
+      const int bw = role_idx(warp);
+      const int smp = bw * 32 + lane;
       const long long s = s0 + smp;
       const uint8_t* xs = static_cast<const uint8_t*>(args.x) + s * (kS * kS * 2);
       const uint8_t* xn = s + static_cast<long long>(gridDim.x) * kTile < args.x_rows && k + 1 < my_tiles
@@ -912,7 +941,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         n += 4;
       }
     }
-  } else if (warp == kBuilders) {
+  } else if (role == kRConv1) {
     // ------------------------------------------------------- conv1 issuer
     const uint32_t tbase = __shfl_sync(0xffffffffu, tmem_base, 0);
     const uint32_t a1_base = __shfl_sync(0xffffffffu, smem_u32(smem + kOffA1), 0);
@@ -938,7 +967,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         slpar ^= 1u;
       }
     }
-  } else if (warp == kBuilders + 1) {
+  } else if (role == kRConv2) {
     // ------------------------------------------------------- conv2 issuer
     Ctx c;
     c.tbase = __shfl_sync(0xffffffffu, tmem_base, 0);
@@ -952,7 +981,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       sweep_strip<kTr, 0>(c, n);
       sweep_strip<kTr, 1>(c, n);
     }
-  } else if (warp == drain0 + kDrain) {
+  } else if (role == kRWatch) {
     // trace only: completion time of every conv2 input (CTA 0)
     if (kTr && trace && lane == 0) {
       const int npos = my_tiles * 63;
@@ -961,12 +990,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         TRACE(13, n);
       }
     }
-  } else if (warp < drain0) {
+  } else if (role == kREpi) {
     // ---------------------------------------------------- conv1 epilogue
     // One warp per lane quadrant: relu(D1 + b1) of its 32 samples' 64
     // channels as bf16 pairs into A2 slot n & 1 (the conv2 UMMAs read A from
     // TMEM).
-    const int e = warp - kBuilders - 2;
+    const int e = role_idx(warp);
     constexpr int kCh = 64, h = 0;
     const uint32_t lf = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const int npos = my_tiles * 63;
@@ -1005,7 +1034,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // 3136 B apart were LSU-bound: the drain, not the tensor pipe, set the
     // kernel's pace).  A partial last tile takes per-lane stores of its valid
     // rows instead (a claimed run must not write past its rows).
-    const int dw = warp - drain0, qd = warp & 3;
+    const int dw = role_idx(warp), qd = warp & 3;
     const uint32_t lf = static_cast<uint32_t>(qd * 32) << 16;
     const int row = qd * 32 + lane;
     uint8_t* const ring = smem + kOffOut + dw * (kOutStages * kOutBox);

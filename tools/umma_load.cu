@@ -44,6 +44,12 @@ __global__ void __launch_bounds__(256, 1) run(int load, int reps, const uint4* g
         umma_bf16_ta(tmem, a, bd, idesc_bf16_f32(128, 160), 1u);
         umma_bf16_ta(tmem + 160u, a, bd + 160u, idesc_bf16_f32(128, 128), 1u);
         if (load == 9 && (r & 3) == 3) umma_commit(&never);        // a commit per 4 pairs
+        if (load == 16 && (r & 3) == 3) tc_fence_after();          // tcgen05.fence::after_thread_sync per 4 pairs
+        if (load == 17 && (r & 3) == 3) tc_fence_before();         // tcgen05.fence::before_thread_sync per 4 pairs
+        if (load == 18 && (r & 3) == 3) {                          // a satisfied try_wait + fence, as per input
+          mbar_try_wait(&bar, 1u);
+          tc_fence_after();
+        }
         if (load == 10 && (r & 3) == 3) {                          // + conv1-like UMMA
           umma_bf16(tmem + 384u, sdesc_planar(smem_u32(smem), 2048), sdesc_planar(smem_u32(smem + 8192), 1024),
                     idesc_bf16_f32(128, 64), 0u);
@@ -134,8 +140,9 @@ int main() {
   const char* names[] = {"none", "tcgen05.st", "tcgen05.ld", "STS", "LDS", "LDG", "try_wait spin", "STG",
                          "STS+fence.proxy.async", "commit per 4 pairs", "conv1 UMMA+commit per 4",
                          "2nd warp conv1 UMMAs", "ld in D cols (paced)", "st in D cols (paced)",
-                         "ld outside D (paced)", "st outside D (paced)"};
-  for (int load = 0; load < 16; ++load) {
+                         "ld outside D (paced)", "st outside D (paced)", "fence::after per 4 pairs",
+                         "fence::before per 4 pairs", "try_wait + fence per 4 pairs"};
+  for (int load = 0; load < 19; ++load) {
     run<<<148, 256, 170 * 1024>>>(load, 4000, gs, gd, d);
     unsigned long long c = 0;
     cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
