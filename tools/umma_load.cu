@@ -41,8 +41,12 @@ __global__ void __launch_bounds__(256, 1) run(int load, int reps, const uint4* g
       const long long t0 = clock64();
       for (int r = 0; r < reps; ++r) {
         const uint32_t a = tmem + 448u + 8u * (r & 3);
-        umma_bf16_ta(tmem, a, bd, idesc_bf16_f32(128, 160), 1u);
-        umma_bf16_ta(tmem + 160u, a, bd + 160u, idesc_bf16_f32(128, 128), 1u);
+        // load 19/20: each group of 4 pairs is one "input" whose D window slides
+        // by 96 columns (partial overlap with the previous input, as in the conv
+        // sweep) / or the previous window is disjoint (20: slide by 288)
+        const uint32_t d0 = load == 19 ? 96u * ((r >> 2) % 2) : load == 20 ? 0u : 0u;
+        umma_bf16_ta(tmem + d0, a, bd, idesc_bf16_f32(128, 160), 1u);
+        umma_bf16_ta(tmem + d0 + 160u, a, bd + 160u, idesc_bf16_f32(128, 128), 1u);
         if (load == 9 && (r & 3) == 3) umma_commit(&never);        // a commit per 4 pairs
         if (load == 16 && (r & 3) == 3) tc_fence_after();          // tcgen05.fence::after_thread_sync per 4 pairs
         if (load == 17 && (r & 3) == 3) tc_fence_before();         // tcgen05.fence::before_thread_sync per 4 pairs
@@ -141,8 +145,9 @@ int main() {
                          "STS+fence.proxy.async", "commit per 4 pairs", "conv1 UMMA+commit per 4",
                          "2nd warp conv1 UMMAs", "ld in D cols (paced)", "st in D cols (paced)",
                          "ld outside D (paced)", "st outside D (paced)", "fence::after per 4 pairs",
-                         "fence::before per 4 pairs", "try_wait + fence per 4 pairs"};
-  for (int load = 0; load < 19; ++load) {
+                         "fence::before per 4 pairs", "try_wait + fence per 4 pairs",
+                         "D slides by 96 per 4 pairs"};
+  for (int load = 0; load < 20; ++load) {
     run<<<148, 256, 170 * 1024>>>(load, 4000, gs, gd, d);
     unsigned long long c = 0;
     cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
