@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "mlp_pair_kernel.cuh"
 #include "batching.cuh"
@@ -386,7 +388,9 @@ bool mlpp_plan(int K, int H, int C, int b, MlpPLayout* out) {
   // Hidden layers wider than one SM's TMEM run in passes of HP <= 512 units:
   // each pass re-streams the X tiles, and the layer-2 partials of the passes
   // are summed in the epilogue's registers.
-  const int passes = (H + 511) / 512;
+  int passes = (H + 511) / 512;
+  // ES_PAIR_PASSES / ES_PAIR_T / ES_PAIR_NBUF / ES_PAIR_VERBOSE: design probes
+  if (const char* fp = std::getenv("ES_PAIR_PASSES")) passes = std::max(passes, std::atoi(fp));
   if (H % passes != 0 || (H / passes) % 128 != 0) return false;
   const int HP = H / passes;
   const int kchunks = (K + 63) / 64;
@@ -395,8 +399,12 @@ bool mlpp_plan(int K, int H, int C, int b, MlpPLayout* out) {
   if (NH % 32 != 0) return false;  // N % 16 per UMMA, NH/2 rows 8-row aligned per SM
   bool found = false;
   MlpPLayout best;
+  const char* ft = std::getenv("ES_PAIR_T");
+  const char* fb = std::getenv("ES_PAIR_NBUF");
   for (int T = 1; T <= kMaxT; ++T) {
+    if (ft && T != std::atoi(ft)) continue;
     for (int nbuf = 1; nbuf <= 2; ++nbuf) {
+      if (fb && nbuf != std::atoi(fb)) continue;
       const int cols = nbuf * T * HP;
       if (cols > 512) continue;
       MlpPLayout L;
@@ -447,6 +455,9 @@ bool mlpp_plan(int K, int H, int C, int b, MlpPLayout* out) {
     }
   }
   if (found) *out = best;
+  if (found && std::getenv("ES_PAIR_VERBOSE"))
+    std::fprintf(stderr, "mlpp_plan K=%d H=%d: passes %d HP %d T %d nbuf %d stages %d\n", K, H, best.passes,
+                 best.HP, best.T, best.nbuf, best.stages);
   return found;
 }
 

@@ -16,6 +16,7 @@
 
 int main(int argc, char** argv) {
   const int H = argc > 1 ? std::atoi(argv[1]) : 512;
+  const int grid_div = argc > 2 ? std::atoi(argv[2]) : 1;  // fewer SMs: per-SM vs aggregate limits
   const long long nb = 1 << 22;
   const int K = 784, C = 10, b = 128;
   __nv_bfloat16 *x, *w1, *w2;
@@ -55,12 +56,14 @@ int main(int argc, char** argv) {
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    es::mlpp_launch(a, x, w1, w2, sms, 0);
+    es::mlpp_launch(a, x, w1, w2, sms / grid_div, 0);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
     cudaEventElapsedTime(&ms, e0, e1);
-    std::printf("rep %d: %.3f ms (%s)\n", rep, ms, cudaGetErrorString(cudaGetLastError()));
+    std::printf("rep %d: %.3f ms = %.1f TFLOP/s per SM-share (grid %d) (%s)\n", rep, ms,
+                2.0 * nb * (double(K) * H + double(H) * C) / (ms * 1e-3) / 1e12 * grid_div, sms / grid_div,
+                cudaGetErrorString(cudaGetLastError()));
   }
   std::vector<unsigned long long> t(32 * 16);
   cudaMemcpy(t.data(), trace, t.size() * 8, cudaMemcpyDeviceToHost);
