@@ -18,6 +18,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "dense_kernel.cuh"
 #include "tma_host.hpp"
@@ -263,63 +265,78 @@ uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
 
 bool dense_pair_plan(int K, int N_total, bool relu, DenseLayout* out) {
   if (K < 1 || K % 8 != 0 || N_total < 128 || N_total % 128 != 0) return false;
-  int N = 0;
-  for (int b : {512, 384, 256, 128})
-    if (N_total % b == 0) {
-      N = b;
-      break;
-    }
   const int kchunks = (K + 63) / 64;
-  const int nh = (N + 255) / 256;
-  const int NH = N / nh;
-  if (NH % 32 != 0) return false;  // N % 16 per UMMA, NH/2 W rows per SM 8-row aligned
+  // Column block N: every divisor of N_total in {512, 384, 256, 128} is costed
+  // over the whole row (ncb blocks).  A 512-wide block fills TMEM (one buffer,
+  // epilogue not overlapped); 256-wide blocks double-buffer but re-stream X
+  // per block.  Measured on 784 -> 512 (tools/time_members.py, MLP-512-512,
+  // 4M samples): N = 256, nbuf = 2 5.89 ms vs N = 512, nbuf = 1 6.09 ms, which
+  // this model reproduces with an effective TMA ingress of 64 B/clk per SM
+  // (tools/tma_mcast.cu: ~80 with enough boxes in flight).
+  // Design probes: ES_DPAIR_N / ES_DPAIR_T / ES_DPAIR_NBUF force the plan.
+  const char* fn = std::getenv("ES_DPAIR_N");
+  const char* ft = std::getenv("ES_DPAIR_T");
+  const char* fb = std::getenv("ES_DPAIR_NBUF");
+  constexpr double kIngressBpc = 64.0;
   bool found = false;
   DenseLayout best;
   double best_cost = 0.0;
-  for (int T = 1; T <= kMaxT; ++T)
-    for (int nbuf = 1; nbuf <= 2; ++nbuf) {
-      const int cols = nbuf * T * N;
-      if (cols > 512) continue;
-      DenseLayout L;
-      L.K = K;
-      L.N = N;
-      L.N_total = N_total;
-      L.ncb = N_total / N;
-      L.kchunks = kchunks;
-      L.T = T;
-      L.nbuf = nbuf;
-      L.nh = nh;
-      L.NH = NH;
-      L.relu = relu ? 1 : 0;
-      L.pair = 1;
-      L.group_cols = T * N;
-      int tc = 32;
-      while (tc < cols) tc <<= 1;
-      L.tmem_cols = tc;
-      L.stage_bytes = static_cast<uint32_t>(T) * 16384u + static_cast<uint32_t>(N) * 64u;
-      const uint32_t out_bytes = 2 * 16384u;
-      const uint32_t tail = out_bytes + static_cast<uint32_t>(N_total) * 4u + 256u + 1024u + 64u;
-      if (tail >= kSmemBudget) continue;
-      const int stages = static_cast<int>(std::min<uint32_t>(8, (kSmemBudget - tail) / L.stage_bytes));
-      if (stages < 2) continue;
-      L.stages = stages;
-      L.off_stage_out = static_cast<uint32_t>(stages) * L.stage_bytes;
-      L.off_bias = L.off_stage_out + out_bytes;
-      L.off_bar = align_up(L.off_bias + static_cast<uint32_t>(N_total) * 4u, 64);
-      L.smem_bytes = std::max(L.off_bar + 256u + 1024u, kMinSmem);
-      if (L.smem_bytes > kSmemBudget) continue;
-      // Per SM per pair-tile group: its half of the M=256 UMMAs vs TMA ingress.
-      const double mma = static_cast<double>(kchunks) * T * 2.0 * N;
-      const double ingress = static_cast<double>(kchunks) * L.stage_bytes / 44.0;
-      const double epi = T * (N / 64.0) * 120.0 + 400.0;
-      const double cost = (std::max(mma, ingress) + (nbuf == 1 ? epi : 0.0)) / T;
-      if (!found || cost < best_cost) {
-        best = L;
-        best_cost = cost;
-        found = true;
+  for (const int N : {512, 384, 256, 128}) {
+    if (N > N_total || N_total % N != 0) continue;
+    if (fn && N != std::atoi(fn)) continue;
+    const int nh = (N + 255) / 256;
+    const int NH = N / nh;
+    if (NH % 32 != 0) continue;  // N % 16 per UMMA, NH/2 W rows per SM 8-row aligned
+    for (int T = 1; T <= kMaxT; ++T)
+      for (int nbuf = 1; nbuf <= 2; ++nbuf) {
+        if ((ft && T != std::atoi(ft)) || (fb && nbuf != std::atoi(fb))) continue;
+        const int cols = nbuf * T * N;
+        if (cols > 512) continue;
+        DenseLayout L;
+        L.K = K;
+        L.N = N;
+        L.N_total = N_total;
+        L.ncb = N_total / N;
+        L.kchunks = kchunks;
+        L.T = T;
+        L.nbuf = nbuf;
+        L.nh = nh;
+        L.NH = NH;
+        L.relu = relu ? 1 : 0;
+        L.pair = 1;
+        L.group_cols = T * N;
+        int tc = 32;
+        while (tc < cols) tc <<= 1;
+        L.tmem_cols = tc;
+        L.stage_bytes = static_cast<uint32_t>(T) * 16384u + static_cast<uint32_t>(N) * 64u;
+        const uint32_t out_bytes = 2 * 16384u;
+        const uint32_t tail = out_bytes + static_cast<uint32_t>(N_total) * 4u + 256u + 1024u + 64u;
+        if (tail >= kSmemBudget) continue;
+        const int stages = static_cast<int>(std::min<uint32_t>(8, (kSmemBudget - tail) / L.stage_bytes));
+        if (stages < 2) continue;
+        L.stages = stages;
+        L.off_stage_out = static_cast<uint32_t>(stages) * L.stage_bytes;
+        L.off_bias = L.off_stage_out + out_bytes;
+        L.off_bar = align_up(L.off_bias + static_cast<uint32_t>(N_total) * 4u, 64);
+        L.smem_bytes = std::max(L.off_bar + 256u + 1024u, kMinSmem);
+        if (L.smem_bytes > kSmemBudget) continue;
+        // Per SM per 128-row tile over the whole row: its half of the M=256
+        // UMMAs vs TMA ingress, plus the un-overlapped epilogue of one buffer.
+        const double mma = static_cast<double>(kchunks) * T * 2.0 * N;
+        const double ingress = static_cast<double>(kchunks) * L.stage_bytes / kIngressBpc;
+        const double epi = T * (N / 64.0) * 120.0 + 400.0;
+        const double cost = L.ncb * (std::max(mma, ingress) + (nbuf == 1 ? epi : 0.0)) / T;
+        if (!found || cost < best_cost) {
+          best = L;
+          best_cost = cost;
+          found = true;
+        }
       }
-    }
+  }
   if (found) *out = best;
+  if (found && std::getenv("ES_PAIR_VERBOSE"))
+    std::fprintf(stderr, "dense_pair_plan K=%d N_total=%d: N %d T %d nbuf %d ncb %d stages %d\n", K, N_total,
+                 best.N, best.T, best.nbuf, best.ncb, best.stages);
   return found;
 }
 
