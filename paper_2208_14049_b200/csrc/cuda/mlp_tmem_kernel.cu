@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstdlib>
 
 #include "mlp_tmem_kernel.cuh"
@@ -337,8 +339,12 @@ bool mlpt_plan(int K, int H, int C, int b, MlpTLayout* out) {
   if (NH % 16 != 0) return false;
   bool found = false;
   MlpTLayout best;
+  const char* ft = std::getenv("ES_TMEM_T");  // design probes: force T, nbuf
+  const char* fb = std::getenv("ES_TMEM_NBUF");
   for (int T = 1; T <= kMaxT; ++T) {
+    if (ft && T != std::atoi(ft)) continue;
     for (int nbuf = 1; nbuf <= 2; ++nbuf) {
+      if (fb && nbuf != std::atoi(fb)) continue;
       const int cols = nbuf * T * H;
       if (cols > 512) continue;
       MlpTLayout L;
@@ -388,6 +394,9 @@ bool mlpt_plan(int K, int H, int C, int b, MlpTLayout* out) {
     }
   }
   if (found) *out = best;
+  if (found && std::getenv("ES_PAIR_VERBOSE"))
+    std::fprintf(stderr, "mlpt_plan K=%d H=%d: T %d nbuf %d stages %d d2_sep %d\n", K, H, best.T, best.nbuf,
+                 best.stages, best.d2_sep);
   return found;
 }
 
