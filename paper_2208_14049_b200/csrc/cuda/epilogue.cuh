@@ -17,11 +17,29 @@ __device__ __forceinline__ uint32_t pack_relu_bf16x2(uint32_t lo_bits, uint32_t 
   return *reinterpret_cast<uint32_t*>(&p);
 }
 
+// bf16x2 {relu(lo + blo), relu(hi + bhi)} with one cvt.rn.relu (the same bits
+// as fmaxf then round-to-nearest-even for every finite input).
+__device__ __forceinline__ uint32_t add_relu_bf16x2(uint32_t lo_bits, uint32_t hi_bits, float blo,
+                                                    float bhi) {
+  const float lo = __uint_as_float(lo_bits) + blo;
+  const float hi = __uint_as_float(hi_bits) + bhi;
+  uint32_t d;
+  asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+  return d;
+}
+
+// 32 fp32 columns -> 16 bf16 pairs in TMEM; biases as float4 loads (`bias`
+// 16-byte aligned).
 __device__ __forceinline__ void relu_bf16_chunk(const uint32_t (&r)[32], const float* bias,
                                                 uint32_t dst) {
   uint32_t p[16];
+  const float4* b4 = reinterpret_cast<const float4*>(bias);
 #pragma unroll
-  for (int j = 0; j < 16; ++j) p[j] = pack_relu_bf16x2(r[2 * j], r[2 * j + 1], bias[2 * j], bias[2 * j + 1]);
+  for (int j = 0; j < 8; ++j) {
+    const float4 bv = b4[j];
+    p[2 * j] = add_relu_bf16x2(r[4 * j], r[4 * j + 1], bv.x, bv.y);
+    p[2 * j + 1] = add_relu_bf16x2(r[4 * j + 2], r[4 * j + 3], bv.z, bv.w);
+  }
   sm100::tmem_st16(dst, p);
 }
 
