@@ -129,3 +129,26 @@ def test_cnn_in_data_parallel_ensemble_matches_reference_pipeline():
     Yr, _, _ = refcpu.ref_run_ensemble(c, A.cells, X, rule=0, softmax=True)
     np.testing.assert_allclose(out.combined, Yr, rtol=0, atol=TOL_P)
     assert_labels_identical_or_tied(out.winners, Yr, TOL_P, "cfg2 shape, CNN data-parallel")
+
+
+@pytest.mark.parametrize("schedule,kernel", [(None, "conv_sweep_sm100"), ("rows", "conv_rows_sm100"),
+                                             ("split", "conv_stack_sm100[split]")])
+def test_cnn_s_schedule_selection(schedule, kernel, monkeypatch):
+    """The CNN-s stack runs the input sweep by default; the
+    row-window and positions-in-M kernels stay selectable for comparison.
+    Checked through the launches an InferenceSystem actually records, and
+    every schedule gives the same logits within the bf16 tolerance."""
+    if schedule:
+        monkeypatch.setenv("ES_CONV_SCHEDULE", schedule)
+    model = es.cnn_model(0, "cnn-s", 14)
+    c = es.ClusterSpec([es.DeviceSpec(0, es.GPU, 180000.0, 1e15, 0.0)], [model], [128], 128)
+    A = es.AllocationMatrix.from_array([[128]])
+    X = refcpu.features(31, 777, 784)
+    sysm = es.InferenceSystem(A, c, es.CombinationRule.averaging(softmax=True), device_map=[0])
+    out = sysm.run(es.SampleStore(X))
+    names = [n for n, _ in sysm.kernel_timing(0)]
+    sysm.close()
+    assert names[0] == kernel, names
+    cpu = refcpu.CpuCnn((28, 4, 64, 32, 128, 10), 14)
+    want, labels = restate.fold("avg", [refcpu.softmax_rows(cpu.forward(X))])
+    assert float(np.abs(out.combined - want).max()) < 1e-3
